@@ -1,0 +1,288 @@
+// oracle/ref_driver.cpp — TEST INFRASTRUCTURE ONLY (the checker, never the product).
+//
+// A thin extern "C" driver around the UNMODIFIED reference simulator, compiled
+// from /root/reference/proj/src/*.cpp by oracle/Makefile into oracle/_ref/.
+// It is used by tests/ (golden-log generation, restatement pinning) and by
+// bench.py's cpu_baseline / --impl reference legs. Nothing in the product
+// path links or loads it.
+//
+// Entry points wrap the reference's own public API:
+//   run_once            experiment.cpp:23-30
+//   Executor::run       executor.cpp:809-851 (trace = nullptr for timing)
+//   ucb_score           policy.cpp:25-30
+//   rebase_widths       policy.cpp:65-118
+//   allocate_budgets    budget.cpp:45-96
+//   roofline_k_total    budget.cpp:23-39
+//   RewardOracle::*     sim.cpp:106-169
+//   unique_kv_tokens    sim.cpp:54-68
+#include <chrono>
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <fstream>
+#include <iostream>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "totsim/budget.hpp"
+#include "totsim/config.hpp"
+#include "totsim/executor.hpp"
+#include "totsim/experiment.hpp"
+#include "totsim/policy.hpp"
+#include "totsim/rng.hpp"
+#include "totsim/sim.hpp"
+#include "totsim/termination.hpp"
+#include "totsim/trace.hpp"
+
+using namespace totsim;
+
+namespace {
+
+thread_local std::string g_err;
+
+char* dup_string(const std::string& s) {
+  char* p = static_cast<char*>(std::malloc(s.size() + 1));
+  std::memcpy(p, s.data(), s.size());
+  p[s.size()] = 0;
+  return p;
+}
+
+ExperimentConfig parse_cfg(const char* config_json) {
+  return ExperimentConfig::from_json(nlohmann::ordered_json::parse(config_json));
+}
+
+void totals_out(const RunTotals& t, double* out) {
+  // [makespan, generated, committed, reused, wasted, queries, correct, early,
+  //  hits[1..8], misses[1..8]]
+  out[0] = t.makespan;
+  out[1] = static_cast<double>(t.generated_tokens);
+  out[2] = static_cast<double>(t.committed_tokens);
+  out[3] = static_cast<double>(t.reused_tokens);
+  out[4] = static_cast<double>(t.wasted_tokens);
+  out[5] = t.queries;
+  out[6] = t.correct_votes;
+  out[7] = t.early_terminated;
+  for (int d = 1; d <= kMaxTrackedDistance; ++d) {
+    out[7 + d] = static_cast<double>(t.hits[d]);
+    out[15 + d] = static_cast<double>(t.misses[d]);
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_err.c_str(); }
+
+void ref_free(void* p) { std::free(p); }
+
+/** Full run with the event log (run_once). Returns 0 or Errc ordinal + 1. */
+int ref_run_log(const char* config_json, std::uint64_t seed, const char* flags_csv,
+                char** out_log, double* out_totals) {
+  try {
+    ExperimentConfig cfg = parse_cfg(config_json);
+    SpexFlags fl = flags_csv ? flags_from_string(flags_csv) : cfg.flags;
+    RunOutcome out = run_once(cfg, seed, fl);
+    std::string s;
+    for (const auto& line : out.log) {
+      s += line;
+      s += '\n';
+    }
+    *out_log = dup_string(s);
+    totals_out(out.totals, out_totals);
+    return 0;
+  } catch (const Error& e) {
+    g_err = e.what();
+    return static_cast<int>(e.code()) + 1;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 100;
+  }
+}
+
+/** Timed runs: `reps` back-to-back Executor::run with or without tracing.
+ *  Returns the total wall seconds through *secs. */
+int ref_run_timed(const char* config_json, std::uint64_t seed, const char* flags_csv,
+                  int with_trace, int reps, double* secs, double* out_totals) {
+  try {
+    ExperimentConfig cfg = parse_cfg(config_json);
+    SpexFlags fl = flags_csv ? flags_from_string(flags_csv) : cfg.flags;
+    auto t0 = std::chrono::steady_clock::now();
+    RunTotals last;
+    for (int r = 0; r < reps; ++r) {
+      if (with_trace) {
+        TraceWriter w = TraceWriter::to_memory();
+        Executor ex(cfg, seed, fl, &w);
+        last = ex.run();
+      } else {
+        Executor ex(cfg, seed, fl, nullptr);
+        last = ex.run();
+      }
+    }
+    auto t1 = std::chrono::steady_clock::now();
+    *secs = std::chrono::duration<double>(t1 - t0).count();
+    if (out_totals) totals_out(last, out_totals);
+    return 0;
+  } catch (const Error& e) {
+    g_err = e.what();
+    return static_cast<int>(e.code()) + 1;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 100;
+  }
+}
+
+/** Parallel repetitions over OpenMP (run_experiment_full, experiment.cpp:50-134)
+ *  as the reference's own multi-core mode. */
+int ref_run_experiment(const char* config_json, double* secs, double* makespan,
+                       double* speedup) {
+  try {
+    ExperimentConfig cfg = parse_cfg(config_json);
+    auto t0 = std::chrono::steady_clock::now();
+    ExperimentResult res = run_experiment_full(cfg);
+    auto t1 = std::chrono::steady_clock::now();
+    *secs = std::chrono::duration<double>(t1 - t0).count();
+    *makespan = res.metrics.makespan;
+    *speedup = res.metrics.speedup;
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 100;
+  }
+}
+
+/** Canonical config JSON (ExperimentConfig::to_json) after strict parsing. */
+int ref_canonical_config(const char* config_json, char** out) {
+  try {
+    *out = dup_string(parse_cfg(config_json).to_json().dump());
+    return 0;
+  } catch (const Error& e) {
+    g_err = e.what();
+    return static_cast<int>(e.code()) + 1;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 100;
+  }
+}
+
+// ---------------------------------------------------------------- pure KATs
+double ref_ucb_score(double value, int cv, int pv, double c) { return ucb_score(value, cv, pv, c); }
+
+int ref_rebase_widths(const double* rewards, int n, int budget, double temp, int sum_preserving,
+                      int* out) {
+  try {
+    std::vector<double> r(rewards, rewards + n);
+    auto w = rebase_widths(r, budget, temp,
+                           sum_preserving ? WidthMode::SumPreserving : WidthMode::HalfAwayFromZero);
+    for (int i = 0; i < n; ++i) out[i] = w[i];
+    return 0;
+  } catch (const Error& e) {
+    return static_cast<int>(e.code()) + 1;
+  }
+}
+
+int ref_allocate_budgets(const int* capacity, const double* hit_ema, const double* kv_bytes, int n,
+                         int k_total, double tau, const double* hw6, int* out) {
+  HardwareProfile hw;
+  hw.weight_bytes = hw6[0];
+  hw.mem_bandwidth = hw6[1];
+  hw.peak_compute = hw6[2];
+  hw.flops_per_token = hw6[3];
+  hw.kv_bytes_per_token = hw6[4];
+  hw.reward_latency = hw6[5];
+  std::vector<QueryState> qs(n);
+  for (int i = 0; i < n; ++i) {
+    qs[i].query_id = i;
+    qs[i].capacity = capacity[i];
+    qs[i].hit_ema = hit_ema[i];
+    qs[i].kv_bytes = kv_bytes[i];
+  }
+  auto g = allocate_budgets(qs, k_total, tau, hw);
+  for (int i = 0; i < n; ++i) out[i] = g[i];
+  return 0;
+}
+
+int ref_roofline_k_total(const double* hw6, int active, double avg_kv, int cap) {
+  HardwareProfile hw;
+  hw.weight_bytes = hw6[0];
+  hw.mem_bandwidth = hw6[1];
+  hw.peak_compute = hw6[2];
+  hw.flops_per_token = hw6[3];
+  hw.kv_bytes_per_token = hw6[4];
+  hw.reward_latency = hw6[5];
+  return roofline_k_total(hw, active, avg_kv, cap);
+}
+
+std::uint64_t ref_splitmix64(std::uint64_t x) { return rng::splitmix64(x); }
+std::uint64_t ref_extend_hash(std::uint64_t h, int slot) { return rng::extend_hash(h, slot); }
+double ref_uniform01(std::uint64_t h, std::uint64_t salt) { return rng::uniform01(h, salt); }
+double ref_normal01(std::uint64_t h, std::uint64_t salt) { return rng::normal01(h, salt); }
+double ref_log(double x) { return std::log(x); }
+double ref_exp(double x) { return std::exp(x); }
+double ref_cos(double x) { return std::cos(x); }
+
+/** Default-workload token length for a child hash (RewardOracle::token_len). */
+int ref_token_len(std::uint64_t child_hash) {
+  WorkloadSpec wl;
+  RewardOracle o(1, wl, 16);
+  return o.token_len(child_hash);
+}
+
+/** Workload seeds: generate_workload (sim.cpp:171-198). out: seed, golden idx, probe depth. */
+int ref_workload(int n, std::uint64_t seed, int max_depth, std::uint64_t* seeds, int* probe_depth) {
+  WorkloadSpec wl;
+  auto p = generate_workload(n, wl, seed, max_depth);
+  for (int i = 0; i < n; ++i) {
+    seeds[i] = p[i].seed;
+    probe_depth[i] = p[i].probe_depth;
+  }
+  return 0;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------ CLI
+#ifdef REF_DRIVER_MAIN
+int main(int argc, char** argv) {
+  std::string config_path, flags, out;
+  std::uint64_t seed = 0;
+  bool have_seed = false, timed = false, no_trace = false;
+  int reps = 1;
+  for (int i = 1; i < argc; ++i) {
+    std::string a = argv[i];
+    auto next = [&]() { return std::string(argv[++i]); };
+    if (a == "--config") config_path = next();
+    else if (a == "--seed") { seed = std::stoull(next()); have_seed = true; }
+    else if (a == "--flags") flags = next();
+    else if (a == "--out") out = next();
+    else if (a == "--time") timed = true;
+    else if (a == "--no-trace") no_trace = true;
+    else if (a == "--reps") reps = std::stoi(next());
+  }
+  std::ifstream in(config_path);
+  std::stringstream ss;
+  ss << in.rdbuf();
+  ExperimentConfig cfg = ExperimentConfig::from_json(nlohmann::ordered_json::parse(ss.str()));
+  if (!have_seed) seed = cfg.seed;
+  const char* fcsv = flags.empty() ? nullptr : (flags == "baseline" ? "" : flags.c_str());
+  SpexFlags fl = fcsv ? flags_from_string(fcsv) : cfg.flags;
+  if (timed) {
+    double secs = 0;
+    double tot[24];
+    ref_run_timed(ss.str().c_str(), seed, fcsv, !no_trace, reps, &secs, tot);
+    std::cout << "{\"secs\": " << secs << ", \"reps\": " << reps << ", \"makespan\": " << tot[0]
+              << ", \"queries\": " << tot[5] << "}\n";
+    return 0;
+  }
+  RunOutcome o = run_once(cfg, seed, fl);
+  std::ostream* os = &std::cout;
+  std::ofstream f;
+  if (!out.empty()) {
+    f.open(out);
+    os = &f;
+  }
+  for (const auto& l : o.log) *os << l << '\n';
+  return 0;
+}
+#endif
