@@ -1,0 +1,93 @@
+/*
+ * spex.h — C-ABI drop-in boundary of the B200 frontier-expansion path.
+ *
+ * The reference (totsim, C++20) has no C ABI; its seams are the concrete C++
+ * classes the executor owns. Each entry point below replaces
+ * one of them and is what a reference-side binding would call:
+ *
+ *   spex_executor_create/run  <- totsim::Executor(cfg, seed, flags, trace) + run()
+ *                                (proj/include/totsim/executor.hpp:50-58,
+ *                                 proj/src/executor.cpp:809-860)
+ *   spex_run_once             <- totsim::run_once (proj/include/totsim/experiment.hpp:27,
+ *                                 proj/src/experiment.cpp:23-30)
+ *   spex_canonical_config     <- ExperimentConfig::from_json + to_json
+ *                                (proj/src/config.cpp:73-137,177-275)
+ *   spex_totals               <- totsim::RunTotals (executor.hpp:20-33)
+ *
+ * Conventions: plain pointers and sizes, no exceptions across the ABI, status
+ * 0 = ok, otherwise totsim::Errc ordinal + 1 (errors.hpp:9-28) or >= 100 for
+ * capacity/device failures. One CUDA stream per executor handle; distinct
+ * handles may be driven from different threads (single writer per handle, as
+ * executor.hpp:92-99 requires). Memory returned through char** is released
+ * with spex_free.
+ */
+#ifndef SPEX_H_
+#define SPEX_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SPEX_MAX_TRACKED 8 /* executor.hpp:16 kMaxTrackedDistance */
+
+typedef struct spex_totals {
+  double makespan;
+  long long generated_tokens;
+  long long committed_tokens;
+  long long reused_tokens;
+  long long wasted_tokens;
+  long long hits[SPEX_MAX_TRACKED + 1];   /* index 1..8 */
+  long long misses[SPEX_MAX_TRACKED + 1]; /* index 1..8 */
+  int queries;
+  int correct_votes;
+  int early_terminated;
+  int pad_;
+} spex_totals;
+
+typedef struct spex_stats {
+  long long iterations;     /* consumer-loop iterations (main_loop) */
+  long long epochs;         /* engine epochs that ended at a completion */
+  long long reward_events;  /* reward events handled */
+  long long decode_steps;   /* virtual decode steps run by the engine */
+  long long decode_rows;    /* sum over decode steps of active streams */
+  long long log_records;    /* binary event records produced */
+  long long nodes;          /* thought nodes created */
+  double device_ms;         /* CUDA-event time of the control kernel */
+} spex_stats;
+
+typedef struct spex_executor spex_executor;
+
+/* Error text of the last failing call on this thread. */
+const char* spex_last_error(void);
+void spex_free(void* p);
+
+/* 1 when the library was built for sm_100a and a CUDA device is usable. */
+int spex_device_ok(void);
+
+/* Strict config parse (unknown keys are errors) -> canonical JSON (to_json). */
+int spex_canonical_config(const char* config_json, char** out_json);
+
+/* Executor(cfg, run_seed, flags, trace). flags_csv: "t1,t2,t3" style, ""
+ * for no flags, NULL to use the config's own run.flags. */
+int spex_executor_create(const char* config_json, uint64_t run_seed, const char* flags_csv,
+                         int device, spex_executor** out);
+/* Run to completion (call once; a second call returns InvalidArgument + 1).
+ * trace != 0 records the event log (trace.hpp:14-29) on the device. */
+int spex_executor_run(spex_executor* ex, int trace, spex_totals* totals);
+/* Event log of a traced run as JSON lines, byte-compatible with TraceWriter. */
+int spex_executor_log(spex_executor* ex, char** out_lines, size_t* out_len);
+int spex_executor_stats(spex_executor* ex, spex_stats* out);
+void spex_executor_destroy(spex_executor* ex);
+
+/* run_once: traced run returning totals and the JSON-lines log. */
+int spex_run_once(const char* config_json, uint64_t seed, const char* flags_csv,
+                  spex_totals* totals, char** out_lines);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SPEX_H_ */

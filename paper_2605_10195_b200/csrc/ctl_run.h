@@ -1,0 +1,894 @@
+// ctl_run.h — the frontier-expansion main loop (executor.cpp:785-807) as a
+// sequence of block-parallel phases:
+//
+//   engine epoch   DecodeEngine::advance (sim.cpp:305-384): joins, roofline step
+//                  cost from incrementally maintained prefix-shared KV tokens,
+//                  bulk token advance, ordered completion list
+//   completions    on_stream_done per finished stream (queries in parallel,
+//                  streams of one query in rank rounds)
+//   reward event   on_reward for the FIFO head
+//   follow-ups     advance_dfs / advance_rest / advance_layer for every query
+//                  whose state changed (consumer_step_followups, executor.cpp:746-763)
+//   scheduling     capacity, T2 budget split (allocate_budgets, budget.cpp:45-96)
+//                  and speculative planning (scheduling_round, executor.cpp:705-740)
+//   commit         exclusive scans place every item's records, new streams and
+//                  reward events in the reference's sequential order
+//
+// The template parameter EX is the execution context: DevExec (one CTA of the
+// persistent kernel, ctl_kernel.cu) or HostExec (single thread, test-only
+// emulation build).
+#pragma once
+
+#include "ctl_drivers.h"
+
+namespace spex {
+
+constexpr double kInf = HUGE_VAL;
+
+struct HostExec {
+  int tid = 0, nthr = 1, warp = 0, nwarp = 1, lane = 0, lanes = 1;
+  int* sm = nullptr;        // scan scratch (nthr + 2 ints)
+  double* smd = nullptr;    // reduction scratch
+  i64* sml = nullptr;
+  void sync() {}
+};
+
+// ------------------------------------------------------------ block primitives
+template <class EX>
+SPEX_HD void ex_scan(EX& ex, int* a, int n, int* total) {
+#if SPEX_DEVICE_PASS
+  const int per = (n + ex.nthr - 1) / ex.nthr;
+  const int lo = ex.tid * per;
+  const int hi = lo + per < n ? lo + per : n;
+  int s = 0;
+  for (int i = lo; i < hi; ++i) s += a[i];
+  ex.sm[ex.tid] = s;
+  ex.sync();
+  if (ex.warp == 0) {
+    const int chunk = (ex.nthr + 31) / 32;
+    const int b0 = ex.lane * chunk;
+    int acc = 0;
+    for (int j = 0; j < chunk; ++j)
+      if (b0 + j < ex.nthr) acc += ex.sm[b0 + j];
+    int incl = acc;
+    for (int off = 1; off < 32; off <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, incl, off);
+      if (ex.lane >= off) incl += y;
+    }
+    int run = incl - acc;
+    for (int j = 0; j < chunk; ++j)
+      if (b0 + j < ex.nthr) {
+        int v = ex.sm[b0 + j];
+        ex.sm[b0 + j] = run;
+        run += v;
+      }
+    if (ex.lane == 31) ex.sm[ex.nthr] = incl;
+  }
+  ex.sync();
+  int run = ex.sm[ex.tid];
+  for (int i = lo; i < hi; ++i) {
+    int v = a[i];
+    a[i] = run;
+    run += v;
+  }
+  *total = ex.sm[ex.nthr];
+  ex.sync();
+#else
+  int run = 0;
+  for (int i = 0; i < n; ++i) {
+    int v = a[i];
+    a[i] = run;
+    run += v;
+  }
+  *total = run;
+#endif
+}
+
+template <class EX>
+SPEX_HD int ex_min_int(EX& ex, int v) {
+#if SPEX_DEVICE_PASS
+  for (int off = 16; off > 0; off >>= 1) {
+    int y = __shfl_xor_sync(0xffffffffu, v, off);
+    v = y < v ? y : v;
+  }
+  if (ex.lane == 0) ex.sm[ex.warp] = v;
+  ex.sync();
+  int r = ex.sm[0];
+  for (int w = 1; w < ex.nwarp; ++w) r = ex.sm[w] < r ? ex.sm[w] : r;
+  ex.sync();
+  return r;
+#else
+  return v;
+#endif
+}
+
+template <class EX>
+SPEX_HD i64 ex_sum_i64(EX& ex, i64 v) {
+#if SPEX_DEVICE_PASS
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  if (ex.lane == 0) ex.sml[ex.warp] = v;
+  ex.sync();
+  i64 r = 0;
+  for (int w = 0; w < ex.nwarp; ++w) r += ex.sml[w];
+  ex.sync();
+  return r;
+#else
+  return v;
+#endif
+}
+
+template <class EX>
+SPEX_HD double ex_minmax_d(EX& ex, double v, bool want_max) {
+#if SPEX_DEVICE_PASS
+  for (int off = 16; off > 0; off >>= 1) {
+    double y = __shfl_xor_sync(0xffffffffu, v, off);
+    if (want_max ? (y > v) : (y < v)) v = y;
+  }
+  if (ex.lane == 0) ex.smd[ex.warp] = v;
+  ex.sync();
+  double r = ex.smd[0];
+  for (int w = 1; w < ex.nwarp; ++w)
+    if (want_max ? (ex.smd[w] > r) : (ex.smd[w] < r)) r = ex.smd[w];
+  ex.sync();
+  return r;
+#else
+  return v;
+#endif
+}
+
+SPEX_HD i64 atomic_add_i64(i64* p, i64 v) {
+#if SPEX_DEVICE_PASS
+  return static_cast<i64>(atomicAdd(reinterpret_cast<unsigned long long*>(p),
+                                    static_cast<unsigned long long>(v)));
+#else
+  i64 o = *p;
+  *p += v;
+  return o;
+#endif
+}
+
+SPEX_HD int atomic_add_int(int* p, int v) {
+#if SPEX_DEVICE_PASS
+  return atomicAdd(p, v);
+#else
+  int o = *p;
+  *p += v;
+  return o;
+#endif
+}
+
+// --------------------------------------------------------------- engine math
+// sim.cpp:277-289
+SPEX_HD double eng_elapsed(const GState* g, int steps) {
+  if (steps <= 0) return 0.0;
+  double m = static_cast<double>(steps);
+  if (g->mem_d_ <= 0.0) return m * (g->compute_ < g->mem_a_ ? g->mem_a_ : g->compute_);
+  int i0 = 0;
+  if (g->compute_ > g->mem_a_) {
+    double cross = (g->compute_ - g->mem_a_) / g->mem_d_;
+    int c = static_cast<int>(floor(cross)) + 1;
+    i0 = steps < c ? steps : c;
+  }
+  double tail = static_cast<double>(steps - i0);
+  return i0 * g->compute_ + tail * g->mem_a_ +
+         g->mem_d_ * (static_cast<double>(i0) + m - 1.0) * tail / 2.0;
+}
+
+// sim.cpp:291-303
+SPEX_HD int eng_steps_within(const GState* g, double budget, int max_steps) {
+  if (budget < -kTimeEps || max_steps <= 0) return 0;
+  if (eng_elapsed(g, max_steps) <= budget + kTimeEps) return max_steps;
+  int lo = 0, hi = max_steps;
+  while (hi - lo > 1) {
+    int mid = lo + (hi - lo) / 2;
+    if (eng_elapsed(g, mid) <= budget + kTimeEps)
+      lo = mid;
+    else
+      hi = mid;
+  }
+  return lo;
+}
+
+// unique_kv_tokens bookkeeping (sim.cpp:54-68): a stream joining/leaving the
+// active batch adds/removes its strict ancestors' token counts the first/last
+// time an ancestor becomes/stops being shared by an active member.
+SPEX_HD void kv_ancestors_adjust(Run* R, int sid, int delta) {
+  const int q = R->st_q[sid];
+  const u32 base = static_cast<u32>(q) * static_cast<u32>(R->cfg.node_cap);
+  i64 acc = 0;
+  for (u32 cur = R->n_parent[base + R->st_node[sid]]; cur != kNoNode;
+       cur = R->n_parent[base + cur]) {
+    int old = atomic_add_int(&R->n_refc[base + cur], delta);
+    if (delta > 0 && old == 0) acc += R->n_tokens[base + cur];
+    if (delta < 0 && old == 1) acc -= R->n_tokens[base + cur];
+  }
+  if (acc != 0) atomic_add_i64(&R->g->u_anc, acc);
+}
+
+// DecodeEngine::advance (sim.cpp:305-384). On return g->engine_now holds the
+// reached boundary and fins[0..nfins) the streams finishing there, in order.
+template <class EX>
+SPEX_HD void engine_advance(Run* R, EX& ex, double limit) {
+  GState* g = R->g;
+  const Cfg& c = R->cfg;
+  // per-call scalars in GState scratch: s_limit = now, s_flag = mode
+  if (ex.tid == 0) {
+    g->s_limit = g->engine_now;
+    g->nfins = 0;
+  }
+  ex.sync();
+  for (int guard = 0;; ++guard) {
+    // ---- joins at this boundary
+    if (ex.tid == 0) {
+      int j = g->n_active_region;
+      const double now = g->s_limit;
+      g->s_k_total = j;  // joined_lo
+      while (j < g->n_live) {
+        int sid = R->live[j];
+        u8 s = R->st_state[sid];
+        if (s == ST_GONE) {
+          ++j;
+          continue;
+        }
+        if (R->st_ready[sid] <= now + kTimeEps) {
+          R->st_state[sid] = ST_ACTIVE;
+          g->n_act += 1;
+          g->n_staged -= 1;
+          ++j;
+        } else {
+          break;
+        }
+      }
+      g->s_leftover = j;  // joined_hi
+      g->n_active_region = j;
+    }
+    ex.sync();
+    for (int i = g->s_k_total + ex.tid; i < g->s_leftover; i += ex.nthr) {
+      int sid = R->live[i];
+      if (R->st_state[sid] == ST_ACTIVE) kv_ancestors_adjust(R, sid, +1);
+    }
+    ex.sync();
+    if (ex.tid == 0) {
+      g->s_flag = 0;  // 0 continue, 1 return
+      if (g->n_act == 0) {
+        if (g->n_staged == 0) {
+          g->s_flag = 1;
+          g->s_limit = limit;
+        } else {
+          double r = kInf;
+          for (int j = g->n_active_region; j < g->n_live; ++j) {
+            int sid = R->live[j];
+            if (R->st_state[sid] == ST_STAGED) {
+              r = R->st_ready[sid];
+              break;
+            }
+          }
+          if (r > limit + kTimeEps) {
+            g->s_flag = 1;
+            g->s_limit = limit;
+          } else {
+            g->s_limit = r;
+            g->s_flag = 2;  // retry joins
+          }
+        }
+      } else {
+        // refresh_costs (sim.cpp:265-275): always recomputed (it is a pure
+        // function of the active set, identical to the cached value when clean)
+        const double B = static_cast<double>(g->n_act);
+        const double U = static_cast<double>(g->u_anc + g->sum_done);
+        g->compute_ = B * c.flops_per_token / c.peak_compute;
+        double kv_bytes = c.kv_bytes_per_token * U;
+        g->mem_a_ = (c.weight_bytes + kv_bytes) / c.mem_bandwidth;
+        g->mem_d_ = c.kv_bytes_per_token * B / c.mem_bandwidth;
+      }
+    }
+    ex.sync();
+    if (g->s_flag == 1) break;
+    if (g->s_flag == 2) continue;
+    // ---- epoch length
+    int mloc = 0x7fffffff;
+    for (int i = ex.tid; i < g->n_active_region; i += ex.nthr) {
+      int sid = R->live[i];
+      if (R->st_state[sid] == ST_ACTIVE && R->st_rem[sid] < mloc) mloc = R->st_rem[sid];
+    }
+    int m_complete = ex_min_int(ex, mloc);
+    if (ex.tid == 0) {
+      const double now = g->s_limit;
+      int m_limit = eng_steps_within(g, limit - now, m_complete);
+      int target = m_complete;
+      if (g->n_staged > 0) {
+        double r = kInf;
+        for (int j = g->n_active_region; j < g->n_live; ++j) {
+          int sid = R->live[j];
+          if (R->st_state[sid] == ST_STAGED) {
+            r = R->st_ready[sid];
+            break;
+          }
+        }
+        int cap = m_complete < m_limit ? m_complete : m_limit;
+        if (cap >= 1 && now + eng_elapsed(g, cap) >= r - kTimeEps) {
+          int lo = 1, hi = cap;
+          while (hi > lo) {
+            int mid = lo + (hi - lo) / 2;
+            if (now + eng_elapsed(g, mid) >= r - kTimeEps)
+              hi = mid;
+            else
+              lo = mid + 1;
+          }
+          target = lo;
+        }
+      }
+      if (target > m_limit) {
+        g->s_k_total = m_limit;  // steps
+        g->s_flag = 1;           // partial epoch: return after advancing
+        if (m_limit > 0) g->s_limit = now + eng_elapsed(g, m_limit);
+      } else {
+        g->s_k_total = target;
+        g->s_flag = 0;
+        g->s_limit = now + eng_elapsed(g, target);
+      }
+      if (g->s_k_total > 0) {
+        g->sum_done += static_cast<i64>(g->s_k_total) * g->n_act;
+        g->decode_steps += g->s_k_total;
+        g->decode_rows += static_cast<i64>(g->s_k_total) * g->n_act;
+      }
+    }
+    ex.sync();
+    const int steps = g->s_k_total;
+    if (steps > 0) {
+      for (int i = ex.tid; i < g->n_active_region; i += ex.nthr) {
+        int sid = R->live[i];
+        if (R->st_state[sid] == ST_ACTIVE) {
+          R->st_done[sid] += steps;
+          R->st_rem[sid] -= steps;
+        }
+      }
+    }
+    ex.sync();
+    if (g->s_flag == 1) break;
+    // ---- full epoch: ordered completions, then compaction of the live list
+    const int nreg = g->n_active_region;
+    for (int i = ex.tid; i < nreg; i += ex.nthr) {
+      int sid = R->live[i];
+      R->it_scan_a[i] = (R->st_state[sid] == ST_ACTIVE && R->st_rem[sid] <= 0) ? 1 : 0;
+    }
+    ex.sync();
+    int nf = 0;
+    ex_scan(ex, R->it_scan_a, nreg, &nf);
+    for (int i = ex.tid; i < nreg; i += ex.nthr) {
+      int sid = R->live[i];
+      if (R->st_state[sid] == ST_ACTIVE && R->st_rem[sid] <= 0) {
+        int f = R->it_scan_a[i];
+        R->fins[f] = sid;
+        R->fin_tokens[f] = R->st_done[sid];
+        R->fin_cancel[f] = R->st_cancel[sid];
+        kv_ancestors_adjust(R, sid, -1);
+        atomic_add_i64(&g->sum_done, -static_cast<i64>(R->st_done[sid]));
+        R->st_state[sid] = ST_GONE;
+      }
+    }
+    ex.sync();
+    // compaction: keep ACTIVE and STAGED entries in order
+    const int nl = g->n_live;
+    for (int i = ex.tid; i < nl; i += ex.nthr) {
+      u8 s = R->st_state[R->live[i]];
+      R->it_scan_b[i] = (s == ST_ACTIVE || s == ST_STAGED) ? 1 : 0;
+    }
+    ex.sync();
+    int kept = 0;
+    ex_scan(ex, R->it_scan_b, nl, &kept);
+    for (int i = ex.tid; i < nl; i += ex.nthr) {
+      int sid = R->live[i];
+      u8 s = R->st_state[sid];
+      if (s == ST_ACTIVE || s == ST_STAGED) R->live_tmp[R->it_scan_b[i]] = sid;
+    }
+    ex.sync();
+    for (int i = ex.tid; i < kept; i += ex.nthr) R->live[i] = R->live_tmp[i];
+    if (ex.tid == 0) {
+      g->nfins = nf;
+      g->n_act -= nf;
+      g->n_live = kept;
+      g->n_active_region = g->n_act;  // ACTIVE entries form the prefix
+      g->epochs += 1;
+    }
+    ex.sync();
+    if (nf > 0) break;
+    if (guard > (1 << 24)) {
+      if (ex.tid == 0) set_err(R, ERR_STALLED, -1, kNoNode);
+      ex.sync();
+      break;
+    }
+  }
+  if (ex.tid == 0) g->engine_now = g->s_limit;
+  ex.sync();
+}
+
+// --------------------------------------------------------------- admission
+// executor.cpp:765-783 plus generate_workload seeds (sim.cpp:177-180)
+SPEX_HD void admit_query(Run* R, int q, Rec* rec_slot) {
+  const Cfg& c = R->cfg;
+  QueryRun* qr = &R->qs[q];
+  const u64 base = splitmix64(c.run_seed ^ kSaltQuery);
+  const u64 seed = hash_mix(base, static_cast<u64>(q) + 1);
+  // zero the query
+  char* p = reinterpret_cast<char*>(qr);
+  for (size_t i = 0; i < sizeof(QueryRun); ++i) p[i] = 0;
+  qr->seed = seed;
+  qr->golden = golden_label_of(c, seed);
+  qr->hit_ema = c.initial_hit_ema;
+  qr->admitted = 1;
+  qr->need_followup = 1;
+  qr->nnodes = 1;
+  qr->chain_tip = kNoNode;
+  qr->rest_cur = 0;
+  qr->live_cache = c.prompt_tokens;
+  qr->plan_empty_version = 0xffffffffu;
+  const u32 b = static_cast<u32>(q) * static_cast<u32>(c.node_cap);
+  R->n_parent[b] = kNoNode;
+  R->n_depth[b] = 0;
+  R->n_slot[b] = 0;
+  R->n_tokens[b] = c.prompt_tokens;
+  R->n_status[b] = kCommitted;
+  R->n_flags[b] = NF_GEN_DONE;
+  R->n_reward[b] = 0.0;
+  R->n_value[b] = 0.0;
+  R->n_visits[b] = 0;
+  R->n_hash[b] = splitmix64(seed);
+  R->n_first_child[b] = kNoNode;
+  R->n_last_child[b] = kNoNode;
+  R->n_next_sib[b] = kNoNode;
+  R->n_nchildren[b] = 0;
+  R->n_pred[b] = 0;
+  R->n_stream[b] = -1;
+  R->n_ready[b] = 0;
+  R->n_refc[b] = 0;
+  if (c.family == kRebaseBfs) {
+    R->q_layer[b] = 0;
+    qr->layer_n = 1;
+  }
+  if (rec_slot) {
+    rec_slot->t = R->g->now;
+    rec_slot->x = 0.0;
+    rec_slot->y = seed;
+    rec_slot->q = q;
+    rec_slot->node = kNoNode;
+    rec_slot->a = rec_slot->b = rec_slot->c = 0;
+    rec_slot->kind = EV_ADMIT;
+    rec_slot->flags = 0;
+    rec_slot->pad = 0;
+  }
+}
+
+// ------------------------------------------------------------------ items
+enum ItemKind { IK_FIN = 0, IK_REWARD = 1, IK_FOLLOWUP = 2, IK_SPEC = 3 };
+
+template <class EX>
+SPEX_HD void process_items(Run* R, EX& ex, int n_items, int kind, int rank_filter,
+                           int* warp_off) {
+  GState* g = R->g;
+  const Cfg& c = R->cfg;
+  if (ex.lane == 0) {
+    int* off = warp_off + ex.warp * 3;
+    for (int i = ex.warp; i < n_items; i += ex.nwarp) {
+      if (kind == IK_FIN && R->it_scan_c[i] != rank_filter) continue;
+      if (g->error) break;
+      Item it;
+      const i64 wb = static_cast<i64>(ex.warp) * c.stage_cap;
+      it.rec = R->stage_rec + wb + off[0];
+      it.nrec = 0;
+      it.rec_cap = c.stage_cap - off[0];
+      it.spw = R->stage_spawn + wb + off[1];
+      it.nspw = 0;
+      it.spw_cap = c.stage_cap - off[1];
+      it.psh = R->stage_push + wb + off[2];
+      it.npsh = 0;
+      it.psh_cap = c.stage_cap - off[2];
+      it.sdelta = 0;
+      it.fin = 0;
+      int q;
+      if (kind == IK_FIN) {
+        int sid = R->fins[i];
+        q = R->st_q[sid];
+        QC x = make_qc(R, q, &it, ex.warp);
+        on_stream_done(x, sid, R->fin_tokens[i], R->fin_cancel[i]);
+        R->qs[q].need_followup = 1;
+      } else if (kind == IK_REWARD) {
+        q = R->it_key[i];
+        QC x = make_qc(R, q, &it, ex.warp);
+        on_reward(x, R->ev_node[g->fifo_head - 1]);
+        R->qs[q].need_followup = 1;
+      } else if (kind == IK_FOLLOWUP) {
+        q = R->it_key[i];
+        QC x = make_qc(R, q, &it, ex.warp);
+        followup(x);
+      } else {
+        q = R->it_key[i];
+        QC x = make_qc(R, q, &it, ex.warp);
+        int k = R->qs[q].grant;
+        int n = issue_speculation(x, k);
+        if (n == 0) R->qs[q].plan_empty_version = R->qs[q].version;
+      }
+      R->it_rec_off[i] = static_cast<int>(wb) + off[0];
+      R->it_rec_n[i] = it.nrec;
+      R->it_spawn_off[i] = static_cast<int>(wb) + off[1];
+      R->it_spawn_n[i] = it.nspw;
+      R->it_push_off[i] = static_cast<int>(wb) + off[2];
+      R->it_push_n[i] = it.npsh;
+      R->it_fin[i] = it.fin;
+      R->it_sdelta[i] = it.sdelta;
+      off[0] += it.nrec;
+      off[1] += it.nspw;
+      off[2] += it.npsh;
+    }
+  }
+  ex.sync();
+}
+
+template <class EX>
+SPEX_HD void reset_warp_offsets(Run* R, EX& ex, int* warp_off) {
+  for (int i = ex.tid; i < ex.nwarp * 3; i += ex.nthr) warp_off[i] = 0;
+  ex.sync();
+}
+
+// drain_remaining (executor.cpp:340-360), run by one thread
+SPEX_HD void drain_remaining(Run* R) {
+  GState* g = R->g;
+  for (int j = 0; j < g->n_live; ++j) {
+    int sid = R->live[j];
+    u8 s = R->st_state[sid];
+    if (s != ST_ACTIVE && s != ST_STAGED) continue;
+    const int q = R->st_q[sid];
+    const u32 node = R->st_node[sid];
+    const int part = s == ST_ACTIVE ? R->st_done[sid] : 0;
+    QueryRun* qr = &R->qs[q];
+    qr->generated += part;
+    qr->wasted += part;
+    if (R->cfg.trace) {
+      if (g->log_n >= R->cfg.log_cap) {
+        set_err(R, ERR_CAP_LOG, q, node);
+        return;
+      }
+      Rec* r = &R->log[g->log_n++];
+      r->t = g->now;
+      r->x = 0.0;
+      r->y = 0;
+      r->q = q;
+      r->node = node;
+      r->a = sid;
+      r->b = part;
+      r->c = 0;
+      r->kind = EV_DONE;
+      r->flags = RF_CANCELLED | RF_STALE;
+      r->pad = 0;
+    }
+    R->st_state[sid] = ST_GONE;
+    R->n_stream[static_cast<u32>(q) * static_cast<u32>(R->cfg.node_cap) + node] = -1;
+  }
+  g->n_live = 0;
+  g->n_active_region = 0;
+  g->n_act = 0;
+  g->n_staged = 0;
+}
+
+// Place the staged output of items [0, n) in item order.
+template <class EX>
+SPEX_HD void commit_items(Run* R, EX& ex, int n) {
+  GState* g = R->g;
+  const Cfg& c = R->cfg;
+  const int Q = c.n_queries;
+  // finish ranks -> admissions (finish j admits iff admitted0 + j < Q)
+  for (int i = ex.tid; i < n; i += ex.nthr) R->it_scan_a[i] = R->it_fin[i];
+  ex.sync();
+  int nfin = 0;
+  ex_scan(ex, R->it_scan_a, n, &nfin);
+  const int ac0 = g->admitted_count;
+  for (int i = ex.tid; i < n; i += ex.nthr) {
+    int admit = (R->it_fin[i] && ac0 + R->it_scan_a[i] < Q) ? 1 : 0;
+    R->it_scan_b[i] = R->it_rec_n[i] + (c.trace ? admit : 0);
+    R->it_scan_c[i] = R->it_spawn_n[i];
+    R->it_scan_d[i] = R->it_push_n[i];
+  }
+  ex.sync();
+  int nrec = 0, nspw = 0, npsh = 0;
+  ex_scan(ex, R->it_scan_b, n, &nrec);
+  ex_scan(ex, R->it_scan_c, n, &nspw);
+  ex_scan(ex, R->it_scan_d, n, &npsh);
+  if (c.trace && g->log_n + nrec > c.log_cap) {
+    if (ex.tid == 0) set_err(R, ERR_CAP_LOG, -1, kNoNode);
+    ex.sync();
+    return;
+  }
+  if (g->next_sid + nspw > c.stream_cap) {
+    if (ex.tid == 0) set_err(R, ERR_CAP_STREAMS, -1, kNoNode);
+    ex.sync();
+    return;
+  }
+  const int log0 = g->log_n, sid0 = g->next_sid, live0 = g->n_live, fifo0 = g->fifo_tail;
+  const double now = g->now;
+  const double t_evt = now + c.reward_latency;
+  // parallel placement: one warp per item, lanes over entries
+  for (int i = ex.warp; i < n; i += ex.nwarp) {
+    const int sbase = sid0 + R->it_scan_c[i];
+    if (c.trace) {
+      const int rb = log0 + R->it_scan_b[i];
+      const Rec* src = R->stage_rec + R->it_rec_off[i];
+      for (int j = ex.lane; j < R->it_rec_n[i]; j += ex.lanes) {
+        Rec r = src[j];
+        if (r.flags & RF_LOCAL_SID) {
+          r.a = sbase + r.a;
+          r.flags = static_cast<u8>(r.flags & ~RF_LOCAL_SID);
+        }
+        R->log[rb + j] = r;
+      }
+    }
+    const SpawnRec* sp = R->stage_spawn + R->it_spawn_off[i];
+    for (int j = ex.lane; j < R->it_spawn_n[i]; j += ex.lanes) {
+      const int sid = sbase + j;
+      const SpawnRec s = sp[j];
+      R->st_q[sid] = s.q;
+      R->st_node[sid] = s.node;
+      R->st_rem[sid] = s.tokens;
+      R->st_done[sid] = 0;
+      R->st_cancel[sid] = 0;
+      R->st_ready[sid] = now;
+      R->st_state[sid] = s.cancelled ? ST_GONE : ST_STAGED;
+      R->live[live0 + R->it_scan_c[i] + j] = sid;
+      if (!s.cancelled) {
+        R->n_stream[static_cast<u32>(s.q) * static_cast<u32>(c.node_cap) + s.node] = sid;
+      }
+    }
+    const PushRec* ps = R->stage_push + R->it_push_off[i];
+    for (int j = ex.lane; j < R->it_push_n[i]; j += ex.lanes) {
+      const int pos = fifo0 + R->it_scan_d[i] + j;
+      R->ev_time[pos] = t_evt;
+      R->ev_q[pos] = ps[j].q;
+      R->ev_node[pos] = ps[j].node;
+    }
+    if (ex.lane == 0 && R->it_fin[i] && ac0 + R->it_scan_a[i] < Q) {
+      const int qa = ac0 + R->it_scan_a[i];
+      Rec* slot = c.trace ? &R->log[log0 + R->it_scan_b[i] + R->it_rec_n[i]] : nullptr;
+      admit_query(R, qa, slot);
+    }
+  }
+  int sd = 0;
+  for (int i = ex.tid; i < n; i += ex.nthr) sd += R->it_sdelta[i];
+  i64 sdelta = ex_sum_i64(ex, sd);
+  if (ex.tid == 0) {
+    g->log_n += c.trace ? nrec : 0;
+    g->next_sid += nspw;
+    g->n_live += nspw;
+    g->n_staged += static_cast<int>(sdelta);
+    g->fifo_tail += npsh;
+    int admits = Q - ac0 < nfin ? Q - ac0 : nfin;
+    if (admits < 0) admits = 0;
+    g->admitted_count += admits;
+    g->finished_count += nfin;
+    if (nfin > 0 && g->finished_count == Q) drain_remaining(R);
+  }
+  ex.sync();
+}
+
+// Build the list of queries with `pred` true, in query order, into it_key.
+template <class EX, class Pred>
+SPEX_HD int collect_queries(Run* R, EX& ex, Pred pred) {
+  const int Q = R->cfg.n_queries;
+  for (int q = ex.tid; q < Q; q += ex.nthr) R->it_scan_a[q] = pred(q) ? 1 : 0;
+  ex.sync();
+  int n = 0;
+  ex_scan(ex, R->it_scan_a, Q, &n);
+  for (int q = ex.tid; q < Q; q += ex.nthr)
+    if (pred(q)) R->it_key[R->it_scan_a[q]] = q;
+  ex.sync();
+  return n;
+}
+
+// scheduling_round (executor.cpp:705-740) with allocate_budgets (budget.cpp:45-96)
+template <class EX>
+SPEX_HD void scheduling_round(Run* R, EX& ex, int* warp_off) {
+  GState* g = R->g;
+  const Cfg& c = R->cfg;
+  if (!c.t1) return;
+  const int Q = c.n_queries;
+  for (int q = ex.tid; q < Q; q += ex.nthr) {
+    QueryRun* qr = &R->qs[q];
+    int cand = 0;
+    if (qr->admitted && !qr->finished) {
+      const int outstanding = qr->n_active_exp;
+      const int cap = c.spec_k - outstanding;
+      if (cap > 0) {
+        cand = 1;
+        qr->capacity = cap;
+        qr->pending_specs = outstanding;
+        if (c.t2) qr->kv_bytes = c.kv_bytes_per_token * static_cast<double>(qr->live_cache);
+        qr->grant = cap;
+      }
+    }
+    R->al_cand[q] = cand;
+  }
+  ex.sync();
+  auto is_cand = [&](int q) { return R->al_cand[q] != 0; };
+  const int n = collect_queries(R, ex, is_cand);
+  if (n == 0) return;
+  if (c.t2) {
+    const int idle = c.producer_slots - (g->n_act + g->n_staged);
+    if (idle <= 0) return;
+    // scores (budget.cpp:41-43), min/max
+    double lo = kInf, hi = -kInf;
+    for (int i = ex.tid; i < n; i += ex.nthr) {
+      const QueryRun* qr = &R->qs[R->it_key[i]];
+      double s = qr->capacity * qr->hit_ema * (c.weight_bytes + qr->kv_bytes);
+      R->al_score[i] = s;
+      if (s < lo) lo = s;
+      if (s > hi) hi = s;
+    }
+    lo = ex_minmax_d(ex, lo, false);
+    hi = ex_minmax_d(ex, hi, true);
+    for (int i = ex.tid; i < n; i += ex.nthr) {
+      double norm = hi > lo ? (R->al_score[i] - lo) / (hi - lo) : 0.0;
+      R->al_w[i] = exp_cr(c.tau * norm);
+    }
+    ex.sync();
+    if (ex.tid == 0) {
+      double total = 0.0;
+      for (int i = 0; i < n; ++i) total += R->al_w[i];
+      g->s_total = total;
+    }
+    ex.sync();
+    const double total = g->s_total;
+    i64 fsum = 0;
+    for (int i = ex.tid; i < n; i += ex.nthr) {
+      int f = static_cast<int>(floor(idle * R->al_w[i] / total));
+      fsum += f;
+      const int cap = R->qs[R->it_key[i]].capacity;
+      R->al_out[i] = cap < f ? cap : f;
+    }
+    const i64 floor_sum = ex_sum_i64(ex, fsum);
+    const int leftover = idle - static_cast<int>(floor_sum);
+    if (leftover > 0) {
+      // stable order by raw score, descending
+      for (int i = ex.tid; i < n; i += ex.nthr) {
+        const double si = R->al_score[i];
+        int rank = 0;
+        for (int j = 0; j < n; ++j) {
+          const double sj = R->al_score[j];
+          if (sj > si || (sj == si && j < i)) ++rank;
+        }
+        R->al_order[rank] = i;
+      }
+      ex.sync();
+      if (ex.tid == 0) {
+        int left = leftover;
+        bool progress = true;
+        while (left > 0 && progress) {
+          progress = false;
+          for (int r = 0; r < n; ++r) {
+            if (left == 0) break;
+            const int idx = R->al_order[r];
+            if (R->al_out[idx] < R->qs[R->it_key[idx]].capacity) {
+              R->al_out[idx] += 1;
+              --left;
+              progress = true;
+            }
+          }
+        }
+      }
+      ex.sync();
+    }
+    for (int i = ex.tid; i < n; i += ex.nthr) R->qs[R->it_key[i]].grant = R->al_out[i];
+    ex.sync();
+  }
+  // issue: candidates with a grant and a plan that may be non-empty
+  auto issue = [&](int q) {
+    const QueryRun* qr = &R->qs[q];
+    return R->al_cand[q] != 0 && qr->grant > 0 && qr->version != qr->plan_empty_version;
+  };
+  const int m = collect_queries(R, ex, issue);
+  if (m == 0) return;
+  reset_warp_offsets(R, ex, warp_off);
+  process_items(R, ex, m, IK_SPEC, 0, warp_off);
+  commit_items(R, ex, m);
+}
+
+// consumer_step_followups (executor.cpp:746-763)
+template <class EX>
+SPEX_HD void followups(Run* R, EX& ex, int* warp_off) {
+  for (int pass = 0; pass < 4; ++pass) {
+    auto need = [&](int q) {
+      const QueryRun* qr = &R->qs[q];
+      return qr->admitted && !qr->finished && qr->need_followup;
+    };
+    const int n = collect_queries(R, ex, need);
+    if (n == 0 || R->g->error) break;
+    for (int i = ex.tid; i < n; i += ex.nthr) R->qs[R->it_key[i]].need_followup = 0;
+    ex.sync();
+    reset_warp_offsets(R, ex, warp_off);
+    process_items(R, ex, n, IK_FOLLOWUP, 0, warp_off);
+    commit_items(R, ex, n);
+  }
+  if (!R->g->error) scheduling_round(R, ex, warp_off);
+}
+
+// Completion phase: on_stream_done for fins in order (executor.cpp:794).
+template <class EX>
+SPEX_HD void completions(Run* R, EX& ex, int* warp_off) {
+  GState* g = R->g;
+  const int nf = g->nfins;
+  // rank of each completion among those of the same query
+  if (ex.tid == 0) {
+    int maxr = 0;
+    for (int f = 0; f < nf; ++f) R->qs[R->st_q[R->fins[f]]].grant = 0;
+    for (int f = 0; f < nf; ++f) {
+      QueryRun* qr = &R->qs[R->st_q[R->fins[f]]];
+      R->it_scan_c[f] = qr->grant;
+      qr->grant += 1;
+      if (qr->grant > maxr) maxr = qr->grant;
+    }
+    g->s_flag = maxr;
+  }
+  ex.sync();
+  const int rounds = g->s_flag;
+  reset_warp_offsets(R, ex, warp_off);
+  for (int r = 0; r < rounds; ++r) process_items(R, ex, nf, IK_FIN, r, warp_off);
+  commit_items(R, ex, nf);
+}
+
+// The whole run: admission of the first batch, then the consumer loop.
+template <class EX>
+SPEX_HD void run_loop(Run* R, EX& ex, int* warp_off) {
+  GState* g = R->g;
+  const Cfg& c = R->cfg;
+  const int Q = c.n_queries;
+  if (ex.tid == 0) {
+    const int first = c.batch_size < Q ? c.batch_size : Q;
+    for (int q = 0; q < first; ++q) {
+      Rec* slot = c.trace ? &R->log[g->log_n++] : nullptr;
+      admit_query(R, q, slot);
+    }
+    g->admitted_count = first;
+  }
+  ex.sync();
+  followups(R, ex, warp_off);
+  for (;;) {
+    ex.sync();
+    if (g->error || g->finished_count >= Q) break;
+    if (ex.tid == 0) g->iterations += 1;
+    const double t_evt = g->fifo_head < g->fifo_tail ? R->ev_time[g->fifo_head] : kInf;
+    if (g->n_act + g->n_staged > 0) {
+      engine_advance(R, ex, t_evt);
+      if (g->nfins > 0) {
+        if (ex.tid == 0 && g->now < g->engine_now) g->now = g->engine_now;
+        ex.sync();
+        completions(R, ex, warp_off);
+        followups(R, ex, warp_off);
+        continue;
+      }
+    }
+    if (g->fifo_head >= g->fifo_tail) {
+      if (ex.tid == 0) set_err(R, ERR_STALLED, -1, kNoNode);
+      ex.sync();
+      break;
+    }
+    if (ex.tid == 0) {
+      const int h = g->fifo_head++;
+      const double et = R->ev_time[h];
+      if (g->now < et) g->now = et;
+      if (g->n_act + g->n_staged == 0 && g->engine_now < et) g->engine_now = et;
+      R->it_key[0] = R->ev_q[h];
+      g->reward_events += 1;
+    }
+    ex.sync();
+    reset_warp_offsets(R, ex, warp_off);
+    process_items(R, ex, 1, IK_REWARD, 0, warp_off);
+    commit_items(R, ex, 1);
+    followups(R, ex, warp_off);
+  }
+  if (ex.tid == 0) {
+    double ms = 0.0;
+    for (int q = 0; q < Q; ++q)
+      if (R->qs[q].finished && R->qs[q].finish_time > ms) ms = R->qs[q].finish_time;
+    g->makespan = ms;
+  }
+  ex.sync();
+}
+
+}  // namespace spex

@@ -1,0 +1,982 @@
+// spex_capi.cpp — host side of the C-ABI (include/spex.h).
+//
+// Parses and validates the experiment config exactly like
+// ExperimentConfig::from_json/validate (proj/src/config.cpp:47-275), sizes the
+// device arena, launches the persistent control kernel (ctl_kernel.cu) and
+// serialises the binary event log with the same nlohmann::ordered_json dump
+// the reference's TraceWriter uses (trace.cpp:32-36), so logs compare byte for
+// byte.
+//
+// Built twice:
+//   * product:  nvcc/g++ + ctl_kernel.cu -> libspex_b200.so (device path only)
+//   * SPEX_EMU: g++ only -> build/emu/libspex_emu.so, a TEST-ONLY single-thread
+//     emulation of the same control code used to check logic on a CPU box.
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstdint>
+#include <cstdlib>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include <json.hpp>
+
+#include "../../include/spex.h"
+#include "ctl_state.h"
+
+#ifdef SPEX_EMU
+#include "ctl_run.h"
+#else
+#include <cuda_runtime.h>
+#endif
+
+using nlohmann::ordered_json;
+using namespace spex;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct SpexError {
+  int code;
+  std::string what;
+};
+
+[[noreturn]] void fail(int code, const std::string& msg) { throw SpexError{code, msg}; }
+
+const char* errc_name(int code) {
+  static const char* names[] = {"",
+                                "UnknownParent",
+                                "ParentPruned",
+                                "NotSpeculative",
+                                "UnknownNode",
+                                "IllegalTransition",
+                                "ZeroVisits",
+                                "NoChildren",
+                                "EmptyRewards",
+                                "SearchComplete",
+                                "NothingExpandable",
+                                "UnknownSpeculation",
+                                "NegativeWeight",
+                                "EmptyTally",
+                                "EmptyBatch",
+                                "ConfigInvalid",
+                                "IncompleteLog",
+                                "IoFailure",
+                                "InvalidArgument"};
+  if (code >= 1 && code <= 18) return names[code];
+  switch (code) {
+    case ERR_CAP_NODES: return "CapacityNodes";
+    case ERR_CAP_STREAMS: return "CapacityStreams";
+    case ERR_CAP_LOG: return "CapacityLog";
+    case ERR_CAP_STAGE: return "CapacityStage";
+    case ERR_CAP_LABELS: return "CapacityLabels";
+    case ERR_STALLED: return "NothingExpandable(stalled)";
+    default: return "Internal";
+  }
+}
+
+// ------------------------------------------------------------------ config
+struct HostConfig {
+  // mirrors ExperimentConfig (config.hpp:41-65)
+  int family = kRstarDfs;
+  double exploration_c = 1.0, balance_temperature = 1.0;
+  int width = 4;
+  std::vector<int> depth_widths;
+  int target_answers = 10, max_depth = 16;
+  double token_mu = 4.2485, token_sigma = 0.30;
+  int token_min = 8, token_max = 400, shallow_min = 3;
+  double shallow_p = 0.30;
+  int shallow_max = 9, deep_min = 11;
+  double deep_p = 0.25;
+  int deep_max = 18;
+  double skew = 0.0, golden_density = 0.55, reward_on = 0.8, reward_off = 0.3, noise_sigma = 0.0;
+  double correct_base = 0.95, correct_slope = 0.07, correct_floor = 0.15;
+  int answer_alphabet = 6, prompt_tokens = 32;
+  double weight_bytes = 14e9, mem_bandwidth = 7e11, peak_compute = 1e14, flops_per_token = 14e9,
+         kv_bytes_per_token = 0.0, reward_latency = 0.1;
+  double tau = 2.0, ema_alpha = 0.2, initial_hit_ema = 0.5;
+  double term_alpha = 0.5, min_frac = 0.6;
+  int batch_size = 1, n_queries = 1, spec_k = 8, max_producers = 64;
+  bool t1 = false, t2 = false, t3 = false;
+  std::uint64_t seed = 1;
+  int repetitions = 1;
+};
+
+const char* family_name(int f) {
+  switch (f) {
+    case kRstarDfs: return "rstar_dfs";
+    case kRestHybrid: return "rest_hybrid";
+    default: return "rebase_bfs";
+  }
+}
+
+int family_from_name(const std::string& n) {
+  if (n == "rstar_dfs") return kRstarDfs;
+  if (n == "rest_hybrid") return kRestHybrid;
+  if (n == "rebase_bfs") return kRebaseBfs;
+  fail(ERR_CONFIG_INVALID, "unknown algorithm '" + n + "'");
+}
+
+// config.cpp:139-175
+class SectionReader {
+ public:
+  SectionReader(const ordered_json& j, std::string name) : j_(j), name_(std::move(name)) {
+    if (!j_.is_object()) fail(ERR_CONFIG_INVALID, name_ + ": expected an object");
+  }
+  template <typename T>
+  void field(const char* key, T& out) {
+    known_.push_back(key);
+    auto it = j_.find(key);
+    if (it == j_.end()) return;
+    try {
+      out = it->template get<T>();
+    } catch (const ordered_json::exception&) {
+      fail(ERR_CONFIG_INVALID, name_ + "." + key + ": wrong type");
+    }
+  }
+  void finish() const {
+    for (const auto& [key, value] : j_.items()) {
+      (void)value;
+      bool ok = false;
+      for (const char* k : known_)
+        if (key == k) ok = true;
+      if (!ok) fail(ERR_CONFIG_INVALID, name_ + "." + key + ": unknown key");
+    }
+  }
+
+ private:
+  const ordered_json& j_;
+  std::string name_;
+  std::vector<const char*> known_;
+};
+
+void validate(const HostConfig& c) {
+  auto bad = [](const std::string& w) { fail(ERR_CONFIG_INVALID, w); };
+  // config.cpp:47-71
+  if (c.exploration_c < 0.0) bad("policy.exploration_c: must be >= 0");
+  if (c.balance_temperature <= 0.0) bad("policy.balance_temperature: must be > 0");
+  if (c.width < 1) bad("policy.width: must be >= 1");
+  for (int w : c.depth_widths)
+    if (w < 1) bad("policy.depth_widths: entries must be >= 1");
+  if (c.target_answers < 1) bad("policy.target_answers: must be >= 1");
+  if (c.max_depth < 1) bad("policy.max_depth: must be >= 1");
+  // sim.cpp:88-104
+  if (c.token_min < 1 || c.token_max < c.token_min) bad("workload: bad token bounds");
+  if (!(c.token_sigma >= 0.0) || !std::isfinite(c.token_mu)) bad("workload: bad token distribution");
+  if (c.shallow_min < 1 || c.shallow_max < c.shallow_min) bad("workload: bad shallow depth range");
+  if (c.deep_min <= c.shallow_max || c.deep_max < c.deep_min)
+    bad("workload: deep range must sit above shallow range");
+  if (c.shallow_p < 0.0 || c.shallow_p > 1.0 || c.deep_p < 0.0 || c.deep_p > 1.0)
+    bad("workload: bad stop probability");
+  if (c.skew < 0.0 || c.skew > 1.0) bad("workload: bad skew");
+  if (c.golden_density < 0.0 || c.golden_density > 1.0) bad("workload: bad golden density");
+  if (c.reward_on < 0.0 || c.reward_on > 1.0 || c.reward_off < 0.0 || c.reward_off > 1.0)
+    bad("workload: rewards outside [0,1]");
+  if (c.noise_sigma < 0.0) bad("workload: negative noise sigma");
+  if (c.correct_base <= 0.0 || c.correct_base > 1.0 || c.correct_slope < 0.0 ||
+      c.correct_floor < 0.0 || c.correct_floor > c.correct_base)
+    bad("workload: bad correctness curve");
+  if (c.answer_alphabet < 2) bad("workload: alphabet needs at least two labels");
+  if (c.prompt_tokens < 0) bad("workload: negative prompt length");
+  // budget.cpp:8-19
+  auto pos = [&](double v, const char* n) {
+    if (!(v > 0.0)) bad(std::string(n) + " must be positive");
+  };
+  pos(c.weight_bytes, "weight_bytes");
+  pos(c.mem_bandwidth, "mem_bandwidth");
+  pos(c.peak_compute, "peak_compute");
+  pos(c.flops_per_token, "flops_per_token");
+  if (c.kv_bytes_per_token < 0.0) bad("kv_bytes_per_token must be non-negative");
+  if (c.reward_latency < 0.0) bad("reward_latency must be non-negative");
+  if (c.tau < 0.0) bad("budget.tau: must be >= 0");
+  if (c.ema_alpha <= 0.0 || c.ema_alpha > 1.0) bad("budget.ema_alpha: must be in (0,1]");
+  if (c.initial_hit_ema < 0.0 || c.initial_hit_ema > 1.0) bad("budget.initial_hit_ema: must be in [0,1]");
+  if (c.term_alpha < 0.0) bad("termination.alpha: must be >= 0");
+  if (c.min_frac < 0.0 || c.min_frac > 1.0) bad("termination.min_frac: must be in [0,1]");
+  if (c.batch_size < 1) bad("run.batch_size: must be >= 1");
+  if (c.n_queries < 1) bad("run.n_queries: must be >= 1");
+  if (c.spec_k < 0) bad("run.spec_k: must be >= 0");
+  if (c.max_producers < 1) bad("run.max_producers: must be >= 1");
+  if (c.repetitions < 1) bad("run.repetitions: must be >= 1");
+  // device-path limits (capacity, not semantics)
+  if (c.answer_alphabet > kMaxLabels) fail(ERR_CAP_LABELS, "answer_alphabet > 64 unsupported");
+  if (c.spec_k > 64) fail(ERR_CAP_STAGE, "spec_k > 64 unsupported");
+  if (static_cast<int>(c.depth_widths.size()) > kMaxDepthWidths)
+    fail(ERR_CAP_STAGE, "more than 64 depth_widths unsupported");
+}
+
+// config.cpp:177-275
+HostConfig parse_config(const std::string& text) {
+  ordered_json j = ordered_json::parse(text, nullptr, false);
+  if (j.is_discarded()) fail(ERR_CONFIG_INVALID, "config is not valid JSON");
+  HostConfig c;
+  if (!j.is_object()) fail(ERR_CONFIG_INVALID, "config: expected a JSON object");
+  for (const auto& [key, value] : j.items()) {
+    (void)value;
+    if (key != "family" && key != "policy" && key != "workload" && key != "hardware" &&
+        key != "budget" && key != "termination" && key != "run")
+      fail(ERR_CONFIG_INVALID, key + ": unknown section");
+  }
+  if (j.contains("family")) {
+    if (!j["family"].is_string()) fail(ERR_CONFIG_INVALID, "family: expected a string");
+    c.family = family_from_name(j["family"].get<std::string>());
+  }
+  if (j.contains("policy")) {
+    SectionReader s(j["policy"], "policy");
+    s.field("exploration_c", c.exploration_c);
+    s.field("balance_temperature", c.balance_temperature);
+    s.field("width", c.width);
+    s.field("depth_widths", c.depth_widths);
+    s.field("target_answers", c.target_answers);
+    s.field("max_depth", c.max_depth);
+    s.finish();
+  }
+  if (j.contains("workload")) {
+    SectionReader s(j["workload"], "workload");
+    s.field("token_mu", c.token_mu);
+    s.field("token_sigma", c.token_sigma);
+    s.field("token_min", c.token_min);
+    s.field("token_max", c.token_max);
+    s.field("shallow_min", c.shallow_min);
+    s.field("shallow_p", c.shallow_p);
+    s.field("shallow_max", c.shallow_max);
+    s.field("deep_min", c.deep_min);
+    s.field("deep_p", c.deep_p);
+    s.field("deep_max", c.deep_max);
+    s.field("skew", c.skew);
+    s.field("golden_density", c.golden_density);
+    s.field("reward_on", c.reward_on);
+    s.field("reward_off", c.reward_off);
+    s.field("noise_sigma", c.noise_sigma);
+    s.field("correct_base", c.correct_base);
+    s.field("correct_slope", c.correct_slope);
+    s.field("correct_floor", c.correct_floor);
+    s.field("answer_alphabet", c.answer_alphabet);
+    s.field("prompt_tokens", c.prompt_tokens);
+    s.finish();
+  }
+  if (j.contains("hardware")) {
+    SectionReader s(j["hardware"], "hardware");
+    s.field("weight_bytes", c.weight_bytes);
+    s.field("mem_bandwidth", c.mem_bandwidth);
+    s.field("peak_compute", c.peak_compute);
+    s.field("flops_per_token", c.flops_per_token);
+    s.field("kv_bytes_per_token", c.kv_bytes_per_token);
+    s.field("reward_latency", c.reward_latency);
+    s.finish();
+  }
+  if (j.contains("budget")) {
+    SectionReader s(j["budget"], "budget");
+    s.field("tau", c.tau);
+    s.field("ema_alpha", c.ema_alpha);
+    s.field("initial_hit_ema", c.initial_hit_ema);
+    s.finish();
+  }
+  if (j.contains("termination")) {
+    SectionReader s(j["termination"], "termination");
+    s.field("alpha", c.term_alpha);
+    s.field("min_frac", c.min_frac);
+    s.finish();
+  }
+  if (j.contains("run")) {
+    SectionReader s(j["run"], "run");
+    s.field("batch_size", c.batch_size);
+    s.field("n_queries", c.n_queries);
+    s.field("spec_k", c.spec_k);
+    s.field("max_producers", c.max_producers);
+    s.field("seed", c.seed);
+    s.field("repetitions", c.repetitions);
+    std::vector<std::string> fl;
+    s.field("flags", fl);
+    s.finish();
+    if (j["run"].contains("flags")) {
+      c.t1 = c.t2 = c.t3 = false;
+      for (const std::string& n : fl) {
+        if (n == "t1") c.t1 = true;
+        else if (n == "t2") c.t2 = true;
+        else if (n == "t3") c.t3 = true;
+        else fail(ERR_CONFIG_INVALID, "run.flags: unknown flag " + n);
+      }
+    }
+  }
+  validate(c);
+  return c;
+}
+
+void flags_from_csv(const std::string& csv, HostConfig& c) {
+  c.t1 = c.t2 = c.t3 = false;
+  std::stringstream ss(csv);
+  std::string item;
+  while (std::getline(ss, item, ',')) {
+    if (item.empty()) continue;
+    if (item == "t1") c.t1 = true;
+    else if (item == "t2") c.t2 = true;
+    else if (item == "t3") c.t3 = true;
+    else fail(ERR_CONFIG_INVALID, "unknown flag: " + item);
+  }
+}
+
+// config.cpp:73-137
+ordered_json to_json(const HostConfig& c, bool t1, bool t2, bool t3) {
+  ordered_json j;
+  j["family"] = family_name(c.family);
+  ordered_json p;
+  p["exploration_c"] = c.exploration_c;
+  p["balance_temperature"] = c.balance_temperature;
+  p["width"] = c.width;
+  p["depth_widths"] = c.depth_widths;
+  p["target_answers"] = c.target_answers;
+  p["max_depth"] = c.max_depth;
+  j["policy"] = p;
+  ordered_json w;
+  w["token_mu"] = c.token_mu;
+  w["token_sigma"] = c.token_sigma;
+  w["token_min"] = c.token_min;
+  w["token_max"] = c.token_max;
+  w["shallow_min"] = c.shallow_min;
+  w["shallow_p"] = c.shallow_p;
+  w["shallow_max"] = c.shallow_max;
+  w["deep_min"] = c.deep_min;
+  w["deep_p"] = c.deep_p;
+  w["deep_max"] = c.deep_max;
+  w["skew"] = c.skew;
+  w["golden_density"] = c.golden_density;
+  w["reward_on"] = c.reward_on;
+  w["reward_off"] = c.reward_off;
+  w["noise_sigma"] = c.noise_sigma;
+  w["correct_base"] = c.correct_base;
+  w["correct_slope"] = c.correct_slope;
+  w["correct_floor"] = c.correct_floor;
+  w["answer_alphabet"] = c.answer_alphabet;
+  w["prompt_tokens"] = c.prompt_tokens;
+  j["workload"] = w;
+  ordered_json h;
+  h["weight_bytes"] = c.weight_bytes;
+  h["mem_bandwidth"] = c.mem_bandwidth;
+  h["peak_compute"] = c.peak_compute;
+  h["flops_per_token"] = c.flops_per_token;
+  h["kv_bytes_per_token"] = c.kv_bytes_per_token;
+  h["reward_latency"] = c.reward_latency;
+  j["hardware"] = h;
+  ordered_json b;
+  b["tau"] = c.tau;
+  b["ema_alpha"] = c.ema_alpha;
+  b["initial_hit_ema"] = c.initial_hit_ema;
+  j["budget"] = b;
+  ordered_json t;
+  t["alpha"] = c.term_alpha;
+  t["min_frac"] = c.min_frac;
+  j["termination"] = t;
+  ordered_json r;
+  r["batch_size"] = c.batch_size;
+  r["n_queries"] = c.n_queries;
+  r["spec_k"] = c.spec_k;
+  r["max_producers"] = c.max_producers;
+  std::vector<std::string> fl;
+  if (t1) fl.push_back("t1");
+  if (t2) fl.push_back("t2");
+  if (t3) fl.push_back("t3");
+  r["flags"] = fl;
+  r["seed"] = c.seed;
+  r["repetitions"] = c.repetitions;
+  j["run"] = r;
+  return j;
+}
+
+// budget.cpp:23-39
+int roofline_k_total(const HostConfig& c, int active, double avg_kv, int cap) {
+  double compute_slope = c.flops_per_token / c.peak_compute;
+  double memory_slope = avg_kv / c.mem_bandwidth;
+  double weight_time = c.weight_bytes / c.mem_bandwidth;
+  int b_star;
+  if (compute_slope <= memory_slope) {
+    b_star = cap;
+  } else {
+    double knee = std::ceil(weight_time / (compute_slope - memory_slope));
+    b_star = knee < static_cast<double>(cap) ? static_cast<int>(knee) : cap;
+  }
+  return std::max(0, b_star - active);
+}
+
+std::vector<double>& log_table() {
+  static std::vector<double> tab;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    tab.resize(1 << 16);
+    tab[0] = -HUGE_VAL;
+    for (size_t n = 1; n < tab.size(); ++n) tab[n] = std::log(static_cast<double>(n));
+  });
+  return tab;
+}
+
+// --------------------------------------------------------------- arena
+struct Arena {
+  std::vector<std::pair<void**, size_t>> parts;
+  size_t total = 0;
+  template <class T>
+  void add(T*& p, size_t count) {
+    parts.push_back({reinterpret_cast<void**>(&p), count * sizeof(T)});
+    total += (count * sizeof(T) + 255) & ~size_t(255);
+  }
+  void carve(char* base) {
+    size_t off = 0;
+    for (auto& [pp, bytes] : parts) {
+      *pp = base + off;
+      off += (bytes + 255) & ~size_t(255);
+    }
+  }
+};
+
+}  // namespace
+
+// ================================================================ executor
+struct spex_executor {
+  HostConfig hc;
+  bool t1 = false, t2 = false, t3 = false;
+  std::uint64_t run_seed = 0;
+  int device = 0;
+  bool ran = false;
+  Run run{};  // host copy holding device pointers
+  char* d_base = nullptr;
+  Run* d_run = nullptr;
+  GState* d_g = nullptr;
+  double* d_logtab = nullptr;
+  GState g{};
+  std::vector<Rec> log;
+  std::vector<QueryRun> qs;
+  std::string cfg_dump;
+  double device_ms = 0.0;
+  int nthreads = 512;
+#ifndef SPEX_EMU
+  cudaStream_t stream = nullptr;
+#endif
+};
+
+#ifndef SPEX_EMU
+extern "C" int spex_launch_control(Run* d_run, int nthreads, cudaStream_t stream, float* ms);
+#define CUDA_OK(x)                                                                  \
+  do {                                                                              \
+    cudaError_t e_ = (x);                                                           \
+    if (e_ != cudaSuccess) fail(200, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+#endif
+
+namespace {
+
+void set_cfg(const spex_executor& ex, Cfg& c, int node_cap, int stream_cap, int log_cap,
+             int stage_cap, int trace) {
+  const HostConfig& h = ex.hc;
+  std::memset(&c, 0, sizeof(c));
+  c.family = h.family;
+  c.exploration_c = h.exploration_c;
+  c.balance_temperature = h.balance_temperature;
+  c.width = h.width;
+  c.n_depth_widths = static_cast<int>(h.depth_widths.size());
+  for (int i = 0; i < c.n_depth_widths; ++i) c.depth_widths[i] = h.depth_widths[i];
+  c.target_answers = h.target_answers;
+  c.max_depth = h.max_depth;
+  c.token_mu = h.token_mu;
+  c.token_sigma = h.token_sigma;
+  c.token_min = h.token_min;
+  c.token_max = h.token_max;
+  c.shallow_min = h.shallow_min;
+  c.shallow_p = h.shallow_p;
+  c.shallow_max = h.shallow_max;
+  c.deep_min = h.deep_min;
+  c.deep_p = h.deep_p;
+  c.deep_max = h.deep_max;
+  c.skew = h.skew;
+  c.golden_density = h.golden_density;
+  c.reward_on = h.reward_on;
+  c.reward_off = h.reward_off;
+  c.noise_sigma = h.noise_sigma;
+  c.correct_base = h.correct_base;
+  c.correct_slope = h.correct_slope;
+  c.correct_floor = h.correct_floor;
+  c.answer_alphabet = h.answer_alphabet;
+  c.prompt_tokens = h.prompt_tokens;
+  c.weight_bytes = h.weight_bytes;
+  c.mem_bandwidth = h.mem_bandwidth;
+  c.peak_compute = h.peak_compute;
+  c.flops_per_token = h.flops_per_token;
+  c.kv_bytes_per_token = h.kv_bytes_per_token;
+  c.reward_latency = h.reward_latency;
+  c.tau = h.tau;
+  c.ema_alpha = h.ema_alpha;
+  c.initial_hit_ema = h.initial_hit_ema;
+  c.term_alpha = h.term_alpha;
+  c.min_frac = h.min_frac;
+  c.min_answers = static_cast<int>(std::ceil(h.min_frac * h.target_answers));  // config.cpp:43-45
+  c.batch_size = h.batch_size;
+  c.n_queries = h.n_queries;
+  c.spec_k = h.spec_k;
+  c.max_producers = h.max_producers;
+  c.t1 = ex.t1;
+  c.t2 = ex.t2;
+  c.t3 = ex.t3;
+  // executor.cpp:817-818
+  c.producer_slots = std::max(1, std::min(h.max_producers, roofline_k_total(h, 0, 0.0, 1024)));
+  c.run_seed = ex.run_seed;
+  c.node_cap = node_cap;
+  c.stream_cap = stream_cap;
+  c.log_cap = log_cap;
+  c.stage_cap = stage_cap;
+  c.trace = trace;
+  // std::map<std::string,...> order of "a0".."a{n-1}" (termination.hpp:39)
+  std::vector<std::pair<std::string, int>> names;
+  for (int i = 0; i < h.answer_alphabet; ++i) names.push_back({"a" + std::to_string(i), i});
+  std::sort(names.begin(), names.end());
+  for (int r = 0; r < h.answer_alphabet; ++r) {
+    c.lex_order[r] = names[r].second;
+    c.lex_rank[names[r].second] = r;
+  }
+}
+
+void layout(Arena& A, Run& R, int Q, int node_cap, int stream_cap, int log_cap, int nwarps,
+            int stage_cap) {
+  const size_t NN = static_cast<size_t>(Q) * node_cap;
+  A.add(R.g, 1);
+  A.add(R.n_parent, NN);
+  A.add(R.n_depth, NN);
+  A.add(R.n_slot, NN);
+  A.add(R.n_tokens, NN);
+  A.add(R.n_status, NN);
+  A.add(R.n_flags, NN);
+  A.add(R.n_reward, NN);
+  A.add(R.n_value, NN);
+  A.add(R.n_visits, NN);
+  A.add(R.n_hash, NN);
+  A.add(R.n_first_child, NN);
+  A.add(R.n_last_child, NN);
+  A.add(R.n_next_sib, NN);
+  A.add(R.n_nchildren, NN);
+  A.add(R.n_pred, NN);
+  A.add(R.n_stream, NN);
+  A.add(R.n_ready, NN);
+  A.add(R.n_refc, NN);
+  A.add(R.qs, Q);
+  A.add(R.q_rest_stack, NN);
+  A.add(R.q_layer, NN);
+  A.add(R.q_cohort, NN);
+  const size_t S = stream_cap;
+  A.add(R.st_q, S);
+  A.add(R.st_node, S);
+  A.add(R.st_rem, S);
+  A.add(R.st_done, S);
+  A.add(R.st_state, S);
+  A.add(R.st_cancel, S);
+  A.add(R.st_ready, S);
+  A.add(R.live, S);
+  A.add(R.live_tmp, S);
+  A.add(R.fins, S);
+  A.add(R.fin_tokens, S);
+  A.add(R.fin_cancel, S);
+  A.add(R.ev_time, S);
+  A.add(R.ev_q, S);
+  A.add(R.ev_node, S);
+  A.add(R.log, static_cast<size_t>(log_cap));
+  const size_t W = static_cast<size_t>(nwarps) * stage_cap;
+  A.add(R.stage_rec, W);
+  A.add(R.stage_spawn, W);
+  A.add(R.stage_push, W);
+  const size_t IC = std::max<size_t>(S, Q) + 64;
+  R.item_cap = static_cast<int>(IC);
+  A.add(R.it_key, IC);
+  A.add(R.it_warp, IC);
+  A.add(R.it_rec_off, IC);
+  A.add(R.it_rec_n, IC);
+  A.add(R.it_spawn_off, IC);
+  A.add(R.it_spawn_n, IC);
+  A.add(R.it_push_off, IC);
+  A.add(R.it_push_n, IC);
+  A.add(R.it_fin, IC);
+  A.add(R.it_sdelta, IC);
+  A.add(R.it_scan_a, IC);
+  A.add(R.it_scan_b, IC);
+  A.add(R.it_scan_c, IC);
+  A.add(R.it_scan_d, IC);
+  const size_t SS = static_cast<size_t>(nwarps) * (node_cap + 64);
+  A.add(R.sp_visits, SS);
+  A.add(R.sp_value, SS);
+  A.add(R.sp_nchild, SS);
+  A.add(R.sp_stack, SS);
+  A.add(R.sp_dbl, 3 * SS);
+  A.add(R.sp_int, 3 * SS);
+  A.add(R.al_cand, Q + 64);
+  A.add(R.al_score, Q + 64);
+  A.add(R.al_w, Q + 64);
+  A.add(R.al_out, Q + 64);
+  A.add(R.al_rank, Q + 64);
+  A.add(R.al_order, Q + 64);
+}
+
+std::string label_str(int idx) { return idx < 0 ? std::string() : "a" + std::to_string(idx); }
+
+// TraceWriter::emit (trace.cpp:32-36) with the executor's field order
+// (executor.cpp:134-155,179-186,214-221,244-250,288-292,318-325,346-354,381-403,421-426)
+void serialize(const spex_executor& ex, std::string& out) {
+  out.clear();
+  out.reserve(ex.log.size() * 96 + 4096);
+  {
+    ordered_json j;
+    j["t"] = 0.0;
+    j["ev"] = "run_begin";
+    j["seed"] = ex.run_seed;
+    j["config"] = ordered_json::parse(ex.cfg_dump);
+    out += j.dump();
+    out += '\n';
+  }
+  for (const Rec& r : ex.log) {
+    ordered_json j;
+    j["t"] = r.t;
+    switch (r.kind) {
+      case EV_ADMIT:
+        j["ev"] = "admit";
+        j["q"] = r.q;
+        j["seed"] = static_cast<std::uint64_t>(r.y);
+        break;
+      case EV_NODE:
+        j["ev"] = "node";
+        j["q"] = r.q;
+        j["node"] = r.node;
+        j["parent"] = static_cast<std::uint32_t>(r.a);
+        j["slot"] = r.b;
+        j["spec"] = (r.flags & RF_SPEC) != 0;
+        j["tokens"] = r.c;
+        j["terminal"] = (r.flags & RF_TERMINAL) != 0;
+        break;
+      case EV_REQ:
+        j["ev"] = "req";
+        j["q"] = r.q;
+        j["node"] = r.node;
+        j["stream"] = r.a;
+        j["spec"] = (r.flags & RF_SPEC) != 0;
+        j["dist"] = r.b;
+        break;
+      case EV_DONE:
+        j["ev"] = "done";
+        j["q"] = r.q;
+        j["node"] = r.node;
+        j["stream"] = r.a;
+        j["tokens"] = r.b;
+        j["cancelled"] = (r.flags & RF_CANCELLED) != 0;
+        j["stale"] = (r.flags & RF_STALE) != 0;
+        break;
+      case EV_REWARD:
+        j["ev"] = "reward";
+        j["q"] = r.q;
+        j["node"] = r.node;
+        j["r"] = r.x;
+        break;
+      case EV_PROMOTE:
+        j["ev"] = "promote";
+        j["q"] = r.q;
+        j["node"] = r.node;
+        j["ready"] = static_cast<long long>(r.y);
+        j["dist"] = r.a;
+        break;
+      case EV_PRUNE:
+        j["ev"] = "prune";
+        j["q"] = r.q;
+        j["node"] = r.node;
+        j["count"] = r.a;
+        break;
+      case EV_ANSWER:
+        j["ev"] = "answer";
+        j["q"] = r.q;
+        j["node"] = r.node;
+        j["label"] = label_str(r.a);
+        j["weight"] = r.x;
+        j["correct"] = (r.flags & RF_CORRECT) != 0;
+        break;
+      case EV_TERMINATE:
+        j["ev"] = "terminate";
+        j["q"] = r.q;
+        j["label"] = label_str(r.a);
+        j["answers"] = r.b;
+        break;
+      case EV_QUERY_DONE:
+        j["ev"] = "query_done";
+        j["q"] = r.q;
+        j["label"] = label_str(r.a);
+        j["correct"] = (r.flags & RF_CORRECT) != 0;
+        j["answers"] = r.b;
+        j["early"] = (r.flags & RF_EARLY) != 0;
+        break;
+      default:
+        j["ev"] = "?";
+        break;
+    }
+    out += j.dump();
+    out += '\n';
+  }
+  {
+    long long gen = 0, com = 0, reu = 0, was = 0;
+    for (const QueryRun& q : ex.qs) {
+      gen += q.generated;
+      com += q.committed;
+      reu += q.reused;
+      was += q.wasted;
+    }
+    ordered_json j;
+    j["t"] = ex.g.makespan;
+    j["ev"] = "run_end";
+    j["makespan"] = ex.g.makespan;
+    j["generated"] = gen;
+    j["committed"] = com;
+    j["reused"] = reu;
+    j["wasted"] = was;
+    j["queries"] = ex.g.finished_count;
+    out += j.dump();
+    out += '\n';
+  }
+}
+
+void fill_totals(const spex_executor& ex, spex_totals* t) {
+  std::memset(t, 0, sizeof(*t));
+  t->makespan = ex.g.makespan;
+  for (const QueryRun& q : ex.qs) {
+    if (!q.admitted) continue;
+    t->generated_tokens += q.generated;
+    t->committed_tokens += q.committed;
+    t->reused_tokens += q.reused;
+    t->wasted_tokens += q.wasted;
+    for (int d = 1; d <= SPEX_MAX_TRACKED; ++d) {
+      t->hits[d] += q.hits[d];
+      t->misses[d] += q.misses[d];
+    }
+    if (q.finished) {
+      t->queries += 1;
+      t->correct_votes += q.correct;
+      t->early_terminated += q.early;
+    }
+  }
+}
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const SpexError& e) {
+    g_err = std::string(errc_name(e.code)) + ": " + e.what;
+    return e.code;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return ERR_INTERNAL;
+  }
+}
+
+void run_executor(spex_executor& ex, int trace) {
+  const HostConfig& h = ex.hc;
+  const int Q = h.n_queries;
+  int node_cap = 512;
+  if (const char* e = std::getenv("SPEX_NODE_CAP")) node_cap = std::max(16, std::atoi(e));
+  for (int attempt = 0; attempt < 4; ++attempt) {
+    const long long sc = static_cast<long long>(Q) * (node_cap - 1) + 64;
+    if (sc > (1LL << 30)) fail(ERR_CAP_STREAMS, "stream table too large");
+    const int stream_cap = static_cast<int>(sc);
+    const long long lc = trace ? static_cast<long long>(Q) * node_cap * 6 + 64 : 64;
+    if (lc > (1LL << 31) - 1) fail(ERR_CAP_LOG, "log too large");
+    const int log_cap = static_cast<int>(lc);
+    const int stage_cap = std::max(4096, node_cap * 8);
+    const int nwarps = ex.nthreads / 32;
+    Run R{};
+    set_cfg(ex, R.cfg, node_cap, stream_cap, log_cap, stage_cap, trace);
+    Arena A;
+    layout(A, R, Q, node_cap, stream_cap, log_cap, nwarps, stage_cap);
+    R.nwarps = nwarps;
+    std::vector<double>& tab = log_table();
+    R.log_tab_n = static_cast<int>(tab.size());
+#ifdef SPEX_EMU
+    std::vector<char> mem(A.total + 256);
+    char* base = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(mem.data()) + 255) & ~uintptr_t(255));
+    std::memset(base, 0, A.total);
+    A.carve(base);
+    R.log_tab = tab.data();
+    R.qs[0].admitted = 0;
+    for (int q = 0; q < Q; ++q) R.qs[q].plan_empty_version = 0xffffffffu;
+    std::vector<int> sm(2048);
+    std::vector<double> smd(64);
+    std::vector<i64> sml(64);
+    std::vector<int> warp_off(3 * 64, 0);
+    HostExec hx;
+    hx.sm = sm.data();
+    hx.smd = smd.data();
+    hx.sml = sml.data();
+    auto t0 = std::chrono::steady_clock::now();
+    run_loop(&R, hx, warp_off.data());
+    auto t1 = std::chrono::steady_clock::now();
+    ex.device_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+    ex.g = *R.g;
+    ex.qs.assign(R.qs, R.qs + Q);
+    if (trace) ex.log.assign(R.log, R.log + ex.g.log_n);
+#else
+    CUDA_OK(cudaSetDevice(ex.device));
+    if (!ex.stream) CUDA_OK(cudaStreamCreateWithFlags(&ex.stream, cudaStreamNonBlocking));
+    char* base = nullptr;
+    CUDA_OK(cudaMalloc(&base, A.total + 256));
+    CUDA_OK(cudaMemsetAsync(base, 0, A.total + 256, ex.stream));
+    A.carve(base);
+    double* d_tab = nullptr;
+    CUDA_OK(cudaMalloc(&d_tab, tab.size() * sizeof(double)));
+    CUDA_OK(cudaMemcpyAsync(d_tab, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice,
+                            ex.stream));
+    R.log_tab = d_tab;
+    Run* d_run = nullptr;
+    CUDA_OK(cudaMalloc(&d_run, sizeof(Run)));
+    CUDA_OK(cudaMemcpyAsync(d_run, &R, sizeof(Run), cudaMemcpyHostToDevice, ex.stream));
+    float ms = 0.f;
+    int lr = spex_launch_control(d_run, ex.nthreads, ex.stream, &ms);
+    if (lr != 0) {
+      cudaFree(base);
+      cudaFree(d_tab);
+      cudaFree(d_run);
+      fail(200, std::string("control kernel launch failed: ") + cudaGetErrorString(static_cast<cudaError_t>(lr)));
+    }
+    ex.device_ms = ms;
+    CUDA_OK(cudaMemcpyAsync(&ex.g, R.g, sizeof(GState), cudaMemcpyDeviceToHost, ex.stream));
+    ex.qs.resize(Q);
+    CUDA_OK(cudaMemcpyAsync(ex.qs.data(), R.qs, sizeof(QueryRun) * Q, cudaMemcpyDeviceToHost, ex.stream));
+    CUDA_OK(cudaStreamSynchronize(ex.stream));
+    if (trace && ex.g.log_n > 0) {
+      ex.log.resize(ex.g.log_n);
+      CUDA_OK(cudaMemcpyAsync(ex.log.data(), R.log, sizeof(Rec) * ex.g.log_n, cudaMemcpyDeviceToHost,
+                              ex.stream));
+      CUDA_OK(cudaStreamSynchronize(ex.stream));
+    }
+    cudaFree(base);
+    cudaFree(d_tab);
+    cudaFree(d_run);
+#endif
+    if (ex.g.error == ERR_CAP_NODES || ex.g.error == ERR_CAP_STAGE) {
+      node_cap *= 2;  // capacity, not semantics: rerun with a larger arena
+      ex.log.clear();
+      continue;
+    }
+    if (ex.g.error != 0 && std::getenv("SPEX_DEBUG")) {
+      std::string dump;
+      serialize(ex, dump);
+      std::fprintf(stderr, "%s", dump.c_str());
+    }
+    if (ex.g.error != 0)
+      fail(ex.g.error, "device control error at query " + std::to_string(ex.g.error_q) + " node " +
+                           std::to_string(static_cast<int>(ex.g.error_node)));
+    return;
+  }
+  fail(ERR_CAP_NODES, "node capacity exhausted");
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* spex_last_error(void) { return g_err.c_str(); }
+
+void spex_free(void* p) { std::free(p); }
+
+int spex_device_ok(void) {
+#ifdef SPEX_EMU
+  return 0;
+#else
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) return 0;
+  cudaDeviceProp p{};
+  if (cudaGetDeviceProperties(&p, 0) != cudaSuccess) return 0;
+  return p.major == 10 ? 1 : 0;
+#endif
+}
+
+int spex_canonical_config(const char* config_json, char** out_json) {
+  return guarded([&] {
+    HostConfig c = parse_config(config_json);
+    std::string s = to_json(c, c.t1, c.t2, c.t3).dump();
+    *out_json = static_cast<char*>(std::malloc(s.size() + 1));
+    std::memcpy(*out_json, s.c_str(), s.size() + 1);
+  });
+}
+
+int spex_executor_create(const char* config_json, uint64_t run_seed, const char* flags_csv,
+                         int device, spex_executor** out) {
+  return guarded([&] {
+    auto ex = new spex_executor();
+    try {
+      ex->hc = parse_config(config_json);
+      HostConfig tmp = ex->hc;
+      if (flags_csv) flags_from_csv(flags_csv, tmp);
+      ex->t1 = tmp.t1;
+      ex->t2 = tmp.t2;
+      ex->t3 = tmp.t3;
+      ex->run_seed = run_seed;
+      ex->device = device;
+      ex->cfg_dump = to_json(ex->hc, ex->t1, ex->t2, ex->t3).dump();
+      if (const char* e = std::getenv("SPEX_CTL_THREADS")) ex->nthreads = std::atoi(e);
+    } catch (...) {
+      delete ex;
+      throw;
+    }
+    *out = ex;
+  });
+}
+
+int spex_executor_run(spex_executor* ex, int trace, spex_totals* totals) {
+  return guarded([&] {
+    if (ex->ran) fail(ERR_INVALID_ARGUMENT, "run() may be called once");
+    ex->ran = true;
+    run_executor(*ex, trace);
+    if (totals) fill_totals(*ex, totals);
+  });
+}
+
+int spex_executor_log(spex_executor* ex, char** out_lines, size_t* out_len) {
+  return guarded([&] {
+    std::string s;
+    serialize(*ex, s);
+    *out_lines = static_cast<char*>(std::malloc(s.size() + 1));
+    std::memcpy(*out_lines, s.data(), s.size());
+    (*out_lines)[s.size()] = 0;
+    if (out_len) *out_len = s.size();
+  });
+}
+
+int spex_executor_stats(spex_executor* ex, spex_stats* out) {
+  return guarded([&] {
+    std::memset(out, 0, sizeof(*out));
+    out->iterations = ex->g.iterations;
+    out->epochs = ex->g.epochs;
+    out->reward_events = ex->g.reward_events;
+    out->decode_steps = ex->g.decode_steps;
+    out->decode_rows = ex->g.decode_rows;
+    out->log_records = ex->g.log_n;
+    long long nodes = 0;
+    for (const QueryRun& q : ex->qs) nodes += q.nnodes;
+    out->nodes = nodes;
+    out->device_ms = ex->device_ms;
+  });
+}
+
+void spex_executor_destroy(spex_executor* ex) {
+#ifndef SPEX_EMU
+  if (ex && ex->stream) cudaStreamDestroy(ex->stream);
+#endif
+  delete ex;
+}
+
+int spex_run_once(const char* config_json, uint64_t seed, const char* flags_csv,
+                  spex_totals* totals, char** out_lines) {
+  spex_executor* ex = nullptr;
+  int rc = spex_executor_create(config_json, seed, flags_csv, 0, &ex);
+  if (rc) return rc;
+  rc = spex_executor_run(ex, 1, totals);
+  if (rc == 0 && out_lines) rc = spex_executor_log(ex, out_lines, nullptr);
+  spex_executor_destroy(ex);
+  return rc;
+}
+
+}  // extern "C"
