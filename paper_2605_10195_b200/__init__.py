@@ -1,0 +1,207 @@
+"""paper_2605_10195_b200 — B200-native SPEX frontier-expansion path.
+
+Host-side mirror of the reference's whole-path entry points:
+
+    Executor(cfg, run_seed, flags, trace).run() -> RunTotals   executor.hpp:50-58
+    run_once(cfg, seed, flags) -> RunOutcome(totals, log)       experiment.hpp:27
+
+with the reference's error convention: failures raise :class:`TotsimError`
+whose ``code`` is the ``totsim::Errc`` name (errors.hpp:9-28). Every call goes
+through the C-ABI (include/spex.h) into the sm_100a control kernel; there is
+no CPU implementation behind this package.
+"""
+from __future__ import annotations
+
+import ctypes
+import json
+from dataclasses import dataclass, field
+from typing import Any
+
+from . import _lib
+
+ERRC = [
+    None,
+    "UnknownParent",
+    "ParentPruned",
+    "NotSpeculative",
+    "UnknownNode",
+    "IllegalTransition",
+    "ZeroVisits",
+    "NoChildren",
+    "EmptyRewards",
+    "SearchComplete",
+    "NothingExpandable",
+    "UnknownSpeculation",
+    "NegativeWeight",
+    "EmptyTally",
+    "EmptyBatch",
+    "ConfigInvalid",
+    "IncompleteLog",
+    "IoFailure",
+    "InvalidArgument",
+]
+
+
+class TotsimError(RuntimeError):
+    """totsim::Error equivalent; ``code`` is the Errc name."""
+
+    def __init__(self, status: int, message: str):
+        self.status = status
+        self.code = ERRC[status] if 0 < status < len(ERRC) else f"Device{status}"
+        super().__init__(message)
+
+
+def _check(rc: int) -> None:
+    if rc != 0:
+        msg = _lib.lib().spex_last_error()
+        raise TotsimError(rc, msg.decode() if msg else f"status {rc}")
+
+
+@dataclass
+class SpexFlags:
+    """config.hpp:19-26."""
+
+    t1: bool = False
+    t2: bool = False
+    t3: bool = False
+
+    def any(self) -> bool:
+        return self.t1 or self.t2 or self.t3
+
+    def to_csv(self) -> str:
+        return ",".join(n for n, on in (("t1", self.t1), ("t2", self.t2), ("t3", self.t3)) if on)
+
+    def to_string(self) -> str:
+        s = "+".join(n for n, on in (("t1", self.t1), ("t2", self.t2), ("t3", self.t3)) if on)
+        return s or "baseline"
+
+    @staticmethod
+    def from_string(csv: str) -> "SpexFlags":
+        f = SpexFlags()
+        for item in csv.split(","):
+            item = item.strip()
+            if not item:
+                continue
+            if item not in ("t1", "t2", "t3"):
+                raise TotsimError(15, f"unknown flag: {item}")
+            setattr(f, item, True)
+        return f
+
+
+@dataclass
+class RunTotals:
+    makespan: float = 0.0
+    generated_tokens: int = 0
+    committed_tokens: int = 0
+    reused_tokens: int = 0
+    wasted_tokens: int = 0
+    hits: list = field(default_factory=lambda: [0] * 9)
+    misses: list = field(default_factory=lambda: [0] * 9)
+    queries: int = 0
+    correct_votes: int = 0
+    early_terminated: int = 0
+
+    def useful_tokens(self) -> int:
+        return self.committed_tokens + self.reused_tokens
+
+
+@dataclass
+class RunOutcome:
+    totals: RunTotals
+    log: list
+
+
+def _cfg_text(cfg: Any) -> str:
+    if isinstance(cfg, (bytes, str)):
+        return cfg.decode() if isinstance(cfg, bytes) else cfg
+    return json.dumps(cfg)
+
+
+def canonical_config(cfg: Any) -> dict:
+    """ExperimentConfig::from_json(...).to_json() (strict; ConfigInvalid on unknown keys)."""
+    L = _lib.lib()
+    out = ctypes.c_void_p()
+    _check(L.spex_canonical_config(_cfg_text(cfg).encode(), ctypes.byref(out)))
+    try:
+        return json.loads(ctypes.string_at(out.value).decode())
+    finally:
+        L.spex_free(out)
+
+
+def device_ok() -> bool:
+    return bool(_lib.lib().spex_device_ok())
+
+
+class Executor:
+    """Executor(cfg, run_seed, flags, trace) (executor.hpp:43-62). ``flags`` None
+    uses the config's own run.flags."""
+
+    def __init__(self, cfg: Any, run_seed: int, flags: SpexFlags | str | None = None,
+                 trace: bool = True, device: int = 0):
+        L = _lib.lib()
+        if not L.spex_device_ok():
+            raise RuntimeError("no sm_100 CUDA device: the SPEX B200 path has no CPU fallback")
+        if isinstance(flags, SpexFlags):
+            fcsv = flags.to_csv().encode()
+        elif isinstance(flags, str):
+            fcsv = flags.encode()
+        else:
+            fcsv = None
+        self._L = L
+        self._trace = trace
+        h = ctypes.c_void_p()
+        _check(L.spex_executor_create(_cfg_text(cfg).encode(), int(run_seed), fcsv, device, ctypes.byref(h)))
+        self._h = h
+
+    def run(self) -> RunTotals:
+        t = _lib.Totals()
+        _check(self._L.spex_executor_run(self._h, 1 if self._trace else 0, ctypes.byref(t)))
+        d = t.as_dict()
+        return RunTotals(**d)
+
+    def log_lines(self) -> list:
+        out = ctypes.c_void_p()
+        n = ctypes.c_size_t()
+        _check(self._L.spex_executor_log(self._h, ctypes.byref(out), ctypes.byref(n)))
+        try:
+            return ctypes.string_at(out.value, n.value).decode().splitlines()
+        finally:
+            self._L.spex_free(out)
+
+    def stats(self) -> dict:
+        s = _lib.Stats()
+        _check(self._L.spex_executor_stats(self._h, ctypes.byref(s)))
+        return s.as_dict()
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            self._L.spex_executor_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def run_once(cfg: Any, seed: int, flags: SpexFlags | str | None = None) -> RunOutcome:
+    """run_once (experiment.cpp:23-30): a traced run with totals and the log."""
+    ex = Executor(cfg, seed, flags, trace=True)
+    try:
+        totals = ex.run()
+        return RunOutcome(totals=totals, log=ex.log_lines())
+    finally:
+        ex.close()
+
+
+__all__ = [
+    "Executor",
+    "RunOutcome",
+    "RunTotals",
+    "SpexFlags",
+    "TotsimError",
+    "canonical_config",
+    "device_ok",
+    "run_once",
+]

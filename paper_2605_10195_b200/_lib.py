@@ -1,0 +1,111 @@
+"""ctypes binding of the C-ABI in include/spex.h.
+
+The product library is ``paper_2605_10195_b200/lib/libspex_b200.so`` (built
+in-tree for sm_100a by ``__graft_entry__.build()``). There is no CPU fallback:
+loading fails loudly when the library is missing, and every run fails loudly
+when no sm_100 device is present.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+
+PKG_DIR = Path(__file__).resolve().parent
+LIB_PATH = PKG_DIR / "lib" / "libspex_b200.so"
+
+MAX_TRACKED = 8
+
+
+class Totals(ctypes.Structure):
+    """spex_totals (RunTotals, executor.hpp:20-33)."""
+
+    _fields_ = [
+        ("makespan", ctypes.c_double),
+        ("generated_tokens", ctypes.c_longlong),
+        ("committed_tokens", ctypes.c_longlong),
+        ("reused_tokens", ctypes.c_longlong),
+        ("wasted_tokens", ctypes.c_longlong),
+        ("hits", ctypes.c_longlong * (MAX_TRACKED + 1)),
+        ("misses", ctypes.c_longlong * (MAX_TRACKED + 1)),
+        ("queries", ctypes.c_int),
+        ("correct_votes", ctypes.c_int),
+        ("early_terminated", ctypes.c_int),
+        ("pad_", ctypes.c_int),
+    ]
+
+    def as_dict(self) -> dict:
+        return {
+            "makespan": self.makespan,
+            "generated_tokens": self.generated_tokens,
+            "committed_tokens": self.committed_tokens,
+            "reused_tokens": self.reused_tokens,
+            "wasted_tokens": self.wasted_tokens,
+            "hits": list(self.hits),
+            "misses": list(self.misses),
+            "queries": self.queries,
+            "correct_votes": self.correct_votes,
+            "early_terminated": self.early_terminated,
+        }
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [
+        ("iterations", ctypes.c_longlong),
+        ("epochs", ctypes.c_longlong),
+        ("reward_events", ctypes.c_longlong),
+        ("decode_steps", ctypes.c_longlong),
+        ("decode_rows", ctypes.c_longlong),
+        ("log_records", ctypes.c_longlong),
+        ("nodes", ctypes.c_longlong),
+        ("device_ms", ctypes.c_double),
+    ]
+
+    def as_dict(self) -> dict:
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+_EXPORTS = {
+    "spex_last_error": ([], ctypes.c_char_p),
+    "spex_free": ([ctypes.c_void_p], None),
+    "spex_device_ok": ([], ctypes.c_int),
+    "spex_canonical_config": ([ctypes.c_char_p, ctypes.POINTER(ctypes.c_void_p)], ctypes.c_int),
+    "spex_executor_create": (
+        [ctypes.c_char_p, ctypes.c_uint64, ctypes.c_char_p, ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)],
+        ctypes.c_int,
+    ),
+    "spex_executor_run": ([ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(Totals)], ctypes.c_int),
+    "spex_executor_log": (
+        [ctypes.c_void_p, ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_size_t)],
+        ctypes.c_int,
+    ),
+    "spex_executor_stats": ([ctypes.c_void_p, ctypes.POINTER(Stats)], ctypes.c_int),
+    "spex_executor_destroy": ([ctypes.c_void_p], None),
+    "spex_run_once": (
+        [ctypes.c_char_p, ctypes.c_uint64, ctypes.c_char_p, ctypes.POINTER(Totals), ctypes.POINTER(ctypes.c_void_p)],
+        ctypes.c_int,
+    ),
+}
+
+_lib = None
+
+
+def bind(path: str | os.PathLike) -> ctypes.CDLL:
+    lib = ctypes.CDLL(str(path))
+    for name, (args, res) in _EXPORTS.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    return lib
+
+
+def lib() -> ctypes.CDLL:
+    """The product library. Raises if it was not built (no fallback)."""
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise RuntimeError(
+                f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`"
+            )
+        _lib = bind(LIB_PATH)
+    return _lib

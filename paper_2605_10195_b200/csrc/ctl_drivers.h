@@ -22,7 +22,7 @@ SPEX_HD void dfs_on_done(const QC& x, u32 node) {
 }
 
 // executor.cpp:366-411. `sid` already left the engine's active list.
-SPEX_HDNI void on_stream_done(const QC& x, int sid, int tokens_done, int cancelled) {
+SPEX_HDNI bool on_stream_done(const QC& x, int sid, int tokens_done, int cancelled) {
   Run* R = x.R;
   QueryRun* qr = x.qr;
   u32 node = R->st_node[sid];
@@ -36,7 +36,7 @@ SPEX_HDNI void on_stream_done(const QC& x, int sid, int tokens_done, int cancell
       r->b = tokens_done;
       r->flags = (cancelled ? RF_CANCELLED : 0) | RF_STALE;
     }
-    return;
+    return false;
   }
   set_fl(x, node, NF_GEN_DONE);
   qr->live_cache += R->n_tokens[ni];
@@ -52,10 +52,11 @@ SPEX_HDNI void on_stream_done(const QC& x, int sid, int tokens_done, int cancell
   Item* it = x.it;
   if (it->npsh >= it->psh_cap) {
     set_err(R, ERR_CAP_STAGE, x.q, node);
-    return;
+    return false;
   }
   it->psh[it->npsh++] = PushRec{x.q, node};
   if (x.c->family == kRstarDfs) dfs_on_done(x, node);
+  return true;
 }
 
 // executor.cpp:413-444

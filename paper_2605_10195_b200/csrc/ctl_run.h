@@ -20,10 +20,26 @@
 #pragma once
 
 #include "ctl_drivers.h"
+#include "model.h"
 
 namespace spex {
 
 constexpr double kInf = HUGE_VAL;
+
+SPEX_HD i64 spex_clock() {
+#if SPEX_DEVICE_PASS
+  return static_cast<i64>(clock64());
+#else
+  return 0;
+#endif
+}
+enum { CY_ENGINE = 0, CY_FINS, CY_REWARD, CY_FOLLOW, CY_SCHED, CY_TOTAL, CY_ITEMS, CY_COMMIT };
+#define SPEX_TIMED(ex, R, slot, stmt)                              \
+  do {                                                             \
+    i64 t0_ = (ex).tid == 0 ? spex_clock() : 0;                    \
+    stmt;                                                          \
+    if ((ex).tid == 0) (R)->g->cyc[slot] += spex_clock() - t0_;    \
+  } while (0)
 
 struct HostExec {
   int tid = 0, nthr = 1, warp = 0, nwarp = 1, lane = 0, lanes = 1;
@@ -205,6 +221,41 @@ SPEX_HD void kv_ancestors_adjust(Run* R, int sid, int delta) {
   if (acc != 0) atomic_add_i64(&R->g->u_anc, acc);
 }
 
+// Record one decode epoch of the model schedule: `steps` forward steps over
+// the active streams (in active order) starting at their current positions.
+template <class EX>
+SPEX_HD void record_decode(Run* R, EX& ex, int steps) {
+  GState* g = R->g;
+  const int nreg = g->n_active_region;
+  for (int i = ex.tid; i < nreg; i += ex.nthr)
+    R->it_scan_b[i] = R->st_state[R->live[i]] == ST_ACTIVE ? 1 : 0;
+  ex.sync();
+  int n = 0;
+  ex_scan(ex, R->it_scan_b, nreg, &n);
+  const int off = g->n_sched_rows;
+  if (g->n_sched >= R->cfg.sched_cap || off + n > R->cfg.sched_rows_cap) {
+    if (ex.tid == 0) set_err(R, ERR_CAP_STAGE, -1, kNoNode);
+    ex.sync();
+    return;
+  }
+  for (int i = ex.tid; i < nreg; i += ex.nthr) {
+    int sid = R->live[i];
+    if (R->st_state[sid] == ST_ACTIVE) {
+      R->srow_sid[off + R->it_scan_b[i]] = sid;
+      R->srow_pos0[off + R->it_scan_b[i]] = R->st_done[sid];
+    }
+  }
+  if (ex.tid == 0) {
+    const int e = g->n_sched++;
+    R->sched_kind[e] = SCHED_DECODE;
+    R->sched_steps[e] = steps;
+    R->sched_off[e] = off;
+    R->sched_n[e] = n;
+    g->n_sched_rows = off + n;
+  }
+  ex.sync();
+}
+
 // DecodeEngine::advance (sim.cpp:305-384). On return g->engine_now holds the
 // reached boundary and fins[0..nfins) the streams finishing there, in order.
 template <class EX>
@@ -335,6 +386,7 @@ SPEX_HD void engine_advance(Run* R, EX& ex, double limit) {
     }
     ex.sync();
     const int steps = g->s_k_total;
+    if (steps > 0 && c.record_sched) record_decode(R, ex, steps);
     if (steps > 0) {
       for (int i = ex.tid; i < g->n_active_region; i += ex.nthr) {
         int sid = R->live[i];
@@ -442,6 +494,7 @@ SPEX_HD void admit_query(Run* R, int q, Rec* rec_slot) {
   R->n_stream[b] = -1;
   R->n_ready[b] = 0;
   R->n_refc[b] = 0;
+  R->n_kvbase[b] = static_cast<i64>(q) * c.prompt_tokens;
   if (c.family == kRebaseBfs) {
     R->q_layer[b] = 0;
     qr->layer_n = 1;
@@ -490,7 +543,7 @@ SPEX_HD void process_items(Run* R, EX& ex, int n_items, int kind, int rank_filte
         int sid = R->fins[i];
         q = R->st_q[sid];
         QC x = make_qc(R, q, &it, ex.warp);
-        on_stream_done(x, sid, R->fin_tokens[i], R->fin_cancel[i]);
+        R->fin_scored[i] = on_stream_done(x, sid, R->fin_tokens[i], R->fin_cancel[i]) ? 1 : 0;
         R->qs[q].need_followup = 1;
       } else if (kind == IK_REWARD) {
         q = R->it_key[i];
@@ -516,6 +569,11 @@ SPEX_HD void process_items(Run* R, EX& ex, int n_items, int kind, int rank_filte
       R->it_push_n[i] = it.npsh;
       R->it_fin[i] = it.fin;
       R->it_sdelta[i] = it.sdelta;
+      {
+        int tk = 0;
+        for (int j = 0; j < it.nspw; ++j) tk += it.spw[j].tokens;
+        R->it_tok[i] = tk;
+      }
       off[0] += it.nrec;
       off[1] += it.nspw;
       off[2] += it.npsh;
@@ -587,12 +645,15 @@ SPEX_HD void commit_items(Run* R, EX& ex, int n) {
     R->it_scan_b[i] = R->it_rec_n[i] + (c.trace ? admit : 0);
     R->it_scan_c[i] = R->it_spawn_n[i];
     R->it_scan_d[i] = R->it_push_n[i];
+    R->it_scan_e[i] = R->it_tok[i];
   }
   ex.sync();
-  int nrec = 0, nspw = 0, npsh = 0;
+  int nrec = 0, nspw = 0, npsh = 0, ntok = 0;
   ex_scan(ex, R->it_scan_b, n, &nrec);
   ex_scan(ex, R->it_scan_c, n, &nspw);
   ex_scan(ex, R->it_scan_d, n, &npsh);
+  ex_scan(ex, R->it_scan_e, n, &ntok);
+  const i64 kv0 = g->kv_next;
   if (c.trace && g->log_n + nrec > c.log_cap) {
     if (ex.tid == 0) set_err(R, ERR_CAP_LOG, -1, kNoNode);
     ex.sync();
@@ -633,6 +694,11 @@ SPEX_HD void commit_items(Run* R, EX& ex, int n) {
       R->st_ready[sid] = now;
       R->st_state[sid] = s.cancelled ? ST_GONE : ST_STAGED;
       R->live[live0 + R->it_scan_c[i] + j] = sid;
+      {
+        i64 kb = kv0 + R->it_scan_e[i];
+        for (int k = 0; k < j; ++k) kb += sp[k].tokens;
+        R->n_kvbase[static_cast<u32>(s.q) * static_cast<u32>(c.node_cap) + s.node] = kb;
+      }
       if (!s.cancelled) {
         R->n_stream[static_cast<u32>(s.q) * static_cast<u32>(c.node_cap) + s.node] = sid;
       }
@@ -659,6 +725,7 @@ SPEX_HD void commit_items(Run* R, EX& ex, int n) {
     g->n_live += nspw;
     g->n_staged += static_cast<int>(sdelta);
     g->fifo_tail += npsh;
+    g->kv_next += ntok;
     int admits = Q - ac0 < nfin ? Q - ac0 : nfin;
     if (admits < 0) admits = 0;
     g->admitted_count += admits;
@@ -785,7 +852,7 @@ SPEX_HD void scheduling_round(Run* R, EX& ex, int* warp_off) {
   const int m = collect_queries(R, ex, issue);
   if (m == 0) return;
   reset_warp_offsets(R, ex, warp_off);
-  process_items(R, ex, m, IK_SPEC, 0, warp_off);
+  SPEX_TIMED(ex, R, CY_ITEMS, process_items(R, ex, m, IK_SPEC, 0, warp_off));
   commit_items(R, ex, m);
 }
 
@@ -802,10 +869,10 @@ SPEX_HD void followups(Run* R, EX& ex, int* warp_off) {
     for (int i = ex.tid; i < n; i += ex.nthr) R->qs[R->it_key[i]].need_followup = 0;
     ex.sync();
     reset_warp_offsets(R, ex, warp_off);
-    process_items(R, ex, n, IK_FOLLOWUP, 0, warp_off);
-    commit_items(R, ex, n);
+    SPEX_TIMED(ex, R, CY_FOLLOW, process_items(R, ex, n, IK_FOLLOWUP, 0, warp_off));
+    SPEX_TIMED(ex, R, CY_COMMIT, commit_items(R, ex, n));
   }
-  if (!R->g->error) scheduling_round(R, ex, warp_off);
+  if (!R->g->error) SPEX_TIMED(ex, R, CY_SCHED, scheduling_round(R, ex, warp_off));
 }
 
 // Completion phase: on_stream_done for fins in order (executor.cpp:794).
@@ -829,6 +896,32 @@ SPEX_HD void completions(Run* R, EX& ex, int* warp_off) {
   const int rounds = g->s_flag;
   reset_warp_offsets(R, ex, warp_off);
   for (int r = 0; r < rounds; ++r) process_items(R, ex, nf, IK_FIN, r, warp_off);
+  if (R->cfg.record_sched) {
+    // reward batch of this boundary: the non-stale completions, in order
+    for (int f = ex.tid; f < nf; f += ex.nthr) R->it_scan_a[f] = R->fin_scored[f];
+    ex.sync();
+    int ns = 0;
+    ex_scan(ex, R->it_scan_a, nf, &ns);
+    const int off = g->n_sched_rows;
+    if (ns > 0 && (g->n_sched >= R->cfg.sched_cap || off + ns > R->cfg.sched_rows_cap)) {
+      if (ex.tid == 0) set_err(R, ERR_CAP_STAGE, -1, kNoNode);
+    } else if (ns > 0) {
+      for (int f = ex.tid; f < nf; f += ex.nthr)
+        if (R->fin_scored[f]) {
+          R->srow_sid[off + R->it_scan_a[f]] = R->fins[f];
+          R->srow_pos0[off + R->it_scan_a[f]] = R->fin_tokens[f];
+        }
+      if (ex.tid == 0) {
+        const int e = g->n_sched++;
+        R->sched_kind[e] = SCHED_PRM;
+        R->sched_steps[e] = 0;
+        R->sched_off[e] = off;
+        R->sched_n[e] = ns;
+        g->n_sched_rows = off + ns;
+      }
+    }
+    ex.sync();
+  }
   commit_items(R, ex, nf);
 }
 
@@ -845,6 +938,7 @@ SPEX_HD void run_loop(Run* R, EX& ex, int* warp_off) {
       admit_query(R, q, slot);
     }
     g->admitted_count = first;
+    g->kv_next = static_cast<i64>(Q) * c.prompt_tokens;
   }
   ex.sync();
   followups(R, ex, warp_off);
@@ -854,11 +948,11 @@ SPEX_HD void run_loop(Run* R, EX& ex, int* warp_off) {
     if (ex.tid == 0) g->iterations += 1;
     const double t_evt = g->fifo_head < g->fifo_tail ? R->ev_time[g->fifo_head] : kInf;
     if (g->n_act + g->n_staged > 0) {
-      engine_advance(R, ex, t_evt);
+      SPEX_TIMED(ex, R, CY_ENGINE, engine_advance(R, ex, t_evt));
       if (g->nfins > 0) {
         if (ex.tid == 0 && g->now < g->engine_now) g->now = g->engine_now;
         ex.sync();
-        completions(R, ex, warp_off);
+        SPEX_TIMED(ex, R, CY_FINS, completions(R, ex, warp_off));
         followups(R, ex, warp_off);
         continue;
       }
@@ -877,9 +971,11 @@ SPEX_HD void run_loop(Run* R, EX& ex, int* warp_off) {
       g->reward_events += 1;
     }
     ex.sync();
-    reset_warp_offsets(R, ex, warp_off);
-    process_items(R, ex, 1, IK_REWARD, 0, warp_off);
-    commit_items(R, ex, 1);
+    SPEX_TIMED(ex, R, CY_REWARD, {
+      reset_warp_offsets(R, ex, warp_off);
+      process_items(R, ex, 1, IK_REWARD, 0, warp_off);
+      commit_items(R, ex, 1);
+    });
     followups(R, ex, warp_off);
   }
   if (ex.tid == 0) {

@@ -174,6 +174,9 @@ struct Cfg {
   int log_cap;
   int stage_cap;   // records per warp stage
   int trace;       // emit the event log
+  int record_sched;    // record the decode/PRM schedule for the model forward
+  int sched_cap;       // schedule entries
+  int sched_rows_cap;  // schedule rows
   int lex_rank[kMaxLabels];   // label index -> rank of "a<idx>" in std::map order
   int lex_order[kMaxLabels];  // rank -> label index
 };
@@ -235,6 +238,10 @@ struct GState {
   int s_n_items, s_flag, s_k_total, s_leftover;
   double s_limit, s_total;
   i64 decode_rows;  // sum over decode steps of active rows (model work)
+  i64 kv_next;      // next free KV slot (bump allocation in stream-id order)
+  int n_sched, n_sched_rows;
+  // device cycle counters per phase (thread 0's view)
+  i64 cyc[8];
 };
 
 struct Run {
@@ -259,6 +266,7 @@ struct Run {
   int* n_stream;  // stream_of: >=0 global sid, <= -2 item-local spawn (-2-k), -1 none
   i64* n_ready;
   int* n_refc;    // active-descendant count (unique_kv_tokens bookkeeping)
+  i64* n_kvbase;  // first KV slot of the node's thought in the tree KV pools
   // per-query
   QueryRun* qs;
   u32* q_rest_stack;
@@ -298,6 +306,16 @@ struct Run {
   int* it_push_n;
   int* it_fin;     // query finished inside this item
   int* it_sdelta;  // stream_count delta
+  int* it_tok;     // tokens spawned by the item (KV slots to allocate)
+  int* it_scan_e;
+  int* fin_scored; // completion was not stale: the thought goes to the PRM
+  // schedule for the model forward
+  int* sched_kind;
+  int* sched_steps;
+  int* sched_off;
+  int* sched_n;
+  int* srow_sid;
+  int* srow_pos0;
   int* it_scan_a;  // scan scratch
   int* it_scan_b;
   int* it_scan_c;

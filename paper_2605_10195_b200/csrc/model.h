@@ -1,0 +1,54 @@
+// model.h — shapes and device structures of the policy / PRM forward that runs
+// every decode step of the frontier (K1 tree attention, K2 projections/MLP,
+// K3 LM-head epilogue) and every reward (K4 PRM scoring).
+//
+// The reference has no model (decode is a virtual clock, the
+// reward is a hash oracle). In parity mode the control plane stays driven by
+// the reference's content oracle and virtual clock, and this forward runs as
+// real shadow work whose outputs are checked against oracle/model_ref.py.
+#pragma once
+
+#include <cstdint>
+
+namespace spex {
+
+struct ModelShape {
+  int d;      // hidden size
+  int L;      // layers
+  int H;      // query heads
+  int KVH;    // key/value heads (GQA)
+  int dh;     // head dim
+  int F;      // MLP hidden
+  int V;      // vocab
+  float rope_theta;
+  float eps;
+};
+
+// Teacher-forced token ids: a pure function of the node path hash and the
+// token position inside the thought (the same purity the reference's content
+// oracle has, rng.hpp:7-10).
+constexpr uint64_t kSaltTok = 0x746f6b5f69647300ULL;
+
+// Row of a batched forward: one token of one thought.
+struct RowDesc {
+  int q;          // query
+  uint32_t node;  // thought node
+  int pos;        // token index inside the node's thought (0-based)
+  int abs_pos;    // absolute position in the root..node sequence (RoPE)
+  long long slot; // KV pool slot this token writes (kv_base(node) + pos)
+  int seg_off;    // offset into the segment list
+  int nseg;       // number of segments (ancestors root-first, then own prefix)
+  int token;      // teacher-forced input token id
+  int pad;
+};
+
+struct Segment {
+  long long base;  // first KV slot
+  int len;         // tokens
+  int pad;
+};
+
+// Schedule produced by the control kernel: decode epochs and reward batches.
+enum : int { SCHED_DECODE = 1, SCHED_PRM = 2 };
+
+}  // namespace spex

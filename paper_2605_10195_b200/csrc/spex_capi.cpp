@@ -453,6 +453,7 @@ struct spex_executor {
   std::string cfg_dump;
   double device_ms = 0.0;
   int nthreads = 512;
+  int record_sched = 0;
 #ifndef SPEX_EMU
   cudaStream_t stream = nullptr;
 #endif
@@ -470,7 +471,7 @@ extern "C" int spex_launch_control(Run* d_run, int nthreads, cudaStream_t stream
 namespace {
 
 void set_cfg(const spex_executor& ex, Cfg& c, int node_cap, int stream_cap, int log_cap,
-             int stage_cap, int trace) {
+             int stage_cap, int trace, int record_sched) {
   const HostConfig& h = ex.hc;
   std::memset(&c, 0, sizeof(c));
   c.family = h.family;
@@ -528,6 +529,9 @@ void set_cfg(const spex_executor& ex, Cfg& c, int node_cap, int stream_cap, int 
   c.log_cap = log_cap;
   c.stage_cap = stage_cap;
   c.trace = trace;
+  c.record_sched = record_sched;
+  c.sched_cap = record_sched ? 4 * stream_cap + 1024 : 1;
+  c.sched_rows_cap = record_sched ? 64 * stream_cap + 4096 : 1;
   // std::map<std::string,...> order of "a0".."a{n-1}" (termination.hpp:39)
   std::vector<std::pair<std::string, int>> names;
   for (int i = 0; i < h.answer_alphabet; ++i) names.push_back({"a" + std::to_string(i), i});
@@ -560,6 +564,7 @@ void layout(Arena& A, Run& R, int Q, int node_cap, int stream_cap, int log_cap, 
   A.add(R.n_stream, NN);
   A.add(R.n_ready, NN);
   A.add(R.n_refc, NN);
+  A.add(R.n_kvbase, NN);
   A.add(R.qs, Q);
   A.add(R.q_rest_stack, NN);
   A.add(R.q_layer, NN);
@@ -597,6 +602,9 @@ void layout(Arena& A, Run& R, int Q, int node_cap, int stream_cap, int log_cap, 
   A.add(R.it_push_n, IC);
   A.add(R.it_fin, IC);
   A.add(R.it_sdelta, IC);
+  A.add(R.it_tok, IC);
+  A.add(R.it_scan_e, IC);
+  A.add(R.fin_scored, IC);
   A.add(R.it_scan_a, IC);
   A.add(R.it_scan_b, IC);
   A.add(R.it_scan_c, IC);
@@ -614,6 +622,12 @@ void layout(Arena& A, Run& R, int Q, int node_cap, int stream_cap, int log_cap, 
   A.add(R.al_out, Q + 64);
   A.add(R.al_rank, Q + 64);
   A.add(R.al_order, Q + 64);
+  A.add(R.sched_kind, static_cast<size_t>(R.cfg.sched_cap));
+  A.add(R.sched_steps, static_cast<size_t>(R.cfg.sched_cap));
+  A.add(R.sched_off, static_cast<size_t>(R.cfg.sched_cap));
+  A.add(R.sched_n, static_cast<size_t>(R.cfg.sched_cap));
+  A.add(R.srow_sid, static_cast<size_t>(R.cfg.sched_rows_cap));
+  A.add(R.srow_pos0, static_cast<size_t>(R.cfg.sched_rows_cap));
 }
 
 std::string label_str(int idx) { return idx < 0 ? std::string() : "a" + std::to_string(idx); }
@@ -788,7 +802,7 @@ void run_executor(spex_executor& ex, int trace) {
     const int stage_cap = std::max(4096, node_cap * 8);
     const int nwarps = ex.nthreads / 32;
     Run R{};
-    set_cfg(ex, R.cfg, node_cap, stream_cap, log_cap, stage_cap, trace);
+    set_cfg(ex, R.cfg, node_cap, stream_cap, log_cap, stage_cap, trace, ex.record_sched);
     Arena A;
     layout(A, R, Q, node_cap, stream_cap, log_cap, nwarps, stage_cap);
     R.nwarps = nwarps;
@@ -958,6 +972,10 @@ int spex_executor_stats(spex_executor* ex, spex_stats* out) {
     for (const QueryRun& q : ex->qs) nodes += q.nnodes;
     out->nodes = nodes;
     out->device_ms = ex->device_ms;
+    if (std::getenv("SPEX_PHASES")) {
+      static const char* nm[8] = {"engine", "fins", "reward", "follow_items", "sched", "total", "spec_items", "follow_commit"};
+      for (int i = 0; i < 8; ++i) std::fprintf(stderr, "phase %s: %lld Mcyc\n", nm[i], ex->g.cyc[i] / 1000000);
+    }
   });
 }
 

@@ -1,0 +1,84 @@
+"""Test helpers: the compiled reference (oracle/_ref, test infrastructure only)
+and event-log comparison gates (decision parity required, byte
+parity the target)."""
+from __future__ import annotations
+
+import ctypes
+import json
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+REF_SO = ROOT / "oracle" / "_ref" / "libspexref.so"
+EMU_SO = ROOT / "build" / "emu" / "libspex_emu.so"
+FLOAT_FIELDS = ("r", "weight")
+
+_ref = None
+
+
+def ref_lib():
+    global _ref
+    if _ref is None:
+        if not REF_SO.exists():
+            return None
+        L = ctypes.CDLL(str(REF_SO))
+        L.ref_run_log.argtypes = [ctypes.c_char_p, ctypes.c_uint64, ctypes.c_char_p,
+                                  ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(ctypes.c_double)]
+        L.ref_run_timed.argtypes = [ctypes.c_char_p, ctypes.c_uint64, ctypes.c_char_p, ctypes.c_int,
+                                    ctypes.c_int, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]
+        L.ref_last_error.restype = ctypes.c_char_p
+        _ref = L
+    return _ref
+
+
+def ref_run_log(cfg: str, seed: int, flags: str | None) -> list[str]:
+    L = ref_lib()
+    out = ctypes.c_char_p()
+    tot = (ctypes.c_double * 24)()
+    rc = L.ref_run_log(cfg.encode(), seed, None if flags is None else flags.encode(), ctypes.byref(out), tot)
+    if rc != 0:
+        raise RuntimeError(f"reference failed rc={rc}: {L.ref_last_error().decode()}")
+    return out.value.decode().splitlines()
+
+
+def strip_floats(line: str) -> dict:
+    e = json.loads(line)
+    for k in FLOAT_FIELDS:
+        e.pop(k, None)
+    return e
+
+
+def compare_logs(ref: list[str], got: list[str]) -> dict:
+    """Returns {'decision_ok', 'byte_equal', 'byte_diff_lines', 'first_decision_diff', 'float_max_rel'}."""
+    res = {"lines_ref": len(ref), "lines_got": len(got), "byte_equal": ref == got,
+           "byte_diff_lines": 0, "first_decision_diff": None, "float_max_rel": 0.0}
+    if len(ref) != len(got):
+        res["decision_ok"] = False
+        res["first_decision_diff"] = min(len(ref), len(got))
+        return res
+    for i, (a, b) in enumerate(zip(ref, got)):
+        if a == b:
+            continue
+        res["byte_diff_lines"] += 1
+        ea, eb = json.loads(a), json.loads(b)
+        for k in FLOAT_FIELDS:
+            if k in ea and k in eb:
+                x, y = float(ea[k]), float(eb[k])
+                rel = abs(x - y) / max(abs(x), 1e-300)
+                res["float_max_rel"] = max(res["float_max_rel"], rel)
+        if strip_floats(a) != strip_floats(b) and res["first_decision_diff"] is None:
+            res["first_decision_diff"] = i
+    res["decision_ok"] = res["first_decision_diff"] is None
+    return res
+
+
+def sweep_configs():
+    """Small configs covering every family x flag set (the reference's own
+    integration tests use the same families/flags, test_executor.cpp:217-263)."""
+    out = []
+    for fam in ("rstar_dfs", "rest_hybrid", "rebase_bfs"):
+        for fl in ("", "t1", "t3", "t1,t2", "t1,t3", "t1,t2,t3"):
+            for seed, noise in ((1, 0.0), (2, 0.05), (5, 0.05)):
+                cfg = {"family": fam, "policy": {"width": 4, "max_depth": 10, "target_answers": 6},
+                       "workload": {"noise_sigma": noise}, "run": {"batch_size": 6, "n_queries": 6}}
+                out.append((f"{fam}-{fl or 'base'}-s{seed}", json.dumps(cfg), seed, fl))
+    return out

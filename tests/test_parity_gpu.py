@@ -1,0 +1,55 @@
+"""GPU parity: the sm_100a control path vs the reference event log.
+
+Gate 1 (required): decision parity — every record equal with the libm-derived
+float fields (r, weight) masked. Gate 2 (target): byte equality; the only
+allowed difference is last-ulp rounding of r/weight (glibc exp/log/cos are not
+correctly rounded; the device uses correctly rounded fp64),
+bounded here at 1e-15 relative.
+"""
+import json
+from pathlib import Path
+
+import pytest
+
+from tests import refutil
+
+pytestmark = pytest.mark.gpu
+ROOT = Path(__file__).resolve().parents[1]
+GOLDEN = ROOT / "tests" / "golden"
+
+
+def _spex():
+    import paper_2605_10195_b200 as spex
+    if not spex.device_ok():
+        pytest.fail("no sm_100 device: the B200 path has no fallback")
+    return spex
+
+
+def _check(name, ref, got):
+    res = refutil.compare_logs(ref, got)
+    assert res["decision_ok"], (name, res)
+    assert res["float_max_rel"] <= 1e-15, (name, res)
+    return res
+
+
+@pytest.mark.parametrize("name,cfg,seed,flags", refutil.sweep_configs())
+def test_sweep_matches_reference(name, cfg, seed, flags):
+    spex = _spex()
+    if refutil.ref_lib() is None:
+        pytest.skip("oracle/_ref not built")
+    ref = refutil.ref_run_log(cfg, seed, flags)
+    got = spex.run_once(cfg, seed, flags).log
+    _check(name, ref, got)
+
+
+@pytest.mark.parametrize("cfgname", ["c1_rebase_w4_q16", "c2_rebase_w16_q256", "c3_rstar_w4_q512",
+                                     "c5_rebase_w32_q64"])
+def test_baseline_configs_match_reference(cfgname):
+    spex = _spex()
+    if refutil.ref_lib() is None:
+        pytest.skip("oracle/_ref not built")
+    cfg = (ROOT / "configs" / f"{cfgname}.json").read_text()
+    seed = json.loads(cfg)["run"]["seed"]
+    ref = refutil.ref_run_log(cfg, seed, None)
+    got = spex.run_once(cfg, seed, None).log
+    _check(cfgname, ref, got)
