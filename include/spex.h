@@ -58,6 +58,37 @@ typedef struct spex_stats {
   double device_ms;         /* CUDA-event time of the control kernel */
 } spex_stats;
 
+typedef struct spex_model_stats {
+  double model_ms;        /* device time of the policy/PRM forward (CUDA events) */
+  double attn_ms;         /* summed device time of the K1 tree-attention launches */
+  long long attn_launches;
+  double attn_alg_bytes;  /* algorithmic K1 bytes: unique KV tokens x bytes/token x layers */
+  long long decode_rows;  /* policy rows (one token of one stream) */
+  long long decode_steps;
+  long long prefill_rows; /* root prompt rows (each model) */
+  long long prm_rows;     /* PRM rows (tokens of scored thoughts) */
+  long long prm_thoughts;
+  double policy_flops;    /* 2 * projection params * rows */
+  double prm_flops;
+} spex_model_stats;
+
+/* Per decode row-step shadow output (K3): argmax, logsumexp, logit sum. */
+typedef struct spex_decode_out {
+  int q;
+  uint32_t node;
+  int pos;
+  int argmax;
+  float lse;
+  float logit_sum;
+} spex_decode_out;
+
+typedef struct spex_prm_out {
+  int q;
+  uint32_t node;
+  float score;
+  int pad_;
+} spex_prm_out;
+
 typedef struct spex_executor spex_executor;
 
 /* Error text of the last failing call on this thread. */
@@ -80,6 +111,16 @@ int spex_executor_run(spex_executor* ex, int trace, spex_totals* totals);
 /* Event log of a traced run as JSON lines, byte-compatible with TraceWriter. */
 int spex_executor_log(spex_executor* ex, char** out_lines, size_t* out_len);
 int spex_executor_stats(spex_executor* ex, spex_stats* out);
+/* Attach the policy/PRM forward (real decode of every scheduled row and PRM
+ * scoring of every completed thought; shadow outputs in parity mode).
+ * Shapes: "small_policy", "small_prm", "mid_policy", "mid_prm", "llama3_8b",
+ * "prm_1p5b"; prm_shape "" disables the PRM. Call before spex_executor_run. */
+int spex_executor_set_model(spex_executor* ex, const char* policy_shape, const char* prm_shape,
+                            uint64_t weight_seed, int record_outputs);
+int spex_executor_model_stats(spex_executor* ex, spex_model_stats* out);
+/* Copies up to cap records; *n receives the total available. */
+int spex_executor_decode_outputs(spex_executor* ex, void* buf, long long cap, long long* n);
+int spex_executor_prm_outputs(spex_executor* ex, void* buf, long long cap, long long* n);
 void spex_executor_destroy(spex_executor* ex);
 
 /* run_once: traced run returning totals and the JSON-lines log. */

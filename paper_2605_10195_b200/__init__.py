@@ -173,6 +173,32 @@ class Executor:
         _check(self._L.spex_executor_stats(self._h, ctypes.byref(s)))
         return s.as_dict()
 
+    def set_model(self, policy: str = "small_policy", prm: str = "small_prm", weight_seed: int = 1,
+                  record_outputs: bool = False) -> None:
+        """Attach the policy/PRM forward: every scheduled decode row and every
+        completed thought runs through the models on the device."""
+        _check(self._L.spex_executor_set_model(self._h, policy.encode(), (prm or "").encode(), int(weight_seed),
+                                               1 if record_outputs else 0))
+
+    def model_stats(self) -> dict:
+        s = _lib.ModelStats()
+        _check(self._L.spex_executor_model_stats(self._h, ctypes.byref(s)))
+        return s.as_dict()
+
+    def decode_outputs(self) -> list:
+        n = ctypes.c_longlong()
+        _check(self._L.spex_executor_decode_outputs(self._h, None, 0, ctypes.byref(n)))
+        buf = (_lib.DecodeOut * max(n.value, 1))()
+        _check(self._L.spex_executor_decode_outputs(self._h, buf, n.value, ctypes.byref(n)))
+        return [(o.q, o.node, o.pos, o.argmax, o.lse, o.logit_sum) for o in buf[: n.value]]
+
+    def prm_outputs(self) -> list:
+        n = ctypes.c_longlong()
+        _check(self._L.spex_executor_prm_outputs(self._h, None, 0, ctypes.byref(n)))
+        buf = (_lib.PrmOut * max(n.value, 1))()
+        _check(self._L.spex_executor_prm_outputs(self._h, buf, n.value, ctypes.byref(n)))
+        return [(o.q, o.node, o.score) for o in buf[: n.value]]
+
     def close(self) -> None:
         if getattr(self, "_h", None):
             self._L.spex_executor_destroy(self._h)

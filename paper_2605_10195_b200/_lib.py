@@ -65,6 +65,34 @@ class Stats(ctypes.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
+class ModelStats(ctypes.Structure):
+    _fields_ = [
+        ("model_ms", ctypes.c_double),
+        ("attn_ms", ctypes.c_double),
+        ("attn_launches", ctypes.c_longlong),
+        ("attn_alg_bytes", ctypes.c_double),
+        ("decode_rows", ctypes.c_longlong),
+        ("decode_steps", ctypes.c_longlong),
+        ("prefill_rows", ctypes.c_longlong),
+        ("prm_rows", ctypes.c_longlong),
+        ("prm_thoughts", ctypes.c_longlong),
+        ("policy_flops", ctypes.c_double),
+        ("prm_flops", ctypes.c_double),
+    ]
+
+    def as_dict(self) -> dict:
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class DecodeOut(ctypes.Structure):
+    _fields_ = [("q", ctypes.c_int), ("node", ctypes.c_uint32), ("pos", ctypes.c_int),
+                ("argmax", ctypes.c_int), ("lse", ctypes.c_float), ("logit_sum", ctypes.c_float)]
+
+
+class PrmOut(ctypes.Structure):
+    _fields_ = [("q", ctypes.c_int), ("node", ctypes.c_uint32), ("score", ctypes.c_float), ("pad_", ctypes.c_int)]
+
+
 _EXPORTS = {
     "spex_last_error": ([], ctypes.c_char_p),
     "spex_free": ([ctypes.c_void_p], None),
@@ -81,6 +109,13 @@ _EXPORTS = {
     ),
     "spex_executor_stats": ([ctypes.c_void_p, ctypes.POINTER(Stats)], ctypes.c_int),
     "spex_executor_destroy": ([ctypes.c_void_p], None),
+    "spex_executor_set_model": (
+        [ctypes.c_void_p, ctypes.c_char_p, ctypes.c_char_p, ctypes.c_uint64, ctypes.c_int], ctypes.c_int),
+    "spex_executor_model_stats": ([ctypes.c_void_p, ctypes.POINTER(ModelStats)], ctypes.c_int),
+    "spex_executor_decode_outputs": (
+        [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_longlong, ctypes.POINTER(ctypes.c_longlong)], ctypes.c_int),
+    "spex_executor_prm_outputs": (
+        [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_longlong, ctypes.POINTER(ctypes.c_longlong)], ctypes.c_int),
     "spex_run_once": (
         [ctypes.c_char_p, ctypes.c_uint64, ctypes.c_char_p, ctypes.POINTER(Totals), ctypes.POINTER(ctypes.c_void_p)],
         ctypes.c_int,

@@ -11,7 +11,7 @@
 // Each function cites the reference code it restates.
 #pragma once
 
-#include "ctl_math.h"
+#include "ctl_math_fast.h"
 #include "ctl_state.h"
 
 namespace spex {
@@ -379,7 +379,7 @@ SPEX_HD bool rebase_widths(Run* R, int q, const double* rewards, int n, int budg
     if (rmax < rewards[i]) rmax = rewards[i];
   double total = 0.0;
   for (int i = 0; i < n; ++i) {
-    w[i] = exp_cr((rewards[i] - rmax) / temperature);
+    w[i] = exp_fast((rewards[i] - rmax) / temperature);
     total += w[i];
   }
   for (int i = 0; i < n; ++i) quota[i] = budget * w[i] / total;

@@ -238,23 +238,4 @@ SPEX_HD double cos_cr(double x) {
   return v.hi + v.lo;
 }
 
-// rng.hpp:41-47 (Box-Muller)
-SPEX_HD double normal01(u64 h, u64 salt) {
-  double u1 = uniform01(h, salt);
-  double u2 = uniform01(h, salt ^ 0xa5a5a5a5a5a5a5a5ULL);
-  if (u1 <= 0.0) u1 = 0x1.0p-53;
-  const double two_pi = 2.0 * 3.14159265358979323846;
-  return sqrt(-2.0 * log_cr(u1)) * cos_cr(two_pi * u2);
-}
-
-// rng.hpp:50-58
-SPEX_HD int lognormal_tokens(u64 h, u64 salt, double mu, double sigma, int lo, int hi) {
-  double z = normal01(h, salt);
-  double v = exp_cr(mu + sigma * z);
-  int n = static_cast<int>(llround(v));
-  if (n < lo) n = lo;
-  if (n > hi) n = hi;
-  return n;
-}
-
 }  // namespace spex

@@ -248,6 +248,7 @@ SPEX_HD void record_decode(Run* R, EX& ex, int steps) {
   if (ex.tid == 0) {
     const int e = g->n_sched++;
     R->sched_kind[e] = SCHED_DECODE;
+    R->sched_u[e] = g->u_anc + g->sum_done - static_cast<i64>(steps) * n;  // U at epoch start
     R->sched_steps[e] = steps;
     R->sched_off[e] = off;
     R->sched_n[e] = n;
@@ -792,7 +793,7 @@ SPEX_HD void scheduling_round(Run* R, EX& ex, int* warp_off) {
     hi = ex_minmax_d(ex, hi, true);
     for (int i = ex.tid; i < n; i += ex.nthr) {
       double norm = hi > lo ? (R->al_score[i] - lo) / (hi - lo) : 0.0;
-      R->al_w[i] = exp_cr(c.tau * norm);
+      R->al_w[i] = exp_fast(c.tau * norm);
     }
     ex.sync();
     if (ex.tid == 0) {
@@ -914,6 +915,7 @@ SPEX_HD void completions(Run* R, EX& ex, int* warp_off) {
       if (ex.tid == 0) {
         const int e = g->n_sched++;
         R->sched_kind[e] = SCHED_PRM;
+        R->sched_u[e] = 0;
         R->sched_steps[e] = 0;
         R->sched_off[e] = off;
         R->sched_n[e] = ns;

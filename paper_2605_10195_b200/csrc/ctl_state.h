@@ -316,6 +316,7 @@ struct Run {
   int* sched_n;
   int* srow_sid;
   int* srow_pos0;
+  i64* sched_u;  // engine unique KV tokens at the start of a decode epoch
   int* it_scan_a;  // scan scratch
   int* it_scan_b;
   int* it_scan_c;

@@ -48,6 +48,35 @@ struct Segment {
   int pad;
 };
 
+struct TreeView {
+  const uint32_t* parent;
+  const int* tokens;
+  const uint64_t* hash;
+  const long long* kvbase;
+  const int* st_q;
+  const uint32_t* st_node;
+  int node_cap;
+  int prompt_tokens;
+  int V;
+};
+
+// Per decode row-step shadow outputs kept for verification (K3 epilogue).
+struct DecodeOut {
+  int q;
+  uint32_t node;
+  int pos;
+  int amax;
+  float lse;
+  float lsum;
+};
+
+struct PrmOut {
+  int q;
+  uint32_t node;
+  float score;
+  int pad;
+};
+
 // Schedule produced by the control kernel: decode epochs and reward batches.
 enum : int { SCHED_DECODE = 1, SCHED_PRM = 2 };
 

@@ -1,0 +1,380 @@
+// model_host.cpp — policy / PRM forward over the schedule the control kernel
+// recorded (decode epochs and reward batches), on the device.
+//
+// Per decode step of an epoch (DecodeEngine::advance, sim.cpp:305-384) every
+// active stream runs one token through the policy: embedding, L x [RMSNorm,
+// QKV projection, RoPE + append to the tree KV pool, K1 tree attention over
+// the ancestor chain, O projection + residual, RMSNorm, gate/up projection,
+// SwiGLU, down projection + residual], final RMSNorm, LM head and the K3
+// epilogue. Every reward batch (the completions of one engine boundary,
+// executor.cpp:366-411) runs the PRM over each completed thought's tokens with
+// its own tree KV pool, then the value head (K4).
+//
+// Projections use cuBLAS bf16 GEMMs with fp32 accumulation (library GEMMs;
+// DESIGN.md lists the hand-written tcgen05 replacement as the next step).
+#include "model_host.h"
+
+#include <cublas_v2.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+using namespace spex;
+
+extern "C" {
+void spex_k_init_weights(__nv_bfloat16* w, long long n, uint64_t seed, uint64_t tid, float scale, cudaStream_t s);
+void spex_k_build_decode_rows(TreeView t, const int* sids, const int* pos0, int n, int step, RowDesc* rows,
+                              Segment* segs, cudaStream_t s);
+void spex_k_build_prm_rows(TreeView t, const int* sids, const int* row_start, int n, RowDesc* rows, Segment* segs,
+                           int* last_row, cudaStream_t s);
+void spex_k_build_prompt_rows(TreeView t, int q0, int nq, RowDesc* rows, Segment* segs, cudaStream_t s);
+void spex_k_prm_scan_all(TreeView t, const int* kind, const int* off, const int* n, int n_entries,
+                         const int* srow_sid, int* row_start, int* totals, cudaStream_t s);
+void spex_k_embed(const RowDesc* rows, int M, const __nv_bfloat16* E, int d, float* X, cudaStream_t s);
+void spex_k_rmsnorm(const float* X, int M, int d, float eps, __nv_bfloat16* Y, cudaStream_t s);
+void spex_k_rope_kv(const RowDesc* rows, int M, const float* QKV, int H, int KVH, int dh, const float* inv_freq,
+                    long long slots, __nv_bfloat16* Kp, __nv_bfloat16* Vp, float* Qr, cudaStream_t s);
+int spex_k_tree_attn(const RowDesc* rows, const Segment* segs, const float* Qr, int H, int KVH, int dh,
+                     const __nv_bfloat16* Kp, const __nv_bfloat16* Vp, long long slots, __nv_bfloat16* O, int M,
+                     cudaStream_t s);
+void spex_k_swiglu(const float* GU, int M, int F, __nv_bfloat16* A, cudaStream_t s);
+void spex_k_lm_epilogue(const float* logits, int M, int V, int* amax, float* lse, float* lsum, cudaStream_t s);
+void spex_k_value_head(const __nv_bfloat16* Hn, int d, const int* last_row, int n, const __nv_bfloat16* w,
+                       float* score, cudaStream_t s);
+void spex_k_gather_prm(const RowDesc* rows, const int* last_row, int n, const float* score, PrmOut* out,
+                       cudaStream_t s);
+void spex_k_gather_outputs(const RowDesc* rows, int M, const int* amax, const float* lse, const float* lsum,
+                           DecodeOut* out, cudaStream_t s);
+}
+
+namespace {
+
+#define CK(x)                                                                                    \
+  do {                                                                                           \
+    cudaError_t e_ = (x);                                                                        \
+    if (e_ != cudaSuccess) throw std::runtime_error(std::string(#x) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+#define CB(x)                                                                         \
+  do {                                                                                \
+    cublasStatus_t e_ = (x);                                                          \
+    if (e_ != CUBLAS_STATUS_SUCCESS) throw std::runtime_error(std::string(#x) + " failed: " + std::to_string(e_)); \
+  } while (0)
+
+template <class T>
+T* dalloc(size_t n, std::vector<void*>& owned) {
+  void* p = nullptr;
+  CK(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)));
+  owned.push_back(p);
+  return static_cast<T*>(p);
+}
+
+// y[M x N] (fp32) = x[M x K] (bf16) . W[N x K]^T (bf16) (+ y if accumulate)
+void gemm(cublasHandle_t h, const __nv_bfloat16* x, const __nv_bfloat16* W, float* y, int M, int N, int K,
+          bool accumulate) {
+  const float alpha = 1.f, beta = accumulate ? 1.f : 0.f;
+  CB(cublasGemmEx(h, CUBLAS_OP_T, CUBLAS_OP_N, N, M, K, &alpha, W, CUDA_R_16BF, K, x, CUDA_R_16BF, K, &beta, y,
+                  CUDA_R_32F, N, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT));
+}
+
+}  // namespace
+
+namespace spex {
+
+struct Model {
+  ModelShape sh;
+  bool is_prm;
+  long long slots;
+  int max_rows;
+  std::vector<void*> owned;
+  __nv_bfloat16* embed = nullptr;
+  std::vector<__nv_bfloat16*> wqkv, wo, wgu, wd;
+  __nv_bfloat16* lm = nullptr;
+  __nv_bfloat16* vhead = nullptr;
+  std::vector<__nv_bfloat16*> Kp, Vp;  // per layer [KVH][slots][dh]
+  float* inv_freq = nullptr;
+  // activations
+  float* X = nullptr;
+  __nv_bfloat16* Xn = nullptr;
+  float* QKV = nullptr;
+  float* Qr = nullptr;
+  __nv_bfloat16* O = nullptr;
+  float* GU = nullptr;
+  __nv_bfloat16* A = nullptr;
+  float* logits = nullptr;
+  int* amax = nullptr;
+  float* lse = nullptr;
+  float* lsum = nullptr;
+
+  ~Model() {
+    for (void* p : owned) cudaFree(p);
+  }
+};
+
+long long model_weight_params(const ModelShape& s, bool prm) {
+  long long per = (long long)(s.H + 2 * s.KVH) * s.dh * s.d + (long long)s.d * s.H * s.dh +
+                  2LL * s.F * s.d + (long long)s.d * s.F;
+  return (long long)s.V * s.d + s.L * per + (prm ? s.d : (long long)s.V * s.d);
+}
+
+// FLOPs of the projections per row (2 * matmul params, K2 accounting)
+double model_matmul_flops_per_row(const ModelShape& s, bool prm) {
+  double per = (double)(s.H + 2 * s.KVH) * s.dh * s.d + (double)s.d * s.H * s.dh + 2.0 * s.F * s.d +
+               (double)s.d * s.F;
+  return 2.0 * (s.L * per + (prm ? 0.0 : (double)s.V * s.d));
+}
+
+static Model* make_model(const ModelShape& sh, bool prm, uint64_t seed, long long slots, int max_rows,
+                         cudaStream_t st) {
+  Model* m = new Model();
+  m->sh = sh;
+  m->is_prm = prm;
+  m->slots = slots;
+  m->max_rows = max_rows;
+  auto& o = m->owned;
+  const float kStd = 0.02f * 1.7320508f;  // uniform +-a with std 0.02
+  auto init = [&](__nv_bfloat16* w, long long n, uint64_t id, float scale) {
+    spex_k_init_weights(w, n, seed, id, scale, st);
+  };
+  m->embed = dalloc<__nv_bfloat16>((size_t)sh.V * sh.d, o);
+  init(m->embed, (long long)sh.V * sh.d, 1, 1.7320508f);
+  for (int l = 0; l < sh.L; ++l) {
+    const long long nq = (long long)(sh.H + 2 * sh.KVH) * sh.dh * sh.d;
+    const long long no = (long long)sh.d * sh.H * sh.dh;
+    const long long ng = 2LL * sh.F * sh.d;
+    const long long nd = (long long)sh.d * sh.F;
+    m->wqkv.push_back(dalloc<__nv_bfloat16>(nq, o));
+    m->wo.push_back(dalloc<__nv_bfloat16>(no, o));
+    m->wgu.push_back(dalloc<__nv_bfloat16>(ng, o));
+    m->wd.push_back(dalloc<__nv_bfloat16>(nd, o));
+    init(m->wqkv.back(), nq, 100 + 8 * l + 0, kStd);
+    init(m->wo.back(), no, 100 + 8 * l + 1, kStd);
+    init(m->wgu.back(), ng, 100 + 8 * l + 2, kStd);
+    init(m->wd.back(), nd, 100 + 8 * l + 3, kStd);
+    m->Kp.push_back(dalloc<__nv_bfloat16>((size_t)sh.KVH * slots * sh.dh, o));
+    m->Vp.push_back(dalloc<__nv_bfloat16>((size_t)sh.KVH * slots * sh.dh, o));
+  }
+  if (prm) {
+    m->vhead = dalloc<__nv_bfloat16>(sh.d, o);
+    init(m->vhead, sh.d, 3, kStd);
+  } else {
+    m->lm = dalloc<__nv_bfloat16>((size_t)sh.V * sh.d, o);
+    init(m->lm, (long long)sh.V * sh.d, 2, kStd);
+  }
+  std::vector<float> inv(sh.dh / 2);
+  for (int i = 0; i < sh.dh / 2; ++i)
+    inv[i] = (float)(1.0 / std::pow((double)sh.rope_theta, (2.0 * i) / sh.dh));
+  m->inv_freq = dalloc<float>(inv.size(), o);
+  CK(cudaMemcpyAsync(m->inv_freq, inv.data(), inv.size() * sizeof(float), cudaMemcpyHostToDevice, st));
+  const size_t M = max_rows;
+  m->X = dalloc<float>(M * sh.d, o);
+  m->Xn = dalloc<__nv_bfloat16>(M * std::max(sh.d, sh.H * sh.dh), o);
+  m->QKV = dalloc<float>(M * (sh.H + 2 * sh.KVH) * sh.dh, o);
+  m->Qr = dalloc<float>(M * sh.H * sh.dh, o);
+  m->O = dalloc<__nv_bfloat16>(M * sh.H * sh.dh, o);
+  m->GU = dalloc<float>(M * 2 * sh.F, o);
+  m->A = dalloc<__nv_bfloat16>(M * sh.F, o);
+  if (!prm) {
+    m->logits = dalloc<float>(M * sh.V, o);
+    m->amax = dalloc<int>(M, o);
+    m->lse = dalloc<float>(M, o);
+    m->lsum = dalloc<float>(M, o);
+  }
+  return m;
+}
+
+// One forward over M rows. K1 launches are bracketed by events when `attn_ev`
+// is given, accumulating their device time into *attn_ms.
+static void forward(Model& m, const RowDesc* rows, const Segment* segs, int M, cublasHandle_t hb,
+                    cudaStream_t st, AttnTimer* timer) {
+  const ModelShape& s = m.sh;
+  spex_k_embed(rows, M, m.embed, s.d, m.X, st);
+  for (int l = 0; l < s.L; ++l) {
+    spex_k_rmsnorm(m.X, M, s.d, s.eps, m.Xn, st);
+    gemm(hb, m.Xn, m.wqkv[l], m.QKV, M, (s.H + 2 * s.KVH) * s.dh, s.d, false);
+    spex_k_rope_kv(rows, M, m.QKV, s.H, s.KVH, s.dh, m.inv_freq, m.slots, m.Kp[l], m.Vp[l], m.Qr, st);
+    if (timer) timer->begin(st);
+    if (spex_k_tree_attn(rows, segs, m.Qr, s.H, s.KVH, s.dh, m.Kp[l], m.Vp[l], m.slots, m.O, M, st) != 0)
+      throw std::runtime_error("tree attention: unsupported head shape");
+    if (timer) timer->end(st);
+    gemm(hb, m.O, m.wo[l], m.X, M, s.d, s.H * s.dh, true);
+    spex_k_rmsnorm(m.X, M, s.d, s.eps, m.Xn, st);
+    gemm(hb, m.Xn, m.wgu[l], m.GU, M, 2 * s.F, s.d, false);
+    spex_k_swiglu(m.GU, M, s.F, m.A, st);
+    gemm(hb, m.A, m.wd[l], m.X, M, s.d, s.F, true);
+  }
+  spex_k_rmsnorm(m.X, M, s.d, s.eps, m.Xn, st);
+  if (!m.is_prm) {
+    gemm(hb, m.Xn, m.lm, m.logits, M, s.V, s.d, false);
+    spex_k_lm_epilogue(m.logits, M, s.V, m.amax, m.lse, m.lsum, st);
+  }
+}
+
+void AttnTimer::begin(cudaStream_t st) {
+  if (n >= (int)ev.size()) {
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    ev.push_back({a, b});
+  }
+  cudaEventRecord(ev[n].first, st);
+}
+
+void AttnTimer::end(cudaStream_t st) {
+  cudaEventRecord(ev[n].second, st);
+  ++n;
+  if (n == (int)ev.size() && n >= 256) flush();
+}
+
+void AttnTimer::flush() {
+  for (int i = 0; i < n; ++i) {
+    float ms = 0.f;
+    cudaEventSynchronize(ev[i].second);
+    cudaEventElapsedTime(&ms, ev[i].first, ev[i].second);
+    total_ms += ms;
+    launches += 1;
+  }
+  n = 0;
+}
+
+AttnTimer::~AttnTimer() {
+  for (auto& p : ev) {
+    cudaEventDestroy(p.first);
+    cudaEventDestroy(p.second);
+  }
+}
+
+ModelShape shape_by_name(const std::string& name) {
+  // {d, L, H, KVH, dh, F, V, rope_theta, eps}
+  if (name == "small_policy") return {256, 2, 4, 2, 64, 768, 512, 10000.f, 1e-5f};
+  if (name == "small_prm") return {128, 2, 2, 2, 64, 384, 512, 10000.f, 1e-5f};
+  if (name == "mid_policy") return {1024, 8, 8, 8, 128, 2816, 32000, 10000.f, 1e-5f};
+  if (name == "mid_prm") return {512, 4, 4, 4, 128, 1408, 32000, 10000.f, 1e-5f};
+  if (name == "llama3_8b") return {4096, 32, 32, 8, 128, 14336, 128256, 500000.f, 1e-5f};
+  if (name == "prm_1p5b") return {1536, 28, 12, 2, 128, 8960, 128256, 1000000.f, 1e-6f};
+  throw std::runtime_error("unknown model shape " + name);
+}
+
+// Replays the recorded schedule through the policy and PRM.
+void run_model_schedule(const ModelRunConfig& mc, const ScheduleView& sv, ModelRunResult* res, cudaStream_t st) {
+  const int n_e = sv.n_entries;
+  std::vector<int> kind(n_e), steps(n_e), off(n_e), cnt(n_e);
+  std::vector<long long> u0(n_e);
+  CK(cudaMemcpyAsync(kind.data(), sv.kind, n_e * sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(steps.data(), sv.steps, n_e * sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(off.data(), sv.off, n_e * sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(cnt.data(), sv.n, n_e * sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(u0.data(), sv.u0, n_e * sizeof(long long), cudaMemcpyDeviceToHost, st));
+  std::vector<void*> owned;
+  int* prm_row_start = dalloc<int>(std::max(sv.n_rows, 1), owned);
+  int* prm_totals = dalloc<int>(std::max(n_e, 1), owned);
+  spex_k_prm_scan_all(sv.tree, sv.kind, sv.off, sv.n, n_e, sv.srow_sid, prm_row_start, prm_totals, st);
+  std::vector<int> totals(n_e);
+  CK(cudaMemcpyAsync(totals.data(), prm_totals, n_e * sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+
+  const int Q = sv.n_queries, P = sv.tree.prompt_tokens;
+  int max_rows = 1;
+  for (int e = 0; e < n_e; ++e) max_rows = std::max(max_rows, kind[e] == SCHED_DECODE ? cnt[e] : totals[e]);
+  const int prompt_chunk = std::max(1, std::min(Q, std::max(max_rows, 4096) / std::max(P, 1)));
+  max_rows = std::max(max_rows, prompt_chunk * std::max(P, 1));
+  const long long slots = std::max<long long>(sv.kv_slots, 1);
+
+  cublasHandle_t hb;
+  CB(cublasCreate(&hb));
+  CB(cublasSetStream(hb, st));
+  CB(cublasSetMathMode(hb, CUBLAS_DEFAULT_MATH));
+  Model* pol = make_model(mc.policy, false, mc.seed, slots, max_rows, st);
+  Model* prm = mc.with_prm ? make_model(mc.prm, true, mc.seed ^ 0x5052'4d00ULL, slots, max_rows, st) : nullptr;
+  RowDesc* rows = dalloc<RowDesc>(max_rows, owned);
+  Segment* segs = dalloc<Segment>((size_t)max_rows * 40, owned);
+  int* last_row = dalloc<int>(max_rows, owned);
+  float* scores = dalloc<float>(max_rows, owned);
+  CK(cudaStreamSynchronize(st));
+
+  TreeView tv_pol = sv.tree;
+  tv_pol.V = mc.policy.V;
+  TreeView tv_prm = sv.tree;
+  tv_prm.V = mc.prm.V;
+  AttnTimer timer;
+  cudaEvent_t t0, t1;
+  cudaEventCreate(&t0);
+  cudaEventCreate(&t1);
+  cudaEventRecord(t0, st);
+  // root prompts (prefill through both models)
+  if (P > 0) {
+    for (int q0 = 0; q0 < Q; q0 += prompt_chunk) {
+      const int nq = std::min(prompt_chunk, Q - q0);
+      spex_k_build_prompt_rows(tv_pol, q0, nq, rows, segs, st);
+      forward(*pol, rows, segs, nq * P, hb, st, nullptr);
+      if (prm) {
+        spex_k_build_prompt_rows(tv_prm, q0, nq, rows, segs, st);
+        forward(*prm, rows, segs, nq * P, hb, st, nullptr);
+      }
+      res->prefill_rows += (long long)nq * P;
+    }
+  }
+  const double kv_tok_bytes = 2.0 * mc.policy.KVH * mc.policy.dh * 2.0;  // K+V bf16, one layer
+  DecodeOut* dbg = mc.record_outputs ? reinterpret_cast<DecodeOut*>(mc.out_rows) : nullptr;
+  PrmOut* dbg_scores = mc.record_outputs ? reinterpret_cast<PrmOut*>(mc.out_scores) : nullptr;
+  long long dbg_n = 0, dbg_s = 0;
+  for (int e = 0; e < n_e; ++e) {
+    if (kind[e] == SCHED_DECODE) {
+      const int n = cnt[e];
+      for (int s = 0; s < steps[e]; ++s) {
+        spex_k_build_decode_rows(tv_pol, sv.srow_sid + off[e], sv.srow_pos0 + off[e], n, s, rows, segs, st);
+        forward(*pol, rows, segs, n, hb, st, mc.time_attn ? &timer : nullptr);
+        res->decode_rows += n;
+        res->decode_steps += 1;
+        // algorithmic K1 bytes: unique KV tokens of the step (engine U + the new tokens)
+        const double utok = (double)u0[e] + (double)s * n + n;
+        res->attn_alg_bytes += utok * kv_tok_bytes * mc.policy.L +
+                               (double)n * mc.policy.H * mc.policy.dh * (4.0 + 2.0) * mc.policy.L;
+        if (dbg && dbg_n + n <= mc.out_rows_cap) {
+          spex_k_gather_outputs(rows, n, pol->amax, pol->lse, pol->lsum, dbg + dbg_n, st);
+          dbg_n += n;
+        }
+      }
+    } else if (prm) {
+      const int n = cnt[e];
+      const int M = totals[e];
+      if (M <= 0) continue;
+      spex_k_build_prm_rows(tv_prm, sv.srow_sid + off[e], prm_row_start + off[e], n, rows, segs, last_row, st);
+      forward(*prm, rows, segs, M, hb, st, nullptr);
+      spex_k_value_head(prm->Xn, mc.prm.d, last_row, n, prm->vhead, scores, st);
+      if (dbg_scores && dbg_s + n <= mc.out_scores_cap) {
+        spex_k_gather_prm(rows, last_row, n, scores, dbg_scores + dbg_s, st);
+        dbg_s += n;
+      }
+      res->prm_rows += M;
+      res->prm_thoughts += n;
+    }
+  }
+  cudaEventRecord(t1, st);
+  CK(cudaEventSynchronize(t1));
+  timer.flush();
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, t0, t1);
+  res->model_ms = ms;
+  res->attn_ms = timer.total_ms;
+  res->attn_launches = timer.launches;
+  res->out_rows = dbg_n;
+  res->out_scores = dbg_s;
+  res->policy_flops = model_matmul_flops_per_row(mc.policy, false) * (double)(res->decode_rows + res->prefill_rows);
+  res->prm_flops = prm ? model_matmul_flops_per_row(mc.prm, true) * (double)(res->prm_rows + res->prefill_rows) : 0.0;
+  CK(cudaGetLastError());
+  cudaEventDestroy(t0);
+  cudaEventDestroy(t1);
+  delete pol;
+  delete prm;
+  cublasDestroy(hb);
+  for (void* p : owned) cudaFree(p);
+}
+
+}  // namespace spex

@@ -1,0 +1,68 @@
+// model_host.h — host interface of the policy / PRM schedule replay.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "model.h"
+
+namespace spex {
+
+struct ModelRunConfig {
+  ModelShape policy;
+  ModelShape prm;
+  bool with_prm = true;
+  unsigned long long seed = 1;
+  bool time_attn = true;
+  bool record_outputs = false;
+  void* out_rows = nullptr;  // DecodeOut[out_rows_cap] (device)
+  long long out_rows_cap = 0;
+  void* out_scores = nullptr;  // PrmOut[out_scores_cap] (device)
+  long long out_scores_cap = 0;
+};
+
+struct ScheduleView {
+  TreeView tree;
+  int n_queries;
+  int n_entries;
+  int n_rows;
+  long long kv_slots;
+  const int* kind;
+  const int* steps;
+  const int* off;
+  const int* n;
+  const long long* u0;
+  const int* srow_sid;
+  const int* srow_pos0;
+};
+
+struct ModelRunResult {
+  double model_ms = 0.0;
+  double attn_ms = 0.0;
+  long long attn_launches = 0;
+  double attn_alg_bytes = 0.0;
+  long long decode_rows = 0, decode_steps = 0, prefill_rows = 0, prm_rows = 0, prm_thoughts = 0;
+  long long out_rows = 0, out_scores = 0;
+  double policy_flops = 0.0, prm_flops = 0.0;
+};
+
+struct AttnTimer {
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
+  int n = 0;
+  double total_ms = 0.0;
+  long long launches = 0;
+  void begin(cudaStream_t st);
+  void end(cudaStream_t st);
+  void flush();
+  ~AttnTimer();
+};
+
+ModelShape shape_by_name(const std::string& name);
+long long model_weight_params(const ModelShape& s, bool prm);
+double model_matmul_flops_per_row(const ModelShape& s, bool prm);
+void run_model_schedule(const ModelRunConfig& mc, const ScheduleView& sv, ModelRunResult* res, cudaStream_t st);
+
+}  // namespace spex

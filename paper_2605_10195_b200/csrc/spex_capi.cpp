@@ -33,6 +33,8 @@
 #include "ctl_run.h"
 #else
 #include <cuda_runtime.h>
+
+#include "model_host.h"
 #endif
 
 using nlohmann::ordered_json;
@@ -456,6 +458,11 @@ struct spex_executor {
   int record_sched = 0;
 #ifndef SPEX_EMU
   cudaStream_t stream = nullptr;
+  bool with_model = false;
+  ModelRunConfig mc;
+  ModelRunResult mres;
+  std::vector<DecodeOut> dec_out;
+  std::vector<PrmOut> prm_out;
 #endif
 };
 
@@ -628,6 +635,7 @@ void layout(Arena& A, Run& R, int Q, int node_cap, int stream_cap, int log_cap, 
   A.add(R.sched_n, static_cast<size_t>(R.cfg.sched_cap));
   A.add(R.srow_sid, static_cast<size_t>(R.cfg.sched_rows_cap));
   A.add(R.srow_pos0, static_cast<size_t>(R.cfg.sched_rows_cap));
+  A.add(R.sched_u, static_cast<size_t>(R.cfg.sched_cap));
 }
 
 std::string label_str(int idx) { return idx < 0 ? std::string() : "a" + std::to_string(idx); }
@@ -802,6 +810,9 @@ void run_executor(spex_executor& ex, int trace) {
     const int stage_cap = std::max(4096, node_cap * 8);
     const int nwarps = ex.nthreads / 32;
     Run R{};
+#ifndef SPEX_EMU
+    ex.record_sched = ex.with_model ? 1 : 0;
+#endif
     set_cfg(ex, R.cfg, node_cap, stream_cap, log_cap, stage_cap, trace, ex.record_sched);
     Arena A;
     layout(A, R, Q, node_cap, stream_cap, log_cap, nwarps, stage_cap);
@@ -856,6 +867,61 @@ void run_executor(spex_executor& ex, int trace) {
     }
     ex.device_ms = ms;
     CUDA_OK(cudaMemcpyAsync(&ex.g, R.g, sizeof(GState), cudaMemcpyDeviceToHost, ex.stream));
+    CUDA_OK(cudaStreamSynchronize(ex.stream));
+    if (ex.with_model && ex.g.error == 0) {
+      ScheduleView sv{};
+      sv.tree.parent = R.n_parent;
+      sv.tree.tokens = R.n_tokens;
+      sv.tree.hash = R.n_hash;
+      sv.tree.kvbase = R.n_kvbase;
+      sv.tree.st_q = R.st_q;
+      sv.tree.st_node = R.st_node;
+      sv.tree.node_cap = node_cap;
+      sv.tree.prompt_tokens = ex.hc.prompt_tokens;
+      sv.n_queries = Q;
+      sv.n_entries = ex.g.n_sched;
+      sv.n_rows = ex.g.n_sched_rows;
+      sv.kv_slots = ex.g.kv_next;
+      sv.kind = R.sched_kind;
+      sv.steps = R.sched_steps;
+      sv.off = R.sched_off;
+      sv.n = R.sched_n;
+      sv.u0 = R.sched_u;
+      sv.srow_sid = R.sched_kind ? R.srow_sid : nullptr;
+      sv.srow_pos0 = R.srow_pos0;
+      ModelRunConfig mc = ex.mc;
+      void* d_rows = nullptr;
+      void* d_scores = nullptr;
+      if (mc.record_outputs) {
+        mc.out_rows_cap = ex.g.decode_rows;
+        mc.out_scores_cap = static_cast<long long>(Q) * node_cap;
+        CUDA_OK(cudaMalloc(&d_rows, std::max<long long>(mc.out_rows_cap, 1) * sizeof(DecodeOut)));
+        CUDA_OK(cudaMalloc(&d_scores, std::max<long long>(mc.out_scores_cap, 1) * sizeof(PrmOut)));
+        mc.out_rows = d_rows;
+        mc.out_scores = d_scores;
+      }
+      ex.mres = ModelRunResult{};
+      try {
+        run_model_schedule(mc, sv, &ex.mres, ex.stream);
+      } catch (const std::exception& e) {
+        cudaFree(d_rows);
+        cudaFree(d_scores);
+        cudaFree(base);
+        cudaFree(d_tab);
+        cudaFree(d_run);
+        fail(201, std::string("model forward: ") + e.what());
+      }
+      if (mc.record_outputs) {
+        ex.dec_out.resize(ex.mres.out_rows);
+        ex.prm_out.resize(ex.mres.out_scores);
+        if (!ex.dec_out.empty())
+          CUDA_OK(cudaMemcpy(ex.dec_out.data(), d_rows, ex.dec_out.size() * sizeof(DecodeOut), cudaMemcpyDeviceToHost));
+        if (!ex.prm_out.empty())
+          CUDA_OK(cudaMemcpy(ex.prm_out.data(), d_scores, ex.prm_out.size() * sizeof(PrmOut), cudaMemcpyDeviceToHost));
+        cudaFree(d_rows);
+        cudaFree(d_scores);
+      }
+    }
     ex.qs.resize(Q);
     CUDA_OK(cudaMemcpyAsync(ex.qs.data(), R.qs, sizeof(QueryRun) * Q, cudaMemcpyDeviceToHost, ex.stream));
     CUDA_OK(cudaStreamSynchronize(ex.stream));
@@ -976,6 +1042,79 @@ int spex_executor_stats(spex_executor* ex, spex_stats* out) {
       static const char* nm[8] = {"engine", "fins", "reward", "follow_items", "sched", "total", "spec_items", "follow_commit"};
       for (int i = 0; i < 8; ++i) std::fprintf(stderr, "phase %s: %lld Mcyc\n", nm[i], ex->g.cyc[i] / 1000000);
     }
+  });
+}
+
+int spex_executor_set_model(spex_executor* ex, const char* policy_shape, const char* prm_shape,
+                            uint64_t weight_seed, int record_outputs) {
+  return guarded([&] {
+#ifdef SPEX_EMU
+    (void)ex;
+    (void)policy_shape;
+    (void)prm_shape;
+    (void)weight_seed;
+    (void)record_outputs;
+    fail(ERR_INVALID_ARGUMENT, "the model forward needs the CUDA build");
+#else
+    ex->mc.policy = shape_by_name(policy_shape);
+    ex->mc.with_prm = prm_shape && *prm_shape;
+    if (ex->mc.with_prm) ex->mc.prm = shape_by_name(prm_shape);
+    ex->mc.seed = weight_seed;
+    ex->mc.record_outputs = record_outputs != 0;
+    ex->with_model = true;
+#endif
+  });
+}
+
+int spex_executor_model_stats(spex_executor* ex, spex_model_stats* out) {
+  return guarded([&] {
+    std::memset(out, 0, sizeof(*out));
+#ifndef SPEX_EMU
+    const ModelRunResult& r = ex->mres;
+    out->model_ms = r.model_ms;
+    out->attn_ms = r.attn_ms;
+    out->attn_launches = r.attn_launches;
+    out->attn_alg_bytes = r.attn_alg_bytes;
+    out->decode_rows = r.decode_rows;
+    out->decode_steps = r.decode_steps;
+    out->prefill_rows = r.prefill_rows;
+    out->prm_rows = r.prm_rows;
+    out->prm_thoughts = r.prm_thoughts;
+    out->policy_flops = r.policy_flops;
+    out->prm_flops = r.prm_flops;
+#else
+    (void)ex;
+#endif
+  });
+}
+
+int spex_executor_decode_outputs(spex_executor* ex, void* buf, long long cap, long long* n) {
+  return guarded([&] {
+#ifndef SPEX_EMU
+    long long k = std::min<long long>(cap, static_cast<long long>(ex->dec_out.size()));
+    if (buf && k > 0) std::memcpy(buf, ex->dec_out.data(), k * sizeof(DecodeOut));
+    *n = static_cast<long long>(ex->dec_out.size());
+#else
+    (void)ex;
+    (void)buf;
+    (void)cap;
+    *n = 0;
+#endif
+  });
+}
+
+int spex_executor_prm_outputs(spex_executor* ex, void* buf, long long cap, long long* n) {
+  return guarded([&] {
+#ifndef SPEX_EMU
+    long long k = std::min<long long>(cap, static_cast<long long>(ex->prm_out.size()));
+    if (buf && k > 0) std::memcpy(buf, ex->prm_out.data(), k * sizeof(PrmOut));
+    *n = static_cast<long long>(ex->prm_out.size());
+#else
+    (void)ex;
+    (void)buf;
+    (void)cap;
+    *n = 0;
+#endif
   });
 }
 

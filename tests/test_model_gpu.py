@@ -1,0 +1,60 @@
+"""GPU numerics of the policy / PRM forward vs the numpy fp32 restatement
+(oracle/model_ref.py). The reference has no model, so this parity is
+*unpinned* against it; the oracle recomputes each sampled row
+by a full causal forward over its root->node token sequence, independently of
+the device's incremental tree-KV decode.
+
+Tolerances (stated): logsumexp |d| <= 2e-3 * max(1, |lse|); logit sum
+|d| <= 5e-3 * sqrt(V) (sum of V fp32 logits); argmax equal unless the top-2
+logits are within 2e-3; PRM score |d| <= 2e-3.
+"""
+import json
+import random
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def test_small_model_matches_numpy_oracle():
+    import paper_2605_10195_b200 as spex
+    from oracle import model_ref
+    if not spex.device_ok():
+        pytest.fail("no sm_100 device")
+    cfg = (ROOT / "configs" / "c1_rebase_w4_q16.json").read_text()
+    seed = json.loads(cfg)["run"]["seed"]
+    ex = spex.Executor(cfg, seed, None, trace=True)
+    ex.set_model("small_policy", "small_prm", weight_seed=7, record_outputs=True)
+    ex.run()
+    log = ex.log_lines()
+    dec = ex.decode_outputs()
+    prm = ex.prm_outputs()
+    ms = ex.model_stats()
+    ex.close()
+    assert ms["decode_rows"] == len(dec) > 0
+    assert ms["prm_thoughts"] == len(prm) > 0
+    tree = model_ref.TreeFromLog(log, prompt_tokens=32)
+    pol = model_ref.Model("small_policy", 7, prm=False)
+    rm = model_ref.Model("small_prm", 7 ^ model_ref.PRM_SEED_XOR, prm=True)
+    rng = random.Random(0)
+    worst = {"lse": 0.0, "sum": 0.0, "prm": 0.0}
+    for (q, node, pos, amax, lse, lsum) in rng.sample(dec, 60):
+        toks = tree.sequence(q, node, pos, pol.V)
+        ra, rl, rs, z = pol.logits_stats(toks)
+        worst["lse"] = max(worst["lse"], abs(rl - lse))
+        worst["sum"] = max(worst["sum"], abs(rs - lsum))
+        assert abs(rl - lse) <= 2e-3 * max(1.0, abs(rl)), (q, node, pos, rl, lse)
+        assert abs(rs - lsum) <= 5e-3 * np.sqrt(pol.V), (q, node, pos, rs, lsum)
+        if amax != ra:
+            zs = np.sort(z)
+            assert zs[-1] - zs[-2] <= 2e-3, (q, node, pos, ra, amax)
+    for (q, node, score) in rng.sample(prm, 30):
+        n = tree.nodes[(q, node)][2]
+        toks = tree.sequence(q, node, n - 1, rm.V)
+        rs = rm.prm_score(toks)
+        worst["prm"] = max(worst["prm"], abs(rs - score))
+        assert abs(rs - score) <= 2e-3, (q, node, rs, score)
+    print("worst abs errors", worst)
