@@ -1,0 +1,337 @@
+#!/usr/bin/env python
+"""bench.py — ToT queries/sec of the B200 frontier-expansion path (BASELINE.json metric).
+
+One *step* = one complete batched ToT search over the config's query batch on
+one GPU: the device-resident control kernel (decode engine, rewards, REBASE /
+REST / RSTAR drivers, T1 speculation, T2 budgets, T3 termination) plus the real
+policy decode of every scheduled row (K1 tree attention, projections, LM-head
+epilogue) and PRM scoring of every completed thought (K4). The workload is
+BASELINE config 2 (rebase_bfs, width 16, T1, 256 queries) with the builder's
+mid-size random-init policy/PRM (the config names no model).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 runs one process per GPU (torchrun): each rank searches a disjoint query
+set (run seed + rank; weak scaling, no data-path collective); rank 0 prints the
+line with the max-over-ranks time. `--impl reference` times the reference's own
+CPU implementation (oracle/_ref, compiled from the reference sources) on all
+host cores for the same config and metric.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+DEFAULT_CONFIG = "c2_rebase_w16_q256"
+PEAKS = ROOT / "MEASURED_PEAKS.json"
+PROFILE_TRAFFIC = ROOT / "profiles" / "k1_traffic.json"
+HBM_FALLBACK_GBS = 6650.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default=DEFAULT_CONFIG)
+    ap.add_argument("--policy", default="mid_policy")
+    ap.add_argument("--prm", default="mid_prm")
+    ap.add_argument("--cpu-sample-runs", type=int, default=4)
+    return ap.parse_args()
+
+
+def dist_env():
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), int(
+        os.environ.get("LOCAL_RANK", "0"))
+
+
+class Clocks:
+    """nvidia-smi sampling of SM clocks and throttle reasons during the timed region."""
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 9:
+                continue
+            try:
+                sm.append(float(p[1]))
+                mx = float(p[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, p[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def load_peaks():
+    try:
+        return json.loads(PEAKS.read_text()), "measured"
+    except Exception:
+        return {"hbm_gbs": HBM_FALLBACK_GBS, "bf16_tflops": 1590.0}, "fallback"
+
+
+# ----------------------------------------------------------------- reference arm
+def ref_lib():
+    so = ROOT / "oracle" / "_ref" / "libspexref.so"
+    if not so.exists():
+        return None
+    L = ctypes.CDLL(str(so))
+    L.ref_run_timed.argtypes = [ctypes.c_char_p, ctypes.c_uint64, ctypes.c_char_p, ctypes.c_int, ctypes.c_int,
+                                ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]
+    return L
+
+
+def ref_runs(cfg_text: str, seeds, threads: int):
+    """Independent reference runs (Executor::run, trace off) on `threads` host
+    threads (ctypes releases the GIL), like run_experiment_full's OpenMP loop."""
+    L = ref_lib()
+    queries = [0.0] * len(seeds)
+    lock = threading.Lock()
+    it = iter(list(enumerate(seeds)))
+
+    def worker():
+        while True:
+            with lock:
+                try:
+                    i, s = next(it)
+                except StopIteration:
+                    return
+            secs = ctypes.c_double()
+            tot = (ctypes.c_double * 24)()
+            rc = L.ref_run_timed(cfg_text.encode(), s, None, 0, 1, ctypes.byref(secs), tot)
+            if rc != 0:
+                raise RuntimeError(f"reference run failed rc={rc}")
+            queries[i] = tot[5]
+    t0 = time.perf_counter()
+    ths = [threading.Thread(target=worker) for _ in range(threads)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    return sum(queries), time.perf_counter() - t0
+
+
+def cpu_baseline(cfg_text: str, seed: int, runs: int):
+    if ref_lib() is None:
+        return None
+    q, secs = ref_runs(cfg_text, [seed + i for i in range(runs)], 1)
+    return {"value": q / secs, "unit": "queries/s", "cores": 1, "kind": "reference",
+            "sample": f"{runs} single-thread Executor::run of the same config (seeds {seed}..{seed + runs - 1}), "
+                      f"{secs:.1f} s; the reference decode is a virtual clock (no model compute)"}
+
+
+def run_reference(args, cfg_text, seed, rank, world):
+    if rank != 0:
+        return
+    ncores = os.cpu_count() or 1
+    metric = "ToT queries/sec"
+    if ref_lib() is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libspexref.so not built"}))
+        return
+    per_step = ncores
+    for _ in range(args.warmup):
+        ref_runs(cfg_text, [seed + i for i in range(per_step)], ncores)
+    tq, tt = 0.0, 0.0
+    for k in range(args.steps):
+        q, s = ref_runs(cfg_text, [seed + 1000 * k + i for i in range(per_step)], ncores)
+        tq += q
+        tt += s
+    v = tq / tt
+    line = {"metric": metric, "value": v, "unit": "queries/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1000 * tt / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "fp64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": args.config, "queries_per_search": json.loads(cfg_text)["run"]["n_queries"],
+                       "searches_per_step": per_step},
+            "cpu_baseline": {"value": v, "unit": "queries/s", "cores": ncores, "kind": "reference",
+                             "sample": f"{per_step} concurrent Executor::run per step on {ncores} host threads"},
+            "e2e": {"value": v, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------ ours
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    cfg_text = (ROOT / "configs" / f"{args.config}.json").read_text()
+    cfg = json.loads(cfg_text)
+    base_seed = cfg["run"]["seed"]
+    seed = base_seed + rank  # disjoint query sets per rank (weak scaling)
+    if args.impl == "reference":
+        run_reference(args, cfg_text, base_seed, rank, world)
+        return
+
+    import torch
+    import paper_2605_10195_b200 as spex
+    torch.cuda.set_device(local)
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        pg = dist
+
+    def barrier():
+        torch.cuda.synchronize()
+        if pg:
+            pg.barrier()
+
+    def one_search(trace: bool):
+        ex = spex.Executor(cfg_text, seed, None, trace=trace, device=local)
+        ex.set_model(args.policy, args.prm, weight_seed=1)
+        tot = ex.run()
+        d2h = 0
+        if trace:
+            log = ex.log_lines()  # the run's event log, copied back and serialised
+            d2h = ex.stats()["log_records"] * 48
+        st, ms = ex.stats(), ex.model_stats()
+        ex.close()
+        return tot, st, ms, d2h
+
+    for _ in range(args.warmup):
+        one_search(False)
+    barrier()
+    peaks, peak_src = load_peaks()
+    with Clocks(local) as clk:
+        # device-resident value: inputs (config, weights, pools) already on the GPU
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
+        t0 = time.perf_counter()
+        agg = {"queries": 0, "ctl_ms": 0.0, "model_ms": 0.0, "attn_ms": 0.0, "attn_bytes": 0.0,
+               "launches": 0, "flops": 0.0, "decode_rows": 0, "prm_rows": 0, "attn_launches": 0}
+        for _ in range(args.steps):
+            tot, st, ms, _ = one_search(False)
+            agg["queries"] += tot.queries
+            agg["ctl_ms"] += st["device_ms"]
+            agg["model_ms"] += ms["model_ms"]
+            agg["attn_ms"] += ms["attn_ms"]
+            agg["attn_bytes"] += ms["attn_alg_bytes"]
+            agg["attn_launches"] += ms["attn_launches"]
+            agg["launches"] += 1 + ms["launches"]
+            agg["flops"] += ms["policy_flops"] + ms["prm_flops"]
+            agg["decode_rows"] += ms["decode_rows"]
+            agg["prm_rows"] += ms["prm_rows"]
+        barrier()
+        wall = time.perf_counter() - t0
+        # device time of the step = control kernel + forward (both CUDA-event timed)
+        dev_s = (agg["ctl_ms"] + agg["model_ms"]) / 1000.0
+        # end to end through the C-ABI with the traced run and the log copied back
+        barrier()
+        t1 = time.perf_counter()
+        e2e_q, e2e_d2h = 0, 0
+        for _ in range(args.steps):
+            tot, st, ms, d2h = one_search(True)
+            e2e_q += tot.queries
+            e2e_d2h += d2h
+        barrier()
+        e2e_wall = time.perf_counter() - t1
+    times = torch.tensor([dev_s, wall, e2e_wall], dtype=torch.float64, device="cuda")
+    if pg:
+        pg.all_reduce(times, op=pg.ReduceOp.MAX)
+        qt = torch.tensor([float(agg["queries"]), float(e2e_q)], dtype=torch.float64, device="cuda")
+        pg.all_reduce(qt)
+        total_q, total_e2e_q = qt.tolist()
+    else:
+        total_q, total_e2e_q = float(agg["queries"]), float(e2e_q)
+    dev_s, wall, e2e_wall = times.tolist()
+    if rank != 0:
+        return
+    achieved = agg["attn_bytes"] / (agg["attn_ms"] / 1000.0) / 1e9 if agg["attn_ms"] > 0 else 0.0
+    traffic = None
+    if PROFILE_TRAFFIC.exists():
+        try:
+            traffic = json.loads(PROFILE_TRAFFIC.read_text()).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    clocks = clk.summary()
+    cpu = cpu_baseline(cfg_text, base_seed, args.cpu_sample_runs)
+    line = {
+        "metric": "ToT queries/sec",
+        "value": total_q / dev_s,
+        "unit": "queries/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": 1000.0 * dev_s / args.steps,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "bf16",
+        "data": "synthetic (hash-seeded prompts and teacher-forced tokens, random-init weights)",
+        "config": {"workload": f"{args.config}: rebase_bfs w16 d16 target16, T1, "
+                               f"{cfg['run']['n_queries']} queries/GPU/step",
+                   "policy": args.policy, "prm": args.prm,
+                   "queries_per_step_per_gpu": cfg["run"]["n_queries"],
+                   "l2": "inputs larger than L2 (tree KV pools of tens of GB per search)",
+                   "parallelism": f"query-sharded x{world}"},
+        "e2e": {"value": total_e2e_q / e2e_wall, "unit": "queries/s",
+                "h2d_bytes_per_step": len(cfg_text.encode()),
+                "d2h_bytes_per_step": int(e2e_d2h / args.steps) + 256},
+        "gpu_launches": int(agg["launches"]),
+        "roofline": {"bound": "hbm", "kernel": "K1 tree_attn_kernel (policy decode)",
+                     "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                     "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
+                     "peak_source": peak_src,
+                     "k1_share_of_step": (agg["attn_ms"] / 1000.0) / dev_s if dev_s > 0 else None},
+        "cpu_baseline": cpu,
+        "clocks": {k: clocks[k] for k in ("sm_mhz", "sm_max_mhz", "reasons")},
+        "breakdown": {"control_ms_per_step": agg["ctl_ms"] / args.steps,
+                      "model_ms_per_step": agg["model_ms"] / args.steps,
+                      "k1_ms_per_step": agg["attn_ms"] / args.steps,
+                      "decode_rows_per_step": agg["decode_rows"] / args.steps,
+                      "prm_rows_per_step": agg["prm_rows"] / args.steps,
+                      "projection_tflops": agg["flops"] / (agg["model_ms"] / 1000.0) / 1e12
+                      if agg["model_ms"] > 0 else None,
+                      "wall_s_per_step": wall / args.steps},
+    }
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

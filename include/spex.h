@@ -70,6 +70,8 @@ typedef struct spex_model_stats {
   long long prm_thoughts;
   double policy_flops;    /* 2 * projection params * rows */
   double prm_flops;
+  long long launches;     /* kernels of this library launched by the forward (cuBLAS excluded) */
+  long long gemm_calls;   /* cuBLAS GEMM calls */
 } spex_model_stats;
 
 /* Per decode row-step shadow output (K3): argmax, logsumexp, logit sum. */

@@ -78,6 +78,8 @@ class ModelStats(ctypes.Structure):
         ("prm_thoughts", ctypes.c_longlong),
         ("policy_flops", ctypes.c_double),
         ("prm_flops", ctypes.c_double),
+        ("launches", ctypes.c_longlong),
+        ("gemm_calls", ctypes.c_longlong),
     ]
 
     def as_dict(self) -> dict:

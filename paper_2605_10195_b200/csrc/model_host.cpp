@@ -191,9 +191,13 @@ static Model* make_model(const ModelShape& sh, bool prm, uint64_t seed, long lon
 
 // One forward over M rows. K1 launches are bracketed by events when `attn_ev`
 // is given, accumulating their device time into *attn_ms.
+static long long g_launches = 0, g_gemms = 0;
+
 static void forward(Model& m, const RowDesc* rows, const Segment* segs, int M, cublasHandle_t hb,
                     cudaStream_t st, AttnTimer* timer) {
   const ModelShape& s = m.sh;
+  g_launches += 2 + 5LL * s.L + (m.is_prm ? 0 : 1);
+  g_gemms += 4LL * s.L + (m.is_prm ? 0 : 1);
   spex_k_embed(rows, M, m.embed, s.d, m.X, st);
   for (int l = 0; l < s.L; ++l) {
     spex_k_rmsnorm(m.X, M, s.d, s.eps, m.Xn, st);
@@ -261,6 +265,42 @@ ModelShape shape_by_name(const std::string& name) {
   throw std::runtime_error("unknown model shape " + name);
 }
 
+// Process-wide cache: weights and tree KV pools stay resident across runs
+// (a serving process keeps them; re-initialising 10s of GB per search would
+// measure cudaMalloc, not the path). Reused when shape/seed match and the
+// capacity suffices.
+struct ModelCache {
+  Model* pol = nullptr;
+  Model* prm = nullptr;
+  unsigned long long seed = 0;
+  cublasHandle_t hb = nullptr;
+};
+static ModelCache g_cache;
+
+static bool same_shape(const ModelShape& a, const ModelShape& b) {
+  return a.d == b.d && a.L == b.L && a.H == b.H && a.KVH == b.KVH && a.dh == b.dh && a.F == b.F && a.V == b.V &&
+         a.rope_theta == b.rope_theta && a.eps == b.eps;
+}
+
+static Model* cached(Model*& slot, const ModelShape& sh, bool prm, uint64_t seed, long long slots, int max_rows,
+                     cudaStream_t st) {
+  if (slot && same_shape(slot->sh, sh) && slot->slots >= slots && slot->max_rows >= max_rows &&
+      g_cache.seed == seed)
+    return slot;
+  delete slot;
+  slot = nullptr;
+  CK(cudaDeviceSynchronize());
+  slot = make_model(sh, prm, prm ? (seed ^ 0x50524d00ULL) : seed, slots + slots / 8 + 1024,
+                    max_rows + max_rows / 8 + 256, st);
+  return slot;
+}
+
+extern "C" void spex_model_cache_clear() {
+  delete g_cache.pol;
+  delete g_cache.prm;
+  g_cache.pol = g_cache.prm = nullptr;
+}
+
 // Replays the recorded schedule through the policy and PRM.
 void run_model_schedule(const ModelRunConfig& mc, const ScheduleView& sv, ModelRunResult* res, cudaStream_t st) {
   const int n_e = sv.n_entries;
@@ -286,12 +326,14 @@ void run_model_schedule(const ModelRunConfig& mc, const ScheduleView& sv, ModelR
   max_rows = std::max(max_rows, prompt_chunk * std::max(P, 1));
   const long long slots = std::max<long long>(sv.kv_slots, 1);
 
-  cublasHandle_t hb;
-  CB(cublasCreate(&hb));
+  if (!g_cache.hb) CB(cublasCreate(&g_cache.hb));
+  cublasHandle_t hb = g_cache.hb;
   CB(cublasSetStream(hb, st));
   CB(cublasSetMathMode(hb, CUBLAS_DEFAULT_MATH));
-  Model* pol = make_model(mc.policy, false, mc.seed, slots, max_rows, st);
-  Model* prm = mc.with_prm ? make_model(mc.prm, true, mc.seed ^ 0x5052'4d00ULL, slots, max_rows, st) : nullptr;
+  if (g_cache.seed != mc.seed) spex_model_cache_clear();
+  Model* pol = cached(g_cache.pol, mc.policy, false, mc.seed, slots, max_rows, st);
+  Model* prm = mc.with_prm ? cached(g_cache.prm, mc.prm, true, mc.seed, slots, max_rows, st) : nullptr;
+  g_cache.seed = mc.seed;
   RowDesc* rows = dalloc<RowDesc>(max_rows, owned);
   Segment* segs = dalloc<Segment>((size_t)max_rows * 40, owned);
   int* last_row = dalloc<int>(max_rows, owned);
@@ -307,11 +349,14 @@ void run_model_schedule(const ModelRunConfig& mc, const ScheduleView& sv, ModelR
   cudaEventCreate(&t0);
   cudaEventCreate(&t1);
   cudaEventRecord(t0, st);
+  g_launches = 1;  // prm scan
+  g_gemms = 0;
   // root prompts (prefill through both models)
   if (P > 0) {
     for (int q0 = 0; q0 < Q; q0 += prompt_chunk) {
       const int nq = std::min(prompt_chunk, Q - q0);
       spex_k_build_prompt_rows(tv_pol, q0, nq, rows, segs, st);
+      g_launches += prm ? 2 : 1;
       forward(*pol, rows, segs, nq * P, hb, st, nullptr);
       if (prm) {
         spex_k_build_prompt_rows(tv_prm, q0, nq, rows, segs, st);
@@ -329,6 +374,7 @@ void run_model_schedule(const ModelRunConfig& mc, const ScheduleView& sv, ModelR
       const int n = cnt[e];
       for (int s = 0; s < steps[e]; ++s) {
         spex_k_build_decode_rows(tv_pol, sv.srow_sid + off[e], sv.srow_pos0 + off[e], n, s, rows, segs, st);
+        g_launches += 1;
         forward(*pol, rows, segs, n, hb, st, mc.time_attn ? &timer : nullptr);
         res->decode_rows += n;
         res->decode_steps += 1;
@@ -348,6 +394,7 @@ void run_model_schedule(const ModelRunConfig& mc, const ScheduleView& sv, ModelR
       spex_k_build_prm_rows(tv_prm, sv.srow_sid + off[e], prm_row_start + off[e], n, rows, segs, last_row, st);
       forward(*prm, rows, segs, M, hb, st, nullptr);
       spex_k_value_head(prm->Xn, mc.prm.d, last_row, n, prm->vhead, scores, st);
+      g_launches += 2;
       if (dbg_scores && dbg_s + n <= mc.out_scores_cap) {
         spex_k_gather_prm(rows, last_row, n, scores, dbg_scores + dbg_s, st);
         dbg_s += n;
@@ -364,6 +411,8 @@ void run_model_schedule(const ModelRunConfig& mc, const ScheduleView& sv, ModelR
   res->model_ms = ms;
   res->attn_ms = timer.total_ms;
   res->attn_launches = timer.launches;
+  res->launches = g_launches;
+  res->gemm_calls = g_gemms;
   res->out_rows = dbg_n;
   res->out_scores = dbg_s;
   res->policy_flops = model_matmul_flops_per_row(mc.policy, false) * (double)(res->decode_rows + res->prefill_rows);
@@ -371,9 +420,6 @@ void run_model_schedule(const ModelRunConfig& mc, const ScheduleView& sv, ModelR
   CK(cudaGetLastError());
   cudaEventDestroy(t0);
   cudaEventDestroy(t1);
-  delete pol;
-  delete prm;
-  cublasDestroy(hb);
   for (void* p : owned) cudaFree(p);
 }
 

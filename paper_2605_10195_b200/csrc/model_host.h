@@ -47,6 +47,8 @@ struct ModelRunResult {
   long long decode_rows = 0, decode_steps = 0, prefill_rows = 0, prm_rows = 0, prm_thoughts = 0;
   long long out_rows = 0, out_scores = 0;
   double policy_flops = 0.0, prm_flops = 0.0;
+  long long launches = 0;  // kernels of this library launched by the replay (cuBLAS excluded)
+  long long gemm_calls = 0;
 };
 
 struct AttnTimer {

@@ -1082,6 +1082,8 @@ int spex_executor_model_stats(spex_executor* ex, spex_model_stats* out) {
     out->prm_thoughts = r.prm_thoughts;
     out->policy_flops = r.policy_flops;
     out->prm_flops = r.prm_flops;
+    out->launches = r.launches;
+    out->gemm_calls = r.gemm_calls;
 #else
     (void)ex;
 #endif
