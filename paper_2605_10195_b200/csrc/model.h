@@ -70,6 +70,14 @@ struct DecodeOut {
   float lsum;
 };
 
+// A tile of consecutive rows of one thought (PRM scoring) sharing one pass
+// over their common context; the last row carries the longest segment list.
+struct TileDesc {
+  int row0;
+  int nrows;
+};
+constexpr int kTileRows = 16;
+
 struct PrmOut {
   int q;
   uint32_t node;

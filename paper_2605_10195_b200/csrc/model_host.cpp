@@ -32,11 +32,16 @@ extern "C" {
 void spex_k_init_weights(__nv_bfloat16* w, long long n, uint64_t seed, uint64_t tid, float scale, cudaStream_t s);
 void spex_k_build_decode_rows(TreeView t, const int* sids, const int* pos0, int n, int step, RowDesc* rows,
                               Segment* segs, cudaStream_t s);
-void spex_k_build_prm_rows(TreeView t, const int* sids, const int* row_start, int n, RowDesc* rows, Segment* segs,
-                           int* last_row, cudaStream_t s);
+void spex_k_build_prm_rows(TreeView t, const int* sids, const int* row_start, const int* tile_start, int n,
+                           RowDesc* rows, Segment* segs, int* last_row, TileDesc* tiles, cudaStream_t s);
+void spex_k_build_prompt_tiles(int nq, int P, TileDesc* tiles, cudaStream_t s);
+int spex_k_tree_attn_tiles(const TileDesc* tiles, int ntiles, const RowDesc* rows, const Segment* segs,
+                           const float* Qr, int H, int KVH, int dh, const __nv_bfloat16* Kp, const __nv_bfloat16* Vp,
+                           long long slots, __nv_bfloat16* O, cudaStream_t s);
 void spex_k_build_prompt_rows(TreeView t, int q0, int nq, RowDesc* rows, Segment* segs, cudaStream_t s);
 void spex_k_prm_scan_all(TreeView t, const int* kind, const int* off, const int* n, int n_entries,
-                         const int* srow_sid, int* row_start, int* totals, cudaStream_t s);
+                         const int* srow_sid, int* row_start, int* tile_start, int* totals, int* tile_totals,
+                         cudaStream_t s);
 void spex_k_embed(const RowDesc* rows, int M, const __nv_bfloat16* E, int d, float* X, cudaStream_t s);
 void spex_k_rmsnorm(const float* X, int M, int d, float eps, __nv_bfloat16* Y, cudaStream_t s);
 void spex_k_rope_kv(const RowDesc* rows, int M, const float* QKV, int H, int KVH, int dh, const float* inv_freq,
@@ -194,7 +199,7 @@ static Model* make_model(const ModelShape& sh, bool prm, uint64_t seed, long lon
 static long long g_launches = 0, g_gemms = 0;
 
 static void forward(Model& m, const RowDesc* rows, const Segment* segs, int M, cublasHandle_t hb,
-                    cudaStream_t st, AttnTimer* timer) {
+                    cudaStream_t st, AttnTimer* timer, const TileDesc* tiles = nullptr, int ntiles = 0) {
   const ModelShape& s = m.sh;
   g_launches += 2 + 5LL * s.L + (m.is_prm ? 0 : 1);
   g_gemms += 4LL * s.L + (m.is_prm ? 0 : 1);
@@ -204,8 +209,10 @@ static void forward(Model& m, const RowDesc* rows, const Segment* segs, int M, c
     gemm(hb, m.Xn, m.wqkv[l], m.QKV, M, (s.H + 2 * s.KVH) * s.dh, s.d, false);
     spex_k_rope_kv(rows, M, m.QKV, s.H, s.KVH, s.dh, m.inv_freq, m.slots, m.Kp[l], m.Vp[l], m.Qr, st);
     if (timer) timer->begin(st);
-    if (spex_k_tree_attn(rows, segs, m.Qr, s.H, s.KVH, s.dh, m.Kp[l], m.Vp[l], m.slots, m.O, M, st) != 0)
-      throw std::runtime_error("tree attention: unsupported head shape");
+    const int rc = tiles ? spex_k_tree_attn_tiles(tiles, ntiles, rows, segs, m.Qr, s.H, s.KVH, s.dh, m.Kp[l],
+                                                  m.Vp[l], m.slots, m.O, st)
+                         : spex_k_tree_attn(rows, segs, m.Qr, s.H, s.KVH, s.dh, m.Kp[l], m.Vp[l], m.slots, m.O, M, st);
+    if (rc != 0) throw std::runtime_error("tree attention: unsupported head shape");
     if (timer) timer->end(st);
     gemm(hb, m.O, m.wo[l], m.X, M, s.d, s.H * s.dh, true);
     spex_k_rmsnorm(m.X, M, s.d, s.eps, m.Xn, st);
@@ -313,10 +320,14 @@ void run_model_schedule(const ModelRunConfig& mc, const ScheduleView& sv, ModelR
   CK(cudaMemcpyAsync(u0.data(), sv.u0, n_e * sizeof(long long), cudaMemcpyDeviceToHost, st));
   std::vector<void*> owned;
   int* prm_row_start = dalloc<int>(std::max(sv.n_rows, 1), owned);
+  int* prm_tile_start = dalloc<int>(std::max(sv.n_rows, 1), owned);
   int* prm_totals = dalloc<int>(std::max(n_e, 1), owned);
-  spex_k_prm_scan_all(sv.tree, sv.kind, sv.off, sv.n, n_e, sv.srow_sid, prm_row_start, prm_totals, st);
-  std::vector<int> totals(n_e);
+  int* prm_tile_totals = dalloc<int>(std::max(n_e, 1), owned);
+  spex_k_prm_scan_all(sv.tree, sv.kind, sv.off, sv.n, n_e, sv.srow_sid, prm_row_start, prm_tile_start, prm_totals,
+                      prm_tile_totals, st);
+  std::vector<int> totals(n_e), tile_totals(n_e);
   CK(cudaMemcpyAsync(totals.data(), prm_totals, n_e * sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(tile_totals.data(), prm_tile_totals, n_e * sizeof(int), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
 
   const int Q = sv.n_queries, P = sv.tree.prompt_tokens;
@@ -337,6 +348,7 @@ void run_model_schedule(const ModelRunConfig& mc, const ScheduleView& sv, ModelR
   RowDesc* rows = dalloc<RowDesc>(max_rows, owned);
   Segment* segs = dalloc<Segment>((size_t)max_rows * 40, owned);
   int* last_row = dalloc<int>(max_rows, owned);
+  TileDesc* tiles = dalloc<TileDesc>(max_rows, owned);
   float* scores = dalloc<float>(max_rows, owned);
   CK(cudaStreamSynchronize(st));
 
@@ -356,11 +368,13 @@ void run_model_schedule(const ModelRunConfig& mc, const ScheduleView& sv, ModelR
     for (int q0 = 0; q0 < Q; q0 += prompt_chunk) {
       const int nq = std::min(prompt_chunk, Q - q0);
       spex_k_build_prompt_rows(tv_pol, q0, nq, rows, segs, st);
-      g_launches += prm ? 2 : 1;
-      forward(*pol, rows, segs, nq * P, hb, st, nullptr);
+      spex_k_build_prompt_tiles(nq, P, tiles, st);
+      const int ntp = nq * ((P + kTileRows - 1) / kTileRows);
+      g_launches += prm ? 3 : 2;
+      forward(*pol, rows, segs, nq * P, hb, st, nullptr, tiles, ntp);
       if (prm) {
         spex_k_build_prompt_rows(tv_prm, q0, nq, rows, segs, st);
-        forward(*prm, rows, segs, nq * P, hb, st, nullptr);
+        forward(*prm, rows, segs, nq * P, hb, st, nullptr, tiles, ntp);
       }
       res->prefill_rows += (long long)nq * P;
     }
@@ -391,8 +405,9 @@ void run_model_schedule(const ModelRunConfig& mc, const ScheduleView& sv, ModelR
       const int n = cnt[e];
       const int M = totals[e];
       if (M <= 0) continue;
-      spex_k_build_prm_rows(tv_prm, sv.srow_sid + off[e], prm_row_start + off[e], n, rows, segs, last_row, st);
-      forward(*prm, rows, segs, M, hb, st, nullptr);
+      spex_k_build_prm_rows(tv_prm, sv.srow_sid + off[e], prm_row_start + off[e], prm_tile_start + off[e], n, rows,
+                            segs, last_row, tiles, st);
+      forward(*prm, rows, segs, M, hb, st, nullptr, tiles, tile_totals[e]);
       spex_k_value_head(prm->Xn, mc.prm.d, last_row, n, prm->vhead, scores, st);
       g_launches += 2;
       if (dbg_scores && dbg_s + n <= mc.out_scores_cap) {

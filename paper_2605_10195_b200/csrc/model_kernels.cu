@@ -13,6 +13,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "ctl_state.h"
 #include "model.h"
@@ -100,8 +101,8 @@ __global__ void build_decode_rows_kernel(TreeView t, const int* sids, const int*
 }
 
 // PRM rows: thought k of the entry occupies rows [row_start[k], row_start[k] + len).
-__global__ void build_prm_rows_kernel(TreeView t, const int* sids, const int* row_start, int n,
-                                      RowDesc* rows, Segment* segs, int* last_row) {
+__global__ void build_prm_rows_kernel(TreeView t, const int* sids, const int* row_start, const int* tile_start,
+                                      int n, RowDesc* rows, Segment* segs, int* last_row, TileDesc* tiles) {
   const int k = blockIdx.x;
   if (k >= n) return;
   const int sid = sids[k];
@@ -127,6 +128,12 @@ __global__ void build_prm_rows_kernel(TreeView t, const int* sids, const int* ro
     rows[i] = r;
   }
   if (threadIdx.x == 0) last_row[k] = r0 + len - 1;
+  for (int j = threadIdx.x; j * kTileRows < len; j += blockDim.x) {
+    TileDesc td;
+    td.row0 = r0 + j * kTileRows;
+    td.nrows = len - j * kTileRows < kTileRows ? len - j * kTileRows : kTileRows;
+    tiles[tile_start[k] + j] = td;
+  }
 }
 
 // Root prompt rows: query q, positions 0..P-1.
@@ -154,23 +161,41 @@ __global__ void build_prompt_rows_kernel(TreeView t, int q0, int nq, RowDesc* ro
   rows[i] = r;
 }
 
+// Tiles over root prompt rows: query-major, kTileRows consecutive positions.
+__global__ void build_prompt_tiles_kernel(int nq, int P, TileDesc* tiles) {
+  const int per = (P + kTileRows - 1) / kTileRows;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nq * per) return;
+  const int q = i / per, j = i % per;
+  TileDesc td;
+  td.row0 = q * P + j * kTileRows;
+  td.nrows = P - j * kTileRows < kTileRows ? P - j * kTileRows : kTileRows;
+  tiles[i] = td;
+}
+
 // PRM row counts per reward batch (sum of token_len of the scored thoughts)
 // and the per-thought exclusive scan; one thread per schedule entry.
 __global__ void prm_scan_all_kernel(TreeView t, const int* kind, const int* off, const int* cnt, int n_entries,
-                                    const int* srow_sid, int* row_start, int* totals) {
+                                    const int* srow_sid, int* row_start, int* tile_start, int* totals,
+                                    int* tile_totals) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= n_entries) return;
   if (kind[e] != SCHED_PRM) {
     totals[e] = 0;
+    tile_totals[e] = 0;
     return;
   }
-  int acc = 0;
+  int acc = 0, tacc = 0;
   for (int k = 0; k < cnt[e]; ++k) {
     const int sid = srow_sid[off[e] + k];
     row_start[off[e] + k] = acc;
-    acc += t.tokens[(uint32_t)t.st_q[sid] * (uint32_t)t.node_cap + t.st_node[sid]];
+    tile_start[off[e] + k] = tacc;
+    const int len = t.tokens[(uint32_t)t.st_q[sid] * (uint32_t)t.node_cap + t.st_node[sid]];
+    acc += len;
+    tacc += (len + kTileRows - 1) / kTileRows;
   }
   totals[e] = acc;
+  tile_totals[e] = tacc;
 }
 
 __global__ void gather_prm_kernel(const RowDesc* rows, const int* last_row, int n, const float* score,
@@ -470,6 +495,296 @@ __global__ void __launch_bounds__(kAttnThreads) tree_attn_kernel(const RowDesc* 
   }
 }
 
+// K1 decode variant: one warp per (row, kv head) streams the row's context with
+// 128-bit coalesced loads — a half-warp covers one 256-byte K (or V) row, so a
+// warp consumes two tokens per load instruction and keeps UNROLL token pairs in
+// flight. Online softmax in registers (log2 domain); no shared memory and no
+// block barriers, so occupancy is bounded only by registers. Decode rows have
+// no intra-row reuse: staging through shared memory would only add latency.
+template <int DH, int G>
+__global__ void __launch_bounds__(256) tree_attn_decode_kernel(const RowDesc* __restrict__ rows,
+                                                              const Segment* __restrict__ segs,
+                                                              const float* __restrict__ Qr, int H, int KVH, int M,
+                                                              const __nv_bfloat16* __restrict__ Kp,
+                                                              const __nv_bfloat16* __restrict__ Vp,
+                                                              long long slots, __nv_bfloat16* __restrict__ O) {
+  constexpr int EPL = 8;              // bf16 elements per lane per token (16 bytes)
+  constexpr int LPT = DH / EPL;       // lanes per token (16 for DH=128, 8 for DH=64)
+  constexpr int TPW = 32 / LPT;       // tokens per warp load (2 or 4)
+  constexpr int UNROLL = 4;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (gw >= M * KVH) return;
+  const int r = gw / KVH, kh = gw % KVH;
+  const int sub = lane / LPT;         // which token of the pair/quad
+  const int li = lane % LPT;          // dim block
+  const RowDesc rd = rows[r];
+  const Segment* sg = segs + rd.seg_off;
+  const __nv_bfloat16* Kh = Kp + (long long)kh * slots * DH + li * EPL;
+  const __nv_bfloat16* Vh = Vp + (long long)kh * slots * DH + li * EPL;
+  float q[G][EPL];
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    const float4* qp = reinterpret_cast<const float4*>(Qr + ((long long)r * H + kh * G + g) * DH + li * EPL);
+    const float4 a = qp[0], b = qp[1];
+    q[g][0] = a.x * 1.4426950408889634f; q[g][1] = a.y * 1.4426950408889634f;
+    q[g][2] = a.z * 1.4426950408889634f; q[g][3] = a.w * 1.4426950408889634f;
+    q[g][4] = b.x * 1.4426950408889634f; q[g][5] = b.y * 1.4426950408889634f;
+    q[g][6] = b.z * 1.4426950408889634f; q[g][7] = b.w * 1.4426950408889634f;
+  }
+  float m[G], l[G], acc[G][EPL];
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    m[g] = -INFINITY;
+    l[g] = 0.f;
+#pragma unroll
+    for (int e = 0; e < EPL; ++e) acc[g][e] = 0.f;
+  }
+  for (int si = 0; si < rd.nseg; ++si) {
+    const long long base = sg[si].base;
+    const int len = sg[si].len;
+    for (int t0 = 0; t0 < len; t0 += TPW * UNROLL) {
+      uint4 kraw[UNROLL], vraw[UNROLL];
+      bool ok[UNROLL];
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u) {
+        const int t = t0 + u * TPW + sub;
+        ok[u] = t < len;
+        const long long off = (base + (ok[u] ? t : 0)) * DH;
+        kraw[u] = __ldg(reinterpret_cast<const uint4*>(Kh + off));
+        vraw[u] = __ldg(reinterpret_cast<const uint4*>(Vh + off));
+      }
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u) {
+        float kf[EPL], vf[EPL];
+        const __nv_bfloat162* k2 = reinterpret_cast<const __nv_bfloat162*>(&kraw[u]);
+        const __nv_bfloat162* v2 = reinterpret_cast<const __nv_bfloat162*>(&vraw[u]);
+#pragma unroll
+        for (int e = 0; e < EPL / 2; ++e) {
+          kf[2 * e] = __low2float(k2[e]);
+          kf[2 * e + 1] = __high2float(k2[e]);
+          vf[2 * e] = __low2float(v2[e]);
+          vf[2 * e + 1] = __high2float(v2[e]);
+        }
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          float sc = 0.f;
+#pragma unroll
+          for (int e = 0; e < EPL; ++e) sc += q[g][e] * kf[e];
+#pragma unroll
+          for (int o = LPT / 2; o > 0; o >>= 1) sc += __shfl_xor_sync(0xffffffffu, sc, o);
+          if (!ok[u]) sc = -INFINITY;
+          // running max shared by all tokens of the warp step
+          float mx = sc;
+#pragma unroll
+          for (int o = LPT; o < 32; o <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+          const float m_new = fmaxf(m[g], mx);
+          const float scale = exp2f(m[g] - m_new);  // m == -inf -> 0
+          const float p = ok[u] ? exp2f(sc - m_new) : 0.f;
+          l[g] = l[g] * scale + p;
+#pragma unroll
+          for (int e = 0; e < EPL; ++e) acc[g][e] = acc[g][e] * scale + p * vf[e];
+          m[g] = m_new;
+        }
+      }
+    }
+  }
+  // combine the TPW token lanes holding the same dims
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+#pragma unroll
+    for (int o = LPT; o < 32; o <<= 1) {
+      l[g] += __shfl_xor_sync(0xffffffffu, l[g], o);
+#pragma unroll
+      for (int e = 0; e < EPL; ++e) acc[g][e] += __shfl_xor_sync(0xffffffffu, acc[g][e], o);
+    }
+    if (sub == 0) {
+      const float inv = 1.f / l[g];
+      __nv_bfloat16* op = O + ((long long)r * H + kh * G + g) * DH + li * EPL;
+      uint4 packed;
+      __nv_bfloat162* pk = reinterpret_cast<__nv_bfloat162*>(&packed);
+#pragma unroll
+      for (int e = 0; e < EPL / 2; ++e) pk[e] = __floats2bfloat162_rn(acc[g][2 * e] * inv, acc[g][2 * e + 1] * inv);
+      *reinterpret_cast<uint4*>(op) = packed;
+    }
+  }
+}
+
+// K1 tile variant for prefill-shaped rows (PRM scoring): kTileRows consecutive
+// rows of one thought share their ancestors and a causal own prefix, so each
+// 64-token K/V chunk is staged once per tile instead of once per row.
+template <int DH, int G>
+__global__ void __launch_bounds__(kAttnThreads) tree_attn_tile_kernel(const TileDesc* __restrict__ tiles,
+                                                                     const RowDesc* __restrict__ rows,
+                                                                     const Segment* __restrict__ segs,
+                                                                     const float* __restrict__ Qr, int H,
+                                                                     const __nv_bfloat16* __restrict__ Kp,
+                                                                     const __nv_bfloat16* __restrict__ Vp,
+                                                                     long long slots,
+                                                                     __nv_bfloat16* __restrict__ O) {
+  constexpr int R = kTileRows;
+  constexpr int NV = R * G;             // query vectors in the tile
+  constexpr int VPL = DH / 32;
+  constexpr int DGRP = kAttnThreads / DH;  // threads sharing one output dim (1 or 2)
+  constexpr int NACC = (NV + DGRP - 1) / DGRP;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __nv_bfloat16* sK = reinterpret_cast<__nv_bfloat16*>(smem_raw);
+  __nv_bfloat16* sV = sK + 2 * kChunk * DH;
+  float* sQ = reinterpret_cast<float*>(sV + 2 * kChunk * DH);  // [NV][DH]
+  float* sS = sQ + NV * DH;                                    // [NV][kChunk]
+  float* sM = sS + NV * kChunk;
+  float* sL = sM + NV;
+  float* sAlpha = sL + NV;
+  __shared__ int sPos[R];
+  __shared__ uint64_t bar[2];
+
+  const TileDesc td = tiles[blockIdx.x];
+  const int kh = blockIdx.y;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const RowDesc last = rows[td.row0 + td.nrows - 1];
+  const Segment* sg = segs + last.seg_off;
+  const int nseg = last.nseg;
+  const __nv_bfloat16* Kh = Kp + (long long)kh * slots * DH;
+  const __nv_bfloat16* Vh = Vp + (long long)kh * slots * DH;
+
+  for (int i = tid; i < NV * DH; i += kAttnThreads) {
+    const int v = i / DH, dcol = i % DH;
+    const int ri = v / G, g = v % G;
+    sQ[i] = ri < td.nrows ? Qr[((long long)(td.row0 + ri) * H + kh * G + g) * DH + dcol] * 1.4426950408889634f : 0.f;
+  }
+  if (tid < R) sPos[tid] = tid < td.nrows ? rows[td.row0 + tid].pos : -1;
+  if (tid < NV) {
+    sM[tid] = -INFINITY;
+    sL[tid] = 0.f;
+  }
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  int nchunks = 0;
+  for (int s = 0; s < nseg; ++s) nchunks += (sg[s].len + kChunk - 1) / kChunk;
+  __syncthreads();
+
+  int seg_i = 0, seg_o = 0;
+  long long cb[2];
+  int cl[2], cown[2];  // chunk base/len; own-segment offset of the chunk (-1: ancestor)
+  auto next_chunk = [&](int b) {
+    while (seg_i < nseg && seg_o >= sg[seg_i].len) {
+      ++seg_i;
+      seg_o = 0;
+    }
+    cb[b] = sg[seg_i].base + seg_o;
+    const int l = sg[seg_i].len - seg_o;
+    cl[b] = l < kChunk ? l : kChunk;
+    cown[b] = (seg_i == nseg - 1) ? seg_o : -1;
+    seg_o += cl[b];
+  };
+  for (int c = 0; c < 2 && c < nchunks; ++c) {
+    next_chunk(c);
+    if (tid == 0) {
+      const uint32_t bytes = (uint32_t)cl[c] * DH * 2;
+      mbar_expect_tx(&bar[c], 2 * bytes);
+      bulk_g2s(sK + c * kChunk * DH, Kh + cb[c] * DH, bytes, &bar[c]);
+      bulk_g2s(sV + c * kChunk * DH, Vh + cb[c] * DH, bytes, &bar[c]);
+    }
+  }
+  const int dcol = tid % DH;
+  const int vgrp = tid / DH;
+  float acc[NACC];
+#pragma unroll
+  for (int k = 0; k < NACC; ++k) acc[k] = 0.f;
+
+  for (int c = 0; c < nchunks; ++c) {
+    const int buf = c & 1;
+    const int len = cl[buf];
+    const int own0 = cown[buf];
+    mbar_wait(&bar[buf], (uint32_t)((c >> 1) & 1));
+    const __nv_bfloat16* K = sK + buf * kChunk * DH;
+    const __nv_bfloat16* Vs = sV + buf * kChunk * DH;
+    for (int t = warp; t < len; t += kAttnThreads / 32) {
+      float kv[VPL];
+#pragma unroll
+      for (int v2 = 0; v2 < VPL / 2; ++v2) {
+        const __nv_bfloat162 a = *reinterpret_cast<const __nv_bfloat162*>(K + t * DH + lane * VPL + 2 * v2);
+        kv[2 * v2] = __low2float(a);
+        kv[2 * v2 + 1] = __high2float(a);
+      }
+#pragma unroll 4
+      for (int v = 0; v < NV; ++v) {
+        const float* q = sQ + v * DH + lane * VPL;
+        float s = 0.f;
+#pragma unroll
+        for (int e = 0; e < VPL; ++e) s += q[e] * kv[e];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) {
+          const bool masked = own0 >= 0 && own0 + t > sPos[v / G];
+          sS[v * kChunk + t] = masked ? -INFINITY : s;
+        }
+      }
+    }
+    __syncthreads();
+    for (int v = warp; v < NV; v += kAttnThreads / 32) {
+      float mx = -INFINITY;
+      for (int t = lane; t < len; t += 32) mx = fmaxf(mx, sS[v * kChunk + t]);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      const float m_old = sM[v], l_old = sL[v];
+      const float m_new = fmaxf(m_old, mx);
+      float sum = 0.f;
+      for (int t = lane; t < len; t += 32) {
+        const float sv = sS[v * kChunk + t];
+        const float p = (m_new == -INFINITY || sv == -INFINITY) ? 0.f : exp2f(sv - m_new);
+        sS[v * kChunk + t] = p;
+        sum += p;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+      const float alpha = (m_old == -INFINITY) ? 0.f : exp2f(m_old - m_new);
+      __syncwarp();
+      if (lane == 0) {
+        sM[v] = m_new;
+        sL[v] = l_old * alpha + sum;
+        sAlpha[v] = alpha;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < NACC; ++k) {
+      const int v = vgrp + k * DGRP;
+      if (v < NV) acc[k] *= sAlpha[v];
+    }
+    for (int t = 0; t < len; ++t) {
+      const float vv = __bfloat162float(Vs[t * DH + dcol]);
+#pragma unroll
+      for (int k = 0; k < NACC; ++k) {
+        const int v = vgrp + k * DGRP;
+        if (v < NV) acc[k] += sS[v * kChunk + t] * vv;
+      }
+    }
+    __syncthreads();
+    if (c + 2 < nchunks) {
+      next_chunk(buf);
+      if (tid == 0) {
+        const uint32_t bytes = (uint32_t)cl[buf] * DH * 2;
+        mbar_expect_tx(&bar[buf], 2 * bytes);
+        bulk_g2s(sK + buf * kChunk * DH, Kh + cb[buf] * DH, bytes, &bar[buf]);
+        bulk_g2s(sV + buf * kChunk * DH, Vh + cb[buf] * DH, bytes, &bar[buf]);
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < NACC; ++k) {
+    const int v = vgrp + k * DGRP;
+    if (v < NV) {
+      const int ri = v / G, g = v % G;
+      if (ri < td.nrows)
+        O[((long long)(td.row0 + ri) * H + kh * G + g) * DH + dcol] = __float2bfloat16_rn(acc[k] / sL[v]);
+    }
+  }
+}
+
 __global__ void swiglu_kernel(const float* GU, int M, int F, __nv_bfloat16* A) {
   const long long n = (long long)M * F;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
@@ -481,63 +796,77 @@ __global__ void swiglu_kernel(const float* GU, int M, int F, __nv_bfloat16* A) {
   }
 }
 
-// K3: per-row argmax (first max), logsumexp and sum of the logits.
-__global__ void lm_epilogue_kernel(const float* logits, int M, int V, int* amax, float* lse, float* lsum) {
+// K3: per-row argmax (first max), logsumexp and sum of the logits in one pass
+// (online max / rescaled exp-sum per thread, then a block combine).
+__global__ void __launch_bounds__(256) lm_epilogue_kernel(const float* logits, int M, int V, int* amax,
+                                                          float* lse, float* lsum) {
   const int r = blockIdx.x;
   if (r >= M) return;
   const float* x = logits + (long long)r * V;
-  float mx = -INFINITY;
-  int mi = 0;
-  float sm = 0.f;
-  for (int i = threadIdx.x; i < V; i += blockDim.x) {
+  float mx = -INFINITY, se = 0.f, sm = 0.f;
+  int mi = 0x7fffffff;
+  const int V4 = (V % 4 == 0) ? V / 4 : 0;
+  for (int i = threadIdx.x; i < V4; i += blockDim.x) {
+    const float4 v4 = reinterpret_cast<const float4*>(x)[i];
+    const float vs[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float v = vs[k];
+      sm += v;
+      if (v > mx) {
+        se = se * __expf(mx - v) + 1.f;
+        mx = v;
+        mi = 4 * i + k;
+      } else {
+        se += __expf(v - mx);
+      }
+    }
+  }
+  for (int i = 4 * V4 + threadIdx.x; i < V; i += blockDim.x) {
     const float v = x[i];
+    sm += v;
     if (v > mx) {
+      se = se * __expf(mx - v) + 1.f;
       mx = v;
       mi = i;
+    } else {
+      se += __expf(v - mx);
     }
-    sm += v;
   }
-  __shared__ float smx[32], ssm[32];
-  __shared__ int smi[32];
+  // warp combine
   for (int o = 16; o > 0; o >>= 1) {
     const float om = __shfl_xor_sync(0xffffffffu, mx, o);
+    const float os = __shfl_xor_sync(0xffffffffu, se, o);
     const int oi = __shfl_xor_sync(0xffffffffu, mi, o);
-    if (om > mx || (om == mx && oi < mi)) {
-      mx = om;
-      mi = oi;
-    }
     sm += __shfl_xor_sync(0xffffffffu, sm, o);
+    const float nm = fmaxf(mx, om);
+    se = (mx == -INFINITY ? 0.f : se * __expf(mx - nm)) + (om == -INFINITY ? 0.f : os * __expf(om - nm));
+    if (om > mx || (om == mx && oi < mi)) mi = oi;
+    mx = nm;
   }
+  __shared__ float smx[8], sse[8], ssm[8];
+  __shared__ int smi[8];
   const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   if ((threadIdx.x & 31) == 0) {
     smx[w] = mx;
-    smi[w] = mi;
+    sse[w] = se;
     ssm[w] = sm;
+    smi[w] = mi;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
+    float M0 = smx[0], S0 = sse[0], T0 = ssm[0];
+    int I0 = smi[0];
     for (int k = 1; k < nw; ++k) {
-      if (smx[k] > smx[0] || (smx[k] == smx[0] && smi[k] < smi[0])) {
-        smx[0] = smx[k];
-        smi[0] = smi[k];
-      }
-      ssm[0] += ssm[k];
+      const float nm = fmaxf(M0, smx[k]);
+      S0 = S0 * __expf(M0 - nm) + sse[k] * __expf(smx[k] - nm);
+      if (smx[k] > M0 || (smx[k] == M0 && smi[k] < I0)) I0 = smi[k];
+      M0 = nm;
+      T0 += ssm[k];
     }
-  }
-  __syncthreads();
-  const float gmax = smx[0];
-  float se = 0.f;
-  for (int i = threadIdx.x; i < V; i += blockDim.x) se += __expf(x[i] - gmax);
-  for (int o = 16; o > 0; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
-  __syncthreads();
-  if ((threadIdx.x & 31) == 0) smx[w] = se;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    float tot = 0.f;
-    for (int k = 0; k < nw; ++k) tot += smx[k];
-    amax[r] = smi[0];
-    lse[r] = gmax + logf(tot);
-    lsum[r] = ssm[0];
+    amax[r] = I0;
+    lse[r] = M0 + logf(S0);
+    lsum[r] = T0;
   }
 }
 
@@ -575,9 +904,10 @@ extern "C" void spex_k_build_decode_rows(TreeView t, const int* sids, const int*
   build_decode_rows_kernel<<<(n + 127) / 128, 128, 0, s>>>(t, sids, pos0, n, step, rows, segs);
 }
 
-extern "C" void spex_k_build_prm_rows(TreeView t, const int* sids, const int* row_start, int n, RowDesc* rows,
-                                      Segment* segs, int* last_row, cudaStream_t s) {
-  build_prm_rows_kernel<<<n, 128, 0, s>>>(t, sids, row_start, n, rows, segs, last_row);
+extern "C" void spex_k_build_prm_rows(TreeView t, const int* sids, const int* row_start, const int* tile_start,
+                                      int n, RowDesc* rows, Segment* segs, int* last_row, TileDesc* tiles,
+                                      cudaStream_t s) {
+  build_prm_rows_kernel<<<n, 128, 0, s>>>(t, sids, row_start, tile_start, n, rows, segs, last_row, tiles);
 }
 
 extern "C" void spex_k_build_prompt_rows(TreeView t, int q0, int nq, RowDesc* rows, Segment* segs,
@@ -586,10 +916,16 @@ extern "C" void spex_k_build_prompt_rows(TreeView t, int q0, int nq, RowDesc* ro
   build_prompt_rows_kernel<<<(n + 127) / 128, 128, 0, s>>>(t, q0, nq, rows, segs);
 }
 
+extern "C" void spex_k_build_prompt_tiles(int nq, int P, TileDesc* tiles, cudaStream_t s) {
+  const int n = nq * ((P + kTileRows - 1) / kTileRows);
+  build_prompt_tiles_kernel<<<(n + 127) / 128, 128, 0, s>>>(nq, P, tiles);
+}
+
 extern "C" void spex_k_prm_scan_all(TreeView t, const int* kind, const int* off, const int* n, int n_entries,
-                                    const int* srow_sid, int* row_start, int* totals, cudaStream_t s) {
+                                    const int* srow_sid, int* row_start, int* tile_start, int* totals,
+                                    int* tile_totals, cudaStream_t s) {
   prm_scan_all_kernel<<<(n_entries + 127) / 128, 128, 0, s>>>(t, kind, off, n, n_entries, srow_sid, row_start,
-                                                              totals);
+                                                              tile_start, totals, tile_totals);
 }
 
 extern "C" void spex_k_gather_prm(const RowDesc* rows, const int* last_row, int n, const float* score,
@@ -617,6 +953,15 @@ extern "C" void spex_k_rope_kv(const RowDesc* rows, int M, const float* QKV, int
 }
 
 template <int DH, int G>
+static void launch_attn_decode(const RowDesc* rows, const Segment* segs, const float* Qr, int H, int KVH,
+                               const __nv_bfloat16* Kp, const __nv_bfloat16* Vp, long long slots, __nv_bfloat16* O,
+                               int M, cudaStream_t s) {
+  const long long warps = (long long)M * KVH;
+  const int blocks = (int)((warps * 32 + 255) / 256);
+  tree_attn_decode_kernel<DH, G><<<blocks, 256, 0, s>>>(rows, segs, Qr, H, KVH, M, Kp, Vp, slots, O);
+}
+
+template <int DH, int G>
 static void launch_attn(const RowDesc* rows, const Segment* segs, const float* Qr, int H, int KVH,
                         const __nv_bfloat16* Kp, const __nv_bfloat16* Vp, long long slots, __nv_bfloat16* O, int M,
                         cudaStream_t s) {
@@ -630,14 +975,20 @@ static void launch_attn(const RowDesc* rows, const Segment* segs, const float* Q
   tree_attn_kernel<DH, G><<<grid, kAttnThreads, smem, s>>>(rows, segs, Qr, H, Kp, Vp, slots, O);
 }
 
+static int g_attn_staged = -1;
+
 extern "C" int spex_k_tree_attn(const RowDesc* rows, const Segment* segs, const float* Qr, int H, int KVH, int dh,
                                 const __nv_bfloat16* Kp, const __nv_bfloat16* Vp, long long slots, __nv_bfloat16* O,
                                 int M, cudaStream_t s) {
   const int G = H / KVH;
-#define SPEX_ATTN_CASE(D, GG) \
-  if (dh == D && G == GG) {   \
-    launch_attn<D, GG>(rows, segs, Qr, H, KVH, Kp, Vp, slots, O, M, s); \
-    return 0;                 \
+  if (g_attn_staged < 0) g_attn_staged = getenv("SPEX_ATTN_STAGED") ? 1 : 0;
+#define SPEX_ATTN_CASE(D, GG)                                                   \
+  if (dh == D && G == GG) {                                                     \
+    if (g_attn_staged)                                                          \
+      launch_attn<D, GG>(rows, segs, Qr, H, KVH, Kp, Vp, slots, O, M, s);       \
+    else                                                                        \
+      launch_attn_decode<D, GG>(rows, segs, Qr, H, KVH, Kp, Vp, slots, O, M, s); \
+    return 0;                                                                   \
   }
   SPEX_ATTN_CASE(128, 1)
   SPEX_ATTN_CASE(128, 2)
@@ -648,6 +999,41 @@ extern "C" int spex_k_tree_attn(const RowDesc* rows, const Segment* segs, const 
   SPEX_ATTN_CASE(64, 2)
   SPEX_ATTN_CASE(64, 4)
 #undef SPEX_ATTN_CASE
+  return -1;
+}
+
+template <int DH, int G>
+static void launch_tile(const TileDesc* tiles, int ntiles, const RowDesc* rows, const Segment* segs, const float* Qr,
+                        int H, int KVH, const __nv_bfloat16* Kp, const __nv_bfloat16* Vp, long long slots,
+                        __nv_bfloat16* O, cudaStream_t s) {
+  constexpr int NV = kTileRows * G;
+  const size_t smem = 4 * kChunk * DH * sizeof(__nv_bfloat16) + (NV * DH + NV * kChunk + 3 * NV) * sizeof(float) + 64;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(tree_attn_tile_kernel<DH, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  dim3 grid(ntiles, KVH);
+  tree_attn_tile_kernel<DH, G><<<grid, kAttnThreads, smem, s>>>(tiles, rows, segs, Qr, H, Kp, Vp, slots, O);
+}
+
+extern "C" int spex_k_tree_attn_tiles(const TileDesc* tiles, int ntiles, const RowDesc* rows, const Segment* segs,
+                                      const float* Qr, int H, int KVH, int dh, const __nv_bfloat16* Kp,
+                                      const __nv_bfloat16* Vp, long long slots, __nv_bfloat16* O, cudaStream_t s) {
+  const int G = H / KVH;
+  if (ntiles <= 0) return 0;
+#define SPEX_TILE_CASE(D, GG)                                                        \
+  if (dh == D && G == GG) {                                                          \
+    launch_tile<D, GG>(tiles, ntiles, rows, segs, Qr, H, KVH, Kp, Vp, slots, O, s);  \
+    return 0;                                                                        \
+  }
+  SPEX_TILE_CASE(128, 1)
+  SPEX_TILE_CASE(128, 2)
+  SPEX_TILE_CASE(128, 4)
+  SPEX_TILE_CASE(128, 6)
+  SPEX_TILE_CASE(64, 1)
+  SPEX_TILE_CASE(64, 2)
+#undef SPEX_TILE_CASE
   return -1;
 }
 
