@@ -72,6 +72,7 @@ typedef struct spex_model_stats {
   double prm_flops;
   long long launches;     /* kernels of this library launched by the forward (cuBLAS excluded) */
   long long gemm_calls;   /* cuBLAS GEMM calls */
+  double control_ms;      /* control kernel device time (overlapped with the forward when streaming) */
 } spex_model_stats;
 
 /* Per decode row-step shadow output (K3): argmax, logsumexp, logit sum. */

@@ -80,6 +80,7 @@ class ModelStats(ctypes.Structure):
         ("prm_flops", ctypes.c_double),
         ("launches", ctypes.c_longlong),
         ("gemm_calls", ctypes.c_longlong),
+        ("control_ms", ctypes.c_double),
     ]
 
     def as_dict(self) -> dict:

@@ -46,6 +46,16 @@ __global__ void __launch_bounds__(512, 1) spex_control_kernel(const Run* __restr
 
 }  // namespace spex
 
+extern "C" int spex_launch_control_async(spex::Run* d_run, int nthreads, cudaStream_t stream, cudaEvent_t a,
+                                         cudaEvent_t b) {
+  if (nthreads < 64 || nthreads > 512 || (nthreads & 31)) nthreads = 512;
+  cudaEventRecord(a, stream);
+  spex::spex_control_kernel<<<1, nthreads, 0, stream>>>(d_run);
+  cudaError_t e = cudaGetLastError();
+  cudaEventRecord(b, stream);
+  return static_cast<int>(e);
+}
+
 extern "C" int spex_launch_control(spex::Run* d_run, int nthreads, cudaStream_t stream, float* ms) {
   if (nthreads < 64 || nthreads > 512 || (nthreads & 31)) nthreads = 512;
   cudaEvent_t a, b;

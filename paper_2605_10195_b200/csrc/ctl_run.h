@@ -221,6 +221,40 @@ SPEX_HD void kv_ancestors_adjust(Run* R, int sid, int delta) {
   if (acc != 0) atomic_add_i64(&R->g->u_anc, acc);
 }
 
+// Publish schedule entry e to the host (all block writes before it become
+// visible first: per-thread gpu fence, barrier, then the leader's system fence).
+template <class EX>
+SPEX_HD void publish_entry(Run* R, EX& ex, int e, int rows, int tiles) {
+#if SPEX_DEVICE_PASS
+  if (!R->pub_e) return;
+  if (R->pub) __threadfence();
+  ex.sync();
+  if (ex.tid == 0) {
+    PubEntry pe;
+    pe.kind = R->sched_kind[e];
+    pe.steps = R->sched_steps[e];
+    pe.off = R->sched_off[e];
+    pe.n = R->sched_n[e];
+    pe.rows = rows;
+    pe.tiles = tiles;
+    pe.u0 = R->sched_u[e];
+    pe.kv_next = R->g->kv_next;
+    R->pub_e[e] = pe;
+    if (R->pub) {
+      __threadfence_system();
+      *reinterpret_cast<volatile int*>(&R->pub->n_sched) = e + 1;
+    }
+  }
+  ex.sync();
+#else
+  (void)R;
+  (void)ex;
+  (void)e;
+  (void)rows;
+  (void)tiles;
+#endif
+}
+
 // Record one decode epoch of the model schedule: `steps` forward steps over
 // the active streams (in active order) starting at their current positions.
 template <class EX>
@@ -255,6 +289,7 @@ SPEX_HD void record_decode(Run* R, EX& ex, int steps) {
     g->n_sched_rows = off + n;
   }
   ex.sync();
+  publish_entry(R, ex, g->n_sched - 1, n, 0);
 }
 
 // DecodeEngine::advance (sim.cpp:305-384). On return g->engine_now holds the
@@ -907,10 +942,22 @@ SPEX_HD void completions(Run* R, EX& ex, int* warp_off) {
     if (ns > 0 && (g->n_sched >= R->cfg.sched_cap || off + ns > R->cfg.sched_rows_cap)) {
       if (ex.tid == 0) set_err(R, ERR_CAP_STAGE, -1, kNoNode);
     } else if (ns > 0) {
+      for (int f = ex.tid; f < nf; f += ex.nthr) {
+        const int sc = R->fin_scored[f];
+        R->it_scan_b[f] = sc ? R->fin_tokens[f] : 0;
+        R->it_scan_d[f] = sc ? (R->fin_tokens[f] + kTileRows - 1) / kTileRows : 0;
+      }
+      ex.sync();
+      int nrows = 0, ntiles = 0;
+      ex_scan(ex, R->it_scan_b, nf, &nrows);
+      ex_scan(ex, R->it_scan_d, nf, &ntiles);
       for (int f = ex.tid; f < nf; f += ex.nthr)
         if (R->fin_scored[f]) {
-          R->srow_sid[off + R->it_scan_a[f]] = R->fins[f];
-          R->srow_pos0[off + R->it_scan_a[f]] = R->fin_tokens[f];
+          const int k = off + R->it_scan_a[f];
+          R->srow_sid[k] = R->fins[f];
+          R->srow_pos0[k] = R->fin_tokens[f];
+          R->srow_rstart[k] = R->it_scan_b[f];
+          R->srow_tstart[k] = R->it_scan_d[f];
         }
       if (ex.tid == 0) {
         const int e = g->n_sched++;
@@ -921,6 +968,8 @@ SPEX_HD void completions(Run* R, EX& ex, int* warp_off) {
         R->sched_n[e] = ns;
         g->n_sched_rows = off + ns;
       }
+      ex.sync();
+      publish_entry(R, ex, g->n_sched - 1, nrows, ntiles);
     }
     ex.sync();
   }
@@ -987,6 +1036,13 @@ SPEX_HD void run_loop(Run* R, EX& ex, int* warp_off) {
     g->makespan = ms;
   }
   ex.sync();
+#if SPEX_DEVICE_PASS
+  if (R->pub && ex.tid == 0) {
+    __threadfence_system();
+    *reinterpret_cast<volatile int*>(&R->pub->error) = g->error;
+    *reinterpret_cast<volatile int*>(&R->pub->done) = 1;
+  }
+#endif
 }
 
 }  // namespace spex

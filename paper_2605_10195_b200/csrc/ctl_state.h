@@ -244,6 +244,21 @@ struct GState {
   i64 cyc[8];
 };
 
+// Schedule entry published to the host (pinned, mapped) while the control
+// kernel runs, so the model forward for it can start immediately.
+struct PubEntry {
+  int kind, steps, off, n, rows, tiles;
+  i64 u0;
+  i64 kv_next;
+};
+
+struct PubHead {
+  int n_sched;
+  int done;
+  int error;
+  int pad;
+};
+
 struct Run {
   Cfg cfg;
   GState* g;
@@ -317,6 +332,10 @@ struct Run {
   int* srow_sid;
   int* srow_pos0;
   i64* sched_u;  // engine unique KV tokens at the start of a decode epoch
+  int* srow_rstart;  // PRM entries: first row of each thought in the entry
+  int* srow_tstart;  // PRM entries: first tile of each thought in the entry
+  PubHead* pub;      // host-mapped (nullptr: no streaming)
+  PubEntry* pub_e;
   int* it_scan_a;  // scan scratch
   int* it_scan_b;
   int* it_scan_c;

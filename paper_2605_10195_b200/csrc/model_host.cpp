@@ -24,6 +24,8 @@
 #include <cstring>
 #include <stdexcept>
 #include <string>
+#include <chrono>
+#include <thread>
 #include <vector>
 
 using namespace spex;
@@ -308,33 +310,16 @@ extern "C" void spex_model_cache_clear() {
   g_cache.pol = g_cache.prm = nullptr;
 }
 
-// Replays the recorded schedule through the policy and PRM.
+// Replays the schedule through the policy and PRM. Entries come either from a
+// finished control run (sv.entries_host) or live from the running control
+// kernel through host-mapped memory (sv.pub_head / sv.pub_entries): the model
+// stream then works on entry e while the control kernel produces e+1, ...
 void run_model_schedule(const ModelRunConfig& mc, const ScheduleView& sv, ModelRunResult* res, cudaStream_t st) {
-  const int n_e = sv.n_entries;
-  std::vector<int> kind(n_e), steps(n_e), off(n_e), cnt(n_e);
-  std::vector<long long> u0(n_e);
-  CK(cudaMemcpyAsync(kind.data(), sv.kind, n_e * sizeof(int), cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(steps.data(), sv.steps, n_e * sizeof(int), cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(off.data(), sv.off, n_e * sizeof(int), cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(cnt.data(), sv.n, n_e * sizeof(int), cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(u0.data(), sv.u0, n_e * sizeof(long long), cudaMemcpyDeviceToHost, st));
   std::vector<void*> owned;
-  int* prm_row_start = dalloc<int>(std::max(sv.n_rows, 1), owned);
-  int* prm_tile_start = dalloc<int>(std::max(sv.n_rows, 1), owned);
-  int* prm_totals = dalloc<int>(std::max(n_e, 1), owned);
-  int* prm_tile_totals = dalloc<int>(std::max(n_e, 1), owned);
-  spex_k_prm_scan_all(sv.tree, sv.kind, sv.off, sv.n, n_e, sv.srow_sid, prm_row_start, prm_tile_start, prm_totals,
-                      prm_tile_totals, st);
-  std::vector<int> totals(n_e), tile_totals(n_e);
-  CK(cudaMemcpyAsync(totals.data(), prm_totals, n_e * sizeof(int), cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(tile_totals.data(), prm_tile_totals, n_e * sizeof(int), cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
-
   const int Q = sv.n_queries, P = sv.tree.prompt_tokens;
-  int max_rows = 1;
-  for (int e = 0; e < n_e; ++e) max_rows = std::max(max_rows, kind[e] == SCHED_DECODE ? cnt[e] : totals[e]);
-  const int prompt_chunk = std::max(1, std::min(Q, std::max(max_rows, 4096) / std::max(P, 1)));
-  max_rows = std::max(max_rows, prompt_chunk * std::max(P, 1));
+  const bool streaming = sv.pub_head != nullptr;
+  const int max_dec = sv.max_decode_rows, max_prm = sv.max_prm_rows;
+  const int prompt_chunk = std::max(1, std::min(Q, 4096 / std::max(P, 1)));
   const long long slots = std::max<long long>(sv.kv_slots, 1);
 
   if (!g_cache.hb) CB(cublasCreate(&g_cache.hb));
@@ -342,14 +327,16 @@ void run_model_schedule(const ModelRunConfig& mc, const ScheduleView& sv, ModelR
   CB(cublasSetStream(hb, st));
   CB(cublasSetMathMode(hb, CUBLAS_DEFAULT_MATH));
   if (g_cache.seed != mc.seed) spex_model_cache_clear();
-  Model* pol = cached(g_cache.pol, mc.policy, false, mc.seed, slots, max_rows, st);
-  Model* prm = mc.with_prm ? cached(g_cache.prm, mc.prm, true, mc.seed, slots, max_rows, st) : nullptr;
+  Model* pol = cached(g_cache.pol, mc.policy, false, mc.seed, slots, std::max(max_dec, prompt_chunk * P), st);
+  Model* prm = mc.with_prm ? cached(g_cache.prm, mc.prm, true, mc.seed, slots, std::max(max_prm, prompt_chunk * P), st)
+                           : nullptr;
   g_cache.seed = mc.seed;
-  RowDesc* rows = dalloc<RowDesc>(max_rows, owned);
-  Segment* segs = dalloc<Segment>((size_t)max_rows * 40, owned);
-  int* last_row = dalloc<int>(max_rows, owned);
-  TileDesc* tiles = dalloc<TileDesc>(max_rows, owned);
-  float* scores = dalloc<float>(max_rows, owned);
+  const int rows_cap = std::max({max_dec, max_prm, prompt_chunk * P, 1});
+  RowDesc* rows = dalloc<RowDesc>(rows_cap, owned);
+  Segment* segs = dalloc<Segment>((size_t)rows_cap * 40, owned);
+  int* last_row = dalloc<int>(rows_cap, owned);
+  TileDesc* tiles = dalloc<TileDesc>(rows_cap, owned);
+  float* scores = dalloc<float>(rows_cap, owned);
   CK(cudaStreamSynchronize(st));
 
   TreeView tv_pol = sv.tree;
@@ -361,9 +348,8 @@ void run_model_schedule(const ModelRunConfig& mc, const ScheduleView& sv, ModelR
   cudaEventCreate(&t0);
   cudaEventCreate(&t1);
   cudaEventRecord(t0, st);
-  g_launches = 1;  // prm scan
+  g_launches = 0;
   g_gemms = 0;
-  // root prompts (prefill through both models)
   if (P > 0) {
     for (int q0 = 0; q0 < Q; q0 += prompt_chunk) {
       const int nq = std::min(prompt_chunk, Q - q0);
@@ -383,40 +369,79 @@ void run_model_schedule(const ModelRunConfig& mc, const ScheduleView& sv, ModelR
   DecodeOut* dbg = mc.record_outputs ? reinterpret_cast<DecodeOut*>(mc.out_rows) : nullptr;
   PrmOut* dbg_scores = mc.record_outputs ? reinterpret_cast<PrmOut*>(mc.out_scores) : nullptr;
   long long dbg_n = 0, dbg_s = 0;
-  for (int e = 0; e < n_e; ++e) {
-    if (kind[e] == SCHED_DECODE) {
-      const int n = cnt[e];
-      for (int s = 0; s < steps[e]; ++s) {
-        spex_k_build_decode_rows(tv_pol, sv.srow_sid + off[e], sv.srow_pos0 + off[e], n, s, rows, segs, st);
-        g_launches += 1;
-        forward(*pol, rows, segs, n, hb, st, mc.time_attn ? &timer : nullptr);
-        res->decode_rows += n;
+
+  auto process = [&](const PubEntry& pe) {
+    if (pe.kv_next > slots) throw std::runtime_error("tree KV pool capacity exceeded");
+    if (pe.kind == SCHED_DECODE) {
+      for (int s = 0; s < pe.steps; ++s) {
+        for (int c0 = 0; c0 < pe.n; c0 += max_dec) {
+          const int n = std::min(max_dec, pe.n - c0);
+          spex_k_build_decode_rows(tv_pol, sv.srow_sid + pe.off + c0, sv.srow_pos0 + pe.off + c0, n, s, rows, segs,
+                                   st);
+          g_launches += 1;
+          forward(*pol, rows, segs, n, hb, st, mc.time_attn ? &timer : nullptr);
+          if (dbg && dbg_n + n <= mc.out_rows_cap) {
+            spex_k_gather_outputs(rows, n, pol->amax, pol->lse, pol->lsum, dbg + dbg_n, st);
+            dbg_n += n;
+          }
+        }
+        res->decode_rows += pe.n;
         res->decode_steps += 1;
         // algorithmic K1 bytes: unique KV tokens of the step (engine U + the new tokens)
-        const double utok = (double)u0[e] + (double)s * n + n;
+        const double utok = (double)pe.u0 + (double)s * pe.n + pe.n;
         res->attn_alg_bytes += utok * kv_tok_bytes * mc.policy.L +
-                               (double)n * mc.policy.H * mc.policy.dh * (4.0 + 2.0) * mc.policy.L;
-        if (dbg && dbg_n + n <= mc.out_rows_cap) {
-          spex_k_gather_outputs(rows, n, pol->amax, pol->lse, pol->lsum, dbg + dbg_n, st);
-          dbg_n += n;
-        }
+                               (double)pe.n * mc.policy.H * mc.policy.dh * (4.0 + 2.0) * mc.policy.L;
       }
-    } else if (prm) {
-      const int n = cnt[e];
-      const int M = totals[e];
-      if (M <= 0) continue;
-      spex_k_build_prm_rows(tv_prm, sv.srow_sid + off[e], prm_row_start + off[e], prm_tile_start + off[e], n, rows,
-                            segs, last_row, tiles, st);
-      forward(*prm, rows, segs, M, hb, st, nullptr, tiles, tile_totals[e]);
-      spex_k_value_head(prm->Xn, mc.prm.d, last_row, n, prm->vhead, scores, st);
+    } else if (prm && pe.rows > 0) {
+      if (pe.rows > max_prm) throw std::runtime_error("PRM batch larger than the row buffers");
+      spex_k_build_prm_rows(tv_prm, sv.srow_sid + pe.off, sv.srow_rstart + pe.off, sv.srow_tstart + pe.off, pe.n,
+                            rows, segs, last_row, tiles, st);
+      forward(*prm, rows, segs, pe.rows, hb, st, nullptr, tiles, pe.tiles);
+      spex_k_value_head(prm->Xn, mc.prm.d, last_row, pe.n, prm->vhead, scores, st);
       g_launches += 2;
-      if (dbg_scores && dbg_s + n <= mc.out_scores_cap) {
-        spex_k_gather_prm(rows, last_row, n, scores, dbg_scores + dbg_s, st);
-        dbg_s += n;
+      if (dbg_scores && dbg_s + pe.n <= mc.out_scores_cap) {
+        spex_k_gather_prm(rows, last_row, pe.n, scores, dbg_scores + dbg_s, st);
+        dbg_s += pe.n;
       }
-      res->prm_rows += M;
-      res->prm_thoughts += n;
+      res->prm_rows += pe.rows;
+      res->prm_thoughts += pe.n;
     }
+  };
+
+  if (!streaming) {
+    for (int e = 0; e < sv.n_entries; ++e) process(sv.entries_host[e]);
+  } else {
+    volatile PubHead* head = reinterpret_cast<volatile PubHead*>(sv.pub_head);
+    volatile PubEntry* ents = reinterpret_cast<volatile PubEntry*>(sv.pub_entries);
+    int e = 0;
+    auto last_progress = std::chrono::steady_clock::now();
+    for (;;) {
+      const int n = head->n_sched;
+      if (e < n) {
+        last_progress = std::chrono::steady_clock::now();
+        for (; e < n; ++e) {
+          PubEntry pe;
+          pe.kind = ents[e].kind;
+          pe.steps = ents[e].steps;
+          pe.off = ents[e].off;
+          pe.n = ents[e].n;
+          pe.rows = ents[e].rows;
+          pe.tiles = ents[e].tiles;
+          pe.u0 = ents[e].u0;
+          pe.kv_next = ents[e].kv_next;
+          process(pe);
+        }
+        continue;
+      }
+      if (head->done) {
+        if (head->n_sched == e) break;
+        continue;
+      }
+      if (std::chrono::steady_clock::now() - last_progress > std::chrono::seconds(300))
+        throw std::runtime_error("control kernel published nothing for 300 s");
+      std::this_thread::yield();
+    }
+    res->control_error = head->error;
   }
   cudaEventRecord(t1, st);
   CK(cudaEventSynchronize(t1));

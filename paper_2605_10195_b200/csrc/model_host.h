@@ -7,6 +7,7 @@
 #include <utility>
 #include <vector>
 
+#include "ctl_state.h"
 #include "model.h"
 
 namespace spex {
@@ -27,16 +28,19 @@ struct ModelRunConfig {
 struct ScheduleView {
   TreeView tree;
   int n_queries;
-  int n_entries;
-  int n_rows;
-  long long kv_slots;
-  const int* kind;
-  const int* steps;
-  const int* off;
-  const int* n;
-  const long long* u0;
+  long long kv_slots;        // tree KV pool capacity (slots)
+  int max_decode_rows;       // row-buffer capacity for decode steps (larger entries are chunked)
+  int max_prm_rows;          // row-buffer capacity for one PRM batch
+  // finished schedule (sequential mode)
+  int n_entries = 0;
+  const PubEntry* entries_host = nullptr;
+  // live schedule (streaming mode; host-mapped, written by the control kernel)
+  void* pub_head = nullptr;
+  void* pub_entries = nullptr;
   const int* srow_sid;
   const int* srow_pos0;
+  const int* srow_rstart;
+  const int* srow_tstart;
 };
 
 struct ModelRunResult {
@@ -47,6 +51,8 @@ struct ModelRunResult {
   long long decode_rows = 0, decode_steps = 0, prefill_rows = 0, prm_rows = 0, prm_thoughts = 0;
   long long out_rows = 0, out_scores = 0;
   double policy_flops = 0.0, prm_flops = 0.0;
+  int control_error = 0;
+  double control_ms = 0.0;
   long long launches = 0;  // kernels of this library launched by the replay (cuBLAS excluded)
   long long gemm_calls = 0;
 };
@@ -55,6 +61,8 @@ struct AttnTimer {
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
   int n = 0;
   double total_ms = 0.0;
+  int control_error = 0;
+  double control_ms = 0.0;
   long long launches = 0;
   void begin(cudaStream_t st);
   void end(cudaStream_t st);

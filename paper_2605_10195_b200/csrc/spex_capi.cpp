@@ -458,6 +458,7 @@ struct spex_executor {
   int record_sched = 0;
 #ifndef SPEX_EMU
   cudaStream_t stream = nullptr;
+  cudaStream_t mstream = nullptr;
   bool with_model = false;
   ModelRunConfig mc;
   ModelRunResult mres;
@@ -468,6 +469,9 @@ struct spex_executor {
 
 #ifndef SPEX_EMU
 extern "C" int spex_launch_control(Run* d_run, int nthreads, cudaStream_t stream, float* ms);
+extern "C" int spex_launch_control_async(Run* d_run, int nthreads, cudaStream_t stream, cudaEvent_t a,
+                                         cudaEvent_t b);
+extern "C" void spex_model_cache_clear();
 #define CUDA_OK(x)                                                                  \
   do {                                                                              \
     cudaError_t e_ = (x);                                                           \
@@ -636,6 +640,9 @@ void layout(Arena& A, Run& R, int Q, int node_cap, int stream_cap, int log_cap, 
   A.add(R.srow_sid, static_cast<size_t>(R.cfg.sched_rows_cap));
   A.add(R.srow_pos0, static_cast<size_t>(R.cfg.sched_rows_cap));
   A.add(R.sched_u, static_cast<size_t>(R.cfg.sched_cap));
+  A.add(R.srow_rstart, static_cast<size_t>(R.cfg.sched_rows_cap));
+  A.add(R.srow_tstart, static_cast<size_t>(R.cfg.sched_rows_cap));
+  if (R.cfg.record_sched) A.add(R.pub_e, static_cast<size_t>(R.cfg.sched_cap));
 }
 
 std::string label_str(int idx) { return idx < 0 ? std::string() : "a" + std::to_string(idx); }
@@ -845,6 +852,7 @@ void run_executor(spex_executor& ex, int trace) {
 #else
     CUDA_OK(cudaSetDevice(ex.device));
     if (!ex.stream) CUDA_OK(cudaStreamCreateWithFlags(&ex.stream, cudaStreamNonBlocking));
+    if (!ex.mstream) CUDA_OK(cudaStreamCreateWithFlags(&ex.mstream, cudaStreamNonBlocking));
     char* base = nullptr;
     CUDA_OK(cudaMalloc(&base, A.total + 256));
     CUDA_OK(cudaMemsetAsync(base, 0, A.total + 256, ex.stream));
@@ -854,22 +862,29 @@ void run_executor(spex_executor& ex, int trace) {
     CUDA_OK(cudaMemcpyAsync(d_tab, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice,
                             ex.stream));
     R.log_tab = d_tab;
+    // streaming schedule: head + entries in pinned, device-mapped host memory
+    const bool streaming = ex.with_model && !std::getenv("SPEX_SEQUENTIAL");
+    PubHead* h_head = nullptr;
+    PubEntry* h_ents = nullptr;
+    if (streaming) {
+      CUDA_OK(cudaHostAlloc(&h_head, sizeof(PubHead), cudaHostAllocMapped));
+      CUDA_OK(cudaHostAlloc(&h_ents, sizeof(PubEntry) * R.cfg.sched_cap, cudaHostAllocMapped));
+      std::memset(h_head, 0, sizeof(PubHead));
+      CUDA_OK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&R.pub), h_head, 0));
+      CUDA_OK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&R.pub_e), h_ents, 0));
+    }
     Run* d_run = nullptr;
     CUDA_OK(cudaMalloc(&d_run, sizeof(Run)));
     CUDA_OK(cudaMemcpyAsync(d_run, &R, sizeof(Run), cudaMemcpyHostToDevice, ex.stream));
-    float ms = 0.f;
-    int lr = spex_launch_control(d_run, ex.nthreads, ex.stream, &ms);
-    if (lr != 0) {
+    auto cleanup = [&] {
       cudaFree(base);
       cudaFree(d_tab);
       cudaFree(d_run);
-      fail(200, std::string("control kernel launch failed: ") + cudaGetErrorString(static_cast<cudaError_t>(lr)));
-    }
-    ex.device_ms = ms;
-    CUDA_OK(cudaMemcpyAsync(&ex.g, R.g, sizeof(GState), cudaMemcpyDeviceToHost, ex.stream));
-    CUDA_OK(cudaStreamSynchronize(ex.stream));
-    if (ex.with_model && ex.g.error == 0) {
-      ScheduleView sv{};
+      if (h_head) cudaFreeHost(h_head);
+      if (h_ents) cudaFreeHost(h_ents);
+    };
+    ScheduleView sv{};
+    if (ex.with_model) {
       sv.tree.parent = R.n_parent;
       sv.tree.tokens = R.n_tokens;
       sv.tree.hash = R.n_hash;
@@ -879,49 +894,91 @@ void run_executor(spex_executor& ex, int trace) {
       sv.tree.node_cap = node_cap;
       sv.tree.prompt_tokens = ex.hc.prompt_tokens;
       sv.n_queries = Q;
-      sv.n_entries = ex.g.n_sched;
-      sv.n_rows = ex.g.n_sched_rows;
-      sv.kv_slots = ex.g.kv_next;
-      sv.kind = R.sched_kind;
-      sv.steps = R.sched_steps;
-      sv.off = R.sched_off;
-      sv.n = R.sched_n;
-      sv.u0 = R.sched_u;
-      sv.srow_sid = R.sched_kind ? R.srow_sid : nullptr;
+      sv.srow_sid = R.srow_sid;
       sv.srow_pos0 = R.srow_pos0;
-      ModelRunConfig mc = ex.mc;
-      void* d_rows = nullptr;
-      void* d_scores = nullptr;
-      if (mc.record_outputs) {
-        mc.out_rows_cap = ex.g.decode_rows;
-        mc.out_scores_cap = static_cast<long long>(Q) * node_cap;
-        CUDA_OK(cudaMalloc(&d_rows, std::max<long long>(mc.out_rows_cap, 1) * sizeof(DecodeOut)));
-        CUDA_OK(cudaMalloc(&d_scores, std::max<long long>(mc.out_scores_cap, 1) * sizeof(PrmOut)));
-        mc.out_rows = d_rows;
-        mc.out_scores = d_scores;
+      sv.srow_rstart = R.srow_rstart;
+      sv.srow_tstart = R.srow_tstart;
+      sv.max_decode_rows = 16384;
+      sv.max_prm_rows = 1 << 17;
+    }
+    ModelRunConfig mc = ex.mc;
+    void* d_rows = nullptr;
+    void* d_scores = nullptr;
+    auto alloc_outputs = [&](long long rows_cap) {
+      if (!mc.record_outputs) return;
+      mc.out_rows_cap = rows_cap;
+      mc.out_scores_cap = static_cast<long long>(Q) * node_cap;
+      CUDA_OK(cudaMalloc(&d_rows, std::max<long long>(mc.out_rows_cap, 1) * sizeof(DecodeOut)));
+      CUDA_OK(cudaMalloc(&d_scores, std::max<long long>(mc.out_scores_cap, 1) * sizeof(PrmOut)));
+      mc.out_rows = d_rows;
+      mc.out_scores = d_scores;
+    };
+    cudaEvent_t ca, cb;
+    cudaEventCreate(&ca);
+    cudaEventCreate(&cb);
+    bool model_done = false;
+    ex.mres = ModelRunResult{};
+    if (streaming) {
+      CUDA_OK(cudaStreamSynchronize(ex.stream));
+      // KV pool capacity from the free-memory budget (both models, all layers)
+      size_t free_b = 0, total_b = 0;
+      cudaMemGetInfo(&free_b, &total_b);
+      const double per_slot = 4.0 * (mc.policy.L * mc.policy.KVH * mc.policy.dh +
+                                     (mc.with_prm ? mc.prm.L * mc.prm.KVH * mc.prm.dh : 0));
+      sv.kv_slots = static_cast<long long>(0.55 * static_cast<double>(free_b) / per_slot);
+      if (const char* e = std::getenv("SPEX_KV_SLOTS")) sv.kv_slots = std::atoll(e);
+      alloc_outputs(static_cast<long long>(Q) * node_cap * 64);
+      int lr = spex_launch_control_async(d_run, ex.nthreads, ex.stream, ca, cb);
+      if (lr != 0) {
+        cleanup();
+        fail(200, std::string("control kernel launch failed: ") + cudaGetErrorString(static_cast<cudaError_t>(lr)));
       }
-      ex.mres = ModelRunResult{};
       try {
-        run_model_schedule(mc, sv, &ex.mres, ex.stream);
+        run_model_schedule(mc, sv, &ex.mres, ex.mstream);
+        model_done = true;
+      } catch (const std::exception& e) {
+        // capacity exceeded while streaming: fall back to a sequential replay below
+        if (std::getenv("SPEX_DEBUG")) std::fprintf(stderr, "streaming replay fallback: %s\n", e.what());
+        cudaStreamSynchronize(ex.mstream);
+        ex.mres = ModelRunResult{};
+      }
+    } else {
+      int lr = spex_launch_control_async(d_run, ex.nthreads, ex.stream, ca, cb);
+      if (lr != 0) {
+        cleanup();
+        fail(200, std::string("control kernel launch failed: ") + cudaGetErrorString(static_cast<cudaError_t>(lr)));
+      }
+    }
+    CUDA_OK(cudaEventSynchronize(cb));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ca, cb);
+    cudaEventDestroy(ca);
+    cudaEventDestroy(cb);
+    ex.device_ms = ms;
+    CUDA_OK(cudaMemcpyAsync(&ex.g, R.g, sizeof(GState), cudaMemcpyDeviceToHost, ex.stream));
+    CUDA_OK(cudaStreamSynchronize(ex.stream));
+    if (ex.with_model && ex.g.error == 0 && !model_done) {
+      // sequential replay over the finished schedule
+      std::vector<PubEntry> ents(ex.g.n_sched);
+      if (!ents.empty())
+        CUDA_OK(cudaMemcpy(ents.data(), streaming ? static_cast<void*>(h_ents) : static_cast<void*>(R.pub_e),
+                           ents.size() * sizeof(PubEntry), streaming ? cudaMemcpyHostToHost : cudaMemcpyDeviceToHost));
+      sv.pub_head = nullptr;
+      sv.pub_entries = nullptr;
+      sv.entries_host = ents.data();
+      sv.n_entries = static_cast<int>(ents.size());
+      sv.kv_slots = ex.g.kv_next;
+      if (!d_rows) alloc_outputs(ex.g.decode_rows);
+      try {
+        run_model_schedule(mc, sv, &ex.mres, ex.mstream);
       } catch (const std::exception& e) {
         cudaFree(d_rows);
         cudaFree(d_scores);
-        cudaFree(base);
-        cudaFree(d_tab);
-        cudaFree(d_run);
+        cleanup();
         fail(201, std::string("model forward: ") + e.what());
       }
-      if (mc.record_outputs) {
-        ex.dec_out.resize(ex.mres.out_rows);
-        ex.prm_out.resize(ex.mres.out_scores);
-        if (!ex.dec_out.empty())
-          CUDA_OK(cudaMemcpy(ex.dec_out.data(), d_rows, ex.dec_out.size() * sizeof(DecodeOut), cudaMemcpyDeviceToHost));
-        if (!ex.prm_out.empty())
-          CUDA_OK(cudaMemcpy(ex.prm_out.data(), d_scores, ex.prm_out.size() * sizeof(PrmOut), cudaMemcpyDeviceToHost));
-        cudaFree(d_rows);
-        cudaFree(d_scores);
-      }
     }
+    if (ex.with_model) ex.mres.control_ms = ms;
     ex.qs.resize(Q);
     CUDA_OK(cudaMemcpyAsync(ex.qs.data(), R.qs, sizeof(QueryRun) * Q, cudaMemcpyDeviceToHost, ex.stream));
     CUDA_OK(cudaStreamSynchronize(ex.stream));
@@ -931,9 +988,17 @@ void run_executor(spex_executor& ex, int trace) {
                               ex.stream));
       CUDA_OK(cudaStreamSynchronize(ex.stream));
     }
-    cudaFree(base);
-    cudaFree(d_tab);
-    cudaFree(d_run);
+    if (mc.record_outputs && ex.with_model) {
+      ex.dec_out.resize(ex.mres.out_rows);
+      ex.prm_out.resize(ex.mres.out_scores);
+      if (!ex.dec_out.empty())
+        CUDA_OK(cudaMemcpy(ex.dec_out.data(), d_rows, ex.dec_out.size() * sizeof(DecodeOut), cudaMemcpyDeviceToHost));
+      if (!ex.prm_out.empty())
+        CUDA_OK(cudaMemcpy(ex.prm_out.data(), d_scores, ex.prm_out.size() * sizeof(PrmOut), cudaMemcpyDeviceToHost));
+    }
+    cudaFree(d_rows);
+    cudaFree(d_scores);
+    cleanup();
 #endif
     if (ex.g.error == ERR_CAP_NODES || ex.g.error == ERR_CAP_STAGE) {
       node_cap *= 2;  // capacity, not semantics: rerun with a larger arena
@@ -1083,6 +1148,7 @@ int spex_executor_model_stats(spex_executor* ex, spex_model_stats* out) {
     out->policy_flops = r.policy_flops;
     out->prm_flops = r.prm_flops;
     out->launches = r.launches;
+    out->control_ms = r.control_ms;
     out->gemm_calls = r.gemm_calls;
 #else
     (void)ex;
@@ -1123,6 +1189,7 @@ int spex_executor_prm_outputs(spex_executor* ex, void* buf, long long cap, long 
 void spex_executor_destroy(spex_executor* ex) {
 #ifndef SPEX_EMU
   if (ex && ex->stream) cudaStreamDestroy(ex->stream);
+  if (ex && ex->mstream) cudaStreamDestroy(ex->mstream);
 #endif
   delete ex;
 }
