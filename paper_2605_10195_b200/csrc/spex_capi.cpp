@@ -927,6 +927,8 @@ void run_executor(spex_executor& ex, int trace) {
                                      (mc.with_prm ? mc.prm.L * mc.prm.KVH * mc.prm.dh : 0));
       sv.kv_slots = static_cast<long long>(0.55 * static_cast<double>(free_b) / per_slot);
       if (const char* e = std::getenv("SPEX_KV_SLOTS")) sv.kv_slots = std::atoll(e);
+      sv.pub_head = h_head;
+      sv.pub_entries = h_ents;
       alloc_outputs(static_cast<long long>(Q) * node_cap * 64);
       int lr = spex_launch_control_async(d_run, ex.nthreads, ex.stream, ca, cb);
       if (lr != 0) {
