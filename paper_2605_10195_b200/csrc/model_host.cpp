@@ -298,7 +298,7 @@ static Model* cached(Model*& slot, const ModelShape& sh, bool prm, uint64_t seed
     return slot;
   delete slot;
   slot = nullptr;
-  CK(cudaDeviceSynchronize());
+  CK(cudaStreamSynchronize(st));
   slot = make_model(sh, prm, prm ? (seed ^ 0x50524d00ULL) : seed, slots + slots / 8 + 1024,
                     max_rows + max_rows / 8 + 256, st);
   return slot;

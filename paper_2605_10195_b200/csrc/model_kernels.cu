@@ -260,16 +260,23 @@ __global__ void rope_kv_kernel(const RowDesc* rows, int M, const float* QKV, int
                                float* Qr) {
   const int r = blockIdx.x;
   if (r >= M) return;
+  __shared__ float sc[128], ss[128];
   const RowDesc rd = rows[r];
   const int width = (H + 2 * KVH) * dh;
   const float* src = QKV + (long long)r * width;
   const int half = dh / 2;
   const float qscale = rsqrtf((float)dh);
-  for (int idx = threadIdx.x; idx < (H + KVH) * half; idx += blockDim.x) {
-    const int head = idx / half;
-    const int i = idx % half;
+  for (int i = threadIdx.x; i < half; i += blockDim.x) {
     float s, c;
     sincosf((float)rd.abs_pos * inv_freq[i], &s, &c);
+    sc[i] = c;
+    ss[i] = s;
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < (H + KVH) * half; idx += blockDim.x) {
+    const int head = idx / half;
+    const int i = idx - head * half;
+    const float c = sc[i], s = ss[i];
     const float* x = src + head * dh;
     const float a = x[i], b = x[i + half];
     const float ya = a * c - b * s;
@@ -287,7 +294,7 @@ __global__ void rope_kv_kernel(const RowDesc* rows, int M, const float* QKV, int
   }
   for (int idx = threadIdx.x; idx < KVH * dh; idx += blockDim.x) {
     const int kh = idx / dh;
-    const int i = idx % dh;
+    const int i = idx - kh * dh;
     Vp[((long long)kh * slots + rd.slot) * dh + i] = __float2bfloat16_rn(src[(H + KVH) * dh + kh * dh + i]);
   }
 }
@@ -786,13 +793,16 @@ __global__ void __launch_bounds__(kAttnThreads) tree_attn_tile_kernel(const Tile
 }
 
 __global__ void swiglu_kernel(const float* GU, int M, int F, __nv_bfloat16* A) {
-  const long long n = (long long)M * F;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-       i += (long long)gridDim.x * blockDim.x) {
-    const long long r = i / F, j = i % F;
-    const float g = GU[r * 2 * F + j];
-    const float u = GU[r * 2 * F + F + j];
-    A[i] = __float2bfloat16_rn(g / (1.f + __expf(-g)) * u);
+  const int r = blockIdx.y;
+  const float* g = GU + (long long)r * 2 * F;
+  const float* u = g + F;
+  __nv_bfloat16* a = A + (long long)r * F;
+  for (int j = (blockIdx.x * blockDim.x + threadIdx.x) * 2; j < F; j += gridDim.x * blockDim.x * 2) {
+    const float2 gv = *reinterpret_cast<const float2*>(g + j);
+    const float2 uv = *reinterpret_cast<const float2*>(u + j);
+    const float o0 = gv.x / (1.f + __expf(-gv.x)) * uv.x;
+    const float o1 = gv.y / (1.f + __expf(-gv.y)) * uv.y;
+    *reinterpret_cast<__nv_bfloat162*>(a + j) = __floats2bfloat162_rn(o0, o1);
   }
 }
 
@@ -1038,7 +1048,8 @@ extern "C" int spex_k_tree_attn_tiles(const TileDesc* tiles, int ntiles, const R
 }
 
 extern "C" void spex_k_swiglu(const float* GU, int M, int F, __nv_bfloat16* A, cudaStream_t s) {
-  swiglu_kernel<<<1184, 256, 0, s>>>(GU, M, F, A);
+  dim3 grid((F / 2 + 255) / 256, M);
+  swiglu_kernel<<<grid, 256, 0, s>>>(GU, M, F, A);
 }
 
 extern "C" void spex_k_lm_epilogue(const float* logits, int M, int V, int* amax, float* lse, float* lsum,
