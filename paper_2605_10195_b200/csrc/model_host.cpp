@@ -15,12 +15,14 @@
 #include "model_host.h"
 
 #include <cublas_v2.h>
+#include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -37,6 +39,9 @@ void spex_k_build_decode_rows(TreeView t, const int* sids, const int* pos0, int 
 void spex_k_build_prm_rows(TreeView t, const int* sids, const int* row_start, const int* tile_start, int n,
                            RowDesc* rows, Segment* segs, int* last_row, TileDesc* tiles, cudaStream_t s);
 void spex_k_build_prompt_tiles(int nq, int P, TileDesc* tiles, cudaStream_t s);
+int spex_k_tree_attn_tiles_mma(const CUtensorMap* kmap, const CUtensorMap* vmap, const TileDesc* tiles, int ntiles,
+                               const RowDesc* rows, const Segment* segs, const float* Qr, int H, int KVH, int dh,
+                               long long slots, __nv_bfloat16* O, cudaStream_t s);
 int spex_k_tree_attn_tiles(const TileDesc* tiles, int ntiles, const RowDesc* rows, const Segment* segs,
                            const float* Qr, int H, int KVH, int dh, const __nv_bfloat16* Kp, const __nv_bfloat16* Vp,
                            long long slots, __nv_bfloat16* O, cudaStream_t s);
@@ -94,8 +99,41 @@ void gemm(cublasHandle_t h, const __nv_bfloat16* x, const __nv_bfloat16* W, floa
 
 namespace spex {
 
+// TMA descriptor of one KV pool viewed as a 2D [KVH*slots][dh] bf16 tensor,
+// 64x64-element boxes with 128-byte swizzle (tree_attn_tile_mma_kernel).
+typedef CUresult (*PFN_tmap_encode)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static PFN_tmap_encode tmap_encoder() {
+  static PFN_tmap_encode fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_tmap_encode>(p);
+  }
+  return fn;
+}
+
+static bool make_kv_tmap(CUtensorMap* m, void* base, long long rows, int dh) {
+  PFN_tmap_encode enc = tmap_encoder();
+  if (!enc || dh != 128) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)dh, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)dh * 2};
+  cuuint32_t box[2] = {64, 64};
+  cuuint32_t es[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 struct Model {
   ModelShape sh;
+  std::vector<CUtensorMap> kmap, vmap;  // per layer (empty when TMA maps are unavailable)
   bool is_prm;
   long long slots;
   int max_rows;
@@ -167,6 +205,18 @@ static Model* make_model(const ModelShape& sh, bool prm, uint64_t seed, long lon
     m->Kp.push_back(dalloc<__nv_bfloat16>((size_t)sh.KVH * slots * sh.dh, o));
     m->Vp.push_back(dalloc<__nv_bfloat16>((size_t)sh.KVH * slots * sh.dh, o));
   }
+  if (!getenv("SPEX_NO_MMA_ATTN")) {
+    m->kmap.resize(sh.L);
+    m->vmap.resize(sh.L);
+    for (int l = 0; l < sh.L; ++l) {
+      if (!make_kv_tmap(&m->kmap[l], m->Kp[l], (long long)sh.KVH * slots, sh.dh) ||
+          !make_kv_tmap(&m->vmap[l], m->Vp[l], (long long)sh.KVH * slots, sh.dh)) {
+        m->kmap.clear();
+        m->vmap.clear();
+        break;
+      }
+    }
+  }
   if (prm) {
     m->vhead = dalloc<__nv_bfloat16>(sh.d, o);
     init(m->vhead, sh.d, 3, kStd);
@@ -211,7 +261,12 @@ static void forward(Model& m, const RowDesc* rows, const Segment* segs, int M, c
     gemm(hb, m.Xn, m.wqkv[l], m.QKV, M, (s.H + 2 * s.KVH) * s.dh, s.d, false);
     spex_k_rope_kv(rows, M, m.QKV, s.H, s.KVH, s.dh, m.inv_freq, m.slots, m.Kp[l], m.Vp[l], m.Qr, st);
     if (timer) timer->begin(st);
-    const int rc = tiles ? spex_k_tree_attn_tiles(tiles, ntiles, rows, segs, m.Qr, s.H, s.KVH, s.dh, m.Kp[l],
+    int rc = -1;
+    if (tiles && !m.kmap.empty())
+      rc = spex_k_tree_attn_tiles_mma(&m.kmap[l], &m.vmap[l], tiles, ntiles, rows, segs, m.Qr, s.H, s.KVH, s.dh,
+                                      m.slots, m.O, st);
+    if (rc != 0)
+      rc = tiles ? spex_k_tree_attn_tiles(tiles, ntiles, rows, segs, m.Qr, s.H, s.KVH, s.dh, m.Kp[l],
                                                   m.Vp[l], m.slots, m.O, st)
                          : spex_k_tree_attn(rows, segs, m.Qr, s.H, s.KVH, s.dh, m.Kp[l], m.Vp[l], m.slots, m.O, M, st);
     if (rc != 0) throw std::runtime_error("tree attention: unsupported head shape");
@@ -283,6 +338,13 @@ struct ModelCache {
   Model* prm = nullptr;
   unsigned long long seed = 0;
   cublasHandle_t hb = nullptr;
+  // replay row buffers (kept resident: no cudaMalloc while the control kernel runs)
+  int rows_cap = 0;
+  RowDesc* rows = nullptr;
+  Segment* segs = nullptr;
+  int* last_row = nullptr;
+  TileDesc* tiles = nullptr;
+  float* scores = nullptr;
 };
 static ModelCache g_cache;
 
@@ -322,7 +384,12 @@ void run_model_schedule(const ModelRunConfig& mc, const ScheduleView& sv, ModelR
   const int prompt_chunk = std::max(1, std::min(Q, 4096 / std::max(P, 1)));
   const long long slots = std::max<long long>(sv.kv_slots, 1);
 
-  if (!g_cache.hb) CB(cublasCreate(&g_cache.hb));
+  if (!g_cache.hb) {
+    CB(cublasCreate(&g_cache.hb));
+    void* ws = nullptr;
+    CK(cudaMalloc(&ws, 64 << 20));  // fixed workspace: no lazy allocation while streaming
+    CB(cublasSetWorkspace(g_cache.hb, ws, 64 << 20));
+  }
   cublasHandle_t hb = g_cache.hb;
   CB(cublasSetStream(hb, st));
   CB(cublasSetMathMode(hb, CUBLAS_DEFAULT_MATH));
@@ -332,12 +399,25 @@ void run_model_schedule(const ModelRunConfig& mc, const ScheduleView& sv, ModelR
                            : nullptr;
   g_cache.seed = mc.seed;
   const int rows_cap = std::max({max_dec, max_prm, prompt_chunk * P, 1});
-  RowDesc* rows = dalloc<RowDesc>(rows_cap, owned);
-  Segment* segs = dalloc<Segment>((size_t)rows_cap * 40, owned);
-  int* last_row = dalloc<int>(rows_cap, owned);
-  TileDesc* tiles = dalloc<TileDesc>(rows_cap, owned);
-  float* scores = dalloc<float>(rows_cap, owned);
-  CK(cudaStreamSynchronize(st));
+  if (g_cache.rows_cap < rows_cap) {
+    cudaFree(g_cache.rows);
+    cudaFree(g_cache.segs);
+    cudaFree(g_cache.last_row);
+    cudaFree(g_cache.tiles);
+    cudaFree(g_cache.scores);
+    std::vector<void*> keep;
+    g_cache.rows = dalloc<RowDesc>(rows_cap, keep);
+    g_cache.segs = dalloc<Segment>((size_t)rows_cap * 40, keep);
+    g_cache.last_row = dalloc<int>(rows_cap, keep);
+    g_cache.tiles = dalloc<TileDesc>(rows_cap, keep);
+    g_cache.scores = dalloc<float>(rows_cap, keep);
+    g_cache.rows_cap = rows_cap;
+  }
+  RowDesc* rows = g_cache.rows;
+  Segment* segs = g_cache.segs;
+  int* last_row = g_cache.last_row;
+  TileDesc* tiles = g_cache.tiles;
+  float* scores = g_cache.scores;
 
   TreeView tv_pol = sv.tree;
   tv_pol.V = mc.policy.V;

@@ -10,6 +10,7 @@
 //   K4 value_head_kernel   PRM score sigmoid(w . h_last)
 //   plus weight init, row descriptors, embedding, RMSNorm->bf16, RoPE + KV
 //   append, SwiGLU.
+#include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -617,6 +618,300 @@ __global__ void __launch_bounds__(256) tree_attn_decode_kernel(const RowDesc* __
   }
 }
 
+// ----------------------------------------------------------------------------
+// K1 tile variant on tensor cores (PRM / prompt prefill rows, DH = 128).
+// K/V chunks of 64 tokens arrive by TMA (2D tensor maps over the pool viewed as
+// [KVH*slots][128], two 64-element boxes per chunk, 128-byte swizzle) into a
+// double buffer guarded by mbarriers. Each warp takes (head g, token slice of
+// 64/SPLIT tokens): S = Q K^T and O += P V with mma.sync m16n8k16 (bf16 in,
+// fp32 accumulate), fragments via ldmatrix (.trans for V), online softmax in
+// registers; warps of the same head merge (m, l, O) through shared memory.
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+      ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(map), "r"(c0), "r"(c1),
+      "r"((uint32_t)__cvta_generic_to_shared(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr));
+}
+
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr));
+}
+
+__device__ __forceinline__ void mma_bf16(float* c, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
+                                         uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+// byte offset of (row, 16-byte chunk c in [0,16)) in a swizzled [2 halves][64 rows][128 B] chunk buffer
+__device__ __forceinline__ uint32_t swz(int row, int c) {
+  const int half = c >> 3, cc = c & 7;
+  return (uint32_t)(half * 8192 + row * 128 + ((cc ^ (row & 7)) << 4));
+}
+
+template <int G>
+__global__ void __launch_bounds__(128) tree_attn_tile_mma_kernel(const __grid_constant__ CUtensorMap kmap,
+                                                                const __grid_constant__ CUtensorMap vmap,
+                                                                const TileDesc* __restrict__ tiles,
+                                                                const RowDesc* __restrict__ rows,
+                                                                const Segment* __restrict__ segs,
+                                                                const float* __restrict__ Qr, int H, long long slots,
+                                                                __nv_bfloat16* __restrict__ O) {
+  constexpr int DH = 128;
+  constexpr int SPLIT = 4 / G;          // warps per head
+  constexpr int TW = kChunk / SPLIT;    // tokens per warp per chunk (16, 32 or 64)
+  constexpr int NT = TW / 8;            // n8 score tiles per warp
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* sbase = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // [buf][K|V][16 KB]
+  __shared__ uint64_t bar[2];
+  __shared__ int sPos[kTileRows];
+  __shared__ float sMl[4][2][kTileRows];  // per warp: m, l per row
+  const TileDesc td = tiles[blockIdx.x];
+  const int kh = blockIdx.y;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = warp / SPLIT, slice = warp % SPLIT;
+  const RowDesc last = rows[td.row0 + td.nrows - 1];
+  const Segment* sg = segs + last.seg_off;
+  const int nseg = last.nseg;
+  if (tid < kTileRows) sPos[tid] = tid < td.nrows ? rows[td.row0 + tid].pos : -1;
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  int nchunks = 0;
+  for (int s = 0; s < nseg; ++s) nchunks += (sg[s].len + kChunk - 1) / kChunk;
+  // Q fragments (A operand, 16 rows x 128), rows beyond nrows are zero
+  const int gq = lane >> 2, tq = lane & 3;
+  uint32_t qa[8][4];
+  {
+    const int r0 = gq, r1 = gq + 8;
+    const bool v0 = r0 < td.nrows, v1 = r1 < td.nrows;
+    const float* q0 = Qr + ((long long)(td.row0 + (v0 ? r0 : 0)) * H + kh * G + g) * DH;
+    const float* q1 = Qr + ((long long)(td.row0 + (v1 ? r1 : 0)) * H + kh * G + g) * DH;
+    const float sc = 1.4426950408889634f;
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks) {
+      const int k0 = ks * 16 + tq * 2;
+      const float2 x00 = v0 ? *reinterpret_cast<const float2*>(q0 + k0) : make_float2(0.f, 0.f);
+      const float2 x10 = v1 ? *reinterpret_cast<const float2*>(q1 + k0) : make_float2(0.f, 0.f);
+      const float2 x01 = v0 ? *reinterpret_cast<const float2*>(q0 + k0 + 8) : make_float2(0.f, 0.f);
+      const float2 x11 = v1 ? *reinterpret_cast<const float2*>(q1 + k0 + 8) : make_float2(0.f, 0.f);
+      qa[ks][0] = pack_bf16(x00.x * sc, x00.y * sc);
+      qa[ks][1] = pack_bf16(x10.x * sc, x10.y * sc);
+      qa[ks][2] = pack_bf16(x01.x * sc, x01.y * sc);
+      qa[ks][3] = pack_bf16(x11.x * sc, x11.y * sc);
+    }
+  }
+  __syncthreads();
+  int seg_i = 0, seg_o = 0;
+  long long cb[2];
+  int cl[2], cown[2];
+  auto next_chunk = [&](int b) {
+    while (seg_i < nseg && seg_o >= sg[seg_i].len) {
+      ++seg_i;
+      seg_o = 0;
+    }
+    cb[b] = sg[seg_i].base + seg_o;
+    const int l = sg[seg_i].len - seg_o;
+    cl[b] = l < kChunk ? l : kChunk;
+    cown[b] = (seg_i == nseg - 1) ? seg_o : -1;
+    seg_o += cl[b];
+  };
+  auto issue = [&](int b) {
+    unsigned char* kb = sbase + b * 32768;
+    unsigned char* vb = kb + 16384;
+    const int rowc = (int)((long long)kh * slots + cb[b]);
+    mbar_expect_tx(&bar[b], 32768);
+    tma_load_2d(kb, &kmap, 0, rowc, &bar[b]);
+    tma_load_2d(kb + 8192, &kmap, 64, rowc, &bar[b]);
+    tma_load_2d(vb, &vmap, 0, rowc, &bar[b]);
+    tma_load_2d(vb + 8192, &vmap, 64, rowc, &bar[b]);
+  };
+  for (int c = 0; c < 2 && c < nchunks; ++c) {
+    next_chunk(c);
+    if (tid == 0) issue(c);
+  }
+  float oacc[16][4];
+#pragma unroll
+  for (int n = 0; n < 16; ++n) oacc[n][0] = oacc[n][1] = oacc[n][2] = oacc[n][3] = 0.f;
+  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;  // rows gq and gq+8
+  const int pos0 = sPos[gq], pos1 = sPos[gq + 8];
+  for (int c = 0; c < nchunks; ++c) {
+    const int b = c & 1;
+    const int len = cl[b], own0 = cown[b];
+    mbar_wait(&bar[b], (uint32_t)((c >> 1) & 1));
+    const uint32_t kb = (uint32_t)__cvta_generic_to_shared(sbase + b * 32768);
+    const uint32_t vb = kb + 16384;
+    const int t_base = slice * TW;
+    // S = Q K^T for this warp's token slice
+    float sacc[NT][4];
+#pragma unroll
+    for (int n = 0; n < NT; ++n) sacc[n][0] = sacc[n][1] = sacc[n][2] = sacc[n][3] = 0.f;
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks) {
+#pragma unroll
+      for (int n2 = 0; n2 < NT / 2; ++n2) {
+        // two n8 tiles (16 tokens) x k16: matrices {tok 0-7,k0-7},{tok 0-7,k8-15},{tok 8-15,k0-7},{tok 8-15,k8-15}
+        const int mi = lane >> 3, ri = lane & 7;
+        const int tok = t_base + n2 * 16 + (mi >> 1) * 8 + ri;
+        const int chunk16 = ks * 2 + (mi & 1);
+        uint32_t b0, b1, b2, b3;
+        ldsm_x4(kb + swz(tok, chunk16), b0, b1, b2, b3);
+        mma_bf16(sacc[2 * n2], qa[ks][0], qa[ks][1], qa[ks][2], qa[ks][3], b0, b1);
+        mma_bf16(sacc[2 * n2 + 1], qa[ks][0], qa[ks][1], qa[ks][2], qa[ks][3], b2, b3);
+      }
+    }
+    // mask and online softmax (rows gq: c0,c1; gq+8: c2,c3)
+    float mx0 = -INFINITY, mx1 = -INFINITY;
+#pragma unroll
+    for (int n = 0; n < NT; ++n) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int t = t_base + n * 8 + tq * 2 + e;
+        const bool in = t < len;
+        const bool ok0 = in && (own0 < 0 || own0 + t <= pos0);
+        const bool ok1 = in && (own0 < 0 || own0 + t <= pos1);
+        sacc[n][e] = ok0 ? sacc[n][e] : -INFINITY;
+        sacc[n][2 + e] = ok1 ? sacc[n][2 + e] : -INFINITY;
+        mx0 = fmaxf(mx0, sacc[n][e]);
+        mx1 = fmaxf(mx1, sacc[n][2 + e]);
+      }
+    }
+#pragma unroll
+    for (int o = 1; o < 4; o <<= 1) {
+      mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, o));
+      mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, o));
+    }
+    const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
+    const float a0 = mn0 == -INFINITY ? 1.f : exp2f(m0 - mn0);
+    const float a1 = mn1 == -INFINITY ? 1.f : exp2f(m1 - mn1);
+    float ps0 = 0.f, ps1 = 0.f;
+    uint32_t pa[NT / 2][4];
+#pragma unroll
+    for (int n = 0; n < NT; ++n) {
+      const float p00 = mn0 == -INFINITY ? 0.f : exp2f(sacc[n][0] - mn0);
+      const float p01 = mn0 == -INFINITY ? 0.f : exp2f(sacc[n][1] - mn0);
+      const float p10 = mn1 == -INFINITY ? 0.f : exp2f(sacc[n][2] - mn1);
+      const float p11 = mn1 == -INFINITY ? 0.f : exp2f(sacc[n][3] - mn1);
+      ps0 += p00 + p01;
+      ps1 += p10 + p11;
+      // C layout of n8 tile n -> A layout of k16 step n/2 (regs 0,1 for even n, 2,3 for odd n)
+      if ((n & 1) == 0) {
+        pa[n / 2][0] = pack_bf16(p00, p01);
+        pa[n / 2][1] = pack_bf16(p10, p11);
+      } else {
+        pa[n / 2][2] = pack_bf16(p00, p01);
+        pa[n / 2][3] = pack_bf16(p10, p11);
+      }
+    }
+    l0 = l0 * a0 + ps0;
+    l1 = l1 * a1 + ps1;
+    m0 = mn0;
+    m1 = mn1;
+#pragma unroll
+    for (int n = 0; n < 16; ++n) {
+      oacc[n][0] *= a0;
+      oacc[n][1] *= a0;
+      oacc[n][2] *= a1;
+      oacc[n][3] *= a1;
+    }
+    // O += P V : k = this warp's tokens (NT/2 k16 steps), n = 128 dh (16 n8 tiles)
+#pragma unroll
+    for (int kk = 0; kk < NT / 2; ++kk) {
+#pragma unroll
+      for (int n2 = 0; n2 < 8; ++n2) {
+        // V^T fragments via ldmatrix.trans: matrices {tok 0-7, dh 8j..}, {tok 8-15, dh 8j..}, {tok 0-7, dh 8j+8..}, {tok 8-15, dh 8j+8..}
+        const int mi = lane >> 3, ri = lane & 7;
+        const int tok = t_base + kk * 16 + (mi & 1) * 8 + ri;
+        const int chunk16 = n2 * 2 + (mi >> 1);
+        uint32_t b0, b1, b2, b3;
+        ldsm_x4_t(vb + swz(tok, chunk16), b0, b1, b2, b3);
+        mma_bf16(oacc[2 * n2], pa[kk][0], pa[kk][1], pa[kk][2], pa[kk][3], b0, b1);
+        mma_bf16(oacc[2 * n2 + 1], pa[kk][0], pa[kk][1], pa[kk][2], pa[kk][3], b2, b3);
+      }
+    }
+    __syncthreads();
+    if (c + 2 < nchunks) {
+      next_chunk(b);
+      if (tid == 0) issue(b);
+    }
+  }
+  // row sums within the quad
+#pragma unroll
+  for (int o = 1; o < 4; o <<= 1) {
+    l0 += __shfl_xor_sync(0xffffffffu, l0, o);
+    l1 += __shfl_xor_sync(0xffffffffu, l1, o);
+  }
+  // merge the SPLIT warps of head g through shared memory (reuse the K/V buffers)
+  float* sO = reinterpret_cast<float*>(sbase);  // [4 warps][16 rows][128] fp32 = 32 KB
+  if (tq == 0) {
+    sMl[warp][0][gq] = m0;
+    sMl[warp][0][gq + 8] = m1;
+    sMl[warp][1][gq] = l0;
+    sMl[warp][1][gq + 8] = l1;
+  }
+  __syncthreads();
+  float M0 = -INFINITY, M1 = -INFINITY;
+  for (int w = g * SPLIT; w < (g + 1) * SPLIT; ++w) {
+    M0 = fmaxf(M0, sMl[w][0][gq]);
+    M1 = fmaxf(M1, sMl[w][0][gq + 8]);
+  }
+  float L0 = 0.f, L1 = 0.f;
+  for (int w = g * SPLIT; w < (g + 1) * SPLIT; ++w) {
+    const float mw0 = sMl[w][0][gq], mw1 = sMl[w][0][gq + 8];
+    L0 += (mw0 == -INFINITY) ? 0.f : sMl[w][1][gq] * exp2f(mw0 - M0);
+    L1 += (mw1 == -INFINITY) ? 0.f : sMl[w][1][gq + 8] * exp2f(mw1 - M1);
+  }
+  const float f0 = (m0 == -INFINITY) ? 0.f : exp2f(m0 - M0);
+  const float f1 = (m1 == -INFINITY) ? 0.f : exp2f(m1 - M1);
+#pragma unroll
+  for (int n = 0; n < 16; ++n) {
+    const int col = n * 8 + tq * 2;
+    float* r0p = sO + (warp * 16 + gq) * DH + col;
+    float* r1p = sO + (warp * 16 + gq + 8) * DH + col;
+    r0p[0] = oacc[n][0] * f0;
+    r0p[1] = oacc[n][1] * f0;
+    r1p[0] = oacc[n][2] * f1;
+    r1p[1] = oacc[n][3] * f1;
+  }
+  __syncthreads();
+  // warp `slice 0` of each head writes the merged rows
+  if (slice == 0) {
+    for (int i = lane; i < kTileRows * DH; i += 32) {
+      const int row = i / DH, col = i % DH;
+      if (row >= td.nrows) continue;
+      float acc = 0.f;
+      for (int w = g * SPLIT; w < (g + 1) * SPLIT; ++w) acc += sO[(w * 16 + row) * DH + col];
+      float Lr = 0.f, Mr = -INFINITY;
+      for (int w = g * SPLIT; w < (g + 1) * SPLIT; ++w) Mr = fmaxf(Mr, sMl[w][0][row]);
+      for (int w = g * SPLIT; w < (g + 1) * SPLIT; ++w) {
+        const float mw = sMl[w][0][row];
+        Lr += (mw == -INFINITY) ? 0.f : sMl[w][1][row] * exp2f(mw - Mr);
+      }
+      O[((long long)(td.row0 + row) * H + kh * G + g) * DH + col] = __float2bfloat16_rn(acc / Lr);
+    }
+  }
+  (void)L0;
+  (void)L1;
+}
+
 // K1 tile variant for prefill-shaped rows (PRM scoring): kTileRows consecutive
 // rows of one thought share their ancestors and a causal own prefix, so each
 // 64-token K/V chunk is staged once per tile instead of once per row.
@@ -1025,6 +1320,32 @@ static void launch_tile(const TileDesc* tiles, int ntiles, const RowDesc* rows, 
   }
   dim3 grid(ntiles, KVH);
   tree_attn_tile_kernel<DH, G><<<grid, kAttnThreads, smem, s>>>(tiles, rows, segs, Qr, H, Kp, Vp, slots, O);
+}
+
+extern "C" int spex_k_tree_attn_tiles_mma(const CUtensorMap* kmap, const CUtensorMap* vmap, const TileDesc* tiles,
+                                          int ntiles, const RowDesc* rows, const Segment* segs, const float* Qr, int H,
+                                          int KVH, int dh, long long slots, __nv_bfloat16* O, cudaStream_t s) {
+  const int G = H / KVH;
+  if (ntiles <= 0) return 0;
+  if (dh != 128 || (G != 1 && G != 2 && G != 4)) return -1;
+  const size_t smem = 2 * 32768 + 1024;
+  dim3 grid(ntiles, KVH);
+#define SPEX_MMA_CASE(GG)                                                                             \
+  if (G == GG) {                                                                                     \
+    static bool attr = false;                                                                        \
+    if (!attr) {                                                                                     \
+      cudaFuncSetAttribute(tree_attn_tile_mma_kernel<GG>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                           (int)smem);                                                               \
+      attr = true;                                                                                   \
+    }                                                                                                \
+    tree_attn_tile_mma_kernel<GG><<<grid, 128, smem, s>>>(*kmap, *vmap, tiles, rows, segs, Qr, H, slots, O); \
+    return 0;                                                                                        \
+  }
+  SPEX_MMA_CASE(1)
+  SPEX_MMA_CASE(2)
+  SPEX_MMA_CASE(4)
+#undef SPEX_MMA_CASE
+  return -1;
 }
 
 extern "C" int spex_k_tree_attn_tiles(const TileDesc* tiles, int ntiles, const RowDesc* rows, const Segment* segs,

@@ -58,3 +58,29 @@ def test_small_model_matches_numpy_oracle():
         worst["prm"] = max(worst["prm"], abs(rs - score))
         assert abs(rs - score) <= 2e-3, (q, node, rs, score)
     print("worst abs errors", worst)
+
+
+def test_mid_model_tensor_core_paths_match_numpy_oracle():
+    """dh=128 shapes: PRM/prompt rows go through the TMA + mma.sync tile kernel,
+    decode rows through the streaming decode kernel."""
+    import paper_2605_10195_b200 as spex
+    from oracle import model_ref
+    cfg = json.dumps({"family": "rebase_bfs", "policy": {"width": 3, "max_depth": 6, "target_answers": 3},
+                      "workload": {"noise_sigma": 0.05}, "run": {"batch_size": 3, "n_queries": 3, "flags": ["t1"]}})
+    ex = spex.Executor(cfg, 5, None, trace=True)
+    ex.set_model("mid_policy", "mid_prm", weight_seed=3, record_outputs=True)
+    ex.run()
+    log, dec, prm = ex.log_lines(), ex.decode_outputs(), ex.prm_outputs()
+    ex.close()
+    assert dec and prm
+    tree = model_ref.TreeFromLog(log, prompt_tokens=32)
+    rm = model_ref.Model("mid_prm", 3 ^ model_ref.PRM_SEED_XOR, prm=True)
+    rng = random.Random(1)
+    for (q, node, score) in rng.sample(prm, 4):
+        n = tree.nodes[(q, node)][2]
+        rs = rm.prm_score(tree.sequence(q, node, n - 1, rm.V))
+        assert abs(rs - score) <= 2e-3, (q, node, rs, score)
+    pol = model_ref.Model("mid_policy", 3, prm=False)
+    for (q, node, pos, amax, lse, lsum) in rng.sample(dec, 2):
+        _, rl, rs, _ = pol.logits_stats(tree.sequence(q, node, pos, pol.V))
+        assert abs(rl - lse) <= 2e-3 * max(1.0, abs(rl)), (q, node, pos, rl, lse)
