@@ -28,28 +28,34 @@ SPEX_HD bool round_safe(double hi, double lo, double abs_err) {
   return fabs(lo) + abs_err < half_ulp;
 }
 
+// Cody-Waite splits: the leading parts carry 42 significant bits, so k * C_1
+// is exact for |k| < 2^11 and x - k * C_1 is exact (Sterbenz).
+constexpr double kLn2o64cw_1 = 0x1.62e42fefa3800p-7;
+constexpr double kLn2o64cw_2 = 0x1.ef35793c76730p-51;
+constexpr double kLn2cw_1 = 0x1.62e42fefa3800p-1;
+constexpr double kLn2cw_2 = 0x1.ef35793c76730p-45;
+constexpr double kPio128cw_1 = 0x1.921fb54443000p-6;
+constexpr double kPio128cw_2 = -0x1.73dcb3b399d74p-49;
+constexpr double kPio128cw_3 = -0x1.fc8f8cbb5bf6cp-103;
+
 SPEX_HD double exp_fast(double x) {
-  if (!(fabs(x) < 700.0)) return exp_cr(x);
+  if (!(fabs(x) < 16.0)) return exp_cr(x);
   if (x == 0.0) return 1.0;
-  const double kd = nearbyint(x * 0x1.71547652b82fep+6);  // x * 64 / ln2
+  const double kd = nearbyint(x * 0x1.71547652b82fep+6);  // x * 64 / ln2, |kd| < 2^11
   const int k = static_cast<int>(kd);
   const int j = k & 63;
   const int e = (k - j) / 64;
-  dd r = two_sum(x, 0.0);
-  r = dd_add(r, dd_neg(two_prod(kd, kLn2o64_1)));
-  r = dd_add(r, dd_neg(two_prod(kd, kLn2o64_2)));
-  r = dd_add_d(r, -kd * kLn2o64_3);
-  const double rh = r.hi;
-  // expm1(r) = r + r^2/2 + ... ; |r| <= ln2/128
-  double tail = rh * rh *
-                (0.5 + rh * (1.0 / 6.0 + rh * (1.0 / 24.0 + rh * (1.0 / 120.0 + rh * (1.0 / 720.0 + rh / 5040.0)))));
-  tail += rh * r.lo;
-  const dd p = dd_add_d(r, tail);
-  const dd T = {SPEX_TAB(kExp2Tab)[j][0], SPEX_TAB(kExp2Tab)[j][1]};
-  const dd y = dd_add(T, dd_mul(T, p));
-  if (round_safe(y.hi, y.lo, y.hi * 0x1p-65)) {
-    if (e > -1020 && e < 1020) return ldexp(y.hi, e);
-  }
+  const double rh = x - kd * kLn2o64cw_1;  // exact
+  const double rl = -kd * kLn2o64cw_2;
+  const double r = rh + rl;
+  // expm1(r) = rh + rl + t
+  double t = r * r * (0.5 + r * (1.0 / 6.0 + r * (1.0 / 24.0 + r * (1.0 / 120.0 + r * (1.0 / 720.0 + r / 5040.0)))));
+  const double Th = SPEX_TAB(kExp2Tab)[j][0], Tl = SPEX_TAB(kExp2Tab)[j][1];
+  const dd P = two_prod(Th, rh);
+  const dd s = two_sum(Th, P.hi);
+  const double lo = ((P.lo + Th * (rl + t)) + (Tl + Tl * (rh + rl))) + s.lo;
+  const dd y = quick_two_sum(s.hi, lo);
+  if (round_safe(y.hi, y.lo, y.hi * 0x1p-64)) return ldexp(y.hi, e);
   return exp_cr(x);
 }
 
@@ -66,56 +72,60 @@ SPEX_HD double log_fast(double x) {
   j = j < 0 ? 0 : (j > 192 ? 192 : j);
   const double inv = SPEX_TAB(kLogInv)[j];
   const dd pr = two_prod(m, inv);
-  const dd r = two_sum(pr.hi - 1.0, pr.lo);  // exact
+  const dd r = two_sum(pr.hi - 1.0, pr.lo);  // m * inv - 1, exact
   const double rh = r.hi;
-  // log1p(r) = r - r^2/2 + r^3/3 - ... ; |r| <= 2^-8.5
-  double tail = rh * rh *
-                (-0.5 + rh * (1.0 / 3.0 + rh * (-0.25 + rh * (0.2 + rh * (-1.0 / 6.0 + rh * (1.0 / 7.0 - rh * 0.125))))));
-  tail -= rh * r.lo;
-  dd L = dd_add_d(r, tail);
-  const dd C = {SPEX_TAB(kLogC)[j][0], SPEX_TAB(kLogC)[j][1]};
-  dd y = dd_add(C, L);
+  // log1p(r) = rh + rl + tail
+  const double tail = rh * rh * (-0.5 + rh * (1.0 / 3.0 + rh * (-0.25 + rh * (0.2 + rh * (-1.0 / 6.0 +
+                                                                                          rh * (1.0 / 7.0 - rh * 0.125)))))) -
+                      rh * r.lo;
   const double ed = static_cast<double>(e);
-  if (e != 0) {
-    dd el = two_prod(ed, kLn2_1);
-    el = dd_add(el, two_prod(ed, kLn2_2));
-    y = dd_add(el, y);
-  }
-  const double err = (fabs(ed) * 0.7 + fabs(C.hi) + fabs(L.hi) + 1e-300) * 0x1p-64;
+  const double Ch = SPEX_TAB(kLogC)[j][0], Cl = SPEX_TAB(kLogC)[j][1];
+  const dd s1 = two_sum(ed * kLn2cw_1, Ch);  // ed * kLn2cw_1 exact (|e| < 2^11)
+  const dd s2 = two_sum(s1.hi, rh);
+  const double lo = (((r.lo + tail) + (Cl + ed * kLn2cw_2)) + s1.lo) + s2.lo;
+  const dd y = quick_two_sum(s2.hi, lo);
+  const double err = (fabs(ed) + fabs(Ch) + fabs(rh) + 1e-300) * 0x1p-63;
   if (round_safe(y.hi, y.lo, err)) return y.hi;
   return log_cr(x);
 }
 
 SPEX_HD double cos_fast(double x) {
   const double ax = fabs(x);
-  if (!(ax < 1048576.0)) return cos_cr(x);
-  const double kd = nearbyint(ax * 0x1.45f306dc9c883p+5);  // ax / (pi/128)
+  if (!(ax < 48.0)) return cos_cr(x);  // keeps kd < 2^11 (exact k * C_1)
+  const double kd = nearbyint(ax * 0x1.45f306dc9c883p+5);  // ax / (pi/128), < 2^13
   const int k = static_cast<int>(kd);
-  dd r = two_sum(ax, 0.0);
-  r = dd_add(r, dd_neg(two_prod(kd, kPio128_1)));
-  r = dd_add(r, dd_neg(two_prod(kd, kPio128_2)));
-  r = dd_add_d(r, -kd * kPio128_3);
+  const double rh0 = ax - kd * kPio128cw_1;  // exact
+  const dd r = two_sum(rh0, -kd * kPio128cw_2);
+  const double rh = r.hi, rl = r.lo - kd * kPio128cw_3;
   const int q = (k >> 6) & 3;
   const int j = k & 63;
-  const double rh = r.hi;
   const double r2 = rh * rh;
-  // sin r = r + s_tail ; cos r - 1 = c_lead + c_tail
   const double s_tail = rh * r2 * (-1.0 / 6.0 + r2 * (1.0 / 120.0 + r2 * (-1.0 / 5040.0 + r2 / 362880.0)));
-  const dd sinr = dd_add_d(r, s_tail);
-  dd cm1 = two_prod(rh, rh);
-  cm1 = {-0.5 * cm1.hi, -0.5 * cm1.lo};
-  const double c_tail = r2 * r2 * (1.0 / 24.0 + r2 * (-1.0 / 720.0 + r2 / 40320.0)) - rh * r.lo;
-  cm1 = dd_add_d(cm1, c_tail);
-  const dd S = {SPEX_TAB(kSinTab)[j][0], SPEX_TAB(kSinTab)[j][1]};
-  const dd C = {SPEX_TAB(kCosTab)[j][0], SPEX_TAB(kCosTab)[j][1]};
-  // cos(a + r) = C + C*(cos r - 1) - S*sin r ; sin(a + r) = S + S*(cos r - 1) + C*sin r
-  dd y;
-  if ((q & 1) == 0)
-    y = dd_add(dd_add(C, dd_mul(C, cm1)), dd_neg(dd_mul(S, sinr)));
-  else
-    y = dd_add(dd_add(S, dd_mul(S, cm1)), dd_mul(C, sinr));
+  const double c_tail = r2 * r2 * (1.0 / 24.0 + r2 * (-1.0 / 720.0 + r2 / 40320.0));
+  const dd rr = two_prod(rh, rh);
+  double Ah, Al, Bh, Bl;  // value = A*(1 + cos r - 1) +/- B * sin r
+  if ((q & 1) == 0) {
+    Ah = SPEX_TAB(kCosTab)[j][0];
+    Al = SPEX_TAB(kCosTab)[j][1];
+    Bh = -SPEX_TAB(kSinTab)[j][0];
+    Bl = -SPEX_TAB(kSinTab)[j][1];
+  } else {
+    Ah = SPEX_TAB(kSinTab)[j][0];
+    Al = SPEX_TAB(kSinTab)[j][1];
+    Bh = SPEX_TAB(kCosTab)[j][0];
+    Bl = SPEX_TAB(kCosTab)[j][1];
+  }
+  // A + B*rh - A*rh^2/2 + [B*(rl + s_tail) + A*(c_tail - rh*rl) + Al + Bl*rh - Al*rh^2/2]
+  const dd P = two_prod(Bh, rh);
+  const dd Q2 = two_prod(-0.5 * Ah, rr.hi);
+  const dd s1 = two_sum(Ah, P.hi);
+  const dd s2 = two_sum(s1.hi, Q2.hi);
+  const double lo = ((((P.lo + Q2.lo) - 0.5 * Ah * rr.lo) + (Bh * (rl + s_tail) + Ah * (c_tail - rh * rl))) +
+                     ((Al + Bl * rh) - 0.5 * Al * r2)) +
+                    (s1.lo + s2.lo);
+  dd y = quick_two_sum(s2.hi, lo);
   if (q == 1 || q == 2) y = dd_neg(y);
-  if (round_safe(y.hi, y.lo, 0x1p-72)) return y.hi;
+  if (round_safe(y.hi, y.lo, 0x1p-68)) return y.hi;
   return cos_cr(x);
 }
 
