@@ -73,6 +73,9 @@ typedef struct spex_model_stats {
   long long launches;     /* kernels of this library launched by the forward (cuBLAS excluded) */
   long long gemm_calls;   /* cuBLAS GEMM calls */
   double control_ms;      /* control kernel device time (overlapped with the forward when streaming) */
+  double step_ms;         /* device time of the whole search: control start -> last kernel (CUDA events) */
+  int streamed;           /* 1: the forward ran concurrently with the control kernel */
+  int pad_;
 } spex_model_stats;
 
 /* Per decode row-step shadow output (K3): argmax, logsumexp, logit sum. */

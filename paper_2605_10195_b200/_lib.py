@@ -81,6 +81,9 @@ class ModelStats(ctypes.Structure):
         ("launches", ctypes.c_longlong),
         ("gemm_calls", ctypes.c_longlong),
         ("control_ms", ctypes.c_double),
+        ("step_ms", ctypes.c_double),
+        ("streamed", ctypes.c_int),
+        ("pad_", ctypes.c_int),
     ]
 
     def as_dict(self) -> dict:

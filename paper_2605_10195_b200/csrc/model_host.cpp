@@ -296,6 +296,8 @@ void AttnTimer::begin(cudaStream_t st) {
 
 void AttnTimer::end(cudaStream_t st) {
   cudaEventRecord(ev[n].second, st);
+  if ((int)bytes.size() <= n) bytes.resize(n + 1);
+  bytes[n] = cur_bytes;
   ++n;
   if (n == (int)ev.size() && n >= 256) flush();
 }
@@ -305,6 +307,7 @@ void AttnTimer::flush() {
     float ms = 0.f;
     cudaEventSynchronize(ev[i].second);
     cudaEventElapsedTime(&ms, ev[i].first, ev[i].second);
+    if (dump) std::fprintf(dump, "%lld %.0f %.6f\n", launches, bytes[i], ms);
     total_ms += ms;
     launches += 1;
   }
@@ -312,6 +315,7 @@ void AttnTimer::flush() {
 }
 
 AttnTimer::~AttnTimer() {
+  if (dump) std::fclose(dump);
   for (auto& p : ev) {
     cudaEventDestroy(p.first);
     cudaEventDestroy(p.second);
@@ -398,6 +402,8 @@ void run_model_schedule(const ModelRunConfig& mc, const ScheduleView& sv, ModelR
   Model* prm = mc.with_prm ? cached(g_cache.prm, mc.prm, true, mc.seed, slots, std::max(max_prm, prompt_chunk * P), st)
                            : nullptr;
   g_cache.seed = mc.seed;
+  // capacity actually resident (a cached pool may be larger than this run's request)
+  const long long cap_slots = prm ? std::min(pol->slots, prm->slots) : pol->slots;
   const int rows_cap = std::max({max_dec, max_prm, prompt_chunk * P, 1});
   if (g_cache.rows_cap < rows_cap) {
     cudaFree(g_cache.rows);
@@ -424,6 +430,7 @@ void run_model_schedule(const ModelRunConfig& mc, const ScheduleView& sv, ModelR
   TreeView tv_prm = sv.tree;
   tv_prm.V = mc.prm.V;
   AttnTimer timer;
+  if (const char* p = std::getenv("SPEX_ATTN_LOG")) timer.dump = std::fopen(p, "w");
   cudaEvent_t t0, t1;
   cudaEventCreate(&t0);
   cudaEventCreate(&t1);
@@ -451,7 +458,7 @@ void run_model_schedule(const ModelRunConfig& mc, const ScheduleView& sv, ModelR
   long long dbg_n = 0, dbg_s = 0;
 
   auto process = [&](const PubEntry& pe) {
-    if (pe.kv_next > slots) throw std::runtime_error("tree KV pool capacity exceeded");
+    if (pe.kv_next > cap_slots) throw std::runtime_error("tree KV pool capacity exceeded");
     if (pe.kind == SCHED_DECODE) {
       for (int s = 0; s < pe.steps; ++s) {
         for (int c0 = 0; c0 < pe.n; c0 += max_dec) {
@@ -459,6 +466,9 @@ void run_model_schedule(const ModelRunConfig& mc, const ScheduleView& sv, ModelR
           spex_k_build_decode_rows(tv_pol, sv.srow_sid + pe.off + c0, sv.srow_pos0 + pe.off + c0, n, s, rows, segs,
                                    st);
           g_launches += 1;
+          // one K1 launch per layer: the step's unique KV tokens (this chunk's share) + Q/O rows
+          timer.cur_bytes = ((double)pe.u0 + (double)s * pe.n + pe.n) * kv_tok_bytes * ((double)n / pe.n) +
+                            (double)n * mc.policy.H * mc.policy.dh * (4.0 + 2.0);
           forward(*pol, rows, segs, n, hb, st, mc.time_attn ? &timer : nullptr);
           if (dbg && dbg_n + n <= mc.out_rows_cap) {
             spex_k_gather_outputs(rows, n, pol->amax, pol->lse, pol->lsum, dbg + dbg_n, st);

@@ -5,6 +5,7 @@
 
 #include <string>
 #include <utility>
+#include <cstdio>
 #include <vector>
 
 #include "ctl_state.h"
@@ -55,6 +56,8 @@ struct ModelRunResult {
   double control_ms = 0.0;
   long long launches = 0;  // kernels of this library launched by the replay (cuBLAS excluded)
   long long gemm_calls = 0;
+  double step_ms = 0.0;  // control start -> last of (control end, forward end), CUDA events
+  int streamed = 0;      // 1: forward overlapped with the control kernel; 0: replayed after it
 };
 
 struct AttnTimer {
@@ -64,6 +67,9 @@ struct AttnTimer {
   int control_error = 0;
   double control_ms = 0.0;
   long long launches = 0;
+  double cur_bytes = 0.0;       // algorithmic bytes of each launch of the current forward
+  std::vector<double> bytes;    // per pending launch
+  FILE* dump = nullptr;         // SPEX_ATTN_LOG: one line per launch (index, alg bytes, ms)
   void begin(cudaStream_t st);
   void end(cudaStream_t st);
   void flush();

@@ -506,16 +506,46 @@ __global__ void __launch_bounds__(kAttnThreads) tree_attn_kernel(const RowDesc* 
 // K1 decode variant: one warp per (row, kv head) streams the row's context with
 // 128-bit coalesced loads — a half-warp covers one 256-byte K (or V) row, so a
 // warp consumes two tokens per load instruction and keeps UNROLL token pairs in
-// flight. Online softmax in registers (log2 domain); no shared memory and no
-// block barriers, so occupancy is bounded only by registers. Decode rows have
-// no intra-row reuse: staging through shared memory would only add latency.
+// flight. Scores and P.V use the sm_100 mixed-precision FMA (FHFMA.BF16:
+// fp32 += bf16 x bf16, the bf16 product exact) straight on the packed K/V
+// registers — no bf16->fp32 unpacking; q and p enter as bf16 exactly like the
+// operands of the tensor-core tile kernel. One online-softmax update per UNROLL
+// group (warp-uniform running max; the rescale is skipped when it does not
+// move). No shared memory and no block barriers: decode rows have no intra-row
+// reuse, occupancy is bounded only by registers.
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+__device__ __forceinline__ void fma2_bf16(float& acc, uint32_t a2, uint32_t b2) {
+  asm("{.reg .b16 al, ah, bl, bh;\n\t"
+      "mov.b32 {al, ah}, %1;\n\t"
+      "mov.b32 {bl, bh}, %2;\n\t"
+      "fma.rn.f32.bf16 %0, al, bl, %0;\n\t"
+      "fma.rn.f32.bf16 %0, ah, bh, %0;}"
+      : "+f"(acc)
+      : "r"(a2), "r"(b2));
+}
+
+// acc[2e], acc[2e+1] += p * v2.{lo,hi}  (p already bf16 in both halves of p2)
+__device__ __forceinline__ void fma_pv_bf16(float& a0, float& a1, uint32_t p2, uint32_t v2) {
+  asm("{.reg .b16 pl, ph, vl, vh;\n\t"
+      "mov.b32 {pl, ph}, %2;\n\t"
+      "mov.b32 {vl, vh}, %3;\n\t"
+      "fma.rn.f32.bf16 %0, pl, vl, %0;\n\t"
+      "fma.rn.f32.bf16 %1, pl, vh, %1;}"
+      : "+f"(a0), "+f"(a1)
+      : "r"(p2), "r"(v2));
+}
+
 template <int DH, int G>
-__global__ void __launch_bounds__(256) tree_attn_decode_kernel(const RowDesc* __restrict__ rows,
-                                                              const Segment* __restrict__ segs,
-                                                              const float* __restrict__ Qr, int H, int KVH, int M,
-                                                              const __nv_bfloat16* __restrict__ Kp,
-                                                              const __nv_bfloat16* __restrict__ Vp,
-                                                              long long slots, __nv_bfloat16* __restrict__ O) {
+__global__ void __launch_bounds__(256, (G == 1 ? 4 : (G <= 4 ? 2 : 1))) tree_attn_decode_kernel(const RowDesc* __restrict__ rows,
+                                                                 const Segment* __restrict__ segs,
+                                                                 const float* __restrict__ Qr, int H, int KVH, int M,
+                                                                 const __nv_bfloat16* __restrict__ Kp,
+                                                                 const __nv_bfloat16* __restrict__ Vp,
+                                                                 long long slots, __nv_bfloat16* __restrict__ O) {
   constexpr int EPL = 8;              // bf16 elements per lane per token (16 bytes)
   constexpr int LPT = DH / EPL;       // lanes per token (16 for DH=128, 8 for DH=64)
   constexpr int TPW = 32 / LPT;       // tokens per warp load (2 or 4)
@@ -530,15 +560,16 @@ __global__ void __launch_bounds__(256) tree_attn_decode_kernel(const RowDesc* __
   const Segment* sg = segs + rd.seg_off;
   const __nv_bfloat16* Kh = Kp + (long long)kh * slots * DH + li * EPL;
   const __nv_bfloat16* Vh = Vp + (long long)kh * slots * DH + li * EPL;
-  float q[G][EPL];
+  uint32_t q2[G][EPL / 2];  // q * log2(e), bf16 pairs
 #pragma unroll
   for (int g = 0; g < G; ++g) {
     const float4* qp = reinterpret_cast<const float4*>(Qr + ((long long)r * H + kh * G + g) * DH + li * EPL);
     const float4 a = qp[0], b = qp[1];
-    q[g][0] = a.x * 1.4426950408889634f; q[g][1] = a.y * 1.4426950408889634f;
-    q[g][2] = a.z * 1.4426950408889634f; q[g][3] = a.w * 1.4426950408889634f;
-    q[g][4] = b.x * 1.4426950408889634f; q[g][5] = b.y * 1.4426950408889634f;
-    q[g][6] = b.z * 1.4426950408889634f; q[g][7] = b.w * 1.4426950408889634f;
+    constexpr float L2E = 1.4426950408889634f;
+    q2[g][0] = pack_bf16(a.x * L2E, a.y * L2E);
+    q2[g][1] = pack_bf16(a.z * L2E, a.w * L2E);
+    q2[g][2] = pack_bf16(b.x * L2E, b.y * L2E);
+    q2[g][3] = pack_bf16(b.z * L2E, b.w * L2E);
   }
   float m[G], l[G], acc[G][EPL];
 #pragma unroll
@@ -563,36 +594,46 @@ __global__ void __launch_bounds__(256) tree_attn_decode_kernel(const RowDesc* __
         vraw[u] = __ldg(reinterpret_cast<const uint4*>(Vh + off));
       }
 #pragma unroll
-      for (int u = 0; u < UNROLL; ++u) {
-        float kf[EPL], vf[EPL];
-        const __nv_bfloat162* k2 = reinterpret_cast<const __nv_bfloat162*>(&kraw[u]);
-        const __nv_bfloat162* v2 = reinterpret_cast<const __nv_bfloat162*>(&vraw[u]);
+      for (int g = 0; g < G; ++g) {
+        float sc[UNROLL];
 #pragma unroll
-        for (int e = 0; e < EPL / 2; ++e) {
-          kf[2 * e] = __low2float(k2[e]);
-          kf[2 * e + 1] = __high2float(k2[e]);
-          vf[2 * e] = __low2float(v2[e]);
-          vf[2 * e + 1] = __high2float(v2[e]);
+        for (int u = 0; u < UNROLL; ++u) {
+          float a = 0.f;
+          fma2_bf16(a, q2[g][0], kraw[u].x);
+          fma2_bf16(a, q2[g][1], kraw[u].y);
+          fma2_bf16(a, q2[g][2], kraw[u].z);
+          fma2_bf16(a, q2[g][3], kraw[u].w);
+          sc[u] = a;
         }
 #pragma unroll
-        for (int g = 0; g < G; ++g) {
-          float sc = 0.f;
+        for (int o = LPT / 2; o > 0; o >>= 1)
 #pragma unroll
-          for (int e = 0; e < EPL; ++e) sc += q[g][e] * kf[e];
+          for (int u = 0; u < UNROLL; ++u) sc[u] += __shfl_xor_sync(0xffffffffu, sc[u], o);
+        float mx = -INFINITY;
 #pragma unroll
-          for (int o = LPT / 2; o > 0; o >>= 1) sc += __shfl_xor_sync(0xffffffffu, sc, o);
-          if (!ok[u]) sc = -INFINITY;
-          // running max shared by all tokens of the warp step
-          float mx = sc;
+        for (int u = 0; u < UNROLL; ++u) {
+          if (!ok[u]) sc[u] = -INFINITY;
+          mx = fmaxf(mx, sc[u]);
+        }
 #pragma unroll
-          for (int o = LPT; o < 32; o <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-          const float m_new = fmaxf(m[g], mx);
-          const float scale = exp2f(m[g] - m_new);  // m == -inf -> 0
-          const float p = ok[u] ? exp2f(sc - m_new) : 0.f;
-          l[g] = l[g] * scale + p;
+        for (int o = LPT; o < 32; o <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        if (mx > m[g]) {  // warp-uniform
+          const float scale = exp2f(m[g] - mx);  // m == -inf -> 0
+          l[g] *= scale;
 #pragma unroll
-          for (int e = 0; e < EPL; ++e) acc[g][e] = acc[g][e] * scale + p * vf[e];
-          m[g] = m_new;
+          for (int e = 0; e < EPL; ++e) acc[g][e] *= scale;
+          m[g] = mx;
+        }
+#pragma unroll
+        for (int u = 0; u < UNROLL; ++u) {
+          const float p = exp2f(sc[u] - m[g]);  // masked tokens: exp2(-inf) = 0
+          const __nv_bfloat16 pb = __float2bfloat16_rn(p);
+          l[g] += __bfloat162float(pb);
+          const uint32_t p2 = (uint32_t)__bfloat16_as_ushort(pb) * 0x10001u;
+          fma_pv_bf16(acc[g][0], acc[g][1], p2, vraw[u].x);
+          fma_pv_bf16(acc[g][2], acc[g][3], p2, vraw[u].y);
+          fma_pv_bf16(acc[g][4], acc[g][5], p2, vraw[u].z);
+          fma_pv_bf16(acc[g][6], acc[g][7], p2, vraw[u].w);
         }
       }
     }
@@ -653,10 +694,6 @@ __device__ __forceinline__ void mma_bf16(float* c, uint32_t a0, uint32_t a1, uin
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
-__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
-  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
-  return *reinterpret_cast<uint32_t*>(&v);
-}
 
 // byte offset of (row, 16-byte chunk c in [0,16)) in a swizzled [2 halves][64 rows][128 B] chunk buffer
 __device__ __forceinline__ uint32_t swz(int row, int c) {

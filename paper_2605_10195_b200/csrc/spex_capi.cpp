@@ -460,6 +460,7 @@ struct spex_executor {
   cudaStream_t stream = nullptr;
   cudaStream_t mstream = nullptr;
   bool with_model = false;
+  std::vector<std::pair<const char*, double>> host_marks;  // SPEX_TIMING: host phase wall times
   ModelRunConfig mc;
   ModelRunResult mres;
   std::vector<DecodeOut> dec_out;
@@ -850,6 +851,10 @@ void run_executor(spex_executor& ex, int trace) {
     ex.qs.assign(R.qs, R.qs + Q);
     if (trace) ex.log.assign(R.log, R.log + ex.g.log_n);
 #else
+    const auto tm0 = std::chrono::steady_clock::now();
+    auto mark = [&](const char* nm) {
+      ex.host_marks.emplace_back(nm, std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tm0).count());
+    };
     CUDA_OK(cudaSetDevice(ex.device));
     if (!ex.stream) CUDA_OK(cudaStreamCreateWithFlags(&ex.stream, cudaStreamNonBlocking));
     if (!ex.mstream) CUDA_OK(cudaStreamCreateWithFlags(&ex.mstream, cudaStreamNonBlocking));
@@ -873,6 +878,7 @@ void run_executor(spex_executor& ex, int trace) {
       CUDA_OK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&R.pub), h_head, 0));
       CUDA_OK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&R.pub_e), h_ents, 0));
     }
+    mark("arena+pinned");
     Run* d_run = nullptr;
     CUDA_OK(cudaMalloc(&d_run, sizeof(Run)));
     CUDA_OK(cudaMemcpyAsync(d_run, &R, sizeof(Run), cudaMemcpyHostToDevice, ex.stream));
@@ -930,6 +936,7 @@ void run_executor(spex_executor& ex, int trace) {
       sv.pub_head = h_head;
       sv.pub_entries = h_ents;
       alloc_outputs(static_cast<long long>(Q) * node_cap * 64);
+      mark("pre-launch");
       int lr = spex_launch_control_async(d_run, ex.nthreads, ex.stream, ca, cb);
       if (lr != 0) {
         cleanup();
@@ -938,9 +945,10 @@ void run_executor(spex_executor& ex, int trace) {
       try {
         run_model_schedule(mc, sv, &ex.mres, ex.mstream);
         model_done = true;
+        mark("model-stream-done");
       } catch (const std::exception& e) {
         // capacity exceeded while streaming: fall back to a sequential replay below
-        if (std::getenv("SPEX_DEBUG")) std::fprintf(stderr, "streaming replay fallback: %s\n", e.what());
+        std::fprintf(stderr, "spex: streaming forward abandoned (%s); replaying after the control kernel\n", e.what());
         cudaStreamSynchronize(ex.mstream);
         ex.mres = ModelRunResult{};
       }
@@ -952,10 +960,9 @@ void run_executor(spex_executor& ex, int trace) {
       }
     }
     CUDA_OK(cudaEventSynchronize(cb));
+    mark("control-done");
     float ms = 0.f;
     cudaEventElapsedTime(&ms, ca, cb);
-    cudaEventDestroy(ca);
-    cudaEventDestroy(cb);
     ex.device_ms = ms;
     CUDA_OK(cudaMemcpyAsync(&ex.g, R.g, sizeof(GState), cudaMemcpyDeviceToHost, ex.stream));
     CUDA_OK(cudaStreamSynchronize(ex.stream));
@@ -980,7 +987,20 @@ void run_executor(spex_executor& ex, int trace) {
         fail(201, std::string("model forward: ") + e.what());
       }
     }
-    if (ex.with_model) ex.mres.control_ms = ms;
+    if (ex.with_model) {
+      ex.mres.control_ms = ms;
+      ex.mres.streamed = model_done ? 1 : 0;
+      cudaEvent_t me;
+      cudaEventCreate(&me);
+      cudaEventRecord(me, ex.mstream);
+      cudaEventSynchronize(me);
+      float sm = 0.f;
+      cudaEventElapsedTime(&sm, ca, me);
+      ex.mres.step_ms = sm > ms ? sm : ms;
+      cudaEventDestroy(me);
+    }
+    cudaEventDestroy(ca);
+    cudaEventDestroy(cb);
     ex.qs.resize(Q);
     CUDA_OK(cudaMemcpyAsync(ex.qs.data(), R.qs, sizeof(QueryRun) * Q, cudaMemcpyDeviceToHost, ex.stream));
     CUDA_OK(cudaStreamSynchronize(ex.stream));
@@ -1001,6 +1021,10 @@ void run_executor(spex_executor& ex, int trace) {
     cudaFree(d_rows);
     cudaFree(d_scores);
     cleanup();
+    mark("cleanup");
+    if (std::getenv("SPEX_TIMING")) {
+      for (auto& m : ex.host_marks) std::fprintf(stderr, "[spex timing] %-20s %10.2f ms\n", m.first, m.second);
+    }
 #endif
     if (ex.g.error == ERR_CAP_NODES || ex.g.error == ERR_CAP_STAGE) {
       node_cap *= 2;  // capacity, not semantics: rerun with a larger arena
@@ -1152,6 +1176,8 @@ int spex_executor_model_stats(spex_executor* ex, spex_model_stats* out) {
     out->launches = r.launches;
     out->control_ms = r.control_ms;
     out->gemm_calls = r.gemm_calls;
+    out->step_ms = r.step_ms;
+    out->streamed = r.streamed;
 #else
     (void)ex;
 #endif

@@ -1,0 +1,105 @@
+"""K1 tree decode attention vs a plain PyTorch fp32 reference of the same op.
+
+The kernel (`spex_k_tree_attn`, model_kernels.cu) is called directly through
+the product library on random paged tree KV pools: each row attends over a
+list of KV segments (its ancestors' thoughts root-first, then its own prefix),
+segments shared between rows as siblings share ancestors. The reference
+gathers each row's K/V in fp32 and computes softmax(q.K^T).V.
+
+Tolerance (stated): the kernel takes q and p in bf16 (like the tensor-core tile
+kernel's mma operands) and writes O in bf16, so |O - O_ref| <= 1.5e-2 elementwise
+and mean |O - O_ref| <= 2e-3 for O of unit scale.
+"""
+import ctypes
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROW = np.dtype([("q", "<i4"), ("node", "<u4"), ("pos", "<i4"), ("abs_pos", "<i4"), ("slot", "<i8"),
+                ("seg_off", "<i4"), ("nseg", "<i4"), ("token", "<i4"), ("pad", "<i4")])
+SEG = np.dtype([("base", "<i8"), ("len", "<i4"), ("pad", "<i4")])
+MAX_SEG = 40
+
+
+def _lib():
+    import paper_2605_10195_b200 as spex
+    from paper_2605_10195_b200 import _lib as L
+    if not spex.device_ok():
+        pytest.fail("no sm_100 device: the B200 path has no fallback")
+    lib = L.lib()
+    f = lib.spex_k_tree_attn
+    f.restype = ctypes.c_int
+    f.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                  ctypes.c_void_p, ctypes.c_void_p, ctypes.c_longlong, ctypes.c_void_p, ctypes.c_int,
+                  ctypes.c_void_p]
+    return f
+
+
+def _make_tree_rows(rng, M, slots, max_depth):
+    """Random tree: nodes own contiguous slot ranges; each row is a path
+    root->...->node with the last segment a partial own prefix."""
+    n_nodes = max(8, M // 2)
+    lens = rng.integers(8, 200, size=n_nodes)
+    bases = np.concatenate([[0], np.cumsum(lens)[:-1]])
+    assert bases[-1] + lens[-1] <= slots
+    parent = np.full(n_nodes, -1)
+    for i in range(1, n_nodes):
+        parent[i] = rng.integers(0, i) if rng.random() < 0.9 else -1
+    rows = np.zeros(M, ROW)
+    segs = np.zeros(M * MAX_SEG, SEG)
+    paths = []
+    for r in range(M):
+        node = int(rng.integers(0, n_nodes))
+        chain = []
+        c = parent[node]
+        while c >= 0 and len(chain) < max_depth:
+            chain.append(c)
+            c = parent[c]
+        chain = chain[::-1]
+        own = int(rng.integers(1, lens[node] + 1))
+        sl = [(int(bases[a]), int(lens[a])) for a in chain] + [(int(bases[node]), own)]
+        for k, (b, n) in enumerate(sl):
+            segs[r * MAX_SEG + k] = (b, n, 0)
+        rows[r] = (0, node, own - 1, 0, bases[node] + own - 1, r * MAX_SEG, len(sl), 0, 0)
+        paths.append(sl)
+    return rows, segs, paths
+
+
+@pytest.mark.parametrize("H,KVH,dh,M", [(8, 8, 128, 300), (32, 8, 128, 97), (4, 2, 64, 150), (16, 4, 64, 64)])
+def test_k1_decode_matches_torch_fp32(H, KVH, dh, M):
+    import torch
+    f = _lib()
+    rng = np.random.default_rng(H * 1000 + dh + M)
+    slots = 200 * max(8, M // 2) + 64
+    rows, segs, paths = _make_tree_rows(rng, M, slots, max_depth=12)
+    dev = torch.device("cuda", 0)
+    g = torch.Generator(device="cpu").manual_seed(M)
+    K = torch.randn(KVH, slots, dh, generator=g).to(torch.bfloat16).to(dev)
+    V = torch.randn(KVH, slots, dh, generator=g).to(torch.bfloat16).to(dev)
+    Q = (torch.randn(M, H, dh, generator=g) * 2.0 / dh ** 0.5).to(dev)  # pre-scaled like rope_kv_kernel
+    O = torch.zeros(M, H, dh, dtype=torch.bfloat16, device=dev)
+    rows_d = torch.from_numpy(rows.view(np.uint8).copy()).to(dev)
+    segs_d = torch.from_numpy(segs.view(np.uint8).copy()).to(dev)
+    st = torch.cuda.current_stream(dev)
+    rc = f(rows_d.data_ptr(), segs_d.data_ptr(), Q.data_ptr(), H, KVH, dh, K.data_ptr(), V.data_ptr(), slots,
+           O.data_ptr(), M, st.cuda_stream)
+    assert rc == 0
+    torch.cuda.synchronize()
+    Kf, Vf = K.float(), V.float()
+    G = H // KVH
+    worst, tot, cnt = 0.0, 0.0, 0
+    for r in range(M):
+        idx = torch.cat([torch.arange(b, b + n) for b, n in paths[r]]).to(dev)
+        for h in range(H):
+            kh = h // G
+            s = Kf[kh, idx] @ Q[r, h]
+            p = torch.softmax(s, dim=0)
+            ref = p @ Vf[kh, idx]
+            d = (O[r, h].float() - ref).abs()
+            worst = max(worst, d.max().item())
+            tot += d.sum().item()
+            cnt += d.numel()
+    assert worst <= 1.5e-2, worst
+    assert tot / cnt <= 2e-3, tot / cnt
