@@ -12,7 +12,7 @@ import os
 from pathlib import Path
 
 PKG_DIR = Path(__file__).resolve().parent
-LIB_PATH = PKG_DIR / "lib" / "libspex_b200.so"
+LIB_PATH = Path(os.environ.get("SPEX_LIB_PATH", PKG_DIR / "lib" / "libspex_b200.so"))
 
 MAX_TRACKED = 8
 

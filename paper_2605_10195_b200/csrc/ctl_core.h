@@ -28,7 +28,7 @@ struct Item {
   int fin;     // the item's query finished
 };
 
-SPEX_HD void set_err(Run* R, int code, int q, u32 node) {
+SPEX_HDNI void set_err(Run* R, int code, int q, u32 node) {
   GState* g = R->g;
 #if SPEX_DEVICE_PASS
   if (atomicCAS(&g->error, 0, code) == 0) {
@@ -89,7 +89,7 @@ SPEX_HD void set_fl(const QC& x, u32 id, u16 f) { x.R->n_flags[NI(x, id)] |= f; 
 SPEX_HD void clr_fl(const QC& x, u32 id, u16 f) { x.R->n_flags[NI(x, id)] &= static_cast<u16>(~f); }
 SPEX_HD void touch(const QC& x) { x.qr->version += 1; }
 
-SPEX_HD Rec* new_rec(const QC& x, u8 kind, u32 node) {
+SPEX_HDNI Rec* new_rec(const QC& x, u8 kind, u32 node) {
   if (!x.c->trace) return nullptr;
   Item* it = x.it;
   if (it->nrec >= it->rec_cap) {
@@ -142,7 +142,7 @@ SPEX_HD bool counted_live(const QC& x, u32 id) {
 }
 
 // tree.cpp:75-94
-SPEX_HD u32 add_node(const QC& x, u32 parent, int token_len, bool spec) {
+SPEX_HDNI u32 add_node(const QC& x, u32 parent, int token_len, bool spec) {
   Run* R = x.R;
   QueryRun* qr = x.qr;
   if (parent >= static_cast<u32>(qr->nnodes)) {
@@ -193,7 +193,7 @@ SPEX_HD u32 add_node(const QC& x, u32 parent, int token_len, bool spec) {
 }
 
 // tree.cpp:102-117
-SPEX_HD void promote(const QC& x, u32 id) {
+SPEX_HDNI void promote(const QC& x, u32 id) {
   u8 s = st_of(x, id);
   if (s != kSpeculative && s != kSpeculativeDone) {
     set_err(x.R, ERR_NOT_SPECULATIVE, x.q, id);
@@ -210,7 +210,7 @@ SPEX_HD void promote(const QC& x, u32 id) {
 }
 
 // tree.cpp:119-141 (iterative DFS; the frontier_ filter is unused by the executor)
-SPEX_HD int prune_subtree(const QC& x, u32 id) {
+SPEX_HDNI int prune_subtree(const QC& x, u32 id) {
   u32* stack = x.stack;
   Run* R = x.R;
   int pruned = 0;
@@ -241,13 +241,13 @@ SPEX_HD int prune_subtree(const QC& x, u32 id) {
 
 // ------------------------------------------------------- content oracle (sim.cpp)
 // sim.cpp:112-115
-SPEX_HD int oracle_token_len(const Cfg& c, u64 child_hash) {
+SPEX_HDNI int oracle_token_len(const Cfg& c, u64 child_hash) {
   return lognormal_tokens(child_hash, kSaltTokens, c.token_mu, c.token_sigma, c.token_min,
                           c.token_max);
 }
 
 // sim.cpp:117-137
-SPEX_HD bool oracle_is_terminal(const QC& x, u32 id) {
+SPEX_HDNI bool oracle_is_terminal(const QC& x, u32 id) {
   Run* R = x.R;
   const Cfg& c = *x.c;
   int depth = R->n_depth[NI(x, id)];
@@ -265,7 +265,7 @@ SPEX_HD bool oracle_is_terminal(const QC& x, u32 id) {
 }
 
 // sim.cpp:139-152
-SPEX_HD double oracle_reward(const QC& x, u32 id) {
+SPEX_HDNI double oracle_reward(const QC& x, u32 id) {
   Run* R = x.R;
   const Cfg& c = *x.c;
   bool golden = true;
@@ -288,7 +288,7 @@ SPEX_HD int golden_label_of(const Cfg& c, u64 query_seed) {
                           static_cast<u64>(c.answer_alphabet));
 }
 
-SPEX_HD int oracle_answer_label(const QC& x, u32 id) {
+SPEX_HDNI int oracle_answer_label(const QC& x, u32 id) {
   Run* R = x.R;
   const Cfg& c = *x.c;
   double p = c.correct_base - c.correct_slope * R->n_depth[NI(x, id)];
@@ -314,7 +314,7 @@ SPEX_HD double ucb_score(const Run* R, double value, int cv, int pv, double c) {
 }
 
 // policy.cpp:32-51
-SPEX_HD u32 ucb_select(const QC& x, u32 id) {
+SPEX_HDNI u32 ucb_select(const QC& x, u32 id) {
   Run* R = x.R;
   u32 pi = NI(x, id);
   bool any = false;
@@ -347,7 +347,7 @@ SPEX_HD u32 ucb_select(const QC& x, u32 id) {
 }
 
 // policy.cpp:53-63
-SPEX_HD void backpropagate(const QC& x, u32 leaf, double reward) {
+SPEX_HDNI void backpropagate(const QC& x, u32 leaf, double reward) {
   Run* R = x.R;
   u8 s = st_of(x, leaf);
   if (s != kCommitted && s != kTerminalAnswer) {
@@ -363,7 +363,7 @@ SPEX_HD void backpropagate(const QC& x, u32 leaf, double reward) {
 }
 
 // policy.cpp:65-118. `w` and `quota` are scratch of length n.
-SPEX_HD bool rebase_widths(Run* R, int q, const double* rewards, int n, int budget,
+SPEX_HDNI bool rebase_widths(Run* R, int q, const double* rewards, int n, int budget,
                            double temperature, bool sum_preserving, int* widths, double* w,
                            double* quota, int* order) {
   if (n <= 0) {
@@ -433,7 +433,7 @@ SPEX_HD void update_hit_rate(QueryRun* qr, bool hit, double alpha) {
 
 // --------------------------------------------------------- speculation.cpp
 // speculation.cpp:253-263 (histograms are kept clamped, executor.cpp:29,311-313)
-SPEX_HD void record_outcome(const QC& x, u32 node, bool hit, int distance) {
+SPEX_HDNI void record_outcome(const QC& x, u32 node, bool hit, int distance) {
   u16 f = fl_of(x, node);
   bool known = (f & (NF_LEDGER_ACTIVE | NF_LEDGER_COMPLETED | NF_HAS_PRED)) != 0;
   if (!known || (f & NF_LEDGER_RESOLVED)) {
@@ -462,43 +462,44 @@ SPEX_HD void tally_record(const QC& x, int label, double weight) {
     set_err(x.R, ERR_NEGATIVE_WEIGHT, x.q, kNoNode);
     return;
   }
-  if (qr->tally_count[label] == 0) qr->n_labels += 1;
-  qr->tally_count[label] += 1;
-  qr->tally_w[label] += weight;
+  QueryTally* ta = &x.R->q_tally[x.q];
+  if (ta->count[label] == 0) qr->n_labels += 1;
+  ta->count[label] += 1;
+  ta->w[label] += weight;
   qr->n_answers += 1;
 }
 
 // termination.cpp:15-23 — labels iterate in std::map (lexicographic string) order
 SPEX_HD int leading_label(const QC& x) {
-  const QueryRun* qr = x.qr;
+  const QueryTally* ta = &x.R->q_tally[x.q];
   int best = -1;
   for (int r = 0; r < x.c->answer_alphabet; ++r) {
     int l = x.c->lex_order[r];
-    if (qr->tally_count[l] == 0) continue;
-    if (best < 0 || qr->tally_w[l] > qr->tally_w[best]) best = l;
+    if (ta->count[l] == 0) continue;
+    if (best < 0 || ta->w[l] > ta->w[best]) best = l;
   }
   return best;
 }
 
 // termination.cpp:30-48
-SPEX_HD bool should_terminate(const QC& x, int min_answers, double alpha) {
+SPEX_HDNI bool should_terminate(const QC& x, int min_answers, double alpha) {
   const QueryRun* qr = x.qr;
   if (qr->n_answers < min_answers || qr->n_labels == 0) return false;
   if (qr->n_labels < 2) return true;
+  const QueryTally* ta = &x.R->q_tally[x.q];
   int first = -1, second = -1;
   for (int r = 0; r < x.c->answer_alphabet; ++r) {
     int l = x.c->lex_order[r];
-    if (qr->tally_count[l] == 0) continue;
-    if (first < 0 || qr->tally_w[l] > qr->tally_w[first]) {
+    if (ta->count[l] == 0) continue;
+    if (first < 0 || ta->w[l] > ta->w[first]) {
       second = first;
       first = l;
-    } else if (second < 0 || qr->tally_w[l] > qr->tally_w[second]) {
+    } else if (second < 0 || ta->w[l] > ta->w[second]) {
       second = l;
     }
   }
-  double margin = qr->tally_w[first] - qr->tally_w[second];
-  double avg_second =
-      qr->tally_count[second] > 0 ? qr->tally_w[second] / qr->tally_count[second] : 0.0;
+  double margin = ta->w[first] - ta->w[second];
+  double avg_second = ta->count[second] > 0 ? ta->w[second] / ta->count[second] : 0.0;
   return margin > alpha * avg_second;
 }
 
@@ -514,7 +515,7 @@ SPEX_HD int stream_done_tokens(const QC& x, int sref) {
 }
 
 // executor.cpp:124-164
-SPEX_HD u32 spawn_child(const QC& x, u32 parent, bool spec, int dist) {
+SPEX_HDNI u32 spawn_child(const QC& x, u32 parent, bool spec, int dist) {
   Run* R = x.R;
   u32 pi = NI(x, parent);
   int slot = R->n_nchildren[pi];
@@ -553,7 +554,7 @@ SPEX_HD u32 spawn_child(const QC& x, u32 parent, bool spec, int dist) {
 }
 
 // executor.cpp:168-187
-SPEX_HD void do_promote(const QC& x, u32 node) {
+SPEX_HDNI void do_promote(const QC& x, u32 node) {
   Run* R = x.R;
   u32 ni = NI(x, node);
   if (!has_fl(x, node, NF_HAS_PRED)) {
@@ -585,7 +586,7 @@ SPEX_HD void do_promote(const QC& x, u32 node) {
 }
 
 // executor.cpp:192-200 with DecodeEngine::cancel (sim.cpp:217-233)
-SPEX_HD void cancel_stream(const QC& x, u32 node) {
+SPEX_HDNI void cancel_stream(const QC& x, u32 node) {
   Run* R = x.R;
   u32 ni = NI(x, node);
   int sref = R->n_stream[ni];

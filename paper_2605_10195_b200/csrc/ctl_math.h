@@ -123,7 +123,7 @@ constexpr double kPio2_3 = -0x1.f1976b7ed8fbcp-110;
 constexpr double kPio2_4 = 0x1.4cf98e804177dp-164;
 
 // exp(x) as double-double, |x| < 708.
-SPEX_HD dd dd_exp(double x, int* k_out) {
+SPEX_HDNI dd dd_exp(double x, int* k_out) {
   double kd = nearbyint(x * 0x1.71547652b82fep+0);  // x / ln2
   int k = static_cast<int>(kd);
   // r = x - k*ln2 in double-double; k*part products are exact via two_prod.
@@ -154,7 +154,7 @@ SPEX_HD dd dd_exp(double x, int* k_out) {
   return dd_add_d(e, 1.0);
 }
 
-SPEX_HD double exp_cr(double x) {
+SPEX_HDNI double exp_cr(double x) {
   if (x != x) return x;
   if (x > 709.782712893384) return HUGE_VAL;
   if (x < -745.1332191019412) return 0.0;
@@ -169,7 +169,7 @@ SPEX_HD double exp_cr(double x) {
 
 // log(x) for finite x > 0, correctly rounded: y0 ~ log(x), then
 // y = y0 + log1p(x*exp(-y0) - 1) with the correction evaluated in double-double.
-SPEX_HD double log_cr(double x) {
+SPEX_HDNI double log_cr(double x) {
   if (!(x > 0.0)) return x == 0.0 ? -HUGE_VAL : (x - x) / (x - x);
   if (x == 1.0) return 0.0;
   double y0 = log(x);
@@ -187,7 +187,7 @@ SPEX_HD double log_cr(double x) {
 }
 
 // sin/cos of a double-double |r| <= pi/4 by Taylor series to ~2^-120.
-SPEX_HD dd dd_sin_small(dd r) {
+SPEX_HDNI dd dd_sin_small(dd r) {
   dd r2 = dd_sqr(r);
   dd acc = {1.0, 0.0};
   for (int n = 31; n >= 3; n -= 2) {
@@ -217,7 +217,7 @@ SPEX_HD dd dd_cos_small(dd r) {
 }
 
 // cos(x) for |x| < 2^20, correctly rounded.
-SPEX_HD double cos_cr(double x) {
+SPEX_HDNI double cos_cr(double x) {
   if (x != x) return x;
   double ax = fabs(x);
   if (ax > 1048576.0) return cos(x);  // outside our domain (x = 2*pi*u in [0, 2*pi))

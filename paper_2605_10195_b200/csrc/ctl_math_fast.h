@@ -38,7 +38,7 @@ constexpr double kPio128cw_1 = 0x1.921fb54443000p-6;
 constexpr double kPio128cw_2 = -0x1.73dcb3b399d74p-49;
 constexpr double kPio128cw_3 = -0x1.fc8f8cbb5bf6cp-103;
 
-SPEX_HD double exp_fast(double x) {
+SPEX_HDNI double exp_fast(double x) {
   if (!(fabs(x) < 16.0)) return exp_cr(x);
   if (x == 0.0) return 1.0;
   const double kd = nearbyint(x * 0x1.71547652b82fep+6);  // x * 64 / ln2, |kd| < 2^11
@@ -59,7 +59,7 @@ SPEX_HD double exp_fast(double x) {
   return exp_cr(x);
 }
 
-SPEX_HD double log_fast(double x) {
+SPEX_HDNI double log_fast(double x) {
   if (!(x > 0.0) || !(x < HUGE_VAL) || x < 0x1p-1020) return log_cr(x);
   if (x == 1.0) return 0.0;
   int e = ilogb(x);
@@ -89,7 +89,7 @@ SPEX_HD double log_fast(double x) {
   return log_cr(x);
 }
 
-SPEX_HD double cos_fast(double x) {
+SPEX_HDNI double cos_fast(double x) {
   const double ax = fabs(x);
   if (!(ax < 48.0)) return cos_cr(x);  // keeps kd < 2^11 (exact k * C_1)
   const double kd = nearbyint(ax * 0x1.45f306dc9c883p+5);  // ax / (pi/128), < 2^13

@@ -51,7 +51,7 @@ struct HostExec {
 
 // ------------------------------------------------------------ block primitives
 template <class EX>
-SPEX_HD void ex_scan(EX& ex, int* a, int n, int* total) {
+SPEX_HDNI void ex_scan(EX& ex, int* a, int n, int* total) {
 #if SPEX_DEVICE_PASS
   const int per = (n + ex.nthr - 1) / ex.nthr;
   const int lo = ex.tid * per;
@@ -101,7 +101,7 @@ SPEX_HD void ex_scan(EX& ex, int* a, int n, int* total) {
 }
 
 template <class EX>
-SPEX_HD int ex_min_int(EX& ex, int v) {
+SPEX_HDNI int ex_min_int(EX& ex, int v) {
 #if SPEX_DEVICE_PASS
   for (int off = 16; off > 0; off >>= 1) {
     int y = __shfl_xor_sync(0xffffffffu, v, off);
@@ -119,7 +119,7 @@ SPEX_HD int ex_min_int(EX& ex, int v) {
 }
 
 template <class EX>
-SPEX_HD i64 ex_sum_i64(EX& ex, i64 v) {
+SPEX_HDNI i64 ex_sum_i64(EX& ex, i64 v) {
 #if SPEX_DEVICE_PASS
   for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
   if (ex.lane == 0) ex.sml[ex.warp] = v;
@@ -134,7 +134,7 @@ SPEX_HD i64 ex_sum_i64(EX& ex, i64 v) {
 }
 
 template <class EX>
-SPEX_HD double ex_minmax_d(EX& ex, double v, bool want_max) {
+SPEX_HDNI double ex_minmax_d(EX& ex, double v, bool want_max) {
 #if SPEX_DEVICE_PASS
   for (int off = 16; off > 0; off >>= 1) {
     double y = __shfl_xor_sync(0xffffffffu, v, off);
@@ -224,7 +224,7 @@ SPEX_HD void kv_ancestors_adjust(Run* R, int sid, int delta) {
 // Publish schedule entry e to the host (all block writes before it become
 // visible first: per-thread gpu fence, barrier, then the leader's system fence).
 template <class EX>
-SPEX_HD void publish_entry(Run* R, EX& ex, int e, int rows, int tiles) {
+SPEX_HDNI void publish_entry(Run* R, EX& ex, int e, int rows, int tiles) {
 #if SPEX_DEVICE_PASS
   if (!R->pub_e) return;
   if (R->pub) __threadfence();
@@ -258,7 +258,7 @@ SPEX_HD void publish_entry(Run* R, EX& ex, int e, int rows, int tiles) {
 // Record one decode epoch of the model schedule: `steps` forward steps over
 // the active streams (in active order) starting at their current positions.
 template <class EX>
-SPEX_HD void record_decode(Run* R, EX& ex, int steps) {
+SPEX_HDNI void record_decode(Run* R, EX& ex, int steps) {
   GState* g = R->g;
   const int nreg = g->n_active_region;
   for (int i = ex.tid; i < nreg; i += ex.nthr)
@@ -295,7 +295,7 @@ SPEX_HD void record_decode(Run* R, EX& ex, int steps) {
 // DecodeEngine::advance (sim.cpp:305-384). On return g->engine_now holds the
 // reached boundary and fins[0..nfins) the streams finishing there, in order.
 template <class EX>
-SPEX_HD void engine_advance(Run* R, EX& ex, double limit) {
+SPEX_HDNI void engine_advance(Run* R, EX& ex, double limit) {
   GState* g = R->g;
   const Cfg& c = R->cfg;
   // per-call scalars in GState scratch: s_limit = now, s_flag = mode
@@ -493,7 +493,7 @@ SPEX_HD void engine_advance(Run* R, EX& ex, double limit) {
 
 // --------------------------------------------------------------- admission
 // executor.cpp:765-783 plus generate_workload seeds (sim.cpp:177-180)
-SPEX_HD void admit_query(Run* R, int q, Rec* rec_slot) {
+SPEX_HDNI void admit_query(Run* R, int q, Rec* rec_slot) {
   const Cfg& c = R->cfg;
   QueryRun* qr = &R->qs[q];
   const u64 base = splitmix64(c.run_seed ^ kSaltQuery);
@@ -552,7 +552,7 @@ SPEX_HD void admit_query(Run* R, int q, Rec* rec_slot) {
 enum ItemKind { IK_FIN = 0, IK_REWARD = 1, IK_FOLLOWUP = 2, IK_SPEC = 3 };
 
 template <class EX>
-SPEX_HD void process_items(Run* R, EX& ex, int n_items, int kind, int rank_filter,
+SPEX_HDNI void process_items(Run* R, EX& ex, int n_items, int kind, int rank_filter,
                            int* warp_off) {
   GState* g = R->g;
   const Cfg& c = R->cfg;
@@ -619,13 +619,13 @@ SPEX_HD void process_items(Run* R, EX& ex, int n_items, int kind, int rank_filte
 }
 
 template <class EX>
-SPEX_HD void reset_warp_offsets(Run* R, EX& ex, int* warp_off) {
+SPEX_HDNI void reset_warp_offsets(Run* R, EX& ex, int* warp_off) {
   for (int i = ex.tid; i < ex.nwarp * 3; i += ex.nthr) warp_off[i] = 0;
   ex.sync();
 }
 
 // drain_remaining (executor.cpp:340-360), run by one thread
-SPEX_HD void drain_remaining(Run* R) {
+SPEX_HDNI void drain_remaining(Run* R) {
   GState* g = R->g;
   for (int j = 0; j < g->n_live; ++j) {
     int sid = R->live[j];
@@ -666,7 +666,7 @@ SPEX_HD void drain_remaining(Run* R) {
 
 // Place the staged output of items [0, n) in item order.
 template <class EX>
-SPEX_HD void commit_items(Run* R, EX& ex, int n) {
+SPEX_HDNI void commit_items(Run* R, EX& ex, int n) {
   GState* g = R->g;
   const Cfg& c = R->cfg;
   const int Q = c.n_queries;
@@ -787,7 +787,7 @@ SPEX_HD int collect_queries(Run* R, EX& ex, Pred pred) {
 
 // scheduling_round (executor.cpp:705-740) with allocate_budgets (budget.cpp:45-96)
 template <class EX>
-SPEX_HD void scheduling_round(Run* R, EX& ex, int* warp_off) {
+SPEX_HDNI void scheduling_round(Run* R, EX& ex, int* warp_off) {
   GState* g = R->g;
   const Cfg& c = R->cfg;
   if (!c.t1) return;
@@ -894,7 +894,7 @@ SPEX_HD void scheduling_round(Run* R, EX& ex, int* warp_off) {
 
 // consumer_step_followups (executor.cpp:746-763)
 template <class EX>
-SPEX_HD void followups(Run* R, EX& ex, int* warp_off) {
+SPEX_HDNI void followups(Run* R, EX& ex, int* warp_off) {
   for (int pass = 0; pass < 4; ++pass) {
     auto need = [&](int q) {
       const QueryRun* qr = &R->qs[q];
@@ -913,7 +913,7 @@ SPEX_HD void followups(Run* R, EX& ex, int* warp_off) {
 
 // Completion phase: on_stream_done for fins in order (executor.cpp:794).
 template <class EX>
-SPEX_HD void completions(Run* R, EX& ex, int* warp_off) {
+SPEX_HDNI void completions(Run* R, EX& ex, int* warp_off) {
   GState* g = R->g;
   const int nf = g->nfins;
   // rank of each completion among those of the same query
@@ -1008,7 +1008,11 @@ SPEX_HD void run_loop(Run* R, EX& ex, int* warp_off) {
         continue;
       }
     }
-    if (g->fifo_head >= g->fifo_tail) {
+    // every thread reads the FIFO state before thread 0 pops it (a block-uniform
+    // branch: without this barrier a slow thread could see the popped head)
+    const bool fifo_empty = g->fifo_head >= g->fifo_tail;
+    ex.sync();
+    if (fifo_empty) {
       if (ex.tid == 0) set_err(R, ERR_STALLED, -1, kNoNode);
       ex.sync();
       break;

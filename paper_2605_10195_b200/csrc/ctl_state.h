@@ -213,8 +213,14 @@ struct QueryRun {
   int need_followup;
   int grant;
   int hits[kMaxTracked + 1], misses[kMaxTracked + 1];
-  int tally_count[kMaxLabels];
-  double tally_w[kMaxLabels];
+};
+
+// AnswerTally::by_label_ (termination.hpp:15-43), by label index; kept apart
+// from QueryRun so the hot per-query records stay small (shared-memory resident
+// in the control kernel).
+struct QueryTally {
+  int count[kMaxLabels];
+  double w[kMaxLabels];
 };
 
 // Global scalars of one run (the executor's Impl scalars + engine scalars).
@@ -284,6 +290,7 @@ struct Run {
   i64* n_kvbase;  // first KV slot of the node's thought in the tree KV pools
   // per-query
   QueryRun* qs;
+  QueryTally* q_tally;
   u32* q_rest_stack;
   u32* q_layer;
   u32* q_cohort;

@@ -10,6 +10,7 @@
 //   K4 value_head_kernel   PRM score sigmoid(w . h_last)
 //   plus weight init, row descriptors, embedding, RMSNorm->bf16, RoPE + KV
 //   append, SwiGLU.
+#include <algorithm>
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -44,6 +45,11 @@ __global__ void init_weights_kernel(__nv_bfloat16* w, long long n, uint64_t seed
 __device__ __forceinline__ int token_id(uint64_t node_hash, int pos, int V) {
   uint64_t h = d_splitmix64(node_hash ^ ((uint64_t)(pos + 1) * 0x9e3779b97f4a7c15ULL) ^ kSaltTok);
   return (int)(h % (uint64_t)V);
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
 }
 
 constexpr int kMaxSegFwd = 40;
@@ -226,31 +232,42 @@ __global__ void gather_outputs_kernel(const RowDesc* rows, int M, const int* ama
 }
 
 __global__ void embed_kernel(const RowDesc* rows, int M, const __nv_bfloat16* E, int d, float* X) {
-  const int r = blockIdx.x;
+  // one warp per row, 8 bf16 per lane per step (d % 8 == 0)
+  const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (r >= M) return;
-  const __nv_bfloat16* e = E + (long long)rows[r].token * d;
-  for (int i = threadIdx.x; i < d; i += blockDim.x) X[(long long)r * d + i] = __bfloat162float(e[i]);
+  const uint4* e = reinterpret_cast<const uint4*>(E + (long long)rows[r].token * d);
+  float4* x = reinterpret_cast<float4*>(X + (long long)r * d);
+  for (int i = lane; i < d / 8; i += 32) {
+    const uint4 v = e[i];
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+    x[2 * i] = make_float4(__low2float(h[0]), __high2float(h[0]), __low2float(h[1]), __high2float(h[1]));
+    x[2 * i + 1] = make_float4(__low2float(h[2]), __high2float(h[2]), __low2float(h[3]), __high2float(h[3]));
+  }
 }
 
 // y = bf16(x * rsqrt(mean(x^2) + eps))  (unit gains)
 __global__ void rmsnorm_bf16_kernel(const float* X, int M, int d, float eps, __nv_bfloat16* Y) {
-  const int r = blockIdx.x;
+  // one warp per row, float4 loads (d % 4 == 0); the second pass re-reads the
+  // row from L1
+  const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (r >= M) return;
-  const float* x = X + (long long)r * d;
+  const float4* x = reinterpret_cast<const float4*>(X + (long long)r * d);
   float ss = 0.f;
-  for (int i = threadIdx.x; i < d; i += blockDim.x) ss += x[i] * x[i];
-  __shared__ float red[32];
-  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (threadIdx.x == 0) red[0] = v;
+  for (int i = lane; i < d / 4; i += 32) {
+    const float4 v = x[i];
+    ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
   }
-  __syncthreads();
-  const float inv = rsqrtf(red[0] / (float)d + eps);
-  for (int i = threadIdx.x; i < d; i += blockDim.x) Y[(long long)r * d + i] = __float2bfloat16_rn(x[i] * inv);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  const float inv = rsqrtf(ss / (float)d + eps);
+  uint2* y = reinterpret_cast<uint2*>(Y + (long long)r * d);
+  for (int i = lane; i < d / 4; i += 32) {
+    const float4 v = x[i];
+    uint2 o;
+    o.x = pack_bf16(v.x * inv, v.y * inv);
+    o.y = pack_bf16(v.z * inv, v.w * inv);
+    y[i] = o;
+  }
 }
 
 // RoPE on q and k at the row's absolute position; append k, v (bf16) to the
@@ -259,6 +276,8 @@ __global__ void rmsnorm_bf16_kernel(const float* X, int M, int d, float eps, __n
 __global__ void rope_kv_kernel(const RowDesc* rows, int M, const float* QKV, int H, int KVH, int dh,
                                const float* inv_freq, long long slots, __nv_bfloat16* Kp, __nv_bfloat16* Vp,
                                float* Qr) {
+  // one block per row; rotate-half RoPE on (x[i], x[i+half]) pairs two at a time
+  // (float2), V copied 4 at a time
   const int r = blockIdx.x;
   if (r >= M) return;
   __shared__ float sc[128], ss[128];
@@ -268,35 +287,42 @@ __global__ void rope_kv_kernel(const RowDesc* rows, int M, const float* QKV, int
   const int half = dh / 2;
   const float qscale = rsqrtf((float)dh);
   for (int i = threadIdx.x; i < half; i += blockDim.x) {
-    float s, c;
-    sincosf((float)rd.abs_pos * inv_freq[i], &s, &c);
-    sc[i] = c;
-    ss[i] = s;
+    float sn, cs;
+    sincosf((float)rd.abs_pos * inv_freq[i], &sn, &cs);
+    sc[i] = cs;
+    ss[i] = sn;
   }
   __syncthreads();
-  for (int idx = threadIdx.x; idx < (H + KVH) * half; idx += blockDim.x) {
-    const int head = idx / half;
-    const int i = idx - head * half;
-    const float c = sc[i], s = ss[i];
+  const int hp = half / 2;  // float2 pairs per half
+  for (int idx = threadIdx.x; idx < (H + KVH) * hp; idx += blockDim.x) {
+    const int head = idx / hp;
+    const int i = (idx - head * hp) * 2;
     const float* x = src + head * dh;
-    const float a = x[i], b = x[i + half];
-    const float ya = a * c - b * s;
-    const float yb = a * s + b * c;
+    const float2 a = *reinterpret_cast<const float2*>(x + i);
+    const float2 b = *reinterpret_cast<const float2*>(x + i + half);
+    const float c0 = sc[i], c1 = sc[i + 1], s0 = ss[i], s1 = ss[i + 1];
+    const float ya0 = a.x * c0 - b.x * s0, ya1 = a.y * c1 - b.y * s1;
+    const float yb0 = a.x * s0 + b.x * c0, yb1 = a.y * s1 + b.y * c1;
     if (head < H) {
       float* qd = Qr + ((long long)r * H + head) * dh;
-      qd[i] = ya * qscale;
-      qd[i + half] = yb * qscale;
+      *reinterpret_cast<float2*>(qd + i) = make_float2(ya0 * qscale, ya1 * qscale);
+      *reinterpret_cast<float2*>(qd + i + half) = make_float2(yb0 * qscale, yb1 * qscale);
     } else {
       const int kh = head - H;
       __nv_bfloat16* kd = Kp + ((long long)kh * slots + rd.slot) * dh;
-      kd[i] = __float2bfloat16_rn(ya);
-      kd[i + half] = __float2bfloat16_rn(yb);
+      *reinterpret_cast<uint32_t*>(kd + i) = pack_bf16(ya0, ya1);
+      *reinterpret_cast<uint32_t*>(kd + i + half) = pack_bf16(yb0, yb1);
     }
   }
-  for (int idx = threadIdx.x; idx < KVH * dh; idx += blockDim.x) {
-    const int kh = idx / dh;
-    const int i = idx - kh * dh;
-    Vp[((long long)kh * slots + rd.slot) * dh + i] = __float2bfloat16_rn(src[(H + KVH) * dh + kh * dh + i]);
+  const float* vs = src + (H + KVH) * dh;
+  for (int idx = threadIdx.x; idx < KVH * dh / 4; idx += blockDim.x) {
+    const int e = idx * 4;
+    const int kh = e / dh, i = e - kh * dh;
+    const float4 v = *reinterpret_cast<const float4*>(vs + e);
+    uint2 o;
+    o.x = pack_bf16(v.x, v.y);
+    o.y = pack_bf16(v.z, v.w);
+    *reinterpret_cast<uint2*>(Vp + ((long long)kh * slots + rd.slot) * dh + i) = o;
   }
 }
 
@@ -513,9 +539,13 @@ __global__ void __launch_bounds__(kAttnThreads) tree_attn_kernel(const RowDesc* 
 // group (warp-uniform running max; the rescale is skipped when it does not
 // move). No shared memory and no block barriers: decode rows have no intra-row
 // reuse, occupancy is bounded only by registers.
-__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
-  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
-  return *reinterpret_cast<uint32_t*>(&v);
+
+__device__ __forceinline__ uint4 ld_stream(const __nv_bfloat16* p, uint64_t pol) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p), "l"(pol));
+  return v;
 }
 
 __device__ __forceinline__ void fma2_bf16(float& acc, uint32_t a2, uint32_t b2) {
@@ -560,6 +590,8 @@ __global__ void __launch_bounds__(256, (G == 1 ? 4 : (G <= 4 ? 2 : 1))) tree_att
   const Segment* sg = segs + rd.seg_off;
   const __nv_bfloat16* Kh = Kp + (long long)kh * slots * DH + li * EPL;
   const __nv_bfloat16* Vh = Vp + (long long)kh * slots * DH + li * EPL;
+  uint64_t pol;  // KV is streamed once per step: evict first, keep L2 for reused state
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
   uint32_t q2[G][EPL / 2];  // q * log2(e), bf16 pairs
 #pragma unroll
   for (int g = 0; g < G; ++g) {
@@ -590,8 +622,8 @@ __global__ void __launch_bounds__(256, (G == 1 ? 4 : (G <= 4 ? 2 : 1))) tree_att
         const int t = t0 + u * TPW + sub;
         ok[u] = t < len;
         const long long off = (base + (ok[u] ? t : 0)) * DH;
-        kraw[u] = __ldg(reinterpret_cast<const uint4*>(Kh + off));
-        vraw[u] = __ldg(reinterpret_cast<const uint4*>(Vh + off));
+        kraw[u] = ld_stream(Kh + off, pol);
+        vraw[u] = ld_stream(Vh + off, pol);
       }
 #pragma unroll
       for (int g = 0; g < G; ++g) {
@@ -1125,16 +1157,19 @@ __global__ void __launch_bounds__(kAttnThreads) tree_attn_tile_kernel(const Tile
 }
 
 __global__ void swiglu_kernel(const float* GU, int M, int F, __nv_bfloat16* A) {
-  const int r = blockIdx.y;
-  const float* g = GU + (long long)r * 2 * F;
-  const float* u = g + F;
-  __nv_bfloat16* a = A + (long long)r * F;
-  for (int j = (blockIdx.x * blockDim.x + threadIdx.x) * 2; j < F; j += gridDim.x * blockDim.x * 2) {
-    const float2 gv = *reinterpret_cast<const float2*>(g + j);
-    const float2 uv = *reinterpret_cast<const float2*>(u + j);
-    const float o0 = gv.x / (1.f + __expf(-gv.x)) * uv.x;
-    const float o1 = gv.y / (1.f + __expf(-gv.y)) * uv.y;
-    *reinterpret_cast<__nv_bfloat162*>(a + j) = __floats2bfloat162_rn(o0, o1);
+  // flat grid-stride over M * F/4 quads (F % 4 == 0)
+  const int F4 = F / 4;
+  const long long n = (long long)M * F4;
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x) {
+    const long long r = k / F4;
+    const int j = (int)(k - r * F4) * 4;
+    const float* g = GU + r * 2 * F;
+    const float4 gv = *reinterpret_cast<const float4*>(g + j);
+    const float4 uv = *reinterpret_cast<const float4*>(g + F + j);
+    uint2 o;
+    o.x = pack_bf16(gv.x / (1.f + __expf(-gv.x)) * uv.x, gv.y / (1.f + __expf(-gv.y)) * uv.y);
+    o.y = pack_bf16(gv.z / (1.f + __expf(-gv.z)) * uv.z, gv.w / (1.f + __expf(-gv.w)) * uv.w);
+    *reinterpret_cast<uint2*>(A + r * F + j) = o;
   }
 }
 
@@ -1142,70 +1177,62 @@ __global__ void swiglu_kernel(const float* GU, int M, int F, __nv_bfloat16* A) {
 // (online max / rescaled exp-sum per thread, then a block combine).
 __global__ void __launch_bounds__(256) lm_epilogue_kernel(const float* logits, int M, int V, int* amax,
                                                           float* lse, float* lsum) {
+  // two branch-free passes over the row (V % 4 == 0): max / first argmax / sum,
+  // then sum exp(x - max) (the row is still in L2)
   const int r = blockIdx.x;
   if (r >= M) return;
-  const float* x = logits + (long long)r * V;
-  float mx = -INFINITY, se = 0.f, sm = 0.f;
+  const float4* x = reinterpret_cast<const float4*>(logits + (long long)r * V);
+  const int V4 = V / 4;
+  float mx = -INFINITY, sm = 0.f;
   int mi = 0x7fffffff;
-  const int V4 = (V % 4 == 0) ? V / 4 : 0;
   for (int i = threadIdx.x; i < V4; i += blockDim.x) {
-    const float4 v4 = reinterpret_cast<const float4*>(x)[i];
-    const float vs[4] = {v4.x, v4.y, v4.z, v4.w};
+    const float4 v = x[i];
+    sm += (v.x + v.y) + (v.z + v.w);
+    const float m01 = fmaxf(v.x, v.y), m23 = fmaxf(v.z, v.w), m4 = fmaxf(m01, m23);
+    if (m4 > mx) {  // first index of the max inside the quad
+      mx = m4;
+      mi = 4 * i + (v.x == m4 ? 0 : v.y == m4 ? 1 : v.z == m4 ? 2 : 3);
+    }
+  }
+  __shared__ float smx[8], ssm[8], sse[8];
+  __shared__ int smi[8];
+  const int w = threadIdx.x >> 5, nw = blockDim.x >> 5, lane = threadIdx.x & 31;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const float v = vs[k];
-      sm += v;
-      if (v > mx) {
-        se = se * __expf(mx - v) + 1.f;
-        mx = v;
-        mi = 4 * i + k;
-      } else {
-        se += __expf(v - mx);
-      }
-    }
-  }
-  for (int i = 4 * V4 + threadIdx.x; i < V; i += blockDim.x) {
-    const float v = x[i];
-    sm += v;
-    if (v > mx) {
-      se = se * __expf(mx - v) + 1.f;
-      mx = v;
-      mi = i;
-    } else {
-      se += __expf(v - mx);
-    }
-  }
-  // warp combine
   for (int o = 16; o > 0; o >>= 1) {
     const float om = __shfl_xor_sync(0xffffffffu, mx, o);
-    const float os = __shfl_xor_sync(0xffffffffu, se, o);
     const int oi = __shfl_xor_sync(0xffffffffu, mi, o);
     sm += __shfl_xor_sync(0xffffffffu, sm, o);
-    const float nm = fmaxf(mx, om);
-    se = (mx == -INFINITY ? 0.f : se * __expf(mx - nm)) + (om == -INFINITY ? 0.f : os * __expf(om - nm));
     if (om > mx || (om == mx && oi < mi)) mi = oi;
-    mx = nm;
+    mx = fmaxf(mx, om);
   }
-  __shared__ float smx[8], sse[8], ssm[8];
-  __shared__ int smi[8];
-  const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  if ((threadIdx.x & 31) == 0) {
+  if (lane == 0) {
     smx[w] = mx;
-    sse[w] = se;
-    ssm[w] = sm;
     smi[w] = mi;
+    ssm[w] = sm;
   }
   __syncthreads();
+  float M0 = smx[0];
+  int I0 = smi[0];
+  float T0 = ssm[0];
+  for (int k = 1; k < nw; ++k) {
+    if (smx[k] > M0 || (smx[k] == M0 && smi[k] < I0)) I0 = smi[k];
+    M0 = fmaxf(M0, smx[k]);
+    T0 += ssm[k];
+  }
+  float se = 0.f;
+  const float ml2 = M0 * 1.4426950408889634f;
+  for (int i = threadIdx.x; i < V4; i += blockDim.x) {
+    const float4 v = x[i];
+    se += exp2f(fmaf(v.x, 1.4426950408889634f, -ml2)) + exp2f(fmaf(v.y, 1.4426950408889634f, -ml2)) +
+          exp2f(fmaf(v.z, 1.4426950408889634f, -ml2)) + exp2f(fmaf(v.w, 1.4426950408889634f, -ml2));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
+  if (lane == 0) sse[w] = se;
+  __syncthreads();
   if (threadIdx.x == 0) {
-    float M0 = smx[0], S0 = sse[0], T0 = ssm[0];
-    int I0 = smi[0];
-    for (int k = 1; k < nw; ++k) {
-      const float nm = fmaxf(M0, smx[k]);
-      S0 = S0 * __expf(M0 - nm) + sse[k] * __expf(smx[k] - nm);
-      if (smx[k] > M0 || (smx[k] == M0 && smi[k] < I0)) I0 = smi[k];
-      M0 = nm;
-      T0 += ssm[k];
-    }
+    float S0 = 0.f;
+    for (int k = 0; k < nw; ++k) S0 += sse[k];
     amax[r] = I0;
     lse[r] = M0 + logf(S0);
     lsum[r] = T0;
@@ -1281,11 +1308,11 @@ extern "C" void spex_k_gather_outputs(const RowDesc* rows, int M, const int* ama
 }
 
 extern "C" void spex_k_embed(const RowDesc* rows, int M, const __nv_bfloat16* E, int d, float* X, cudaStream_t s) {
-  embed_kernel<<<M, 128, 0, s>>>(rows, M, E, d, X);
+  embed_kernel<<<(M + 7) / 8, 256, 0, s>>>(rows, M, E, d, X);
 }
 
 extern "C" void spex_k_rmsnorm(const float* X, int M, int d, float eps, __nv_bfloat16* Y, cudaStream_t s) {
-  rmsnorm_bf16_kernel<<<M, 256, 0, s>>>(X, M, d, eps, Y);
+  rmsnorm_bf16_kernel<<<(M + 7) / 8, 256, 0, s>>>(X, M, d, eps, Y);
 }
 
 extern "C" void spex_k_rope_kv(const RowDesc* rows, int M, const float* QKV, int H, int KVH, int dh,
@@ -1406,8 +1433,9 @@ extern "C" int spex_k_tree_attn_tiles(const TileDesc* tiles, int ntiles, const R
 }
 
 extern "C" void spex_k_swiglu(const float* GU, int M, int F, __nv_bfloat16* A, cudaStream_t s) {
-  dim3 grid((F / 2 + 255) / 256, M);
-  swiglu_kernel<<<grid, 256, 0, s>>>(GU, M, F, A);
+  const long long quads = (long long)M * (F / 4);
+  const int blocks = (int)std::min<long long>((quads + 255) / 256, 148 * 16);
+  swiglu_kernel<<<blocks, 256, 0, s>>>(GU, M, F, A);
 }
 
 extern "C" void spex_k_lm_epilogue(const float* logits, int M, int V, int* amax, float* lse, float* lsum,

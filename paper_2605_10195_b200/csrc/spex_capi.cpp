@@ -421,6 +421,8 @@ std::vector<double>& log_table() {
 struct Arena {
   std::vector<std::pair<void**, size_t>> parts;
   size_t total = 0;
+  size_t hot = 0;  // bytes of the leading control-state region (L2 access-policy window)
+  void mark_hot() { hot = total; }
   template <class T>
   void add(T*& p, size_t count) {
     parts.push_back({reinterpret_cast<void**>(&p), count * sizeof(T)});
@@ -469,8 +471,8 @@ struct spex_executor {
 };
 
 #ifndef SPEX_EMU
-extern "C" int spex_launch_control(Run* d_run, int nthreads, cudaStream_t stream, float* ms);
-extern "C" int spex_launch_control_async(Run* d_run, int nthreads, cudaStream_t stream, cudaEvent_t a,
+extern "C" int spex_launch_control(Run* d_run, int n_queries, int nthreads, cudaStream_t stream, float* ms);
+extern "C" int spex_launch_control_async(Run* d_run, int n_queries, int nthreads, cudaStream_t stream, cudaEvent_t a,
                                          cudaEvent_t b);
 extern "C" void spex_model_cache_clear();
 #define CUDA_OK(x)                                                                  \
@@ -578,6 +580,7 @@ void layout(Arena& A, Run& R, int Q, int node_cap, int stream_cap, int log_cap, 
   A.add(R.n_refc, NN);
   A.add(R.n_kvbase, NN);
   A.add(R.qs, Q);
+  A.add(R.q_tally, Q);
   A.add(R.q_rest_stack, NN);
   A.add(R.q_layer, NN);
   A.add(R.q_cohort, NN);
@@ -597,7 +600,6 @@ void layout(Arena& A, Run& R, int Q, int node_cap, int stream_cap, int log_cap, 
   A.add(R.ev_time, S);
   A.add(R.ev_q, S);
   A.add(R.ev_node, S);
-  A.add(R.log, static_cast<size_t>(log_cap));
   const size_t W = static_cast<size_t>(nwarps) * stage_cap;
   A.add(R.stage_rec, W);
   A.add(R.stage_spawn, W);
@@ -634,6 +636,8 @@ void layout(Arena& A, Run& R, int Q, int node_cap, int stream_cap, int log_cap, 
   A.add(R.al_out, Q + 64);
   A.add(R.al_rank, Q + 64);
   A.add(R.al_order, Q + 64);
+  A.mark_hot();  // everything above is touched every consumer iteration; below: log and model schedule
+  A.add(R.log, static_cast<size_t>(log_cap));
   A.add(R.sched_kind, static_cast<size_t>(R.cfg.sched_cap));
   A.add(R.sched_steps, static_cast<size_t>(R.cfg.sched_cap));
   A.add(R.sched_off, static_cast<size_t>(R.cfg.sched_cap));
@@ -862,6 +866,30 @@ void run_executor(spex_executor& ex, int trace) {
     CUDA_OK(cudaMalloc(&base, A.total + 256));
     CUDA_OK(cudaMemsetAsync(base, 0, A.total + 256, ex.stream));
     A.carve(base);
+    // Keep the control state L2-resident while the forward streams tens of GB
+    // of tree KV through HBM: the control CTA is latency-bound and its misses
+    // otherwise queue behind the K1 traffic (window = the hot region only).
+    if (!std::getenv("SPEX_NO_L2PERSIST")) {
+      int max_win = 0, max_persist = 0;
+      cudaDeviceGetAttribute(&max_win, cudaDevAttrMaxAccessPolicyWindowSize, ex.device);
+      cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, ex.device);
+      if (max_win > 0 && max_persist > 0) {
+        const size_t win = std::min<size_t>(A.hot, static_cast<size_t>(max_win));
+        const size_t per = std::min<size_t>(win, static_cast<size_t>(max_persist));
+        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, per);
+        cudaStreamAttrValue av{};
+        av.accessPolicyWindow.base_ptr = base;
+        av.accessPolicyWindow.num_bytes = win;
+        av.accessPolicyWindow.hitRatio = static_cast<float>(static_cast<double>(per) / static_cast<double>(win));
+        av.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        av.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        cudaStreamSetAttribute(ex.stream, cudaStreamAttributeAccessPolicyWindow, &av);
+        cudaGetLastError();
+      }
+      if (std::getenv("SPEX_TIMING"))
+        std::fprintf(stderr, "[spex timing] arena %zu bytes, hot %zu, L2 window max %d, persist max %d\n", A.total,
+                     A.hot, max_win, max_persist);
+    }
     double* d_tab = nullptr;
     CUDA_OK(cudaMalloc(&d_tab, tab.size() * sizeof(double)));
     CUDA_OK(cudaMemcpyAsync(d_tab, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice,
@@ -937,7 +965,7 @@ void run_executor(spex_executor& ex, int trace) {
       sv.pub_entries = h_ents;
       alloc_outputs(static_cast<long long>(Q) * node_cap * 64);
       mark("pre-launch");
-      int lr = spex_launch_control_async(d_run, ex.nthreads, ex.stream, ca, cb);
+      int lr = spex_launch_control_async(d_run, Q, ex.nthreads, ex.stream, ca, cb);
       if (lr != 0) {
         cleanup();
         fail(200, std::string("control kernel launch failed: ") + cudaGetErrorString(static_cast<cudaError_t>(lr)));
@@ -953,7 +981,7 @@ void run_executor(spex_executor& ex, int trace) {
         ex.mres = ModelRunResult{};
       }
     } else {
-      int lr = spex_launch_control_async(d_run, ex.nthreads, ex.stream, ca, cb);
+      int lr = spex_launch_control_async(d_run, Q, ex.nthreads, ex.stream, ca, cb);
       if (lr != 0) {
         cleanup();
         fail(200, std::string("control kernel launch failed: ") + cudaGetErrorString(static_cast<cudaError_t>(lr)));
