@@ -287,10 +287,11 @@ def main():
     if rank != 0:
         return
     achieved = agg["attn_bytes"] / (agg["attn_ms"] / 1000.0) / 1e9 if agg["attn_ms"] > 0 else 0.0
-    traffic = None
-    if PROFILE_TRAFFIC.exists():
+    traffic, traffic_alg = None, None
+    if PROFILE_TRAFFIC.exists():  # committed ncu --set full capture of K1 (profiles/k1_traffic.json)
         try:
-            traffic = json.loads(PROFILE_TRAFFIC.read_text()).get("dram_bytes_per_launch")
+            tj = json.loads(PROFILE_TRAFFIC.read_text())
+            traffic, traffic_alg = tj.get("dram_bytes_per_launch"), tj.get("alg_bytes_per_launch")
         except Exception:
             traffic = None
     clocks = clk.summary()
@@ -321,6 +322,8 @@ def main():
         "roofline": {"bound": "hbm", "kernel": "K1 tree_attn_kernel (policy decode)",
                      "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                      "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
+                     "traffic_alg_bytes_same_launches": traffic_alg,
+                     "alg_bytes_per_launch": agg["attn_bytes"] / max(1, agg["attn_launches"]),
                      "peak_source": peak_src,
                      "k1_share_of_step": (agg["attn_ms"] / 1000.0) / dev_s if dev_s > 0 else None},
         "cpu_baseline": cpu,

@@ -85,6 +85,24 @@ struct PrmOut {
   int pad;
 };
 
+// Decode work list of one forward step (shared by its L K1 launches): every
+// row's concatenated context is cut into at most kMaxRowChunks chunks of at
+// least kMinChunk tokens; one warp per (chunk, kv head) pulled from a device
+// work queue, partial softmax states merged by the last warp of the row.
+constexpr int kMaxRowChunks = 8;
+constexpr int kMinChunk = 128;
+constexpr int kQueueSlots = 256;  // per-launch work-queue counters (one per layer)
+struct DecodeChunks {
+  int2* items;      // (row, chunk) in row order
+  int* row_nch;     // chunks of row r
+  int* row_ch;      // chunk length (tokens) of row r
+  int* row_item0;   // first item of row r
+  int* n_items;     // device scalar
+  int* qctr;        // [kQueueSlots] work-queue heads, zeroed by the builder
+  float* part;      // partial (acc, m, l) per (item, kv head): G * DH + round4(2G) floats
+  int* cnt;         // [rows_cap * KVH] arrival counters (self-resetting)
+};
+
 // Schedule produced by the control kernel: decode epochs and reward batches.
 enum : int { SCHED_DECODE = 1, SCHED_PRM = 2 };
 

@@ -56,6 +56,10 @@ void spex_k_rope_kv(const RowDesc* rows, int M, const float* QKV, int H, int KVH
 int spex_k_tree_attn(const RowDesc* rows, const Segment* segs, const float* Qr, int H, int KVH, int dh,
                      const __nv_bfloat16* Kp, const __nv_bfloat16* Vp, long long slots, __nv_bfloat16* O, int M,
                      cudaStream_t s);
+void spex_k_build_decode_chunks(const RowDesc* rows, const Segment* segs, int M, DecodeChunks w, cudaStream_t s);
+int spex_k_tree_attn_chunked(const RowDesc* rows, const Segment* segs, const float* Qr, int H, int KVH, int dh,
+                             const __nv_bfloat16* Kp, const __nv_bfloat16* Vp, long long slots, __nv_bfloat16* O,
+                             DecodeChunks w, int qslot, cudaStream_t s);
 void spex_k_swiglu(const float* GU, int M, int F, __nv_bfloat16* A, cudaStream_t s);
 void spex_k_lm_epilogue(const float* logits, int M, int V, int* amax, float* lse, float* lsum, cudaStream_t s);
 void spex_k_value_head(const __nv_bfloat16* Hn, int d, const int* last_row, int n, const __nv_bfloat16* w,
@@ -251,7 +255,8 @@ static Model* make_model(const ModelShape& sh, bool prm, uint64_t seed, long lon
 static long long g_launches = 0, g_gemms = 0;
 
 static void forward(Model& m, const RowDesc* rows, const Segment* segs, int M, cublasHandle_t hb,
-                    cudaStream_t st, AttnTimer* timer, const TileDesc* tiles = nullptr, int ntiles = 0) {
+                    cudaStream_t st, AttnTimer* timer, const TileDesc* tiles = nullptr, int ntiles = 0,
+                    const DecodeChunks* chunks = nullptr) {
   const ModelShape& s = m.sh;
   g_launches += 2 + 5LL * s.L + (m.is_prm ? 0 : 1);
   g_gemms += 4LL * s.L + (m.is_prm ? 0 : 1);
@@ -265,6 +270,9 @@ static void forward(Model& m, const RowDesc* rows, const Segment* segs, int M, c
     if (tiles && !m.kmap.empty())
       rc = spex_k_tree_attn_tiles_mma(&m.kmap[l], &m.vmap[l], tiles, ntiles, rows, segs, m.Qr, s.H, s.KVH, s.dh,
                                       m.slots, m.O, st);
+    if (rc != 0 && chunks)
+      rc = spex_k_tree_attn_chunked(rows, segs, m.Qr, s.H, s.KVH, s.dh, m.Kp[l], m.Vp[l], m.slots, m.O, *chunks, l,
+                                    st);
     if (rc != 0)
       rc = tiles ? spex_k_tree_attn_tiles(tiles, ntiles, rows, segs, m.Qr, s.H, s.KVH, s.dh, m.Kp[l],
                                                   m.Vp[l], m.slots, m.O, st)
@@ -349,8 +357,40 @@ struct ModelCache {
   int* last_row = nullptr;
   TileDesc* tiles = nullptr;
   float* scores = nullptr;
+  // decode work list (K1 chunked), sized for rows_cap rows of the policy shape
+  DecodeChunks dc{};
+  int dc_rows = 0;
+  long long dc_part = 0;
 };
 static ModelCache g_cache;
+
+static void ensure_decode_chunks(int rows_cap, const ModelShape& sh) {
+  // per item: KVH * (G * dh + round4(2G)) <= H * (dh + 4) floats
+  const long long part = (long long)rows_cap * kMaxRowChunks * sh.H * (sh.dh + 4);
+  if (g_cache.dc_rows >= rows_cap && g_cache.dc_part >= part && g_cache.dc.cnt) return;
+  DecodeChunks& w = g_cache.dc;
+  cudaFree(w.items);
+  cudaFree(w.row_nch);
+  cudaFree(w.row_ch);
+  cudaFree(w.row_item0);
+  cudaFree(w.n_items);
+  cudaFree(w.qctr);
+  cudaFree(w.part);
+  cudaFree(w.cnt);
+  std::vector<void*> keep;
+  w.items = dalloc<int2>((size_t)rows_cap * kMaxRowChunks, keep);
+  w.row_nch = dalloc<int>(rows_cap, keep);
+  w.row_ch = dalloc<int>(rows_cap, keep);
+  w.row_item0 = dalloc<int>(rows_cap, keep);
+  w.n_items = dalloc<int>(1, keep);
+  w.qctr = dalloc<int>(kQueueSlots, keep);
+  w.part = dalloc<float>((size_t)part, keep);
+  const size_t ncnt = (size_t)rows_cap * std::max(sh.KVH, 1) * 8;  // any KVH up to 8x the policy's
+  w.cnt = dalloc<int>(ncnt, keep);
+  CK(cudaMemset(w.cnt, 0, ncnt * sizeof(int)));
+  g_cache.dc_rows = rows_cap;
+  g_cache.dc_part = part;
+}
 
 static bool same_shape(const ModelShape& a, const ModelShape& b) {
   return a.d == b.d && a.L == b.L && a.H == b.H && a.KVH == b.KVH && a.dh == b.dh && a.F == b.F && a.V == b.V &&
@@ -422,6 +462,11 @@ void run_model_schedule(const ModelRunConfig& mc, const ScheduleView& sv, ModelR
   RowDesc* rows = g_cache.rows;
   Segment* segs = g_cache.segs;
   int* last_row = g_cache.last_row;
+  // Chunked K1 (bounded per-warp work, merged partials) is opt-in: on the
+  // benchmark's context lengths (~250 tokens/row) the one-warp-per-(row, head)
+  // kernel is faster (measured 78% vs 72% of HBM peak, profiles/r01e_*).
+  const bool chunked = std::getenv("SPEX_K1_CHUNKED") != nullptr;
+  if (chunked) ensure_decode_chunks(std::max(max_dec, 1), mc.policy);
   TileDesc* tiles = g_cache.tiles;
   float* scores = g_cache.scores;
 
@@ -469,7 +514,9 @@ void run_model_schedule(const ModelRunConfig& mc, const ScheduleView& sv, ModelR
           // one K1 launch per layer: the step's unique KV tokens (this chunk's share) + Q/O rows
           timer.cur_bytes = ((double)pe.u0 + (double)s * pe.n + pe.n) * kv_tok_bytes * ((double)n / pe.n) +
                             (double)n * mc.policy.H * mc.policy.dh * (4.0 + 2.0);
-          forward(*pol, rows, segs, n, hb, st, mc.time_attn ? &timer : nullptr);
+          if (chunked) spex_k_build_decode_chunks(rows, segs, n, g_cache.dc, st);
+          forward(*pol, rows, segs, n, hb, st, mc.time_attn ? &timer : nullptr, nullptr, 0,
+                  chunked ? &g_cache.dc : nullptr);
           if (dbg && dbg_n + n <= mc.out_rows_cap) {
             spex_k_gather_outputs(rows, n, pol->amax, pol->lse, pol->lsum, dbg + dbg_n, st);
             dbg_n += n;

@@ -691,6 +691,237 @@ __global__ void __launch_bounds__(256, (G == 1 ? 4 : (G <= 4 ? 2 : 1))) tree_att
   }
 }
 
+// Decode work list: per-row context length -> chunk count/length, exclusive
+// scan over rows (one block), (row, chunk) items; zeroes the work queues.
+__global__ void __launch_bounds__(1024) build_decode_chunks_kernel(const RowDesc* __restrict__ rows,
+                                                                  const Segment* __restrict__ segs, int M,
+                                                                  DecodeChunks w) {
+  __shared__ int sums[1024];
+  const int tid = threadIdx.x;
+  if (tid < kQueueSlots) w.qctr[tid] = 0;
+  const int per = (M + 1023) / 1024;
+  const int r0 = tid * per, r1 = min(M, r0 + per);
+  int local = 0;
+  for (int r = r0; r < r1; ++r) {
+    const RowDesc rd = rows[r];
+    int L = 0;
+    for (int k = 0; k < rd.nseg; ++k) L += segs[rd.seg_off + k].len;
+    int ch = (L + kMaxRowChunks - 1) / kMaxRowChunks;
+    if (ch < kMinChunk) ch = kMinChunk;
+    const int nch = (L + ch - 1) / ch;
+    w.row_nch[r] = nch;
+    w.row_ch[r] = ch;
+    local += nch;
+  }
+  sums[tid] = local;
+  __syncthreads();
+  for (int o = 1; o < 1024; o <<= 1) {
+    const int v = tid >= o ? sums[tid - o] : 0;
+    __syncthreads();
+    sums[tid] += v;
+    __syncthreads();
+  }
+  int base = sums[tid] - local;
+  for (int r = r0; r < r1; ++r) {
+    w.row_item0[r] = base;
+    for (int c = 0; c < w.row_nch[r]; ++c) w.items[base + c] = make_int2(r, c);
+    base += w.row_nch[r];
+  }
+  if (tid == 1023) *w.n_items = sums[1023];
+}
+
+// K1 decode, chunked: a persistent grid of warps pulls (chunk, kv head) work
+// from a device queue; each streams its chunk of the row's tree context with
+// 128-bit loads and FHFMA.BF16 (as tree_attn_decode_kernel). Single-chunk rows
+// write O directly; multi-chunk rows leave a partial (m, l, acc) and the last
+// arriving warp of the (row, head) merges them. Bounded chunks keep every warp's
+// work within ~kMinChunk..ctx/8 tokens, so no long row forms a tail.
+template <int DH, int G>
+__global__ void __launch_bounds__(256, (G == 1 ? 4 : (G <= 4 ? 2 : 1)))
+    tree_attn_chunk_kernel(const RowDesc* __restrict__ rows, const Segment* __restrict__ segs,
+                           const float* __restrict__ Qr, int H, int KVH, const __nv_bfloat16* __restrict__ Kp,
+                           const __nv_bfloat16* __restrict__ Vp, long long slots, __nv_bfloat16* __restrict__ O,
+                           DecodeChunks w, int* __restrict__ qctr) {
+  constexpr int EPL = 8;
+  constexpr int LPT = DH / EPL;
+  constexpr int TPW = 32 / LPT;
+  constexpr int UNROLL = 4;
+  constexpr float L2E = 1.4426950408889634f;
+  const int lane = threadIdx.x & 31;
+  const int sub = lane / LPT;
+  const int li = lane % LPT;
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  const int total = *w.n_items * KVH;
+  for (;;) {
+    int wi = 0;
+    if (lane == 0) wi = atomicAdd(qctr, 1);
+    wi = __shfl_sync(0xffffffffu, wi, 0);
+    if (wi >= total) break;
+    const int item = wi / KVH, kh = wi - item * KVH;
+    const int2 rc = w.items[item];
+    const int r = rc.x, c = rc.y;
+    const int nch = w.row_nch[r], ch = w.row_ch[r];
+    const int tbeg = c * ch, tend = tbeg + ch;
+    const RowDesc rd = rows[r];
+    const Segment* sg = segs + rd.seg_off;
+    const __nv_bfloat16* Kh = Kp + (long long)kh * slots * DH + li * EPL;
+    const __nv_bfloat16* Vh = Vp + (long long)kh * slots * DH + li * EPL;
+    uint32_t q2[G][EPL / 2];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const float4* qp = reinterpret_cast<const float4*>(Qr + ((long long)r * H + kh * G + g) * DH + li * EPL);
+      const float4 a = qp[0], b = qp[1];
+      q2[g][0] = pack_bf16(a.x * L2E, a.y * L2E);
+      q2[g][1] = pack_bf16(a.z * L2E, a.w * L2E);
+      q2[g][2] = pack_bf16(b.x * L2E, b.y * L2E);
+      q2[g][3] = pack_bf16(b.z * L2E, b.w * L2E);
+    }
+    float m[G], l[G], acc[G][EPL];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      m[g] = -INFINITY;
+      l[g] = 0.f;
+#pragma unroll
+      for (int e = 0; e < EPL; ++e) acc[g][e] = 0.f;
+    }
+    int off = 0;
+    for (int si = 0; si < rd.nseg && off < tend; ++si) {
+      const int len = sg[si].len;
+      const int lo = max(tbeg - off, 0), hi = min(tend - off, len);
+      const long long base = sg[si].base;
+      off += len;
+      for (int t0 = lo; t0 < hi; t0 += TPW * UNROLL) {
+        uint4 kraw[UNROLL], vraw[UNROLL];
+        bool ok[UNROLL];
+#pragma unroll
+        for (int u = 0; u < UNROLL; ++u) {
+          const int t = t0 + u * TPW + sub;
+          ok[u] = t < hi;
+          const long long o = (base + (ok[u] ? t : lo)) * DH;
+          kraw[u] = ld_stream(Kh + o, pol);
+          vraw[u] = ld_stream(Vh + o, pol);
+        }
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          float sc[UNROLL];
+#pragma unroll
+          for (int u = 0; u < UNROLL; ++u) {
+            float a = 0.f;
+            fma2_bf16(a, q2[g][0], kraw[u].x);
+            fma2_bf16(a, q2[g][1], kraw[u].y);
+            fma2_bf16(a, q2[g][2], kraw[u].z);
+            fma2_bf16(a, q2[g][3], kraw[u].w);
+            sc[u] = a;
+          }
+#pragma unroll
+          for (int o = LPT / 2; o > 0; o >>= 1)
+#pragma unroll
+            for (int u = 0; u < UNROLL; ++u) sc[u] += __shfl_xor_sync(0xffffffffu, sc[u], o);
+          float mx = -INFINITY;
+#pragma unroll
+          for (int u = 0; u < UNROLL; ++u) {
+            if (!ok[u]) sc[u] = -INFINITY;
+            mx = fmaxf(mx, sc[u]);
+          }
+#pragma unroll
+          for (int o = LPT; o < 32; o <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+          if (mx > m[g]) {
+            const float scale = exp2f(m[g] - mx);
+            l[g] *= scale;
+#pragma unroll
+            for (int e = 0; e < EPL; ++e) acc[g][e] *= scale;
+            m[g] = mx;
+          }
+#pragma unroll
+          for (int u = 0; u < UNROLL; ++u) {
+            const float p = exp2f(sc[u] - m[g]);
+            const __nv_bfloat16 pb = __float2bfloat16_rn(p);
+            l[g] += __bfloat162float(pb);
+            const uint32_t p2 = (uint32_t)__bfloat16_as_ushort(pb) * 0x10001u;
+            fma_pv_bf16(acc[g][0], acc[g][1], p2, vraw[u].x);
+            fma_pv_bf16(acc[g][2], acc[g][3], p2, vraw[u].y);
+            fma_pv_bf16(acc[g][4], acc[g][5], p2, vraw[u].z);
+            fma_pv_bf16(acc[g][6], acc[g][7], p2, vraw[u].w);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+#pragma unroll
+      for (int o = LPT; o < 32; o <<= 1) {
+        l[g] += __shfl_xor_sync(0xffffffffu, l[g], o);
+#pragma unroll
+        for (int e = 0; e < EPL; ++e) acc[g][e] += __shfl_xor_sync(0xffffffffu, acc[g][e], o);
+      }
+    }
+    if (nch == 1) {
+      if (sub == 0) {
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          const float inv = 1.f / l[g];
+          uint4 packed;
+          packed.x = pack_bf16(acc[g][0] * inv, acc[g][1] * inv);
+          packed.y = pack_bf16(acc[g][2] * inv, acc[g][3] * inv);
+          packed.z = pack_bf16(acc[g][4] * inv, acc[g][5] * inv);
+          packed.w = pack_bf16(acc[g][6] * inv, acc[g][7] * inv);
+          *reinterpret_cast<uint4*>(O + ((long long)r * H + kh * G + g) * DH + li * EPL) = packed;
+        }
+      }
+      continue;
+    }
+    // partial state of this chunk: [G][DH] acc, then m[G], l[G]
+    constexpr int PS = G * DH + ((2 * G + 3) & ~3);  // 16-byte aligned per (item, head)
+    float* pp = w.part + ((long long)item * KVH + kh) * PS;
+    if (sub == 0) {
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        float4* ap = reinterpret_cast<float4*>(pp + g * DH + li * EPL);
+        ap[0] = make_float4(acc[g][0], acc[g][1], acc[g][2], acc[g][3]);
+        ap[1] = make_float4(acc[g][4], acc[g][5], acc[g][6], acc[g][7]);
+      }
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        pp[G * DH + g] = m[g];
+        pp[G * DH + G + g] = l[g];
+      }
+    }
+    __threadfence();
+    __syncwarp();
+    int last = 0;
+    if (lane == 0) last = atomicAdd(&w.cnt[r * KVH + kh], 1) == nch - 1;
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (!last) continue;
+    __threadfence();
+    // merge the row's nch partials: each lane owns DH/32 dims of every head
+    constexpr int DPL = DH / 32;
+    const float* p0 = w.part + ((long long)w.row_item0[r] * KVH + kh) * PS;
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      float M = -INFINITY;
+      for (int k = 0; k < nch; ++k) M = fmaxf(M, __ldcg(p0 + (long long)k * KVH * PS + G * DH + g));
+      float Lsum = 0.f, a[DPL];
+#pragma unroll
+      for (int e = 0; e < DPL; ++e) a[e] = 0.f;
+      for (int k = 0; k < nch; ++k) {
+        const float* pk = p0 + (long long)k * KVH * PS;
+        const float sk = exp2f(__ldcg(pk + G * DH + g) - M);
+        Lsum += __ldcg(pk + G * DH + G + g) * sk;
+#pragma unroll
+        for (int e = 0; e < DPL; ++e) a[e] += __ldcg(pk + g * DH + lane * DPL + e) * sk;
+      }
+      const float inv = 1.f / Lsum;
+      __nv_bfloat16* op = O + ((long long)r * H + kh * G + g) * DH + lane * DPL;
+#pragma unroll
+      for (int e = 0; e < DPL; e += 2) *reinterpret_cast<uint32_t*>(op + e) = pack_bf16(a[e] * inv, a[e + 1] * inv);
+    }
+    if (lane == 0) w.cnt[r * KVH + kh] = 0;
+  }
+}
+
 // ----------------------------------------------------------------------------
 // K1 tile variant on tensor cores (PRM / prompt prefill rows, DH = 128).
 // K/V chunks of 64 tokens arrive by TMA (2D tensor maps over the pool viewed as
@@ -1368,6 +1599,49 @@ extern "C" int spex_k_tree_attn(const RowDesc* rows, const Segment* segs, const 
   SPEX_ATTN_CASE(64, 2)
   SPEX_ATTN_CASE(64, 4)
 #undef SPEX_ATTN_CASE
+  return -1;
+}
+
+extern "C" void spex_k_build_decode_chunks(const RowDesc* rows, const Segment* segs, int M, DecodeChunks w,
+                                           cudaStream_t s) {
+  build_decode_chunks_kernel<<<1, 1024, 0, s>>>(rows, segs, M, w);
+}
+
+template <int DH, int G>
+static void launch_attn_chunk(const RowDesc* rows, const Segment* segs, const float* Qr, int H, int KVH,
+                              const __nv_bfloat16* Kp, const __nv_bfloat16* Vp, long long slots, __nv_bfloat16* O,
+                              const DecodeChunks& w, int* qctr, cudaStream_t s) {
+  static int blocks = 0;
+  if (!blocks) {
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, tree_attn_chunk_kernel<DH, G>, 256, 0);
+    blocks = sms * (per > 0 ? per : 1);
+  }
+  tree_attn_chunk_kernel<DH, G><<<blocks, 256, 0, s>>>(rows, segs, Qr, H, KVH, Kp, Vp, slots, O, w, qctr);
+}
+
+// K1 decode over the step's chunked work list (spex_k_build_decode_chunks);
+// qslot selects this launch's work-queue counter (one per layer).
+extern "C" int spex_k_tree_attn_chunked(const RowDesc* rows, const Segment* segs, const float* Qr, int H, int KVH,
+                                        int dh, const __nv_bfloat16* Kp, const __nv_bfloat16* Vp, long long slots,
+                                        __nv_bfloat16* O, DecodeChunks w, int qslot, cudaStream_t s) {
+  const int G = H / KVH;
+  int* qctr = w.qctr + (qslot % kQueueSlots);
+#define SPEX_CHUNK_CASE(D, GG)                                                        \
+  if (dh == D && G == GG) {                                                           \
+    launch_attn_chunk<D, GG>(rows, segs, Qr, H, KVH, Kp, Vp, slots, O, w, qctr, s);   \
+    return 0;                                                                         \
+  }
+  SPEX_CHUNK_CASE(128, 1)
+  SPEX_CHUNK_CASE(128, 2)
+  SPEX_CHUNK_CASE(128, 4)
+  SPEX_CHUNK_CASE(128, 8)
+  SPEX_CHUNK_CASE(64, 1)
+  SPEX_CHUNK_CASE(64, 2)
+  SPEX_CHUNK_CASE(64, 4)
+#undef SPEX_CHUNK_CASE
   return -1;
 }
 

@@ -23,6 +23,12 @@ SEG = np.dtype([("base", "<i8"), ("len", "<i4"), ("pad", "<i4")])
 MAX_SEG = 40
 
 
+class DecodeChunks(ctypes.Structure):
+    """model.h DecodeChunks (device pointers)."""
+    _fields_ = [(n, ctypes.c_void_p) for n in
+                ("items", "row_nch", "row_ch", "row_item0", "n_items", "qctr", "part", "cnt")]
+
+
 def _lib():
     import paper_2605_10195_b200 as spex
     from paper_2605_10195_b200 import _lib as L
@@ -34,7 +40,15 @@ def _lib():
     f.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                   ctypes.c_void_p, ctypes.c_void_p, ctypes.c_longlong, ctypes.c_void_p, ctypes.c_int,
                   ctypes.c_void_p]
-    return f
+    b = lib.spex_k_build_decode_chunks
+    b.restype = None
+    b.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, DecodeChunks, ctypes.c_void_p]
+    c = lib.spex_k_tree_attn_chunked
+    c.restype = ctypes.c_int
+    c.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                  ctypes.c_void_p, ctypes.c_void_p, ctypes.c_longlong, ctypes.c_void_p, DecodeChunks, ctypes.c_int,
+                  ctypes.c_void_p]
+    return f, b, c
 
 
 def _make_tree_rows(rng, M, slots, max_depth):
@@ -67,10 +81,15 @@ def _make_tree_rows(rng, M, slots, max_depth):
     return rows, segs, paths
 
 
+@pytest.mark.parametrize("impl", ["row", "chunked"])
 @pytest.mark.parametrize("H,KVH,dh,M", [(8, 8, 128, 300), (32, 8, 128, 97), (4, 2, 64, 150), (16, 4, 64, 64)])
-def test_k1_decode_matches_torch_fp32(H, KVH, dh, M):
+def test_k1_decode_matches_torch_fp32(H, KVH, dh, M, impl):
+    """impl "row": one warp per (row, kv head) (spex_k_tree_attn); "chunked": the
+    decode work list (spex_k_build_decode_chunks + spex_k_tree_attn_chunked),
+    rows up to ~2.4k tokens split into up to 8 chunks merged by the last warp,
+    launched twice to exercise the self-resetting arrival counters."""
     import torch
-    f = _lib()
+    f, build, chunked = _lib()
     rng = np.random.default_rng(H * 1000 + dh + M)
     slots = 200 * max(8, M // 2) + 64
     rows, segs, paths = _make_tree_rows(rng, M, slots, max_depth=12)
@@ -83,9 +102,29 @@ def test_k1_decode_matches_torch_fp32(H, KVH, dh, M):
     rows_d = torch.from_numpy(rows.view(np.uint8).copy()).to(dev)
     segs_d = torch.from_numpy(segs.view(np.uint8).copy()).to(dev)
     st = torch.cuda.current_stream(dev)
-    rc = f(rows_d.data_ptr(), segs_d.data_ptr(), Q.data_ptr(), H, KVH, dh, K.data_ptr(), V.data_ptr(), slots,
-           O.data_ptr(), M, st.cuda_stream)
-    assert rc == 0
+    if impl == "row":
+        rc = f(rows_d.data_ptr(), segs_d.data_ptr(), Q.data_ptr(), H, KVH, dh, K.data_ptr(), V.data_ptr(), slots,
+               O.data_ptr(), M, st.cuda_stream)
+        assert rc == 0
+    else:
+        bufs = {"items": torch.zeros(M * 8 * 2, dtype=torch.int32, device=dev),
+                "row_nch": torch.zeros(M, dtype=torch.int32, device=dev),
+                "row_ch": torch.zeros(M, dtype=torch.int32, device=dev),
+                "row_item0": torch.zeros(M, dtype=torch.int32, device=dev),
+                "n_items": torch.zeros(1, dtype=torch.int32, device=dev),
+                "qctr": torch.zeros(256, dtype=torch.int32, device=dev),
+                "part": torch.zeros(M * 8 * H * (dh + 4), dtype=torch.float32, device=dev),
+                "cnt": torch.zeros(M * KVH, dtype=torch.int32, device=dev)}
+        w = DecodeChunks(**{k: v.data_ptr() for k, v in bufs.items()})
+        build(rows_d.data_ptr(), segs_d.data_ptr(), M, w, st.cuda_stream)
+        for slot in range(2):
+            O.zero_()
+            rc = chunked(rows_d.data_ptr(), segs_d.data_ptr(), Q.data_ptr(), H, KVH, dh, K.data_ptr(), V.data_ptr(),
+                         slots, O.data_ptr(), w, slot, st.cuda_stream)
+            assert rc == 0
+        torch.cuda.synchronize()
+        assert int(bufs["cnt"].abs().sum()) == 0  # counters reset by the merging warps
+        assert int(bufs["row_nch"].max()) > 1      # multi-chunk rows exercised
     torch.cuda.synchronize()
     Kf, Vf = K.float(), V.float()
     G = H // KVH

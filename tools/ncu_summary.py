@@ -24,7 +24,14 @@ WANT = [
 ]
 
 
-def main(rep: str, name: str, alg_bytes_per_launch: float = 0.0):
+def main(rep: str, name: str, alg_log: str = "", first: int = 400):
+    """alg_log: the SPEX_ATTN_LOG file of the profiled command (launch index,
+    algorithmic bytes, ms); the ncu capture skipped `first` K1 launches, so its
+    launches are alg_log lines first, first+1, ..."""
+    alg = []
+    if alg_log:
+        rows = [ln.split() for ln in open(alg_log) if ln.strip()]
+        alg = [float(r[1]) for r in rows if first <= int(r[0])]
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     hdr, units = rows[0], rows[1]
@@ -55,10 +62,17 @@ def main(rep: str, name: str, alg_bytes_per_launch: float = 0.0):
             return d.get(k, 0.0) * mult
         traffic = sum(to_bytes(d, "dram__bytes_read.sum") + to_bytes(d, "dram__bytes_write.sum")
                       for d in launches) / len(launches)
-        (ROOT / "profiles" / f"{name}.json").write_text(json.dumps(
-            {"dram_bytes_per_launch": traffic, "launches": launches}, indent=1))
+        out = {"dram_bytes_per_launch": traffic, "launches": launches}
+        if alg:
+            k = min(len(alg), len(launches))
+            out["alg_bytes_per_launch"] = sum(alg[:k]) / k
+            out["dram_over_alg"] = traffic / out["alg_bytes_per_launch"]
+            md.append(f"algorithmic bytes per launch (same launches): {out['alg_bytes_per_launch']:.4g}; "
+                      f"DRAM/algorithmic = {out['dram_over_alg']:.3f}")
+            (ROOT / "profiles" / f"{name}.md").write_text("\n".join(md))
+        (ROOT / "profiles" / f"{name}.json").write_text(json.dumps(out, indent=1))
     print("\n".join(md[:40]))
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2])
+    main(*sys.argv[1:3], *(sys.argv[3:4]), *([int(sys.argv[4])] if len(sys.argv) > 4 else []))
