@@ -357,6 +357,13 @@ struct ModelCache {
   int* last_row = nullptr;
   TileDesc* tiles = nullptr;
   float* scores = nullptr;
+  // PRM side: its own stream, cuBLAS handle and row buffers, so reward scoring
+  // (tensor-bound prefill GEMMs) overlaps the policy decode (HBM-bound K1)
+  cudaStream_t st2 = nullptr;
+  cublasHandle_t hb2 = nullptr;
+  RowDesc* rows2 = nullptr;
+  Segment* segs2 = nullptr;
+  TileDesc* tiles2 = nullptr;
   // decode work list (K1 chunked), sized for rows_cap rows of the policy shape
   DecodeChunks dc{};
   int dc_rows = 0;
@@ -433,10 +440,21 @@ void run_model_schedule(const ModelRunConfig& mc, const ScheduleView& sv, ModelR
     void* ws = nullptr;
     CK(cudaMalloc(&ws, 64 << 20));  // fixed workspace: no lazy allocation while streaming
     CB(cublasSetWorkspace(g_cache.hb, ws, 64 << 20));
+    CB(cublasCreate(&g_cache.hb2));
+    void* ws2 = nullptr;
+    CK(cudaMalloc(&ws2, 64 << 20));
+    CB(cublasSetWorkspace(g_cache.hb2, ws2, 64 << 20));
+    CK(cudaStreamCreateWithFlags(&g_cache.st2, cudaStreamNonBlocking));
   }
   cublasHandle_t hb = g_cache.hb;
   CB(cublasSetStream(hb, st));
   CB(cublasSetMathMode(hb, CUBLAS_DEFAULT_MATH));
+  // PRM stream: same device, ordered after everything already queued on st
+  const bool prm_overlap = !std::getenv("SPEX_PRM_SAME_STREAM");
+  cudaStream_t st2 = prm_overlap ? g_cache.st2 : st;
+  cublasHandle_t hb2 = prm_overlap ? g_cache.hb2 : hb;
+  CB(cublasSetStream(hb2, st2));
+  CB(cublasSetMathMode(hb2, CUBLAS_DEFAULT_MATH));
   if (g_cache.seed != mc.seed) spex_model_cache_clear();
   Model* pol = cached(g_cache.pol, mc.policy, false, mc.seed, slots, std::max(max_dec, prompt_chunk * P), st);
   Model* prm = mc.with_prm ? cached(g_cache.prm, mc.prm, true, mc.seed, slots, std::max(max_prm, prompt_chunk * P), st)
@@ -446,21 +464,32 @@ void run_model_schedule(const ModelRunConfig& mc, const ScheduleView& sv, ModelR
   const long long cap_slots = prm ? std::min(pol->slots, prm->slots) : pol->slots;
   const int rows_cap = std::max({max_dec, max_prm, prompt_chunk * P, 1});
   if (g_cache.rows_cap < rows_cap) {
+    CK(cudaStreamSynchronize(st));
+    CK(cudaStreamSynchronize(g_cache.st2));
     cudaFree(g_cache.rows);
     cudaFree(g_cache.segs);
     cudaFree(g_cache.last_row);
     cudaFree(g_cache.tiles);
     cudaFree(g_cache.scores);
+    cudaFree(g_cache.rows2);
+    cudaFree(g_cache.segs2);
+    cudaFree(g_cache.tiles2);
     std::vector<void*> keep;
     g_cache.rows = dalloc<RowDesc>(rows_cap, keep);
     g_cache.segs = dalloc<Segment>((size_t)rows_cap * 40, keep);
     g_cache.last_row = dalloc<int>(rows_cap, keep);
     g_cache.tiles = dalloc<TileDesc>(rows_cap, keep);
     g_cache.scores = dalloc<float>(rows_cap, keep);
+    g_cache.rows2 = dalloc<RowDesc>(rows_cap, keep);
+    g_cache.segs2 = dalloc<Segment>((size_t)rows_cap * 40, keep);
+    g_cache.tiles2 = dalloc<TileDesc>(rows_cap, keep);
     g_cache.rows_cap = rows_cap;
   }
   RowDesc* rows = g_cache.rows;
   Segment* segs = g_cache.segs;
+  RowDesc* rows2 = prm_overlap ? g_cache.rows2 : g_cache.rows;
+  Segment* segs2 = prm_overlap ? g_cache.segs2 : g_cache.segs;
+  TileDesc* tiles2 = prm_overlap ? g_cache.tiles2 : g_cache.tiles;
   int* last_row = g_cache.last_row;
   // Chunked K1 (bounded per-warp work, merged partials) is opt-in: on the
   // benchmark's context lengths (~250 tokens/row) the one-warp-per-(row, head)
@@ -480,19 +509,26 @@ void run_model_schedule(const ModelRunConfig& mc, const ScheduleView& sv, ModelR
   cudaEventCreate(&t0);
   cudaEventCreate(&t1);
   cudaEventRecord(t0, st);
+  cudaEvent_t e_fork, e_join;
+  cudaEventCreateWithFlags(&e_fork, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&e_join, cudaEventDisableTiming);
+  cudaEventRecord(e_fork, st);  // weights / pools initialised on st
+  if (st2 != st) CK(cudaStreamWaitEvent(st2, e_fork, 0));
   g_launches = 0;
   g_gemms = 0;
   if (P > 0) {
     for (int q0 = 0; q0 < Q; q0 += prompt_chunk) {
       const int nq = std::min(prompt_chunk, Q - q0);
+      const int ntp = nq * ((P + kTileRows - 1) / kTileRows);
       spex_k_build_prompt_rows(tv_pol, q0, nq, rows, segs, st);
       spex_k_build_prompt_tiles(nq, P, tiles, st);
-      const int ntp = nq * ((P + kTileRows - 1) / kTileRows);
-      g_launches += prm ? 3 : 2;
+      g_launches += 2;
       forward(*pol, rows, segs, nq * P, hb, st, nullptr, tiles, ntp);
       if (prm) {
-        spex_k_build_prompt_rows(tv_prm, q0, nq, rows, segs, st);
-        forward(*prm, rows, segs, nq * P, hb, st, nullptr, tiles, ntp);
+        spex_k_build_prompt_rows(tv_prm, q0, nq, rows2, segs2, st2);
+        spex_k_build_prompt_tiles(nq, P, tiles2, st2);
+        g_launches += 2;
+        forward(*prm, rows2, segs2, nq * P, hb2, st2, nullptr, tiles2, ntp);
       }
       res->prefill_rows += (long long)nq * P;
     }
@@ -532,12 +568,12 @@ void run_model_schedule(const ModelRunConfig& mc, const ScheduleView& sv, ModelR
     } else if (prm && pe.rows > 0) {
       if (pe.rows > max_prm) throw std::runtime_error("PRM batch larger than the row buffers");
       spex_k_build_prm_rows(tv_prm, sv.srow_sid + pe.off, sv.srow_rstart + pe.off, sv.srow_tstart + pe.off, pe.n,
-                            rows, segs, last_row, tiles, st);
-      forward(*prm, rows, segs, pe.rows, hb, st, nullptr, tiles, pe.tiles);
-      spex_k_value_head(prm->Xn, mc.prm.d, last_row, pe.n, prm->vhead, scores, st);
+                            rows2, segs2, last_row, tiles2, st2);
+      forward(*prm, rows2, segs2, pe.rows, hb2, st2, nullptr, tiles2, pe.tiles);
+      spex_k_value_head(prm->Xn, mc.prm.d, last_row, pe.n, prm->vhead, scores, st2);
       g_launches += 2;
       if (dbg_scores && dbg_s + pe.n <= mc.out_scores_cap) {
-        spex_k_gather_prm(rows, last_row, pe.n, scores, dbg_scores + dbg_s, st);
+        spex_k_gather_prm(rows2, last_row, pe.n, scores, dbg_scores + dbg_s, st2);
         dbg_s += pe.n;
       }
       res->prm_rows += pe.rows;
@@ -580,8 +616,12 @@ void run_model_schedule(const ModelRunConfig& mc, const ScheduleView& sv, ModelR
     }
     res->control_error = head->error;
   }
+  cudaEventRecord(e_join, st2);
+  if (st2 != st) CK(cudaStreamWaitEvent(st, e_join, 0));
   cudaEventRecord(t1, st);
   CK(cudaEventSynchronize(t1));
+  cudaEventDestroy(e_fork);
+  cudaEventDestroy(e_join);
   timer.flush();
   float ms = 0.f;
   cudaEventElapsedTime(&ms, t0, t1);

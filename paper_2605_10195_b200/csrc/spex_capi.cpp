@@ -977,7 +977,7 @@ void run_executor(spex_executor& ex, int trace) {
       } catch (const std::exception& e) {
         // capacity exceeded while streaming: fall back to a sequential replay below
         std::fprintf(stderr, "spex: streaming forward abandoned (%s); replaying after the control kernel\n", e.what());
-        cudaStreamSynchronize(ex.mstream);
+        cudaDeviceSynchronize();  // the forward's streams (policy + PRM) and the control kernel
         ex.mres = ModelRunResult{};
       }
     } else {

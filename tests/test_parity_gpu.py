@@ -53,3 +53,21 @@ def test_baseline_configs_match_reference(cfgname):
     ref = refutil.ref_run_log(cfg, seed, None)
     got = spex.run_once(cfg, seed, None).log
     _check(cfgname, ref, got)
+
+
+def test_config4_matches_reference_digest():
+    """Config 4 (rest_hybrid, 4096 queries, t1+t2+t3): the reference log has
+    520k lines, so it is pinned by a SHA-256 of the decision-masked log and the
+    line count (tests/golden/c4_digest.json, made by make_c4_digest.py from the
+    compiled reference)."""
+    import hashlib
+    spex = _spex()
+    dg = json.loads((GOLDEN / "c4_digest.json").read_text())
+    cfg = (ROOT / "configs" / f"{dg['config']}.json").read_text()
+    got = spex.run_once(cfg, dg["seed"], None).log
+    assert len(got) == dg["lines"]
+    h = hashlib.sha256()
+    for ln in got:
+        h.update(json.dumps(refutil.strip_floats(ln), sort_keys=True).encode())
+        h.update(b"\n")
+    assert h.hexdigest() == dg["masked_sha256"]
