@@ -569,8 +569,8 @@ __device__ __forceinline__ void fma_pv_bf16(float& a0, float& a1, uint32_t p2, u
       : "r"(p2), "r"(v2));
 }
 
-template <int DH, int G>
-__global__ void __launch_bounds__(256, (G == 1 ? 4 : (G <= 4 ? 2 : 1))) tree_attn_decode_kernel(const RowDesc* __restrict__ rows,
+template <int DH, int G, int UNROLL>
+__global__ void __launch_bounds__(256, (UNROLL > 4 ? 2 : (G == 1 ? 4 : (G <= 4 ? 2 : 1)))) tree_attn_decode_kernel(const RowDesc* __restrict__ rows,
                                                                  const Segment* __restrict__ segs,
                                                                  const float* __restrict__ Qr, int H, int KVH, int M,
                                                                  const __nv_bfloat16* __restrict__ Kp,
@@ -579,7 +579,6 @@ __global__ void __launch_bounds__(256, (G == 1 ? 4 : (G <= 4 ? 2 : 1))) tree_att
   constexpr int EPL = 8;              // bf16 elements per lane per token (16 bytes)
   constexpr int LPT = DH / EPL;       // lanes per token (16 for DH=128, 8 for DH=64)
   constexpr int TPW = 32 / LPT;       // tokens per warp load (2 or 4)
-  constexpr int UNROLL = 4;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (gw >= M * KVH) return;
@@ -1558,7 +1557,12 @@ static void launch_attn_decode(const RowDesc* rows, const Segment* segs, const f
                                int M, cudaStream_t s) {
   const long long warps = (long long)M * KVH;
   const int blocks = (int)((warps * 32 + 255) / 256);
-  tree_attn_decode_kernel<DH, G><<<blocks, 256, 0, s>>>(rows, segs, Qr, H, KVH, M, Kp, Vp, slots, O);
+  // 8 token pairs in flight per lane when registers allow (G == 1: 64 regs, no spill), else 4
+  static const int unroll = getenv("SPEX_K1_UNROLL") ? atoi(getenv("SPEX_K1_UNROLL")) : (G == 1 ? 8 : 4);
+  if (unroll == 8)
+    tree_attn_decode_kernel<DH, G, 8><<<blocks, 256, 0, s>>>(rows, segs, Qr, H, KVH, M, Kp, Vp, slots, O);
+  else
+    tree_attn_decode_kernel<DH, G, 4><<<blocks, 256, 0, s>>>(rows, segs, Qr, H, KVH, M, Kp, Vp, slots, O);
 }
 
 template <int DH, int G>
