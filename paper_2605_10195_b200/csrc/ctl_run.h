@@ -33,6 +33,11 @@ SPEX_HD i64 spex_clock() {
   return 0;
 #endif
 }
+// shared int scratch (ex.sm, 1032 ints): [0, nthr] slow scan, [0, nwarp) reductions,
+// then disjoint regions for the fast scan, commit totals and query collection
+constexpr int kSmScan = 560;     // 33 ints
+constexpr int kSmCommit = 600;   // 8 ints
+constexpr int kSmCollect = 640;  // 32 ints
 enum { CY_ENGINE = 0, CY_FINS, CY_REWARD, CY_FOLLOW, CY_SCHED, CY_TOTAL, CY_ITEMS, CY_COMMIT };
 #define SPEX_TIMED(ex, R, slot, stmt)                              \
   do {                                                             \
@@ -53,6 +58,33 @@ struct HostExec {
 template <class EX>
 SPEX_HDNI void ex_scan(EX& ex, int* a, int n, int* total) {
 #if SPEX_DEVICE_PASS
+  if (n <= ex.nthr) {
+    // one element per thread: warp shuffle scans, warp totals in shared memory
+    int* ws = ex.sm + kSmScan;
+    const int v = ex.tid < n ? a[ex.tid] : 0;
+    int incl = v;
+    for (int off = 1; off < 32; off <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, off);
+      if (ex.lane >= off) incl += y;
+    }
+    if (ex.lane == 31) ws[ex.warp] = incl;
+    ex.sync();
+    if (ex.warp == 0) {
+      const int wv = ex.lane < ex.nwarp ? ws[ex.lane] : 0;
+      int winc = wv;
+      for (int off = 1; off < 32; off <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, winc, off);
+        if (ex.lane >= off) winc += y;
+      }
+      ws[ex.lane] = winc - wv;
+      if (ex.lane == 31) ws[32] = winc;
+    }
+    ex.sync();
+    if (ex.tid < n) a[ex.tid] = ws[ex.warp] + incl - v;
+    *total = ws[32];
+    ex.sync();
+    return;
+  }
   const int per = (n + ex.nthr - 1) / ex.nthr;
   const int lo = ex.tid * per;
   const int hi = lo + per < n ? lo + per : n;
@@ -671,24 +703,72 @@ SPEX_HDNI void commit_items(Run* R, EX& ex, int n) {
   const Cfg& c = R->cfg;
   const int Q = c.n_queries;
   // finish ranks -> admissions (finish j admits iff admitted0 + j < Q)
-  for (int i = ex.tid; i < n; i += ex.nthr) R->it_scan_a[i] = R->it_fin[i];
-  ex.sync();
-  int nfin = 0;
-  ex_scan(ex, R->it_scan_a, n, &nfin);
   const int ac0 = g->admitted_count;
-  for (int i = ex.tid; i < n; i += ex.nthr) {
-    int admit = (R->it_fin[i] && ac0 + R->it_scan_a[i] < Q) ? 1 : 0;
-    R->it_scan_b[i] = R->it_rec_n[i] + (c.trace ? admit : 0);
-    R->it_scan_c[i] = R->it_spawn_n[i];
-    R->it_scan_d[i] = R->it_push_n[i];
-    R->it_scan_e[i] = R->it_tok[i];
+  int nfin = 0, nrec = 0, nspw = 0, npsh = 0, ntok = 0;
+#if SPEX_DEVICE_PASS
+  if (n <= 32) {
+    // all five scans in warp 0 with shuffles, one barrier to publish
+    int* tot = ex.sm + kSmCommit;
+    if (ex.warp == 0) {
+      const int i = ex.lane;
+      const bool in = i < n;
+      auto xscan = [&](int v, int* t) {
+        int incl = v;
+        for (int off = 1; off < 32; off <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, incl, off);
+          if (i >= off) incl += y;
+        }
+        *t = __shfl_sync(0xffffffffu, incl, 31);
+        return incl - v;
+      };
+      int t0, t1, t2, t3, t4;
+      const int f = in ? R->it_fin[i] : 0;
+      const int fx = xscan(f, &t0);
+      const int admit = (f && ac0 + fx < Q) ? 1 : 0;
+      const int bx = xscan(in ? R->it_rec_n[i] + (c.trace ? admit : 0) : 0, &t1);
+      const int cx = xscan(in ? R->it_spawn_n[i] : 0, &t2);
+      const int dx = xscan(in ? R->it_push_n[i] : 0, &t3);
+      const int ex_ = xscan(in ? R->it_tok[i] : 0, &t4);
+      if (in) {
+        R->it_scan_a[i] = fx;
+        R->it_scan_b[i] = bx;
+        R->it_scan_c[i] = cx;
+        R->it_scan_d[i] = dx;
+        R->it_scan_e[i] = ex_;
+      }
+      if (i == 0) {
+        tot[0] = t0;
+        tot[1] = t1;
+        tot[2] = t2;
+        tot[3] = t3;
+        tot[4] = t4;
+      }
+    }
+    ex.sync();
+    nfin = tot[0];
+    nrec = tot[1];
+    nspw = tot[2];
+    npsh = tot[3];
+    ntok = tot[4];
+  } else
+#endif
+  {
+    for (int i = ex.tid; i < n; i += ex.nthr) R->it_scan_a[i] = R->it_fin[i];
+    ex.sync();
+    ex_scan(ex, R->it_scan_a, n, &nfin);
+    for (int i = ex.tid; i < n; i += ex.nthr) {
+      int admit = (R->it_fin[i] && ac0 + R->it_scan_a[i] < Q) ? 1 : 0;
+      R->it_scan_b[i] = R->it_rec_n[i] + (c.trace ? admit : 0);
+      R->it_scan_c[i] = R->it_spawn_n[i];
+      R->it_scan_d[i] = R->it_push_n[i];
+      R->it_scan_e[i] = R->it_tok[i];
+    }
+    ex.sync();
+    ex_scan(ex, R->it_scan_b, n, &nrec);
+    ex_scan(ex, R->it_scan_c, n, &nspw);
+    ex_scan(ex, R->it_scan_d, n, &npsh);
+    ex_scan(ex, R->it_scan_e, n, &ntok);
   }
-  ex.sync();
-  int nrec = 0, nspw = 0, npsh = 0, ntok = 0;
-  ex_scan(ex, R->it_scan_b, n, &nrec);
-  ex_scan(ex, R->it_scan_c, n, &nspw);
-  ex_scan(ex, R->it_scan_d, n, &npsh);
-  ex_scan(ex, R->it_scan_e, n, &ntok);
   const i64 kv0 = g->kv_next;
   if (c.trace && g->log_n + nrec > c.log_cap) {
     if (ex.tid == 0) set_err(R, ERR_CAP_LOG, -1, kNoNode);
@@ -775,6 +855,28 @@ SPEX_HDNI void commit_items(Run* R, EX& ex, int n) {
 template <class EX, class Pred>
 SPEX_HD int collect_queries(Run* R, EX& ex, Pred pred) {
   const int Q = R->cfg.n_queries;
+#if SPEX_DEVICE_PASS
+  // warp ballots + per-warp counts: two barriers per nthr queries, no global scratch
+  int* wc = ex.sm + kSmCollect;
+  int total = 0;
+  for (int base = 0; base < Q; base += ex.nthr) {
+    const int q = base + ex.tid;
+    const bool p = q < Q && pred(q);
+    const unsigned bal = __ballot_sync(0xffffffffu, p);
+    if (ex.lane == 0) wc[ex.warp] = __popc(bal);
+    ex.sync();
+    int off = total, chunk = 0;
+    for (int w = 0; w < ex.nwarp; ++w) {
+      const int cw = wc[w];
+      if (w < ex.warp) off += cw;
+      chunk += cw;
+    }
+    if (p) R->it_key[off + __popc(bal & ((1u << ex.lane) - 1u))] = q;
+    total += chunk;
+    ex.sync();
+  }
+  return total;
+#endif
   for (int q = ex.tid; q < Q; q += ex.nthr) R->it_scan_a[q] = pred(q) ? 1 : 0;
   ex.sync();
   int n = 0;

@@ -92,8 +92,12 @@ struct PrmOut {
 constexpr int kMaxRowChunks = 8;
 constexpr int kMinChunk = 128;
 constexpr int kQueueSlots = 256;  // per-launch work-queue counters (one per layer)
+struct ChunkItem {
+  int row;
+  int chunk;
+};
 struct DecodeChunks {
-  int2* items;      // (row, chunk) in row order
+  ChunkItem* items;  // (row, chunk) in row order
   int* row_nch;     // chunks of row r
   int* row_ch;      // chunk length (tokens) of row r
   int* row_item0;   // first item of row r

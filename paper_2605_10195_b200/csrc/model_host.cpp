@@ -385,7 +385,7 @@ static void ensure_decode_chunks(int rows_cap, const ModelShape& sh) {
   cudaFree(w.part);
   cudaFree(w.cnt);
   std::vector<void*> keep;
-  w.items = dalloc<int2>((size_t)rows_cap * kMaxRowChunks, keep);
+  w.items = dalloc<ChunkItem>((size_t)rows_cap * kMaxRowChunks, keep);
   w.row_nch = dalloc<int>(rows_cap, keep);
   w.row_ch = dalloc<int>(rows_cap, keep);
   w.row_item0 = dalloc<int>(rows_cap, keep);

@@ -723,7 +723,7 @@ __global__ void __launch_bounds__(1024) build_decode_chunks_kernel(const RowDesc
   int base = sums[tid] - local;
   for (int r = r0; r < r1; ++r) {
     w.row_item0[r] = base;
-    for (int c = 0; c < w.row_nch[r]; ++c) w.items[base + c] = make_int2(r, c);
+    for (int c = 0; c < w.row_nch[r]; ++c) w.items[base + c] = ChunkItem{r, c};
     base += w.row_nch[r];
   }
   if (tid == 1023) *w.n_items = sums[1023];
@@ -758,8 +758,8 @@ __global__ void __launch_bounds__(256, (G == 1 ? 4 : (G <= 4 ? 2 : 1)))
     wi = __shfl_sync(0xffffffffu, wi, 0);
     if (wi >= total) break;
     const int item = wi / KVH, kh = wi - item * KVH;
-    const int2 rc = w.items[item];
-    const int r = rc.x, c = rc.y;
+    const ChunkItem rc = w.items[item];
+    const int r = rc.row, c = rc.chunk;
     const int nch = w.row_nch[r], ch = w.row_ch[r];
     const int tbeg = c * ch, tend = tbeg + ch;
     const RowDesc rd = rows[r];
