@@ -1,0 +1,404 @@
+// gemm_tc.cu — K2: hand-written tcgen05 GEMM for the policy / PRM projections,
+// with the elementwise work of the forward fused into its epilogue.
+//
+//   Y[M x N] = X[M x K] . W[N x K]^T      (bf16 operands, fp32 accumulate in TMEM)
+//
+// One CTA computes one 128 x 128 output tile (UMMA M=128, N=128, K=16 per
+// instruction, cta_group::1). Warp roles:
+//   warp 0      TMA producer: 128x64 bf16 boxes of X and W (128-byte swizzle)
+//               into a 3-stage shared-memory ring (full/empty mbarriers)
+//   warp 1      TMEM allocator (128 columns) and MMA issuer: one elected lane
+//               issues 4 tcgen05.mma per stage from shared-memory descriptors,
+//               tcgen05.commit frees the stage / signals the epilogue
+//   warps 2..5  epilogue: tcgen05.ld of the accumulator (one TMEM lane = one
+//               output row per thread, 128 columns), then one of
+//     EPI_STORE    y (+)= acc                       (O / down projections: residual add)
+//     EPI_ROPE_KV  rotate-half RoPE; Q heads -> Qr (fp32, pre-scaled), K/V heads
+//                  -> bf16 tree-KV pool at the row's slot     (fuses rope_kv_kernel)
+//     EPI_SWIGLU   silu(gate) * up -> bf16 MLP activation, with the gate/up weight
+//                  rows interleaved per 64-column block       (fuses swiglu_kernel)
+//     EPI_LSE      per-row partial max / first argmax / sum exp / sum over the
+//                  tile's vocab columns; a combine kernel finishes K3
+//                  (the fp32 logits are never written to HBM)
+// 3 stages x 32 KB keep two CTAs resident per SM, so one CTA's epilogue overlaps
+// the other's main loop.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "model.h"
+
+namespace spex {
+
+namespace tc {
+
+constexpr int BM = 128, BN = 128, BK = 64, STAGES = 3;
+constexpr int kThreads = 192;
+constexpr uint32_t kStageBytes = (BM + BN) * BK * 2;  // 32 KB
+constexpr uint32_t kTmemCols = 128;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// K-major operand tile [rows][64 bf16] with 128-byte swizzle: 8-row atoms of
+// 1024 B (SBO), LBO unused (1), descriptor version 1 (sm_100), layout SWIZZLE_128B.
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr) {
+  return (uint64_t)((addr >> 4) & 0x3FFFu) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+
+// kind::f16 instruction descriptor: D f32, A/B bf16, both K-major, M=128, N=128
+constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                            ((uint32_t)(BM >> 4) << 24);
+
+__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(kIdesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ uint32_t pack2(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+}  // namespace tc
+
+template <int EPI, int DH>
+__global__ void __launch_bounds__(tc::kThreads, 2)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
+                   int K, TcEpilogue ep) {
+  using namespace tc;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  // 1024-byte alignment for the 128B-swizzled tiles
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  unsigned char* sA = smem;                          // [STAGES][BM][BK]
+  unsigned char* sB = smem + STAGES * BM * BK * 2;   // [STAGES][BN][BK]
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * kStageBytes);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nb = blockIdx.x, mb = blockIdx.y;
+  const int kblocks = K / BK;
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tfull, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int kb = 0; kb < kblocks; ++kb) {
+        const int s = kb % STAGES;
+        if (kb >= STAGES) mbar_wait(&empty[s], ((kb / STAGES) - 1) & 1);
+        mbar_arrive_tx(&full[s], kStageBytes);
+        tma_load_2d(sA + s * BM * BK * 2, &tmA, kb * BK, mb * BM, &full[s]);
+        tma_load_2d(sB + s * BN * BK * 2, &tmB, kb * BK, nb * BN, &full[s]);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      for (int kb = 0; kb < kblocks; ++kb) {
+        const int s = kb % STAGES;
+        mbar_wait(&full[s], (kb / STAGES) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint64_t da = smem_desc(smem_u32(sA + s * BM * BK * 2));
+        const uint64_t db = smem_desc(smem_u32(sB + s * BN * BK * 2));
+#pragma unroll
+        for (int k = 0; k < BK / 16; ++k)  // 16 bf16 = 32 bytes = 2 descriptor units per step
+          mma_bf16(tmem, da + 2 * k, db + 2 * k, (kb | k) != 0);
+        mma_commit(&empty[s]);
+      }
+      mma_commit(tfull);
+    }
+    __syncwarp();
+  } else {
+    // ---------------- epilogue: warps 2..5 own TMEM lane quarters (warp % 4)
+    const int quarter = warp & 3;
+    const int row = mb * BM + quarter * 32 + lane;
+    mbar_wait(tfull, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    float v[BN];
+    const uint32_t tbase = tmem + ((uint32_t)(quarter * 32) << 16);
+#pragma unroll
+    for (int c = 0; c < BN / 32; ++c) tmem_ld32(tbase + c * 32, v + c * 32);
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    if (row < M) {
+      const int n0 = nb * BN;
+      if constexpr (EPI == TC_EPI_STORE) {
+        float4* y = reinterpret_cast<float4*>(ep.y + (long long)row * ep.ldy + n0);
+#pragma unroll
+        for (int i = 0; i < BN / 4; ++i) {
+          float4 o = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+          if (ep.accumulate) {
+            const float4 a = y[i];
+            o.x += a.x;
+            o.y += a.y;
+            o.z += a.z;
+            o.w += a.w;
+          }
+          y[i] = o;
+        }
+      } else if constexpr (EPI == TC_EPI_ROPE_KV) {
+        const RowDesc rd = ep.rows[row];
+        constexpr int half = DH / 2;
+        const float2* cs = reinterpret_cast<const float2*>(ep.rope) + (long long)row * half;
+#pragma unroll
+        for (int h0 = 0; h0 < BN; h0 += DH) {
+          const int head = (n0 + h0) / DH;
+          if (head < ep.H + ep.KVH) {
+            // rotate-half RoPE on (x[i], x[i + half])
+#pragma unroll
+            for (int i = 0; i < half; ++i) {
+              const float2 c = cs[i];
+              const float a = v[h0 + i], b = v[h0 + half + i];
+              v[h0 + i] = a * c.x - b * c.y;
+              v[h0 + half + i] = a * c.y + b * c.x;
+            }
+          }
+          if (head < ep.H) {
+            float4* q = reinterpret_cast<float4*>(ep.Qr + ((long long)row * ep.H + head) * DH);
+#pragma unroll
+            for (int i = 0; i < DH / 4; ++i)
+              q[i] = make_float4(v[h0 + 4 * i] * ep.qscale, v[h0 + 4 * i + 1] * ep.qscale,
+                                 v[h0 + 4 * i + 2] * ep.qscale, v[h0 + 4 * i + 3] * ep.qscale);
+          } else {
+            const bool is_k = head < ep.H + ep.KVH;
+            const int kh = is_k ? head - ep.H : head - ep.H - ep.KVH;
+            __nv_bfloat16* dst =
+                reinterpret_cast<__nv_bfloat16*>(is_k ? ep.Kp : ep.Vp) + ((long long)kh * ep.slots + rd.slot) * DH;
+            uint4* d4 = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+            for (int i = 0; i < DH / 8; ++i)
+              d4[i] = make_uint4(pack2(v[h0 + 8 * i], v[h0 + 8 * i + 1]), pack2(v[h0 + 8 * i + 2], v[h0 + 8 * i + 3]),
+                                 pack2(v[h0 + 8 * i + 4], v[h0 + 8 * i + 5]),
+                                 pack2(v[h0 + 8 * i + 6], v[h0 + 8 * i + 7]));
+          }
+        }
+      } else if constexpr (EPI == TC_EPI_SWIGLU) {
+        // tile nb: columns [0,64) gate j, [64,128) up j for j in [64 nb, 64 nb + 64)
+        uint4* a4 = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(ep.act) + (long long)row * ep.F + nb * (BN / 2));
+#pragma unroll
+        for (int i = 0; i < BN / 16; ++i) {
+          float o[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const float g = v[8 * i + e], u = v[BN / 2 + 8 * i + e];
+            o[e] = g / (1.f + __expf(-g)) * u;
+          }
+          a4[i] = make_uint4(pack2(o[0], o[1]), pack2(o[2], o[3]), pack2(o[4], o[5]), pack2(o[6], o[7]));
+        }
+      } else {  // TC_EPI_LSE
+        float mx = -INFINITY, sm = 0.f;
+        int mi = 0;
+        const int lim = min(BN, ep.V - n0);
+#pragma unroll
+        for (int i = 0; i < BN; ++i) {
+          if (i < lim) {
+            sm += v[i];
+            if (v[i] > mx) {
+              mx = v[i];
+              mi = i;
+            }
+          }
+        }
+        float se = 0.f;
+        const float ml2 = mx * 1.4426950408889634f;
+#pragma unroll
+        for (int i = 0; i < BN; ++i)
+          if (i < lim) se += exp2f(fmaf(v[i], 1.4426950408889634f, -ml2));
+        reinterpret_cast<float4*>(ep.part)[(long long)row * ep.n_tiles + nb] = make_float4(mx, se, sm, __int_as_float(n0 + mi));
+      }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tc::kTmemCols));
+  }
+}
+
+// K3 combine: per row over the LM-head tiles' partials (first argmax on ties).
+__global__ void lse_combine_kernel(const float4* __restrict__ part, int M, int n_tiles, int* amax, float* lse,
+                                   float* lsum) {
+  const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (r >= M) return;
+  const float4* p = part + (long long)r * n_tiles;
+  float mx = -INFINITY, sm = 0.f;
+  int mi = 0x7fffffff;
+  for (int t = lane; t < n_tiles; t += 32) {
+    const float4 q = p[t];
+    sm += q.z;
+    const int qi = __float_as_int(q.w);
+    if (q.x > mx || (q.x == mx && qi < mi)) {
+      mx = q.x;
+      mi = qi;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float om = __shfl_xor_sync(0xffffffffu, mx, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, mi, o);
+    sm += __shfl_xor_sync(0xffffffffu, sm, o);
+    if (om > mx || (om == mx && oi < mi)) mi = oi;
+    mx = fmaxf(mx, om);
+  }
+  float se = 0.f;
+  for (int t = lane; t < n_tiles; t += 32) {
+    const float4 q = p[t];
+    se += q.y * exp2f((q.x - mx) * 1.4426950408889634f);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
+  if (lane == 0) {
+    amax[r] = mi;
+    lse[r] = mx + logf(se);
+    lsum[r] = sm;
+  }
+}
+
+// (cos, sin) of every row's absolute position, once per forward (all layers).
+__global__ void rope_table_kernel(const RowDesc* __restrict__ rows, int M, const float* __restrict__ inv_freq,
+                                  int half, float2* __restrict__ out) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= (long long)M * half) return;
+  const int r = (int)(i / half), k = (int)(i - (long long)r * half);
+  float s, c;
+  sincosf((float)rows[r].abs_pos * inv_freq[k], &s, &c);
+  out[i] = make_float2(c, s);
+}
+
+// Gate/up weight rows interleaved per 64-row block: out block j = [gate 64j..64j+63 ; up 64j..64j+63].
+__global__ void interleave_gu_kernel(const __nv_bfloat16* __restrict__ wgu, int F, int d,
+                                     __nv_bfloat16* __restrict__ out) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= 2LL * F * d) return;
+  const long long orow = i / d, col = i - orow * d;
+  const int blk = (int)(orow / 128), within = (int)(orow % 128);
+  const long long src = within < 64 ? (long long)blk * 64 + within : (long long)F + blk * 64 + (within - 64);
+  out[i] = wgu[src * d + col];
+}
+
+}  // namespace spex
+
+using namespace spex;
+
+extern "C" int spex_k_gemm_tc(const CUtensorMap* tmA, const CUtensorMap* tmB, int M, int N, int K,
+                              const TcEpilogue* ep, cudaStream_t s) {
+  if (M <= 0) return 0;
+  if (N % tc::BN || K % tc::BK) return -1;
+  const size_t smem = tc::STAGES * tc::kStageBytes + 1024 + 256;
+  dim3 grid(N / tc::BN, (M + tc::BM - 1) / tc::BM);
+#define SPEX_TC_LAUNCH(E, D)                                                                               \
+  {                                                                                                        \
+    static bool attr = false;                                                                              \
+    if (!attr) {                                                                                           \
+      cudaFuncSetAttribute(gemm_tc_kernel<E, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);  \
+      attr = true;                                                                                         \
+    }                                                                                                      \
+    gemm_tc_kernel<E, D><<<grid, tc::kThreads, smem, s>>>(*tmA, *tmB, M, N, K, *ep);                       \
+    return (int)cudaGetLastError();                                                                        \
+  }
+  switch (ep->kind) {
+    case TC_EPI_STORE:
+      SPEX_TC_LAUNCH(TC_EPI_STORE, 128)
+    case TC_EPI_SWIGLU:
+      SPEX_TC_LAUNCH(TC_EPI_SWIGLU, 128)
+    case TC_EPI_LSE:
+      SPEX_TC_LAUNCH(TC_EPI_LSE, 128)
+    case TC_EPI_ROPE_KV:
+      if (ep->dh == 128) SPEX_TC_LAUNCH(TC_EPI_ROPE_KV, 128)
+      if (ep->dh == 64) SPEX_TC_LAUNCH(TC_EPI_ROPE_KV, 64)
+      return -1;
+    default:
+      return -1;
+  }
+#undef SPEX_TC_LAUNCH
+}
+
+extern "C" void spex_k_lse_combine(const float* part, int M, int n_tiles, int* amax, float* lse, float* lsum,
+                                   cudaStream_t s) {
+  if (M <= 0) return;
+  lse_combine_kernel<<<(M + 7) / 8, 256, 0, s>>>(reinterpret_cast<const float4*>(part), M, n_tiles, amax, lse, lsum);
+}
+
+extern "C" void spex_k_rope_table(const RowDesc* rows, int M, const float* inv_freq, int half, float* out,
+                                  cudaStream_t s) {
+  const long long n = (long long)M * half;
+  if (n <= 0) return;
+  rope_table_kernel<<<(int)((n + 255) / 256), 256, 0, s>>>(rows, M, inv_freq, half, reinterpret_cast<float2*>(out));
+}
+
+extern "C" void spex_k_interleave_gu(const __nv_bfloat16* wgu, int F, int d, __nv_bfloat16* out, cudaStream_t s) {
+  const long long n = 2LL * F * d;
+  interleave_gu_kernel<<<(int)((n + 255) / 256), 256, 0, s>>>(wgu, F, d, out);
+}

@@ -107,6 +107,32 @@ struct DecodeChunks {
   int* cnt;         // [rows_cap * KVH] arrival counters (self-resetting)
 };
 
+// K2 tcgen05 GEMM epilogues (gemm_tc.cu)
+enum TcEpi : int { TC_EPI_STORE = 0, TC_EPI_ROPE_KV = 1, TC_EPI_SWIGLU = 2, TC_EPI_LSE = 3 };
+struct TcEpilogue {
+  int kind;  // TcEpi
+  // TC_EPI_STORE: y[row * ldy + col] (+)= acc
+  float* y;
+  int ldy;
+  int accumulate;
+  // TC_EPI_ROPE_KV
+  const RowDesc* rows;
+  const float* rope;  // [M][dh/2] (cos, sin) pairs at each row's absolute position
+  int H, KVH, dh;
+  float qscale;
+  float* Qr;           // [M][H][dh] fp32, q * qscale
+  void* Kp;            // bf16 [KVH][slots][dh]
+  void* Vp;
+  long long slots;
+  // TC_EPI_SWIGLU: act[row][F] bf16 (gate/up weight rows interleaved per 64)
+  void* act;
+  int F;
+  // TC_EPI_LSE: part[row][n_tiles] = (max, sum exp(x - max), sum x, first argmax bits)
+  float* part;
+  int n_tiles;
+  int V;
+};
+
 // Schedule produced by the control kernel: decode epochs and reward batches.
 enum : int { SCHED_DECODE = 1, SCHED_PRM = 2 };
 

@@ -61,6 +61,11 @@ int spex_k_tree_attn_chunked(const RowDesc* rows, const Segment* segs, const flo
                              const __nv_bfloat16* Kp, const __nv_bfloat16* Vp, long long slots, __nv_bfloat16* O,
                              DecodeChunks w, int qslot, cudaStream_t s);
 void spex_k_swiglu(const float* GU, int M, int F, __nv_bfloat16* A, cudaStream_t s);
+int spex_k_gemm_tc(const CUtensorMap* tmA, const CUtensorMap* tmB, int M, int N, int K, const TcEpilogue* ep,
+                   cudaStream_t s);
+void spex_k_lse_combine(const float* part, int M, int n_tiles, int* amax, float* lse, float* lsum, cudaStream_t s);
+void spex_k_rope_table(const RowDesc* rows, int M, const float* inv_freq, int half, float* out, cudaStream_t s);
+void spex_k_interleave_gu(const __nv_bfloat16* wgu, int F, int d, __nv_bfloat16* out, cudaStream_t s);
 void spex_k_lm_epilogue(const float* logits, int M, int V, int* amax, float* lse, float* lsum, cudaStream_t s);
 void spex_k_value_head(const __nv_bfloat16* Hn, int d, const int* last_row, int n, const __nv_bfloat16* w,
                        float* score, cudaStream_t s);
@@ -135,6 +140,28 @@ static bool make_kv_tmap(CUtensorMap* m, void* base, long long rows, int dh) {
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// TMA descriptor of a row-major bf16 matrix [rows][cols] as a GEMM operand of
+// gemm_tc.cu: 64 x 128 (cols x rows) boxes, 128-byte swizzle.
+extern "C" int spex_tmap_operand(CUtensorMap* m, const void* base, long long rows, long long cols) {
+  PFN_tmap_encode enc = tmap_encoder();
+  if (!enc || cols % 64 != 0) return -1;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+  cuuint32_t box[2] = {64, 128};
+  cuuint32_t es[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS
+             ? 0
+             : -1;
+}
+
+// K2 on hand-written tcgen05 (gemm_tc.cu): operand maps of one weight matrix
+struct TcWeight {
+  CUtensorMap map;
+  int N = 0, K = 0;
+};
+
 struct Model {
   ModelShape sh;
   std::vector<CUtensorMap> kmap, vmap;  // per layer (empty when TMA maps are unavailable)
@@ -157,6 +184,14 @@ struct Model {
   float* GU = nullptr;
   __nv_bfloat16* A = nullptr;
   float* logits = nullptr;
+  // tcgen05 path (use_tc): weight maps, activation maps, RoPE table, LM-head partials
+  bool use_tc = false;
+  std::vector<TcWeight> tq, to, tgu, td;
+  TcWeight tlm;
+  std::vector<__nv_bfloat16*> wgu_il;  // gate/up rows interleaved per 64
+  CUtensorMap a_xn, a_o, a_act;        // activation operands [max_rows][*]
+  float* rope_tab = nullptr;           // [max_rows][dh/2] (cos, sin)
+  float* lse_part = nullptr;           // [max_rows][V/128] float4
   int* amax = nullptr;
   float* lse = nullptr;
   float* lsum = nullptr;
@@ -242,12 +277,47 @@ static Model* make_model(const ModelShape& sh, bool prm, uint64_t seed, long lon
   m->GU = dalloc<float>(M * 2 * sh.F, o);
   m->A = dalloc<__nv_bfloat16>(M * sh.F, o);
   if (!prm) {
-    m->logits = dalloc<float>(M * sh.V, o);
     m->amax = dalloc<int>(M, o);
     m->lse = dalloc<float>(M, o);
     m->lsum = dalloc<float>(M, o);
   }
+  // K2 on the hand-written tcgen05 GEMM when every projection tiles by 128 x 64
+  // (all shapes here do); SPEX_CUBLAS=1 keeps the cuBLAS + elementwise path.
+  const int qkv_n = (sh.H + 2 * sh.KVH) * sh.dh;
+  m->use_tc = !getenv("SPEX_CUBLAS") && sh.d % 128 == 0 && sh.d % 64 == 0 && qkv_n % 128 == 0 &&
+              (sh.H * sh.dh) % 64 == 0 && (2 * sh.F) % 128 == 0 && sh.F % 64 == 0 && (sh.dh == 64 || sh.dh == 128) &&
+              (prm || sh.V % 128 == 0);
+  if (m->use_tc) {
+    auto wmap = [&](TcWeight& w, const __nv_bfloat16* base, int N, int K) {
+      w.N = N;
+      w.K = K;
+      if (spex_tmap_operand(&w.map, base, N, K) != 0) m->use_tc = false;
+    };
+    m->tq.resize(sh.L);
+    m->to.resize(sh.L);
+    m->tgu.resize(sh.L);
+    m->td.resize(sh.L);
+    for (int l = 0; l < sh.L; ++l) {
+      m->wgu_il.push_back(dalloc<__nv_bfloat16>((size_t)2 * sh.F * sh.d, o));
+      spex_k_interleave_gu(m->wgu[l], sh.F, sh.d, m->wgu_il.back(), st);
+      wmap(m->tq[l], m->wqkv[l], qkv_n, sh.d);
+      wmap(m->to[l], m->wo[l], sh.d, sh.H * sh.dh);
+      wmap(m->tgu[l], m->wgu_il[l], 2 * sh.F, sh.d);
+      wmap(m->td[l], m->wd[l], sh.d, sh.F);
+    }
+    if (!prm) wmap(m->tlm, m->lm, sh.V, sh.d);
+    if (spex_tmap_operand(&m->a_xn, m->Xn, (long long)M, sh.d) || spex_tmap_operand(&m->a_o, m->O, (long long)M, sh.H * sh.dh) ||
+        spex_tmap_operand(&m->a_act, m->A, (long long)M, sh.F))
+      m->use_tc = false;
+    m->rope_tab = dalloc<float>(M * sh.dh, o);
+    if (!prm) m->lse_part = dalloc<float>(M * (size_t)(sh.V / 128) * 4, o);
+  }
+  if (!m->use_tc && !prm) m->logits = dalloc<float>(M * sh.V, o);
   return m;
+}
+
+static void tc_gemm(const CUtensorMap& a, const TcWeight& w, int M, const TcEpilogue& ep, cudaStream_t st) {
+  if (spex_k_gemm_tc(&a, &w.map, M, w.N, w.K, &ep, st) != 0) throw std::runtime_error("tcgen05 GEMM launch failed");
 }
 
 // One forward over M rows. K1 launches are bracketed by events when `attn_ev`
@@ -258,6 +328,68 @@ static void forward(Model& m, const RowDesc* rows, const Segment* segs, int M, c
                     cudaStream_t st, AttnTimer* timer, const TileDesc* tiles = nullptr, int ntiles = 0,
                     const DecodeChunks* chunks = nullptr) {
   const ModelShape& s = m.sh;
+  if (m.use_tc) {
+    // embed -> L x [RMSNorm, QKV+RoPE+KV-append (tcgen05), K1, O-proj + residual
+    // (tcgen05), RMSNorm, gate/up + SwiGLU (tcgen05), down + residual (tcgen05)]
+    // -> RMSNorm -> LM head + logsumexp/argmax partials (tcgen05) -> combine
+    g_launches += 3 + 7LL * s.L + (m.is_prm ? 0 : 2);
+    spex_k_rope_table(rows, M, m.inv_freq, s.dh / 2, m.rope_tab, st);
+    spex_k_embed(rows, M, m.embed, s.d, m.X, st);
+    TcEpilogue eq{};
+    eq.kind = TC_EPI_ROPE_KV;
+    eq.rows = rows;
+    eq.rope = m.rope_tab;
+    eq.H = s.H;
+    eq.KVH = s.KVH;
+    eq.dh = s.dh;
+    eq.qscale = 1.0f / std::sqrt((float)s.dh);
+    eq.Qr = m.Qr;
+    eq.slots = m.slots;
+    TcEpilogue er{};
+    er.kind = TC_EPI_STORE;
+    er.y = m.X;
+    er.ldy = s.d;
+    er.accumulate = 1;
+    TcEpilogue eg{};
+    eg.kind = TC_EPI_SWIGLU;
+    eg.act = m.A;
+    eg.F = s.F;
+    for (int l = 0; l < s.L; ++l) {
+      spex_k_rmsnorm(m.X, M, s.d, s.eps, m.Xn, st);
+      eq.Kp = m.Kp[l];
+      eq.Vp = m.Vp[l];
+      tc_gemm(m.a_xn, m.tq[l], M, eq, st);
+      if (timer) timer->begin(st);
+      int rc = -1;
+      if (tiles && !m.kmap.empty())
+        rc = spex_k_tree_attn_tiles_mma(&m.kmap[l], &m.vmap[l], tiles, ntiles, rows, segs, m.Qr, s.H, s.KVH, s.dh,
+                                        m.slots, m.O, st);
+      if (rc != 0 && chunks)
+        rc = spex_k_tree_attn_chunked(rows, segs, m.Qr, s.H, s.KVH, s.dh, m.Kp[l], m.Vp[l], m.slots, m.O, *chunks, l,
+                                      st);
+      if (rc != 0)
+        rc = tiles ? spex_k_tree_attn_tiles(tiles, ntiles, rows, segs, m.Qr, s.H, s.KVH, s.dh, m.Kp[l], m.Vp[l],
+                                            m.slots, m.O, st)
+                   : spex_k_tree_attn(rows, segs, m.Qr, s.H, s.KVH, s.dh, m.Kp[l], m.Vp[l], m.slots, m.O, M, st);
+      if (rc != 0) throw std::runtime_error("tree attention: unsupported head shape");
+      if (timer) timer->end(st);
+      tc_gemm(m.a_o, m.to[l], M, er, st);
+      spex_k_rmsnorm(m.X, M, s.d, s.eps, m.Xn, st);
+      tc_gemm(m.a_xn, m.tgu[l], M, eg, st);
+      tc_gemm(m.a_act, m.td[l], M, er, st);
+    }
+    spex_k_rmsnorm(m.X, M, s.d, s.eps, m.Xn, st);
+    if (!m.is_prm) {
+      TcEpilogue el{};
+      el.kind = TC_EPI_LSE;
+      el.part = m.lse_part;
+      el.n_tiles = s.V / 128;
+      el.V = s.V;
+      tc_gemm(m.a_xn, m.tlm, M, el, st);
+      spex_k_lse_combine(m.lse_part, M, s.V / 128, m.amax, m.lse, m.lsum, st);
+    }
+    return;
+  }
   g_launches += 2 + 5LL * s.L + (m.is_prm ? 0 : 1);
   g_gemms += 4LL * s.L + (m.is_prm ? 0 : 1);
   spex_k_embed(rows, M, m.embed, s.d, m.X, st);

@@ -1,0 +1,181 @@
+"""K2: the hand-written tcgen05 GEMM (gemm_tc.cu) and its fused epilogues vs
+plain PyTorch fp32 references of the same ops.
+
+Y = X . W^T with bf16 operands and fp32 accumulation in TMEM; tolerance
+(stated): fp32 outputs |Y - Y_ref| <= 2e-3 * (1 + |Y_ref|) (accumulation
+order differs from torch's), bf16 outputs |Y - Y_ref| <= 2e-2 * (1 + |Y_ref|)
+(one bf16 rounding). Shapes cover ragged M (TMA zero-fills the tail rows),
+K spanning more k-blocks than pipeline stages, and every epilogue:
+STORE (plain and residual-accumulate), SWIGLU (interleaved gate/up rows),
+ROPE_KV (dh 128 and 64; Q to fp32, K/V to the bf16 pool at each row's slot)
+and LSE (+ combine: logsumexp, first argmax, logit sum).
+"""
+import ctypes
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROW = np.dtype([("q", "<i4"), ("node", "<u4"), ("pos", "<i4"), ("abs_pos", "<i4"), ("slot", "<i8"),
+                ("seg_off", "<i4"), ("nseg", "<i4"), ("token", "<i4"), ("pad", "<i4")])
+EPI_STORE, EPI_ROPE_KV, EPI_SWIGLU, EPI_LSE = 0, 1, 2, 3
+
+
+class TcEpilogue(ctypes.Structure):
+    """model.h TcEpilogue."""
+    _fields_ = [("kind", ctypes.c_int), ("y", ctypes.c_void_p), ("ldy", ctypes.c_int), ("accumulate", ctypes.c_int),
+                ("rows", ctypes.c_void_p), ("rope", ctypes.c_void_p), ("H", ctypes.c_int), ("KVH", ctypes.c_int),
+                ("dh", ctypes.c_int), ("qscale", ctypes.c_float), ("Qr", ctypes.c_void_p), ("Kp", ctypes.c_void_p),
+                ("Vp", ctypes.c_void_p), ("slots", ctypes.c_longlong), ("act", ctypes.c_void_p), ("F", ctypes.c_int),
+                ("part", ctypes.c_void_p), ("n_tiles", ctypes.c_int), ("V", ctypes.c_int)]
+
+
+class TMap:
+    """64-byte aligned CUtensorMap storage (128 bytes)."""
+
+    def __init__(self):
+        self.buf = ctypes.create_string_buffer(256)
+        addr = ctypes.addressof(self.buf)
+        self.ptr = ctypes.c_void_p((addr + 63) & ~63)
+
+
+def _lib():
+    import paper_2605_10195_b200 as spex
+    from paper_2605_10195_b200 import _lib as L
+    if not spex.device_ok():
+        pytest.fail("no sm_100 device: the B200 path has no fallback")
+    lib = L.lib()
+    lib.spex_tmap_operand.restype = ctypes.c_int
+    lib.spex_tmap_operand.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_longlong, ctypes.c_longlong]
+    lib.spex_k_gemm_tc.restype = ctypes.c_int
+    lib.spex_k_gemm_tc.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                   ctypes.POINTER(TcEpilogue), ctypes.c_void_p]
+    lib.spex_k_lse_combine.restype = None
+    lib.spex_k_lse_combine.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_void_p,
+                                       ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+    lib.spex_k_rope_table.restype = None
+    lib.spex_k_rope_table.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p,
+                                      ctypes.c_void_p]
+    return lib
+
+
+def _maps(lib, x, w):
+    a, b = TMap(), TMap()
+    assert lib.spex_tmap_operand(a.ptr, x.data_ptr(), x.shape[0], x.shape[1]) == 0
+    assert lib.spex_tmap_operand(b.ptr, w.data_ptr(), w.shape[0], w.shape[1]) == 0
+    return a, b
+
+
+def _run(lib, x, w, ep):
+    import torch
+    a, b = _maps(lib, x, w)
+    st = torch.cuda.current_stream()
+    rc = lib.spex_k_gemm_tc(a.ptr, b.ptr, x.shape[0], w.shape[0], x.shape[1], ctypes.byref(ep), st.cuda_stream)
+    assert rc == 0
+    torch.cuda.synchronize()
+
+
+def _rand(*shape, scale=1.0, seed=0):
+    import torch
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    return (torch.randn(*shape, generator=g) * scale).to(torch.bfloat16).cuda()
+
+
+@pytest.mark.parametrize("M,N,K", [(300, 256, 192), (128, 128, 64), (2157, 1024, 1024), (77, 384, 2816)])
+@pytest.mark.parametrize("accumulate", [0, 1])
+def test_store(M, N, K, accumulate):
+    import torch
+    lib = _lib()
+    x, w = _rand(M, K, seed=1), _rand(N, K, scale=K ** -0.5, seed=2)
+    y0 = torch.randn(M, N, device="cuda")
+    y = y0.clone()
+    ep = TcEpilogue(kind=EPI_STORE, y=y.data_ptr(), ldy=N, accumulate=accumulate)
+    _run(lib, x, w, ep)
+    ref = x.float() @ w.float().T + (y0 if accumulate else 0)
+    err = ((y - ref).abs() / (1 + ref.abs())).max().item()
+    assert err <= 2e-3, err
+
+
+def test_swiglu_interleaved():
+    import torch
+    lib = _lib()
+    M, d, F = 333, 512, 1408
+    x = _rand(M, d, seed=3)
+    wg, wu = _rand(F, d, scale=d ** -0.5, seed=4), _rand(F, d, scale=d ** -0.5, seed=5)
+    il = torch.empty(2 * F, d, dtype=torch.bfloat16, device="cuda")
+    for j in range(F // 64):
+        il[128 * j:128 * j + 64] = wg[64 * j:64 * j + 64]
+        il[128 * j + 64:128 * j + 128] = wu[64 * j:64 * j + 64]
+    act = torch.zeros(M, F, dtype=torch.bfloat16, device="cuda")
+    ep = TcEpilogue(kind=EPI_SWIGLU, act=act.data_ptr(), F=F)
+    _run(lib, x, il, ep)
+    g, u = x.float() @ wg.float().T, x.float() @ wu.float().T
+    ref = torch.nn.functional.silu(g) * u
+    err = ((act.float() - ref).abs() / (1 + ref.abs())).max().item()
+    assert err <= 2e-2, err
+
+
+@pytest.mark.parametrize("H,KVH,dh", [(8, 8, 128), (4, 2, 64), (2, 2, 64)])
+def test_rope_kv(H, KVH, dh):
+    import torch
+    lib = _lib()
+    M, d, slots = 261, 256, 4096
+    x = _rand(M, d, seed=6)
+    N = (H + 2 * KVH) * dh
+    w = _rand(N, d, scale=d ** -0.5, seed=7)
+    rng = np.random.default_rng(dh + H)
+    rows = np.zeros(M, ROW)
+    rows["abs_pos"] = rng.integers(0, 3000, M)
+    rows["slot"] = rng.permutation(slots)[:M]
+    rows_d = torch.from_numpy(rows.view(np.uint8).copy()).cuda()
+    inv_freq = torch.tensor([1.0 / (10000.0 ** (2.0 * i / dh)) for i in range(dh // 2)], dtype=torch.float32).cuda()
+    rope = torch.zeros(M, dh, dtype=torch.float32, device="cuda")
+    st = torch.cuda.current_stream()
+    lib.spex_k_rope_table(rows_d.data_ptr(), M, inv_freq.data_ptr(), dh // 2, rope.data_ptr(), st.cuda_stream)
+    Qr = torch.zeros(M, H, dh, device="cuda")
+    Kp = torch.zeros(KVH, slots, dh, dtype=torch.bfloat16, device="cuda")
+    Vp = torch.zeros(KVH, slots, dh, dtype=torch.bfloat16, device="cuda")
+    ep = TcEpilogue(kind=EPI_ROPE_KV, rows=rows_d.data_ptr(), rope=rope.data_ptr(), H=H, KVH=KVH, dh=dh,
+                    qscale=dh ** -0.5, Qr=Qr.data_ptr(), Kp=Kp.data_ptr(), Vp=Vp.data_ptr(), slots=slots)
+    _run(lib, x, w, ep)
+    y = (x.float() @ w.float().T).view(M, H + 2 * KVH, dh)
+    pos = torch.from_numpy(rows["abs_pos"].astype(np.float64)).cuda()
+    ang = pos[:, None] * inv_freq.double()[None, :]
+    c, s = torch.cos(ang).float()[:, None, :], torch.sin(ang).float()[:, None, :]
+    a, b = y[:, :H + KVH, :dh // 2], y[:, :H + KVH, dh // 2:]
+    rot = torch.cat([a * c - b * s, a * s + b * c], dim=-1)
+    q_ref = rot[:, :H] * dh ** -0.5
+    k_ref = rot[:, H:]
+    v_ref = y[:, H + KVH:]
+    slot = torch.from_numpy(rows["slot"]).cuda()
+    assert ((Qr - q_ref).abs() / (1 + q_ref.abs())).max().item() <= 2e-3
+    kg = Kp[:, slot].permute(1, 0, 2).float()
+    vg = Vp[:, slot].permute(1, 0, 2).float()
+    assert ((kg - k_ref).abs() / (1 + k_ref.abs())).max().item() <= 2e-2
+    assert ((vg - v_ref).abs() / (1 + v_ref.abs())).max().item() <= 2e-2
+
+
+@pytest.mark.parametrize("M,V,d", [(300, 512, 256), (129, 32000, 1024)])
+def test_lse_argmax(M, V, d):
+    import torch
+    lib = _lib()
+    x, w = _rand(M, d, seed=8), _rand(V, d, scale=2.0 * d ** -0.5, seed=9)
+    nt = V // 128
+    part = torch.zeros(M, nt, 4, device="cuda")
+    ep = TcEpilogue(kind=EPI_LSE, part=part.data_ptr(), n_tiles=nt, V=V)
+    _run(lib, x, w, ep)
+    amax = torch.zeros(M, dtype=torch.int32, device="cuda")
+    lse = torch.zeros(M, device="cuda")
+    lsum = torch.zeros(M, device="cuda")
+    st = torch.cuda.current_stream()
+    lib.spex_k_lse_combine(part.data_ptr(), M, nt, amax.data_ptr(), lse.data_ptr(), lsum.data_ptr(), st.cuda_stream)
+    torch.cuda.synchronize()
+    z = x.float() @ w.float().T
+    assert (lse - torch.logsumexp(z, dim=1)).abs().max().item() <= 2e-3
+    assert ((lsum - z.sum(dim=1)).abs() / (1 + z.abs().sum(dim=1))).max().item() <= 1e-4
+    ra = z.argmax(dim=1)
+    bad = (amax.long() != ra).nonzero().flatten()
+    for r in bad.tolist():  # only near-ties may differ
+        top = torch.topk(z[r], 2).values
+        assert (top[0] - top[1]).item() <= 2e-3
