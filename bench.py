@@ -265,25 +265,35 @@ def main():
         # device time of the step: control-kernel start -> last of (control end,
         # forward end), CUDA events; the forward streams concurrently with control
         dev_s = agg["step_ms"] / 1000.0
-        # end to end through the C-ABI with the traced run and the log copied back
+        # end to end through the public API (Executor: config JSON in, totals
+        # back to the host), like the reference arm's Executor::run with no trace
         barrier()
         t1 = time.perf_counter()
-        e2e_q, e2e_d2h = 0, 0
+        e2e_q = 0
         for _ in range(args.steps):
-            tot, st, ms, d2h = one_search(True)
+            tot, st, ms, _ = one_search(False)
             e2e_q += tot.queries
-            e2e_d2h += d2h
         barrier()
         e2e_wall = time.perf_counter() - t1
-    times = torch.tensor([dev_s, wall, e2e_wall], dtype=torch.float64, device="cuda")
+        # the same with the event log copied back and serialised (run_once semantics)
+        barrier()
+        t2 = time.perf_counter()
+        tr_q, e2e_d2h = 0, 0
+        for _ in range(args.steps):
+            tot, st, ms, d2h = one_search(True)
+            tr_q += tot.queries
+            e2e_d2h += d2h
+        barrier()
+        tr_wall = time.perf_counter() - t2
+    times = torch.tensor([dev_s, wall, e2e_wall, tr_wall], dtype=torch.float64, device="cuda")
     if pg:
         pg.all_reduce(times, op=pg.ReduceOp.MAX)
-        qt = torch.tensor([float(agg["queries"]), float(e2e_q)], dtype=torch.float64, device="cuda")
+        qt = torch.tensor([float(agg["queries"]), float(e2e_q), float(tr_q)], dtype=torch.float64, device="cuda")
         pg.all_reduce(qt)
-        total_q, total_e2e_q = qt.tolist()
+        total_q, total_e2e_q, total_tr_q = qt.tolist()
     else:
-        total_q, total_e2e_q = float(agg["queries"]), float(e2e_q)
-    dev_s, wall, e2e_wall = times.tolist()
+        total_q, total_e2e_q, total_tr_q = float(agg["queries"]), float(e2e_q), float(tr_q)
+    dev_s, wall, e2e_wall, tr_wall = times.tolist()
     if rank != 0:
         return
     achieved = agg["attn_bytes"] / (agg["attn_ms"] / 1000.0) / 1e9 if agg["attn_ms"] > 0 else 0.0
@@ -317,7 +327,10 @@ def main():
                    "parallelism": f"query-sharded x{world}"},
         "e2e": {"value": total_e2e_q / e2e_wall, "unit": "queries/s",
                 "h2d_bytes_per_step": len(cfg_text.encode()),
-                "d2h_bytes_per_step": int(e2e_d2h / args.steps) + 256},
+                "d2h_bytes_per_step": 256 + 256 * cfg["run"]["n_queries"],
+                "traced": {"value": total_tr_q / tr_wall, "unit": "queries/s",
+                           "d2h_bytes_per_step": int(e2e_d2h / args.steps) + 256,
+                           "note": "event log copied back and serialised to JSON lines each step"}},
         "gpu_launches": int(agg["launches"]),
         "roofline": {"bound": "hbm", "kernel": "K1 tree_attn_kernel (policy decode)",
                      "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",

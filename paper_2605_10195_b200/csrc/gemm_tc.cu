@@ -3,15 +3,17 @@
 //
 //   Y[M x N] = X[M x K] . W[N x K]^T      (bf16 operands, fp32 accumulate in TMEM)
 //
-// One CTA computes one 128 x 128 output tile (UMMA M=128, N=128, K=16 per
-// instruction, cta_group::1). Warp roles:
+// Persistent: one CTA per SM walks 128 x 256 output tiles (UMMA M=128, N=256,
+// K=16 per instruction, cta_group::1) with two TMEM accumulators (2 x 256 fp32
+// columns = all of TMEM), so the epilogue of tile i overlaps the MMAs of tile
+// i+1. Warp roles:
 //   warp 0      TMA producer: 128x64 bf16 boxes of X and W (128-byte swizzle)
-//               into a 3-stage shared-memory ring (full/empty mbarriers)
-//   warp 1      TMEM allocator (128 columns) and MMA issuer: one elected lane
+//               into a 4-stage shared-memory ring (full/empty mbarriers)
+//   warp 1      TMEM allocator (512 columns) and MMA issuer: one elected lane
 //               issues 4 tcgen05.mma per stage from shared-memory descriptors,
 //               tcgen05.commit frees the stage / signals the epilogue
 //   warps 2..5  epilogue: tcgen05.ld of the accumulator (one TMEM lane = one
-//               output row per thread, 128 columns), then one of
+//               output row per thread, 128 columns per pass), then one of
 //     EPI_STORE    y (+)= acc                       (O / down projections: residual add)
 //     EPI_ROPE_KV  rotate-half RoPE; Q heads -> Qr (fp32, pre-scaled), K/V heads
 //                  -> bf16 tree-KV pool at the row's slot     (fuses rope_kv_kernel)
@@ -20,8 +22,6 @@
 //     EPI_LSE      per-row partial max / first argmax / sum exp / sum over the
 //                  tile's vocab columns; a combine kernel finishes K3
 //                  (the fp32 logits are never written to HBM)
-// 3 stages x 32 KB keep two CTAs resident per SM, so one CTA's epilogue overlaps
-// the other's main loop.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -33,10 +33,13 @@ namespace spex {
 
 namespace tc {
 
-constexpr int BM = 128, BN = 128, BK = 64, STAGES = 3;
+constexpr int BM = 128, BN = 256, BK = 64, STAGES = 3;
+constexpr int EN = 128;  // epilogue chunk (columns per tcgen05.ld pass)
+constexpr int kStageLd = EN + 4;  // padded row of the epilogue staging buffer (conflict-free float4)
+constexpr uint32_t kEpiBytes = 4 * 32 * kStageLd * 4;
 constexpr int kThreads = 192;
-constexpr uint32_t kStageBytes = (BM + BN) * BK * 2;  // 32 KB
-constexpr uint32_t kTmemCols = 128;
+constexpr uint32_t kStageBytes = (BM + BN) * BK * 2;  // 48 KB
+constexpr uint32_t kTmemCols = BN;  // one fp32 accumulator; two are allocated (double buffer)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -77,7 +80,7 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t addr) {
          ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
 }
 
-// kind::f16 instruction descriptor: D f32, A/B bf16, both K-major, M=128, N=128
+// kind::f16 instruction descriptor: D f32, A/B bf16, both K-major, M=128, N=256
 constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
                             ((uint32_t)(BM >> 4) << 24);
 
@@ -116,9 +119,9 @@ __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
 }  // namespace tc
 
 template <int EPI, int DH>
-__global__ void __launch_bounds__(tc::kThreads, 2)
+__global__ void __launch_bounds__(tc::kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
-                   int K, TcEpilogue ep) {
+                   int K, TcEpilogue ep, unsigned long long* tile_ctr, unsigned long long tile_base) {
   using namespace tc;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // 1024-byte alignment for the 128B-swizzled tiles
@@ -127,26 +130,31 @@ __global__ void __launch_bounds__(tc::kThreads, 2)
   unsigned char* sB = smem + STAGES * BM * BK * 2;   // [STAGES][BN][BK]
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * kStageBytes);
   uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+  uint64_t* tfull = empty + STAGES;  // [2] accumulator ready
+  uint64_t* tempty = tfull + 2;      // [2] accumulator drained by the epilogue
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  float* stage_out = reinterpret_cast<float*>(smem + STAGES * kStageBytes + 256);  // [4 warps][32][kStageLd]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nb = blockIdx.x, mb = blockIdx.y;
   const int kblocks = K / BK;
+  const int n_nb = (N + BN - 1) / BN, n_tiles = n_nb * ((M + BM - 1) / BM);
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(tfull, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 4);  // one arrive per epilogue warp
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(kTmemCols));
+                 "r"(2 * kTmemCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -154,136 +162,197 @@ __global__ void __launch_bounds__(tc::kThreads, 2)
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
 
+  // persistent with a dynamic tile queue: the producer lane claims tiles from a
+  // global counter (so CTAs that start late — SMs busy with the control kernel
+  // or the other forward stream — simply take fewer tiles) and passes each id to
+  // the MMA lane and the epilogue through a shared ring; id -1 ends the CTA.
+  // tile t = (mb, nb), nb fastest
+  int* tq = reinterpret_cast<int*>(tmem_slot + 4);  // [8]
   if (warp == 0) {
     if (lane == 0) {
-      for (int kb = 0; kb < kblocks; ++kb) {
-        const int s = kb % STAGES;
-        if (kb >= STAGES) mbar_wait(&empty[s], ((kb / STAGES) - 1) & 1);
-        mbar_arrive_tx(&full[s], kStageBytes);
-        tma_load_2d(sA + s * BM * BK * 2, &tmA, kb * BK, mb * BM, &full[s]);
-        tma_load_2d(sB + s * BN * BK * 2, &tmB, kb * BK, nb * BN, &full[s]);
+      int g = 0;  // k-block counter across tiles (stage ring position)
+      for (int it = 0;; ++it) {
+        long long tl = (long long)(atomicAdd(tile_ctr, 1ull) - tile_base);
+        const int t = tl < n_tiles ? (int)tl : -1;
+        tq[it & 7] = t;
+        if (t < 0) {  // sentinel stage: no data, wakes the MMA lane
+          const int s = g % STAGES;
+          if (g >= STAGES) mbar_wait(&empty[s], ((g / STAGES) - 1) & 1);
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&full[s])) : "memory");
+          break;
+        }
+        const int mb = t / n_nb, nb = t - mb * n_nb;
+        for (int kb = 0; kb < kblocks; ++kb, ++g) {
+          const int s = g % STAGES;
+          if (g >= STAGES) mbar_wait(&empty[s], ((g / STAGES) - 1) & 1);
+          mbar_arrive_tx(&full[s], kStageBytes);
+          tma_load_2d(sA + s * BM * BK * 2, &tmA, kb * BK, mb * BM, &full[s]);
+#pragma unroll
+          for (int r = 0; r < BN / 128; ++r)  // the operand maps use 128-row boxes
+            tma_load_2d(sB + s * BN * BK * 2 + r * 128 * BK * 2, &tmB, kb * BK, nb * BN + r * 128, &full[s]);
+        }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      for (int kb = 0; kb < kblocks; ++kb) {
-        const int s = kb % STAGES;
-        mbar_wait(&full[s], (kb / STAGES) & 1);
+      int g = 0;
+      for (int it = 0;; ++it) {
+        const int acc = it & 1;
+        mbar_wait(&full[g % STAGES], (g / STAGES) & 1);  // first stage of tile `it` (or the sentinel)
+        const int t = tq[it & 7];
+        // accumulator `acc` must be drained before its barrier moves again
+        // (also for the sentinel: two unobserved phases would alias the parity)
+        if (it >= 2) mbar_wait(&tempty[acc], ((it >> 1) - 1) & 1);
+        if (t < 0) {
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tfull[acc])) : "memory");
+          break;
+        }
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint64_t da = smem_desc(smem_u32(sA + s * BM * BK * 2));
-        const uint64_t db = smem_desc(smem_u32(sB + s * BN * BK * 2));
+        const uint32_t dt = tmem + acc * kTmemCols;
+        for (int kb = 0; kb < kblocks; ++kb, ++g) {
+          const int s = g % STAGES;
+          if (kb > 0) mbar_wait(&full[s], (g / STAGES) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint64_t da = smem_desc(smem_u32(sA + s * BM * BK * 2));
+          const uint64_t db = smem_desc(smem_u32(sB + s * BN * BK * 2));
 #pragma unroll
-        for (int k = 0; k < BK / 16; ++k)  // 16 bf16 = 32 bytes = 2 descriptor units per step
-          mma_bf16(tmem, da + 2 * k, db + 2 * k, (kb | k) != 0);
-        mma_commit(&empty[s]);
+          for (int k = 0; k < BK / 16; ++k)  // 16 bf16 = 32 bytes = 2 descriptor units per step
+            mma_bf16(dt, da + 2 * k, db + 2 * k, (kb | k) != 0);
+          mma_commit(&empty[s]);
+        }
+        mma_commit(&tfull[acc]);
       }
-      mma_commit(tfull);
     }
     __syncwarp();
   } else {
     // ---------------- epilogue: warps 2..5 own TMEM lane quarters (warp % 4)
     const int quarter = warp & 3;
-    const int row = mb * BM + quarter * 32 + lane;
-    mbar_wait(tfull, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    float v[BN];
-    const uint32_t tbase = tmem + ((uint32_t)(quarter * 32) << 16);
+    for (int it = 0;; ++it) {
+      const int acc = it & 1;
+      mbar_wait(&tfull[acc], (it >> 1) & 1);
+      const int t = tq[it & 7];
+      if (t < 0) break;
+      const int mb = t / n_nb, nb = t - mb * n_nb;
+      const int row = mb * BM + quarter * 32 + lane;
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t tbase = tmem + acc * kTmemCols + ((uint32_t)(quarter * 32) << 16);
+#pragma unroll 1
+      for (int h = 0; h < BN / EN; ++h) {
+        float v[EN];
 #pragma unroll
-    for (int c = 0; c < BN / 32; ++c) tmem_ld32(tbase + c * 32, v + c * 32);
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-    if (row < M) {
-      const int n0 = nb * BN;
-      if constexpr (EPI == TC_EPI_STORE) {
-        float4* y = reinterpret_cast<float4*>(ep.y + (long long)row * ep.ldy + n0);
-#pragma unroll
-        for (int i = 0; i < BN / 4; ++i) {
-          float4 o = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-          if (ep.accumulate) {
-            const float4 a = y[i];
-            o.x += a.x;
-            o.y += a.y;
-            o.z += a.z;
-            o.w += a.w;
-          }
-          y[i] = o;
+        for (int c = 0; c < EN / 32; ++c) tmem_ld32(tbase + h * EN + c * 32, v + c * 32);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (h == BN / EN - 1) {  // accumulator fully read: the MMA warp may reuse it
+          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+          __syncwarp();
+          if (lane == 0)
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tempty[acc])) : "memory");
         }
-      } else if constexpr (EPI == TC_EPI_ROPE_KV) {
-        const RowDesc rd = ep.rows[row];
-        constexpr int half = DH / 2;
-        const float2* cs = reinterpret_cast<const float2*>(ep.rope) + (long long)row * half;
+        const int n0 = nb * BN + h * EN;
+        if (n0 >= N) continue;  // partial last N tile (its B rows were zero-filled)
+        const int row0 = mb * BM + quarter * 32;  // this warp's 32 rows
+        if constexpr (EPI == TC_EPI_LSE) {
+          if (row < M) {
+            float mx = -INFINITY, sm = 0.f;
+            int mi = 0;
+            const int lim = min(EN, ep.V - n0);
 #pragma unroll
-        for (int h0 = 0; h0 < BN; h0 += DH) {
-          const int head = (n0 + h0) / DH;
-          if (head < ep.H + ep.KVH) {
-            // rotate-half RoPE on (x[i], x[i + half])
+            for (int i = 0; i < EN; ++i) {
+              if (i < lim) {
+                sm += v[i];
+                if (v[i] > mx) {
+                  mx = v[i];
+                  mi = i;
+                }
+              }
+            }
+            float se = 0.f;
+            const float ml2 = mx * 1.4426950408889634f;
 #pragma unroll
-            for (int i = 0; i < half; ++i) {
-              const float2 c = cs[i];
-              const float a = v[h0 + i], b = v[h0 + half + i];
-              v[h0 + i] = a * c.x - b * c.y;
-              v[h0 + half + i] = a * c.y + b * c.x;
+            for (int i = 0; i < EN; ++i)
+              if (i < lim) se += exp2f(fmaf(v[i], 1.4426950408889634f, -ml2));
+            reinterpret_cast<float4*>(ep.part)[(long long)row * ep.n_tiles + n0 / EN] =
+                make_float4(mx, se, sm, __int_as_float(n0 + mi));
+          }
+          continue;
+        }
+        // per-row transform in registers (thread = row)
+        if constexpr (EPI == TC_EPI_ROPE_KV) {
+          constexpr int half = DH / 2;
+          const float2* cs = reinterpret_cast<const float2*>(ep.rope) + (long long)(row < M ? row : 0) * half;
+#pragma unroll
+          for (int h0 = 0; h0 < EN; h0 += DH) {
+            const int head = (n0 + h0) / DH;
+            if (head < ep.H + ep.KVH) {  // rotate-half RoPE on (x[i], x[i + half]); Q also scaled
+              const float sc = head < ep.H ? ep.qscale : 1.f;
+#pragma unroll
+              for (int i = 0; i < half; ++i) {
+                const float2 c = cs[i];
+                const float a = v[h0 + i], b = v[h0 + half + i];
+                v[h0 + i] = (a * c.x - b * c.y) * sc;
+                v[h0 + half + i] = (a * c.y + b * c.x) * sc;
+              }
             }
           }
-          if (head < ep.H) {
-            float4* q = reinterpret_cast<float4*>(ep.Qr + ((long long)row * ep.H + head) * DH);
+        } else if constexpr (EPI == TC_EPI_SWIGLU) {
+          // chunk n0: columns [0,64) gate j, [64,128) up j for j in [n0/2, n0/2 + 64)
 #pragma unroll
-            for (int i = 0; i < DH / 4; ++i)
-              q[i] = make_float4(v[h0 + 4 * i] * ep.qscale, v[h0 + 4 * i + 1] * ep.qscale,
-                                 v[h0 + 4 * i + 2] * ep.qscale, v[h0 + 4 * i + 3] * ep.qscale);
-          } else {
-            const bool is_k = head < ep.H + ep.KVH;
-            const int kh = is_k ? head - ep.H : head - ep.H - ep.KVH;
-            __nv_bfloat16* dst =
-                reinterpret_cast<__nv_bfloat16*>(is_k ? ep.Kp : ep.Vp) + ((long long)kh * ep.slots + rd.slot) * DH;
-            uint4* d4 = reinterpret_cast<uint4*>(dst);
-#pragma unroll
-            for (int i = 0; i < DH / 8; ++i)
-              d4[i] = make_uint4(pack2(v[h0 + 8 * i], v[h0 + 8 * i + 1]), pack2(v[h0 + 8 * i + 2], v[h0 + 8 * i + 3]),
-                                 pack2(v[h0 + 8 * i + 4], v[h0 + 8 * i + 5]),
-                                 pack2(v[h0 + 8 * i + 6], v[h0 + 8 * i + 7]));
+          for (int i = 0; i < EN / 2; ++i) {
+            const float g = v[i], u = v[EN / 2 + i];
+            v[i] = g / (1.f + __expf(-g)) * u;
           }
         }
-      } else if constexpr (EPI == TC_EPI_SWIGLU) {
-        // tile nb: columns [0,64) gate j, [64,128) up j for j in [64 nb, 64 nb + 64)
-        uint4* a4 = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(ep.act) + (long long)row * ep.F + nb * (BN / 2));
+        // stage the warp's 32 x EN block in shared memory, then write it out
+        // row by row with the lanes along the columns (512 B per instruction)
+        float* buf = stage_out + (warp - 2) * 32 * kStageLd;
+        constexpr int NW = EPI == TC_EPI_SWIGLU ? EN / 2 : EN;  // columns written
 #pragma unroll
-        for (int i = 0; i < BN / 16; ++i) {
-          float o[8];
-#pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const float g = v[8 * i + e], u = v[BN / 2 + 8 * i + e];
-            o[e] = g / (1.f + __expf(-g)) * u;
-          }
-          a4[i] = make_uint4(pack2(o[0], o[1]), pack2(o[2], o[3]), pack2(o[4], o[5]), pack2(o[6], o[7]));
-        }
-      } else {  // TC_EPI_LSE
-        float mx = -INFINITY, sm = 0.f;
-        int mi = 0;
-        const int lim = min(BN, ep.V - n0);
-#pragma unroll
-        for (int i = 0; i < BN; ++i) {
-          if (i < lim) {
-            sm += v[i];
-            if (v[i] > mx) {
-              mx = v[i];
-              mi = i;
+        for (int i = 0; i < NW / 4; ++i)
+          *reinterpret_cast<float4*>(buf + lane * kStageLd + 4 * i) =
+              make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+        __syncwarp();
+        const int c = 4 * lane;  // this lane's 4 columns of each row
+        for (int r = 0; r < 32; ++r) {
+          const int grow = row0 + r;
+          if (grow >= M) break;
+          if (c >= NW) continue;
+          const float4 o = *reinterpret_cast<const float4*>(buf + r * kStageLd + c);
+          if constexpr (EPI == TC_EPI_STORE) {
+            float4* y = reinterpret_cast<float4*>(ep.y + (long long)grow * ep.ldy + n0 + c);
+            float4 w = o;
+            if (ep.accumulate) {
+              const float4 a = *y;
+              w.x += a.x;
+              w.y += a.y;
+              w.z += a.z;
+              w.w += a.w;
+            }
+            *y = w;
+          } else if constexpr (EPI == TC_EPI_SWIGLU) {
+            *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(ep.act) + (long long)grow * ep.F + n0 / 2 + c) =
+                make_uint2(pack2(o.x, o.y), pack2(o.z, o.w));
+          } else {  // TC_EPI_ROPE_KV
+            const int col = n0 + c, head = col / DH, d0 = col - head * DH;
+            if (head < ep.H) {
+              *reinterpret_cast<float4*>(ep.Qr + ((long long)grow * ep.H + head) * DH + d0) = o;
+            } else {
+              const bool is_k = head < ep.H + ep.KVH;
+              const int kh = is_k ? head - ep.H : head - ep.H - ep.KVH;
+              __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(is_k ? ep.Kp : ep.Vp) +
+                                   ((long long)kh * ep.slots + ep.rows[grow].slot) * DH + d0;
+              *reinterpret_cast<uint2*>(dst) = make_uint2(pack2(o.x, o.y), pack2(o.z, o.w));
             }
           }
         }
-        float se = 0.f;
-        const float ml2 = mx * 1.4426950408889634f;
-#pragma unroll
-        for (int i = 0; i < BN; ++i)
-          if (i < lim) se += exp2f(fmaf(v[i], 1.4426950408889634f, -ml2));
-        reinterpret_cast<float4*>(ep.part)[(long long)row * ep.n_tiles + nb] = make_float4(mx, se, sm, __int_as_float(n0 + mi));
+        __syncwarp();
       }
     }
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tc::kTmemCols));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * tc::kTmemCols));
   }
 }
 
@@ -355,9 +424,38 @@ using namespace spex;
 extern "C" int spex_k_gemm_tc(const CUtensorMap* tmA, const CUtensorMap* tmB, int M, int N, int K,
                               const TcEpilogue* ep, cudaStream_t s) {
   if (M <= 0) return 0;
-  if (N % tc::BN || K % tc::BK) return -1;
-  const size_t smem = tc::STAGES * tc::kStageBytes + 1024 + 256;
-  dim3 grid(N / tc::BN, (M + tc::BM - 1) / tc::BM);
+  if (N % tc::EN || K % tc::BK) return -1;
+  const size_t smem = tc::STAGES * tc::kStageBytes + 1024 + 256 + tc::kEpiBytes;
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int tiles = ((N + tc::BN - 1) / tc::BN) * ((M + tc::BM - 1) / tc::BM);
+  dim3 grid(tiles < sms ? tiles : sms);
+  // per-stream monotone tile counter: launch j claims ids [base_j, base_j + tiles + grid)
+  struct Ctr {
+    cudaStream_t st;
+    unsigned long long* d;
+    unsigned long long base;
+  };
+  static Ctr ctrs[16];
+  static int n_ctrs = 0;
+  Ctr* c = nullptr;
+  for (int i = 0; i < n_ctrs; ++i)
+    if (ctrs[i].st == s) c = &ctrs[i];
+  if (!c) {
+    if (n_ctrs == 16) return -2;
+    c = &ctrs[n_ctrs++];
+    c->st = s;
+    c->base = 0;
+    if (cudaMalloc(&c->d, sizeof(unsigned long long)) != cudaSuccess) return -3;
+    cudaMemsetAsync(c->d, 0, sizeof(unsigned long long), s);
+  }
+  unsigned long long* const tile_ctr = c->d;
+  const unsigned long long tile_base = c->base;
+  c->base += (unsigned long long)tiles + grid.x;
 #define SPEX_TC_LAUNCH(E, D)                                                                               \
   {                                                                                                        \
     static bool attr = false;                                                                              \
@@ -365,7 +463,7 @@ extern "C" int spex_k_gemm_tc(const CUtensorMap* tmA, const CUtensorMap* tmB, in
       cudaFuncSetAttribute(gemm_tc_kernel<E, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);  \
       attr = true;                                                                                         \
     }                                                                                                      \
-    gemm_tc_kernel<E, D><<<grid, tc::kThreads, smem, s>>>(*tmA, *tmB, M, N, K, *ep);                       \
+    gemm_tc_kernel<E, D><<<grid, tc::kThreads, smem, s>>>(*tmA, *tmB, M, N, K, *ep, tile_ctr, tile_base);                       \
     return (int)cudaGetLastError();                                                                        \
   }
   switch (ep->kind) {

@@ -281,10 +281,13 @@ static Model* make_model(const ModelShape& sh, bool prm, uint64_t seed, long lon
     m->lse = dalloc<float>(M, o);
     m->lsum = dalloc<float>(M, o);
   }
-  // K2 on the hand-written tcgen05 GEMM when every projection tiles by 128 x 64
-  // (all shapes here do); SPEX_CUBLAS=1 keeps the cuBLAS + elementwise path.
+  // K2 on the hand-written tcgen05 GEMM with fused epilogues (gemm_tc.cu) is
+  // opt-in (SPEX_TC_GEMM=1): it is correct (tests/test_gemm_tc_gpu.py) and beats
+  // cuBLAS + the separate elementwise kernels per op at decode shapes, but over a
+  // whole search the cuBLAS path is faster (3.2 s vs 3.75 s on c2; small-M steps
+  // and the concurrent PRM stream), so cuBLAS stays the default.
   const int qkv_n = (sh.H + 2 * sh.KVH) * sh.dh;
-  m->use_tc = !getenv("SPEX_CUBLAS") && sh.d % 128 == 0 && sh.d % 64 == 0 && qkv_n % 128 == 0 &&
+  m->use_tc = getenv("SPEX_TC_GEMM") != nullptr && sh.d % 128 == 0 && sh.d % 64 == 0 && qkv_n % 128 == 0 &&
               (sh.H * sh.dh) % 64 == 0 && (2 * sh.F) % 128 == 0 && sh.F % 64 == 0 && (sh.dh == 64 || sh.dh == 128) &&
               (prm || sh.V % 128 == 0);
   if (m->use_tc) {
