@@ -222,8 +222,8 @@ def main():
         if pg:
             pg.barrier()
 
-    def one_search(trace: bool):
-        ex = spex.Executor(cfg_text, seed, None, trace=trace, device=local)
+    def one_search(trace: bool, flags=None):
+        ex = spex.Executor(cfg_text, seed, flags, trace=trace, device=local)
         ex.set_model(args.policy, args.prm, weight_seed=1)
         tot = ex.run()
         d2h = 0
@@ -231,6 +231,7 @@ def main():
             log = ex.log_lines()  # the run's event log, copied back and serialised
             d2h = ex.stats()["log_records"] * 48
         st, ms = ex.stats(), ex.model_stats()
+        ms["p50_latency_virtual_s"] = statistics.median(ex.query_finish_times())
         ex.close()
         return tot, st, ms, d2h
 
@@ -285,6 +286,11 @@ def main():
             e2e_d2h += d2h
         barrier()
         tr_wall = time.perf_counter() - t2
+    # the same search barrier-synchronously (no T1/T2/T3: the reference's
+    # baseline arm, experiment.cpp:68-70), same model work, for the metric's
+    # "vs barrier-synchronous search"
+    bs_tot, bs_st, bs_ms, _ = one_search(False, "")
+    sp_makespan = tot.makespan
     times = torch.tensor([dev_s, wall, e2e_wall, tr_wall], dtype=torch.float64, device="cuda")
     if pg:
         pg.all_reduce(times, op=pg.ReduceOp.MAX)
@@ -331,6 +337,12 @@ def main():
                 "traced": {"value": total_tr_q / tr_wall, "unit": "queries/s",
                            "d2h_bytes_per_step": int(e2e_d2h / args.steps) + 256,
                            "note": "event log copied back and serialised to JSON lines each step"}},
+        "vs_barrier_sync": {"barrier_sync_queries_per_s": bs_tot.queries / (bs_ms["step_ms"] / 1000.0),
+                            "speedup": (total_q / dev_s / world) / (bs_tot.queries / (bs_ms["step_ms"] / 1000.0)),
+                            "virtual_makespan_spex": sp_makespan, "virtual_makespan_barrier_sync": bs_tot.makespan,
+                            "p50_search_latency_virtual_s": {"spex": ms["p50_latency_virtual_s"],
+                                                             "barrier_sync": bs_ms["p50_latency_virtual_s"]},
+                            "note": "one GPU, same config/seed/model, flags '' vs the config's flags"},
         "gpu_launches": int(agg["launches"]),
         "roofline": {"bound": "hbm", "kernel": "K1 tree_attn_kernel (policy decode)",
                      "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",

@@ -127,6 +127,9 @@ int spex_executor_model_stats(spex_executor* ex, spex_model_stats* out);
 /* Copies up to cap records; *n receives the total available. */
 int spex_executor_decode_outputs(spex_executor* ex, void* buf, long long cap, long long* n);
 int spex_executor_prm_outputs(spex_executor* ex, void* buf, long long cap, long long* n);
+/* Per-query virtual finish time (query_done.t; admission is at t = 0 when
+ * batch_size = n_queries): the search latency of each query. */
+int spex_executor_query_finish(spex_executor* ex, double* out, int cap, int* n);
 void spex_executor_destroy(spex_executor* ex);
 
 /* run_once: traced run returning totals and the JSON-lines log. */

@@ -199,6 +199,14 @@ class Executor:
         _check(self._L.spex_executor_prm_outputs(self._h, buf, n.value, ctypes.byref(n)))
         return [(o.q, o.node, o.score) for o in buf[: n.value]]
 
+    def query_finish_times(self) -> list:
+        """Virtual finish time of every query (its search latency when all are admitted at t=0)."""
+        n = ctypes.c_int()
+        cap = 1 << 16
+        buf = (ctypes.c_double * cap)()
+        _check(self._L.spex_executor_query_finish(self._h, buf, cap, ctypes.byref(n)))
+        return list(buf[: min(n.value, cap)])
+
     def close(self) -> None:
         if getattr(self, "_h", None):
             self._L.spex_executor_destroy(self._h)

@@ -115,6 +115,8 @@ _EXPORTS = {
     ),
     "spex_executor_stats": ([ctypes.c_void_p, ctypes.POINTER(Stats)], ctypes.c_int),
     "spex_executor_destroy": ([ctypes.c_void_p], None),
+    "spex_executor_query_finish": (
+        [ctypes.c_void_p, ctypes.POINTER(ctypes.c_double), ctypes.c_int, ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
     "spex_executor_set_model": (
         [ctypes.c_void_p, ctypes.c_char_p, ctypes.c_char_p, ctypes.c_uint64, ctypes.c_int], ctypes.c_int),
     "spex_executor_model_stats": ([ctypes.c_void_p, ctypes.POINTER(ModelStats)], ctypes.c_int),

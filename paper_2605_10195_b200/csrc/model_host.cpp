@@ -51,7 +51,7 @@ void spex_k_prm_scan_all(TreeView t, const int* kind, const int* off, const int*
                          cudaStream_t s);
 void spex_k_embed(const RowDesc* rows, int M, const __nv_bfloat16* E, int d, float* X, cudaStream_t s);
 void spex_k_rmsnorm(const float* X, int M, int d, float eps, __nv_bfloat16* Y, cudaStream_t s);
-void spex_k_rope_kv(const RowDesc* rows, int M, const float* QKV, int H, int KVH, int dh, const float* inv_freq,
+void spex_k_rope_kv(const RowDesc* rows, int M, const __nv_bfloat16* QKV, int H, int KVH, int dh, const float* inv_freq,
                     long long slots, __nv_bfloat16* Kp, __nv_bfloat16* Vp, float* Qr, cudaStream_t s);
 int spex_k_tree_attn(const RowDesc* rows, const Segment* segs, const float* Qr, int H, int KVH, int dh,
                      const __nv_bfloat16* Kp, const __nv_bfloat16* Vp, long long slots, __nv_bfloat16* O, int M,
@@ -60,7 +60,7 @@ void spex_k_build_decode_chunks(const RowDesc* rows, const Segment* segs, int M,
 int spex_k_tree_attn_chunked(const RowDesc* rows, const Segment* segs, const float* Qr, int H, int KVH, int dh,
                              const __nv_bfloat16* Kp, const __nv_bfloat16* Vp, long long slots, __nv_bfloat16* O,
                              DecodeChunks w, int qslot, cudaStream_t s);
-void spex_k_swiglu(const float* GU, int M, int F, __nv_bfloat16* A, cudaStream_t s);
+void spex_k_swiglu(const __nv_bfloat16* GU, int M, int F, __nv_bfloat16* A, cudaStream_t s);
 int spex_k_gemm_tc(const CUtensorMap* tmA, const CUtensorMap* tmB, int M, int N, int K, const TcEpilogue* ep,
                    cudaStream_t s);
 void spex_k_lse_combine(const float* part, int M, int n_tiles, int* amax, float* lse, float* lsum, cudaStream_t s);
@@ -102,6 +102,14 @@ void gemm(cublasHandle_t h, const __nv_bfloat16* x, const __nv_bfloat16* W, floa
   const float alpha = 1.f, beta = accumulate ? 1.f : 0.f;
   CB(cublasGemmEx(h, CUBLAS_OP_T, CUBLAS_OP_N, N, M, K, &alpha, W, CUDA_R_16BF, K, x, CUDA_R_16BF, K, &beta, y,
                   CUDA_R_32F, N, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT));
+}
+
+// y[M x N] (bf16, fp32 accumulate) = x[M x K] (bf16) . W[N x K]^T (bf16)
+void gemm_bf16out(cublasHandle_t h, const __nv_bfloat16* x, const __nv_bfloat16* W, __nv_bfloat16* y, int M, int N,
+                  int K) {
+  const float alpha = 1.f, beta = 0.f;
+  CB(cublasGemmEx(h, CUBLAS_OP_T, CUBLAS_OP_N, N, M, K, &alpha, W, CUDA_R_16BF, K, x, CUDA_R_16BF, K, &beta, y,
+                  CUDA_R_16BF, N, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT));
 }
 
 }  // namespace
@@ -178,10 +186,10 @@ struct Model {
   // activations
   float* X = nullptr;
   __nv_bfloat16* Xn = nullptr;
-  float* QKV = nullptr;
+  __nv_bfloat16* QKV = nullptr;  // bf16 projection outputs feeding RoPE / SwiGLU
   float* Qr = nullptr;
   __nv_bfloat16* O = nullptr;
-  float* GU = nullptr;
+  __nv_bfloat16* GU = nullptr;
   __nv_bfloat16* A = nullptr;
   float* logits = nullptr;
   // tcgen05 path (use_tc): weight maps, activation maps, RoPE table, LM-head partials
@@ -271,10 +279,10 @@ static Model* make_model(const ModelShape& sh, bool prm, uint64_t seed, long lon
   const size_t M = max_rows;
   m->X = dalloc<float>(M * sh.d, o);
   m->Xn = dalloc<__nv_bfloat16>(M * std::max(sh.d, sh.H * sh.dh), o);
-  m->QKV = dalloc<float>(M * (sh.H + 2 * sh.KVH) * sh.dh, o);
+  m->QKV = dalloc<__nv_bfloat16>(M * (sh.H + 2 * sh.KVH) * sh.dh, o);
   m->Qr = dalloc<float>(M * sh.H * sh.dh, o);
   m->O = dalloc<__nv_bfloat16>(M * sh.H * sh.dh, o);
-  m->GU = dalloc<float>(M * 2 * sh.F, o);
+  m->GU = dalloc<__nv_bfloat16>(M * 2 * sh.F, o);
   m->A = dalloc<__nv_bfloat16>(M * sh.F, o);
   if (!prm) {
     m->amax = dalloc<int>(M, o);
@@ -398,7 +406,7 @@ static void forward(Model& m, const RowDesc* rows, const Segment* segs, int M, c
   spex_k_embed(rows, M, m.embed, s.d, m.X, st);
   for (int l = 0; l < s.L; ++l) {
     spex_k_rmsnorm(m.X, M, s.d, s.eps, m.Xn, st);
-    gemm(hb, m.Xn, m.wqkv[l], m.QKV, M, (s.H + 2 * s.KVH) * s.dh, s.d, false);
+    gemm_bf16out(hb, m.Xn, m.wqkv[l], m.QKV, M, (s.H + 2 * s.KVH) * s.dh, s.d);
     spex_k_rope_kv(rows, M, m.QKV, s.H, s.KVH, s.dh, m.inv_freq, m.slots, m.Kp[l], m.Vp[l], m.Qr, st);
     if (timer) timer->begin(st);
     int rc = -1;
@@ -416,7 +424,7 @@ static void forward(Model& m, const RowDesc* rows, const Segment* segs, int M, c
     if (timer) timer->end(st);
     gemm(hb, m.O, m.wo[l], m.X, M, s.d, s.H * s.dh, true);
     spex_k_rmsnorm(m.X, M, s.d, s.eps, m.Xn, st);
-    gemm(hb, m.Xn, m.wgu[l], m.GU, M, 2 * s.F, s.d, false);
+    gemm_bf16out(hb, m.Xn, m.wgu[l], m.GU, M, 2 * s.F, s.d);
     spex_k_swiglu(m.GU, M, s.F, m.A, st);
     gemm(hb, m.A, m.wd[l], m.X, M, s.d, s.F, true);
   }

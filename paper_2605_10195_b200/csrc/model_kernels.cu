@@ -273,17 +273,17 @@ __global__ void rmsnorm_bf16_kernel(const float* X, int M, int d, float eps, __n
 // RoPE on q and k at the row's absolute position; append k, v (bf16) to the
 // layer's KV pool at the row's slot; q (fp32, pre-scaled by 1/sqrt(dh)) to Qr.
 // Pools are [KVH][slots][dh].
-__global__ void rope_kv_kernel(const RowDesc* rows, int M, const float* QKV, int H, int KVH, int dh,
+__global__ void rope_kv_kernel(const RowDesc* rows, int M, const __nv_bfloat16* QKV, int H, int KVH, int dh,
                                const float* inv_freq, long long slots, __nv_bfloat16* Kp, __nv_bfloat16* Vp,
                                float* Qr) {
-  // one block per row; rotate-half RoPE on (x[i], x[i+half]) pairs two at a time
-  // (float2), V copied 4 at a time
+  // one block per row; rotate-half RoPE on (x[i], x[i+half]) pairs two at a
+  // time from the bf16 projection output; V copied 8 bytes at a time
   const int r = blockIdx.x;
   if (r >= M) return;
   __shared__ float sc[128], ss[128];
   const RowDesc rd = rows[r];
   const int width = (H + 2 * KVH) * dh;
-  const float* src = QKV + (long long)r * width;
+  const __nv_bfloat16* src = QKV + (long long)r * width;
   const int half = dh / 2;
   const float qscale = rsqrtf((float)dh);
   for (int i = threadIdx.x; i < half; i += blockDim.x) {
@@ -293,16 +293,17 @@ __global__ void rope_kv_kernel(const RowDesc* rows, int M, const float* QKV, int
     ss[i] = sn;
   }
   __syncthreads();
-  const int hp = half / 2;  // float2 pairs per half
+  const int hp = half / 2;  // bf16 pairs per half
   for (int idx = threadIdx.x; idx < (H + KVH) * hp; idx += blockDim.x) {
     const int head = idx / hp;
     const int i = (idx - head * hp) * 2;
-    const float* x = src + head * dh;
-    const float2 a = *reinterpret_cast<const float2*>(x + i);
-    const float2 b = *reinterpret_cast<const float2*>(x + i + half);
+    const __nv_bfloat16* x = src + head * dh;
+    const __nv_bfloat162 a2 = *reinterpret_cast<const __nv_bfloat162*>(x + i);
+    const __nv_bfloat162 b2 = *reinterpret_cast<const __nv_bfloat162*>(x + i + half);
+    const float ax = __low2float(a2), ay = __high2float(a2), bx = __low2float(b2), by = __high2float(b2);
     const float c0 = sc[i], c1 = sc[i + 1], s0 = ss[i], s1 = ss[i + 1];
-    const float ya0 = a.x * c0 - b.x * s0, ya1 = a.y * c1 - b.y * s1;
-    const float yb0 = a.x * s0 + b.x * c0, yb1 = a.y * s1 + b.y * c1;
+    const float ya0 = ax * c0 - bx * s0, ya1 = ay * c1 - by * s1;
+    const float yb0 = ax * s0 + bx * c0, yb1 = ay * s1 + by * c1;
     if (head < H) {
       float* qd = Qr + ((long long)r * H + head) * dh;
       *reinterpret_cast<float2*>(qd + i) = make_float2(ya0 * qscale, ya1 * qscale);
@@ -314,15 +315,12 @@ __global__ void rope_kv_kernel(const RowDesc* rows, int M, const float* QKV, int
       *reinterpret_cast<uint32_t*>(kd + i + half) = pack_bf16(yb0, yb1);
     }
   }
-  const float* vs = src + (H + KVH) * dh;
+  const __nv_bfloat16* vs = src + (H + KVH) * dh;
   for (int idx = threadIdx.x; idx < KVH * dh / 4; idx += blockDim.x) {
     const int e = idx * 4;
     const int kh = e / dh, i = e - kh * dh;
-    const float4 v = *reinterpret_cast<const float4*>(vs + e);
-    uint2 o;
-    o.x = pack_bf16(v.x, v.y);
-    o.y = pack_bf16(v.z, v.w);
-    *reinterpret_cast<uint2*>(Vp + ((long long)kh * slots + rd.slot) * dh + i) = o;
+    *reinterpret_cast<uint2*>(Vp + ((long long)kh * slots + rd.slot) * dh + i) =
+        *reinterpret_cast<const uint2*>(vs + e);
   }
 }
 
@@ -1386,19 +1384,23 @@ __global__ void __launch_bounds__(kAttnThreads) tree_attn_tile_kernel(const Tile
   }
 }
 
-__global__ void swiglu_kernel(const float* GU, int M, int F, __nv_bfloat16* A) {
-  // flat grid-stride over M * F/4 quads (F % 4 == 0)
+__global__ void swiglu_kernel(const __nv_bfloat16* GU, int M, int F, __nv_bfloat16* A) {
+  // flat grid-stride over M * F/4 quads (F % 4 == 0), bf16 gate/up in
   const int F4 = F / 4;
   const long long n = (long long)M * F4;
   for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x) {
     const long long r = k / F4;
     const int j = (int)(k - r * F4) * 4;
-    const float* g = GU + r * 2 * F;
-    const float4 gv = *reinterpret_cast<const float4*>(g + j);
-    const float4 uv = *reinterpret_cast<const float4*>(g + F + j);
+    const __nv_bfloat16* g = GU + r * 2 * F;
+    const uint2 gr = *reinterpret_cast<const uint2*>(g + j);
+    const uint2 ur = *reinterpret_cast<const uint2*>(g + F + j);
+    const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&gr);
+    const __nv_bfloat162* u2 = reinterpret_cast<const __nv_bfloat162*>(&ur);
+    float gv[4] = {__low2float(g2[0]), __high2float(g2[0]), __low2float(g2[1]), __high2float(g2[1])};
+    float uv[4] = {__low2float(u2[0]), __high2float(u2[0]), __low2float(u2[1]), __high2float(u2[1])};
     uint2 o;
-    o.x = pack_bf16(gv.x / (1.f + __expf(-gv.x)) * uv.x, gv.y / (1.f + __expf(-gv.y)) * uv.y);
-    o.y = pack_bf16(gv.z / (1.f + __expf(-gv.z)) * uv.z, gv.w / (1.f + __expf(-gv.w)) * uv.w);
+    o.x = pack_bf16(gv[0] / (1.f + __expf(-gv[0])) * uv[0], gv[1] / (1.f + __expf(-gv[1])) * uv[1]);
+    o.y = pack_bf16(gv[2] / (1.f + __expf(-gv[2])) * uv[2], gv[3] / (1.f + __expf(-gv[3])) * uv[3]);
     *reinterpret_cast<uint2*>(A + r * F + j) = o;
   }
 }
@@ -1545,7 +1547,7 @@ extern "C" void spex_k_rmsnorm(const float* X, int M, int d, float eps, __nv_bfl
   rmsnorm_bf16_kernel<<<(M + 7) / 8, 256, 0, s>>>(X, M, d, eps, Y);
 }
 
-extern "C" void spex_k_rope_kv(const RowDesc* rows, int M, const float* QKV, int H, int KVH, int dh,
+extern "C" void spex_k_rope_kv(const RowDesc* rows, int M, const __nv_bfloat16* QKV, int H, int KVH, int dh,
                                const float* inv_freq, long long slots, __nv_bfloat16* Kp, __nv_bfloat16* Vp,
                                float* Qr, cudaStream_t s) {
   rope_kv_kernel<<<M, 128, 0, s>>>(rows, M, QKV, H, KVH, dh, inv_freq, slots, Kp, Vp, Qr);
@@ -1710,7 +1712,7 @@ extern "C" int spex_k_tree_attn_tiles(const TileDesc* tiles, int ntiles, const R
   return -1;
 }
 
-extern "C" void spex_k_swiglu(const float* GU, int M, int F, __nv_bfloat16* A, cudaStream_t s) {
+extern "C" void spex_k_swiglu(const __nv_bfloat16* GU, int M, int F, __nv_bfloat16* A, cudaStream_t s) {
   const long long quads = (long long)M * (F / 4);
   const int blocks = (int)std::min<long long>((quads + 255) / 256, 148 * 16);
   swiglu_kernel<<<blocks, 256, 0, s>>>(GU, M, F, A);

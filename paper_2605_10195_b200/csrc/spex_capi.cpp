@@ -1242,6 +1242,14 @@ int spex_executor_prm_outputs(spex_executor* ex, void* buf, long long cap, long 
   });
 }
 
+int spex_executor_query_finish(spex_executor* ex, double* out, int cap, int* n) {
+  return guarded([&] {
+    const int q = static_cast<int>(ex->qs.size());
+    for (int i = 0; i < q && i < cap; ++i) out[i] = ex->qs[i].finish_time;
+    *n = q;
+  });
+}
+
 void spex_executor_destroy(spex_executor* ex) {
 #ifndef SPEX_EMU
   if (ex && ex->stream) cudaStreamDestroy(ex->stream);
