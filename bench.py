@@ -289,6 +289,7 @@ def main():
     # the same search barrier-synchronously (no T1/T2/T3: the reference's
     # baseline arm, experiment.cpp:68-70), same model work, for the metric's
     # "vs barrier-synchronous search"
+    one_search(False, "")  # warm-up (its own schedule shapes)
     bs_tot, bs_st, bs_ms, _ = one_search(False, "")
     sp_makespan = tot.makespan
     times = torch.tensor([dev_s, wall, e2e_wall, tr_wall], dtype=torch.float64, device="cuda")
@@ -342,7 +343,11 @@ def main():
                             "virtual_makespan_spex": sp_makespan, "virtual_makespan_barrier_sync": bs_tot.makespan,
                             "p50_search_latency_virtual_s": {"spex": ms["p50_latency_virtual_s"],
                                                              "barrier_sync": bs_ms["p50_latency_virtual_s"]},
-                            "note": "one GPU, same config/seed/model, flags '' vs the config's flags"},
+                            "barrier_sync_decode_steps": bs_ms["decode_steps"],
+                            "barrier_sync_decode_rows": bs_ms["decode_rows"],
+                            "spex_decode_steps": ms["decode_steps"], "spex_decode_rows": ms["decode_rows"],
+                            "note": "one GPU, same config/seed/model, flags '' vs the config's flags; "
+                                    "device step time of one warm search each"},
         "gpu_launches": int(agg["launches"]),
         "roofline": {"bound": "hbm", "kernel": "K1 tree_attn_kernel (policy decode)",
                      "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
