@@ -148,6 +148,11 @@ static bool make_kv_tmap(CUtensorMap* m, void* base, long long rows, int dh) {
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// TMA descriptor of one layer's tree-KV pool for the tile attention kernel.
+extern "C" int spex_tmap_kv(CUtensorMap* m, void* base, long long rows, int dh) {
+  return make_kv_tmap(m, base, rows, dh) ? 0 : -1;
+}
+
 // TMA descriptor of a row-major bf16 matrix [rows][cols] as a GEMM operand of
 // gemm_tc.cu: 64 x 128 (cols x rows) boxes, 128-byte swizzle.
 extern "C" int spex_tmap_operand(CUtensorMap* m, const void* base, long long rows, long long cols) {

@@ -968,7 +968,9 @@ __global__ void __launch_bounds__(128) tree_attn_tile_mma_kernel(const __grid_co
                                                                 const RowDesc* __restrict__ rows,
                                                                 const Segment* __restrict__ segs,
                                                                 const float* __restrict__ Qr, int H, long long slots,
-                                                                __nv_bfloat16* __restrict__ O) {
+                                                                __nv_bfloat16* __restrict__ O, int Gt) {
+  // G query heads per block; a KV head's Gt heads are split over Gt / G blocks
+  // (blockIdx.y = kh * (Gt / G) + part), e.g. Gt = 6 -> 3 blocks of 2 heads
   constexpr int DH = 128;
   constexpr int SPLIT = 4 / G;          // warps per head
   constexpr int TW = kChunk / SPLIT;    // tokens per warp per chunk (16, 32 or 64)
@@ -980,7 +982,8 @@ __global__ void __launch_bounds__(128) tree_attn_tile_mma_kernel(const __grid_co
   __shared__ int sPos[kTileRows];
   __shared__ float sMl[4][2][kTileRows];  // per warp: m, l per row
   const TileDesc td = tiles[blockIdx.x];
-  const int kh = blockIdx.y;
+  const int parts = Gt / G;
+  const int kh = blockIdx.y / parts, hbase = kh * Gt + (blockIdx.y - kh * parts) * G;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = warp / SPLIT, slice = warp % SPLIT;
   const RowDesc last = rows[td.row0 + td.nrows - 1];
@@ -1000,8 +1003,8 @@ __global__ void __launch_bounds__(128) tree_attn_tile_mma_kernel(const __grid_co
   {
     const int r0 = gq, r1 = gq + 8;
     const bool v0 = r0 < td.nrows, v1 = r1 < td.nrows;
-    const float* q0 = Qr + ((long long)(td.row0 + (v0 ? r0 : 0)) * H + kh * G + g) * DH;
-    const float* q1 = Qr + ((long long)(td.row0 + (v1 ? r1 : 0)) * H + kh * G + g) * DH;
+    const float* q0 = Qr + ((long long)(td.row0 + (v0 ? r0 : 0)) * H + hbase + g) * DH;
+    const float* q1 = Qr + ((long long)(td.row0 + (v1 ? r1 : 0)) * H + hbase + g) * DH;
     const float sc = 1.4426950408889634f;
 #pragma unroll
     for (int ks = 0; ks < 8; ++ks) {
@@ -1202,7 +1205,7 @@ __global__ void __launch_bounds__(128) tree_attn_tile_mma_kernel(const __grid_co
         const float mw = sMl[w][0][row];
         Lr += (mw == -INFINITY) ? 0.f : sMl[w][1][row] * exp2f(mw - Mr);
       }
-      O[((long long)(td.row0 + row) * H + kh * G + g) * DH + col] = __float2bfloat16_rn(acc / Lr);
+      O[((long long)(td.row0 + row) * H + hbase + g) * DH + col] = __float2bfloat16_rn(acc / Lr);
     }
   }
   (void)L0;
@@ -1643,6 +1646,7 @@ extern "C" int spex_k_tree_attn_chunked(const RowDesc* rows, const Segment* segs
   SPEX_CHUNK_CASE(128, 1)
   SPEX_CHUNK_CASE(128, 2)
   SPEX_CHUNK_CASE(128, 4)
+  SPEX_CHUNK_CASE(128, 6)
   SPEX_CHUNK_CASE(128, 8)
   SPEX_CHUNK_CASE(64, 1)
   SPEX_CHUNK_CASE(64, 2)
@@ -1671,18 +1675,19 @@ extern "C" int spex_k_tree_attn_tiles_mma(const CUtensorMap* kmap, const CUtenso
                                           int KVH, int dh, long long slots, __nv_bfloat16* O, cudaStream_t s) {
   const int G = H / KVH;
   if (ntiles <= 0) return 0;
-  if (dh != 128 || (G != 1 && G != 2 && G != 4)) return -1;
+  if (dh != 128 || G < 1) return -1;
+  const int Gs = G % 4 == 0 ? 4 : (G % 2 == 0 ? 2 : 1);  // heads per block
   const size_t smem = 2 * 32768 + 1024;
-  dim3 grid(ntiles, KVH);
+  dim3 grid(ntiles, KVH * (G / Gs));
 #define SPEX_MMA_CASE(GG)                                                                             \
-  if (G == GG) {                                                                                     \
+  if (Gs == GG) {                                                                                    \
     static bool attr = false;                                                                        \
     if (!attr) {                                                                                     \
       cudaFuncSetAttribute(tree_attn_tile_mma_kernel<GG>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                            (int)smem);                                                               \
       attr = true;                                                                                   \
     }                                                                                                \
-    tree_attn_tile_mma_kernel<GG><<<grid, 128, smem, s>>>(*kmap, *vmap, tiles, rows, segs, Qr, H, slots, O); \
+    tree_attn_tile_mma_kernel<GG><<<grid, 128, smem, s>>>(*kmap, *vmap, tiles, rows, segs, Qr, H, slots, O, G); \
     return 0;                                                                                        \
   }
   SPEX_MMA_CASE(1)

@@ -6,9 +6,9 @@ list of KV segments (its ancestors' thoughts root-first, then its own prefix),
 segments shared between rows as siblings share ancestors. The reference
 gathers each row's K/V in fp32 and computes softmax(q.K^T).V.
 
-Tolerance (stated): the kernel takes q and p in bf16 (like the tensor-core tile
-kernel's mma operands) and writes O in bf16, so |O - O_ref| <= 1.5e-2 elementwise
-and mean |O - O_ref| <= 2e-3 for O of unit scale.
+Tolerance (stated): the kernels take q and p in bf16 (the tensor-core tile
+kernel's mma operands, the decode kernel's FHFMA operands) and write O in bf16,
+so |O - O_ref| <= 2e-2 (1 + |O_ref|) elementwise and mean |O - O_ref| <= 2e-3.
 """
 import ctypes
 
@@ -82,7 +82,7 @@ def _make_tree_rows(rng, M, slots, max_depth):
 
 
 @pytest.mark.parametrize("impl", ["row", "chunked"])
-@pytest.mark.parametrize("H,KVH,dh,M", [(8, 8, 128, 300), (32, 8, 128, 97), (4, 2, 64, 150), (16, 4, 64, 64)])
+@pytest.mark.parametrize("H,KVH,dh,M", [(8, 8, 128, 300), (32, 8, 128, 97), (12, 2, 128, 80), (4, 2, 64, 150), (16, 4, 64, 64)])
 def test_k1_decode_matches_torch_fp32(H, KVH, dh, M, impl):
     """impl "row": one warp per (row, kv head) (spex_k_tree_attn); "chunked": the
     decode work list (spex_k_build_decode_chunks + spex_k_tree_attn_chunked),
@@ -137,8 +137,90 @@ def test_k1_decode_matches_torch_fp32(H, KVH, dh, M, impl):
             p = torch.softmax(s, dim=0)
             ref = p @ Vf[kh, idx]
             d = (O[r, h].float() - ref).abs()
-            worst = max(worst, d.max().item())
+            worst = max(worst, (d / (1.0 + ref.abs())).max().item())
             tot += d.sum().item()
             cnt += d.numel()
-    assert worst <= 1.5e-2, worst
+    assert worst <= 2e-2, worst
     assert tot / cnt <= 2e-3, tot / cnt
+
+
+TILE = np.dtype([("row0", "<i4"), ("nrows", "<i4")])
+
+
+@pytest.mark.parametrize("H,KVH", [(8, 8), (16, 8), (32, 8), (12, 2)])
+def test_k1_tile_mma_matches_torch_fp32(H, KVH):
+    """PRM / prompt rows: 16 consecutive positions of one thought share one pass
+    over their context (TMA-staged 64-token chunks, mma.sync), the own segment
+    causally masked per row; GQA group sizes 1, 2, 4 and 6 (12/2, the 1.5B PRM)."""
+    import torch
+    import paper_2605_10195_b200 as spex
+    from paper_2605_10195_b200 import _lib as L
+    if not spex.device_ok():
+        pytest.fail("no sm_100 device")
+    lib = L.lib()
+    lib.spex_tmap_kv.restype = ctypes.c_int
+    lib.spex_tmap_kv.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_longlong, ctypes.c_int]
+    f = lib.spex_k_tree_attn_tiles_mma
+    f.restype = ctypes.c_int
+    f.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
+                  ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_longlong, ctypes.c_void_p,
+                  ctypes.c_void_p]
+    dh = 128
+    rng = np.random.default_rng(H + KVH)
+    n_nodes = 24
+    lens = rng.integers(8, 150, size=n_nodes)
+    bases = np.concatenate([[0], np.cumsum(lens)[:-1]])
+    slots = int(bases[-1] + lens[-1]) + 64
+    parent = np.full(n_nodes, -1)
+    for i in range(1, n_nodes):
+        parent[i] = rng.integers(0, i)
+    rows, segs, tiles, ctx = [], [], [], []
+    for node in rng.choice(n_nodes, size=6, replace=False):
+        chain, c = [], parent[node]
+        while c >= 0:
+            chain.append(c)
+            c = parent[c]
+        anc = [(int(bases[a]), int(lens[a])) for a in chain[::-1]]
+        n = int(lens[node])
+        for j0 in range(0, n, 16):
+            tiles.append((len(rows), min(16, n - j0)))
+            for j in range(j0, min(n, j0 + 16)):
+                sl = anc + [(int(bases[node]), j + 1)]
+                rows.append((0, node, j, 0, int(bases[node]) + j, len(rows) * MAX_SEG, len(sl), 0, 0))
+                segs.append(sl)
+                ctx.append(sl)
+    M = len(rows)
+    rows_np = np.array(rows, ROW)
+    segs_np = np.zeros(M * MAX_SEG, SEG)
+    for r, sl in enumerate(segs):
+        for k, (b, n) in enumerate(sl):
+            segs_np[r * MAX_SEG + k] = (b, n, 0)
+    tiles_np = np.array(tiles, TILE)
+    dev = torch.device("cuda", 0)
+    g = torch.Generator(device="cpu").manual_seed(H * 7 + KVH)
+    K = torch.randn(KVH, slots, dh, generator=g).to(torch.bfloat16).to(dev)
+    V = torch.randn(KVH, slots, dh, generator=g).to(torch.bfloat16).to(dev)
+    Q = (torch.randn(M, H, dh, generator=g) * 2.0 / dh ** 0.5).to(dev)
+    O = torch.zeros(M, H, dh, dtype=torch.bfloat16, device=dev)
+    bufs = [torch.from_numpy(a.view(np.uint8).copy()).to(dev) for a in (rows_np, segs_np, tiles_np)]
+    km, vm = ctypes.create_string_buffer(256), ctypes.create_string_buffer(256)
+    kp = (ctypes.addressof(km) + 63) & ~63
+    vp = (ctypes.addressof(vm) + 63) & ~63
+    assert lib.spex_tmap_kv(kp, K.data_ptr(), KVH * slots, dh) == 0
+    assert lib.spex_tmap_kv(vp, V.data_ptr(), KVH * slots, dh) == 0
+    st = torch.cuda.current_stream(dev)
+    rc = f(kp, vp, bufs[2].data_ptr(), len(tiles), bufs[0].data_ptr(), bufs[1].data_ptr(), Q.data_ptr(), H, KVH, dh,
+           slots, O.data_ptr(), st.cuda_stream)
+    assert rc == 0
+    torch.cuda.synchronize()
+    Kf, Vf = K.float(), V.float()
+    G = H // KVH
+    worst = 0.0
+    for r in range(M):
+        idx = torch.cat([torch.arange(b, b + n) for b, n in ctx[r]]).to(dev)
+        for h in range(H):
+            kh = h // G
+            p = torch.softmax(Kf[kh, idx] @ Q[r, h], dim=0)
+            ref = p @ Vf[kh, idx]
+            worst = max(worst, ((O[r, h].float() - ref).abs() / (1.0 + ref.abs())).max().item())
+    assert worst <= 2e-2, worst
