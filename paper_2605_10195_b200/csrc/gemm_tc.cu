@@ -26,6 +26,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <cstdlib>
 
 #include "model.h"
 
@@ -433,7 +434,9 @@ extern "C" int spex_k_gemm_tc(const CUtensorMap* tmA, const CUtensorMap* tmB, in
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
   const int tiles = ((N + tc::BN - 1) / tc::BN) * ((M + tc::BM - 1) / tc::BM);
-  dim3 grid(tiles < sms ? tiles : sms);
+  static const int cap = getenv("SPEX_TC_GRID") ? atoi(getenv("SPEX_TC_GRID")) : sms;
+  const int gmax = cap > 0 && cap < sms ? cap : sms;
+  dim3 grid(tiles < gmax ? tiles : gmax);
   // per-stream monotone tile counter: launch j claims ids [base_j, base_j + tiles + grid)
   struct Ctr {
     cudaStream_t st;
