@@ -312,7 +312,8 @@ def main():
         except Exception:
             traffic = None
     clocks = clk.summary()
-    cpu = cpu_baseline(cfg_text, base_seed, args.cpu_sample_runs)
+    # reported on rank 0 at N=1 only (the reference arm times all host cores separately)
+    cpu = cpu_baseline(cfg_text, base_seed, args.cpu_sample_runs) if world == 1 else None
     line = {
         "metric": "ToT queries/sec",
         "value": total_q / dev_s,
