@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--policy", default="mid_policy")
     ap.add_argument("--prm", default="mid_prm")
     ap.add_argument("--cpu-sample-runs", type=int, default=4)
+    ap.add_argument("--named-shapes", type=int, default=1,
+                    help="also time config 5 with the Llama-3-8B-shaped policy + 1.5B-shaped PRM (1 = on)")
     return ap.parse_args()
 
 
@@ -114,7 +116,7 @@ def load_peaks():
     try:
         return json.loads(PEAKS.read_text()), "measured"
     except Exception:
-        return {"hbm_gbs": HBM_FALLBACK_GBS, "bf16_tflops": 1590.0}, "fallback"
+        return {"hbm_gbs": HBM_FALLBACK_GBS, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
 
 
 # ----------------------------------------------------------------- reference arm
@@ -246,7 +248,7 @@ def main():
         t0 = time.perf_counter()
         agg = {"queries": 0, "ctl_ms": 0.0, "model_ms": 0.0, "step_ms": 0.0, "streamed": 0, "attn_ms": 0.0,
                "attn_bytes": 0.0,
-               "launches": 0, "flops": 0.0, "decode_rows": 0, "prm_rows": 0, "attn_launches": 0}
+               "launches": 0, "flops": 0.0, "decode_rows": 0, "prm_rows": 0, "attn_launches": 0, "prm_thoughts": 0}
         for _ in range(args.steps):
             tot, st, ms, _ = one_search(False)
             agg["queries"] += tot.queries
@@ -261,6 +263,7 @@ def main():
             agg["flops"] += ms["policy_flops"] + ms["prm_flops"]
             agg["decode_rows"] += ms["decode_rows"]
             agg["prm_rows"] += ms["prm_rows"]
+            agg["prm_thoughts"] += ms["prm_thoughts"]
         barrier()
         wall = time.perf_counter() - t0
         # device time of the step: control-kernel start -> last of (control end,
@@ -286,6 +289,32 @@ def main():
             e2e_d2h += d2h
         barrier()
         tr_wall = time.perf_counter() - t2
+    # the named model shapes (north star): config 5, Llama-3-8B-shaped policy +
+    # 1.5B-shaped PRM, one warm + one timed search on this GPU
+    named = None
+    if args.named_shapes:
+        c5 = (ROOT / "configs" / "c5_rebase_w32_q64.json").read_text()
+
+        def c5_search():
+            ex = spex.Executor(c5, json.loads(c5)["run"]["seed"] + rank, None, trace=False, device=local)
+            ex.set_model("llama3_8b", "prm_1p5b", weight_seed=1)
+            t = ex.run()
+            m = ex.model_stats()
+            ex.close()
+            return t, m
+
+        c5_search()
+        n_tot, n_ms = c5_search()
+        sec = n_ms["step_ms"] / 1000.0
+        named = {"workload": "c5_rebase_w32_q64: rebase_bfs w32 d16 target32, T1+T2+T3, 64 queries",
+                 "policy": "llama3_8b (32 L, d 4096, 32/8 heads x 128, FFN 14336, vocab 128256)",
+                 "prm": "prm_1p5b (28 L, d 1536, 12/2 heads x 128, FFN 8960)",
+                 "queries_per_s": n_tot.queries / sec, "thoughts_per_s": n_ms["prm_thoughts"] / sec,
+                 "step_ms": n_ms["step_ms"], "decode_rows": n_ms["decode_rows"], "prm_rows": n_ms["prm_rows"],
+                 "k1_hbm_frac": (n_ms["attn_alg_bytes"] / (n_ms["attn_ms"] / 1000.0) / 1e9) / load_peaks()[0]["hbm_gbs"],
+                 "projection_tflops": (n_ms["policy_flops"] + n_ms["prm_flops"]) / sec / 1e12,
+                 "projection_tensor_frac": (n_ms["policy_flops"] + n_ms["prm_flops"]) / sec / 1e12 /
+                 load_peaks()[0].get("bf16_tflops_sustained", load_peaks()[0].get("bf16_tflops", 1590.0))}
     # the same search barrier-synchronously (no T1/T2/T3: the reference's
     # baseline arm, experiment.cpp:68-70), same model work, for the metric's
     # "vs barrier-synchronous search"
@@ -349,6 +378,8 @@ def main():
                             "spex_decode_steps": ms["decode_steps"], "spex_decode_rows": ms["decode_rows"],
                             "note": "one GPU, same config/seed/model, flags '' vs the config's flags; "
                                     "device step time of one warm search each"},
+        "thoughts_per_s": agg["prm_thoughts"] / dev_s,
+        "named_model_shapes": named,
         "gpu_launches": int(agg["launches"]),
         "roofline": {"bound": "hbm", "kernel": "K1 tree_attn_kernel (policy decode)",
                      "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",

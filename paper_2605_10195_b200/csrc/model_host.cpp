@@ -51,7 +51,7 @@ void spex_k_prm_scan_all(TreeView t, const int* kind, const int* off, const int*
                          cudaStream_t s);
 void spex_k_embed(const RowDesc* rows, int M, const __nv_bfloat16* E, int d, float* X, cudaStream_t s);
 void spex_k_rmsnorm(const float* X, int M, int d, float eps, __nv_bfloat16* Y, cudaStream_t s);
-void spex_k_rope_kv(const RowDesc* rows, int M, const __nv_bfloat16* QKV, int H, int KVH, int dh, const float* inv_freq,
+void spex_k_rope_kv(const RowDesc* rows, int M, const __nv_bfloat16* QKV, int H, int KVH, int dh, const float* cs_tab,
                     long long slots, __nv_bfloat16* Kp, __nv_bfloat16* Vp, float* Qr, cudaStream_t s);
 int spex_k_tree_attn(const RowDesc* rows, const Segment* segs, const float* Qr, int H, int KVH, int dh,
                      const __nv_bfloat16* Kp, const __nv_bfloat16* Vp, long long slots, __nv_bfloat16* O, int M,
@@ -294,6 +294,7 @@ static Model* make_model(const ModelShape& sh, bool prm, uint64_t seed, long lon
     m->lse = dalloc<float>(M, o);
     m->lsum = dalloc<float>(M, o);
   }
+  m->rope_tab = dalloc<float>(M * sh.dh, o);  // [max_rows][dh/2] (cos, sin)
   // K2 on the hand-written tcgen05 GEMM with fused epilogues (gemm_tc.cu) is
   // opt-in (SPEX_TC_GEMM=1): it is correct (tests/test_gemm_tc_gpu.py) and beats
   // cuBLAS + the separate elementwise kernels per op at decode shapes, but over a
@@ -325,7 +326,6 @@ static Model* make_model(const ModelShape& sh, bool prm, uint64_t seed, long lon
     if (spex_tmap_operand(&m->a_xn, m->Xn, (long long)M, sh.d) || spex_tmap_operand(&m->a_o, m->O, (long long)M, sh.H * sh.dh) ||
         spex_tmap_operand(&m->a_act, m->A, (long long)M, sh.F))
       m->use_tc = false;
-    m->rope_tab = dalloc<float>(M * sh.dh, o);
     if (!prm) m->lse_part = dalloc<float>(M * (size_t)(sh.V / 128) * 4, o);
   }
   if (!m->use_tc && !prm) m->logits = dalloc<float>(M * sh.V, o);
@@ -406,13 +406,14 @@ static void forward(Model& m, const RowDesc* rows, const Segment* segs, int M, c
     }
     return;
   }
-  g_launches += 2 + 5LL * s.L + (m.is_prm ? 0 : 1);
+  g_launches += 3 + 5LL * s.L + (m.is_prm ? 0 : 1);
   g_gemms += 4LL * s.L + (m.is_prm ? 0 : 1);
+  spex_k_rope_table(rows, M, m.inv_freq, s.dh / 2, m.rope_tab, st);  // (cos, sin) once for all layers
   spex_k_embed(rows, M, m.embed, s.d, m.X, st);
   for (int l = 0; l < s.L; ++l) {
     spex_k_rmsnorm(m.X, M, s.d, s.eps, m.Xn, st);
     gemm_bf16out(hb, m.Xn, m.wqkv[l], m.QKV, M, (s.H + 2 * s.KVH) * s.dh, s.d);
-    spex_k_rope_kv(rows, M, m.QKV, s.H, s.KVH, s.dh, m.inv_freq, m.slots, m.Kp[l], m.Vp[l], m.Qr, st);
+    spex_k_rope_kv(rows, M, m.QKV, s.H, s.KVH, s.dh, m.rope_tab, m.slots, m.Kp[l], m.Vp[l], m.Qr, st);
     if (timer) timer->begin(st);
     int rc = -1;
     if (tiles && !m.kmap.empty())

@@ -274,53 +274,46 @@ __global__ void rmsnorm_bf16_kernel(const float* X, int M, int d, float eps, __n
 // layer's KV pool at the row's slot; q (fp32, pre-scaled by 1/sqrt(dh)) to Qr.
 // Pools are [KVH][slots][dh].
 __global__ void rope_kv_kernel(const RowDesc* rows, int M, const __nv_bfloat16* QKV, int H, int KVH, int dh,
-                               const float* inv_freq, long long slots, __nv_bfloat16* Kp, __nv_bfloat16* Vp,
-                               float* Qr) {
-  // one block per row; rotate-half RoPE on (x[i], x[i+half]) pairs two at a
-  // time from the bf16 projection output; V copied 8 bytes at a time
-  const int r = blockIdx.x;
+                               const float2* __restrict__ cs_tab, long long slots, __nv_bfloat16* Kp,
+                               __nv_bfloat16* Vp, float* Qr) {
+  // one warp per row; (cos, sin) from the per-forward table (rope_table_kernel),
+  // rotate-half RoPE on (x[i], x[i+half]) pairs two at a time from the bf16
+  // projection output; V copied 8 bytes at a time
+  const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (r >= M) return;
-  __shared__ float sc[128], ss[128];
-  const RowDesc rd = rows[r];
+  const long long slot = rows[r].slot;
   const int width = (H + 2 * KVH) * dh;
   const __nv_bfloat16* src = QKV + (long long)r * width;
   const int half = dh / 2;
+  const float2* cs = cs_tab + (long long)r * half;
   const float qscale = rsqrtf((float)dh);
-  for (int i = threadIdx.x; i < half; i += blockDim.x) {
-    float sn, cs;
-    sincosf((float)rd.abs_pos * inv_freq[i], &sn, &cs);
-    sc[i] = cs;
-    ss[i] = sn;
-  }
-  __syncthreads();
   const int hp = half / 2;  // bf16 pairs per half
-  for (int idx = threadIdx.x; idx < (H + KVH) * hp; idx += blockDim.x) {
+  for (int idx = lane; idx < (H + KVH) * hp; idx += 32) {
     const int head = idx / hp;
     const int i = (idx - head * hp) * 2;
     const __nv_bfloat16* x = src + head * dh;
     const __nv_bfloat162 a2 = *reinterpret_cast<const __nv_bfloat162*>(x + i);
     const __nv_bfloat162 b2 = *reinterpret_cast<const __nv_bfloat162*>(x + i + half);
     const float ax = __low2float(a2), ay = __high2float(a2), bx = __low2float(b2), by = __high2float(b2);
-    const float c0 = sc[i], c1 = sc[i + 1], s0 = ss[i], s1 = ss[i + 1];
-    const float ya0 = ax * c0 - bx * s0, ya1 = ay * c1 - by * s1;
-    const float yb0 = ax * s0 + bx * c0, yb1 = ay * s1 + by * c1;
+    const float2 t0 = cs[i], t1 = cs[i + 1];
+    const float ya0 = ax * t0.x - bx * t0.y, ya1 = ay * t1.x - by * t1.y;
+    const float yb0 = ax * t0.y + bx * t0.x, yb1 = ay * t1.y + by * t1.x;
     if (head < H) {
       float* qd = Qr + ((long long)r * H + head) * dh;
       *reinterpret_cast<float2*>(qd + i) = make_float2(ya0 * qscale, ya1 * qscale);
       *reinterpret_cast<float2*>(qd + i + half) = make_float2(yb0 * qscale, yb1 * qscale);
     } else {
       const int kh = head - H;
-      __nv_bfloat16* kd = Kp + ((long long)kh * slots + rd.slot) * dh;
+      __nv_bfloat16* kd = Kp + ((long long)kh * slots + slot) * dh;
       *reinterpret_cast<uint32_t*>(kd + i) = pack_bf16(ya0, ya1);
       *reinterpret_cast<uint32_t*>(kd + i + half) = pack_bf16(yb0, yb1);
     }
   }
   const __nv_bfloat16* vs = src + (H + KVH) * dh;
-  for (int idx = threadIdx.x; idx < KVH * dh / 4; idx += blockDim.x) {
+  for (int idx = lane; idx < KVH * dh / 4; idx += 32) {
     const int e = idx * 4;
     const int kh = e / dh, i = e - kh * dh;
-    *reinterpret_cast<uint2*>(Vp + ((long long)kh * slots + rd.slot) * dh + i) =
-        *reinterpret_cast<const uint2*>(vs + e);
+    *reinterpret_cast<uint2*>(Vp + ((long long)kh * slots + slot) * dh + i) = *reinterpret_cast<const uint2*>(vs + e);
   }
 }
 
@@ -1388,23 +1381,24 @@ __global__ void __launch_bounds__(kAttnThreads) tree_attn_tile_kernel(const Tile
 }
 
 __global__ void swiglu_kernel(const __nv_bfloat16* GU, int M, int F, __nv_bfloat16* A) {
-  // flat grid-stride over M * F/4 quads (F % 4 == 0), bf16 gate/up in
-  const int F4 = F / 4;
-  const long long n = (long long)M * F4;
+  // flat grid-stride over M * F/8 octets (F % 8 == 0), bf16 gate/up in, 16-byte loads
+  const int F8 = F / 8;
+  const long long n = (long long)M * F8;
   for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x) {
-    const long long r = k / F4;
-    const int j = (int)(k - r * F4) * 4;
+    const long long r = k / F8;
+    const int j = (int)(k - r * F8) * 8;
     const __nv_bfloat16* g = GU + r * 2 * F;
-    const uint2 gr = *reinterpret_cast<const uint2*>(g + j);
-    const uint2 ur = *reinterpret_cast<const uint2*>(g + F + j);
+    const uint4 gr = *reinterpret_cast<const uint4*>(g + j);
+    const uint4 ur = *reinterpret_cast<const uint4*>(g + F + j);
     const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&gr);
     const __nv_bfloat162* u2 = reinterpret_cast<const __nv_bfloat162*>(&ur);
-    float gv[4] = {__low2float(g2[0]), __high2float(g2[0]), __low2float(g2[1]), __high2float(g2[1])};
-    float uv[4] = {__low2float(u2[0]), __high2float(u2[0]), __low2float(u2[1]), __high2float(u2[1])};
-    uint2 o;
-    o.x = pack_bf16(gv[0] / (1.f + __expf(-gv[0])) * uv[0], gv[1] / (1.f + __expf(-gv[1])) * uv[1]);
-    o.y = pack_bf16(gv[2] / (1.f + __expf(-gv[2])) * uv[2], gv[3] / (1.f + __expf(-gv[3])) * uv[3]);
-    *reinterpret_cast<uint2*>(A + r * F + j) = o;
+    uint32_t o[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float ga = __low2float(g2[e]), gb = __high2float(g2[e]);
+      o[e] = pack_bf16(ga / (1.f + __expf(-ga)) * __low2float(u2[e]), gb / (1.f + __expf(-gb)) * __high2float(u2[e]));
+    }
+    *reinterpret_cast<uint4*>(A + r * F + j) = make_uint4(o[0], o[1], o[2], o[3]);
   }
 }
 
@@ -1551,9 +1545,10 @@ extern "C" void spex_k_rmsnorm(const float* X, int M, int d, float eps, __nv_bfl
 }
 
 extern "C" void spex_k_rope_kv(const RowDesc* rows, int M, const __nv_bfloat16* QKV, int H, int KVH, int dh,
-                               const float* inv_freq, long long slots, __nv_bfloat16* Kp, __nv_bfloat16* Vp,
+                               const float* cs_tab, long long slots, __nv_bfloat16* Kp, __nv_bfloat16* Vp,
                                float* Qr, cudaStream_t s) {
-  rope_kv_kernel<<<M, 128, 0, s>>>(rows, M, QKV, H, KVH, dh, inv_freq, slots, Kp, Vp, Qr);
+  rope_kv_kernel<<<(M + 7) / 8, 256, 0, s>>>(rows, M, QKV, H, KVH, dh, reinterpret_cast<const float2*>(cs_tab), slots,
+                                             Kp, Vp, Qr);
 }
 
 template <int DH, int G>
@@ -1718,8 +1713,8 @@ extern "C" int spex_k_tree_attn_tiles(const TileDesc* tiles, int ntiles, const R
 }
 
 extern "C" void spex_k_swiglu(const __nv_bfloat16* GU, int M, int F, __nv_bfloat16* A, cudaStream_t s) {
-  const long long quads = (long long)M * (F / 4);
-  const int blocks = (int)std::min<long long>((quads + 255) / 256, 148 * 16);
+  const long long octets = (long long)M * (F / 8);
+  const int blocks = (int)std::min<long long>((octets + 255) / 256, 148 * 16);
   swiglu_kernel<<<blocks, 256, 0, s>>>(GU, M, F, A);
 }
 
