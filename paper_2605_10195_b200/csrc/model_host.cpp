@@ -57,6 +57,9 @@ int spex_k_tree_attn(const RowDesc* rows, const Segment* segs, const float* Qr, 
                      const __nv_bfloat16* Kp, const __nv_bfloat16* Vp, long long slots, __nv_bfloat16* O, int M,
                      cudaStream_t s);
 void spex_k_build_decode_chunks(const RowDesc* rows, const Segment* segs, int M, DecodeChunks w, cudaStream_t s);
+int spex_k_tree_attn_decode_mma(const CUtensorMap* kmap, const CUtensorMap* vmap, const RowDesc* rows,
+                                const Segment* segs, const float* Qr, int H, int KVH, int dh, long long slots,
+                                __nv_bfloat16* O, int M, cudaStream_t s);
 int spex_k_tree_attn_chunked(const RowDesc* rows, const Segment* segs, const float* Qr, int H, int KVH, int dh,
                              const __nv_bfloat16* Kp, const __nv_bfloat16* Vp, long long slots, __nv_bfloat16* O,
                              DecodeChunks w, int qslot, cudaStream_t s);
@@ -332,6 +335,15 @@ static Model* make_model(const ModelShape& sh, bool prm, uint64_t seed, long lon
   return m;
 }
 
+// Decode rows of GQA models (>= 4 query heads per KV head) go to the tensor-core
+// decode kernel: its staged K/V chunks serve the whole group, while the
+// per-lane FHFMA kernel's work per byte grows with the group size.
+static bool decode_mma_wanted(const ModelShape& s) {
+  static const int force = getenv("SPEX_K1_DECODE_MMA") ? atoi(getenv("SPEX_K1_DECODE_MMA")) : -1;
+  if (force >= 0) return force != 0;
+  return s.dh == 128 && s.H / s.KVH >= 4;
+}
+
 static void tc_gemm(const CUtensorMap& a, const TcWeight& w, int M, const TcEpilogue& ep, cudaStream_t st) {
   if (spex_k_gemm_tc(&a, &w.map, M, w.N, w.K, &ep, st) != 0) throw std::runtime_error("tcgen05 GEMM launch failed");
 }
@@ -380,6 +392,9 @@ static void forward(Model& m, const RowDesc* rows, const Segment* segs, int M, c
       if (tiles && !m.kmap.empty())
         rc = spex_k_tree_attn_tiles_mma(&m.kmap[l], &m.vmap[l], tiles, ntiles, rows, segs, m.Qr, s.H, s.KVH, s.dh,
                                         m.slots, m.O, st);
+      if (rc != 0 && !tiles && !m.kmap.empty() && decode_mma_wanted(s))
+        rc = spex_k_tree_attn_decode_mma(&m.kmap[l], &m.vmap[l], rows, segs, m.Qr, s.H, s.KVH, s.dh, m.slots, m.O, M,
+                                         st);
       if (rc != 0 && chunks)
         rc = spex_k_tree_attn_chunked(rows, segs, m.Qr, s.H, s.KVH, s.dh, m.Kp[l], m.Vp[l], m.slots, m.O, *chunks, l,
                                       st);
@@ -419,6 +434,9 @@ static void forward(Model& m, const RowDesc* rows, const Segment* segs, int M, c
     if (tiles && !m.kmap.empty())
       rc = spex_k_tree_attn_tiles_mma(&m.kmap[l], &m.vmap[l], tiles, ntiles, rows, segs, m.Qr, s.H, s.KVH, s.dh,
                                       m.slots, m.O, st);
+    if (rc != 0 && !tiles && !m.kmap.empty() && decode_mma_wanted(s))
+      rc = spex_k_tree_attn_decode_mma(&m.kmap[l], &m.vmap[l], rows, segs, m.Qr, s.H, s.KVH, s.dh, m.slots, m.O, M,
+                                       st);
     if (rc != 0 && chunks)
       rc = spex_k_tree_attn_chunked(rows, segs, m.Qr, s.H, s.KVH, s.dh, m.Kp[l], m.Vp[l], m.slots, m.O, *chunks, l,
                                     st);

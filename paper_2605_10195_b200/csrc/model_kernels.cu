@@ -1205,6 +1205,249 @@ __global__ void __launch_bounds__(128) tree_attn_tile_mma_kernel(const __grid_co
   (void)L1;
 }
 
+// K1 decode on tensor cores for GQA groups: block = (decode row, KV head); the
+// MMA rows are that KV head's G query heads (zero-padded to 16), so every
+// staged 64-token K/V chunk (TMA, 2 buffers) serves all G heads; the 4 warps
+// take 16-token slices of each chunk and merge (m, l, O) through shared memory.
+// For G >= 4 this replaces the per-lane FHFMA kernel, whose work per byte
+// grows with G.
+__global__ void __launch_bounds__(128) tree_attn_decode_mma_kernel(const __grid_constant__ CUtensorMap kmap,
+                                                                  const __grid_constant__ CUtensorMap vmap,
+                                                                  const RowDesc* __restrict__ rows,
+                                                                  const Segment* __restrict__ segs,
+                                                                  const float* __restrict__ Qr, int H, long long slots,
+                                                                  __nv_bfloat16* __restrict__ O, int G) {
+  constexpr int DH = 128;
+  constexpr int SPLIT = 4;              // warps over the chunk's tokens
+  constexpr int TW = kChunk / SPLIT;    // tokens per warp per chunk (16, 32 or 64)
+  constexpr int NT = TW / 8;            // n8 score tiles per warp
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* sbase = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // [buf][K|V][16 KB]
+  __shared__ uint64_t bar[2];
+  __shared__ float sMl[4][2][kTileRows];  // per warp: m, l per row
+  const int r = blockIdx.x, kh = blockIdx.y, hbase = kh * G;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int slice = warp;
+  const RowDesc last = rows[r];
+  const Segment* sg = segs + last.seg_off;
+  const int nseg = last.nseg;
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  int nchunks = 0;
+  for (int s = 0; s < nseg; ++s) nchunks += (sg[s].len + kChunk - 1) / kChunk;
+  // Q fragments (A operand, 16 rows = the group's heads x 128), rows >= G are zero
+  const int gq = lane >> 2, tq = lane & 3;
+  uint32_t qa[8][4];
+  {
+    const int r0 = gq, r1 = gq + 8;
+    const bool v0 = r0 < G, v1 = r1 < G;
+    const float* q0 = Qr + ((long long)r * H + hbase + (v0 ? r0 : 0)) * DH;
+    const float* q1 = Qr + ((long long)r * H + hbase + (v1 ? r1 : 0)) * DH;
+    const float sc = 1.4426950408889634f;
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks) {
+      const int k0 = ks * 16 + tq * 2;
+      const float2 x00 = v0 ? *reinterpret_cast<const float2*>(q0 + k0) : make_float2(0.f, 0.f);
+      const float2 x10 = v1 ? *reinterpret_cast<const float2*>(q1 + k0) : make_float2(0.f, 0.f);
+      const float2 x01 = v0 ? *reinterpret_cast<const float2*>(q0 + k0 + 8) : make_float2(0.f, 0.f);
+      const float2 x11 = v1 ? *reinterpret_cast<const float2*>(q1 + k0 + 8) : make_float2(0.f, 0.f);
+      qa[ks][0] = pack_bf16(x00.x * sc, x00.y * sc);
+      qa[ks][1] = pack_bf16(x10.x * sc, x10.y * sc);
+      qa[ks][2] = pack_bf16(x01.x * sc, x01.y * sc);
+      qa[ks][3] = pack_bf16(x11.x * sc, x11.y * sc);
+    }
+  }
+  __syncthreads();
+  int seg_i = 0, seg_o = 0;
+  long long cb[2];
+  int cl[2], cown[2];
+  auto next_chunk = [&](int b) {
+    while (seg_i < nseg && seg_o >= sg[seg_i].len) {
+      ++seg_i;
+      seg_o = 0;
+    }
+    cb[b] = sg[seg_i].base + seg_o;
+    const int l = sg[seg_i].len - seg_o;
+    cl[b] = l < kChunk ? l : kChunk;
+    cown[b] = (seg_i == nseg - 1) ? seg_o : -1;
+    seg_o += cl[b];
+  };
+  auto issue = [&](int b) {
+    unsigned char* kb = sbase + b * 32768;
+    unsigned char* vb = kb + 16384;
+    const int rowc = (int)((long long)kh * slots + cb[b]);
+    mbar_expect_tx(&bar[b], 32768);
+    tma_load_2d(kb, &kmap, 0, rowc, &bar[b]);
+    tma_load_2d(kb + 8192, &kmap, 64, rowc, &bar[b]);
+    tma_load_2d(vb, &vmap, 0, rowc, &bar[b]);
+    tma_load_2d(vb + 8192, &vmap, 64, rowc, &bar[b]);
+  };
+  for (int c = 0; c < 2 && c < nchunks; ++c) {
+    next_chunk(c);
+    if (tid == 0) issue(c);
+  }
+  float oacc[16][4];
+#pragma unroll
+  for (int n = 0; n < 16; ++n) oacc[n][0] = oacc[n][1] = oacc[n][2] = oacc[n][3] = 0.f;
+  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;  // rows gq and gq+8
+  for (int c = 0; c < nchunks; ++c) {
+    const int b = c & 1;
+    const int len = cl[b];
+    mbar_wait(&bar[b], (uint32_t)((c >> 1) & 1));
+    const uint32_t kb = (uint32_t)__cvta_generic_to_shared(sbase + b * 32768);
+    const uint32_t vb = kb + 16384;
+    const int t_base = slice * TW;
+    // S = Q K^T for this warp's token slice
+    float sacc[NT][4];
+#pragma unroll
+    for (int n = 0; n < NT; ++n) sacc[n][0] = sacc[n][1] = sacc[n][2] = sacc[n][3] = 0.f;
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks) {
+#pragma unroll
+      for (int n2 = 0; n2 < NT / 2; ++n2) {
+        // two n8 tiles (16 tokens) x k16: matrices {tok 0-7,k0-7},{tok 0-7,k8-15},{tok 8-15,k0-7},{tok 8-15,k8-15}
+        const int mi = lane >> 3, ri = lane & 7;
+        const int tok = t_base + n2 * 16 + (mi >> 1) * 8 + ri;
+        const int chunk16 = ks * 2 + (mi & 1);
+        uint32_t b0, b1, b2, b3;
+        ldsm_x4(kb + swz(tok, chunk16), b0, b1, b2, b3);
+        mma_bf16(sacc[2 * n2], qa[ks][0], qa[ks][1], qa[ks][2], qa[ks][3], b0, b1);
+        mma_bf16(sacc[2 * n2 + 1], qa[ks][0], qa[ks][1], qa[ks][2], qa[ks][3], b2, b3);
+      }
+    }
+    // mask and online softmax (rows gq: c0,c1; gq+8: c2,c3)
+    float mx0 = -INFINITY, mx1 = -INFINITY;
+#pragma unroll
+    for (int n = 0; n < NT; ++n) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int t = t_base + n * 8 + tq * 2 + e;
+        const bool ok0 = t < len;  // a decode row sees its whole context
+        const bool ok1 = ok0;
+        sacc[n][e] = ok0 ? sacc[n][e] : -INFINITY;
+        sacc[n][2 + e] = ok1 ? sacc[n][2 + e] : -INFINITY;
+        mx0 = fmaxf(mx0, sacc[n][e]);
+        mx1 = fmaxf(mx1, sacc[n][2 + e]);
+      }
+    }
+#pragma unroll
+    for (int o = 1; o < 4; o <<= 1) {
+      mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, o));
+      mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, o));
+    }
+    const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
+    const float a0 = mn0 == -INFINITY ? 1.f : exp2f(m0 - mn0);
+    const float a1 = mn1 == -INFINITY ? 1.f : exp2f(m1 - mn1);
+    float ps0 = 0.f, ps1 = 0.f;
+    uint32_t pa[NT / 2][4];
+#pragma unroll
+    for (int n = 0; n < NT; ++n) {
+      const float p00 = mn0 == -INFINITY ? 0.f : exp2f(sacc[n][0] - mn0);
+      const float p01 = mn0 == -INFINITY ? 0.f : exp2f(sacc[n][1] - mn0);
+      const float p10 = mn1 == -INFINITY ? 0.f : exp2f(sacc[n][2] - mn1);
+      const float p11 = mn1 == -INFINITY ? 0.f : exp2f(sacc[n][3] - mn1);
+      ps0 += p00 + p01;
+      ps1 += p10 + p11;
+      // C layout of n8 tile n -> A layout of k16 step n/2 (regs 0,1 for even n, 2,3 for odd n)
+      if ((n & 1) == 0) {
+        pa[n / 2][0] = pack_bf16(p00, p01);
+        pa[n / 2][1] = pack_bf16(p10, p11);
+      } else {
+        pa[n / 2][2] = pack_bf16(p00, p01);
+        pa[n / 2][3] = pack_bf16(p10, p11);
+      }
+    }
+    l0 = l0 * a0 + ps0;
+    l1 = l1 * a1 + ps1;
+    m0 = mn0;
+    m1 = mn1;
+#pragma unroll
+    for (int n = 0; n < 16; ++n) {
+      oacc[n][0] *= a0;
+      oacc[n][1] *= a0;
+      oacc[n][2] *= a1;
+      oacc[n][3] *= a1;
+    }
+    // O += P V : k = this warp's tokens (NT/2 k16 steps), n = 128 dh (16 n8 tiles)
+#pragma unroll
+    for (int kk = 0; kk < NT / 2; ++kk) {
+#pragma unroll
+      for (int n2 = 0; n2 < 8; ++n2) {
+        // V^T fragments via ldmatrix.trans: matrices {tok 0-7, dh 8j..}, {tok 8-15, dh 8j..}, {tok 0-7, dh 8j+8..}, {tok 8-15, dh 8j+8..}
+        const int mi = lane >> 3, ri = lane & 7;
+        const int tok = t_base + kk * 16 + (mi & 1) * 8 + ri;
+        const int chunk16 = n2 * 2 + (mi >> 1);
+        uint32_t b0, b1, b2, b3;
+        ldsm_x4_t(vb + swz(tok, chunk16), b0, b1, b2, b3);
+        mma_bf16(oacc[2 * n2], pa[kk][0], pa[kk][1], pa[kk][2], pa[kk][3], b0, b1);
+        mma_bf16(oacc[2 * n2 + 1], pa[kk][0], pa[kk][1], pa[kk][2], pa[kk][3], b2, b3);
+      }
+    }
+    __syncthreads();
+    if (c + 2 < nchunks) {
+      next_chunk(b);
+      if (tid == 0) issue(b);
+    }
+  }
+  // row sums within the quad
+#pragma unroll
+  for (int o = 1; o < 4; o <<= 1) {
+    l0 += __shfl_xor_sync(0xffffffffu, l0, o);
+    l1 += __shfl_xor_sync(0xffffffffu, l1, o);
+  }
+  // merge the SPLIT warps of head g through shared memory (reuse the K/V buffers)
+  float* sO = reinterpret_cast<float*>(sbase);  // [4 warps][16 rows][128] fp32 = 32 KB
+  if (tq == 0) {
+    sMl[warp][0][gq] = m0;
+    sMl[warp][0][gq + 8] = m1;
+    sMl[warp][1][gq] = l0;
+    sMl[warp][1][gq + 8] = l1;
+  }
+  __syncthreads();
+  float M0 = -INFINITY, M1 = -INFINITY;
+  for (int w = 0; w < SPLIT; ++w) {
+    M0 = fmaxf(M0, sMl[w][0][gq]);
+    M1 = fmaxf(M1, sMl[w][0][gq + 8]);
+  }
+  float L0 = 0.f, L1 = 0.f;
+  for (int w = 0; w < SPLIT; ++w) {
+    const float mw0 = sMl[w][0][gq], mw1 = sMl[w][0][gq + 8];
+    L0 += (mw0 == -INFINITY) ? 0.f : sMl[w][1][gq] * exp2f(mw0 - M0);
+    L1 += (mw1 == -INFINITY) ? 0.f : sMl[w][1][gq + 8] * exp2f(mw1 - M1);
+  }
+  const float f0 = (m0 == -INFINITY) ? 0.f : exp2f(m0 - M0);
+  const float f1 = (m1 == -INFINITY) ? 0.f : exp2f(m1 - M1);
+#pragma unroll
+  for (int n = 0; n < 16; ++n) {
+    const int col = n * 8 + tq * 2;
+    float* r0p = sO + (warp * 16 + gq) * DH + col;
+    float* r1p = sO + (warp * 16 + gq + 8) * DH + col;
+    r0p[0] = oacc[n][0] * f0;
+    r0p[1] = oacc[n][1] * f0;
+    r1p[0] = oacc[n][2] * f1;
+    r1p[1] = oacc[n][3] * f1;
+  }
+  __syncthreads();
+  // all 128 threads write the merged rows of the G heads
+  for (int i = tid; i < G * DH; i += 128) {
+    const int row = i / DH, col = i % DH;
+    float acc = 0.f, Lr = 0.f, Mr = -INFINITY;
+    for (int w = 0; w < SPLIT; ++w) acc += sO[(w * 16 + row) * DH + col];
+    for (int w = 0; w < SPLIT; ++w) Mr = fmaxf(Mr, sMl[w][0][row]);
+    for (int w = 0; w < SPLIT; ++w) {
+      const float mw = sMl[w][0][row];
+      Lr += (mw == -INFINITY) ? 0.f : sMl[w][1][row] * exp2f(mw - Mr);
+    }
+    O[((long long)r * H + hbase + row) * DH + col] = __float2bfloat16_rn(acc / Lr);
+  }
+  (void)L0;
+  (void)L1;
+}
+
 // K1 tile variant for prefill-shaped rows (PRM scoring): kTileRows consecutive
 // rows of one thought share their ancestors and a causal own prefix, so each
 // 64-token K/V chunk is staged once per tile instead of once per row.
@@ -1690,6 +1933,24 @@ extern "C" int spex_k_tree_attn_tiles_mma(const CUtensorMap* kmap, const CUtenso
   SPEX_MMA_CASE(4)
 #undef SPEX_MMA_CASE
   return -1;
+}
+
+// K1 decode rows on tensor cores (GQA groups G in [2, 16], dh = 128).
+extern "C" int spex_k_tree_attn_decode_mma(const CUtensorMap* kmap, const CUtensorMap* vmap, const RowDesc* rows,
+                                           const Segment* segs, const float* Qr, int H, int KVH, int dh,
+                                           long long slots, __nv_bfloat16* O, int M, cudaStream_t s) {
+  const int G = H / KVH;
+  if (M <= 0) return 0;
+  if (dh != 128 || G < 1 || G > 16) return -1;
+  const size_t smem = 2 * 32768 + 1024;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(tree_attn_decode_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  dim3 grid(M, KVH);
+  tree_attn_decode_mma_kernel<<<grid, 128, smem, s>>>(*kmap, *vmap, rows, segs, Qr, H, slots, O, G);
+  return (int)cudaGetLastError();
 }
 
 extern "C" int spex_k_tree_attn_tiles(const TileDesc* tiles, int ntiles, const RowDesc* rows, const Segment* segs,
