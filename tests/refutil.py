@@ -82,3 +82,34 @@ def sweep_configs():
                        "workload": {"noise_sigma": noise}, "run": {"batch_size": 6, "n_queries": 6}}
                 out.append((f"{fam}-{fl or 'base'}-s{seed}", json.dumps(cfg), seed, fl))
     return out
+
+
+def edge_configs():
+    """Edge cases of the search (the reference's integration tests exercise
+    admission staggering, test_executor.cpp:265-286): queued admission
+    (batch_size < n_queries), a single query, width 1, depth 1-2, noise-free and
+    noisy rewards, T2 with a tiny producer budget, a large speculation window."""
+    base = {"policy": {"width": 4, "max_depth": 8, "target_answers": 6}, "workload": {"noise_sigma": 0.05},
+            "run": {"batch_size": 6, "n_queries": 6}}
+    cases = []
+
+    def add(name, fam, flags, seed=3, **upd):
+        c = json.loads(json.dumps(base))
+        c["family"] = fam
+        for sect, kv in upd.items():
+            c.setdefault(sect, {}).update(kv)
+        cases.append((name, json.dumps(c), seed, flags))
+
+    for fam in ("rstar_dfs", "rest_hybrid", "rebase_bfs"):
+        add(f"{fam}-queued", fam, "t1,t2,t3", run={"batch_size": 2, "n_queries": 9})
+        add(f"{fam}-single", fam, "t1,t3", run={"batch_size": 1, "n_queries": 1})
+        add(f"{fam}-width1", fam, "t1,t2,t3", policy={"width": 1})
+        add(f"{fam}-depth1", fam, "t1,t2", policy={"max_depth": 1, "target_answers": 2})
+        add(f"{fam}-depth2-wide", fam, "t1,t3", policy={"width": 12, "max_depth": 2, "target_answers": 12})
+        add(f"{fam}-noisy", fam, "t1,t2,t3", 7, workload={"noise_sigma": 0.4})
+        add(f"{fam}-tiny-producers", fam, "t1,t2", run={"max_producers": 2})
+        add(f"{fam}-specwin", fam, "t1", run={"spec_k": 32})
+        add(f"{fam}-depth-widths", fam, "t1,t2,t3", policy={"depth_widths": [6, 3, 2]})
+        add(f"{fam}-kv-latency", fam, "t1,t2,t3", hardware={"kv_bytes_per_token": 131072.0, "reward_latency": 0.5})
+        add(f"{fam}-skewed", fam, "t1,t3", 11, workload={"skew": 0.6, "answer_alphabet": 12})
+    return cases

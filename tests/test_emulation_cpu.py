@@ -56,3 +56,13 @@ def test_emulation_sweep_vs_reference(name, cfg, seed, flags):
     got, _ = emu_run(L, cfg, seed, flags)
     res = refutil.compare_logs(refutil.ref_run_log(cfg, seed, flags), got)
     assert res["decision_ok"], (name, res)
+
+
+@pytest.mark.skipif(refutil.ref_lib() is None, reason="oracle/_ref not built")
+@pytest.mark.parametrize("name,cfg,seed,flags", refutil.edge_configs())
+def test_emulation_edge_configs_vs_reference(name, cfg, seed, flags):
+    L = emu()
+    got, t = emu_run(L, cfg, seed, flags)
+    res = refutil.compare_logs(refutil.ref_run_log(cfg, seed, flags), got)
+    assert res["decision_ok"], (name, res)
+    assert t.generated_tokens == t.committed_tokens + t.reused_tokens + t.wasted_tokens

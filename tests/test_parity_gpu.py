@@ -42,6 +42,14 @@ def test_sweep_matches_reference(name, cfg, seed, flags):
     _check(name, ref, got)
 
 
+@pytest.mark.parametrize("name,cfg,seed,flags", refutil.edge_configs())
+def test_edge_configs_match_reference(name, cfg, seed, flags):
+    spex = _spex()
+    if refutil.ref_lib() is None:
+        pytest.skip("oracle/_ref not built")
+    _check(name, refutil.ref_run_log(cfg, seed, flags), spex.run_once(cfg, seed, flags).log)
+
+
 @pytest.mark.parametrize("cfgname", ["c1_rebase_w4_q16", "c2_rebase_w16_q256", "c3_rstar_w4_q512",
                                      "c5_rebase_w32_q64"])
 def test_baseline_configs_match_reference(cfgname):
