@@ -208,6 +208,7 @@ struct Model {
   CUtensorMap a_xn, a_o, a_act;        // activation operands [max_rows][*]
   float* rope_tab = nullptr;           // [max_rows][dh/2] (cos, sin)
   float* lse_part = nullptr;           // [max_rows][V/128] float4
+  bool lm_tc = false;                  // LM head on the tcgen05 GEMM with the LSE epilogue (cuBLAS path)
   int* amax = nullptr;
   float* lse = nullptr;
   float* lsum = nullptr;
@@ -332,6 +333,16 @@ static Model* make_model(const ModelShape& sh, bool prm, uint64_t seed, long lon
     if (!prm) m->lse_part = dalloc<float>(M * (size_t)(sh.V / 128) * 4, o);
   }
   if (!m->use_tc && !prm) m->logits = dalloc<float>(M * sh.V, o);
+  // LM head + logsumexp/argmax fused on the tcgen05 GEMM (EPI_LSE) even on the
+  // cuBLAS path: the fp32 logits round trip (rows x V x 8 bytes) disappears
+  if (!m->use_tc && !prm && sh.V % 128 == 0 && sh.d % 64 == 0 && !getenv("SPEX_LM_CUBLAS")) {
+    m->tlm.N = sh.V;
+    m->tlm.K = sh.d;
+    if (spex_tmap_operand(&m->tlm.map, m->lm, sh.V, sh.d) == 0 && spex_tmap_operand(&m->a_xn, m->Xn, (long long)M, sh.d) == 0) {
+      m->lse_part = dalloc<float>(M * (size_t)(sh.V / 128) * 4, o);
+      m->lm_tc = true;
+    }
+  }
   return m;
 }
 
@@ -454,8 +465,18 @@ static void forward(Model& m, const RowDesc* rows, const Segment* segs, int M, c
   }
   spex_k_rmsnorm(m.X, M, s.d, s.eps, m.Xn, st);
   if (!m.is_prm) {
-    gemm(hb, m.Xn, m.lm, m.logits, M, s.V, s.d, false);
-    spex_k_lm_epilogue(m.logits, M, s.V, m.amax, m.lse, m.lsum, st);
+    if (m.lm_tc) {
+      TcEpilogue el{};
+      el.kind = TC_EPI_LSE;
+      el.part = m.lse_part;
+      el.n_tiles = s.V / 128;
+      el.V = s.V;
+      tc_gemm(m.a_xn, m.tlm, M, el, st);
+      spex_k_lse_combine(m.lse_part, M, s.V / 128, m.amax, m.lse, m.lsum, st);
+    } else {
+      gemm(hb, m.Xn, m.lm, m.logits, M, s.V, s.d, false);
+      spex_k_lm_epilogue(m.logits, M, s.V, m.amax, m.lse, m.lsum, st);
+    }
   }
 }
 
