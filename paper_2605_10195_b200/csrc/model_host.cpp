@@ -209,6 +209,7 @@ struct Model {
   float* rope_tab = nullptr;           // [max_rows][dh/2] (cos, sin)
   float* lse_part = nullptr;           // [max_rows][V/128] float4
   bool lm_tc = false;                  // LM head on the tcgen05 GEMM with the LSE epilogue (cuBLAS path)
+  bool tc_qkv = false, tc_gu = false;  // per-op tcgen05 (cuBLAS path, large row counts)
   int* amax = nullptr;
   float* lse = nullptr;
   float* lsum = nullptr;
@@ -333,6 +334,31 @@ static Model* make_model(const ModelShape& sh, bool prm, uint64_t seed, long lon
     if (!prm) m->lse_part = dalloc<float>(M * (size_t)(sh.V / 128) * 4, o);
   }
   if (!m->use_tc && !prm) m->logits = dalloc<float>(M * sh.V, o);
+  // Per-op tcgen05 on the cuBLAS path (policy decode, large row counts):
+  // QKV + RoPE/KV-append (SPEX_TC_QKV=1), gate/up + SwiGLU (SPEX_TC_GU=1)
+  if (!m->use_tc && !prm && sh.d % 64 == 0 && qkv_n % 128 == 0 && (sh.dh == 64 || sh.dh == 128) &&
+      spex_tmap_operand(&m->a_xn, m->Xn, (long long)M, sh.d) == 0) {
+    if (getenv("SPEX_TC_QKV")) {
+      m->tq.resize(sh.L);
+      m->tc_qkv = true;
+      for (int l = 0; l < sh.L; ++l) {
+        m->tq[l].N = qkv_n;
+        m->tq[l].K = sh.d;
+        if (spex_tmap_operand(&m->tq[l].map, m->wqkv[l], qkv_n, sh.d) != 0) m->tc_qkv = false;
+      }
+    }
+    if (getenv("SPEX_TC_GU") && (2 * sh.F) % 128 == 0 && sh.F % 64 == 0) {
+      m->tgu.resize(sh.L);
+      m->tc_gu = true;
+      for (int l = 0; l < sh.L; ++l) {
+        m->wgu_il.push_back(dalloc<__nv_bfloat16>((size_t)2 * sh.F * sh.d, o));
+        spex_k_interleave_gu(m->wgu[l], sh.F, sh.d, m->wgu_il.back(), st);
+        m->tgu[l].N = 2 * sh.F;
+        m->tgu[l].K = sh.d;
+        if (spex_tmap_operand(&m->tgu[l].map, m->wgu_il[l], 2 * sh.F, sh.d) != 0) m->tc_gu = false;
+      }
+    }
+  }
   // LM head + logsumexp/argmax fused on the tcgen05 GEMM (EPI_LSE) even on the
   // cuBLAS path: the fp32 logits round trip (rows x V x 8 bytes) disappears
   if (!m->use_tc && !prm && sh.V % 128 == 0 && sh.d % 64 == 0 && !getenv("SPEX_LM_CUBLAS")) {
@@ -354,6 +380,8 @@ static bool decode_mma_wanted(const ModelShape& s) {
   if (force >= 0) return force != 0;
   return s.dh == 128 && s.H / s.KVH >= 4;
 }
+
+constexpr int kTcMinRows = 1024;  // per-op tcgen05 below this row count loses to cuBLAS's small-M kernels
 
 static void tc_gemm(const CUtensorMap& a, const TcWeight& w, int M, const TcEpilogue& ep, cudaStream_t st) {
   if (spex_k_gemm_tc(&a, &w.map, M, w.N, w.K, &ep, st) != 0) throw std::runtime_error("tcgen05 GEMM launch failed");
@@ -438,8 +466,24 @@ static void forward(Model& m, const RowDesc* rows, const Segment* segs, int M, c
   spex_k_embed(rows, M, m.embed, s.d, m.X, st);
   for (int l = 0; l < s.L; ++l) {
     spex_k_rmsnorm(m.X, M, s.d, s.eps, m.Xn, st);
-    gemm_bf16out(hb, m.Xn, m.wqkv[l], m.QKV, M, (s.H + 2 * s.KVH) * s.dh, s.d);
-    spex_k_rope_kv(rows, M, m.QKV, s.H, s.KVH, s.dh, m.rope_tab, m.slots, m.Kp[l], m.Vp[l], m.Qr, st);
+    if (m.tc_qkv && M >= kTcMinRows) {
+      TcEpilogue eq{};
+      eq.kind = TC_EPI_ROPE_KV;
+      eq.rows = rows;
+      eq.rope = m.rope_tab;
+      eq.H = s.H;
+      eq.KVH = s.KVH;
+      eq.dh = s.dh;
+      eq.qscale = 1.0f / std::sqrt((float)s.dh);
+      eq.Qr = m.Qr;
+      eq.Kp = m.Kp[l];
+      eq.Vp = m.Vp[l];
+      eq.slots = m.slots;
+      tc_gemm(m.a_xn, m.tq[l], M, eq, st);
+    } else {
+      gemm_bf16out(hb, m.Xn, m.wqkv[l], m.QKV, M, (s.H + 2 * s.KVH) * s.dh, s.d);
+      spex_k_rope_kv(rows, M, m.QKV, s.H, s.KVH, s.dh, m.rope_tab, m.slots, m.Kp[l], m.Vp[l], m.Qr, st);
+    }
     if (timer) timer->begin(st);
     int rc = -1;
     if (tiles && !m.kmap.empty())
@@ -459,8 +503,16 @@ static void forward(Model& m, const RowDesc* rows, const Segment* segs, int M, c
     if (timer) timer->end(st);
     gemm(hb, m.O, m.wo[l], m.X, M, s.d, s.H * s.dh, true);
     spex_k_rmsnorm(m.X, M, s.d, s.eps, m.Xn, st);
-    gemm_bf16out(hb, m.Xn, m.wgu[l], m.GU, M, 2 * s.F, s.d);
-    spex_k_swiglu(m.GU, M, s.F, m.A, st);
+    if (m.tc_gu && M >= kTcMinRows) {
+      TcEpilogue eg{};
+      eg.kind = TC_EPI_SWIGLU;
+      eg.act = m.A;
+      eg.F = s.F;
+      tc_gemm(m.a_xn, m.tgu[l], M, eg, st);
+    } else {
+      gemm_bf16out(hb, m.Xn, m.wgu[l], m.GU, M, 2 * s.F, s.d);
+      spex_k_swiglu(m.GU, M, s.F, m.A, st);
+    }
     gemm(hb, m.A, m.wd[l], m.X, M, s.d, s.F, true);
   }
   spex_k_rmsnorm(m.X, M, s.d, s.eps, m.Xn, st);
