@@ -1,11 +1,12 @@
 // model_kernels.cu — device kernels of the policy / PRM forward over a batch
 // of tree rows (one token of one thought per row).
 //
-//   K1 tree_attn_kernel    decode attention over a thought's ancestor chain in
-//                          the paged tree KV pool: per (row, kv head) block,
-//                          64-token K/V chunks staged into shared memory by
-//                          cp.async.bulk (TMA bulk copy) with an mbarrier,
-//                          double-buffered, online softmax in fp32
+//   K1 tree attention over a thought's ancestor chain in the paged tree KV
+//                          pool: tree_attn_decode_kernel (decode rows, FHFMA.BF16),
+//                          tree_attn_chunk_kernel (bounded chunks, opt-in),
+//                          tree_attn_decode_mma_kernel (GQA decode on tensor cores),
+//                          tree_attn_tile_mma_kernel (PRM/prompt rows, TMA + mma.sync),
+//                          tree_attn_tile_kernel (PRM/prompt rows, dh = 64)
 //   K3 lm_epilogue_kernel  per-row argmax / logsumexp / checksum of the logits
 //   K4 value_head_kernel   PRM score sigmoid(w . h_last)
 //   plus weight init, row descriptors, embedding, RMSNorm->bf16, RoPE + KV
@@ -354,171 +355,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 constexpr int kChunk = 64;
 constexpr int kAttnThreads = 128;
 
-template <int DH, int G>
-__global__ void __launch_bounds__(kAttnThreads) tree_attn_kernel(const RowDesc* __restrict__ rows,
-                                                                const Segment* __restrict__ segs,
-                                                                const float* __restrict__ Qr, int H,
-                                                                const __nv_bfloat16* __restrict__ Kp,
-                                                                const __nv_bfloat16* __restrict__ Vp,
-                                                                long long slots,
-                                                                __nv_bfloat16* __restrict__ O) {
-  constexpr int VPL = DH / 32;  // elements per lane in a K row
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  __nv_bfloat16* sK = reinterpret_cast<__nv_bfloat16*>(smem_raw);            // [2][kChunk][DH]
-  __nv_bfloat16* sV = sK + 2 * kChunk * DH;                                     // [2][kChunk][DH]
-  float* sS = reinterpret_cast<float*>(sV + 2 * kChunk * DH);                  // [G][kChunk]
-  float* sAlpha = sS + G * kChunk;                                              // [G]
-  float* sL = sAlpha + G;                                                       // [G] running sum
-  float* sM = sL + G;                                                           // [G] running max
-  __shared__ uint64_t bar[2];
-
-  const int r = blockIdx.x;
-  const int kh = blockIdx.y;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const RowDesc rd = rows[r];
-  const Segment* sg = segs + rd.seg_off;
-  const __nv_bfloat16* Kh = Kp + (long long)kh * slots * DH;
-  const __nv_bfloat16* Vh = Vp + (long long)kh * slots * DH;
-
-  // q of the G heads of this group, VPL values per lane (log2e folded in)
-  float qreg[G][VPL];
-#pragma unroll
-  for (int g = 0; g < G; ++g)
-#pragma unroll
-    for (int v = 0; v < VPL; ++v)
-      qreg[g][v] = Qr[((long long)r * H + kh * G + g) * DH + lane * VPL + v] * 1.4426950408889634f;
-
-  // count chunks
-  int nchunks = 0;
-  for (int s = 0; s < rd.nseg; ++s) nchunks += (sg[s].len + kChunk - 1) / kChunk;
-
-  if (tid < G) {
-    sM[tid] = -INFINITY;
-    sL[tid] = 0.f;
-  }
-  if (tid == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-
-  // chunk cursor (identical in every thread)
-  int seg_i = 0, seg_o = 0;
-  auto next_chunk = [&](long long* base, int* len) {
-    while (seg_i < rd.nseg && seg_o >= sg[seg_i].len) {
-      ++seg_i;
-      seg_o = 0;
-    }
-    *base = sg[seg_i].base + seg_o;
-    int l = sg[seg_i].len - seg_o;
-    *len = l < kChunk ? l : kChunk;
-    seg_o += *len;
-  };
-  long long cb[2];
-  int cl[2];
-  // prologue: issue chunk 0 (and 1)
-  for (int c = 0; c < 2 && c < nchunks; ++c) {
-    next_chunk(&cb[c], &cl[c]);
-    if (tid == 0) {
-      const uint32_t bytes = (uint32_t)cl[c] * DH * 2;
-      mbar_expect_tx(&bar[c], 2 * bytes);
-      bulk_g2s(sK + c * kChunk * DH, Kh + cb[c] * DH, bytes, &bar[c]);
-      bulk_g2s(sV + c * kChunk * DH, Vh + cb[c] * DH, bytes, &bar[c]);
-    }
-  }
-
-  // accumulators: thread handles output dims (g, d) for d = tid % DH
-  constexpr int OUT_PER_THREAD = (G * DH + kAttnThreads - 1) / kAttnThreads;
-  float acc[OUT_PER_THREAD];
-#pragma unroll
-  for (int k = 0; k < OUT_PER_THREAD; ++k) acc[k] = 0.f;
-
-  for (int c = 0; c < nchunks; ++c) {
-    const int buf = c & 1;
-    const int len = cl[buf];
-    mbar_wait(&bar[buf], (uint32_t)((c >> 1) & 1));
-    const __nv_bfloat16* K = sK + buf * kChunk * DH;
-    const __nv_bfloat16* Vs = sV + buf * kChunk * DH;
-    // scores
-    for (int t = warp; t < len; t += kAttnThreads / 32) {
-      float kv[VPL];
-#pragma unroll
-      for (int v2 = 0; v2 < VPL / 2; ++v2) {
-        const __nv_bfloat162 a = *reinterpret_cast<const __nv_bfloat162*>(K + t * DH + lane * VPL + 2 * v2);
-        kv[2 * v2] = __low2float(a);
-        kv[2 * v2 + 1] = __high2float(a);
-      }
-#pragma unroll
-      for (int g = 0; g < G; ++g) {
-        float s = 0.f;
-#pragma unroll
-        for (int v = 0; v < VPL; ++v) s += qreg[g][v] * kv[v];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        if (lane == 0) sS[g * kChunk + t] = s;
-      }
-    }
-    __syncthreads();
-    // online softmax per head (warp g handles head g)
-    for (int g = warp; g < G; g += kAttnThreads / 32) {
-      float mx = -INFINITY;
-      for (int t = lane; t < len; t += 32) mx = fmaxf(mx, sS[g * kChunk + t]);
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-      const float m_old = sM[g];
-      const float l_old = sL[g];
-      const float m_new = fmaxf(m_old, mx);
-      float sum = 0.f;
-      for (int t = lane; t < len; t += 32) {
-        const float p = exp2f(sS[g * kChunk + t] - m_new);
-        sS[g * kChunk + t] = p;
-        sum += p;
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-      const float alpha = exp2f(m_old - m_new);
-      __syncwarp();
-      if (lane == 0) {
-        sM[g] = m_new;
-        sL[g] = l_old * alpha + sum;
-        sAlpha[g] = alpha;
-      }
-    }
-    __syncthreads();
-    // PV
-#pragma unroll
-    for (int k = 0; k < OUT_PER_THREAD; ++k) {
-      const int o = tid + k * kAttnThreads;
-      if (o < G * DH) {
-        const int g = o / DH, dcol = o % DH;
-        float a = acc[k] * sAlpha[g];
-        const float* p = sS + g * kChunk;
-        for (int t = 0; t < len; ++t) a += p[t] * __bfloat162float(Vs[t * DH + dcol]);
-        acc[k] = a;
-      }
-    }
-    __syncthreads();
-    // refill this buffer with chunk c + 2
-    if (c + 2 < nchunks) {
-      next_chunk(&cb[buf], &cl[buf]);
-      if (tid == 0) {
-        const uint32_t bytes = (uint32_t)cl[buf] * DH * 2;
-        mbar_expect_tx(&bar[buf], 2 * bytes);
-        bulk_g2s(sK + buf * kChunk * DH, Kh + cb[buf] * DH, bytes, &bar[buf]);
-        bulk_g2s(sV + buf * kChunk * DH, Vh + cb[buf] * DH, bytes, &bar[buf]);
-      }
-    }
-  }
-#pragma unroll
-  for (int k = 0; k < OUT_PER_THREAD; ++k) {
-    const int o = tid + k * kAttnThreads;
-    if (o < G * DH) {
-      const int g = o / DH, dcol = o % DH;
-      O[((long long)r * H + kh * G + g) * DH + dcol] = __float2bfloat16_rn(acc[k] / sL[g]);
-    }
-  }
-}
 
 // K1 decode variant: one warp per (row, kv head) streams the row's context with
 // 128-bit coalesced loads — a half-warp covers one 256-byte K (or V) row, so a
@@ -1808,33 +1644,15 @@ static void launch_attn_decode(const RowDesc* rows, const Segment* segs, const f
     tree_attn_decode_kernel<DH, G, 4><<<blocks, 256, 0, s>>>(rows, segs, Qr, H, KVH, M, Kp, Vp, slots, O);
 }
 
-template <int DH, int G>
-static void launch_attn(const RowDesc* rows, const Segment* segs, const float* Qr, int H, int KVH,
-                        const __nv_bfloat16* Kp, const __nv_bfloat16* Vp, long long slots, __nv_bfloat16* O, int M,
-                        cudaStream_t s) {
-  const size_t smem = 4 * kChunk * DH * sizeof(__nv_bfloat16) + (G * kChunk + 3 * G) * sizeof(float) + 64;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(tree_attn_kernel<DH, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
-  dim3 grid(M, KVH);
-  tree_attn_kernel<DH, G><<<grid, kAttnThreads, smem, s>>>(rows, segs, Qr, H, Kp, Vp, slots, O);
-}
 
-static int g_attn_staged = -1;
 
 extern "C" int spex_k_tree_attn(const RowDesc* rows, const Segment* segs, const float* Qr, int H, int KVH, int dh,
                                 const __nv_bfloat16* Kp, const __nv_bfloat16* Vp, long long slots, __nv_bfloat16* O,
                                 int M, cudaStream_t s) {
   const int G = H / KVH;
-  if (g_attn_staged < 0) g_attn_staged = getenv("SPEX_ATTN_STAGED") ? 1 : 0;
 #define SPEX_ATTN_CASE(D, GG)                                                   \
   if (dh == D && G == GG) {                                                     \
-    if (g_attn_staged)                                                          \
-      launch_attn<D, GG>(rows, segs, Qr, H, KVH, Kp, Vp, slots, O, M, s);       \
-    else                                                                        \
-      launch_attn_decode<D, GG>(rows, segs, Qr, H, KVH, Kp, Vp, slots, O, M, s); \
+    launch_attn_decode<D, GG>(rows, segs, Qr, H, KVH, Kp, Vp, slots, O, M, s);   \
     return 0;                                                                   \
   }
   SPEX_ATTN_CASE(128, 1)
