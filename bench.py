@@ -381,7 +381,7 @@ def main():
         "thoughts_per_s": agg["prm_thoughts"] / dev_s,
         "named_model_shapes": named,
         "gpu_launches": int(agg["launches"]),
-        "roofline": {"bound": "hbm", "kernel": "K1 tree_attn_kernel (policy decode)",
+        "roofline": {"bound": "hbm", "kernel": "K1 tree_attn_bulk_kernel (policy decode rows, bulk-copy pipeline)",
                      "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                      "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
                      "traffic_alg_bytes_same_launches": traffic_alg,

@@ -57,6 +57,9 @@ int spex_k_tree_attn(const RowDesc* rows, const Segment* segs, const float* Qr, 
                      const __nv_bfloat16* Kp, const __nv_bfloat16* Vp, long long slots, __nv_bfloat16* O, int M,
                      cudaStream_t s);
 void spex_k_build_decode_chunks(const RowDesc* rows, const Segment* segs, int M, DecodeChunks w, cudaStream_t s);
+int spex_k_tree_attn_bulk(const RowDesc* rows, const Segment* segs, const float* Qr, int H, int KVH, int dh,
+                          const __nv_bfloat16* Kp, const __nv_bfloat16* Vp, long long slots, __nv_bfloat16* O, int M,
+                          int* item_ctr, cudaStream_t s);
 int spex_k_tree_attn_decode_mma(const CUtensorMap* kmap, const CUtensorMap* vmap, const RowDesc* rows,
                                 const Segment* segs, const float* Qr, int H, int KVH, int dh, long long slots,
                                 __nv_bfloat16* O, int M, cudaStream_t s);
@@ -381,6 +384,15 @@ static bool decode_mma_wanted(const ModelShape& s) {
   return s.dh == 128 && s.H / s.KVH >= 4;
 }
 
+// Decode rows with one KV head per query head (G = 1) stream through the
+// bulk-copy pipeline kernel (measured 1.98 s vs 2.10 s per c2 search for the
+// register-pipelined FHFMA kernel); SPEX_K1_BULK=0 selects the latter.
+static bool bulk_wanted() {
+  static const bool on = !getenv("SPEX_K1_BULK") || atoi(getenv("SPEX_K1_BULK")) != 0;
+  return on;
+}
+static int* g_item_ctr = nullptr;  // K1 bulk kernel's work counter (policy stream)
+
 constexpr int kTcMinRows = 1024;  // per-op tcgen05 below this row count loses to cuBLAS's small-M kernels
 
 static void tc_gemm(const CUtensorMap& a, const TcWeight& w, int M, const TcEpilogue& ep, cudaStream_t st) {
@@ -492,6 +504,9 @@ static void forward(Model& m, const RowDesc* rows, const Segment* segs, int M, c
     if (rc != 0 && !tiles && !m.kmap.empty() && decode_mma_wanted(s))
       rc = spex_k_tree_attn_decode_mma(&m.kmap[l], &m.vmap[l], rows, segs, m.Qr, s.H, s.KVH, s.dh, m.slots, m.O, M,
                                        st);
+    if (rc != 0 && !tiles && bulk_wanted() && g_item_ctr)
+      rc = spex_k_tree_attn_bulk(rows, segs, m.Qr, s.H, s.KVH, s.dh, m.Kp[l], m.Vp[l], m.slots, m.O, M, g_item_ctr,
+                                 st);
     if (rc != 0 && chunks)
       rc = spex_k_tree_attn_chunked(rows, segs, m.Qr, s.H, s.KVH, s.dh, m.Kp[l], m.Vp[l], m.slots, m.O, *chunks, l,
                                     st);
@@ -604,6 +619,7 @@ struct ModelCache {
   RowDesc* rows2 = nullptr;
   Segment* segs2 = nullptr;
   TileDesc* tiles2 = nullptr;
+  int* item_ctr = nullptr;  // K1 bulk kernel's work counter (policy stream)
   // decode work list (K1 chunked), sized for rows_cap rows of the policy shape
   DecodeChunks dc{};
   int dc_rows = 0;
@@ -703,6 +719,11 @@ void run_model_schedule(const ModelRunConfig& mc, const ScheduleView& sv, ModelR
   // capacity actually resident (a cached pool may be larger than this run's request)
   const long long cap_slots = prm ? std::min(pol->slots, prm->slots) : pol->slots;
   const int rows_cap = std::max({max_dec, max_prm, prompt_chunk * P, 1});
+  if (!g_cache.item_ctr) {
+    std::vector<void*> keep;
+    g_cache.item_ctr = dalloc<int>(64, keep);
+    g_item_ctr = g_cache.item_ctr;
+  }
   if (g_cache.rows_cap < rows_cap) {
     CK(cudaStreamSynchronize(st));
     CK(cudaStreamSynchronize(g_cache.st2));

@@ -556,6 +556,174 @@ __global__ void __launch_bounds__(1024) build_decode_chunks_kernel(const RowDesc
   if (tid == 1023) *w.n_items = sums[1023];
 }
 
+// K1 decode, bulk-copy pipeline (G = 1): a persistent grid of warps; each warp
+// claims (row, kv head) items from a device counter and streams their tree
+// context through its own ring of NST shared-memory stages of CH tokens (K and
+// V rows of one head are contiguous in the pool, so a stage is two
+// cp.async.bulk copies completing on one mbarrier). The copy engine keeps
+// NST-1 chunks in flight per warp across item and segment boundaries without
+// holding registers; lanes read the staged rows with 128-bit shared loads
+// (half a warp per 256-byte row) into the same FHFMA.BF16 math as
+// tree_attn_decode_kernel, one online-softmax update per chunk.
+template <int kBulkCH, int kBulkNST, int kBulkWarps>  // tokens per stage, stages per warp, warps per block
+__global__ void __launch_bounds__(kBulkWarps * 32, 1)
+    tree_attn_bulk_kernel(const RowDesc* __restrict__ rows, const Segment* __restrict__ segs,
+                          const float* __restrict__ Qr, int H, int KVH, int n_items,
+                          const __nv_bfloat16* __restrict__ Kp, const __nv_bfloat16* __restrict__ Vp, long long slots,
+                          __nv_bfloat16* __restrict__ O, int* __restrict__ item_ctr) {
+  constexpr int DH = 128, EPL = 8, LPT = 16, STAGE = kBulkCH * DH * 2;  // 4 KB of K (and of V) per stage
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ uint64_t bar[kBulkWarps][kBulkNST];
+  __shared__ int queue[kBulkWarps][8];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned char* ring = smem_raw + (size_t)warp * kBulkNST * 2 * STAGE;  // [stage][K|V][STAGE]
+  const int sub = lane / LPT, li = lane % LPT;
+  if (lane == 0) {
+    for (int i = 0; i < kBulkNST; ++i) mbar_init(&bar[warp][i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  // ---- producer cursor (lane 0 only): item, segment, offset
+  int p_q = 0;                   // items claimed so far (queue position)
+  int p_item = -1, p_seg = 0, p_off = 0, p_nseg = 0;
+  long long p_segoff = 0;
+  const Segment* p_sg = nullptr;
+  bool p_done = false;
+  int issued = 0;
+  auto produce = [&]() {  // lane 0: issue the next chunk into stage issued % NST
+    while (!p_done) {
+      if (p_item < 0 || p_seg >= p_nseg) {  // next item
+        const int it = atomicAdd(item_ctr, 1);
+        if (it >= n_items) {
+          queue[warp][p_q & 7] = -1;
+          p_done = true;
+          return;
+        }
+        queue[warp][p_q & 7] = it;
+        ++p_q;
+        p_item = it;
+        const RowDesc rd = rows[it / KVH];
+        p_sg = segs + rd.seg_off;
+        p_nseg = rd.nseg;
+        p_seg = 0;
+        p_off = 0;
+        p_segoff = (long long)(it % KVH) * slots;
+      }
+      const int len = p_sg[p_seg].len;
+      if (p_off >= len) {
+        ++p_seg;
+        p_off = 0;
+        continue;
+      }
+      const int n = min(kBulkCH, len - p_off);
+      const long long tok = p_segoff + p_sg[p_seg].base + p_off;
+      const int st = issued % kBulkNST;
+      unsigned char* kb = ring + st * 2 * STAGE;
+      mbar_expect_tx(&bar[warp][st], 2u * n * DH * 2);
+      bulk_g2s(kb, Kp + tok * DH, n * DH * 2, &bar[warp][st]);
+      bulk_g2s(kb + STAGE, Vp + tok * DH, n * DH * 2, &bar[warp][st]);
+      p_off += n;
+      ++issued;
+      return;
+    }
+  };
+  if (lane == 0)
+    for (int i = 0; i < kBulkNST - 1; ++i) produce();
+  __syncwarp();
+  // ---- consumer cursor (all lanes)
+  int c_q = 0, consumed = 0;
+  for (;;) {
+    const int it = queue[warp][c_q & 7];
+    if (it < 0) break;
+    ++c_q;
+    const int r = it / KVH, kh = it % KVH;
+    const RowDesc rd = rows[r];
+    const Segment* sg = segs + rd.seg_off;
+    uint32_t q2[EPL / 2];
+    {
+      const float4* qp = reinterpret_cast<const float4*>(Qr + ((long long)r * H + kh) * DH + li * EPL);
+      const float4 a = qp[0], b = qp[1];
+      constexpr float L2E = 1.4426950408889634f;
+      q2[0] = pack_bf16(a.x * L2E, a.y * L2E);
+      q2[1] = pack_bf16(a.z * L2E, a.w * L2E);
+      q2[2] = pack_bf16(b.x * L2E, b.y * L2E);
+      q2[3] = pack_bf16(b.z * L2E, b.w * L2E);
+    }
+    float m = -INFINITY, l = 0.f, acc[EPL];
+#pragma unroll
+    for (int e = 0; e < EPL; ++e) acc[e] = 0.f;
+    for (int si = 0; si < rd.nseg; ++si) {
+      const int len = sg[si].len;
+      for (int off = 0; off < len; off += kBulkCH) {
+        const int n = min(kBulkCH, len - off);
+        if (lane == 0) produce();  // keep NST-1 chunks in flight (stage consumed last round is free)
+        const int st = consumed % kBulkNST;
+        mbar_wait(&bar[warp][st], (uint32_t)((consumed / kBulkNST) & 1));
+        const unsigned char* kb = ring + st * 2 * STAGE;
+        float sc[kBulkCH / 2];
+        uint4 vr[kBulkCH / 2];
+#pragma unroll
+        for (int u = 0; u < kBulkCH / 2; ++u) {
+          const int t = 2 * u + sub;
+          const uint4 kr = *reinterpret_cast<const uint4*>(kb + t * DH * 2 + li * 16);
+          vr[u] = *reinterpret_cast<const uint4*>(kb + STAGE + t * DH * 2 + li * 16);
+          float a = 0.f;
+          fma2_bf16(a, q2[0], kr.x);
+          fma2_bf16(a, q2[1], kr.y);
+          fma2_bf16(a, q2[2], kr.z);
+          fma2_bf16(a, q2[3], kr.w);
+          sc[u] = a;
+        }
+#pragma unroll
+        for (int o = LPT / 2; o > 0; o >>= 1)
+#pragma unroll
+          for (int u = 0; u < kBulkCH / 2; ++u) sc[u] += __shfl_xor_sync(0xffffffffu, sc[u], o);
+        float mx = -INFINITY;
+#pragma unroll
+        for (int u = 0; u < kBulkCH / 2; ++u) {
+          if (2 * u + sub >= n) sc[u] = -INFINITY;
+          mx = fmaxf(mx, sc[u]);
+        }
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, LPT));
+        if (mx > m) {  // warp-uniform
+          const float scale = exp2f(m - mx);
+          l *= scale;
+#pragma unroll
+          for (int e = 0; e < EPL; ++e) acc[e] *= scale;
+          m = mx;
+        }
+#pragma unroll
+        for (int u = 0; u < kBulkCH / 2; ++u) {
+          if (2 * u + sub < n) {  // staged rows beyond n are stale: never touch them
+            const __nv_bfloat16 pb = __float2bfloat16_rn(exp2f(sc[u] - m));
+            l += __bfloat162float(pb);
+            const uint32_t p2 = (uint32_t)__bfloat16_as_ushort(pb) * 0x10001u;
+            fma_pv_bf16(acc[0], acc[1], p2, vr[u].x);
+            fma_pv_bf16(acc[2], acc[3], p2, vr[u].y);
+            fma_pv_bf16(acc[4], acc[5], p2, vr[u].z);
+            fma_pv_bf16(acc[6], acc[7], p2, vr[u].w);
+          }
+        }
+        ++consumed;
+        __syncwarp();  // stage st fully read before lane 0 refills it
+      }
+    }
+    // combine the two token halves, write O
+    l += __shfl_xor_sync(0xffffffffu, l, LPT);
+#pragma unroll
+    for (int e = 0; e < EPL; ++e) acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], LPT);
+    if (sub == 0) {
+      const float inv = 1.f / l;
+      uint4 packed;
+      packed.x = pack_bf16(acc[0] * inv, acc[1] * inv);
+      packed.y = pack_bf16(acc[2] * inv, acc[3] * inv);
+      packed.z = pack_bf16(acc[4] * inv, acc[5] * inv);
+      packed.w = pack_bf16(acc[6] * inv, acc[7] * inv);
+      *reinterpret_cast<uint4*>(O + ((long long)r * H + kh) * DH + li * EPL) = packed;
+    }
+  }
+}
+
 // K1 decode, chunked: a persistent grid of warps pulls (chunk, kv head) work
 // from a device queue; each streams its chunk of the row's tree context with
 // 128-bit loads and FHFMA.BF16 (as tree_attn_decode_kernel). Single-chunk rows
@@ -1665,6 +1833,51 @@ extern "C" int spex_k_tree_attn(const RowDesc* rows, const Segment* segs, const 
   SPEX_ATTN_CASE(64, 4)
 #undef SPEX_ATTN_CASE
   return -1;
+}
+
+// K1 decode rows through the bulk-copy pipeline (G = 1, dh = 128); item_ctr is
+// a zeroed device int per launch.
+template <int CH, int NST, int W>
+static int launch_bulk(const RowDesc* rows, const Segment* segs, const float* Qr, int H, int KVH,
+                       const __nv_bfloat16* Kp, const __nv_bfloat16* Vp, long long slots, __nv_bfloat16* O, int M,
+                       int* item_ctr, cudaStream_t s) {
+  const size_t smem = (size_t)W * NST * 2 * CH * 128 * 2;
+  static int blocks = 0;
+  if (!blocks) {
+    cudaFuncSetAttribute(tree_attn_bulk_kernel<CH, NST, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    blocks = sms;
+  }
+  const int n_items = M * KVH;
+  const int grid = std::min(blocks, (n_items + W - 1) / W);
+  cudaMemsetAsync(item_ctr, 0, sizeof(int), s);
+  tree_attn_bulk_kernel<CH, NST, W><<<grid, W * 32, smem, s>>>(rows, segs, Qr, H, KVH, n_items, Kp, Vp, slots, O,
+                                                               item_ctr);
+  return (int)cudaGetLastError();
+}
+
+// K1 decode rows through the bulk-copy pipeline (G = 1, dh = 128); item_ctr is
+// a device int (zeroed here per launch).
+extern "C" int spex_k_tree_attn_bulk(const RowDesc* rows, const Segment* segs, const float* Qr, int H, int KVH, int dh,
+                                     const __nv_bfloat16* Kp, const __nv_bfloat16* Vp, long long slots,
+                                     __nv_bfloat16* O, int M, int* item_ctr, cudaStream_t s) {
+  if (M <= 0) return 0;
+  if (dh != 128 || H != KVH) return -1;
+  static const int cfg = getenv("SPEX_K1_BULK_CFG") ? atoi(getenv("SPEX_K1_BULK_CFG")) : 0;
+  switch (cfg) {
+    case 1: return launch_bulk<8, 3, 16>(rows, segs, Qr, H, KVH, Kp, Vp, slots, O, M, item_ctr, s);
+    case 2: return launch_bulk<16, 2, 12>(rows, segs, Qr, H, KVH, Kp, Vp, slots, O, M, item_ctr, s);
+    case 3: return launch_bulk<32, 2, 6>(rows, segs, Qr, H, KVH, Kp, Vp, slots, O, M, item_ctr, s);
+    case 4: return launch_bulk<8, 2, 24>(rows, segs, Qr, H, KVH, Kp, Vp, slots, O, M, item_ctr, s);
+    case 5: return launch_bulk<16, 2, 14>(rows, segs, Qr, H, KVH, Kp, Vp, slots, O, M, item_ctr, s);
+    case 6: return launch_bulk<8, 3, 18>(rows, segs, Qr, H, KVH, Kp, Vp, slots, O, M, item_ctr, s);
+    case 7: return launch_bulk<8, 4, 14>(rows, segs, Qr, H, KVH, Kp, Vp, slots, O, M, item_ctr, s);
+    case 8: return launch_bulk<16, 3, 8>(rows, segs, Qr, H, KVH, Kp, Vp, slots, O, M, item_ctr, s);
+    default:  // measured best on c2 (tools: SPEX_K1_BULK_CFG sweep)
+      return launch_bulk<16, 2, 14>(rows, segs, Qr, H, KVH, Kp, Vp, slots, O, M, item_ctr, s);
+  }
 }
 
 extern "C" void spex_k_build_decode_chunks(const RowDesc* rows, const Segment* segs, int M, DecodeChunks w,

@@ -81,7 +81,7 @@ def _make_tree_rows(rng, M, slots, max_depth):
     return rows, segs, paths
 
 
-@pytest.mark.parametrize("impl", ["row", "chunked", "mma"])
+@pytest.mark.parametrize("impl", ["row", "chunked", "mma", "bulk"])
 @pytest.mark.parametrize("H,KVH,dh,M", [(8, 8, 128, 300), (32, 8, 128, 97), (12, 2, 128, 80), (4, 2, 64, 150), (16, 4, 64, 64)])
 def test_k1_decode_matches_torch_fp32(H, KVH, dh, M, impl):
     """impl "row": one warp per (row, kv head) (spex_k_tree_attn); "chunked": the
@@ -105,6 +105,19 @@ def test_k1_decode_matches_torch_fp32(H, KVH, dh, M, impl):
     if impl == "row":
         rc = f(rows_d.data_ptr(), segs_d.data_ptr(), Q.data_ptr(), H, KVH, dh, K.data_ptr(), V.data_ptr(), slots,
                O.data_ptr(), M, st.cuda_stream)
+        assert rc == 0
+    elif impl == "bulk":
+        if dh != 128 or H != KVH:
+            pytest.skip("bulk-copy decode kernel is dh=128, G=1")
+        from paper_2605_10195_b200 import _lib as L
+        fb = L.lib().spex_k_tree_attn_bulk
+        fb.restype = ctypes.c_int
+        fb.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                       ctypes.c_void_p, ctypes.c_void_p, ctypes.c_longlong, ctypes.c_void_p, ctypes.c_int,
+                       ctypes.c_void_p, ctypes.c_void_p]
+        ctr = torch.zeros(1, dtype=torch.int32, device=dev)
+        rc = fb(rows_d.data_ptr(), segs_d.data_ptr(), Q.data_ptr(), H, KVH, dh, K.data_ptr(), V.data_ptr(), slots,
+                O.data_ptr(), M, ctr.data_ptr(), st.cuda_stream)
         assert rc == 0
     elif impl == "mma":
         if dh != 128:

@@ -22,6 +22,6 @@ if [ "$MODE" = "full" ]; then
     python tools/model_timing.py c2_rebase_w16_q256 mid_policy mid_prm > $OUT/ncu_gemm_$TAG.log 2>&1
 fi
 SPEX_ATTN_LOG=$OUT/k1_bytes_$TAG.txt timeout 900 ncu --set full --clock-control none --import-source on \
-  -k 'regex:tree_attn_(decode|chunk)' -s 400 -c 3 -o $OUT/k1_$TAG \
+  -k 'regex:tree_attn_(decode|chunk|bulk)' -s 400 -c 3 -o $OUT/k1_$TAG \
   python tools/model_timing.py c2_rebase_w16_q256 mid_policy mid_prm > $OUT/ncu_k1_$TAG.log 2>&1
 echo done
