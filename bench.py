@@ -32,6 +32,10 @@ from pathlib import Path
 
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
+# concurrent searches (control_only) each run on their own stream: give the
+# device 32 hardware queues instead of 8 so independent control CTAs do not
+# serialise behind each other (read at CUDA initialisation)
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 
 DEFAULT_CONFIG = "c2_rebase_w16_q256"
 PEAKS = ROOT / "MEASURED_PEAKS.json"
@@ -49,6 +53,8 @@ def parse():
     ap.add_argument("--policy", default="mid_policy")
     ap.add_argument("--prm", default="mid_prm")
     ap.add_argument("--cpu-sample-runs", type=int, default=4)
+    ap.add_argument("--control-only", type=int, default=64,
+                    help="also time N concurrent control-only searches (no model), 0 = off")
     ap.add_argument("--named-shapes", type=int, default=1,
                     help="also time config 5 with the Llama-3-8B-shaped policy + 1.5B-shaped PRM (1 = on)")
     return ap.parse_args()
@@ -289,6 +295,32 @@ def main():
             e2e_d2h += d2h
         barrier()
         tr_wall = time.perf_counter() - t2
+    # the search path alone, as the reference arm runs it (virtual decode, no
+    # model): each search is one control CTA on its own SM, so many run at once
+    ctl_only = None
+    if args.control_only > 0:
+        def ctl_search(out, k):
+            ex = spex.Executor(cfg_text, seed + k, None, trace=False, device=local)
+            t = ex.run()
+            out[k] = (t.queries, ex.stats()["device_ms"])
+            ex.close()
+
+        def ctl_round(n):
+            res = [None] * n
+            ths = [threading.Thread(target=ctl_search, args=(res, k)) for k in range(n)]
+            t0 = time.perf_counter()
+            for th in ths:
+                th.start()
+            for th in ths:
+                th.join()
+            return res, time.perf_counter() - t0
+
+        ctl_round(min(8, args.control_only))  # warm-up
+        res, wall_c = ctl_round(args.control_only)
+        ctl_only = {"concurrent_searches": args.control_only, "queries_per_s": sum(r[0] for r in res) / wall_c,
+                    "wall_s": wall_c, "per_search_device_ms_median": statistics.median(r[1] for r in res),
+                    "note": "device control kernel only (the reference arm's virtual-clock decode, no model), "
+                            "one CTA per search, searches on concurrent host threads; compare with --impl reference"}
     # the named model shapes (north star): config 5, Llama-3-8B-shaped policy +
     # 1.5B-shaped PRM, one warm + one timed search on this GPU
     named = None
@@ -380,6 +412,7 @@ def main():
                                     "device step time of one warm search each"},
         "thoughts_per_s": agg["prm_thoughts"] / dev_s,
         "named_model_shapes": named,
+        "control_only": ctl_only,
         "gpu_launches": int(agg["launches"]),
         "roofline": {"bound": "hbm", "kernel": "K1 tree_attn_bulk_kernel (policy decode rows, bulk-copy pipeline)",
                      "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",

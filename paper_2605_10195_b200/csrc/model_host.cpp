@@ -673,6 +673,22 @@ static Model* cached(Model*& slot, const ModelShape& sh, bool prm, uint64_t seed
   return slot;
 }
 
+// Frees cached models whose shape or seed differ from the next run's (before
+// the caller sizes the KV pools from the free memory).
+extern "C" void spex_model_cache_release_mismatch(const ModelRunConfig* mc) {
+  const bool seed_ok = g_cache.seed == mc->seed;
+  if (g_cache.pol && (!seed_ok || !same_shape(g_cache.pol->sh, mc->policy))) {
+    cudaDeviceSynchronize();
+    delete g_cache.pol;
+    g_cache.pol = nullptr;
+  }
+  if (g_cache.prm && (!seed_ok || !mc->with_prm || !same_shape(g_cache.prm->sh, mc->prm))) {
+    cudaDeviceSynchronize();
+    delete g_cache.prm;
+    g_cache.prm = nullptr;
+  }
+}
+
 extern "C" void spex_model_cache_clear() {
   delete g_cache.pol;
   delete g_cache.prm;

@@ -475,6 +475,7 @@ extern "C" int spex_launch_control(Run* d_run, int n_queries, int nthreads, cuda
 extern "C" int spex_launch_control_async(Run* d_run, int n_queries, int nthreads, cudaStream_t stream, cudaEvent_t a,
                                          cudaEvent_t b);
 extern "C" void spex_model_cache_clear();
+extern "C" void spex_model_cache_release_mismatch(const ModelRunConfig* mc);
 #define CUDA_OK(x)                                                                  \
   do {                                                                              \
     cudaError_t e_ = (x);                                                           \
@@ -863,7 +864,9 @@ void run_executor(spex_executor& ex, int trace) {
     if (!ex.stream) CUDA_OK(cudaStreamCreateWithFlags(&ex.stream, cudaStreamNonBlocking));
     if (!ex.mstream) CUDA_OK(cudaStreamCreateWithFlags(&ex.mstream, cudaStreamNonBlocking));
     char* base = nullptr;
-    CUDA_OK(cudaMalloc(&base, A.total + 256));
+    // stream-ordered allocations: concurrent searches (one control CTA each)
+    // never synchronise the device through cudaMalloc/cudaFree
+    CUDA_OK(cudaMallocAsync(reinterpret_cast<void**>(&base), A.total + 256, ex.stream));
     CUDA_OK(cudaMemsetAsync(base, 0, A.total + 256, ex.stream));
     A.carve(base);
     // Keep the control state L2-resident while the forward streams tens of GB
@@ -876,7 +879,11 @@ void run_executor(spex_executor& ex, int trace) {
       if (max_win > 0 && max_persist > 0) {
         const size_t win = std::min<size_t>(A.hot, static_cast<size_t>(max_win));
         const size_t per = std::min<size_t>(win, static_cast<size_t>(max_persist));
-        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, per);
+        static size_t persist_set = 0;  // set once per process (may synchronize the device)
+        if (persist_set < per) {
+          cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, per);
+          persist_set = per;
+        }
         cudaStreamAttrValue av{};
         av.accessPolicyWindow.base_ptr = base;
         av.accessPolicyWindow.num_bytes = win;
@@ -891,7 +898,7 @@ void run_executor(spex_executor& ex, int trace) {
                      A.hot, max_win, max_persist);
     }
     double* d_tab = nullptr;
-    CUDA_OK(cudaMalloc(&d_tab, tab.size() * sizeof(double)));
+    CUDA_OK(cudaMallocAsync(reinterpret_cast<void**>(&d_tab), tab.size() * sizeof(double), ex.stream));
     CUDA_OK(cudaMemcpyAsync(d_tab, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice,
                             ex.stream));
     R.log_tab = d_tab;
@@ -908,12 +915,13 @@ void run_executor(spex_executor& ex, int trace) {
     }
     mark("arena+pinned");
     Run* d_run = nullptr;
-    CUDA_OK(cudaMalloc(&d_run, sizeof(Run)));
+    CUDA_OK(cudaMallocAsync(reinterpret_cast<void**>(&d_run), sizeof(Run), ex.stream));
     CUDA_OK(cudaMemcpyAsync(d_run, &R, sizeof(Run), cudaMemcpyHostToDevice, ex.stream));
     auto cleanup = [&] {
-      cudaFree(base);
-      cudaFree(d_tab);
-      cudaFree(d_run);
+      cudaFreeAsync(base, ex.stream);
+      cudaFreeAsync(d_tab, ex.stream);
+      cudaFreeAsync(d_run, ex.stream);
+      cudaStreamSynchronize(ex.stream);
       if (h_head) cudaFreeHost(h_head);
       if (h_ents) cudaFreeHost(h_ents);
     };
@@ -954,7 +962,9 @@ void run_executor(spex_executor& ex, int trace) {
     ex.mres = ModelRunResult{};
     if (streaming) {
       CUDA_OK(cudaStreamSynchronize(ex.stream));
-      // KV pool capacity from the free-memory budget (both models, all layers)
+      // KV pool capacity from the free-memory budget (both models, all layers),
+      // after releasing cached models of other shapes
+      spex_model_cache_release_mismatch(&mc);
       size_t free_b = 0, total_b = 0;
       cudaMemGetInfo(&free_b, &total_b);
       const double per_slot = 4.0 * (mc.policy.L * mc.policy.KVH * mc.policy.dh +
