@@ -60,6 +60,9 @@ void spex_k_build_decode_chunks(const RowDesc* rows, const Segment* segs, int M,
 int spex_k_tree_attn_bulk(const RowDesc* rows, const Segment* segs, const float* Qr, int H, int KVH, int dh,
                           const __nv_bfloat16* Kp, const __nv_bfloat16* Vp, long long slots, __nv_bfloat16* O, int M,
                           int* item_ctr, cudaStream_t s);
+int spex_k_tree_attn_wmma(const CUtensorMap* kmap16, const CUtensorMap* vmap16, const RowDesc* rows,
+                          const Segment* segs, const float* Qr, int H, int KVH, int dh, long long slots,
+                          __nv_bfloat16* O, int M, int* item_ctr, cudaStream_t s);
 int spex_k_tree_attn_decode_mma(const CUtensorMap* kmap, const CUtensorMap* vmap, const RowDesc* rows,
                                 const Segment* segs, const float* Qr, int H, int KVH, int dh, long long slots,
                                 __nv_bfloat16* O, int M, cudaStream_t s);
@@ -142,12 +145,12 @@ static PFN_tmap_encode tmap_encoder() {
   return fn;
 }
 
-static bool make_kv_tmap(CUtensorMap* m, void* base, long long rows, int dh) {
+static bool make_kv_tmap(CUtensorMap* m, void* base, long long rows, int dh, int box_rows = 64) {
   PFN_tmap_encode enc = tmap_encoder();
   if (!enc || dh != 128) return false;
   cuuint64_t dims[2] = {(cuuint64_t)dh, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)dh * 2};
-  cuuint32_t box[2] = {64, 64};
+  cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
   cuuint32_t es[2] = {1, 1};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
@@ -157,6 +160,11 @@ static bool make_kv_tmap(CUtensorMap* m, void* base, long long rows, int dh) {
 // TMA descriptor of one layer's tree-KV pool for the tile attention kernel.
 extern "C" int spex_tmap_kv(CUtensorMap* m, void* base, long long rows, int dh) {
   return make_kv_tmap(m, base, rows, dh) ? 0 : -1;
+}
+
+// ... with 16-row boxes for the per-warp decode pipeline (tree_attn_wmma_kernel).
+extern "C" int spex_tmap_kv16(CUtensorMap* m, void* base, long long rows, int dh) {
+  return make_kv_tmap(m, base, rows, dh, 16) ? 0 : -1;
 }
 
 // TMA descriptor of a row-major bf16 matrix [rows][cols] as a GEMM operand of
@@ -183,7 +191,8 @@ struct TcWeight {
 
 struct Model {
   ModelShape sh;
-  std::vector<CUtensorMap> kmap, vmap;  // per layer (empty when TMA maps are unavailable)
+  std::vector<CUtensorMap> kmap, vmap;      // per layer (empty when TMA maps are unavailable)
+  std::vector<CUtensorMap> kmap16, vmap16;  // 16-row boxes (decode pipeline)
   bool is_prm;
   long long slots;
   int max_rows;
@@ -264,6 +273,10 @@ static Model* make_model(const ModelShape& sh, bool prm, uint64_t seed, long lon
     init(m->wd.back(), nd, 100 + 8 * l + 3, kStd);
     m->Kp.push_back(dalloc<__nv_bfloat16>((size_t)sh.KVH * slots * sh.dh, o));
     m->Vp.push_back(dalloc<__nv_bfloat16>((size_t)sh.KVH * slots * sh.dh, o));
+    // zero-filled: decode boxes may cover slots past a segment (masked to p = 0,
+    // which must not meet a NaN bit pattern)
+    CK(cudaMemsetAsync(m->Kp.back(), 0, (size_t)sh.KVH * slots * sh.dh * 2, st));
+    CK(cudaMemsetAsync(m->Vp.back(), 0, (size_t)sh.KVH * slots * sh.dh * 2, st));
   }
   if (!getenv("SPEX_NO_MMA_ATTN")) {
     m->kmap.resize(sh.L);
@@ -273,6 +286,16 @@ static Model* make_model(const ModelShape& sh, bool prm, uint64_t seed, long lon
           !make_kv_tmap(&m->vmap[l], m->Vp[l], (long long)sh.KVH * slots, sh.dh)) {
         m->kmap.clear();
         m->vmap.clear();
+        break;
+      }
+    }
+    m->kmap16.resize(sh.L);
+    m->vmap16.resize(sh.L);
+    for (int l = 0; l < sh.L && !m->kmap.empty(); ++l) {
+      if (!make_kv_tmap(&m->kmap16[l], m->Kp[l], (long long)sh.KVH * slots, sh.dh, 16) ||
+          !make_kv_tmap(&m->vmap16[l], m->Vp[l], (long long)sh.KVH * slots, sh.dh, 16)) {
+        m->kmap16.clear();
+        m->vmap16.clear();
         break;
       }
     }
@@ -392,6 +415,13 @@ static bool bulk_wanted() {
   return on;
 }
 static int* g_item_ctr = nullptr;  // K1 bulk kernel's work counter (policy stream)
+// Per-warp TMA + mma.sync decode pipeline: default for GQA groups (G >= 4:
+// config 5's K1 5.2 s -> 3.2 s); for G = 1 the FHFMA bulk kernel is faster
+// (1.98 s vs 2.13 s on c2). SPEX_K1_WMMA=1 forces it for every group size, 0 off.
+static bool wmma_wanted(const ModelShape& s) {
+  static const int mode = getenv("SPEX_K1_WMMA") ? atoi(getenv("SPEX_K1_WMMA")) : 2;
+  return mode == 1 || (mode == 2 && s.H / s.KVH >= 4);
+}
 
 constexpr int kTcMinRows = 1024;  // per-op tcgen05 below this row count loses to cuBLAS's small-M kernels
 
@@ -501,6 +531,9 @@ static void forward(Model& m, const RowDesc* rows, const Segment* segs, int M, c
     if (tiles && !m.kmap.empty())
       rc = spex_k_tree_attn_tiles_mma(&m.kmap[l], &m.vmap[l], tiles, ntiles, rows, segs, m.Qr, s.H, s.KVH, s.dh,
                                       m.slots, m.O, st);
+    if (rc != 0 && !tiles && !m.kmap16.empty() && wmma_wanted(s) && g_item_ctr)
+      rc = spex_k_tree_attn_wmma(&m.kmap16[l], &m.vmap16[l], rows, segs, m.Qr, s.H, s.KVH, s.dh, m.slots, m.O, M,
+                                 g_item_ctr, st);
     if (rc != 0 && !tiles && !m.kmap.empty() && decode_mma_wanted(s))
       rc = spex_k_tree_attn_decode_mma(&m.kmap[l], &m.vmap[l], rows, segs, m.Qr, s.H, s.KVH, s.dh, m.slots, m.O, M,
                                        st);

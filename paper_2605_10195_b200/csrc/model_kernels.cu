@@ -1452,6 +1452,216 @@ __global__ void __launch_bounds__(128) tree_attn_decode_mma_kernel(const __grid_
   (void)L1;
 }
 
+// K1 decode, per-warp TMA pipeline on tensor cores (any GQA group G <= 16,
+// dh = 128): the bulk kernel's structure — a persistent grid of warps claiming
+// (row, KV head) items from a device counter, each warp streaming its items'
+// tree context through its own ring of NST shared-memory stages of 16 tokens,
+// loads in flight across item and segment boundaries — with the stages filled
+// by 2D TMA (16-row boxes, 128-byte swizzle, so ldmatrix reads are conflict
+// free) and the math on mma.sync m16n8k16: the MMA rows are the KV head's G
+// query heads (zero-padded to 16), so each staged K/V row serves the whole
+// group at the cost of one row-vector of MMA work. The pools are zero-filled at
+// allocation, so rows of a box past a segment's end are finite (masked to p = 0).
+constexpr int kMmaNST = 2;     // stages per warp
+constexpr int kMmaWarps = 12;  // warps per block (12 x 2 x 8 KB = 192 KB; 170 registers)
+
+// byte offset of (row, 16-byte chunk c in [0,16)) in a swizzled [2 halves][16 rows][128 B] box pair
+__device__ __forceinline__ uint32_t swz16(int row, int c) {
+  const int half = c >> 3, cc = c & 7;
+  return (uint32_t)(half * 2048 + row * 128 + ((cc ^ (row & 7)) << 4));
+}
+
+__global__ void __launch_bounds__(kMmaWarps * 32, 1)
+    tree_attn_wmma_kernel(const __grid_constant__ CUtensorMap kmap16, const __grid_constant__ CUtensorMap vmap16,
+                          const RowDesc* __restrict__ rows, const Segment* __restrict__ segs,
+                          const float* __restrict__ Qr, int H, int KVH, int G, int n_items, long long slots,
+                          __nv_bfloat16* __restrict__ O, int* __restrict__ item_ctr) {
+  constexpr int DH = 128, CH = 16, STAGE = CH * DH * 2;  // 4 KB of K (and of V) per stage
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t bar[kMmaWarps][kMmaNST];
+  __shared__ int queue[kMmaWarps][8];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned char* ring = sm + (size_t)warp * kMmaNST * 2 * STAGE;  // [stage][K|V][STAGE]
+  if (lane == 0) {
+    for (int i = 0; i < kMmaNST; ++i) mbar_init(&bar[warp][i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  // ---- producer cursor (lane 0 only)
+  int p_q = 0, p_item = -1, p_seg = 0, p_off = 0, p_nseg = 0, issued = 0;
+  long long p_row0 = 0;
+  const Segment* p_sg = nullptr;
+  bool p_done = false;
+  auto produce = [&]() {
+    while (!p_done) {
+      if (p_item < 0 || p_seg >= p_nseg) {
+        const int it = atomicAdd(item_ctr, 1);
+        if (it >= n_items) {
+          queue[warp][p_q & 7] = -1;
+          p_done = true;
+          return;
+        }
+        queue[warp][p_q & 7] = it;
+        ++p_q;
+        p_item = it;
+        const RowDesc rd = rows[it / KVH];
+        p_sg = segs + rd.seg_off;
+        p_nseg = rd.nseg;
+        p_seg = 0;
+        p_off = 0;
+        p_row0 = (long long)(it % KVH) * slots;
+      }
+      const int len = p_sg[p_seg].len;
+      if (p_off >= len) {
+        ++p_seg;
+        p_off = 0;
+        continue;
+      }
+      const int rowc = (int)(p_row0 + p_sg[p_seg].base + p_off);
+      const int st = issued % kMmaNST;
+      unsigned char* kb = ring + st * 2 * STAGE;
+      mbar_expect_tx(&bar[warp][st], 2 * STAGE);
+      tma_load_2d(kb, &kmap16, 0, rowc, &bar[warp][st]);
+      tma_load_2d(kb + 2048, &kmap16, 64, rowc, &bar[warp][st]);
+      tma_load_2d(kb + STAGE, &vmap16, 0, rowc, &bar[warp][st]);
+      tma_load_2d(kb + STAGE + 2048, &vmap16, 64, rowc, &bar[warp][st]);
+      p_off += CH;
+      ++issued;
+      return;
+    }
+  };
+  if (lane == 0)
+    for (int i = 0; i < kMmaNST - 1; ++i) produce();
+  __syncwarp();
+  const int gq = lane >> 2, tq = lane & 3, mi = lane >> 3, ri = lane & 7;
+  int c_q = 0, consumed = 0;
+  for (;;) {
+    const int it = queue[warp][c_q & 7];
+    if (it < 0) break;
+    ++c_q;
+    const int r = it / KVH, kh = it % KVH;
+    const RowDesc rd = rows[r];
+    const Segment* sg = segs + rd.seg_off;
+    // Q fragments: rows = the group's heads (gq, gq + 8 < G), dims as k
+    uint32_t qa[8][4];
+    {
+      const bool v0 = gq < G, v1 = gq + 8 < G;
+      const float* q0 = Qr + ((long long)r * H + kh * G + (v0 ? gq : 0)) * DH;
+      const float* q1 = Qr + ((long long)r * H + kh * G + (v1 ? gq + 8 : 0)) * DH;
+      constexpr float sc = 1.4426950408889634f;
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks) {
+        const int k0 = ks * 16 + tq * 2;
+        const float2 x00 = v0 ? *reinterpret_cast<const float2*>(q0 + k0) : make_float2(0.f, 0.f);
+        const float2 x10 = v1 ? *reinterpret_cast<const float2*>(q1 + k0) : make_float2(0.f, 0.f);
+        const float2 x01 = v0 ? *reinterpret_cast<const float2*>(q0 + k0 + 8) : make_float2(0.f, 0.f);
+        const float2 x11 = v1 ? *reinterpret_cast<const float2*>(q1 + k0 + 8) : make_float2(0.f, 0.f);
+        qa[ks][0] = pack_bf16(x00.x * sc, x00.y * sc);
+        qa[ks][1] = pack_bf16(x10.x * sc, x10.y * sc);
+        qa[ks][2] = pack_bf16(x01.x * sc, x01.y * sc);
+        qa[ks][3] = pack_bf16(x11.x * sc, x11.y * sc);
+      }
+    }
+    float oacc[16][4];
+#pragma unroll
+    for (int n = 0; n < 16; ++n) oacc[n][0] = oacc[n][1] = oacc[n][2] = oacc[n][3] = 0.f;
+    float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+    for (int si = 0; si < rd.nseg; ++si) {
+      const int len = sg[si].len;
+      for (int off = 0; off < len; off += CH) {
+        const int n = min(CH, len - off);
+        if (lane == 0) produce();
+        const int st = consumed % kMmaNST;
+        mbar_wait(&bar[warp][st], (uint32_t)((consumed / kMmaNST) & 1));
+        const uint32_t kb = (uint32_t)__cvta_generic_to_shared(ring + st * 2 * STAGE);
+        const uint32_t vb = kb + STAGE;
+        float sacc[2][4];
+#pragma unroll
+        for (int t = 0; t < 2; ++t) sacc[t][0] = sacc[t][1] = sacc[t][2] = sacc[t][3] = 0.f;
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks) {
+          uint32_t b0, b1, b2, b3;
+          ldsm_x4(kb + swz16((mi >> 1) * 8 + ri, ks * 2 + (mi & 1)), b0, b1, b2, b3);
+          mma_bf16(sacc[0], qa[ks][0], qa[ks][1], qa[ks][2], qa[ks][3], b0, b1);
+          mma_bf16(sacc[1], qa[ks][0], qa[ks][1], qa[ks][2], qa[ks][3], b2, b3);
+        }
+        float mx0 = -INFINITY, mx1 = -INFINITY;
+#pragma unroll
+        for (int t = 0; t < 2; ++t)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const bool ok = t * 8 + tq * 2 + e < n;
+            sacc[t][e] = ok ? sacc[t][e] : -INFINITY;
+            sacc[t][2 + e] = ok ? sacc[t][2 + e] : -INFINITY;
+            mx0 = fmaxf(mx0, sacc[t][e]);
+            mx1 = fmaxf(mx1, sacc[t][2 + e]);
+          }
+#pragma unroll
+        for (int o = 1; o < 4; o <<= 1) {
+          mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, o));
+          mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, o));
+        }
+        const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
+        const float a0 = mn0 == -INFINITY ? 1.f : exp2f(m0 - mn0);
+        const float a1 = mn1 == -INFINITY ? 1.f : exp2f(m1 - mn1);
+        uint32_t pa[4];
+        float ps0 = 0.f, ps1 = 0.f;
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+          const float p00 = mn0 == -INFINITY ? 0.f : exp2f(sacc[t][0] - mn0);
+          const float p01 = mn0 == -INFINITY ? 0.f : exp2f(sacc[t][1] - mn0);
+          const float p10 = mn1 == -INFINITY ? 0.f : exp2f(sacc[t][2] - mn1);
+          const float p11 = mn1 == -INFINITY ? 0.f : exp2f(sacc[t][3] - mn1);
+          ps0 += p00 + p01;
+          ps1 += p10 + p11;
+          pa[2 * t] = pack_bf16(p00, p01);
+          pa[2 * t + 1] = pack_bf16(p10, p11);
+        }
+        l0 = l0 * a0 + ps0;
+        l1 = l1 * a1 + ps1;
+        m0 = mn0;
+        m1 = mn1;
+#pragma unroll
+        for (int nn = 0; nn < 16; ++nn) {
+          oacc[nn][0] *= a0;
+          oacc[nn][1] *= a0;
+          oacc[nn][2] *= a1;
+          oacc[nn][3] *= a1;
+        }
+#pragma unroll
+        for (int n2 = 0; n2 < 8; ++n2) {
+          uint32_t b0, b1, b2, b3;
+          ldsm_x4_t(vb + swz16((mi & 1) * 8 + ri, n2 * 2 + (mi >> 1)), b0, b1, b2, b3);
+          mma_bf16(oacc[2 * n2], pa[0], pa[1], pa[2], pa[3], b0, b1);
+          mma_bf16(oacc[2 * n2 + 1], pa[0], pa[1], pa[2], pa[3], b2, b3);
+        }
+        ++consumed;
+        __syncwarp();  // stage fully read before lane 0 refills it
+      }
+    }
+#pragma unroll
+    for (int o = 1; o < 4; o <<= 1) {
+      l0 += __shfl_xor_sync(0xffffffffu, l0, o);
+      l1 += __shfl_xor_sync(0xffffffffu, l1, o);
+    }
+    if (gq < G) {
+      __nv_bfloat16* o0 = O + ((long long)r * H + kh * G + gq) * DH + tq * 2;
+      const float inv = 1.f / l0;
+#pragma unroll
+      for (int nn = 0; nn < 16; ++nn)
+        *reinterpret_cast<uint32_t*>(o0 + nn * 8) = pack_bf16(oacc[nn][0] * inv, oacc[nn][1] * inv);
+    }
+    if (gq + 8 < G) {
+      __nv_bfloat16* o1 = O + ((long long)r * H + kh * G + gq + 8) * DH + tq * 2;
+      const float inv = 1.f / l1;
+#pragma unroll
+      for (int nn = 0; nn < 16; ++nn)
+        *reinterpret_cast<uint32_t*>(o1 + nn * 8) = pack_bf16(oacc[nn][2] * inv, oacc[nn][3] * inv);
+    }
+  }
+}
+
 // K1 tile variant for prefill-shaped rows (PRM scoring): kTileRows consecutive
 // rows of one thought share their ancestors and a causal own prefix, so each
 // 64-token K/V chunk is staged once per tile instead of once per row.
@@ -1878,6 +2088,31 @@ extern "C" int spex_k_tree_attn_bulk(const RowDesc* rows, const Segment* segs, c
     default:  // measured best on c2 (tools: SPEX_K1_BULK_CFG sweep)
       return launch_bulk<16, 2, 14>(rows, segs, Qr, H, KVH, Kp, Vp, slots, O, M, item_ctr, s);
   }
+}
+
+// K1 decode rows on the per-warp TMA + mma.sync pipeline (G <= 16, dh = 128);
+// kmap16/vmap16 are the pools' 2D maps with 64 x 16 boxes (spex_tmap_kv16).
+extern "C" int spex_k_tree_attn_wmma(const CUtensorMap* kmap16, const CUtensorMap* vmap16, const RowDesc* rows,
+                                     const Segment* segs, const float* Qr, int H, int KVH, int dh, long long slots,
+                                     __nv_bfloat16* O, int M, int* item_ctr, cudaStream_t s) {
+  const int G = H / KVH;
+  if (M <= 0) return 0;
+  if (dh != 128 || G < 1 || G > 16) return -1;
+  const size_t smem = (size_t)kMmaWarps * kMmaNST * 2 * 16 * 128 * 2 + 1024;
+  static int blocks = 0;
+  if (!blocks) {
+    cudaFuncSetAttribute(tree_attn_wmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    blocks = sms;
+  }
+  const int n_items = M * KVH;
+  const int grid = std::min(blocks, (n_items + kMmaWarps - 1) / kMmaWarps);
+  cudaMemsetAsync(item_ctr, 0, sizeof(int), s);
+  tree_attn_wmma_kernel<<<grid, kMmaWarps * 32, smem, s>>>(*kmap16, *vmap16, rows, segs, Qr, H, KVH, G, n_items, slots,
+                                                           O, item_ctr);
+  return (int)cudaGetLastError();
 }
 
 extern "C" void spex_k_build_decode_chunks(const RowDesc* rows, const Segment* segs, int M, DecodeChunks w,

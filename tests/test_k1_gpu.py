@@ -81,7 +81,7 @@ def _make_tree_rows(rng, M, slots, max_depth):
     return rows, segs, paths
 
 
-@pytest.mark.parametrize("impl", ["row", "chunked", "mma", "bulk"])
+@pytest.mark.parametrize("impl", ["row", "chunked", "mma", "bulk", "wmma"])
 @pytest.mark.parametrize("H,KVH,dh,M", [(8, 8, 128, 300), (32, 8, 128, 97), (12, 2, 128, 80), (4, 2, 64, 150), (16, 4, 64, 64)])
 def test_k1_decode_matches_torch_fp32(H, KVH, dh, M, impl):
     """impl "row": one warp per (row, kv head) (spex_k_tree_attn); "chunked": the
@@ -105,6 +105,26 @@ def test_k1_decode_matches_torch_fp32(H, KVH, dh, M, impl):
     if impl == "row":
         rc = f(rows_d.data_ptr(), segs_d.data_ptr(), Q.data_ptr(), H, KVH, dh, K.data_ptr(), V.data_ptr(), slots,
                O.data_ptr(), M, st.cuda_stream)
+        assert rc == 0
+    elif impl == "wmma":
+        if dh != 128:
+            pytest.skip("per-warp TMA decode kernel is dh=128")
+        from paper_2605_10195_b200 import _lib as L
+        lib = L.lib()
+        lib.spex_tmap_kv16.restype = ctypes.c_int
+        lib.spex_tmap_kv16.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_longlong, ctypes.c_int]
+        fw = lib.spex_k_tree_attn_wmma
+        fw.restype = ctypes.c_int
+        fw.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                       ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_longlong, ctypes.c_void_p, ctypes.c_int,
+                       ctypes.c_void_p, ctypes.c_void_p]
+        km, vm = ctypes.create_string_buffer(256), ctypes.create_string_buffer(256)
+        kp, vp = (ctypes.addressof(km) + 63) & ~63, (ctypes.addressof(vm) + 63) & ~63
+        assert lib.spex_tmap_kv16(kp, K.data_ptr(), KVH * slots, dh) == 0
+        assert lib.spex_tmap_kv16(vp, V.data_ptr(), KVH * slots, dh) == 0
+        ctr = torch.zeros(1, dtype=torch.int32, device=dev)
+        rc = fw(kp, vp, rows_d.data_ptr(), segs_d.data_ptr(), Q.data_ptr(), H, KVH, dh, slots, O.data_ptr(), M,
+                ctr.data_ptr(), st.cuda_stream)
         assert rc == 0
     elif impl == "bulk":
         if dh != 128 or H != KVH:
