@@ -277,10 +277,10 @@ __global__ void rmsnorm_bf16_kernel(const float* X, int M, int d, float eps, __n
 __global__ void rope_kv_kernel(const RowDesc* rows, int M, const __nv_bfloat16* QKV, int H, int KVH, int dh,
                                const float2* __restrict__ cs_tab, long long slots, __nv_bfloat16* Kp,
                                __nv_bfloat16* Vp, float* Qr) {
-  // one warp per row; (cos, sin) from the per-forward table (rope_table_kernel),
-  // rotate-half RoPE on (x[i], x[i+half]) pairs two at a time from the bf16
-  // projection output; V copied 8 bytes at a time
-  const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  // one block (128 threads) per row; (cos, sin) from the per-forward table
+  // (rope_table_kernel), rotate-half RoPE on (x[i], x[i+half]) pairs two at a
+  // time from the bf16 projection output; V copied 8 bytes at a time
+  const int r = blockIdx.x, lane = threadIdx.x;
   if (r >= M) return;
   const long long slot = rows[r].slot;
   const int width = (H + 2 * KVH) * dh;
@@ -289,7 +289,7 @@ __global__ void rope_kv_kernel(const RowDesc* rows, int M, const __nv_bfloat16* 
   const float2* cs = cs_tab + (long long)r * half;
   const float qscale = rsqrtf((float)dh);
   const int hp = half / 2;  // bf16 pairs per half
-  for (int idx = lane; idx < (H + KVH) * hp; idx += 32) {
+  for (int idx = lane; idx < (H + KVH) * hp; idx += blockDim.x) {
     const int head = idx / hp;
     const int i = (idx - head * hp) * 2;
     const __nv_bfloat16* x = src + head * dh;
@@ -311,7 +311,7 @@ __global__ void rope_kv_kernel(const RowDesc* rows, int M, const __nv_bfloat16* 
     }
   }
   const __nv_bfloat16* vs = src + (H + KVH) * dh;
-  for (int idx = lane; idx < KVH * dh / 4; idx += 32) {
+  for (int idx = lane; idx < KVH * dh / 4; idx += blockDim.x) {
     const int e = idx * 4;
     const int kh = e / dh, i = e - kh * dh;
     *reinterpret_cast<uint2*>(Vp + ((long long)kh * slots + slot) * dh + i) = *reinterpret_cast<const uint2*>(vs + e);
@@ -2004,8 +2004,8 @@ extern "C" void spex_k_rmsnorm(const float* X, int M, int d, float eps, __nv_bfl
 extern "C" void spex_k_rope_kv(const RowDesc* rows, int M, const __nv_bfloat16* QKV, int H, int KVH, int dh,
                                const float* cs_tab, long long slots, __nv_bfloat16* Kp, __nv_bfloat16* Vp,
                                float* Qr, cudaStream_t s) {
-  rope_kv_kernel<<<(M + 7) / 8, 256, 0, s>>>(rows, M, QKV, H, KVH, dh, reinterpret_cast<const float2*>(cs_tab), slots,
-                                             Kp, Vp, Qr);
+  rope_kv_kernel<<<M, 128, 0, s>>>(rows, M, QKV, H, KVH, dh, reinterpret_cast<const float2*>(cs_tab), slots, Kp, Vp,
+                                   Qr);
 }
 
 template <int DH, int G>
