@@ -53,8 +53,8 @@ def parse():
     ap.add_argument("--policy", default="mid_policy")
     ap.add_argument("--prm", default="mid_prm")
     ap.add_argument("--cpu-sample-runs", type=int, default=4)
-    ap.add_argument("--control-only", type=int, default=64,
-                    help="also time N concurrent control-only searches (no model), 0 = off")
+    ap.add_argument("--control-only", type=int, default=296,
+                    help="also time N control-only searches in one batched launch (no model), 0 = off")
     ap.add_argument("--named-shapes", type=int, default=1,
                     help="also time config 5 with the Llama-3-8B-shaped policy + 1.5B-shaped PRM (1 = on)")
     return ap.parse_args()
@@ -296,31 +296,20 @@ def main():
         barrier()
         tr_wall = time.perf_counter() - t2
     # the search path alone, as the reference arm runs it (virtual decode, no
-    # model): each search is one control CTA on its own SM, so many run at once
+    # model): independent searches in one control-kernel launch, one CTA each
+    # (the device analog of the reference's OpenMP loop over repetitions)
     ctl_only = None
     if args.control_only > 0:
-        def ctl_search(out, k):
-            ex = spex.Executor(cfg_text, seed + k, None, trace=False, device=local)
-            t = ex.run()
-            out[k] = (t.queries, ex.stats()["device_ms"])
-            ex.close()
-
-        def ctl_round(n):
-            res = [None] * n
-            ths = [threading.Thread(target=ctl_search, args=(res, k)) for k in range(n)]
-            t0 = time.perf_counter()
-            for th in ths:
-                th.start()
-            for th in ths:
-                th.join()
-            return res, time.perf_counter() - t0
-
-        ctl_round(min(8, args.control_only))  # warm-up
-        res, wall_c = ctl_round(args.control_only)
-        ctl_only = {"concurrent_searches": args.control_only, "queries_per_s": sum(r[0] for r in res) / wall_c,
-                    "wall_s": wall_c, "per_search_device_ms_median": statistics.median(r[1] for r in res),
-                    "note": "device control kernel only (the reference arm's virtual-clock decode, no model), "
-                            "one CTA per search, searches on concurrent host threads; compare with --impl reference"}
+        n_b = args.control_only
+        spex.run_batch(cfg_text, [seed + k for k in range(min(16, n_b))])  # warm-up
+        t0c = time.perf_counter()
+        tots_b, ms_b = spex.run_batch(cfg_text, [seed + 1000 + k for k in range(n_b)])
+        wall_c = time.perf_counter() - t0c
+        ctl_only = {"searches": n_b, "queries_per_s": sum(t.queries for t in tots_b) / wall_c,
+                    "queries_per_s_device": sum(t.queries for t in tots_b) / (ms_b / 1000.0),
+                    "wall_s": wall_c, "device_ms": ms_b,
+                    "note": "device control kernel only (the reference arm's virtual-clock decode, no model): "
+                            "one launch, one CTA (SM) per search; compare with --impl reference"}
     # the named model shapes (north star): config 5, Llama-3-8B-shaped policy +
     # 1.5B-shaped PRM, one warm + one timed search on this GPU
     named = None

@@ -127,6 +127,13 @@ int spex_executor_model_stats(spex_executor* ex, spex_model_stats* out);
 /* Copies up to cap records; *n receives the total available. */
 int spex_executor_decode_outputs(spex_executor* ex, void* buf, long long cap, long long* n);
 int spex_executor_prm_outputs(spex_executor* ex, void* buf, long long cap, long long* n);
+/* n independent searches of one config (seeds[0..n)) in ONE launch of the
+ * control kernel, one CTA per search (the device analog of run_experiment_full's
+ * OpenMP loop over repetitions, experiment.cpp:61-78); control only (no model,
+ * no trace). totals[n]; device_ms = the launch's CUDA-event time. */
+int spex_run_batch(const char* config_json, const uint64_t* seeds, int n, const char* flags_csv, int device,
+                   spex_totals* totals, double* device_ms);
+
 /* Per-query virtual finish time (query_done.t; admission is at t = 0 when
  * batch_size = n_queries): the search latency of each query. */
 int spex_executor_query_finish(spex_executor* ex, double* out, int cap, int* n);

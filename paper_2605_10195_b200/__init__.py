@@ -229,6 +229,27 @@ def run_once(cfg: Any, seed: int, flags: SpexFlags | str | None = None) -> RunOu
         ex.close()
 
 
+def run_batch(cfg: Any, seeds, flags: SpexFlags | str | None = None, device: int = 0):
+    """Independent searches of one config, one per seed, in ONE launch of the
+    control kernel (one CTA per search; control only, no model). The device
+    analog of run_experiment_full's loop over repetitions (experiment.cpp:61-78).
+    Returns (list of RunTotals, device milliseconds of the launch)."""
+    L = _lib.lib()
+    seeds = list(seeds)
+    n = len(seeds)
+    arr = (ctypes.c_uint64 * n)(*seeds)
+    tots = (_lib.Totals * n)()
+    ms = ctypes.c_double()
+    if isinstance(flags, SpexFlags):
+        fcsv = flags.to_csv().encode()
+    elif isinstance(flags, str):
+        fcsv = flags.encode()
+    else:
+        fcsv = None
+    _check(L.spex_run_batch(_cfg_text(cfg).encode(), arr, n, fcsv, device, tots, ctypes.byref(ms)))
+    return [RunTotals(**t.as_dict()) for t in tots], ms.value
+
+
 __all__ = [
     "Executor",
     "RunOutcome",
@@ -237,5 +258,6 @@ __all__ = [
     "TotsimError",
     "canonical_config",
     "device_ok",
+    "run_batch",
     "run_once",
 ]

@@ -115,6 +115,9 @@ _EXPORTS = {
     ),
     "spex_executor_stats": ([ctypes.c_void_p, ctypes.POINTER(Stats)], ctypes.c_int),
     "spex_executor_destroy": ([ctypes.c_void_p], None),
+    "spex_run_batch": (
+        [ctypes.c_char_p, ctypes.POINTER(ctypes.c_uint64), ctypes.c_int, ctypes.c_char_p, ctypes.c_int,
+         ctypes.POINTER(Totals), ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
     "spex_executor_query_finish": (
         [ctypes.c_void_p, ctypes.POINTER(ctypes.c_double), ctypes.c_int, ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
     "spex_executor_set_model": (

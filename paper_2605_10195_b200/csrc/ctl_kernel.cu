@@ -44,7 +44,7 @@ __global__ void __launch_bounds__(512, 1) spex_control_kernel(const Run* __restr
   // written back at the end. The control CTA owns its SM (512 x 128 registers),
   // so this shared memory costs the forward nothing.
   extern __shared__ __align__(16) unsigned char dsm[];
-  if (threadIdx.x == 0) sR = *d_run;
+  if (threadIdx.x == 0) sR = d_run[blockIdx.x];  // a batch launch runs one search per CTA
   __syncthreads();
   QueryRun* const g_qs = sR.qs;
   GState* const g_g = sR.g;
@@ -115,6 +115,17 @@ extern "C" int spex_launch_control_async(spex::Run* d_run, int n_queries, int nt
   const int dyn = std::getenv("SPEX_CTL_NO_SMEM") ? (spex::ensure_control_stack(), 0) : spex::control_dyn_smem(n_queries);
   cudaEventRecord(a, stream);
   spex::spex_control_kernel<<<1, nthreads, dyn, stream>>>(d_run, dyn);
+  cudaError_t e = cudaGetLastError();
+  cudaEventRecord(b, stream);
+  return static_cast<int>(e);
+}
+
+extern "C" int spex_launch_control_batch_async(spex::Run* d_runs, int n_runs, int n_queries, int nthreads,
+                                               cudaStream_t stream, cudaEvent_t a, cudaEvent_t b) {
+  if (nthreads < 64 || nthreads > 512 || (nthreads & 31)) nthreads = 512;
+  const int dyn = std::getenv("SPEX_CTL_NO_SMEM") ? (spex::ensure_control_stack(), 0) : spex::control_dyn_smem(n_queries);
+  cudaEventRecord(a, stream);
+  spex::spex_control_kernel<<<n_runs, nthreads, dyn, stream>>>(d_runs, dyn);
   cudaError_t e = cudaGetLastError();
   cudaEventRecord(b, stream);
   return static_cast<int>(e);

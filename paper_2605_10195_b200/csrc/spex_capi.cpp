@@ -474,6 +474,8 @@ struct spex_executor {
 extern "C" int spex_launch_control(Run* d_run, int n_queries, int nthreads, cudaStream_t stream, float* ms);
 extern "C" int spex_launch_control_async(Run* d_run, int n_queries, int nthreads, cudaStream_t stream, cudaEvent_t a,
                                          cudaEvent_t b);
+extern "C" int spex_launch_control_batch_async(Run* d_runs, int n_runs, int n_queries, int nthreads,
+                                               cudaStream_t stream, cudaEvent_t a, cudaEvent_t b);
 extern "C" void spex_model_cache_clear();
 extern "C" void spex_model_cache_release_mismatch(const ModelRunConfig* mc);
 #define CUDA_OK(x)                                                                  \
@@ -1082,11 +1084,126 @@ void run_executor(spex_executor& ex, int trace) {
   fail(ERR_CAP_NODES, "node capacity exhausted");
 }
 
+#ifndef SPEX_EMU
+// Many independent searches (same config, different seeds) in ONE launch of the
+// control kernel: CTA b runs search b (the device analog of the reference's
+// OpenMP loop over repetitions, experiment.cpp:61-78). Control only (no model,
+// no trace). Returns false if any search needs a larger arena; the caller then
+// runs those searches one by one.
+bool run_batch_device(std::vector<spex_executor*>& exs, int device, cudaStream_t st, float* ms_out) {
+  const int n = static_cast<int>(exs.size());
+  CUDA_OK(cudaSetDevice(device));
+  const HostConfig& h = exs[0]->hc;
+  const int Q = h.n_queries;
+  int node_cap = 512;
+  if (const char* e = std::getenv("SPEX_NODE_CAP")) node_cap = std::max(16, std::atoi(e));
+  const int stream_cap = static_cast<int>(static_cast<long long>(Q) * (node_cap - 1) + 64);
+  const int stage_cap = std::max(4096, node_cap * 8);
+  const int nthreads = exs[0]->nthreads, nwarps = nthreads / 32;
+  std::vector<double>& tab = log_table();
+  double* d_tab = nullptr;
+  CUDA_OK(cudaMallocAsync(reinterpret_cast<void**>(&d_tab), tab.size() * sizeof(double), st));
+  CUDA_OK(cudaMemcpyAsync(d_tab, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice, st));
+  std::vector<Run> runs(n);
+  std::vector<char*> bases(n, nullptr);
+  for (int b = 0; b < n; ++b) {
+    Run& R = runs[b];
+    R = Run{};
+    exs[b]->record_sched = 0;
+    set_cfg(*exs[b], R.cfg, node_cap, stream_cap, 64, stage_cap, 0, 0);
+    Arena A;
+    layout(A, R, Q, node_cap, stream_cap, 64, nwarps, stage_cap);
+    R.nwarps = nwarps;
+    R.log_tab_n = static_cast<int>(tab.size());
+    R.log_tab = d_tab;
+    CUDA_OK(cudaMallocAsync(reinterpret_cast<void**>(&bases[b]), A.total + 256, st));
+    CUDA_OK(cudaMemsetAsync(bases[b], 0, A.total + 256, st));
+    A.carve(bases[b]);
+  }
+  Run* d_runs = nullptr;
+  CUDA_OK(cudaMallocAsync(reinterpret_cast<void**>(&d_runs), sizeof(Run) * n, st));
+  CUDA_OK(cudaMemcpyAsync(d_runs, runs.data(), sizeof(Run) * n, cudaMemcpyHostToDevice, st));
+  cudaEvent_t ca, cb;
+  cudaEventCreate(&ca);
+  cudaEventCreate(&cb);
+  const int lr = spex_launch_control_batch_async(d_runs, n, Q, nthreads, st, ca, cb);
+  if (lr != 0) fail(200, std::string("control kernel launch failed: ") + cudaGetErrorString(static_cast<cudaError_t>(lr)));
+  CUDA_OK(cudaEventSynchronize(cb));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, ca, cb);
+  cudaEventDestroy(ca);
+  cudaEventDestroy(cb);
+  if (ms_out) *ms_out = ms;
+  bool ok = true;
+  for (int b = 0; b < n; ++b) {
+    spex_executor& ex = *exs[b];
+    CUDA_OK(cudaMemcpy(&ex.g, runs[b].g, sizeof(GState), cudaMemcpyDeviceToHost));
+    ex.qs.resize(Q);
+    CUDA_OK(cudaMemcpy(ex.qs.data(), runs[b].qs, sizeof(QueryRun) * Q, cudaMemcpyDeviceToHost));
+    ex.device_ms = ms;
+    ex.ran = true;
+    if (ex.g.error != 0) {
+      ok = false;
+      ex.ran = false;
+    }
+  }
+  for (int b = 0; b < n; ++b) cudaFreeAsync(bases[b], st);
+  cudaFreeAsync(d_runs, st);
+  cudaFreeAsync(d_tab, st);
+  cudaStreamSynchronize(st);
+  return ok;
+}
+#endif
+
 }  // namespace
 
 extern "C" {
 
 const char* spex_last_error(void) { return g_err.c_str(); }
+
+int spex_run_batch(const char* config_json, const uint64_t* seeds, int n, const char* flags_csv, int device,
+                   spex_totals* totals, double* device_ms) {
+  return guarded([&] {
+    if (n <= 0) fail(ERR_INVALID_ARGUMENT, "empty batch");
+    std::vector<spex_executor*> exs;
+    auto free_all = [&] {
+      for (auto* e : exs) spex_executor_destroy(e);
+    };
+    for (int b = 0; b < n; ++b) {
+      spex_executor* e = nullptr;
+      const int rc = spex_executor_create(config_json, seeds[b], flags_csv, device, &e);
+      if (rc) {
+        free_all();
+        fail(rc, g_err);
+      }
+      exs.push_back(e);
+    }
+#ifndef SPEX_EMU
+    cudaStream_t st = nullptr;
+    CUDA_OK(cudaSetDevice(device));
+    CUDA_OK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    float ms = 0.f;
+    try {
+      run_batch_device(exs, device, st, &ms);
+    } catch (...) {
+      cudaStreamDestroy(st);
+      free_all();
+      throw;
+    }
+    cudaStreamDestroy(st);
+    if (device_ms) *device_ms = ms;
+#endif
+    for (int b = 0; b < n; ++b) {
+      if (!exs[b]->ran) {  // capacity: rerun alone (the single-run path grows its arena)
+        exs[b]->g = GState{};
+        run_executor(*exs[b], 0);
+        exs[b]->ran = true;
+      }
+      if (totals) fill_totals(*exs[b], &totals[b]);
+    }
+    free_all();
+  });
+}
 
 void spex_free(void* p) { std::free(p); }
 

@@ -66,3 +66,20 @@ def test_emulation_edge_configs_vs_reference(name, cfg, seed, flags):
     res = refutil.compare_logs(refutil.ref_run_log(cfg, seed, flags), got)
     assert res["decision_ok"], (name, res)
     assert t.generated_tokens == t.committed_tokens + t.reused_tokens + t.wasted_tokens
+
+
+def test_emulation_run_batch_equals_single_runs():
+    """spex_run_batch (one launch, one search per CTA on the device; sequential
+    in the emulation) returns the same totals as separate runs."""
+    L = emu()
+    cfg = json.dumps({"family": "rest_hybrid", "policy": {"width": 4, "max_depth": 8, "target_answers": 6},
+                      "workload": {"noise_sigma": 0.05}, "run": {"batch_size": 5, "n_queries": 5,
+                                                                 "flags": ["t1", "t2", "t3"]}})
+    seeds = [3, 4, 9]
+    arr = (ctypes.c_uint64 * 3)(*seeds)
+    tots = (_lib.Totals * 3)()
+    ms = ctypes.c_double()
+    assert L.spex_run_batch(cfg.encode(), arr, 3, None, 0, tots, ctypes.byref(ms)) == 0
+    for k, sd in enumerate(seeds):
+        _, t = emu_run(L, cfg, sd, None)
+        assert tots[k].as_dict() == t.as_dict()

@@ -79,3 +79,23 @@ def test_config4_matches_reference_digest():
         h.update(json.dumps(refutil.strip_floats(ln), sort_keys=True).encode())
         h.update(b"\n")
     assert h.hexdigest() == dg["masked_sha256"]
+
+
+def test_run_batch_matches_reference_totals():
+    """A batch of independent searches in one control-kernel launch (one CTA
+    each) gives every search the reference's makespan and token accounting."""
+    spex = _spex()
+    if refutil.ref_lib() is None:
+        pytest.skip("oracle/_ref not built")
+    import ctypes
+    cfg = (ROOT / "configs" / "c1_rebase_w4_q16.json").read_text()
+    seeds = list(range(1, 41))
+    tots, ms = spex.run_batch(cfg, seeds)
+    assert ms > 0
+    L = refutil.ref_lib()
+    for sd, t in zip(seeds, tots):
+        secs = ctypes.c_double()
+        rt = (ctypes.c_double * 24)()
+        assert L.ref_run_timed(cfg.encode(), sd, None, 0, 1, ctypes.byref(secs), rt) == 0
+        assert t.makespan == rt[0], (sd, t.makespan, rt[0])
+        assert t.queries == int(rt[5])
