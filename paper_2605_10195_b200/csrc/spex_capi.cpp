@@ -1093,6 +1093,15 @@ void run_executor(spex_executor& ex, int trace) {
 bool run_batch_device(std::vector<spex_executor*>& exs, int device, cudaStream_t st, float* ms_out) {
   const int n = static_cast<int>(exs.size());
   CUDA_OK(cudaSetDevice(device));
+  static bool pool_kept = false;  // keep freed arenas in the stream-ordered pool
+  if (!pool_kept) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      unsigned long long keep = ~0ULL;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    pool_kept = true;
+  }
   const HostConfig& h = exs[0]->hc;
   const int Q = h.n_queries;
   int node_cap = 512;
@@ -1137,9 +1146,13 @@ bool run_batch_device(std::vector<spex_executor*>& exs, int device, cudaStream_t
   bool ok = true;
   for (int b = 0; b < n; ++b) {
     spex_executor& ex = *exs[b];
-    CUDA_OK(cudaMemcpy(&ex.g, runs[b].g, sizeof(GState), cudaMemcpyDeviceToHost));
     ex.qs.resize(Q);
-    CUDA_OK(cudaMemcpy(ex.qs.data(), runs[b].qs, sizeof(QueryRun) * Q, cudaMemcpyDeviceToHost));
+    CUDA_OK(cudaMemcpyAsync(&ex.g, runs[b].g, sizeof(GState), cudaMemcpyDeviceToHost, st));
+    CUDA_OK(cudaMemcpyAsync(ex.qs.data(), runs[b].qs, sizeof(QueryRun) * Q, cudaMemcpyDeviceToHost, st));
+  }
+  CUDA_OK(cudaStreamSynchronize(st));
+  for (int b = 0; b < n; ++b) {
+    spex_executor& ex = *exs[b];
     ex.device_ms = ms;
     ex.ran = true;
     if (ex.g.error != 0) {
