@@ -1093,15 +1093,6 @@ void run_executor(spex_executor& ex, int trace) {
 bool run_batch_device(std::vector<spex_executor*>& exs, int device, cudaStream_t st, float* ms_out) {
   const int n = static_cast<int>(exs.size());
   CUDA_OK(cudaSetDevice(device));
-  static bool pool_kept = false;  // keep freed arenas in the stream-ordered pool
-  if (!pool_kept) {
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
-      unsigned long long keep = ~0ULL;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-    }
-    pool_kept = true;
-  }
   const HostConfig& h = exs[0]->hc;
   const int Q = h.n_queries;
   int node_cap = 512;
@@ -1114,21 +1105,23 @@ bool run_batch_device(std::vector<spex_executor*>& exs, int device, cudaStream_t
   CUDA_OK(cudaMallocAsync(reinterpret_cast<void**>(&d_tab), tab.size() * sizeof(double), st));
   CUDA_OK(cudaMemcpyAsync(d_tab, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice, st));
   std::vector<Run> runs(n);
-  std::vector<char*> bases(n, nullptr);
+  std::vector<Arena> arenas(n);
   for (int b = 0; b < n; ++b) {
     Run& R = runs[b];
     R = Run{};
     exs[b]->record_sched = 0;
     set_cfg(*exs[b], R.cfg, node_cap, stream_cap, 64, stage_cap, 0, 0);
-    Arena A;
-    layout(A, R, Q, node_cap, stream_cap, 64, nwarps, stage_cap);
+    layout(arenas[b], R, Q, node_cap, stream_cap, 64, nwarps, stage_cap);
     R.nwarps = nwarps;
     R.log_tab_n = static_cast<int>(tab.size());
     R.log_tab = d_tab;
-    CUDA_OK(cudaMallocAsync(reinterpret_cast<void**>(&bases[b]), A.total + 256, st));
-    CUDA_OK(cudaMemsetAsync(bases[b], 0, A.total + 256, st));
-    A.carve(bases[b]);
   }
+  // one allocation and one memset for all searches (same config: same layout)
+  const size_t per = (arenas[0].total + 255) & ~size_t(255);
+  char* big = nullptr;
+  CUDA_OK(cudaMallocAsync(reinterpret_cast<void**>(&big), per * n + 256, st));
+  CUDA_OK(cudaMemsetAsync(big, 0, per * n + 256, st));
+  for (int b = 0; b < n; ++b) arenas[b].carve(big + per * b);
   Run* d_runs = nullptr;
   CUDA_OK(cudaMallocAsync(reinterpret_cast<void**>(&d_runs), sizeof(Run) * n, st));
   CUDA_OK(cudaMemcpyAsync(d_runs, runs.data(), sizeof(Run) * n, cudaMemcpyHostToDevice, st));
@@ -1160,7 +1153,7 @@ bool run_batch_device(std::vector<spex_executor*>& exs, int device, cudaStream_t
       ex.ran = false;
     }
   }
-  for (int b = 0; b < n; ++b) cudaFreeAsync(bases[b], st);
+  cudaFreeAsync(big, st);
   cudaFreeAsync(d_runs, st);
   cudaFreeAsync(d_tab, st);
   cudaStreamSynchronize(st);
