@@ -301,9 +301,9 @@ def main():
     ctl_only = None
     if args.control_only > 0:
         n_b = args.control_only
-        spex.run_batch(cfg_text, [seed + k for k in range(n_b)])  # warm-up (grows the memory pool)
+        spex.run_batch(cfg_text, [seed + k for k in range(n_b)], device=local)  # warm-up
         t0c = time.perf_counter()
-        tots_b, ms_b = spex.run_batch(cfg_text, [seed + 1000 + k for k in range(n_b)])
+        tots_b, ms_b = spex.run_batch(cfg_text, [seed + 1000 + k for k in range(n_b)], device=local)
         wall_c = time.perf_counter() - t0c
         ctl_only = {"searches": n_b, "queries_per_s": sum(t.queries for t in tots_b) / wall_c,
                     "queries_per_s_device": sum(t.queries for t in tots_b) / (ms_b / 1000.0),
