@@ -152,6 +152,23 @@ int ref_run_experiment(const char* config_json, double* secs, double* makespan,
   }
 }
 
+/** run_experiment_full metrics as JSON (RunMetrics::to_json) — the oracle of
+ *  the experiment harness (treatment + baseline pairs over repetitions). */
+int ref_run_experiment_json(const char* config_json, char** out) {
+  try {
+    ExperimentConfig cfg = parse_cfg(config_json);
+    ExperimentResult res = run_experiment_full(cfg);
+    *out = dup_string(res.metrics.to_json().dump());
+    return 0;
+  } catch (const Error& e) {
+    g_err = e.what();
+    return static_cast<int>(e.code()) + 1;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 100;
+  }
+}
+
 /** Canonical config JSON (ExperimentConfig::to_json) after strict parsing. */
 int ref_canonical_config(const char* config_json, char** out) {
   try {

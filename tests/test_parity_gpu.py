@@ -99,3 +99,24 @@ def test_run_batch_matches_reference_totals():
         assert L.ref_run_timed(cfg.encode(), sd, None, 0, 1, ctypes.byref(secs), rt) == 0
         assert t.makespan == rt[0], (sd, t.makespan, rt[0])
         assert t.queries == int(rt[5])
+
+
+@pytest.mark.parametrize("family,flags", [("rebase_bfs", ["t1", "t2", "t3"]), ("rstar_dfs", ["t1", "t3"]),
+                                          ("rest_hybrid", [])])
+def test_experiment_metrics_match_reference(family, flags):
+    """run_experiment_full over the device path (treatment and baseline
+    repetitions each one batched control launch) equals the reference's
+    RunMetrics exactly (experiment.cpp:50-191)."""
+    _spex()
+    if refutil.ref_lib() is None:
+        pytest.skip("oracle/_ref not built")
+    import ctypes
+    from paper_2605_10195_b200.experiment import run_experiment
+    cfg = json.dumps({"family": family, "policy": {"width": 4, "max_depth": 8, "target_answers": 6},
+                      "workload": {"noise_sigma": 0.05},
+                      "run": {"batch_size": 6, "n_queries": 6, "flags": flags, "repetitions": 8, "seed": 3}})
+    R = refutil.ref_lib()
+    R.ref_run_experiment_json.argtypes = [ctypes.c_char_p, ctypes.POINTER(ctypes.c_char_p)]
+    out = ctypes.c_char_p()
+    assert R.ref_run_experiment_json(cfg.encode(), ctypes.byref(out)) == 0
+    assert run_experiment(cfg) == json.loads(out.value.decode())
