@@ -169,6 +169,42 @@ int ref_run_experiment_json(const char* config_json, char** out) {
   }
 }
 
+/** validate_trace over newline-separated JSON lines: report as JSON
+ *  {ok, problems, generated, committed, reused, wasted, queries, makespan}. */
+int ref_validate_trace(const char* lines_text, char** out) {
+  try {
+    std::vector<std::string> lines;
+    std::string cur;
+    for (const char* p = lines_text; *p; ++p) {
+      if (*p == '\n') {
+        if (!cur.empty()) lines.push_back(cur);
+        cur.clear();
+      } else {
+        cur.push_back(*p);
+      }
+    }
+    if (!cur.empty()) lines.push_back(cur);
+    ReplayReport r = validate_trace(parse_trace_lines(lines));
+    nlohmann::ordered_json j;
+    j["ok"] = r.ok;
+    j["problems"] = r.problems;
+    j["generated"] = r.generated;
+    j["committed"] = r.committed;
+    j["reused"] = r.reused;
+    j["wasted"] = r.wasted;
+    j["queries"] = r.queries;
+    j["makespan"] = r.makespan;
+    *out = dup_string(j.dump());
+    return 0;
+  } catch (const Error& e) {
+    g_err = e.what();
+    return static_cast<int>(e.code()) + 1;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 100;
+  }
+}
+
 /** Canonical config JSON (ExperimentConfig::to_json) after strict parsing. */
 int ref_canonical_config(const char* config_json, char** out) {
   try {
