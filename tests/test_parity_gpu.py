@@ -120,3 +120,19 @@ def test_experiment_metrics_match_reference(family, flags):
     out = ctypes.c_char_p()
     assert R.ref_run_experiment_json(cfg.encode(), ctypes.byref(out)) == 0
     assert run_experiment(cfg) == json.loads(out.value.decode())
+
+
+@pytest.mark.parametrize("cfgname", ["c2_rebase_w16_q256", "c3_rstar_w4_q512", "c4_rest_w4_q4096"])
+def test_device_logs_pass_the_validator(cfgname):
+    """The device event logs of the large configs pass the lifecycle /
+    conservation validator (validate_trace restated) with run_end agreeing."""
+    spex = _spex()
+    from paper_2605_10195_b200.replay import validate_log
+    cfg = (ROOT / "configs" / f"{cfgname}.json").read_text()
+    out = spex.run_once(cfg, json.loads(cfg)["run"]["seed"], None)
+    rep = validate_log(out.log)
+    assert rep.ok, rep.problems[:5]
+    t = out.totals
+    assert (rep.generated, rep.committed, rep.reused, rep.wasted) == (
+        t.generated_tokens, t.committed_tokens, t.reused_tokens, t.wasted_tokens)
+    assert rep.queries == t.queries
