@@ -34,13 +34,20 @@ namespace spex {
 
 namespace tc {
 
-constexpr int BM = 128, BN = 256, BK = 64, STAGES = 3;
+constexpr int BM = 128, BK = 64;
 constexpr int EN = 128;  // epilogue chunk (columns per tcgen05.ld pass)
 constexpr int kStageLd = EN + 4;  // padded row of the epilogue staging buffer (conflict-free float4)
 constexpr uint32_t kEpiBytes = 4 * 32 * kStageLd * 4;
 constexpr int kThreads = 192;
-constexpr uint32_t kStageBytes = (BM + BN) * BK * 2;  // 48 KB
-constexpr uint32_t kTmemCols = BN;  // one fp32 accumulator; two are allocated (double buffer)
+// per tile width BN (128 or 256): pipeline depth, bytes per stage, TMEM columns
+template <int BN> struct TileCfg {
+  static constexpr int STAGES = BN == 256 ? 3 : 4;
+  static constexpr uint32_t kStageBytes = (BM + BN) * BK * 2;  // 48 KB / 32 KB
+  static constexpr uint32_t kTmemCols = BN;                    // one fp32 accumulator; two allocated
+  // kind::f16 instruction descriptor: D f32, A/B bf16, both K-major, M=128, N=BN
+  static constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                                     ((uint32_t)(BM >> 4) << 24);
+};
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -81,16 +88,13 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t addr) {
          ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
 }
 
-// kind::f16 instruction descriptor: D f32, A/B bf16, both K-major, M=128, N=256
-constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
-                            ((uint32_t)(BM >> 4) << 24);
-
-__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t accumulate) {
+__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
+                                         uint32_t accumulate) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
-      "l"(da), "l"(db), "r"(kIdesc), "r"(accumulate));
+      "l"(da), "l"(db), "r"(idesc), "r"(accumulate));
 }
 
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
@@ -119,11 +123,15 @@ __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
 
 }  // namespace tc
 
-template <int EPI, int DH>
+template <int EPI, int DH, int BN>
 __global__ void __launch_bounds__(tc::kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
                    int K, TcEpilogue ep, unsigned long long* tile_ctr, unsigned long long tile_base) {
   using namespace tc;
+  using T = TileCfg<BN>;
+  constexpr int STAGES = T::STAGES;
+  constexpr uint32_t kStageBytes = T::kStageBytes;
+  constexpr uint32_t kTmemCols = T::kTmemCols;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // 1024-byte alignment for the 128B-swizzled tiles
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -218,7 +226,7 @@ __global__ void __launch_bounds__(tc::kThreads, 1)
           const uint64_t db = smem_desc(smem_u32(sB + s * BN * BK * 2));
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k)  // 16 bf16 = 32 bytes = 2 descriptor units per step
-            mma_bf16(dt, da + 2 * k, db + 2 * k, (kb | k) != 0);
+            mma_bf16(dt, da + 2 * k, db + 2 * k, T::kIdesc, (kb | k) != 0);
           mma_commit(&empty[s]);
         }
         mma_commit(&tfull[acc]);
@@ -353,7 +361,7 @@ __global__ void __launch_bounds__(tc::kThreads, 1)
   __syncthreads();
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * tc::kTmemCols));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * kTmemCols));
   }
 }
 
@@ -422,21 +430,52 @@ __global__ void interleave_gu_kernel(const __nv_bfloat16* __restrict__ wgu, int 
 
 using namespace spex;
 
+template <int EPI, int DH, int BN>
+static int launch_gemm_tc(const CUtensorMap* tmA, const CUtensorMap* tmB, int M, int N, int K, const TcEpilogue* ep,
+                          cudaStream_t s, int grid_x, unsigned long long* tile_ctr, unsigned long long tile_base) {
+  using T = tc::TileCfg<BN>;
+  const size_t smem = T::STAGES * T::kStageBytes + 1024 + 256 + tc::kEpiBytes;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(gemm_tc_kernel<EPI, DH, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  gemm_tc_kernel<EPI, DH, BN><<<grid_x, tc::kThreads, smem, s>>>(*tmA, *tmB, M, N, K, *ep, tile_ctr, tile_base);
+  return (int)cudaGetLastError();
+}
+
+template <int EPI, int DH>
+static int launch_bn(int bn, const CUtensorMap* tmA, const CUtensorMap* tmB, int M, int N, int K,
+                     const TcEpilogue* ep, cudaStream_t s, int grid_x, unsigned long long* ctr,
+                     unsigned long long base) {
+  return bn == 256 ? launch_gemm_tc<EPI, DH, 256>(tmA, tmB, M, N, K, ep, s, grid_x, ctr, base)
+                   : launch_gemm_tc<EPI, DH, 128>(tmA, tmB, M, N, K, ep, s, grid_x, ctr, base);
+}
+
 extern "C" int spex_k_gemm_tc(const CUtensorMap* tmA, const CUtensorMap* tmB, int M, int N, int K,
                               const TcEpilogue* ep, cudaStream_t s) {
   if (M <= 0) return 0;
   if (N % tc::EN || K % tc::BK) return -1;
-  const size_t smem = tc::STAGES * tc::kStageBytes + 1024 + 256 + tc::kEpiBytes;
   static int sms = 0;
   if (!sms) {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  const int tiles = ((N + tc::BN - 1) / tc::BN) * ((M + tc::BM - 1) / tc::BM);
   static const int cap = getenv("SPEX_TC_GRID") ? atoi(getenv("SPEX_TC_GRID")) : sms;
   const int gmax = cap > 0 && cap < sms ? cap : sms;
-  dim3 grid(tiles < gmax ? tiles : gmax);
+  // tile width: the one whose last wave is fuller (128-wide tiles cost a second
+  // A-tile read per 256 columns but fill the SMs on mid-size problems)
+  const int mb = (M + tc::BM - 1) / tc::BM;
+  auto eff = [&](int bn) {
+    const long long t = (long long)mb * ((N + bn - 1) / bn);
+    const long long waves = (t + gmax - 1) / gmax;
+    return (double)t / (double)(waves * gmax) * (bn == 256 ? 1.0 : 0.92);
+  };
+  static const int force_bn = getenv("SPEX_TC_BN") ? atoi(getenv("SPEX_TC_BN")) : 0;
+  const int bn = force_bn == 128 || force_bn == 256 ? force_bn : (eff(256) >= eff(128) ? 256 : 128);
+  const int tiles = mb * ((N + bn - 1) / bn);
+  const int grid_x = tiles < gmax ? tiles : gmax;
   // per-stream monotone tile counter: launch j claims ids [base_j, base_j + tiles + grid)
   struct Ctr {
     cudaStream_t st;
@@ -456,34 +495,23 @@ extern "C" int spex_k_gemm_tc(const CUtensorMap* tmA, const CUtensorMap* tmB, in
     if (cudaMalloc(&c->d, sizeof(unsigned long long)) != cudaSuccess) return -3;
     cudaMemsetAsync(c->d, 0, sizeof(unsigned long long), s);
   }
-  unsigned long long* const tile_ctr = c->d;
-  const unsigned long long tile_base = c->base;
-  c->base += (unsigned long long)tiles + grid.x;
-#define SPEX_TC_LAUNCH(E, D)                                                                               \
-  {                                                                                                        \
-    static bool attr = false;                                                                              \
-    if (!attr) {                                                                                           \
-      cudaFuncSetAttribute(gemm_tc_kernel<E, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);  \
-      attr = true;                                                                                         \
-    }                                                                                                      \
-    gemm_tc_kernel<E, D><<<grid, tc::kThreads, smem, s>>>(*tmA, *tmB, M, N, K, *ep, tile_ctr, tile_base);                       \
-    return (int)cudaGetLastError();                                                                        \
-  }
+  unsigned long long* const ctr = c->d;
+  const unsigned long long base = c->base;
+  c->base += (unsigned long long)tiles + grid_x;
   switch (ep->kind) {
     case TC_EPI_STORE:
-      SPEX_TC_LAUNCH(TC_EPI_STORE, 128)
+      return launch_bn<TC_EPI_STORE, 128>(bn, tmA, tmB, M, N, K, ep, s, grid_x, ctr, base);
     case TC_EPI_SWIGLU:
-      SPEX_TC_LAUNCH(TC_EPI_SWIGLU, 128)
+      return launch_bn<TC_EPI_SWIGLU, 128>(bn, tmA, tmB, M, N, K, ep, s, grid_x, ctr, base);
     case TC_EPI_LSE:
-      SPEX_TC_LAUNCH(TC_EPI_LSE, 128)
+      return launch_bn<TC_EPI_LSE, 128>(bn, tmA, tmB, M, N, K, ep, s, grid_x, ctr, base);
     case TC_EPI_ROPE_KV:
-      if (ep->dh == 128) SPEX_TC_LAUNCH(TC_EPI_ROPE_KV, 128)
-      if (ep->dh == 64) SPEX_TC_LAUNCH(TC_EPI_ROPE_KV, 64)
+      if (ep->dh == 128) return launch_bn<TC_EPI_ROPE_KV, 128>(bn, tmA, tmB, M, N, K, ep, s, grid_x, ctr, base);
+      if (ep->dh == 64) return launch_bn<TC_EPI_ROPE_KV, 64>(bn, tmA, tmB, M, N, K, ep, s, grid_x, ctr, base);
       return -1;
     default:
       return -1;
   }
-#undef SPEX_TC_LAUNCH
 }
 
 extern "C" void spex_k_lse_combine(const float* part, int M, int n_tiles, int* amax, float* lse, float* lsum,
