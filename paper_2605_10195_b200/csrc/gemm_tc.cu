@@ -470,7 +470,7 @@ extern "C" int spex_k_gemm_tc(const CUtensorMap* tmA, const CUtensorMap* tmB, in
   auto eff = [&](int bn) {
     const long long t = (long long)mb * ((N + bn - 1) / bn);
     const long long waves = (t + gmax - 1) / gmax;
-    return (double)t / (double)(waves * gmax) * (bn == 256 ? 1.0 : 0.92);
+    return (double)t / (double)(waves * gmax) * (bn == 256 ? 1.0 : 0.85);
   };
   static const int force_bn = getenv("SPEX_TC_BN") ? atoi(getenv("SPEX_TC_BN")) : 0;
   const int bn = force_bn == 128 || force_bn == 256 ? force_bn : (eff(256) >= eff(128) ? 256 : 128);
