@@ -113,3 +113,30 @@ def edge_configs():
         add(f"{fam}-kv-latency", fam, "t1,t2,t3", hardware={"kv_bytes_per_token": 131072.0, "reward_latency": 0.5})
         add(f"{fam}-skewed", fam, "t1,t3", 11, workload={"skew": 0.6, "answer_alphabet": 12})
     return cases
+
+
+def random_configs(n=60, seed=2026):
+    """Random configurations across the families, flag sets, widths, depths,
+    targets, noise, batch/queue sizes, latency and KV pricing (seeded)."""
+    import random
+    rng = random.Random(seed)
+    fams = ("rstar_dfs", "rest_hybrid", "rebase_bfs")
+    flagsets = ("", "t1", "t2", "t3", "t1,t2", "t1,t3", "t2,t3", "t1,t2,t3")
+    out = []
+    for i in range(n):
+        fam = rng.choice(fams)
+        nq = rng.randint(1, 12)
+        cfg = {"family": fam,
+               "policy": {"width": rng.randint(1, 10), "max_depth": rng.randint(1, 14),
+                          "target_answers": rng.randint(1, 12), "exploration_c": rng.choice([0.5, 1.0, 2.0]),
+                          "balance_temperature": rng.choice([0.5, 1.0, 3.0])},
+               "workload": {"noise_sigma": rng.choice([0.0, 0.05, 0.2]), "skew": rng.choice([0.0, 0.3]),
+                            "answer_alphabet": rng.randint(2, 12)},
+               "hardware": {"kv_bytes_per_token": rng.choice([0.0, 131072.0]),
+                            "reward_latency": rng.choice([0.05, 0.1, 0.4])},
+               "budget": {"tau": rng.choice([1.0, 2.0, 4.0])},
+               "termination": {"alpha": rng.choice([0.25, 0.5, 1.0]), "min_frac": rng.choice([0.4, 0.6])},
+               "run": {"batch_size": rng.randint(1, nq), "n_queries": nq, "spec_k": rng.randint(1, 12),
+                       "max_producers": rng.choice([4, 16, 64])}}
+        out.append((f"rand{i}-{fam}", json.dumps(cfg), rng.randint(1, 10000), rng.choice(flagsets)))
+    return out

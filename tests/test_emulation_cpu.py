@@ -83,3 +83,12 @@ def test_emulation_run_batch_equals_single_runs():
     for k, sd in enumerate(seeds):
         _, t = emu_run(L, cfg, sd, None)
         assert tots[k].as_dict() == t.as_dict()
+
+
+@pytest.mark.skipif(refutil.ref_lib() is None, reason="oracle/_ref not built")
+@pytest.mark.parametrize("name,cfg,seed,flags", refutil.random_configs(200, seed=7))
+def test_emulation_random_configs_vs_reference(name, cfg, seed, flags):
+    L = emu()
+    got, _ = emu_run(L, cfg, seed, flags)
+    res = refutil.compare_logs(refutil.ref_run_log(cfg, seed, flags), got)
+    assert res["decision_ok"], (name, res)

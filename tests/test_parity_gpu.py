@@ -136,3 +136,11 @@ def test_device_logs_pass_the_validator(cfgname):
     assert (rep.generated, rep.committed, rep.reused, rep.wasted) == (
         t.generated_tokens, t.committed_tokens, t.reused_tokens, t.wasted_tokens)
     assert rep.queries == t.queries
+
+
+@pytest.mark.parametrize("name,cfg,seed,flags", refutil.random_configs())
+def test_random_configs_match_reference(name, cfg, seed, flags):
+    spex = _spex()
+    if refutil.ref_lib() is None:
+        pytest.skip("oracle/_ref not built")
+    _check(name, refutil.ref_run_log(cfg, seed, flags), spex.run_once(cfg, seed, flags).log)
