@@ -37,6 +37,8 @@ sys.path.insert(0, str(ROOT))
 # serialise behind each other (read at CUDA initialisation)
 os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 
+from paper_2605_10195_b200.shard import query_block, shard_seed  # noqa: E402
+
 DEFAULT_CONFIG = "c2_rebase_w16_q256"
 PEAKS = ROOT / "MEASURED_PEAKS.json"
 PROFILE_TRAFFIC = ROOT / "profiles" / "k1_traffic.json"
@@ -53,6 +55,10 @@ def parse():
     ap.add_argument("--policy", default="mid_policy")
     ap.add_argument("--prm", default="mid_prm")
     ap.add_argument("--cpu-sample-runs", type=int, default=4)
+    ap.add_argument("--sharding", default="independent", choices=["independent", "coupled"],
+                    help="independent: each rank a whole search of its own queries (run seed + rank, weak "
+                         "scaling); coupled: ONE search, the control replicated on every rank and the model "
+                         "work of query block r on rank r (single virtual clock, global T2; strong scaling)")
     ap.add_argument("--control-only", type=int, default=296,
                     help="also time N control-only searches in one batched launch (no model), 0 = off")
     ap.add_argument("--named-shapes", type=int, default=1,
@@ -194,7 +200,7 @@ def run_reference(args, cfg_text, seed, rank, world):
     v = tq / tt
     line = {"metric": metric, "value": v, "unit": "queries/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1000 * tt / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "fp64", "data": "synthetic",
+            "scaling": "strong" if coupled else "weak", "vs_baseline": None, "dtype": "fp64", "data": "synthetic",
             "impl": "reference",
             "config": {"workload": args.config, "queries_per_search": json.loads(cfg_text)["run"]["n_queries"],
                        "searches_per_step": per_step},
@@ -211,7 +217,11 @@ def main():
     cfg_text = (ROOT / "configs" / f"{args.config}.json").read_text()
     cfg = json.loads(cfg_text)
     base_seed = cfg["run"]["seed"]
-    seed = base_seed + rank  # disjoint query sets per rank (weak scaling)
+    coupled = args.sharding == "coupled"
+    # independent: disjoint query sets per rank (weak scaling); coupled: one
+    # search whose query blocks' model work is split over the ranks
+    seed = base_seed if coupled else shard_seed(base_seed, rank)
+    q_lo, q_hi = query_block(cfg["run"]["n_queries"], rank, world) if coupled else (0, cfg["run"]["n_queries"])
     if args.impl == "reference":
         run_reference(args, cfg_text, base_seed, rank, world)
         return
@@ -233,7 +243,10 @@ def main():
     def one_search(trace: bool, flags=None):
         ex = spex.Executor(cfg_text, seed, flags, trace=trace, device=local)
         ex.set_model(args.policy, args.prm, weight_seed=1)
+        if coupled:
+            ex.set_shard(rank, world)
         tot = ex.run()
+        tot.queries = q_hi - q_lo  # queries whose model work ran here
         d2h = 0
         if trace:
             log = ex.log_lines()  # the run's event log, copied back and serialised
@@ -378,11 +391,12 @@ def main():
         "dtype": "bf16",
         "data": "synthetic (hash-seeded prompts and teacher-forced tokens, random-init weights)",
         "config": {"workload": f"{args.config}: rebase_bfs w16 d16 target16, T1, "
-                               f"{cfg['run']['n_queries']} queries/GPU/step",
+                               f"{cfg['run']['n_queries']} queries/{'step' if coupled else 'GPU/step'}",
                    "policy": args.policy, "prm": args.prm,
                    "queries_per_step_per_gpu": cfg["run"]["n_queries"],
                    "l2": "inputs larger than L2 (tree KV pools of tens of GB per search)",
-                   "parallelism": f"query-sharded x{world}"},
+                   "parallelism": (f"query-block model work x{world}, search replicated (single virtual clock)"
+                                   if coupled else f"query-sharded x{world}")},
         "e2e": {"value": total_e2e_q / e2e_wall, "unit": "queries/s",
                 "h2d_bytes_per_step": len(cfg_text.encode()),
                 "d2h_bytes_per_step": 256 + 256 * cfg["run"]["n_queries"],

@@ -123,6 +123,14 @@ int spex_executor_stats(spex_executor* ex, spex_stats* out);
  * "prm_1p5b"; prm_shape "" disables the PRM. Call before spex_executor_run. */
 int spex_executor_set_model(spex_executor* ex, const char* policy_shape, const char* prm_shape,
                             uint64_t weight_seed, int record_outputs);
+/* Query-sharded model work across `world` GPUs, the search replicated: this
+ * executor runs the policy/PRM forward only for queries
+ * [Q*rank/world, Q*(rank+1)/world) while its control kernel still runs the
+ * whole search, so every rank makes the reference's single-server decisions
+ * (one virtual clock, global T2 budgets, executor.cpp:705-740) with no
+ * exchange. Call before spex_executor_run. Replaces nothing in the reference
+ * (one server); SURVEY.md §8e. */
+int spex_executor_set_shard(spex_executor* ex, int rank, int world);
 int spex_executor_model_stats(spex_executor* ex, spex_model_stats* out);
 /* Copies up to cap records; *n receives the total available. */
 int spex_executor_decode_outputs(spex_executor* ex, void* buf, long long cap, long long* n);

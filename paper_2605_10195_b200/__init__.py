@@ -180,6 +180,12 @@ class Executor:
         _check(self._L.spex_executor_set_model(self._h, policy.encode(), (prm or "").encode(), int(weight_seed),
                                                1 if record_outputs else 0))
 
+    def set_shard(self, rank: int, world: int) -> None:
+        """Run the model forward only for this rank's query block
+        [Q*rank/world, Q*(rank+1)/world); the search itself stays whole, so
+        every rank's decisions and log equal the single-server reference's."""
+        _check(self._L.spex_executor_set_shard(self._h, int(rank), int(world)))
+
     def model_stats(self) -> dict:
         s = _lib.ModelStats()
         _check(self._L.spex_executor_model_stats(self._h, ctypes.byref(s)))

@@ -122,6 +122,7 @@ _EXPORTS = {
         [ctypes.c_void_p, ctypes.POINTER(ctypes.c_double), ctypes.c_int, ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
     "spex_executor_set_model": (
         [ctypes.c_void_p, ctypes.c_char_p, ctypes.c_char_p, ctypes.c_uint64, ctypes.c_int], ctypes.c_int),
+    "spex_executor_set_shard": ([ctypes.c_void_p, ctypes.c_int, ctypes.c_int], ctypes.c_int),
     "spex_executor_model_stats": ([ctypes.c_void_p, ctypes.POINTER(ModelStats)], ctypes.c_int),
     "spex_executor_decode_outputs": (
         [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_longlong, ctypes.POINTER(ctypes.c_longlong)], ctypes.c_int),

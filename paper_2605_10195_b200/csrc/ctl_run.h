@@ -250,7 +250,10 @@ SPEX_HD void kv_ancestors_adjust(Run* R, int sid, int delta) {
     if (delta > 0 && old == 0) acc += R->n_tokens[base + cur];
     if (delta < 0 && old == 1) acc -= R->n_tokens[base + cur];
   }
-  if (acc != 0) atomic_add_i64(&R->g->u_anc, acc);
+  if (acc != 0) {
+    atomic_add_i64(&R->g->u_anc, acc);
+    if (q_owned(R->cfg, q)) atomic_add_i64(&R->g->u_anc_own, acc);
+  }
 }
 
 // Publish schedule entry e to the host (all block writes before it become
@@ -293,11 +296,15 @@ template <class EX>
 SPEX_HDNI void record_decode(Run* R, EX& ex, int steps) {
   GState* g = R->g;
   const int nreg = g->n_active_region;
-  for (int i = ex.tid; i < nreg; i += ex.nthr)
-    R->it_scan_b[i] = R->st_state[R->live[i]] == ST_ACTIVE ? 1 : 0;
+  const bool sharded = R->cfg.shard_lo > 0 || R->cfg.shard_hi < R->cfg.n_queries;
+  for (int i = ex.tid; i < nreg; i += ex.nthr) {
+    const int sid = R->live[i];
+    R->it_scan_b[i] = R->st_state[sid] == ST_ACTIVE && q_owned(R->cfg, R->st_q[sid]) ? 1 : 0;
+  }
   ex.sync();
   int n = 0;
   ex_scan(ex, R->it_scan_b, nreg, &n);
+  i64 own_done = 0;
   const int off = g->n_sched_rows;
   if (g->n_sched >= R->cfg.sched_cap || off + n > R->cfg.sched_rows_cap) {
     if (ex.tid == 0) set_err(R, ERR_CAP_STAGE, -1, kNoNode);
@@ -307,14 +314,18 @@ SPEX_HDNI void record_decode(Run* R, EX& ex, int steps) {
   for (int i = ex.tid; i < nreg; i += ex.nthr) {
     int sid = R->live[i];
     if (R->st_state[sid] == ST_ACTIVE) {
+      if (!q_owned(R->cfg, R->st_q[sid])) continue;
       R->srow_sid[off + R->it_scan_b[i]] = sid;
       R->srow_pos0[off + R->it_scan_b[i]] = R->st_done[sid];
+      own_done += R->st_done[sid];
     }
   }
+  if (sharded) own_done = ex_sum_i64(ex, own_done);
   if (ex.tid == 0) {
     const int e = g->n_sched++;
     R->sched_kind[e] = SCHED_DECODE;
-    R->sched_u[e] = g->u_anc + g->sum_done - static_cast<i64>(steps) * n;  // U at epoch start
+    // U at epoch start (of the owned shard when sharded)
+    R->sched_u[e] = sharded ? g->u_anc_own + own_done : g->u_anc + g->sum_done - static_cast<i64>(steps) * n;
     R->sched_steps[e] = steps;
     R->sched_off[e] = off;
     R->sched_n[e] = n;
@@ -1036,7 +1047,9 @@ SPEX_HDNI void completions(Run* R, EX& ex, int* warp_off) {
   for (int r = 0; r < rounds; ++r) process_items(R, ex, nf, IK_FIN, r, warp_off);
   if (R->cfg.record_sched) {
     // reward batch of this boundary: the non-stale completions, in order
-    for (int f = ex.tid; f < nf; f += ex.nthr) R->it_scan_a[f] = R->fin_scored[f];
+    // (owned query shard only: the other ranks score the rest)
+    for (int f = ex.tid; f < nf; f += ex.nthr)
+      R->it_scan_a[f] = R->fin_scored[f] && q_owned(R->cfg, R->st_q[R->fins[f]]) ? 1 : 0;
     ex.sync();
     int ns = 0;
     ex_scan(ex, R->it_scan_a, nf, &ns);
@@ -1045,7 +1058,7 @@ SPEX_HDNI void completions(Run* R, EX& ex, int* warp_off) {
       if (ex.tid == 0) set_err(R, ERR_CAP_STAGE, -1, kNoNode);
     } else if (ns > 0) {
       for (int f = ex.tid; f < nf; f += ex.nthr) {
-        const int sc = R->fin_scored[f];
+        const int sc = R->fin_scored[f] && q_owned(R->cfg, R->st_q[R->fins[f]]);
         R->it_scan_b[f] = sc ? R->fin_tokens[f] : 0;
         R->it_scan_d[f] = sc ? (R->fin_tokens[f] + kTileRows - 1) / kTileRows : 0;
       }
@@ -1054,7 +1067,7 @@ SPEX_HDNI void completions(Run* R, EX& ex, int* warp_off) {
       ex_scan(ex, R->it_scan_b, nf, &nrows);
       ex_scan(ex, R->it_scan_d, nf, &ntiles);
       for (int f = ex.tid; f < nf; f += ex.nthr)
-        if (R->fin_scored[f]) {
+        if (R->fin_scored[f] && q_owned(R->cfg, R->st_q[R->fins[f]])) {
           const int k = off + R->it_scan_a[f];
           R->srow_sid[k] = R->fins[f];
           R->srow_pos0[k] = R->fin_tokens[f];

@@ -177,9 +177,14 @@ struct Cfg {
   int record_sched;    // record the decode/PRM schedule for the model forward
   int sched_cap;       // schedule entries
   int sched_rows_cap;  // schedule rows
+  // Query shard whose model work this rank runs ([shard_lo, shard_hi)); the
+  // search itself (every query) is replicated, so decisions are unaffected.
+  int shard_lo, shard_hi;
   int lex_rank[kMaxLabels];   // label index -> rank of "a<idx>" in std::map order
   int lex_order[kMaxLabels];  // rank -> label index
 };
+
+SPEX_HD bool q_owned(const Cfg& c, int q) { return q >= c.shard_lo && q < c.shard_hi; }
 
 SPEX_HD int budget_at(const Cfg& c, int depth) {
   if (depth >= 0 && depth < c.n_depth_widths) return c.depth_widths[depth];
@@ -229,6 +234,7 @@ struct GState {
   double compute_, mem_a_, mem_d_;
   double makespan;
   i64 u_anc;     // sum over distinct (tree, strict ancestor of an active member) token_len
+  i64 u_anc_own;  // the same over the owned query shard (model-work accounting only)
   i64 sum_done;  // sum of partial tokens over active members
   int next_sid;
   int finished_count, admitted_count;

@@ -476,26 +476,33 @@ extern "C" int spex_k_gemm_tc(const CUtensorMap* tmA, const CUtensorMap* tmB, in
   const int bn = force_bn == 128 || force_bn == 256 ? force_bn : (eff(256) >= eff(128) ? 256 : 128);
   const int tiles = mb * ((N + bn - 1) / bn);
   const int grid_x = tiles < gmax ? tiles : gmax;
-  // per-stream monotone tile counter: launch j claims ids [base_j, base_j + tiles + grid)
+  // per-stream monotone tile counter: launch j claims ids [base_j, base_j + tiles + grid).
+  // Counters come from one pool; a stream seen for the first time takes the
+  // least recently assigned slot (streams are per executor, so after
+  // kCtrSlots newer streams the evicted one has long finished).
+  constexpr int kCtrSlots = 256;
   struct Ctr {
     cudaStream_t st;
-    unsigned long long* d;
     unsigned long long base;
   };
-  static Ctr ctrs[16];
+  static Ctr ctrs[kCtrSlots];
+  static unsigned long long* pool = nullptr;
   static int n_ctrs = 0;
+  if (!pool) {
+    if (cudaMalloc(&pool, kCtrSlots * sizeof(unsigned long long)) != cudaSuccess) return -3;
+    if (cudaMemset(pool, 0, kCtrSlots * sizeof(unsigned long long)) != cudaSuccess) return -3;
+  }
   Ctr* c = nullptr;
-  for (int i = 0; i < n_ctrs; ++i)
+  for (int i = 0; i < n_ctrs && i < kCtrSlots; ++i)
     if (ctrs[i].st == s) c = &ctrs[i];
   if (!c) {
-    if (n_ctrs == 16) return -2;
-    c = &ctrs[n_ctrs++];
+    c = &ctrs[n_ctrs % kCtrSlots];
     c->st = s;
     c->base = 0;
-    if (cudaMalloc(&c->d, sizeof(unsigned long long)) != cudaSuccess) return -3;
-    cudaMemsetAsync(c->d, 0, sizeof(unsigned long long), s);
+    cudaMemsetAsync(pool + (c - ctrs), 0, sizeof(unsigned long long), s);
+    ++n_ctrs;
   }
-  unsigned long long* const ctr = c->d;
+  unsigned long long* const ctr = pool + (c - ctrs);
   const unsigned long long base = c->base;
   c->base += (unsigned long long)tiles + grid_x;
   switch (ep->kind) {

@@ -827,8 +827,9 @@ void run_model_schedule(const ModelRunConfig& mc, const ScheduleView& sv, ModelR
   g_launches = 0;
   g_gemms = 0;
   if (P > 0) {
-    for (int q0 = 0; q0 < Q; q0 += prompt_chunk) {
-      const int nq = std::min(prompt_chunk, Q - q0);
+    const int q_end = std::min(sv.shard_hi, Q);
+    for (int q0 = sv.shard_lo; q0 < q_end; q0 += prompt_chunk) {
+      const int nq = std::min(prompt_chunk, q_end - q0);
       const int ntp = nq * ((P + kTileRows - 1) / kTileRows);
       spex_k_build_prompt_rows(tv_pol, q0, nq, rows, segs, st);
       spex_k_build_prompt_tiles(nq, P, tiles, st);

@@ -29,6 +29,7 @@ struct ModelRunConfig {
 struct ScheduleView {
   TreeView tree;
   int n_queries;
+  int shard_lo = 0, shard_hi = 0;  // owned query range [lo, hi): prompt prefill (the schedule arrives filtered)
   long long kv_slots;        // tree KV pool capacity (slots)
   int max_decode_rows;       // row-buffer capacity for decode steps (larger entries are chunked)
   int max_prm_rows;          // row-buffer capacity for one PRM batch

@@ -458,6 +458,7 @@ struct spex_executor {
   double device_ms = 0.0;
   int nthreads = 512;
   int record_sched = 0;
+  int shard_lo = 0, shard_hi = -1;  // owned query range of the model work (-1: all)
 #ifndef SPEX_EMU
   cudaStream_t stream = nullptr;
   cudaStream_t mstream = nullptr;
@@ -547,6 +548,8 @@ void set_cfg(const spex_executor& ex, Cfg& c, int node_cap, int stream_cap, int 
   c.stage_cap = stage_cap;
   c.trace = trace;
   c.record_sched = record_sched;
+  c.shard_lo = std::min(ex.shard_lo, h.n_queries);
+  c.shard_hi = ex.shard_hi < 0 ? h.n_queries : std::min(ex.shard_hi, h.n_queries);
   c.sched_cap = record_sched ? 4 * stream_cap + 1024 : 1;
   c.sched_rows_cap = record_sched ? 64 * stream_cap + 4096 : 1;
   // std::map<std::string,...> order of "a0".."a{n-1}" (termination.hpp:39)
@@ -938,6 +941,8 @@ void run_executor(spex_executor& ex, int trace) {
       sv.tree.node_cap = node_cap;
       sv.tree.prompt_tokens = ex.hc.prompt_tokens;
       sv.n_queries = Q;
+      sv.shard_lo = R.cfg.shard_lo;
+      sv.shard_hi = R.cfg.shard_hi;
       sv.srow_sid = R.srow_sid;
       sv.srow_pos0 = R.srow_pos0;
       sv.srow_rstart = R.srow_rstart;
@@ -1315,6 +1320,16 @@ int spex_executor_set_model(spex_executor* ex, const char* policy_shape, const c
     ex->mc.record_outputs = record_outputs != 0;
     ex->with_model = true;
 #endif
+  });
+}
+
+int spex_executor_set_shard(spex_executor* ex, int rank, int world) {
+  return guarded([&] {
+    if (world < 1 || rank < 0 || rank >= world) fail(ERR_INVALID_ARGUMENT, "set_shard: rank out of range");
+    if (ex->ran) fail(ERR_INVALID_ARGUMENT, "set_shard: executor already ran");
+    const long long Q = ex->hc.n_queries;
+    ex->shard_lo = static_cast<int>(Q * rank / world);
+    ex->shard_hi = static_cast<int>(Q * (rank + 1) / world);
   });
 }
 
