@@ -200,7 +200,7 @@ def run_reference(args, cfg_text, seed, rank, world):
     v = tq / tt
     line = {"metric": metric, "value": v, "unit": "queries/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1000 * tt / args.steps, "higher_is_better": True,
-            "scaling": "strong" if coupled else "weak", "vs_baseline": None, "dtype": "fp64", "data": "synthetic",
+            "scaling": "weak", "vs_baseline": None, "dtype": "fp64", "data": "synthetic",
             "impl": "reference",
             "config": {"workload": args.config, "queries_per_search": json.loads(cfg_text)["run"]["n_queries"],
                        "searches_per_step": per_step},
@@ -386,7 +386,7 @@ def main():
         "warmup": args.warmup,
         "ms_per_step": 1000.0 * dev_s / args.steps,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong" if coupled else "weak",
         "vs_baseline": None,
         "dtype": "bf16",
         "data": "synthetic (hash-seeded prompts and teacher-forced tokens, random-init weights)",

@@ -62,7 +62,7 @@ struct QC {
 
 SPEX_HD int scratch_stride(const Cfg& c) { return c.node_cap + 64; }
 
-SPEX_HD QC make_qc(Run* R, int q, Item* it, int warp) {
+SPEX_HD QC make_qc(Run* R, int q, Item* it, int slot) {
   QC x;
   x.R = R;
   x.q = q;
@@ -71,12 +71,12 @@ SPEX_HD QC make_qc(Run* R, int q, Item* it, int warp) {
   x.it = it;
   x.c = &R->cfg;
   const int S = scratch_stride(R->cfg);
-  x.stack = R->sp_stack + static_cast<i64>(warp) * S;
-  x.sv = R->sp_visits + static_cast<i64>(warp) * S;
-  x.sval = R->sp_value + static_cast<i64>(warp) * S;
-  x.snch = R->sp_nchild + static_cast<i64>(warp) * S;
-  x.dbl = R->sp_dbl + static_cast<i64>(warp) * 3 * S;
-  x.ints = R->sp_int + static_cast<i64>(warp) * 3 * S;
+  x.stack = R->sp_stack + static_cast<i64>(slot) * S;
+  x.sv = R->sp_visits + static_cast<i64>(slot) * S;
+  x.sval = R->sp_value + static_cast<i64>(slot) * S;
+  x.snch = R->sp_nchild + static_cast<i64>(slot) * S;
+  x.dbl = R->sp_dbl + static_cast<i64>(slot) * 3 * S;
+  x.ints = R->sp_int + static_cast<i64>(slot) * 3 * S;
   return x;
 }
 

@@ -37,7 +37,7 @@ __global__ void __launch_bounds__(512, 1) spex_control_kernel(const Run* __restr
   __shared__ int sm[1024 + 8];
   __shared__ double smd[32];
   __shared__ long long sml[32];
-  __shared__ int warp_off[32 * 3];
+  __shared__ int warp_off[512 * 3];  // per-thread item staging offsets
   // The per-query records and the run scalars are touched by every phase of
   // every consumer iteration: when they fit, they live in shared memory for
   // the whole run (generic pointers, so the control code is unchanged) and are

@@ -69,19 +69,16 @@ SPEX_HDNI void ex_scan(EX& ex, int* a, int n, int* total) {
     }
     if (ex.lane == 31) ws[ex.warp] = incl;
     ex.sync();
-    if (ex.warp == 0) {
-      const int wv = ex.lane < ex.nwarp ? ws[ex.lane] : 0;
-      int winc = wv;
-      for (int off = 1; off < 32; off <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, winc, off);
-        if (ex.lane >= off) winc += y;
-      }
-      ws[ex.lane] = winc - wv;
-      if (ex.lane == 31) ws[32] = winc;
+    // every warp reduces the warp totals itself (lane w holds warp w's):
+    // its exclusive offset and the grand total, no second barrier
+    const int wv = ex.lane < ex.nwarp ? ws[ex.lane] : 0;
+    int before = ex.lane < ex.warp ? wv : 0, all = wv;
+    for (int off = 16; off > 0; off >>= 1) {
+      before += __shfl_xor_sync(0xffffffffu, before, off);
+      all += __shfl_xor_sync(0xffffffffu, all, off);
     }
-    ex.sync();
-    if (ex.tid < n) a[ex.tid] = ws[ex.warp] + incl - v;
-    *total = ws[32];
+    if (ex.tid < n) a[ex.tid] = before + incl - v;
+    *total = all;
     ex.sync();
     return;
   }
@@ -141,8 +138,11 @@ SPEX_HDNI int ex_min_int(EX& ex, int v) {
   }
   if (ex.lane == 0) ex.sm[ex.warp] = v;
   ex.sync();
-  int r = ex.sm[0];
-  for (int w = 1; w < ex.nwarp; ++w) r = ex.sm[w] < r ? ex.sm[w] : r;
+  int r = ex.lane < ex.nwarp ? ex.sm[ex.lane] : ex.sm[0];
+  for (int off = 16; off > 0; off >>= 1) {
+    const int y = __shfl_xor_sync(0xffffffffu, r, off);
+    r = y < r ? y : r;
+  }
   ex.sync();
   return r;
 #else
@@ -156,8 +156,8 @@ SPEX_HDNI i64 ex_sum_i64(EX& ex, i64 v) {
   for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
   if (ex.lane == 0) ex.sml[ex.warp] = v;
   ex.sync();
-  i64 r = 0;
-  for (int w = 0; w < ex.nwarp; ++w) r += ex.sml[w];
+  i64 r = ex.lane < ex.nwarp ? ex.sml[ex.lane] : 0;
+  for (int off = 16; off > 0; off >>= 1) r += __shfl_xor_sync(0xffffffffu, r, off);
   ex.sync();
   return r;
 #else
@@ -599,13 +599,19 @@ SPEX_HDNI void process_items(Run* R, EX& ex, int n_items, int kind, int rank_fil
                            int* warp_off) {
   GState* g = R->g;
   const Cfg& c = R->cfg;
-  if (ex.lane == 0) {
-    int* off = warp_off + ex.warp * 3;
-    for (int i = ex.warp; i < n_items; i += ex.nwarp) {
+  {
+    // one item per thread: every thread is an independent sequential state
+    // machine with its own staging slot and scratch (the items of a phase
+    // touch disjoint queries). Items are dealt round-robin over the warps
+    // first (item i -> warp i % nwarp, lane i / nwarp) so all warps share
+    // the work and their memory latencies overlap.
+    const int slot = ex.tid;
+    int* off = warp_off + slot * 3;
+    for (int i = ex.lane * ex.nwarp + ex.warp; i < n_items; i += ex.nthr) {
       if (kind == IK_FIN && R->it_scan_c[i] != rank_filter) continue;
       if (g->error) break;
       Item it;
-      const i64 wb = static_cast<i64>(ex.warp) * c.stage_cap;
+      const i64 wb = static_cast<i64>(slot) * c.stage_cap;
       it.rec = R->stage_rec + wb + off[0];
       it.nrec = 0;
       it.rec_cap = c.stage_cap - off[0];
@@ -621,21 +627,21 @@ SPEX_HDNI void process_items(Run* R, EX& ex, int n_items, int kind, int rank_fil
       if (kind == IK_FIN) {
         int sid = R->fins[i];
         q = R->st_q[sid];
-        QC x = make_qc(R, q, &it, ex.warp);
+        QC x = make_qc(R, q, &it, slot);
         R->fin_scored[i] = on_stream_done(x, sid, R->fin_tokens[i], R->fin_cancel[i]) ? 1 : 0;
         R->qs[q].need_followup = 1;
       } else if (kind == IK_REWARD) {
         q = R->it_key[i];
-        QC x = make_qc(R, q, &it, ex.warp);
+        QC x = make_qc(R, q, &it, slot);
         on_reward(x, R->ev_node[g->fifo_head - 1]);
         R->qs[q].need_followup = 1;
       } else if (kind == IK_FOLLOWUP) {
         q = R->it_key[i];
-        QC x = make_qc(R, q, &it, ex.warp);
+        QC x = make_qc(R, q, &it, slot);
         followup(x);
       } else {
         q = R->it_key[i];
-        QC x = make_qc(R, q, &it, ex.warp);
+        QC x = make_qc(R, q, &it, slot);
         int k = R->qs[q].grant;
         int n = issue_speculation(x, k);
         if (n == 0) R->qs[q].plan_empty_version = R->qs[q].version;
@@ -663,7 +669,7 @@ SPEX_HDNI void process_items(Run* R, EX& ex, int n_items, int kind, int rank_fil
 
 template <class EX>
 SPEX_HDNI void reset_warp_offsets(Run* R, EX& ex, int* warp_off) {
-  for (int i = ex.tid; i < ex.nwarp * 3; i += ex.nthr) warp_off[i] = 0;
+  for (int i = ex.tid; i < ex.nthr * 3; i += ex.nthr) warp_off[i] = 0;
   ex.sync();
 }
 
@@ -876,12 +882,13 @@ SPEX_HD int collect_queries(Run* R, EX& ex, Pred pred) {
     const unsigned bal = __ballot_sync(0xffffffffu, p);
     if (ex.lane == 0) wc[ex.warp] = __popc(bal);
     ex.sync();
-    int off = total, chunk = 0;
-    for (int w = 0; w < ex.nwarp; ++w) {
-      const int cw = wc[w];
-      if (w < ex.warp) off += cw;
-      chunk += cw;
+    const int cw = ex.lane < ex.nwarp ? wc[ex.lane] : 0;
+    int before = ex.lane < ex.warp ? cw : 0, chunk = cw;
+    for (int o = 16; o > 0; o >>= 1) {
+      before += __shfl_xor_sync(0xffffffffu, before, o);
+      chunk += __shfl_xor_sync(0xffffffffu, chunk, o);
     }
+    const int off = total + before;
     if (p) R->it_key[off + __popc(bal & ((1u << ex.lane) - 1u))] = q;
     total += chunk;
     ex.sync();

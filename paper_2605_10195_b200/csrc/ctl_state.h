@@ -319,7 +319,7 @@ struct Run {
   u32* ev_node;
   // log
   Rec* log;
-  // per-warp staging (nwarps * stage_cap)
+  // per-thread staging (nthreads * stage_cap)
   Rec* stage_rec;
   SpawnRec* stage_spawn;
   PushRec* stage_push;
@@ -354,7 +354,7 @@ struct Run {
   int* it_scan_c;
   int* it_scan_d;
   int item_cap;
-  // per-warp speculation scratch (nwarps * (node_cap + 64))
+  // per-thread speculation scratch (nthreads * (node_cap + 64))
   int* sp_visits;
   double* sp_value;
   int* sp_nchild;

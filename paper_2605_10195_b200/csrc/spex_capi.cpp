@@ -562,7 +562,7 @@ void set_cfg(const spex_executor& ex, Cfg& c, int node_cap, int stream_cap, int 
   }
 }
 
-void layout(Arena& A, Run& R, int Q, int node_cap, int stream_cap, int log_cap, int nwarps,
+void layout(Arena& A, Run& R, int Q, int node_cap, int stream_cap, int log_cap, int slots,
             int stage_cap) {
   const size_t NN = static_cast<size_t>(Q) * node_cap;
   A.add(R.g, 1);
@@ -606,7 +606,7 @@ void layout(Arena& A, Run& R, int Q, int node_cap, int stream_cap, int log_cap, 
   A.add(R.ev_time, S);
   A.add(R.ev_q, S);
   A.add(R.ev_node, S);
-  const size_t W = static_cast<size_t>(nwarps) * stage_cap;
+  const size_t W = static_cast<size_t>(slots) * stage_cap;  // one staging slot per control thread
   A.add(R.stage_rec, W);
   A.add(R.stage_spawn, W);
   A.add(R.stage_push, W);
@@ -629,7 +629,7 @@ void layout(Arena& A, Run& R, int Q, int node_cap, int stream_cap, int log_cap, 
   A.add(R.it_scan_b, IC);
   A.add(R.it_scan_c, IC);
   A.add(R.it_scan_d, IC);
-  const size_t SS = static_cast<size_t>(nwarps) * (node_cap + 64);
+  const size_t SS = static_cast<size_t>(slots) * (node_cap + 64);
   A.add(R.sp_visits, SS);
   A.add(R.sp_value, SS);
   A.add(R.sp_nchild, SS);
@@ -825,7 +825,7 @@ void run_executor(spex_executor& ex, int trace) {
     const long long lc = trace ? static_cast<long long>(Q) * node_cap * 6 + 64 : 64;
     if (lc > (1LL << 31) - 1) fail(ERR_CAP_LOG, "log too large");
     const int log_cap = static_cast<int>(lc);
-    const int stage_cap = std::max(4096, node_cap * 8);
+    const int stage_cap = std::max(512, node_cap);  // records per thread slot per phase
     const int nwarps = ex.nthreads / 32;
     Run R{};
 #ifndef SPEX_EMU
@@ -833,7 +833,7 @@ void run_executor(spex_executor& ex, int trace) {
 #endif
     set_cfg(ex, R.cfg, node_cap, stream_cap, log_cap, stage_cap, trace, ex.record_sched);
     Arena A;
-    layout(A, R, Q, node_cap, stream_cap, log_cap, nwarps, stage_cap);
+    layout(A, R, Q, node_cap, stream_cap, log_cap, ex.nthreads, stage_cap);
     R.nwarps = nwarps;
     std::vector<double>& tab = log_table();
     R.log_tab_n = static_cast<int>(tab.size());
@@ -1103,7 +1103,7 @@ bool run_batch_device(std::vector<spex_executor*>& exs, int device, cudaStream_t
   int node_cap = 512;
   if (const char* e = std::getenv("SPEX_NODE_CAP")) node_cap = std::max(16, std::atoi(e));
   const int stream_cap = static_cast<int>(static_cast<long long>(Q) * (node_cap - 1) + 64);
-  const int stage_cap = std::max(4096, node_cap * 8);
+  const int stage_cap = std::max(512, node_cap);
   const int nthreads = exs[0]->nthreads, nwarps = nthreads / 32;
   std::vector<double>& tab = log_table();
   double* d_tab = nullptr;
@@ -1116,7 +1116,7 @@ bool run_batch_device(std::vector<spex_executor*>& exs, int device, cudaStream_t
     R = Run{};
     exs[b]->record_sched = 0;
     set_cfg(*exs[b], R.cfg, node_cap, stream_cap, 64, stage_cap, 0, 0);
-    layout(arenas[b], R, Q, node_cap, stream_cap, 64, nwarps, stage_cap);
+    layout(arenas[b], R, Q, node_cap, stream_cap, 64, nthreads, stage_cap);
     R.nwarps = nwarps;
     R.log_tab_n = static_cast<int>(tab.size());
     R.log_tab = d_tab;
@@ -1253,7 +1253,10 @@ int spex_executor_create(const char* config_json, uint64_t run_seed, const char*
       ex->run_seed = run_seed;
       ex->device = device;
       ex->cfg_dump = to_json(ex->hc, ex->t1, ex->t2, ex->t3).dump();
-      if (const char* e = std::getenv("SPEX_CTL_THREADS")) ex->nthreads = std::atoi(e);
+      if (const char* e = std::getenv("SPEX_CTL_THREADS")) {
+        const int t = std::atoi(e);  // same clamp as the launcher: slots must match threads
+        ex->nthreads = (t < 64 || t > 512 || (t & 31)) ? 512 : t;
+      }
     } catch (...) {
       delete ex;
       throw;
