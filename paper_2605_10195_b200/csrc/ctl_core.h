@@ -169,11 +169,19 @@ SPEX_HDNI u32 add_node(const QC& x, u32 parent, int token_len, bool spec) {
   R->n_slot[ni] = slot;
   R->n_tokens[ni] = token_len;
   R->n_status[ni] = spec ? kSpeculative : kExpanding;
-  R->n_flags[ni] = spec ? NF_SPEC_ORIGIN : 0;
+  const u64 h = extend_hash(R->n_hash[pi], slot);
+  // the oracle's two path walks, memoised per node: id's path is golden iff
+  // its parent's is and id's own draw passes (on_golden_path, sim.cpp:139-144);
+  // "deep" is the draw of the depth-1 ancestor (deep_dominant, sim.cpp:118-123)
+  const u16 pf = R->n_flags[pi];
+  const bool golden = (pf & NF_GOLDEN_PATH) != 0 && uniform01(h, kSaltGolden) < x.c->golden_density;
+  const bool deep = R->n_depth[pi] == 0 ? uniform01(h, kSaltDeep) < x.c->skew : (pf & NF_DEEP) != 0;
+  R->n_flags[ni] =
+      static_cast<u16>((spec ? NF_SPEC_ORIGIN : 0) | (golden ? NF_GOLDEN_PATH : 0) | (deep ? NF_DEEP : 0));
   R->n_reward[ni] = 0.0;
   R->n_value[ni] = 0.0;
   R->n_visits[ni] = 0;
-  R->n_hash[ni] = extend_hash(R->n_hash[pi], slot);
+  R->n_hash[ni] = h;
   R->n_first_child[ni] = kNoNode;
   R->n_last_child[ni] = kNoNode;
   R->n_next_sib[ni] = kNoNode;
@@ -252,9 +260,7 @@ SPEX_HDNI bool oracle_is_terminal(const QC& x, u32 id) {
   const Cfg& c = *x.c;
   int depth = R->n_depth[NI(x, id)];
   if (depth == 0) return false;
-  u32 a = id;
-  while (R->n_depth[NI(x, a)] > 1) a = R->n_parent[NI(x, a)];
-  bool deep = uniform01(R->n_hash[NI(x, a)], kSaltDeep) < c.skew;
+  const bool deep = (R->n_flags[NI(x, id)] & NF_DEEP) != 0;  // memoised by add_node
   int lo = deep ? c.deep_min : c.shallow_min;
   int hi = deep ? c.deep_max : c.shallow_max;
   double p = deep ? c.deep_p : c.shallow_p;
@@ -268,13 +274,9 @@ SPEX_HDNI bool oracle_is_terminal(const QC& x, u32 id) {
 SPEX_HDNI double oracle_reward(const QC& x, u32 id) {
   Run* R = x.R;
   const Cfg& c = *x.c;
-  bool golden = true;
-  for (u32 n = id; R->n_depth[NI(x, n)] > 0; n = R->n_parent[NI(x, n)]) {
-    if (uniform01(R->n_hash[NI(x, n)], kSaltGolden) >= c.golden_density) {
-      golden = false;
-      break;
-    }
-  }
+  // the reference walks id's path to the root testing each node's golden draw
+  // (on_golden_path, sim.cpp:139-144); add_node memoised the walk in NF_GOLDEN_PATH
+  const bool golden = (R->n_flags[NI(x, id)] & NF_GOLDEN_PATH) != 0;
   double r = golden ? c.reward_on : c.reward_off;
   if (c.noise_sigma > 0.0) r += c.noise_sigma * normal01(R->n_hash[NI(x, id)], kSaltNoise);
   if (r < 0.0) r = 0.0;
@@ -363,9 +365,9 @@ SPEX_HDNI void backpropagate(const QC& x, u32 leaf, double reward) {
 }
 
 // policy.cpp:65-118. `w` and `quota` are scratch of length n.
-SPEX_HDNI bool rebase_widths(Run* R, int q, const double* rewards, int n, int budget,
-                           double temperature, bool sum_preserving, int* widths, double* w,
-                           double* quota, int* order) {
+SPEX_HDNI bool rebase_widths(Run* R, int q, const double* __restrict__ rewards, int n, int budget,
+                           double temperature, bool sum_preserving, int* __restrict__ widths,
+                           double* __restrict__ w, double* __restrict__ quota, int* __restrict__ order) {
   if (n <= 0) {
     set_err(R, ERR_EMPTY_REWARDS, q, kNoNode);
     return false;

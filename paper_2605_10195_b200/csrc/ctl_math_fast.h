@@ -38,14 +38,16 @@ constexpr double kPio128cw_1 = 0x1.921fb54443000p-6;
 constexpr double kPio128cw_2 = -0x1.73dcb3b399d74p-49;
 constexpr double kPio128cw_3 = -0x1.fc8f8cbb5bf6cp-103;
 
-SPEX_HDNI double exp_fast(double x) {
-  if (!(fabs(x) < 16.0)) return exp_cr(x);
-  if (x == 0.0) return 1.0;
-  const double kd = nearbyint(x * 0x1.71547652b82fep+6);  // x * 64 / ln2, |kd| < 2^11
+// The fast path of exp_fast, branch-free: the candidate RN(e^x) and whether
+// it is proven correctly rounded (otherwise the caller takes exp_cr).
+SPEX_HD double exp_fast_try(double x, bool* ok) {
+  const bool in = fabs(x) < 16.0;  // false for NaN
+  const double xs = in ? x : 0.0;
+  const double kd = nearbyint(xs * 0x1.71547652b82fep+6);  // x * 64 / ln2, |kd| < 2^11
   const int k = static_cast<int>(kd);
   const int j = k & 63;
   const int e = (k - j) / 64;
-  const double rh = x - kd * kLn2o64cw_1;  // exact
+  const double rh = xs - kd * kLn2o64cw_1;  // exact
   const double rl = -kd * kLn2o64cw_2;
   const double r = rh + rl;
   // expm1(r) = rh + rl + t
@@ -55,8 +57,14 @@ SPEX_HDNI double exp_fast(double x) {
   const dd s = two_sum(Th, P.hi);
   const double lo = ((P.lo + Th * (rl + t)) + (Tl + Tl * (rh + rl))) + s.lo;
   const dd y = quick_two_sum(s.hi, lo);
-  if (round_safe(y.hi, y.lo, y.hi * 0x1p-64)) return ldexp(y.hi, e);
-  return exp_cr(x);
+  *ok = x == 0.0 || (in && round_safe(y.hi, y.lo, y.hi * 0x1p-64));
+  return x == 0.0 ? 1.0 : ldexp(y.hi, e);
+}
+
+SPEX_HDNI double exp_fast(double x) {
+  bool ok;
+  const double v = exp_fast_try(x, &ok);
+  return ok ? v : exp_cr(x);
 }
 
 SPEX_HDNI double log_fast(double x) {

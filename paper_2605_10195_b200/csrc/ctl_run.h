@@ -560,7 +560,7 @@ SPEX_HDNI void admit_query(Run* R, int q, Rec* rec_slot) {
   R->n_slot[b] = 0;
   R->n_tokens[b] = c.prompt_tokens;
   R->n_status[b] = kCommitted;
-  R->n_flags[b] = NF_GEN_DONE;
+  R->n_flags[b] = NF_GEN_DONE | NF_GOLDEN_PATH;  // the root's path is empty: golden
   R->n_reward[b] = 0.0;
   R->n_value[b] = 0.0;
   R->n_visits[b] = 0;

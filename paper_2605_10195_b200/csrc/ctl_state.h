@@ -52,6 +52,8 @@ enum : u16 {
   NF_BATCH_PENDING = 1u << 8,     // QueryRun::batch_pending
   NF_COHORT_PENDING = 1u << 9,    // QueryRun::cohort_pending
   NF_HAS_READY = 1u << 10,        // ready_at_promote
+  NF_GOLDEN_PATH = 1u << 11,      // every node on the path to the root passes the golden draw (oracle_reward)
+  NF_DEEP = 1u << 12,             // the depth-1 ancestor's deep draw passed (oracle_is_terminal)
 };
 
 // stream states
