@@ -57,6 +57,7 @@ int spex_k_tree_attn(const RowDesc* rows, const Segment* segs, const float* Qr, 
                      const __nv_bfloat16* Kp, const __nv_bfloat16* Vp, long long slots, __nv_bfloat16* O, int M,
                      cudaStream_t s);
 void spex_k_build_decode_chunks(const RowDesc* rows, const Segment* segs, int M, DecodeChunks w, cudaStream_t s);
+void spex_k1_set_kv_evict_first(int on);
 int spex_k_tree_attn_bulk(const RowDesc* rows, const Segment* segs, const float* Qr, int H, int KVH, int dh,
                           const __nv_bfloat16* Kp, const __nv_bfloat16* Vp, long long slots, __nv_bfloat16* O, int M,
                           int* item_ctr, cudaStream_t s);
@@ -815,6 +816,9 @@ void run_model_schedule(const ModelRunConfig& mc, const ScheduleView& sv, ModelR
   tv_prm.V = mc.prm.V;
   AttnTimer timer;
   if (const char* p = std::getenv("SPEX_ATTN_LOG")) timer.dump = std::fopen(p, "w");
+  // a query-block shard's forward is a fraction of the step, the replicated
+  // control is the floor: stream the KV evict-first to keep L2 for control
+  spex_k1_set_kv_evict_first(sv.shard_hi - sv.shard_lo < Q ? 1 : 0);
   cudaEvent_t t0, t1;
   cudaEventCreate(&t0);
   cudaEventCreate(&t1);

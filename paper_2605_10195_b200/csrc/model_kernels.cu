@@ -339,6 +339,18 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+// The same with an L2 eviction-priority policy (tree KV streamed once per
+// step: evict_first keeps it from displacing reused lines — weights, the
+// control kernel's state and code).
+__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                              uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          (uint32_t)__cvta_generic_to_shared(dst)),
+      "l"(src), "r"(bytes), "r"((uint32_t)__cvta_generic_to_shared(bar)), "l"(policy)
+      : "memory");
+}
+
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t addr = (uint32_t)__cvta_generic_to_shared(bar);
   asm volatile(
@@ -570,7 +582,7 @@ __global__ void __launch_bounds__(kBulkWarps * 32, 1)
     tree_attn_bulk_kernel(const RowDesc* __restrict__ rows, const Segment* __restrict__ segs,
                           const float* __restrict__ Qr, int H, int KVH, int n_items,
                           const __nv_bfloat16* __restrict__ Kp, const __nv_bfloat16* __restrict__ Vp, long long slots,
-                          __nv_bfloat16* __restrict__ O, int* __restrict__ item_ctr) {
+                          __nv_bfloat16* __restrict__ O, int* __restrict__ item_ctr, int kv_evict_first) {
   constexpr int DH = 128, EPL = 8, LPT = 16, STAGE = kBulkCH * DH * 2;  // 4 KB of K (and of V) per stage
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ uint64_t bar[kBulkWarps][kBulkNST];
@@ -583,6 +595,8 @@ __global__ void __launch_bounds__(kBulkWarps * 32, 1)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncwarp();
+  uint64_t kv_pol;  // KV is streamed once per step: evict first
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(kv_pol));
   // ---- producer cursor (lane 0 only): item, segment, offset
   int p_q = 0;                   // items claimed so far (queue position)
   int p_item = -1, p_seg = 0, p_off = 0, p_nseg = 0;
@@ -620,8 +634,13 @@ __global__ void __launch_bounds__(kBulkWarps * 32, 1)
       const int st = issued % kBulkNST;
       unsigned char* kb = ring + st * 2 * STAGE;
       mbar_expect_tx(&bar[warp][st], 2u * n * DH * 2);
-      bulk_g2s(kb, Kp + tok * DH, n * DH * 2, &bar[warp][st]);
-      bulk_g2s(kb + STAGE, Vp + tok * DH, n * DH * 2, &bar[warp][st]);
+      if (kv_evict_first) {
+        bulk_g2s_hint(kb, Kp + tok * DH, n * DH * 2, &bar[warp][st], kv_pol);
+        bulk_g2s_hint(kb + STAGE, Vp + tok * DH, n * DH * 2, &bar[warp][st], kv_pol);
+      } else {
+        bulk_g2s(kb, Kp + tok * DH, n * DH * 2, &bar[warp][st]);
+        bulk_g2s(kb + STAGE, Vp + tok * DH, n * DH * 2, &bar[warp][st]);
+      }
       p_off += n;
       ++issued;
       return;
@@ -2045,8 +2064,12 @@ extern "C" int spex_k_tree_attn(const RowDesc* rows, const Segment* segs, const 
   return -1;
 }
 
+static int g_k1_kv_evict_first = 0;  // L2 policy of K1's bulk KV copies (set per forward)
+extern "C" void spex_k1_set_kv_evict_first(int on) { g_k1_kv_evict_first = on ? 1 : 0; }
+
 // K1 decode rows through the bulk-copy pipeline (G = 1, dh = 128); item_ctr is
 // a zeroed device int per launch.
+
 template <int CH, int NST, int W>
 static int launch_bulk(const RowDesc* rows, const Segment* segs, const float* Qr, int H, int KVH,
                        const __nv_bfloat16* Kp, const __nv_bfloat16* Vp, long long slots, __nv_bfloat16* O, int M,
@@ -2062,9 +2085,15 @@ static int launch_bulk(const RowDesc* rows, const Segment* segs, const float* Qr
   }
   const int n_items = M * KVH;
   const int grid = std::min(blocks, (n_items + W - 1) / W);
+  // L2 policy of the KV chunks: evict-first frees L2 for the control kernel
+  // (-15% control time under load) but costs K1 its cross-row prefix hits
+  // (+2.5% K1 time), so it is on only when the forward is not the bottleneck
+  // (coupled shards); SPEX_K1_EVICT_FIRST=0/1 overrides.
+  static const int env_ef = getenv("SPEX_K1_EVICT_FIRST") ? atoi(getenv("SPEX_K1_EVICT_FIRST")) : -1;
+  const int kv_ef = env_ef >= 0 ? env_ef : g_k1_kv_evict_first;
   cudaMemsetAsync(item_ctr, 0, sizeof(int), s);
   tree_attn_bulk_kernel<CH, NST, W><<<grid, W * 32, smem, s>>>(rows, segs, Qr, H, KVH, n_items, Kp, Vp, slots, O,
-                                                               item_ctr);
+                                                               item_ctr, kv_ef);
   return (int)cudaGetLastError();
 }
 
