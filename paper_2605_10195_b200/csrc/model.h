@@ -107,6 +107,37 @@ struct DecodeChunks {
   int* cnt;         // [rows_cap * KVH] arrival counters (self-resetting)
 };
 
+// Query groups of one decode step (K1 tree-group kernel): the step's rows of
+// one query, at most kGroupRows per group (in row order), and the union of
+// their context segments with a bit mask of the rows that read each one, so a
+// shared ancestor's K/V is staged once for the whole group.
+constexpr int kGroupRows = 16;
+struct GroupDesc {
+  int nrows;
+  int seg_off;  // into GroupSeg[]
+  int nseg;
+  int pad;
+  int row[kGroupRows];
+};
+struct GroupSeg {
+  long long base;  // first KV slot
+  int len;         // tokens
+  uint32_t mask;   // bit i: group row i attends to this segment
+};
+struct TreeGroups {
+  int* q_cnt;          // [q_cap] rows per query
+  int* q_off;          // [q_cap] first sorted position of query q
+  int* q_goff;         // [q_cap] first group of query q
+  int* q_fill;         // [q_cap]
+  int* sorted;         // [rows_cap] row indices grouped by query, ascending within a query
+  GroupDesc* groups;   // [rows_cap]
+  GroupSeg* gsegs;     // [seg_cap]
+  int* n_groups;       // device scalar
+  int* seg_ctr;        // device scalar (zeroed by the builder)
+  int q_cap;
+  long long seg_cap;
+};
+
 // K2 tcgen05 GEMM epilogues (gemm_tc.cu)
 enum TcEpi : int { TC_EPI_STORE = 0, TC_EPI_ROPE_KV = 1, TC_EPI_SWIGLU = 2, TC_EPI_LSE = 3 };
 struct TcEpilogue {

@@ -58,6 +58,10 @@ int spex_k_tree_attn(const RowDesc* rows, const Segment* segs, const float* Qr, 
                      cudaStream_t s);
 void spex_k_build_decode_chunks(const RowDesc* rows, const Segment* segs, int M, DecodeChunks w, cudaStream_t s);
 void spex_k1_set_kv_evict_first(int on);
+void spex_k_build_groups(const RowDesc* rows, const Segment* segs, int M, int Q, TreeGroups g, cudaStream_t s);
+int spex_k_tree_attn_group(const CUtensorMap* kmap16, const CUtensorMap* vmap16, const TreeGroups* g, const float* Qr,
+                           int H, int KVH, int dh, long long slots, __nv_bfloat16* O, int M, int* item_ctr,
+                           cudaStream_t s);
 int spex_k_tree_attn_bulk(const RowDesc* rows, const Segment* segs, const float* Qr, int H, int KVH, int dh,
                           const __nv_bfloat16* Kp, const __nv_bfloat16* Vp, long long slots, __nv_bfloat16* O, int M,
                           int* item_ctr, cudaStream_t s);
@@ -436,7 +440,7 @@ static long long g_launches = 0, g_gemms = 0;
 
 static void forward(Model& m, const RowDesc* rows, const Segment* segs, int M, cublasHandle_t hb,
                     cudaStream_t st, AttnTimer* timer, const TileDesc* tiles = nullptr, int ntiles = 0,
-                    const DecodeChunks* chunks = nullptr) {
+                    const DecodeChunks* chunks = nullptr, const TreeGroups* groups = nullptr) {
   const ModelShape& s = m.sh;
   if (m.use_tc) {
     // embed -> L x [RMSNorm, QKV+RoPE+KV-append (tcgen05), K1, O-proj + residual
@@ -532,6 +536,9 @@ static void forward(Model& m, const RowDesc* rows, const Segment* segs, int M, c
     if (tiles && !m.kmap.empty())
       rc = spex_k_tree_attn_tiles_mma(&m.kmap[l], &m.vmap[l], tiles, ntiles, rows, segs, m.Qr, s.H, s.KVH, s.dh,
                                       m.slots, m.O, st);
+    if (rc != 0 && !tiles && groups && !m.kmap16.empty() && g_item_ctr)
+      rc = spex_k_tree_attn_group(&m.kmap16[l], &m.vmap16[l], groups, m.Qr, s.H, s.KVH, s.dh, m.slots, m.O, M,
+                                  g_item_ctr, st);
     if (rc != 0 && !tiles && !m.kmap16.empty() && wmma_wanted(s) && g_item_ctr)
       rc = spex_k_tree_attn_wmma(&m.kmap16[l], &m.vmap16[l], rows, segs, m.Qr, s.H, s.KVH, s.dh, m.slots, m.O, M,
                                  g_item_ctr, st);
@@ -654,6 +661,9 @@ struct ModelCache {
   Segment* segs2 = nullptr;
   TileDesc* tiles2 = nullptr;
   int* item_ctr = nullptr;  // K1 bulk kernel's work counter (policy stream)
+  // query groups of a decode step (K1 tree-group kernel)
+  TreeGroups tg{};
+  int tg_rows = 0, tg_q = 0;
   // decode work list (K1 chunked), sized for rows_cap rows of the policy shape
   DecodeChunks dc{};
   int dc_rows = 0;
@@ -687,6 +697,43 @@ static void ensure_decode_chunks(int rows_cap, const ModelShape& sh) {
   CK(cudaMemset(w.cnt, 0, ncnt * sizeof(int)));
   g_cache.dc_rows = rows_cap;
   g_cache.dc_part = part;
+}
+
+static void ensure_groups(int rows_cap, int Q) {
+  if (g_cache.tg_rows >= rows_cap && g_cache.tg_q >= Q && g_cache.tg.groups) return;
+  TreeGroups& g = g_cache.tg;
+  cudaFree(g.q_cnt);
+  cudaFree(g.q_off);
+  cudaFree(g.q_goff);
+  cudaFree(g.q_fill);
+  cudaFree(g.sorted);
+  cudaFree(g.groups);
+  cudaFree(g.gsegs);
+  cudaFree(g.n_groups);
+  cudaFree(g.seg_ctr);
+  std::vector<void*> keep;
+  const int qc = std::max(Q, 1);
+  g.q_cnt = dalloc<int>(qc, keep);
+  g.q_off = dalloc<int>(qc, keep);
+  g.q_goff = dalloc<int>(qc, keep);
+  g.q_fill = dalloc<int>(qc, keep);
+  g.sorted = dalloc<int>(rows_cap, keep);
+  g.groups = dalloc<GroupDesc>(rows_cap, keep);
+  g.seg_cap = (long long)rows_cap * 40;  // >= the rows' segments (kMaxSeg each)
+  g.gsegs = dalloc<GroupSeg>((size_t)g.seg_cap, keep);
+  g.n_groups = dalloc<int>(1, keep);
+  g.seg_ctr = dalloc<int>(1, keep);
+  g.q_cap = qc;
+  g_cache.tg_rows = rows_cap;
+  g_cache.tg_q = qc;
+}
+
+// K1 decode rows by query groups (shared segments staged once per group).
+// SPEX_K1_GROUP=0/1 overrides the default.
+static bool group_wanted(const ModelShape& s) {
+  static const int env = getenv("SPEX_K1_GROUP") ? atoi(getenv("SPEX_K1_GROUP")) : -1;
+  const int on = env >= 0 ? env : 0;
+  return on != 0 && s.H == s.KVH && s.dh == 128;
 }
 
 static bool same_shape(const ModelShape& a, const ModelShape& b) {
@@ -807,6 +854,7 @@ void run_model_schedule(const ModelRunConfig& mc, const ScheduleView& sv, ModelR
   // kernel is faster (measured 78% vs 72% of HBM peak, profiles/r01e_*).
   const bool chunked = std::getenv("SPEX_K1_CHUNKED") != nullptr;
   if (chunked) ensure_decode_chunks(std::max(max_dec, 1), mc.policy);
+  if (group_wanted(mc.policy)) ensure_groups(std::max(max_dec, 1), Q);
   TileDesc* tiles = g_cache.tiles;
   float* scores = g_cache.scores;
 
@@ -862,12 +910,17 @@ void run_model_schedule(const ModelRunConfig& mc, const ScheduleView& sv, ModelR
           spex_k_build_decode_rows(tv_pol, sv.srow_sid + pe.off + c0, sv.srow_pos0 + pe.off + c0, n, s, rows, segs,
                                    st);
           g_launches += 1;
+          const bool grouped = group_wanted(mc.policy);
+          if (grouped) {
+            spex_k_build_groups(rows, segs, n, Q, g_cache.tg, st);
+            g_launches += 2;
+          }
           // one K1 launch per layer: the step's unique KV tokens (this chunk's share) + Q/O rows
           timer.cur_bytes = ((double)pe.u0 + (double)s * pe.n + pe.n) * kv_tok_bytes * ((double)n / pe.n) +
                             (double)n * mc.policy.H * mc.policy.dh * (4.0 + 2.0);
           if (chunked) spex_k_build_decode_chunks(rows, segs, n, g_cache.dc, st);
           forward(*pol, rows, segs, n, hb, st, mc.time_attn ? &timer : nullptr, nullptr, 0,
-                  chunked ? &g_cache.dc : nullptr);
+                  chunked ? &g_cache.dc : nullptr, grouped ? &g_cache.tg : nullptr);
           if (dbg && dbg_n + n <= mc.out_rows_cap) {
             spex_k_gather_outputs(rows, n, pol->amax, pol->lse, pol->lsum, dbg + dbg_n, st);
             dbg_n += n;

@@ -1681,6 +1681,321 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1)
   }
 }
 
+// ---------------------------------------------------------------------------
+// K1 tree-group decode (G = 1, dh = 128): the rows of one decode step are
+// grouped by query (at most kGroupRows per group); each group's context is the
+// union of its rows' segments, each segment tagged with the rows that read it.
+// One warp per (group, head) streams every distinct segment ONCE through its
+// TMA ring and runs the group's rows as the M dimension of mma.sync m16n8k16:
+// a shared ancestor (the prompt, a parent thought) is read from L2/HBM and
+// multiplied once per group instead of once per row, and rows that do not
+// read a segment are masked to p = 0. Per-row numerics are those of the
+// per-row kernels up to fp32 summation order.
+
+// Groups of one step: one block; rows grouped by query, ascending row index
+// within a query (deterministic), kGroupRows per group.
+__global__ void __launch_bounds__(1024) build_groups_kernel(const RowDesc* __restrict__ rows, int n, int Q,
+                                                            TreeGroups g) {
+  __shared__ int part_r[1024], part_g[1024];
+  const int tid = threadIdx.x;
+  for (int q = tid; q < Q; q += 1024) {
+    g.q_cnt[q] = 0;
+    g.q_fill[q] = 0;
+  }
+  if (tid == 0) *g.seg_ctr = 0;
+  __syncthreads();
+  for (int r = tid; r < n; r += 1024) atomicAdd(&g.q_cnt[rows[r].q], 1);
+  __syncthreads();
+  const int per = (Q + 1023) / 1024, q0 = tid * per, q1 = min(Q, q0 + per);
+  int sr = 0, sg = 0;
+  for (int q = q0; q < q1; ++q) {
+    const int c = g.q_cnt[q];
+    sr += c;
+    sg += (c + kGroupRows - 1) / kGroupRows;
+  }
+  part_r[tid] = sr;
+  part_g[tid] = sg;
+  __syncthreads();
+  for (int o = 1; o < 1024; o <<= 1) {
+    const int a = tid >= o ? part_r[tid - o] : 0, b = tid >= o ? part_g[tid - o] : 0;
+    __syncthreads();
+    part_r[tid] += a;
+    part_g[tid] += b;
+    __syncthreads();
+  }
+  int rr = part_r[tid] - sr, gg = part_g[tid] - sg;
+  for (int q = q0; q < q1; ++q) {
+    const int c = g.q_cnt[q];
+    g.q_off[q] = rr;
+    g.q_goff[q] = gg;
+    rr += c;
+    gg += (c + kGroupRows - 1) / kGroupRows;
+  }
+  if (tid == 1023) *g.n_groups = part_g[1023];
+  __syncthreads();
+  for (int r = tid; r < n; r += 1024) {
+    const int q = rows[r].q;
+    g.sorted[g.q_off[q] + atomicAdd(&g.q_fill[q], 1)] = r;
+  }
+  __syncthreads();
+  for (int q = tid; q < Q; q += 1024) {
+    const int c = g.q_cnt[q];
+    if (c == 0) continue;
+    int* sl = g.sorted + g.q_off[q];
+    for (int i = 1; i < c; ++i) {  // the atomic fill order is arbitrary: sort
+      const int v = sl[i];
+      int j = i - 1;
+      while (j >= 0 && sl[j] > v) {
+        sl[j + 1] = sl[j];
+        --j;
+      }
+      sl[j + 1] = v;
+    }
+    for (int k = 0; k * kGroupRows < c; ++k) {
+      GroupDesc* gd = g.groups + g.q_goff[q] + k;
+      const int m = min(kGroupRows, c - k * kGroupRows);
+      gd->nrows = m;
+      for (int i = 0; i < m; ++i) gd->row[i] = sl[k * kGroupRows + i];
+    }
+  }
+}
+
+// Union of each group's segments (one thread per group): row 0's segments in
+// path order, then each further row's segments not seen yet; shared ancestors
+// sit at the same index in every row of the group, so they are found in O(1).
+__global__ void build_group_segs_kernel(const RowDesc* __restrict__ rows, const Segment* __restrict__ segs,
+                                        TreeGroups g, int max_groups) {
+  const int gi = blockIdx.x * blockDim.x + threadIdx.x;
+  if (gi >= max_groups || gi >= *g.n_groups) return;
+  GroupDesc* gd = g.groups + gi;
+  const int nr = gd->nrows;
+  int total = 0;
+  for (int i = 0; i < nr; ++i) total += rows[gd->row[i]].nseg;
+  const int off = atomicAdd(g.seg_ctr, total);
+  GroupSeg* out = g.gsegs + off;
+  int cnt = 0;
+  for (int i = 0; i < nr; ++i) {
+    const RowDesc rd = rows[gd->row[i]];
+    for (int k = 0; k < rd.nseg; ++k) {
+      const Segment sgm = segs[rd.seg_off + k];
+      int j;
+      if (k < cnt && out[k].base == sgm.base && out[k].len == sgm.len) {
+        j = k;
+      } else {
+        for (j = 0; j < cnt; ++j)
+          if (out[j].base == sgm.base && out[j].len == sgm.len) break;
+      }
+      if (j < cnt) {
+        out[j].mask |= 1u << i;
+      } else {
+        out[cnt].base = sgm.base;
+        out[cnt].len = sgm.len;
+        out[cnt].mask = 1u << i;
+        ++cnt;
+      }
+    }
+  }
+  gd->seg_off = off;
+  gd->nseg = cnt;
+}
+
+__global__ void __launch_bounds__(kMmaWarps * 32, 1)
+    tree_attn_group_kernel(const __grid_constant__ CUtensorMap kmap16, const __grid_constant__ CUtensorMap vmap16,
+                           const GroupDesc* __restrict__ groups, const GroupSeg* __restrict__ gsegs,
+                           const int* __restrict__ n_groups, const float* __restrict__ Qr, int H, long long slots,
+                           __nv_bfloat16* __restrict__ O, int* __restrict__ item_ctr) {
+  constexpr int DH = 128, CH = 16, STAGE = CH * DH * 2;  // 4 KB of K (and of V) per stage
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t bar[kMmaWarps][kMmaNST];
+  __shared__ int queue[kMmaWarps][8];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_items = *n_groups * H;
+  unsigned char* ring = sm + (size_t)warp * kMmaNST * 2 * STAGE;  // [stage][K|V][STAGE]
+  if (lane == 0) {
+    for (int i = 0; i < kMmaNST; ++i) mbar_init(&bar[warp][i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  // ---- producer cursor (lane 0 only): item, segment, offset
+  int p_q = 0, p_item = -1, p_seg = 0, p_off = 0, p_nseg = 0, issued = 0;
+  long long p_row0 = 0;
+  const GroupSeg* p_sg = nullptr;
+  bool p_done = false;
+  auto produce = [&]() {
+    while (!p_done) {
+      if (p_item < 0 || p_seg >= p_nseg) {
+        const int it = atomicAdd(item_ctr, 1);
+        if (it >= n_items) {
+          queue[warp][p_q & 7] = -1;
+          p_done = true;
+          return;
+        }
+        queue[warp][p_q & 7] = it;
+        ++p_q;
+        p_item = it;
+        const GroupDesc* gd = groups + it / H;
+        p_sg = gsegs + gd->seg_off;
+        p_nseg = gd->nseg;
+        p_seg = 0;
+        p_off = 0;
+        p_row0 = (long long)(it % H) * slots;
+      }
+      const int len = p_sg[p_seg].len;
+      if (p_off >= len) {
+        ++p_seg;
+        p_off = 0;
+        continue;
+      }
+      const int rowc = (int)(p_row0 + p_sg[p_seg].base + p_off);
+      const int st = issued % kMmaNST;
+      unsigned char* kb = ring + st * 2 * STAGE;
+      mbar_expect_tx(&bar[warp][st], 2 * STAGE);
+      tma_load_2d(kb, &kmap16, 0, rowc, &bar[warp][st]);
+      tma_load_2d(kb + 2048, &kmap16, 64, rowc, &bar[warp][st]);
+      tma_load_2d(kb + STAGE, &vmap16, 0, rowc, &bar[warp][st]);
+      tma_load_2d(kb + STAGE + 2048, &vmap16, 64, rowc, &bar[warp][st]);
+      p_off += CH;
+      ++issued;
+      return;
+    }
+  };
+  if (lane == 0)
+    for (int i = 0; i < kMmaNST - 1; ++i) produce();
+  __syncwarp();
+  const int gq = lane >> 2, tq = lane & 3, mi = lane >> 3, ri = lane & 7;
+  int c_q = 0, consumed = 0;
+  for (;;) {
+    const int it = queue[warp][c_q & 7];
+    if (it < 0) break;
+    ++c_q;
+    const int h = it % H;
+    const GroupDesc* gd = groups + it / H;
+    const int nr = gd->nrows;
+    const bool v0 = gq < nr, v1 = gq + 8 < nr;
+    const int r0 = v0 ? gd->row[gq] : 0, r1 = v1 ? gd->row[gq + 8] : 0;
+    const GroupSeg* sg = gsegs + gd->seg_off;
+    const int nseg = gd->nseg;
+    // Q fragments: MMA rows = the group's rows (gq, gq + 8 < nrows), dims as k
+    uint32_t qa[8][4];
+    {
+      const float* q0 = Qr + ((long long)r0 * H + h) * DH;
+      const float* q1 = Qr + ((long long)r1 * H + h) * DH;
+      constexpr float sc = 1.4426950408889634f;
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks) {
+        const int k0 = ks * 16 + tq * 2;
+        const float2 x00 = v0 ? *reinterpret_cast<const float2*>(q0 + k0) : make_float2(0.f, 0.f);
+        const float2 x10 = v1 ? *reinterpret_cast<const float2*>(q1 + k0) : make_float2(0.f, 0.f);
+        const float2 x01 = v0 ? *reinterpret_cast<const float2*>(q0 + k0 + 8) : make_float2(0.f, 0.f);
+        const float2 x11 = v1 ? *reinterpret_cast<const float2*>(q1 + k0 + 8) : make_float2(0.f, 0.f);
+        qa[ks][0] = pack_bf16(x00.x * sc, x00.y * sc);
+        qa[ks][1] = pack_bf16(x10.x * sc, x10.y * sc);
+        qa[ks][2] = pack_bf16(x01.x * sc, x01.y * sc);
+        qa[ks][3] = pack_bf16(x11.x * sc, x11.y * sc);
+      }
+    }
+    float oacc[16][4];
+#pragma unroll
+    for (int n = 0; n < 16; ++n) oacc[n][0] = oacc[n][1] = oacc[n][2] = oacc[n][3] = 0.f;
+    float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+    for (int si = 0; si < nseg; ++si) {
+      const int len = sg[si].len;
+      const uint32_t mask = sg[si].mask;
+      const bool in0 = (mask >> gq) & 1u, in1 = (mask >> (gq + 8)) & 1u;
+      for (int off = 0; off < len; off += CH) {
+        const int n = min(CH, len - off);
+        if (lane == 0) produce();
+        const int st = consumed % kMmaNST;
+        mbar_wait(&bar[warp][st], (uint32_t)((consumed / kMmaNST) & 1));
+        const uint32_t kb = (uint32_t)__cvta_generic_to_shared(ring + st * 2 * STAGE);
+        const uint32_t vb = kb + STAGE;
+        float sacc[2][4];
+#pragma unroll
+        for (int t = 0; t < 2; ++t) sacc[t][0] = sacc[t][1] = sacc[t][2] = sacc[t][3] = 0.f;
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks) {
+          uint32_t b0, b1, b2, b3;
+          ldsm_x4(kb + swz16((mi >> 1) * 8 + ri, ks * 2 + (mi & 1)), b0, b1, b2, b3);
+          mma_bf16(sacc[0], qa[ks][0], qa[ks][1], qa[ks][2], qa[ks][3], b0, b1);
+          mma_bf16(sacc[1], qa[ks][0], qa[ks][1], qa[ks][2], qa[ks][3], b2, b3);
+        }
+        float mx0 = -INFINITY, mx1 = -INFINITY;
+#pragma unroll
+        for (int t = 0; t < 2; ++t)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const bool tok = t * 8 + tq * 2 + e < n;
+            sacc[t][e] = tok && in0 ? sacc[t][e] : -INFINITY;
+            sacc[t][2 + e] = tok && in1 ? sacc[t][2 + e] : -INFINITY;
+            mx0 = fmaxf(mx0, sacc[t][e]);
+            mx1 = fmaxf(mx1, sacc[t][2 + e]);
+          }
+#pragma unroll
+        for (int o = 1; o < 4; o <<= 1) {
+          mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, o));
+          mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, o));
+        }
+        const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
+        const float a0 = mn0 == -INFINITY ? 1.f : exp2f(m0 - mn0);
+        const float a1 = mn1 == -INFINITY ? 1.f : exp2f(m1 - mn1);
+        uint32_t pa[4];
+        float ps0 = 0.f, ps1 = 0.f;
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+          const float p00 = mn0 == -INFINITY ? 0.f : exp2f(sacc[t][0] - mn0);
+          const float p01 = mn0 == -INFINITY ? 0.f : exp2f(sacc[t][1] - mn0);
+          const float p10 = mn1 == -INFINITY ? 0.f : exp2f(sacc[t][2] - mn1);
+          const float p11 = mn1 == -INFINITY ? 0.f : exp2f(sacc[t][3] - mn1);
+          ps0 += p00 + p01;
+          ps1 += p10 + p11;
+          pa[2 * t] = pack_bf16(p00, p01);
+          pa[2 * t + 1] = pack_bf16(p10, p11);
+        }
+        l0 = l0 * a0 + ps0;
+        l1 = l1 * a1 + ps1;
+        m0 = mn0;
+        m1 = mn1;
+#pragma unroll
+        for (int nn = 0; nn < 16; ++nn) {
+          oacc[nn][0] *= a0;
+          oacc[nn][1] *= a0;
+          oacc[nn][2] *= a1;
+          oacc[nn][3] *= a1;
+        }
+#pragma unroll
+        for (int n2 = 0; n2 < 8; ++n2) {
+          uint32_t b0, b1, b2, b3;
+          ldsm_x4_t(vb + swz16((mi & 1) * 8 + ri, n2 * 2 + (mi >> 1)), b0, b1, b2, b3);
+          mma_bf16(oacc[2 * n2], pa[0], pa[1], pa[2], pa[3], b0, b1);
+          mma_bf16(oacc[2 * n2 + 1], pa[0], pa[1], pa[2], pa[3], b2, b3);
+        }
+        ++consumed;
+        __syncwarp();  // stage fully read before lane 0 refills it
+      }
+    }
+#pragma unroll
+    for (int o = 1; o < 4; o <<= 1) {
+      l0 += __shfl_xor_sync(0xffffffffu, l0, o);
+      l1 += __shfl_xor_sync(0xffffffffu, l1, o);
+    }
+    if (v0) {
+      __nv_bfloat16* o0 = O + ((long long)r0 * H + h) * DH + tq * 2;
+      const float inv = 1.f / l0;
+#pragma unroll
+      for (int nn = 0; nn < 16; ++nn)
+        *reinterpret_cast<uint32_t*>(o0 + nn * 8) = pack_bf16(oacc[nn][0] * inv, oacc[nn][1] * inv);
+    }
+    if (v1) {
+      __nv_bfloat16* o1 = O + ((long long)r1 * H + h) * DH + tq * 2;
+      const float inv = 1.f / l1;
+#pragma unroll
+      for (int nn = 0; nn < 16; ++nn)
+        *reinterpret_cast<uint32_t*>(o1 + nn * 8) = pack_bf16(oacc[nn][2] * inv, oacc[nn][3] * inv);
+    }
+  }
+}
+
 // K1 tile variant for prefill-shaped rows (PRM scoring): kTileRows consecutive
 // rows of one thought share their ancestors and a causal own prefix, so each
 // 64-token K/V chunk is staged once per tile instead of once per row.
@@ -2121,6 +2436,37 @@ extern "C" int spex_k_tree_attn_bulk(const RowDesc* rows, const Segment* segs, c
 
 // K1 decode rows on the per-warp TMA + mma.sync pipeline (G <= 16, dh = 128);
 // kmap16/vmap16 are the pools' 2D maps with 64 x 16 boxes (spex_tmap_kv16).
+// Groups of one decode step (shared by its L K1 launches).
+extern "C" void spex_k_build_groups(const RowDesc* rows, const Segment* segs, int M, int Q, TreeGroups g,
+                                    cudaStream_t s) {
+  if (M <= 0) return;
+  build_groups_kernel<<<1, 1024, 0, s>>>(rows, M, Q, g);
+  build_group_segs_kernel<<<(M + 127) / 128, 128, 0, s>>>(rows, segs, g, M);
+}
+
+// K1 decode rows by query groups (G = 1, dh = 128); the groups come from
+// spex_k_build_groups of the same rows. item_ctr is zeroed here per launch.
+extern "C" int spex_k_tree_attn_group(const CUtensorMap* kmap16, const CUtensorMap* vmap16, const TreeGroups* g,
+                                      const float* Qr, int H, int KVH, int dh, long long slots, __nv_bfloat16* O,
+                                      int M, int* item_ctr, cudaStream_t s) {
+  if (M <= 0) return 0;
+  if (dh != 128 || H != KVH) return -1;
+  constexpr int smem = kMmaWarps * kMmaNST * 2 * 16 * 128 * 2 + 1024;
+  static int blocks = 0;
+  if (!blocks) {
+    cudaFuncSetAttribute(tree_attn_group_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    blocks = sms;
+  }
+  const int grid = std::min(blocks, (M * H + kMmaWarps - 1) / kMmaWarps);  // groups <= rows
+  cudaMemsetAsync(item_ctr, 0, sizeof(int), s);
+  tree_attn_group_kernel<<<grid, kMmaWarps * 32, smem, s>>>(*kmap16, *vmap16, g->groups, g->gsegs, g->n_groups, Qr,
+                                                            H, slots, O, item_ctr);
+  return (int)cudaGetLastError();
+}
+
 extern "C" int spex_k_tree_attn_wmma(const CUtensorMap* kmap16, const CUtensorMap* vmap16, const RowDesc* rows,
                                      const Segment* segs, const float* Qr, int H, int KVH, int dh, long long slots,
                                      __nv_bfloat16* O, int M, int* item_ctr, cudaStream_t s) {
