@@ -1490,7 +1490,8 @@ __device__ __forceinline__ uint32_t swz16(int row, int c) {
   return (uint32_t)(half * 2048 + row * 128 + ((cc ^ (row & 7)) << 4));
 }
 
-__global__ void __launch_bounds__(kMmaWarps * 32, 1)
+template <int kNST, int kWarps>  // stages per warp, warps per block
+__global__ void __launch_bounds__(kWarps * 32, 1)
     tree_attn_wmma_kernel(const __grid_constant__ CUtensorMap kmap16, const __grid_constant__ CUtensorMap vmap16,
                           const RowDesc* __restrict__ rows, const Segment* __restrict__ segs,
                           const float* __restrict__ Qr, int H, int KVH, int G, int n_items, long long slots,
@@ -1498,12 +1499,12 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1)
   constexpr int DH = 128, CH = 16, STAGE = CH * DH * 2;  // 4 KB of K (and of V) per stage
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ uint64_t bar[kMmaWarps][kMmaNST];
-  __shared__ int queue[kMmaWarps][8];
+  __shared__ uint64_t bar[kWarps][kNST];
+  __shared__ int queue[kWarps][8];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  unsigned char* ring = sm + (size_t)warp * kMmaNST * 2 * STAGE;  // [stage][K|V][STAGE]
+  unsigned char* ring = sm + (size_t)warp * kNST * 2 * STAGE;  // [stage][K|V][STAGE]
   if (lane == 0) {
-    for (int i = 0; i < kMmaNST; ++i) mbar_init(&bar[warp][i], 1);
+    for (int i = 0; i < kNST; ++i) mbar_init(&bar[warp][i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncwarp();
@@ -1538,7 +1539,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1)
         continue;
       }
       const int rowc = (int)(p_row0 + p_sg[p_seg].base + p_off);
-      const int st = issued % kMmaNST;
+      const int st = issued % kNST;
       unsigned char* kb = ring + st * 2 * STAGE;
       mbar_expect_tx(&bar[warp][st], 2 * STAGE);
       tma_load_2d(kb, &kmap16, 0, rowc, &bar[warp][st]);
@@ -1551,7 +1552,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1)
     }
   };
   if (lane == 0)
-    for (int i = 0; i < kMmaNST - 1; ++i) produce();
+    for (int i = 0; i < kNST - 1; ++i) produce();
   __syncwarp();
   const int gq = lane >> 2, tq = lane & 3, mi = lane >> 3, ri = lane & 7;
   int c_q = 0, consumed = 0;
@@ -1591,8 +1592,8 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1)
       for (int off = 0; off < len; off += CH) {
         const int n = min(CH, len - off);
         if (lane == 0) produce();
-        const int st = consumed % kMmaNST;
-        mbar_wait(&bar[warp][st], (uint32_t)((consumed / kMmaNST) & 1));
+        const int st = consumed % kNST;
+        mbar_wait(&bar[warp][st], (uint32_t)((consumed / kNST) & 1));
         const uint32_t kb = (uint32_t)__cvta_generic_to_shared(ring + st * 2 * STAGE);
         const uint32_t vb = kb + STAGE;
         float sacc[2][4];
@@ -2467,27 +2468,43 @@ extern "C" int spex_k_tree_attn_group(const CUtensorMap* kmap16, const CUtensorM
   return (int)cudaGetLastError();
 }
 
-extern "C" int spex_k_tree_attn_wmma(const CUtensorMap* kmap16, const CUtensorMap* vmap16, const RowDesc* rows,
-                                     const Segment* segs, const float* Qr, int H, int KVH, int dh, long long slots,
-                                     __nv_bfloat16* O, int M, int* item_ctr, cudaStream_t s) {
-  const int G = H / KVH;
-  if (M <= 0) return 0;
-  if (dh != 128 || G < 1 || G > 16) return -1;
-  const size_t smem = (size_t)kMmaWarps * kMmaNST * 2 * 16 * 128 * 2 + 1024;
+template <int NST, int W>
+static int launch_wmma(const CUtensorMap* kmap16, const CUtensorMap* vmap16, const RowDesc* rows, const Segment* segs,
+                       const float* Qr, int H, int KVH, int G, long long slots, __nv_bfloat16* O, int M,
+                       int* item_ctr, cudaStream_t s) {
+  const size_t smem = (size_t)W * NST * 2 * 16 * 128 * 2 + 1024;
   static int blocks = 0;
   if (!blocks) {
-    cudaFuncSetAttribute(tree_attn_wmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(tree_attn_wmma_kernel<NST, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     blocks = sms;
   }
   const int n_items = M * KVH;
-  const int grid = std::min(blocks, (n_items + kMmaWarps - 1) / kMmaWarps);
+  const int grid = std::min(blocks, (n_items + W - 1) / W);
   cudaMemsetAsync(item_ctr, 0, sizeof(int), s);
-  tree_attn_wmma_kernel<<<grid, kMmaWarps * 32, smem, s>>>(*kmap16, *vmap16, rows, segs, Qr, H, KVH, G, n_items, slots,
-                                                           O, item_ctr);
+  tree_attn_wmma_kernel<NST, W><<<grid, W * 32, smem, s>>>(*kmap16, *vmap16, rows, segs, Qr, H, KVH, G, n_items,
+                                                           slots, O, item_ctr);
   return (int)cudaGetLastError();
+}
+
+extern "C" int spex_k_tree_attn_wmma(const CUtensorMap* kmap16, const CUtensorMap* vmap16, const RowDesc* rows,
+                                     const Segment* segs, const float* Qr, int H, int KVH, int dh, long long slots,
+                                     __nv_bfloat16* O, int M, int* item_ctr, cudaStream_t s) {
+  const int G = H / KVH;
+  if (M <= 0) return 0;
+  if (dh != 128 || G < 1 || G > 16) return -1;
+  // stages x warps (8 KB per stage): bytes in flight per SM vs warps to hide the math
+  static const int cfg = getenv("SPEX_K1_WMMA_CFG") ? atoi(getenv("SPEX_K1_WMMA_CFG")) : 0;
+  switch (cfg) {
+    case 1: return launch_wmma<3, 8>(kmap16, vmap16, rows, segs, Qr, H, KVH, G, slots, O, M, item_ctr, s);
+    case 2: return launch_wmma<4, 6>(kmap16, vmap16, rows, segs, Qr, H, KVH, G, slots, O, M, item_ctr, s);
+    case 3: return launch_wmma<3, 9>(kmap16, vmap16, rows, segs, Qr, H, KVH, G, slots, O, M, item_ctr, s);
+    case 4: return launch_wmma<2, 13>(kmap16, vmap16, rows, segs, Qr, H, KVH, G, slots, O, M, item_ctr, s);
+    default: return launch_wmma<kMmaNST, kMmaWarps>(kmap16, vmap16, rows, segs, Qr, H, KVH, G, slots, O, M, item_ctr,
+                                                    s);
+  }
 }
 
 extern "C" void spex_k_build_decode_chunks(const RowDesc* rows, const Segment* segs, int M, DecodeChunks w,
