@@ -22,6 +22,7 @@
 #include <mutex>
 #include <sstream>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include <json.hpp>
@@ -488,6 +489,64 @@ extern "C" void spex_model_cache_release_mismatch(const ModelRunConfig* mc);
 
 namespace {
 
+#ifndef SPEX_EMU
+// The default stream-ordered pool returns freed memory to the driver at every
+// synchronisation (release threshold 0): each search would unmap and remap its
+// arena (measured: 0.1-1 s of host time per search). Keep it cached instead.
+void keep_pool_memory(int device) {
+  static std::mutex mu;
+  static unsigned long long done = 0;
+  std::lock_guard<std::mutex> lk(mu);
+  if (device < 0 || device >= 64 || (done >> device) & 1ULL) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  cudaGetLastError();
+  done |= 1ULL << device;
+}
+
+// Pinned, device-mapped host buffers for the streamed schedule, recycled
+// across searches (cudaHostAlloc / cudaFreeHost cost milliseconds and may
+// synchronise the device).
+struct PinnedCache {
+  std::mutex mu;
+  std::vector<std::pair<void*, size_t>> free_list;
+};
+PinnedCache& pinned_cache() {
+  static PinnedCache c;
+  return c;
+}
+std::unordered_map<void*, size_t>& pinned_sizes() {
+  static std::unordered_map<void*, size_t> m;
+  return m;
+}
+void* pinned_acquire(size_t bytes) {
+  PinnedCache& c = pinned_cache();
+  {
+    std::lock_guard<std::mutex> lk(c.mu);
+    for (size_t i = 0; i < c.free_list.size(); ++i)
+      if (c.free_list[i].second >= bytes) {
+        void* p = c.free_list[i].first;
+        c.free_list.erase(c.free_list.begin() + static_cast<long>(i));
+        return p;
+      }
+  }
+  void* p = nullptr;
+  if (cudaHostAlloc(&p, bytes, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess)
+    fail(200, "cudaHostAlloc failed");
+  std::lock_guard<std::mutex> lk(c.mu);
+  pinned_sizes()[p] = bytes;
+  return p;
+}
+void pinned_release(void* p) {
+  PinnedCache& c = pinned_cache();
+  std::lock_guard<std::mutex> lk(c.mu);
+  c.free_list.push_back({p, pinned_sizes()[p]});
+}
+#endif
+
 void set_cfg(const spex_executor& ex, Cfg& c, int node_cap, int stream_cap, int log_cap,
              int stage_cap, int trace, int record_sched) {
   const HostConfig& h = ex.hc;
@@ -868,6 +927,7 @@ void run_executor(spex_executor& ex, int trace) {
     CUDA_OK(cudaSetDevice(ex.device));
     if (!ex.stream) CUDA_OK(cudaStreamCreateWithFlags(&ex.stream, cudaStreamNonBlocking));
     if (!ex.mstream) CUDA_OK(cudaStreamCreateWithFlags(&ex.mstream, cudaStreamNonBlocking));
+    keep_pool_memory(ex.device);
     char* base = nullptr;
     // stream-ordered allocations: concurrent searches (one control CTA each)
     // never synchronise the device through cudaMalloc/cudaFree
@@ -912,8 +972,8 @@ void run_executor(spex_executor& ex, int trace) {
     PubHead* h_head = nullptr;
     PubEntry* h_ents = nullptr;
     if (streaming) {
-      CUDA_OK(cudaHostAlloc(&h_head, sizeof(PubHead), cudaHostAllocMapped));
-      CUDA_OK(cudaHostAlloc(&h_ents, sizeof(PubEntry) * R.cfg.sched_cap, cudaHostAllocMapped));
+      h_head = static_cast<PubHead*>(pinned_acquire(sizeof(PubHead)));
+      h_ents = static_cast<PubEntry*>(pinned_acquire(sizeof(PubEntry) * R.cfg.sched_cap));
       std::memset(h_head, 0, sizeof(PubHead));
       CUDA_OK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&R.pub), h_head, 0));
       CUDA_OK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&R.pub_e), h_ents, 0));
@@ -927,8 +987,8 @@ void run_executor(spex_executor& ex, int trace) {
       cudaFreeAsync(d_tab, ex.stream);
       cudaFreeAsync(d_run, ex.stream);
       cudaStreamSynchronize(ex.stream);
-      if (h_head) cudaFreeHost(h_head);
-      if (h_ents) cudaFreeHost(h_ents);
+      if (h_head) pinned_release(h_head);
+      if (h_ents) pinned_release(h_ents);
     };
     ScheduleView sv{};
     if (ex.with_model) {
