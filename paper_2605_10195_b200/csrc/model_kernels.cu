@@ -1490,7 +1490,7 @@ __device__ __forceinline__ uint32_t swz16(int row, int c) {
   return (uint32_t)(half * 2048 + row * 128 + ((cc ^ (row & 7)) << 4));
 }
 
-template <int kNST, int kWarps>  // stages per warp, warps per block
+template <int kNST, int kWarps, bool kSkipRescale>  // stages per warp, warps per block
 __global__ void __launch_bounds__(kWarps * 32, 1)
     tree_attn_wmma_kernel(const __grid_constant__ CUtensorMap kmap16, const __grid_constant__ CUtensorMap vmap16,
                           const RowDesc* __restrict__ rows, const Segment* __restrict__ segs,
@@ -1640,15 +1640,18 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
         }
         l0 = l0 * a0 + ps0;
         l1 = l1 * a1 + ps1;
+        // a == 1 exactly when a row's running max did not move: the rescale can be skipped
+        if (!kSkipRescale || !__all_sync(0xffffffffu, mn0 == m0 && mn1 == m1)) {
+#pragma unroll
+          for (int nn = 0; nn < 16; ++nn) {
+            oacc[nn][0] *= a0;
+            oacc[nn][1] *= a0;
+            oacc[nn][2] *= a1;
+            oacc[nn][3] *= a1;
+          }
+        }
         m0 = mn0;
         m1 = mn1;
-#pragma unroll
-        for (int nn = 0; nn < 16; ++nn) {
-          oacc[nn][0] *= a0;
-          oacc[nn][1] *= a0;
-          oacc[nn][2] *= a1;
-          oacc[nn][3] *= a1;
-        }
 #pragma unroll
         for (int n2 = 0; n2 < 8; ++n2) {
           uint32_t b0, b1, b2, b3;
@@ -2468,14 +2471,14 @@ extern "C" int spex_k_tree_attn_group(const CUtensorMap* kmap16, const CUtensorM
   return (int)cudaGetLastError();
 }
 
-template <int NST, int W>
+template <int NST, int W, bool SKIP = false>
 static int launch_wmma(const CUtensorMap* kmap16, const CUtensorMap* vmap16, const RowDesc* rows, const Segment* segs,
                        const float* Qr, int H, int KVH, int G, long long slots, __nv_bfloat16* O, int M,
                        int* item_ctr, cudaStream_t s) {
   const size_t smem = (size_t)W * NST * 2 * 16 * 128 * 2 + 1024;
   static int blocks = 0;
   if (!blocks) {
-    cudaFuncSetAttribute(tree_attn_wmma_kernel<NST, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(tree_attn_wmma_kernel<NST, W, SKIP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -2484,7 +2487,7 @@ static int launch_wmma(const CUtensorMap* kmap16, const CUtensorMap* vmap16, con
   const int n_items = M * KVH;
   const int grid = std::min(blocks, (n_items + W - 1) / W);
   cudaMemsetAsync(item_ctr, 0, sizeof(int), s);
-  tree_attn_wmma_kernel<NST, W><<<grid, W * 32, smem, s>>>(*kmap16, *vmap16, rows, segs, Qr, H, KVH, G, n_items,
+  tree_attn_wmma_kernel<NST, W, SKIP><<<grid, W * 32, smem, s>>>(*kmap16, *vmap16, rows, segs, Qr, H, KVH, G, n_items,
                                                            slots, O, item_ctr);
   return (int)cudaGetLastError();
 }
@@ -2502,6 +2505,8 @@ extern "C" int spex_k_tree_attn_wmma(const CUtensorMap* kmap16, const CUtensorMa
     case 2: return launch_wmma<4, 6>(kmap16, vmap16, rows, segs, Qr, H, KVH, G, slots, O, M, item_ctr, s);
     case 3: return launch_wmma<3, 9>(kmap16, vmap16, rows, segs, Qr, H, KVH, G, slots, O, M, item_ctr, s);
     case 4: return launch_wmma<2, 13>(kmap16, vmap16, rows, segs, Qr, H, KVH, G, slots, O, M, item_ctr, s);
+    case 5: return launch_wmma<kMmaNST, kMmaWarps, true>(kmap16, vmap16, rows, segs, Qr, H, KVH, G, slots, O, M,
+                                                         item_ctr, s);
     default: return launch_wmma<kMmaNST, kMmaWarps>(kmap16, vmap16, rows, segs, Qr, H, KVH, G, slots, O, M, item_ctr,
                                                     s);
   }
