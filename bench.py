@@ -206,7 +206,9 @@ def run_reference(args, cfg_text, seed, rank, world):
                        "searches_per_step": per_step},
             "cpu_baseline": {"value": v, "unit": "queries/s", "cores": ncores, "kind": "reference",
                              "sample": f"{per_step} concurrent Executor::run per step on {ncores} host threads"},
-            "e2e": {"value": v, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "e2e": {"value": v, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "work_note": "the reference prices decode with a virtual clock and runs no model: this arm does the "
+                         "search control only; the GPU arm's `control_only` object measures the same work"}
     print(json.dumps(line), flush=True)
 
 
@@ -413,6 +415,9 @@ def main():
                             "spex_decode_steps": ms["decode_steps"], "spex_decode_rows": ms["decode_rows"],
                             "note": "one GPU, same config/seed/model, flags '' vs the config's flags; "
                                     "device step time of one warm search each"},
+        "work_note": "value/e2e include the real policy decode and PRM scoring of every scheduled row, which the "
+                     "reference only prices (virtual clock, no model); `control_only` is the like-for-like "
+                     "comparison with the reference arm",
         "thoughts_per_s": agg["prm_thoughts"] / dev_s,
         "named_model_shapes": named,
         "control_only": ctl_only,
