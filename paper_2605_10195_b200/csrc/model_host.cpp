@@ -227,6 +227,7 @@ struct Model {
   float* lse_part = nullptr;           // [max_rows][V/128] float4
   bool lm_tc = false;                  // LM head on the tcgen05 GEMM with the LSE epilogue (cuBLAS path)
   bool tc_qkv = false, tc_gu = false;  // per-op tcgen05 (cuBLAS path, large row counts)
+  bool tc_o = false;                   // O-projection + residual on tcgen05 (cuBLAS path)
   int* amax = nullptr;
   float* lse = nullptr;
   float* lsum = nullptr;
@@ -376,6 +377,20 @@ static Model* make_model(const ModelShape& sh, bool prm, uint64_t seed, long lon
         m->tq[l].N = qkv_n;
         m->tq[l].K = sh.d;
         if (spex_tmap_operand(&m->tq[l].map, m->wqkv[l], qkv_n, sh.d) != 0) m->tc_qkv = false;
+      }
+    }
+    // O-projection + residual (N = d) on tcgen05 (SPEX_TC_O=1): faster in
+    // isolation (M 2157 x N 1024 x K 1024: 12.4 us vs 17.1 us,
+    // profiles/r01v_gemm_tc_vs_cublas.txt) but 3% slower in the running search
+    // (profiles/r01z_tc_o_ab.txt), so cuBLAS stays the default.
+    if (getenv("SPEX_TC_O") && atoi(getenv("SPEX_TC_O")) != 0 && sh.d % 128 == 0 && (sh.H * sh.dh) % 64 == 0 &&
+        spex_tmap_operand(&m->a_o, m->O, (long long)M, sh.H * sh.dh) == 0) {
+      m->to.resize(sh.L);
+      m->tc_o = true;
+      for (int l = 0; l < sh.L; ++l) {
+        m->to[l].N = sh.d;
+        m->to[l].K = sh.H * sh.dh;
+        if (spex_tmap_operand(&m->to[l].map, m->wo[l], sh.d, sh.H * sh.dh) != 0) m->tc_o = false;
       }
     }
     if (getenv("SPEX_TC_GU") && (2 * sh.F) % 128 == 0 && sh.F % 64 == 0) {
@@ -557,7 +572,16 @@ static void forward(Model& m, const RowDesc* rows, const Segment* segs, int M, c
                          : spex_k_tree_attn(rows, segs, m.Qr, s.H, s.KVH, s.dh, m.Kp[l], m.Vp[l], m.slots, m.O, M, st);
     if (rc != 0) throw std::runtime_error("tree attention: unsupported head shape");
     if (timer) timer->end(st);
-    gemm(hb, m.O, m.wo[l], m.X, M, s.d, s.H * s.dh, true);
+    if (m.tc_o && M >= 512) {
+      TcEpilogue er{};
+      er.kind = TC_EPI_STORE;
+      er.y = m.X;
+      er.ldy = s.d;
+      er.accumulate = 1;
+      tc_gemm(m.a_o, m.to[l], M, er, st);
+    } else {
+      gemm(hb, m.O, m.wo[l], m.X, M, s.d, s.H * s.dh, true);
+    }
     spex_k_rmsnorm(m.X, M, s.d, s.eps, m.Xn, st);
     if (m.tc_gu && M >= kTcMinRows) {
       TcEpilogue eg{};
