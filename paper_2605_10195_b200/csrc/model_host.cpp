@@ -843,6 +843,7 @@ void run_model_schedule(const ModelRunConfig& mc, const ScheduleView& sv, ModelR
   if (!g_cache.item_ctr) {
     std::vector<void*> keep;
     g_cache.item_ctr = dalloc<int>(64, keep);
+    CK(cudaMemset(g_cache.item_ctr, 0, 64 * sizeof(int)));  // the bulk K1 kernel keeps [0..1] self-resetting
     g_item_ctr = g_cache.item_ctr;
   }
   if (g_cache.rows_cap < rows_cap) {

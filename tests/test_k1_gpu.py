@@ -178,9 +178,15 @@ def test_k1_decode_matches_torch_fp32(H, KVH, dh, M, impl):
         fb.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                        ctypes.c_void_p, ctypes.c_void_p, ctypes.c_longlong, ctypes.c_void_p, ctypes.c_int,
                        ctypes.c_void_p, ctypes.c_void_p]
-        ctr = torch.zeros(1, dtype=torch.int32, device=dev)
+        ctr = torch.zeros(2, dtype=torch.int32, device=dev)  # [claims, finished warps], self-resetting
         rc = fb(rows_d.data_ptr(), segs_d.data_ptr(), Q.data_ptr(), H, KVH, dh, K.data_ptr(), V.data_ptr(), slots,
                 O.data_ptr(), M, ctr.data_ptr(), st.cuda_stream)
+        assert rc == 0
+        torch.cuda.synchronize()
+        assert ctr.tolist() == [0, 0]  # re-zeroed by the last warp
+        O.zero_()
+        rc = fb(rows_d.data_ptr(), segs_d.data_ptr(), Q.data_ptr(), H, KVH, dh, K.data_ptr(), V.data_ptr(), slots,
+                O.data_ptr(), M, ctr.data_ptr(), st.cuda_stream)  # second launch on the reset counter
         assert rc == 0
     elif impl == "mma":
         if dh != 128:
