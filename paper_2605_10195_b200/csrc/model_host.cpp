@@ -58,6 +58,8 @@ int spex_k_tree_attn(const RowDesc* rows, const Segment* segs, const float* Qr, 
                      cudaStream_t s);
 void spex_k_build_decode_chunks(const RowDesc* rows, const Segment* segs, int M, DecodeChunks w, cudaStream_t s);
 void spex_k1_set_kv_evict_first(int on);
+void spex_k1_set_row_order(const int* order);
+void spex_k_order_rows(const RowDesc* rows, int M, int Q, int* order, cudaStream_t s);
 void spex_k_build_groups(const RowDesc* rows, const Segment* segs, int M, int Q, TreeGroups g, cudaStream_t s);
 int spex_k_tree_attn_group(const CUtensorMap* kmap16, const CUtensorMap* vmap16, const TreeGroups* g, const float* Qr,
                            int H, int KVH, int dh, long long slots, __nv_bfloat16* O, int M, int* item_ctr,
@@ -685,6 +687,8 @@ struct ModelCache {
   Segment* segs2 = nullptr;
   TileDesc* tiles2 = nullptr;
   int* item_ctr = nullptr;  // K1 bulk kernel's work counter (policy stream)
+  int* row_order = nullptr;  // decode rows grouped by query (K1 bulk claim order)
+  int row_order_cap = 0;
   // query groups of a decode step (K1 tree-group kernel)
   TreeGroups tg{};
   int tg_rows = 0, tg_q = 0;
@@ -758,6 +762,12 @@ static bool group_wanted(const ModelShape& s) {
   static const int env = getenv("SPEX_K1_GROUP") ? atoi(getenv("SPEX_K1_GROUP")) : -1;
   const int on = env >= 0 ? env : 0;
   return on != 0 && s.H == s.KVH && s.dh == 128;
+}
+
+// K1 bulk claim order grouped by query (SPEX_K1_QORDER=0: active order).
+static bool qorder_wanted() {
+  static const bool on = !getenv("SPEX_K1_QORDER") || atoi(getenv("SPEX_K1_QORDER")) != 0;
+  return on;
 }
 
 static bool same_shape(const ModelShape& a, const ModelShape& b) {
@@ -880,6 +890,12 @@ void run_model_schedule(const ModelRunConfig& mc, const ScheduleView& sv, ModelR
   const bool chunked = std::getenv("SPEX_K1_CHUNKED") != nullptr;
   if (chunked) ensure_decode_chunks(std::max(max_dec, 1), mc.policy);
   if (group_wanted(mc.policy)) ensure_groups(std::max(max_dec, 1), Q);
+  if (g_cache.row_order_cap < max_dec) {
+    cudaFree(g_cache.row_order);
+    std::vector<void*> keep;
+    g_cache.row_order = dalloc<int>(std::max(max_dec, 1), keep);
+    g_cache.row_order_cap = max_dec;
+  }
   TileDesc* tiles = g_cache.tiles;
   float* scores = g_cache.scores;
 
@@ -936,6 +952,11 @@ void run_model_schedule(const ModelRunConfig& mc, const ScheduleView& sv, ModelR
                                    st);
           g_launches += 1;
           const bool grouped = group_wanted(mc.policy);
+          if (qorder_wanted()) {
+            spex_k_order_rows(rows, n, Q, g_cache.row_order, st);
+            spex_k1_set_row_order(g_cache.row_order);
+            g_launches += 1;
+          }
           if (grouped) {
             spex_k_build_groups(rows, segs, n, Q, g_cache.tg, st);
             g_launches += 2;
@@ -946,6 +967,7 @@ void run_model_schedule(const ModelRunConfig& mc, const ScheduleView& sv, ModelR
           if (chunked) spex_k_build_decode_chunks(rows, segs, n, g_cache.dc, st);
           forward(*pol, rows, segs, n, hb, st, mc.time_attn ? &timer : nullptr, nullptr, 0,
                   chunked ? &g_cache.dc : nullptr, grouped ? &g_cache.tg : nullptr);
+          spex_k1_set_row_order(nullptr);  // read at launch: other callers get row order
           if (dbg && dbg_n + n <= mc.out_rows_cap) {
             spex_k_gather_outputs(rows, n, pol->amax, pol->lse, pol->lsum, dbg + dbg_n, st);
             dbg_n += n;

@@ -589,7 +589,8 @@ __global__ void __launch_bounds__(kBulkWarps * 32, 1)
     tree_attn_bulk_kernel(const RowDesc* __restrict__ rows, const Segment* __restrict__ segs,
                           const float* __restrict__ Qr, int H, int KVH, int n_items,
                           const __nv_bfloat16* __restrict__ Kp, const __nv_bfloat16* __restrict__ Vp, long long slots,
-                          __nv_bfloat16* __restrict__ O, int* __restrict__ item_ctr, int kv_evict_first) {
+                          __nv_bfloat16* __restrict__ O, int* __restrict__ item_ctr, int kv_evict_first,
+                          const int* __restrict__ row_order) {
   constexpr int DH = 128, EPL = 8, LPT = 16, STAGE = kBulkCH * DH * 2;  // 4 KB of K (and of V) per stage
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ uint64_t bar[kBulkWarps][kBulkNST];
@@ -630,7 +631,7 @@ __global__ void __launch_bounds__(kBulkWarps * 32, 1)
         queue[warp][p_q & 7] = it;
         ++p_q;
         p_item = it;
-        const RowDesc rd = rows[it / KVH];
+        const RowDesc rd = rows[row_order ? row_order[it / KVH] : it / KVH];
         p_sg = segs + rd.seg_off;
         p_nseg = rd.nseg;
         p_seg = 0;
@@ -669,7 +670,7 @@ __global__ void __launch_bounds__(kBulkWarps * 32, 1)
     const int it = queue[warp][c_q & 7];
     if (it < 0) break;
     ++c_q;
-    const int r = it / KVH, kh = it % KVH;
+    const int r = row_order ? row_order[it / KVH] : it / KVH, kh = it % KVH;
     const RowDesc rd = rows[r];
     const Segment* sg = segs + rd.seg_off;
     uint32_t q2[EPL / 2];
@@ -2427,6 +2428,40 @@ extern "C" int spex_k_tree_attn(const RowDesc* rows, const Segment* segs, const 
 }
 
 static int g_k1_kv_evict_first = 0;  // L2 policy of K1's bulk KV copies (set per forward)
+static const int* g_k1_row_order = nullptr;  // claim order of the decode rows (set per step), or null
+extern "C" void spex_k1_set_row_order(const int* order) { g_k1_row_order = order; }
+
+// Rows of a decode step grouped by query (counting sort, one block; order
+// within a query arbitrary): the bulk K1's warps then work on one tree's rows
+// at the same time, so their shared prefixes are read from L2 while resident.
+__global__ void __launch_bounds__(1024) order_rows_kernel(const RowDesc* __restrict__ rows, int M, int Q,
+                                                           int* __restrict__ order) {
+  constexpr int NB = 1024;
+  __shared__ int hist[NB], part[NB];
+  const int tid = threadIdx.x;
+  hist[tid] = 0;
+  __syncthreads();
+  auto bucket = [&](int q) { return (int)(((long long)q * NB) / (Q > 0 ? Q : 1)); };
+  for (int r = tid; r < M; r += 1024) atomicAdd(&hist[min(bucket(rows[r].q), NB - 1)], 1);
+  __syncthreads();
+  const int v = hist[tid];
+  part[tid] = v;
+  __syncthreads();
+  for (int o = 1; o < NB; o <<= 1) {
+    const int a = tid >= o ? part[tid - o] : 0;
+    __syncthreads();
+    part[tid] += a;
+    __syncthreads();
+  }
+  hist[tid] = part[tid] - v;
+  __syncthreads();
+  for (int r = tid; r < M; r += 1024) order[atomicAdd(&hist[min(bucket(rows[r].q), NB - 1)], 1)] = r;
+}
+
+extern "C" void spex_k_order_rows(const RowDesc* rows, int M, int Q, int* order, cudaStream_t s) {
+  if (M <= 0) return;
+  order_rows_kernel<<<1, 1024, 0, s>>>(rows, M, Q, order);
+}
 extern "C" void spex_k1_set_kv_evict_first(int on) { g_k1_kv_evict_first = on ? 1 : 0; }
 
 // K1 decode rows through the bulk-copy pipeline (G = 1, dh = 128); item_ctr is
@@ -2455,7 +2490,7 @@ static int launch_bulk(const RowDesc* rows, const Segment* segs, const float* Qr
   const int kv_ef = env_ef >= 0 ? env_ef : g_k1_kv_evict_first;
   // item_ctr[0..1] are zero on entry and re-zeroed by the kernel's last warp
   launch_maybe_pdl(tree_attn_bulk_kernel<CH, NST, W>, dim3(grid), dim3(W * 32), smem, s, rows, segs, Qr, H, KVH,
-                   n_items, Kp, Vp, slots, O, item_ctr, kv_ef);
+                   n_items, Kp, Vp, slots, O, item_ctr, kv_ef, g_k1_row_order);
   return (int)cudaGetLastError();
 }
 
