@@ -1510,7 +1510,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
     tree_attn_wmma_kernel(const __grid_constant__ CUtensorMap kmap16, const __grid_constant__ CUtensorMap vmap16,
                           const RowDesc* __restrict__ rows, const Segment* __restrict__ segs,
                           const float* __restrict__ Qr, int H, int KVH, int G, int n_items, long long slots,
-                          __nv_bfloat16* __restrict__ O, int* __restrict__ item_ctr) {
+                          __nv_bfloat16* __restrict__ O, int* __restrict__ item_ctr,
+                          const int* __restrict__ row_order) {
   constexpr int DH = 128, CH = 16, STAGE = CH * DH * 2;  // 4 KB of K (and of V) per stage
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -1540,7 +1541,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
         queue[warp][p_q & 7] = it;
         ++p_q;
         p_item = it;
-        const RowDesc rd = rows[it / KVH];
+        const RowDesc rd = rows[row_order ? row_order[it / KVH] : it / KVH];
         p_sg = segs + rd.seg_off;
         p_nseg = rd.nseg;
         p_seg = 0;
@@ -1575,7 +1576,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
     const int it = queue[warp][c_q & 7];
     if (it < 0) break;
     ++c_q;
-    const int r = it / KVH, kh = it % KVH;
+    const int r = row_order ? row_order[it / KVH] : it / KVH, kh = it % KVH;
     const RowDesc rd = rows[r];
     const Segment* sg = segs + rd.seg_off;
     // Q fragments: rows = the group's heads (gq, gq + 8 < G), dims as k
@@ -2566,7 +2567,7 @@ static int launch_wmma(const CUtensorMap* kmap16, const CUtensorMap* vmap16, con
   const int grid = std::min(blocks, (n_items + W - 1) / W);
   cudaMemsetAsync(item_ctr, 0, sizeof(int), s);
   tree_attn_wmma_kernel<NST, W, SKIP><<<grid, W * 32, smem, s>>>(*kmap16, *vmap16, rows, segs, Qr, H, KVH, G, n_items,
-                                                           slots, O, item_ctr);
+                                                                 slots, O, item_ctr, g_k1_row_order);
   return (int)cudaGetLastError();
 }
 
