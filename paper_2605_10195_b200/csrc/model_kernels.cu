@@ -285,8 +285,9 @@ __global__ void rope_kv_kernel(const RowDesc* rows, int M, const __nv_bfloat16* 
                                __nv_bfloat16* Vp, float* Qr) {
   pdl_wait();
   // one block (128 threads) per row; (cos, sin) from the per-forward table
-  // (rope_table_kernel), rotate-half RoPE on (x[i], x[i+half]) pairs two at a
-  // time from the bf16 projection output; V copied 8 bytes at a time
+  // (rope_table_kernel), rotate-half RoPE on (x[i], x[i+half]) eight pairs at a
+  // time from the bf16 projection output (16-byte loads and stores; dh % 16 == 0);
+  // V copied 16 bytes at a time
   const int r = blockIdx.x, lane = threadIdx.x;
   if (r >= M) return;
   const long long slot = rows[r].slot;
@@ -295,33 +296,48 @@ __global__ void rope_kv_kernel(const RowDesc* rows, int M, const __nv_bfloat16* 
   const int half = dh / 2;
   const float2* cs = cs_tab + (long long)r * half;
   const float qscale = rsqrtf((float)dh);
-  const int hp = half / 2;  // bf16 pairs per half
-  for (int idx = lane; idx < (H + KVH) * hp; idx += blockDim.x) {
-    const int head = idx / hp;
-    const int i = (idx - head * hp) * 2;
+  const int ho = half / 8;  // octets per half
+  for (int idx = lane; idx < (H + KVH) * ho; idx += blockDim.x) {
+    const int head = idx / ho;
+    const int i = (idx - head * ho) * 8;
     const __nv_bfloat16* x = src + head * dh;
-    const __nv_bfloat162 a2 = *reinterpret_cast<const __nv_bfloat162*>(x + i);
-    const __nv_bfloat162 b2 = *reinterpret_cast<const __nv_bfloat162*>(x + i + half);
-    const float ax = __low2float(a2), ay = __high2float(a2), bx = __low2float(b2), by = __high2float(b2);
-    const float2 t0 = cs[i], t1 = cs[i + 1];
-    const float ya0 = ax * t0.x - bx * t0.y, ya1 = ay * t1.x - by * t1.y;
-    const float yb0 = ax * t0.y + bx * t0.x, yb1 = ay * t1.y + by * t1.x;
+    const uint4 A = *reinterpret_cast<const uint4*>(x + i);
+    const uint4 B = *reinterpret_cast<const uint4*>(x + i + half);
+    const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&A);
+    const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&B);
+    const float4* c4 = reinterpret_cast<const float4*>(cs + i);  // (cos, sin) of pairs i .. i+7
+    float ya[8], yb[8];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float4 c = c4[k];  // (cos, sin) of pairs i+2k, i+2k+1
+      const float ax = __low2float(a2[k]), ay = __high2float(a2[k]);
+      const float bx = __low2float(b2[k]), by = __high2float(b2[k]);
+      ya[2 * k] = ax * c.x - bx * c.y;
+      ya[2 * k + 1] = ay * c.z - by * c.w;
+      yb[2 * k] = ax * c.y + bx * c.x;
+      yb[2 * k + 1] = ay * c.w + by * c.z;
+    }
     if (head < H) {
-      float* qd = Qr + ((long long)r * H + head) * dh;
-      *reinterpret_cast<float2*>(qd + i) = make_float2(ya0 * qscale, ya1 * qscale);
-      *reinterpret_cast<float2*>(qd + i + half) = make_float2(yb0 * qscale, yb1 * qscale);
+      float4* qd = reinterpret_cast<float4*>(Qr + ((long long)r * H + head) * dh + i);
+      float4* qe = reinterpret_cast<float4*>(Qr + ((long long)r * H + head) * dh + i + half);
+      qd[0] = make_float4(ya[0] * qscale, ya[1] * qscale, ya[2] * qscale, ya[3] * qscale);
+      qd[1] = make_float4(ya[4] * qscale, ya[5] * qscale, ya[6] * qscale, ya[7] * qscale);
+      qe[0] = make_float4(yb[0] * qscale, yb[1] * qscale, yb[2] * qscale, yb[3] * qscale);
+      qe[1] = make_float4(yb[4] * qscale, yb[5] * qscale, yb[6] * qscale, yb[7] * qscale);
     } else {
       const int kh = head - H;
       __nv_bfloat16* kd = Kp + ((long long)kh * slots + slot) * dh;
-      *reinterpret_cast<uint32_t*>(kd + i) = pack_bf16(ya0, ya1);
-      *reinterpret_cast<uint32_t*>(kd + i + half) = pack_bf16(yb0, yb1);
+      *reinterpret_cast<uint4*>(kd + i) =
+          make_uint4(pack_bf16(ya[0], ya[1]), pack_bf16(ya[2], ya[3]), pack_bf16(ya[4], ya[5]), pack_bf16(ya[6], ya[7]));
+      *reinterpret_cast<uint4*>(kd + i + half) =
+          make_uint4(pack_bf16(yb[0], yb[1]), pack_bf16(yb[2], yb[3]), pack_bf16(yb[4], yb[5]), pack_bf16(yb[6], yb[7]));
     }
   }
   const __nv_bfloat16* vs = src + (H + KVH) * dh;
-  for (int idx = lane; idx < KVH * dh / 4; idx += blockDim.x) {
-    const int e = idx * 4;
+  for (int idx = lane; idx < KVH * dh / 8; idx += blockDim.x) {
+    const int e = idx * 8;
     const int kh = e / dh, i = e - kh * dh;
-    *reinterpret_cast<uint2*>(Vp + ((long long)kh * slots + slot) * dh + i) = *reinterpret_cast<const uint2*>(vs + e);
+    *reinterpret_cast<uint4*>(Vp + ((long long)kh * slots + slot) * dh + i) = *reinterpret_cast<const uint4*>(vs + e);
   }
 }
 
