@@ -2481,9 +2481,8 @@ extern "C" void spex_k_order_rows(const RowDesc* rows, int M, int Q, int* order,
 }
 extern "C" void spex_k1_set_kv_evict_first(int on) { g_k1_kv_evict_first = on ? 1 : 0; }
 
-// K1 decode rows through the bulk-copy pipeline (G = 1, dh = 128); item_ctr is
-// a zeroed device int per launch.
-
+// K1 decode rows through the bulk-copy pipeline (G = 1, dh = 128); item_ctr
+// points at two device ints, zero on entry and re-zeroed by the kernel.
 template <int CH, int NST, int W>
 static int launch_bulk(const RowDesc* rows, const Segment* segs, const float* Qr, int H, int KVH,
                        const __nv_bfloat16* Kp, const __nv_bfloat16* Vp, long long slots, __nv_bfloat16* O, int M,
