@@ -2510,8 +2510,10 @@ static int launch_bulk(const RowDesc* rows, const Segment* segs, const float* Qr
   return (int)cudaGetLastError();
 }
 
-// K1 decode rows through the bulk-copy pipeline (G = 1, dh = 128); item_ctr is
-// a device int (zeroed here per launch).
+// K1 decode rows through the bulk-copy pipeline (G = 1, dh = 128); item_ctr
+// points at two device ints, zero before the first launch (the kernel's last
+// warp re-zeroes them, so no memset per launch). Items are claimed in the
+// order spex_k1_set_row_order installed for the step, else row order.
 extern "C" int spex_k_tree_attn_bulk(const RowDesc* rows, const Segment* segs, const float* Qr, int H, int KVH, int dh,
                                      const __nv_bfloat16* Kp, const __nv_bfloat16* Vp, long long slots,
                                      __nv_bfloat16* O, int M, int* item_ctr, cudaStream_t s) {
