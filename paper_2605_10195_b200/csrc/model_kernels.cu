@@ -277,6 +277,34 @@ __global__ void rmsnorm_bf16_kernel(const float* X, int M, int d, float eps, __n
   }
 }
 
+// The same with the row held in registers (d == 128 * NV): one pass over HBM,
+// all NV loads of a lane in flight at once; identical arithmetic and order.
+template <int NV>
+__global__ void rmsnorm_bf16_reg_kernel(const float* X, int M, float eps, __nv_bfloat16* Y) {
+  pdl_wait();
+  constexpr int d = 128 * NV;
+  const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (r >= M) return;
+  const float4* x = reinterpret_cast<const float4*>(X + (long long)r * d);
+  float4 v[NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) v[k] = x[lane + 32 * k];
+  float ss = 0.f;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) ss += v[k].x * v[k].x + v[k].y * v[k].y + v[k].z * v[k].z + v[k].w * v[k].w;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  const float inv = rsqrtf(ss / (float)d + eps);
+  uint2* y = reinterpret_cast<uint2*>(Y + (long long)r * d);
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    uint2 o;
+    o.x = pack_bf16(v[k].x * inv, v[k].y * inv);
+    o.y = pack_bf16(v[k].z * inv, v[k].w * inv);
+    y[lane + 32 * k] = o;
+  }
+}
+
 // RoPE on q and k at the row's absolute position; append k, v (bf16) to the
 // layer's KV pool at the row's slot; q (fp32, pre-scaled by 1/sqrt(dh)) to Qr.
 // Pools are [KVH][slots][dh].
@@ -2397,7 +2425,15 @@ static void launch_maybe_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t 
 }
 
 extern "C" void spex_k_rmsnorm(const float* X, int M, int d, float eps, __nv_bfloat16* Y, cudaStream_t s) {
-  launch_maybe_pdl(rmsnorm_bf16_kernel, dim3((M + 7) / 8), dim3(256), 0, s, X, M, d, eps, Y);
+  static const bool reg = !getenv("SPEX_RMSNORM_REG") || atoi(getenv("SPEX_RMSNORM_REG")) != 0;
+  const dim3 grid((M + 7) / 8), block(256);
+  if (reg) switch (d) {
+      case 512: return launch_maybe_pdl(rmsnorm_bf16_reg_kernel<4>, grid, block, 0, s, X, M, eps, Y);
+      case 1024: return launch_maybe_pdl(rmsnorm_bf16_reg_kernel<8>, grid, block, 0, s, X, M, eps, Y);
+      case 1536: return launch_maybe_pdl(rmsnorm_bf16_reg_kernel<12>, grid, block, 0, s, X, M, eps, Y);
+      default: break;
+    }
+  launch_maybe_pdl(rmsnorm_bf16_kernel, grid, block, 0, s, X, M, d, eps, Y);
 }
 
 extern "C" void spex_k_rope_kv(const RowDesc* rows, int M, const __nv_bfloat16* QKV, int H, int KVH, int dh,
