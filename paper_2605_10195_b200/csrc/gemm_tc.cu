@@ -1,31 +1,52 @@
-// gemm_tc.cu — K2: hand-written tcgen05 GEMM for the policy / PRM projections,
-// with the elementwise work of the forward fused into its epilogue.
+// gemm_tc.cu — K2: hand-written tcgen05 GEMM for every policy / PRM projection
+// (QKV, O, gate/up, down, LM head), with the elementwise work of the forward
+// fused into its epilogue.
 //
 //   Y[M x N] = X[M x K] . W[N x K]^T      (bf16 operands, fp32 accumulate in TMEM)
 //
-// Persistent: one CTA per SM walks 128 x 256 output tiles (UMMA M=128, N=256,
-// K=16 per instruction, cta_group::1) with two TMEM accumulators (2 x 256 fp32
-// columns = all of TMEM), so the epilogue of tile i overlaps the MMAs of tile
-// i+1. Warp roles:
-//   warp 0      TMA producer: 128x64 bf16 boxes of X and W (128-byte swizzle)
-//               into a 4-stage shared-memory ring (full/empty mbarriers)
-//   warp 1      TMEM allocator (512 columns) and MMA issuer: one elected lane
-//               issues 4 tcgen05.mma per stage from shared-memory descriptors,
-//               tcgen05.commit frees the stage / signals the epilogue
-//   warps 2..5  epilogue: tcgen05.ld of the accumulator (one TMEM lane = one
-//               output row per thread, 128 columns per pass), then one of
-//     EPI_STORE    y (+)= acc                       (O / down projections: residual add)
+// This is the compute term the reference prices per decode step,
+// B * flops_per_token / peak (proj/src/sim.cpp:74, include/totsim/budget.hpp:17).
+//
+// Two tile shapes, one kernel template:
+//   CG = 2  CTA pair (cluster of 2, tcgen05 cta_group::2): one 256 x BN output
+//           tile per pair. Each CTA stages its own 128 rows of X and HALF of the
+//           BN weight rows; the leader's single thread issues UMMA M=256 over
+//           both CTAs' shared memory, so every weight byte crosses L2 -> SM once
+//           per 256 rows (half the operand traffic of 1-CTA tiles) and each
+//           CTA's pipeline stage is 32 KB -> 6 stages in flight.
+//   CG = 1  one CTA, 128 x BN tile: small row counts, and narrow N where a
+//           pair's 256 rows would leave SMs idle.
+// Persistent over tiles, warp-specialised (192 threads per CTA):
+//   warp 0      TMA producer (64-row x 64-col boxes, 128-byte swizzle) into a
+//               STAGES-deep ring of full/empty mbarriers. The leader claims
+//               tiles (dynamic queue: CTAs that start late — SMs held by the
+//               control kernel or the PRM stream — take fewer) and hands each
+//               id to its peer through distributed shared memory + mbarrier.
+//   warp 1      TMEM allocation (two BN-column fp32 accumulators) and, in the
+//               leader, the MMA issuer: one lane, 4 x UMMA K=16 per stage,
+//               tcgen05.commit (multicast to both CTAs) frees the stage / marks
+//               the accumulator full.
+//   warps 2..5  epilogue: tcgen05.ld of this CTA's 128 TMEM lanes (thread = row)
+//               128 columns at a time, fused transform in registers, then 32 x 32
+//               blocks staged through shared memory: TMA bulk stores (fp32
+//               outputs) or stores whose every instruction writes four full
+//               128-byte row segments (bf16 / scattered outputs):
+//     EPI_STORE    y = acc, or y += acc as a TMA reduce-add performed at L2 (the
+//                  residual update of the O / down projections; no load on the SM)
 //     EPI_ROPE_KV  rotate-half RoPE; Q heads -> Qr (fp32, pre-scaled), K/V heads
 //                  -> bf16 tree-KV pool at the row's slot     (fuses rope_kv_kernel)
 //     EPI_SWIGLU   silu(gate) * up -> bf16 MLP activation, with the gate/up weight
 //                  rows interleaved per 64-column block       (fuses swiglu_kernel)
-//     EPI_LSE      per-row partial max / first argmax / sum exp / sum over the
-//                  tile's vocab columns; a combine kernel finishes K3
+//     EPI_LSE      per-row partial max / first argmax / sum exp / sum over each
+//                  128 vocab columns; a combine kernel finishes K3
 //                  (the fp32 logits are never written to HBM)
+//   The accumulator is released to the MMA issuer as soon as it is in
+//   registers, so the epilogue of tile i overlaps the MMAs of tile i+1.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+
 #include <cstdlib>
 
 #include "model.h"
@@ -34,33 +55,61 @@ namespace spex {
 
 namespace tc {
 
-constexpr int BM = 128, BK = 64;
-constexpr int EN = 128;  // epilogue chunk (columns per tcgen05.ld pass)
-constexpr int kStageLd = EN + 4;  // padded row of the epilogue staging buffer (conflict-free float4)
-constexpr uint32_t kEpiBytes = 4 * 32 * kStageLd * 4;
-constexpr int kThreads = 192;
-// per tile width BN (128 or 256): pipeline depth, bytes per stage, TMEM columns
-template <int BN> struct TileCfg {
-  static constexpr int STAGES = BN == 256 ? 3 : 4;
-  static constexpr uint32_t kStageBytes = (BM + BN) * BK * 2;  // 48 KB / 32 KB
-  static constexpr uint32_t kTmemCols = BN;                    // one fp32 accumulator; two allocated
-  // kind::f16 instruction descriptor: D f32, A/B bf16, both K-major, M=128, N=BN
+constexpr int BM = 128, BK = 64;   // rows per CTA, K per stage
+constexpr int kEpiWarps = 8;
+constexpr uint32_t kWarpStage = 32 * 32 * 4;  // per epilogue warp: one 32 x 32 fp32 box
+constexpr uint32_t kEpiBytes = kEpiWarps * kWarpStage;
+constexpr int kThreads = 64 + 32 * kEpiWarps;
+constexpr int kTq = 16;            // tile-id ring
+constexpr uint32_t kSmemStages = 196608;  // pipeline bytes per CTA
+
+template <int CG, int BN>
+struct Cfg {
+  static constexpr int BNL = BN / CG;  // weight rows staged per CTA
+  static constexpr uint32_t kABytes = BM * BK * 2;
+  static constexpr uint32_t kBBytes = BNL * BK * 2;
+  static constexpr uint32_t kStageBytes = kABytes + kBBytes;
+  static constexpr int STAGES = kSmemStages / kStageBytes > 8 ? 8 : (int)(kSmemStages / kStageBytes);
+  static constexpr uint32_t kTmemCols = BN;                      // one accumulator
+  static constexpr uint32_t kAllocCols = 2 * BN < 32 ? 32 : 2 * BN;  // two, power of 2
+  // kind::f16 instruction descriptor: D f32, A/B bf16, both K-major, M = 128*CG, N = BN
   static constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
-                                     ((uint32_t)(BM >> 4) << 24);
+                                     ((uint32_t)((BM * CG) >> 4) << 24);
+  static constexpr size_t kSmem = (size_t)STAGES * kStageBytes + kEpiBytes + 1024 + 512;
+  static_assert(BNL % 64 == 0, "weight rows per CTA come in 64-row boxes");
+  static_assert(kSmem <= 232448, "shared memory");
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
-
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+// shared::cluster address of the same variable in CTA `cta` of this cluster
+__device__ __forceinline__ uint32_t peer_addr(uint32_t a, uint32_t cta) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(cta));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
 }
-
 __device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
-
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+// arrive on a barrier of another CTA of the cluster (release at cluster scope)
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n"
@@ -72,13 +121,34 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
-
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
   asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
-          smem_u32(dst)),
-      "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      "{\n"
+      ".reg .pred p;\n"
+      "WAITC_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAITC_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
       : "memory");
+}
+
+// 2D TMA load into this CTA's shared memory; completion (bytes) is counted on
+// `mbar` — for a CTA pair the LEADER's barrier (cta_group::2 allows the peer's).
+template <int CG>
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint32_t mbar) {
+  if constexpr (CG == 2)
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(mbar)
+        : "memory");
+  else
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
+            "r"(smem_u32(dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(mbar)
+        : "memory");
 }
 
 // K-major operand tile [rows][64 bf16] with 128-byte swizzle: 8-row atoms of
@@ -88,18 +158,35 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t addr) {
          ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
 }
 
+template <int CG>
 __device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
                                          uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
-      "l"(da), "l"(db), "r"(idesc), "r"(accumulate));
+  if constexpr (CG == 2)
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(idesc), "r"(accumulate));
+  else
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(idesc), "r"(accumulate));
 }
 
+// MMA completion -> mbarrier arrive; for a pair, on the same barrier of both CTAs
+template <int CG>
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-               : "memory");
+  if constexpr (CG == 2)
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"((uint16_t)3)
+        : "memory");
+  else
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
 }
 
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
@@ -116,37 +203,85 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// fp32 32x32 box shared -> global through the TMA: plain store, or an add into
+// the destination performed by the TMA unit at L2 (the residual stream update
+// y += acc needs no load on the SM). One bulk group per box.
+template <bool kAdd>
+__device__ __forceinline__ void tma_store_box(const CUtensorMap* map, const void* src, int c0, int c1) {
+  if constexpr (kAdd)
+    asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                     map),
+                 "r"(smem_u32(src)), "r"(c0), "r"(c1)
+                 : "memory");
+  else
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%2, %3}], [%1];" ::"l"(map),
+                 "r"(smem_u32(src)), "r"(c0), "r"(c1)
+                 : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+
+// 2^x on the SFU, subnormal results flushed (arguments here are <= 0)
+__device__ __forceinline__ float fast_exp2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
+// Write a 32-row x 32-column block (thread `lane` holds its row's 32 values)
+// through the warp's 4 KB staging buffer (128-byte rows, 16-byte chunks XOR-
+// swizzled by row: conflict-free both ways): lanes along the columns, four
+// rows per store instruction. emit(r, c, float4) stores row r, columns c..c+3.
+template <class Emit>
+__device__ __forceinline__ void store_block(float* buf, const float* vals, int lane, Emit&& emit) {
+  unsigned char* b = reinterpret_cast<unsigned char*>(buf);
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+    *reinterpret_cast<float4*>(b + lane * 128 + ((i ^ (lane & 7)) << 4)) =
+        make_float4(vals[4 * i], vals[4 * i + 1], vals[4 * i + 2], vals[4 * i + 3]);
+  __syncwarp();
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int r = 4 * j + (lane >> 3), c = lane & 7;
+    emit(r, 4 * c, *reinterpret_cast<const float4*>(b + r * 128 + ((c ^ (r & 7)) << 4)));
+  }
+  __syncwarp();
+}
+
 }  // namespace tc
 
-template <int EPI, int DH, int BN>
+template <int EPI, int DH, int BN, int CG>
 __global__ void __launch_bounds__(tc::kThreads, 1)
-    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
-                   int K, TcEpilogue ep, unsigned long long* tile_ctr, unsigned long long tile_base) {
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const __grid_constant__ CUtensorMap tmY, int M, int N, int K, TcEpilogue ep, unsigned int* sched) {
   using namespace tc;
-  using T = TileCfg<BN>;
-  constexpr int STAGES = T::STAGES;
-  constexpr uint32_t kStageBytes = T::kStageBytes;
-  constexpr uint32_t kTmemCols = T::kTmemCols;
+  using C = Cfg<CG, BN>;
+  constexpr int STAGES = C::STAGES, BNL = C::BNL;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  // 1024-byte alignment for the 128B-swizzled tiles
+  // 1024-byte alignment for the 128B-swizzled tiles (same offset in both CTAs of a pair)
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  unsigned char* sA = smem;                          // [STAGES][BM][BK]
-  unsigned char* sB = smem + STAGES * BM * BK * 2;   // [STAGES][BN][BK]
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * kStageBytes);
+  unsigned char* sA = smem;                              // [STAGES][BM][BK]
+  unsigned char* sB = smem + STAGES * C::kABytes;        // [STAGES][BNL][BK]
+  unsigned char* stage_out = smem + STAGES * C::kStageBytes;  // [4 warps][kWarpStage], 1024-aligned
+  uint64_t* full = reinterpret_cast<uint64_t*>(stage_out + kEpiBytes);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;  // [2] accumulator ready
-  uint64_t* tempty = tfull + 2;      // [2] accumulator drained by the epilogue
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  float* stage_out = reinterpret_cast<float*>(smem + STAGES * kStageBytes + 256);  // [4 warps][32][kStageLd]
+  uint64_t* tempty = tfull + 2;      // [2] accumulator drained by the epilogue(s)
+  uint64_t* tqbar = tempty + 2;      // [kTq] tile id handed to the peer
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tqbar + kTq);
+  int* tq = reinterpret_cast<int*>(tmem_slot + 4);  // [kTq]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = CG == 2 ? cluster_rank() : 0;
   const int kblocks = K / BK;
-  const int n_nb = (N + BN - 1) / BN, n_tiles = n_nb * ((M + BM - 1) / BM);
+  // tile t = (mb, nb) with mb fastest: the row blocks that share a weight tile
+  // run at the same time, so each weight byte leaves HBM once (L2 serves the rest)
+  const int n_mb = (M + BM * CG - 1) / (BM * CG), n_tiles = n_mb * ((N + BN - 1) / BN);
+  const int cluster_id = blockIdx.x / CG, n_clusters = gridDim.x / CG;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -155,213 +290,315 @@ __global__ void __launch_bounds__(tc::kThreads, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], 4);  // one arrive per epilogue warp
+      mbar_init(&tempty[b], kEpiWarps * CG);  // one arrive per epilogue warp of each CTA
     }
+    for (int i = 0; i < kTq; ++i) mbar_init(&tqbar[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
+    if constexpr (EPI == TC_EPI_STORE) asm volatile("prefetch.tensormap [%0];" ::"l"(&tmY) : "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(2 * kTmemCols));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if constexpr (CG == 2) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(C::kAllocCols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(C::kAllocCols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
+  if constexpr (CG == 2)
+    cluster_sync_all();  // peer barriers initialised before anyone signals them
+  else
+    __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
+  // programmatic dependent launch: everything above overlapped the previous
+  // kernel's tail; operands (and the tile counter's reset) are ready after this
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 
-  // persistent with a dynamic tile queue: the producer lane claims tiles from a
-  // global counter (so CTAs that start late — SMs busy with the control kernel
-  // or the other forward stream — simply take fewer tiles) and passes each id to
-  // the MMA lane and the epilogue through a shared ring; id -1 ends the CTA.
-  // tile t = (mb, nb), nb fastest
-  int* tq = reinterpret_cast<int*>(tmem_slot + 4);  // [8]
   if (warp == 0) {
+    // ---------------- TMA producer
     if (lane == 0) {
+      const uint32_t full_leader = CG == 2 ? peer_addr(smem_u32(full), 0) : smem_u32(full);
       int g = 0;  // k-block counter across tiles (stage ring position)
       for (int it = 0;; ++it) {
-        long long tl = (long long)(atomicAdd(tile_ctr, 1ull) - tile_base);
-        const int t = tl < n_tiles ? (int)tl : -1;
-        tq[it & 7] = t;
-        if (t < 0) {  // sentinel stage: no data, wakes the MMA lane
-          const int s = g % STAGES;
-          if (g >= STAGES) mbar_wait(&empty[s], ((g / STAGES) - 1) & 1);
-          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&full[s])) : "memory");
+        const int slot = it % kTq;
+        int t;
+        if (rank == 0) {
+          long long tl = sched ? (long long)atomicAdd(sched, 1u) : (long long)cluster_id + (long long)it * n_clusters;
+          t = tl < n_tiles ? (int)tl : -1;
+          tq[slot] = t;
+          if constexpr (CG == 2) {
+            asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(peer_addr(smem_u32(&tq[slot]), 1)), "r"(t)
+                         : "memory");
+            mbar_arrive_remote(peer_addr(smem_u32(&tqbar[slot]), 1));
+          }
+        } else {
+          mbar_wait_cluster(&tqbar[slot], (it / kTq) & 1);
+          t = *reinterpret_cast<volatile int*>(&tq[slot]);
+        }
+        if (t < 0) {
+          if (rank == 0) {  // sentinel stage: no data, wakes the MMA lane
+            const int s = g % STAGES;
+            if (g >= STAGES) mbar_wait(&empty[s], ((g / STAGES) - 1) & 1);
+            mbar_arrive(&full[s]);
+          }
           break;
         }
-        const int mb = t / n_nb, nb = t - mb * n_nb;
+        const int nb = t / n_mb, mb = t - nb * n_mb;
+        const int arow = mb * BM * CG + rank * BM, brow = nb * BN + rank * BNL;
         for (int kb = 0; kb < kblocks; ++kb, ++g) {
           const int s = g % STAGES;
           if (g >= STAGES) mbar_wait(&empty[s], ((g / STAGES) - 1) & 1);
-          mbar_arrive_tx(&full[s], kStageBytes);
-          tma_load_2d(sA + s * BM * BK * 2, &tmA, kb * BK, mb * BM, &full[s]);
+          if (rank == 0) mbar_arrive_tx(&full[s], C::kStageBytes * CG);
+          const uint32_t fb = full_leader + s * 8;
+          unsigned char* a = sA + s * C::kABytes;
+          unsigned char* b = sB + s * C::kBBytes;
+          tma_load_2d<CG>(a, &tmA, kb * BK, arow, fb);
+          tma_load_2d<CG>(a + 64 * BK * 2, &tmA, kb * BK, arow + 64, fb);
 #pragma unroll
-          for (int r = 0; r < BN / 128; ++r)  // the operand maps use 128-row boxes
-            tma_load_2d(sB + s * BN * BK * 2 + r * 128 * BK * 2, &tmB, kb * BK, nb * BN + r * 128, &full[s]);
+          for (int r = 0; r < BNL / 64; ++r) tma_load_2d<CG>(b + r * 64 * BK * 2, &tmB, kb * BK, brow + r * 64, fb);
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    // ---------------- MMA issuer (the pair's leader)
+    if (lane == 0 && rank == 0) {
       int g = 0;
       for (int it = 0;; ++it) {
         const int acc = it & 1;
         mbar_wait(&full[g % STAGES], (g / STAGES) & 1);  // first stage of tile `it` (or the sentinel)
-        const int t = tq[it & 7];
+        const int t = tq[it % kTq];
         // accumulator `acc` must be drained before its barrier moves again
         // (also for the sentinel: two unobserved phases would alias the parity)
         if (it >= 2) mbar_wait(&tempty[acc], ((it >> 1) - 1) & 1);
         if (t < 0) {
-          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tfull[acc])) : "memory");
+          mbar_arrive(&tfull[acc]);
+          if constexpr (CG == 2) mbar_arrive_remote(peer_addr(smem_u32(&tfull[acc]), 1));
           break;
         }
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t dt = tmem + acc * kTmemCols;
+        const uint32_t dt = tmem + acc * C::kTmemCols;
         for (int kb = 0; kb < kblocks; ++kb, ++g) {
           const int s = g % STAGES;
           if (kb > 0) mbar_wait(&full[s], (g / STAGES) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint64_t da = smem_desc(smem_u32(sA + s * BM * BK * 2));
-          const uint64_t db = smem_desc(smem_u32(sB + s * BN * BK * 2));
+          const uint64_t da = smem_desc(smem_u32(sA + s * C::kABytes));
+          const uint64_t db = smem_desc(smem_u32(sB + s * C::kBBytes));
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k)  // 16 bf16 = 32 bytes = 2 descriptor units per step
-            mma_bf16(dt, da + 2 * k, db + 2 * k, T::kIdesc, (kb | k) != 0);
-          mma_commit(&empty[s]);
+            mma_bf16<CG>(dt, da + 2 * k, db + 2 * k, C::kIdesc, (kb | k) != 0);
+          mma_commit<CG>(&empty[s]);
         }
-        mma_commit(&tfull[acc]);
+        mma_commit<CG>(&tfull[acc]);
       }
     }
     __syncwarp();
   } else {
-    // ---------------- epilogue: warps 2..5 own TMEM lane quarters (warp % 4)
-    const int quarter = warp & 3;
+    // ---------------- epilogue: 8 warps. Warp w reads TMEM lane quarter w % 4
+    // (hardware rule) = 32 rows of this CTA's 128; the two warps of a quarter
+    // split the tile's column units between them.
+    const int ew = warp - 2, quarter = warp & 3, grp = ew >> 2;
+    unsigned char* wstage = stage_out + ew * kWarpStage;  // 4 KB, 128B-swizzled 32 x 32 fp32
+    const uint32_t tempty_leader0 = CG == 2 ? peer_addr(smem_u32(&tempty[0]), 0) : smem_u32(&tempty[0]);
+    constexpr int NU = EPI == TC_EPI_STORE ? BN / 32 : EPI == TC_EPI_LSE ? BN / 128 : BN / 64;  // units per tile
     for (int it = 0;; ++it) {
       const int acc = it & 1;
       mbar_wait(&tfull[acc], (it >> 1) & 1);
-      const int t = tq[it & 7];
+      if (rank != 0) mbar_wait_cluster(&tqbar[it % kTq], (it / kTq) & 1);
+      const int t = *reinterpret_cast<volatile int*>(&tq[it % kTq]);
       if (t < 0) break;
-      const int mb = t / n_nb, nb = t - mb * n_nb;
-      const int row = mb * BM + quarter * 32 + lane;
+      const int nb = t / n_mb, mb = t - nb * n_mb;
+      const int row0 = mb * BM * CG + rank * BM + quarter * 32;  // this warp's 32 rows
+      const int row = row0 + lane;
+      const int col0 = nb * BN;
+      // per-row operand of the epilogue, loaded before the accumulator
+      long long my_slot = 0;
+      if constexpr (EPI == TC_EPI_ROPE_KV)
+        if (row < M) my_slot = ep.rows[row].slot;
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint32_t tbase = tmem + acc * kTmemCols + ((uint32_t)(quarter * 32) << 16);
-#pragma unroll 1
-      for (int h = 0; h < BN / EN; ++h) {
-        float v[EN];
-#pragma unroll
-        for (int c = 0; c < EN / 32; ++c) tmem_ld32(tbase + h * EN + c * 32, v + c * 32);
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        if (h == BN / EN - 1) {  // accumulator fully read: the MMA warp may reuse it
-          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-          __syncwarp();
-          if (lane == 0)
-            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tempty[acc])) : "memory");
+      const uint32_t tbase = tmem + acc * C::kTmemCols + ((uint32_t)(quarter * 32) << 16);
+      auto release = [&]() {  // accumulator fully read by this warp: the MMA warp may reuse it
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) {
+          if (CG == 2 && rank != 0)
+            mbar_arrive_remote(tempty_leader0 + acc * 8);
+          else
+            mbar_arrive(&tempty[acc]);
         }
-        const int n0 = nb * BN + h * EN;
-        if (n0 >= N) continue;  // partial last N tile (its B rows were zero-filled)
-        const int row0 = mb * BM + quarter * 32;  // this warp's 32 rows
-        if constexpr (EPI == TC_EPI_LSE) {
-          if (row < M) {
-            float mx = -INFINITY, sm = 0.f;
-            int mi = 0;
-            const int lim = min(EN, ep.V - n0);
+      };
+      if (grp >= NU) release();  // no unit for this warp in this tile
+#pragma unroll 1
+      for (int u = grp; u < NU; u += 2) {
+        const bool last = u + 2 >= NU;
+        if constexpr (EPI == TC_EPI_STORE) {
+          // one 32-column piece -> TMA store / reduce-add of a 32 x 32 box
+          float v[32];
+          tmem_ld32(tbase + u * 32, v);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          if (last) release();
+          const int n0 = col0 + u * 32;
+          if (n0 >= N) continue;  // partial last N tile (its weight rows were zero-filled)
+          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // staging free
+          __syncwarp();
 #pragma unroll
-            for (int i = 0; i < EN; ++i) {
-              if (i < lim) {
-                sm += v[i];
-                if (v[i] > mx) {
-                  mx = v[i];
-                  mi = i;
-                }
+          for (int i = 0; i < 8; ++i)
+            *reinterpret_cast<float4*>(wstage + lane * 128 + ((i ^ (lane & 7)) << 4)) =
+                make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) {
+            if (ep.accumulate)
+              tma_store_box<true>(&tmY, wstage, n0, row0);
+            else
+              tma_store_box<false>(&tmY, wstage, n0, row0);
+          }
+        } else if constexpr (EPI == TC_EPI_LSE) {
+          // one 128-column block (4 pieces, online): partial max / first argmax /
+          // sum exp(x - max) / sum x; V % 128 == 0 so every block is full
+          const int n0 = col0 + u * 128;
+          float m = -INFINITY, S = 0.f, T = 0.f;
+          int a = 0;
+#pragma unroll 1
+          for (int pc = 0; pc < 4; ++pc) {
+            float v[32];
+            tmem_ld32(tbase + u * 128 + pc * 32, v);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            if (last && pc == 3) release();
+            float mx[4], sm[4];
+            int mi[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              mx[j] = v[j];
+              mi[j] = j;
+              sm[j] = v[j];
+            }
+#pragma unroll
+            for (int i = 4; i < 32; ++i) {
+              const int j = i & 3;
+              sm[j] += v[i];
+              if (v[i] > mx[j]) {
+                mx[j] = v[i];
+                mi[j] = i;
               }
             }
-            float se = 0.f;
-            const float ml2 = mx * 1.4426950408889634f;
+            float pm = mx[0];
+            int pa = mi[0];
 #pragma unroll
-            for (int i = 0; i < EN; ++i)
-              if (i < lim) se += exp2f(fmaf(v[i], 1.4426950408889634f, -ml2));
-            reinterpret_cast<float4*>(ep.part)[(long long)row * ep.n_tiles + n0 / EN] =
-                make_float4(mx, se, sm, __int_as_float(n0 + mi));
+            for (int j = 1; j < 4; ++j)
+              if (mx[j] > pm || (mx[j] == pm && mi[j] < pa)) {
+                pm = mx[j];
+                pa = mi[j];
+              }
+            if (pm > m) {  // earlier pieces win ties (first argmax)
+              S = pc == 0 ? 0.f : S * fast_exp2((m - pm) * 1.4426950408889634f);
+              m = pm;
+              a = pc * 32 + pa;
+            }
+            const float ml2 = m * 1.4426950408889634f;
+            float se[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+            for (int i = 0; i < 32; ++i) se[i & 3] += fast_exp2(fmaf(v[i], 1.4426950408889634f, -ml2));
+            S += (se[0] + se[1]) + (se[2] + se[3]);
+            T += (sm[0] + sm[1]) + (sm[2] + sm[3]);
           }
-          continue;
-        }
-        // per-row transform in registers (thread = row)
-        if constexpr (EPI == TC_EPI_ROPE_KV) {
-          constexpr int half = DH / 2;
-          const float2* cs = reinterpret_cast<const float2*>(ep.rope) + (long long)(row < M ? row : 0) * half;
-#pragma unroll
-          for (int h0 = 0; h0 < EN; h0 += DH) {
-            const int head = (n0 + h0) / DH;
+          if (row < M && n0 < N)
+            reinterpret_cast<float4*>(ep.part)[(long long)row * ep.n_tiles + n0 / 128] =
+                make_float4(m, S, T, __int_as_float(n0 + a));
+        } else {
+          // a pair of 32-column pieces: (x[i], x[i + half]) of one head (ROPE_KV)
+          // or (gate j, up j) of one 128-row interleaved block (SWIGLU)
+          int lo, hi;
+          if constexpr (EPI == TC_EPI_ROPE_KV) {
+            constexpr int upb = DH / 64;  // units per head
+            lo = (u / upb) * DH + (u % upb) * 32;
+            hi = lo + DH / 2;
+          } else {
+            lo = (u >> 1) * 128 + (u & 1) * 32;
+            hi = lo + 64;
+          }
+          float x[32], y[32];
+          tmem_ld32(tbase + lo, x);
+          tmem_ld32(tbase + hi, y);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          if (last) release();
+          if (col0 + lo >= N) continue;
+          if constexpr (EPI == TC_EPI_ROPE_KV) {
+            const int head = (col0 + lo) / DH, d_lo = (col0 + lo) - head * DH;
             if (head < ep.H + ep.KVH) {  // rotate-half RoPE on (x[i], x[i + half]); Q also scaled
               const float sc = head < ep.H ? ep.qscale : 1.f;
+              const float4* cs =
+                  reinterpret_cast<const float4*>(ep.rope) + ((long long)(row < M ? row : 0) * (DH / 2) + d_lo) / 2;
 #pragma unroll
-              for (int i = 0; i < half; ++i) {
-                const float2 c = cs[i];
-                const float a = v[h0 + i], b = v[h0 + half + i];
-                v[h0 + i] = (a * c.x - b * c.y) * sc;
-                v[h0 + half + i] = (a * c.y + b * c.x) * sc;
+              for (int i = 0; i < 32; i += 2) {
+                const float4 c = cs[i / 2];  // (cos, sin) of pairs d_lo + i, d_lo + i + 1
+                const float a0 = x[i], b0 = y[i], a1 = x[i + 1], b1 = y[i + 1];
+                x[i] = (a0 * c.x - b0 * c.y) * sc;
+                y[i] = (a0 * c.y + b0 * c.x) * sc;
+                x[i + 1] = (a1 * c.z - b1 * c.w) * sc;
+                y[i + 1] = (a1 * c.w + b1 * c.z) * sc;
               }
             }
-          }
-        } else if constexpr (EPI == TC_EPI_SWIGLU) {
-          // chunk n0: columns [0,64) gate j, [64,128) up j for j in [n0/2, n0/2 + 64)
+            const bool is_q = head < ep.H, is_k = !is_q && head < ep.H + ep.KVH;
+            const int kh = is_q ? 0 : is_k ? head - ep.H : head - ep.H - ep.KVH;
+            __nv_bfloat16* pool = reinterpret_cast<__nv_bfloat16*>(is_k ? ep.Kp : ep.Vp);
 #pragma unroll
-          for (int i = 0; i < EN / 2; ++i) {
-            const float g = v[i], u = v[EN / 2 + i];
-            v[i] = g / (1.f + __expf(-g)) * u;
+            for (int half = 0; half < 2; ++half) {
+              const int d0 = d_lo + half * (DH / 2);
+              store_block(reinterpret_cast<float*>(wstage), half ? y : x, lane, [&](int r, int c, float4 o) {
+                const int grow = row0 + r;
+                const long long slot = __shfl_sync(0xffffffffu, my_slot, r);  // row r's tree-KV slot
+                if (grow >= M) return;
+                if (is_q) {
+                  *reinterpret_cast<float4*>(ep.Qr + ((long long)grow * ep.H + head) * DH + d0 + c) = o;
+                } else {
+                  *reinterpret_cast<uint2*>(pool + ((long long)kh * ep.slots + slot) * DH + d0 + c) =
+                      make_uint2(pack2(o.x, o.y), pack2(o.z, o.w));
+                }
+              });
+            }
+          } else {  // TC_EPI_SWIGLU: act[row][(col0 + lo_block) / 2 + j]
+#pragma unroll
+            for (int i = 0; i < 32; ++i) x[i] = __fdividef(x[i], 1.f + __expf(-x[i])) * y[i];
+            const int ac = (col0 + (u >> 1) * 128) / 2 + (u & 1) * 32;
+            store_block(reinterpret_cast<float*>(wstage), x, lane, [&](int r, int c, float4 o) {
+              const int grow = row0 + r;
+              if (grow >= M) return;
+              *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(ep.act) + (long long)grow * ep.F + ac + c) =
+                  make_uint2(pack2(o.x, o.y), pack2(o.z, o.w));
+            });
           }
         }
-        // stage the warp's 32 x EN block in shared memory, then write it out
-        // row by row with the lanes along the columns (512 B per instruction)
-        float* buf = stage_out + (warp - 2) * 32 * kStageLd;
-        constexpr int NW = EPI == TC_EPI_SWIGLU ? EN / 2 : EN;  // columns written
-#pragma unroll
-        for (int i = 0; i < NW / 4; ++i)
-          *reinterpret_cast<float4*>(buf + lane * kStageLd + 4 * i) =
-              make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-        __syncwarp();
-        const int c = 4 * lane;  // this lane's 4 columns of each row
-        for (int r = 0; r < 32; ++r) {
-          const int grow = row0 + r;
-          if (grow >= M) break;
-          if (c >= NW) continue;
-          const float4 o = *reinterpret_cast<const float4*>(buf + r * kStageLd + c);
-          if constexpr (EPI == TC_EPI_STORE) {
-            float4* y = reinterpret_cast<float4*>(ep.y + (long long)grow * ep.ldy + n0 + c);
-            float4 w = o;
-            if (ep.accumulate) {
-              const float4 a = *y;
-              w.x += a.x;
-              w.y += a.y;
-              w.z += a.z;
-              w.w += a.w;
-            }
-            *y = w;
-          } else if constexpr (EPI == TC_EPI_SWIGLU) {
-            *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(ep.act) + (long long)grow * ep.F + n0 / 2 + c) =
-                make_uint2(pack2(o.x, o.y), pack2(o.z, o.w));
-          } else {  // TC_EPI_ROPE_KV
-            const int col = n0 + c, head = col / DH, d0 = col - head * DH;
-            if (head < ep.H) {
-              *reinterpret_cast<float4*>(ep.Qr + ((long long)grow * ep.H + head) * DH + d0) = o;
-            } else {
-              const bool is_k = head < ep.H + ep.KVH;
-              const int kh = is_k ? head - ep.H : head - ep.H - ep.KVH;
-              __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(is_k ? ep.Kp : ep.Vp) +
-                                   ((long long)kh * ep.slots + ep.rows[grow].slot) * DH + d0;
-              *reinterpret_cast<uint2*>(dst) = make_uint2(pack2(o.x, o.y), pack2(o.z, o.w));
-            }
-          }
-        }
-        __syncwarp();
       }
     }
   }
+  if constexpr (EPI == TC_EPI_STORE)
+    if (warp >= 2 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // stores landed
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
+  if constexpr (CG == 2)
+    cluster_sync_all();  // the leader's MMAs wrote into the peer's TMEM: both done before dealloc
+  else
+    __syncthreads();
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * kTmemCols));
+    if constexpr (CG == 2)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C::kAllocCols));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C::kAllocCols));
+  }
+  // self-resetting tile queue: the last leader out zeroes it for the next launch
+  if (sched && threadIdx.x == 0 && rank == 0) {
+    __threadfence();
+    if (atomicAdd(sched + 1, 1u) == (unsigned)n_clusters - 1) {
+      sched[0] = 0;
+      sched[1] = 0;
+      __threadfence();
+    }
   }
 }
 
@@ -369,6 +606,7 @@ __global__ void __launch_bounds__(tc::kThreads, 1)
 __global__ void lse_combine_kernel(const float4* __restrict__ part, int M, int n_tiles, int* amax, float* lse,
                                    float* lsum) {
   const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   if (r >= M) return;
   const float4* p = part + (long long)r * n_tiles;
   float mx = -INFINITY, sm = 0.f;
@@ -430,96 +668,150 @@ __global__ void interleave_gu_kernel(const __nv_bfloat16* __restrict__ wgu, int 
 
 using namespace spex;
 
-template <int EPI, int DH, int BN>
-static int launch_gemm_tc(const CUtensorMap* tmA, const CUtensorMap* tmB, int M, int N, int K, const TcEpilogue* ep,
-                          cudaStream_t s, int grid_x, unsigned long long* tile_ctr, unsigned long long tile_base) {
-  using T = tc::TileCfg<BN>;
-  const size_t smem = T::STAGES * T::kStageBytes + 1024 + 256 + tc::kEpiBytes;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(gemm_tc_kernel<EPI, DH, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
-  gemm_tc_kernel<EPI, DH, BN><<<grid_x, tc::kThreads, smem, s>>>(*tmA, *tmB, M, N, K, *ep, tile_ctr, tile_base);
-  return (int)cudaGetLastError();
+namespace {
+
+int sm_count() {
+  static const int n = [] {
+    int dev = 0, v = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v > 0 ? v : 148;
+  }();
+  return n;
+}
+
+typedef CUresult (*PFN_encode)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+PFN_encode encoder() {
+  static const PFN_encode fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return (PFN_encode) nullptr;
+    return reinterpret_cast<PFN_encode>(p);
+  }();
+  return fn;
+}
+
+// fp32 output [M][N] with row pitch ldy as 32 x 32 boxes, 128-byte swizzle (the
+// epilogue's staging layout); rows >= M and columns >= N are clipped by the TMA.
+bool make_out_map(CUtensorMap* m, const float* y, int M, int N, int ldy) {
+  PFN_encode enc = encoder();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)N, (cuuint64_t)M};
+  cuuint64_t strides[1] = {(cuuint64_t)ldy * 4};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t es[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(y), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int EPI, int DH, int BN, int CG>
+int launch_gemm_tc(const CUtensorMap* tmA, const CUtensorMap* tmB, const CUtensorMap* tmY, int M, int N, int K,
+                   const TcEpilogue* ep, unsigned int* sched, cudaStream_t s) {
+  using C = tc::Cfg<CG, BN>;
+  auto kern = gemm_tc_kernel<EPI, DH, BN, CG>;
+  static const cudaError_t attr =
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::kSmem);
+  if (attr != cudaSuccess) return (int)attr;
+  const int tiles = ((M + tc::BM * CG - 1) / (tc::BM * CG)) * ((N + BN - 1) / BN);
+  const int slots = sm_count() / CG;
+  const int clusters = tiles < slots ? tiles : slots;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(clusters * CG);
+  cfg.blockDim = dim3(tc::kThreads);
+  cfg.dynamicSmemBytes = C::kSmem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  at[1].id = cudaLaunchAttributeClusterDimension;
+  at[1].val.clusterDim.x = CG;
+  at[1].val.clusterDim.y = 1;
+  at[1].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  return (int)cudaLaunchKernelEx(&cfg, kern, *tmA, *tmB, *tmY, M, N, K, *ep, sched);
 }
 
 template <int EPI, int DH>
-static int launch_bn(int bn, const CUtensorMap* tmA, const CUtensorMap* tmB, int M, int N, int K,
-                     const TcEpilogue* ep, cudaStream_t s, int grid_x, unsigned long long* ctr,
-                     unsigned long long base) {
-  return bn == 256 ? launch_gemm_tc<EPI, DH, 256>(tmA, tmB, M, N, K, ep, s, grid_x, ctr, base)
-                   : launch_gemm_tc<EPI, DH, 128>(tmA, tmB, M, N, K, ep, s, grid_x, ctr, base);
+int launch_shape(int cg, int bn, const CUtensorMap* tmA, const CUtensorMap* tmB, int M, int N, int K,
+                 const TcEpilogue* ep, unsigned int* sched, cudaStream_t s) {
+  alignas(64) CUtensorMap tmY{};
+  if constexpr (EPI == TC_EPI_STORE)
+    if (!make_out_map(&tmY, ep->y, M, N, ep->ldy)) return -2;
+  const CUtensorMap* y = &tmY;
+  if (cg == 2 && bn == 256) return launch_gemm_tc<EPI, DH, 256, 2>(tmA, tmB, y, M, N, K, ep, sched, s);
+  if (cg == 2 && bn == 128) return launch_gemm_tc<EPI, DH, 128, 2>(tmA, tmB, y, M, N, K, ep, sched, s);
+  if (cg == 1 && bn == 256) return launch_gemm_tc<EPI, DH, 256, 1>(tmA, tmB, y, M, N, K, ep, sched, s);
+  if (cg == 1 && bn == 128) return launch_gemm_tc<EPI, DH, 128, 1>(tmA, tmB, y, M, N, K, ep, sched, s);
+  if constexpr (EPI == TC_EPI_STORE)
+    if (cg == 1 && bn == 64) return launch_gemm_tc<EPI, DH, 64, 1>(tmA, tmB, y, M, N, K, ep, sched, s);
+  return -1;
 }
 
-extern "C" int spex_k_gemm_tc(const CUtensorMap* tmA, const CUtensorMap* tmB, int M, int N, int K,
-                              const TcEpilogue* ep, cudaStream_t s) {
+// Tile shape: the candidate whose waves of tiles over the SMs finish first.
+// Per-tile cost ~ BN columns x a per-shape efficiency (pairs halve the weight
+// traffic per row; 64-wide tiles re-read X four times per 256 columns).
+void pick_shape(int M, int N, int epi, int* cg, int* bn) {
+  struct Cand {
+    int cg, bn;
+    double eff;
+  };
+  const Cand cands[] = {{2, 256, 1.00}, {2, 128, 1.10}, {1, 256, 1.08}, {1, 128, 1.20}, {1, 64, 1.45}};
+  double best = 1e300;
+  for (const Cand& c : cands) {
+    if (c.bn == 64 && epi != TC_EPI_STORE) continue;
+    const long long tiles = (long long)((M + 128 * c.cg - 1) / (128 * c.cg)) * ((N + c.bn - 1) / c.bn);
+    const int slots = sm_count() / c.cg;
+    const long long waves = (tiles + slots - 1) / slots;
+    const double cost = (double)waves * c.bn * c.eff;
+    if (cost < best - 1e-9) {
+      best = cost;
+      *cg = c.cg;
+      *bn = c.bn;
+    }
+  }
+}
+
+}  // namespace
+
+// Y = X . W^T through the fused-epilogue tcgen05 GEMM. `sched` is a zeroed
+// pair of device counters owned by the caller (one per stream: the kernel
+// resets them on exit) for the dynamic tile queue, or null for a static
+// round-robin schedule. cg/bn = 0 picks the tile shape.
+extern "C" int spex_k_gemm_tc_ex(const CUtensorMap* tmA, const CUtensorMap* tmB, int M, int N, int K,
+                                 const TcEpilogue* ep, unsigned int* sched, int cg, int bn, cudaStream_t s) {
   if (M <= 0) return 0;
-  if (N % tc::EN || K % tc::BK) return -1;
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
-  static const int cap = getenv("SPEX_TC_GRID") ? atoi(getenv("SPEX_TC_GRID")) : sms;
-  const int gmax = cap > 0 && cap < sms ? cap : sms;
-  // tile width: the one whose last wave is fuller (128-wide tiles cost a second
-  // A-tile read per 256 columns but fill the SMs on mid-size problems)
-  const int mb = (M + tc::BM - 1) / tc::BM;
-  auto eff = [&](int bn) {
-    const long long t = (long long)mb * ((N + bn - 1) / bn);
-    const long long waves = (t + gmax - 1) / gmax;
-    return (double)t / (double)(waves * gmax) * (bn == 256 ? 1.0 : 0.85);
-  };
-  static const int force_bn = getenv("SPEX_TC_BN") ? atoi(getenv("SPEX_TC_BN")) : 0;
-  const int bn = force_bn == 128 || force_bn == 256 ? force_bn : (eff(256) >= eff(128) ? 256 : 128);
-  const int tiles = mb * ((N + bn - 1) / bn);
-  const int grid_x = tiles < gmax ? tiles : gmax;
-  // per-stream monotone tile counter: launch j claims ids [base_j, base_j + tiles + grid).
-  // Counters come from one pool; a stream seen for the first time takes the
-  // least recently assigned slot (streams are per executor, so after
-  // kCtrSlots newer streams the evicted one has long finished).
-  constexpr int kCtrSlots = 256;
-  struct Ctr {
-    cudaStream_t st;
-    unsigned long long base;
-  };
-  static Ctr ctrs[kCtrSlots];
-  static unsigned long long* pool = nullptr;
-  static int n_ctrs = 0;
-  if (!pool) {
-    if (cudaMalloc(&pool, kCtrSlots * sizeof(unsigned long long)) != cudaSuccess) return -3;
-    if (cudaMemset(pool, 0, kCtrSlots * sizeof(unsigned long long)) != cudaSuccess) return -3;
-  }
-  Ctr* c = nullptr;
-  for (int i = 0; i < n_ctrs && i < kCtrSlots; ++i)
-    if (ctrs[i].st == s) c = &ctrs[i];
-  if (!c) {
-    c = &ctrs[n_ctrs % kCtrSlots];
-    c->st = s;
-    c->base = 0;
-    cudaMemsetAsync(pool + (c - ctrs), 0, sizeof(unsigned long long), s);
-    ++n_ctrs;
-  }
-  unsigned long long* const ctr = pool + (c - ctrs);
-  const unsigned long long base = c->base;
-  c->base += (unsigned long long)tiles + grid_x;
+  if (N % 64 || K % tc::BK) return -1;
+  if (ep->kind != TC_EPI_STORE && N % 128) return -1;
+  if (cg == 0 || bn == 0) pick_shape(M, N, ep->kind, &cg, &bn);
   switch (ep->kind) {
     case TC_EPI_STORE:
-      return launch_bn<TC_EPI_STORE, 128>(bn, tmA, tmB, M, N, K, ep, s, grid_x, ctr, base);
+      return launch_shape<TC_EPI_STORE, 128>(cg, bn, tmA, tmB, M, N, K, ep, sched, s);
     case TC_EPI_SWIGLU:
-      return launch_bn<TC_EPI_SWIGLU, 128>(bn, tmA, tmB, M, N, K, ep, s, grid_x, ctr, base);
+      return launch_shape<TC_EPI_SWIGLU, 128>(cg, bn, tmA, tmB, M, N, K, ep, sched, s);
     case TC_EPI_LSE:
-      return launch_bn<TC_EPI_LSE, 128>(bn, tmA, tmB, M, N, K, ep, s, grid_x, ctr, base);
+      return launch_shape<TC_EPI_LSE, 128>(cg, bn, tmA, tmB, M, N, K, ep, sched, s);
     case TC_EPI_ROPE_KV:
-      if (ep->dh == 128) return launch_bn<TC_EPI_ROPE_KV, 128>(bn, tmA, tmB, M, N, K, ep, s, grid_x, ctr, base);
-      if (ep->dh == 64) return launch_bn<TC_EPI_ROPE_KV, 64>(bn, tmA, tmB, M, N, K, ep, s, grid_x, ctr, base);
+      if (ep->dh == 128) return launch_shape<TC_EPI_ROPE_KV, 128>(cg, bn, tmA, tmB, M, N, K, ep, sched, s);
+      if (ep->dh == 64) return launch_shape<TC_EPI_ROPE_KV, 64>(cg, bn, tmA, tmB, M, N, K, ep, sched, s);
       return -1;
     default:
       return -1;
   }
 }
+
+extern "C" int spex_k_gemm_tc(const CUtensorMap* tmA, const CUtensorMap* tmB, int M, int N, int K,
+                              const TcEpilogue* ep, unsigned int* sched, cudaStream_t s) {
+  return spex_k_gemm_tc_ex(tmA, tmB, M, N, K, ep, sched, 0, 0, s);
+}
+
+extern "C" void spex_k_gemm_tc_shape(int M, int N, int epi, int* cg, int* bn) { pick_shape(M, N, epi, cg, bn); }
 
 extern "C" void spex_k_lse_combine(const float* part, int M, int n_tiles, int* amax, float* lse, float* lsum,
                                    cudaStream_t s) {

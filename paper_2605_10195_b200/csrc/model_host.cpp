@@ -10,11 +10,10 @@
 // executor.cpp:366-411) runs the PRM over each completed thought's tokens with
 // its own tree KV pool, then the value head (K4).
 //
-// Projections use cuBLAS bf16 GEMMs with fp32 accumulation (library GEMMs;
-// DESIGN.md lists the hand-written tcgen05 replacement as the next step).
+// Every projection runs on the hand-written tcgen05 GEMM (gemm_tc.cu) with the
+// elementwise work fused into its epilogue; no library GEMM is called.
 #include "model_host.h"
 
-#include <cublas_v2.h>
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -78,7 +77,7 @@ int spex_k_tree_attn_chunked(const RowDesc* rows, const Segment* segs, const flo
                              DecodeChunks w, int qslot, cudaStream_t s);
 void spex_k_swiglu(const __nv_bfloat16* GU, int M, int F, __nv_bfloat16* A, cudaStream_t s);
 int spex_k_gemm_tc(const CUtensorMap* tmA, const CUtensorMap* tmB, int M, int N, int K, const TcEpilogue* ep,
-                   cudaStream_t s);
+                   unsigned int* sched, cudaStream_t s);
 void spex_k_lse_combine(const float* part, int M, int n_tiles, int* amax, float* lse, float* lsum, cudaStream_t s);
 void spex_k_rope_table(const RowDesc* rows, int M, const float* inv_freq, int half, float* out, cudaStream_t s);
 void spex_k_interleave_gu(const __nv_bfloat16* wgu, int F, int d, __nv_bfloat16* out, cudaStream_t s);
@@ -98,34 +97,12 @@ namespace {
     cudaError_t e_ = (x);                                                                        \
     if (e_ != cudaSuccess) throw std::runtime_error(std::string(#x) + ": " + cudaGetErrorString(e_)); \
   } while (0)
-#define CB(x)                                                                         \
-  do {                                                                                \
-    cublasStatus_t e_ = (x);                                                          \
-    if (e_ != CUBLAS_STATUS_SUCCESS) throw std::runtime_error(std::string(#x) + " failed: " + std::to_string(e_)); \
-  } while (0)
-
 template <class T>
 T* dalloc(size_t n, std::vector<void*>& owned) {
   void* p = nullptr;
   CK(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)));
   owned.push_back(p);
   return static_cast<T*>(p);
-}
-
-// y[M x N] (fp32) = x[M x K] (bf16) . W[N x K]^T (bf16) (+ y if accumulate)
-void gemm(cublasHandle_t h, const __nv_bfloat16* x, const __nv_bfloat16* W, float* y, int M, int N, int K,
-          bool accumulate) {
-  const float alpha = 1.f, beta = accumulate ? 1.f : 0.f;
-  CB(cublasGemmEx(h, CUBLAS_OP_T, CUBLAS_OP_N, N, M, K, &alpha, W, CUDA_R_16BF, K, x, CUDA_R_16BF, K, &beta, y,
-                  CUDA_R_32F, N, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT));
-}
-
-// y[M x N] (bf16, fp32 accumulate) = x[M x K] (bf16) . W[N x K]^T (bf16)
-void gemm_bf16out(cublasHandle_t h, const __nv_bfloat16* x, const __nv_bfloat16* W, __nv_bfloat16* y, int M, int N,
-                  int K) {
-  const float alpha = 1.f, beta = 0.f;
-  CB(cublasGemmEx(h, CUBLAS_OP_T, CUBLAS_OP_N, N, M, K, &alpha, W, CUDA_R_16BF, K, x, CUDA_R_16BF, K, &beta, y,
-                  CUDA_R_16BF, N, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT));
 }
 
 }  // namespace
@@ -175,13 +152,13 @@ extern "C" int spex_tmap_kv16(CUtensorMap* m, void* base, long long rows, int dh
 }
 
 // TMA descriptor of a row-major bf16 matrix [rows][cols] as a GEMM operand of
-// gemm_tc.cu: 64 x 128 (cols x rows) boxes, 128-byte swizzle.
+// gemm_tc.cu: 64 x 64 (cols x rows) boxes, 128-byte swizzle.
 extern "C" int spex_tmap_operand(CUtensorMap* m, const void* base, long long rows, long long cols) {
   PFN_tmap_encode enc = tmap_encoder();
   if (!enc || cols % 64 != 0) return -1;
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
-  cuuint32_t box[2] = {64, 128};
+  cuuint32_t box[2] = {64, 64};
   cuuint32_t es[2] = {1, 1};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -213,23 +190,16 @@ struct Model {
   // activations
   float* X = nullptr;
   __nv_bfloat16* Xn = nullptr;
-  __nv_bfloat16* QKV = nullptr;  // bf16 projection outputs feeding RoPE / SwiGLU
-  float* Qr = nullptr;
-  __nv_bfloat16* O = nullptr;
-  __nv_bfloat16* GU = nullptr;
-  __nv_bfloat16* A = nullptr;
-  float* logits = nullptr;
-  // tcgen05 path (use_tc): weight maps, activation maps, RoPE table, LM-head partials
-  bool use_tc = false;
+  float* Qr = nullptr;               // [rows][H][dh] fp32, RoPE'd and pre-scaled (QKV epilogue)
+  __nv_bfloat16* O = nullptr;        // attention output
+  __nv_bfloat16* A = nullptr;        // SwiGLU activation (gate/up epilogue)
+  // K2 (tcgen05): weight maps, activation maps, RoPE table, LM-head partials
   std::vector<TcWeight> tq, to, tgu, td;
   TcWeight tlm;
-  std::vector<__nv_bfloat16*> wgu_il;  // gate/up rows interleaved per 64
   CUtensorMap a_xn, a_o, a_act;        // activation operands [max_rows][*]
   float* rope_tab = nullptr;           // [max_rows][dh/2] (cos, sin)
   float* lse_part = nullptr;           // [max_rows][V/128] float4
-  bool lm_tc = false;                  // LM head on the tcgen05 GEMM with the LSE epilogue (cuBLAS path)
-  bool tc_qkv = false, tc_gu = false;  // per-op tcgen05 (cuBLAS path, large row counts)
-  bool tc_o = false;                   // O-projection + residual on tcgen05 (cuBLAS path)
+  unsigned int* sched = nullptr;       // tcgen05 tile queue of this model's stream (self-resetting)
   int* amax = nullptr;
   float* lse = nullptr;
   float* lsum = nullptr;
@@ -323,10 +293,8 @@ static Model* make_model(const ModelShape& sh, bool prm, uint64_t seed, long lon
   const size_t M = max_rows;
   m->X = dalloc<float>(M * sh.d, o);
   m->Xn = dalloc<__nv_bfloat16>(M * std::max(sh.d, sh.H * sh.dh), o);
-  m->QKV = dalloc<__nv_bfloat16>(M * (sh.H + 2 * sh.KVH) * sh.dh, o);
   m->Qr = dalloc<float>(M * sh.H * sh.dh, o);
   m->O = dalloc<__nv_bfloat16>(M * sh.H * sh.dh, o);
-  m->GU = dalloc<__nv_bfloat16>(M * 2 * sh.F, o);
   m->A = dalloc<__nv_bfloat16>(M * sh.F, o);
   if (!prm) {
     m->amax = dalloc<int>(M, o);
@@ -334,89 +302,42 @@ static Model* make_model(const ModelShape& sh, bool prm, uint64_t seed, long lon
     m->lsum = dalloc<float>(M, o);
   }
   m->rope_tab = dalloc<float>(M * sh.dh, o);  // [max_rows][dh/2] (cos, sin)
-  // K2 on the hand-written tcgen05 GEMM with fused epilogues (gemm_tc.cu) is
-  // opt-in (SPEX_TC_GEMM=1): it is correct (tests/test_gemm_tc_gpu.py) and beats
-  // cuBLAS + the separate elementwise kernels per op at decode shapes, but over a
-  // whole search the cuBLAS path is faster (3.2 s vs 3.75 s on c2; small-M steps
-  // and the concurrent PRM stream), so cuBLAS stays the default.
+  // K2: every projection on the hand-written tcgen05 GEMM with fused epilogues
+  // (gemm_tc.cu): QKV + RoPE + KV append, O + residual, gate/up + SwiGLU,
+  // down + residual, LM head + logsumexp/argmax partials. No library GEMM.
   const int qkv_n = (sh.H + 2 * sh.KVH) * sh.dh;
-  m->use_tc = getenv("SPEX_TC_GEMM") != nullptr && sh.d % 128 == 0 && sh.d % 64 == 0 && qkv_n % 128 == 0 &&
-              (sh.H * sh.dh) % 64 == 0 && (2 * sh.F) % 128 == 0 && sh.F % 64 == 0 && (sh.dh == 64 || sh.dh == 128) &&
-              (prm || sh.V % 128 == 0);
-  if (m->use_tc) {
-    auto wmap = [&](TcWeight& w, const __nv_bfloat16* base, int N, int K) {
-      w.N = N;
-      w.K = K;
-      if (spex_tmap_operand(&w.map, base, N, K) != 0) m->use_tc = false;
-    };
-    m->tq.resize(sh.L);
-    m->to.resize(sh.L);
-    m->tgu.resize(sh.L);
-    m->td.resize(sh.L);
-    for (int l = 0; l < sh.L; ++l) {
-      m->wgu_il.push_back(dalloc<__nv_bfloat16>((size_t)2 * sh.F * sh.d, o));
-      spex_k_interleave_gu(m->wgu[l], sh.F, sh.d, m->wgu_il.back(), st);
-      wmap(m->tq[l], m->wqkv[l], qkv_n, sh.d);
-      wmap(m->to[l], m->wo[l], sh.d, sh.H * sh.dh);
-      wmap(m->tgu[l], m->wgu_il[l], 2 * sh.F, sh.d);
-      wmap(m->td[l], m->wd[l], sh.d, sh.F);
-    }
-    if (!prm) wmap(m->tlm, m->lm, sh.V, sh.d);
-    if (spex_tmap_operand(&m->a_xn, m->Xn, (long long)M, sh.d) || spex_tmap_operand(&m->a_o, m->O, (long long)M, sh.H * sh.dh) ||
-        spex_tmap_operand(&m->a_act, m->A, (long long)M, sh.F))
-      m->use_tc = false;
-    if (!prm) m->lse_part = dalloc<float>(M * (size_t)(sh.V / 128) * 4, o);
+  if (!(sh.d % 64 == 0 && qkv_n % 128 == 0 && (sh.H * sh.dh) % 64 == 0 && sh.F % 64 == 0 &&
+        (sh.dh == 64 || sh.dh == 128) && (prm || sh.V % 128 == 0)))
+    throw std::runtime_error("model shape not supported by the tcgen05 projections");
+  auto wmap = [&](TcWeight& w, const __nv_bfloat16* base, int N, int K) {
+    w.N = N;
+    w.K = K;
+    if (spex_tmap_operand(&w.map, base, N, K) != 0) throw std::runtime_error("TMA descriptor of a weight failed");
+  };
+  m->tq.resize(sh.L);
+  m->to.resize(sh.L);
+  m->tgu.resize(sh.L);
+  m->td.resize(sh.L);
+  for (int l = 0; l < sh.L; ++l) {
+    // gate/up rows interleaved per 64 for the SwiGLU epilogue (replaces the plain layout)
+    __nv_bfloat16* il = dalloc<__nv_bfloat16>((size_t)2 * sh.F * sh.d, o);
+    spex_k_interleave_gu(m->wgu[l], sh.F, sh.d, il, st);
+    CK(cudaStreamSynchronize(st));
+    o.erase(std::find(o.begin(), o.end(), static_cast<void*>(m->wgu[l])));
+    CK(cudaFree(m->wgu[l]));
+    m->wgu[l] = il;
+    wmap(m->tq[l], m->wqkv[l], qkv_n, sh.d);
+    wmap(m->to[l], m->wo[l], sh.d, sh.H * sh.dh);
+    wmap(m->tgu[l], m->wgu[l], 2 * sh.F, sh.d);
+    wmap(m->td[l], m->wd[l], sh.d, sh.F);
   }
-  if (!m->use_tc && !prm) m->logits = dalloc<float>(M * sh.V, o);
-  // Per-op tcgen05 on the cuBLAS path (policy decode, large row counts):
-  // QKV + RoPE/KV-append (SPEX_TC_QKV=1), gate/up + SwiGLU (SPEX_TC_GU=1)
-  if (!m->use_tc && !prm && sh.d % 64 == 0 && qkv_n % 128 == 0 && (sh.dh == 64 || sh.dh == 128) &&
-      spex_tmap_operand(&m->a_xn, m->Xn, (long long)M, sh.d) == 0) {
-    if (getenv("SPEX_TC_QKV")) {
-      m->tq.resize(sh.L);
-      m->tc_qkv = true;
-      for (int l = 0; l < sh.L; ++l) {
-        m->tq[l].N = qkv_n;
-        m->tq[l].K = sh.d;
-        if (spex_tmap_operand(&m->tq[l].map, m->wqkv[l], qkv_n, sh.d) != 0) m->tc_qkv = false;
-      }
-    }
-    // O-projection + residual (N = d) on tcgen05 (SPEX_TC_O=1): faster in
-    // isolation (M 2157 x N 1024 x K 1024: 12.4 us vs 17.1 us,
-    // profiles/r01v_gemm_tc_vs_cublas.txt) but 3% slower in the running search
-    // (profiles/r01z_tc_o_ab.txt), so cuBLAS stays the default.
-    if (getenv("SPEX_TC_O") && atoi(getenv("SPEX_TC_O")) != 0 && sh.d % 128 == 0 && (sh.H * sh.dh) % 64 == 0 &&
-        spex_tmap_operand(&m->a_o, m->O, (long long)M, sh.H * sh.dh) == 0) {
-      m->to.resize(sh.L);
-      m->tc_o = true;
-      for (int l = 0; l < sh.L; ++l) {
-        m->to[l].N = sh.d;
-        m->to[l].K = sh.H * sh.dh;
-        if (spex_tmap_operand(&m->to[l].map, m->wo[l], sh.d, sh.H * sh.dh) != 0) m->tc_o = false;
-      }
-    }
-    if (getenv("SPEX_TC_GU") && (2 * sh.F) % 128 == 0 && sh.F % 64 == 0) {
-      m->tgu.resize(sh.L);
-      m->tc_gu = true;
-      for (int l = 0; l < sh.L; ++l) {
-        m->wgu_il.push_back(dalloc<__nv_bfloat16>((size_t)2 * sh.F * sh.d, o));
-        spex_k_interleave_gu(m->wgu[l], sh.F, sh.d, m->wgu_il.back(), st);
-        m->tgu[l].N = 2 * sh.F;
-        m->tgu[l].K = sh.d;
-        if (spex_tmap_operand(&m->tgu[l].map, m->wgu_il[l], 2 * sh.F, sh.d) != 0) m->tc_gu = false;
-      }
-    }
-  }
-  // LM head + logsumexp/argmax fused on the tcgen05 GEMM (EPI_LSE) even on the
-  // cuBLAS path: the fp32 logits round trip (rows x V x 8 bytes) disappears
-  if (!m->use_tc && !prm && sh.V % 128 == 0 && sh.d % 64 == 0 && !getenv("SPEX_LM_CUBLAS")) {
-    m->tlm.N = sh.V;
-    m->tlm.K = sh.d;
-    if (spex_tmap_operand(&m->tlm.map, m->lm, sh.V, sh.d) == 0 && spex_tmap_operand(&m->a_xn, m->Xn, (long long)M, sh.d) == 0) {
-      m->lse_part = dalloc<float>(M * (size_t)(sh.V / 128) * 4, o);
-      m->lm_tc = true;
-    }
-  }
+  if (!prm) wmap(m->tlm, m->lm, sh.V, sh.d);
+  if (spex_tmap_operand(&m->a_xn, m->Xn, (long long)M, sh.d) || spex_tmap_operand(&m->a_o, m->O, (long long)M, sh.H * sh.dh) ||
+      spex_tmap_operand(&m->a_act, m->A, (long long)M, sh.F))
+    throw std::runtime_error("TMA descriptor of an activation failed");
+  if (!prm) m->lse_part = dalloc<float>(M * (size_t)(sh.V / 128) * 4, o);
+  m->sched = dalloc<unsigned int>(2, o);
+  CK(cudaMemsetAsync(m->sched, 0, 2 * sizeof(unsigned int), st));
   return m;
 }
 
@@ -445,172 +366,97 @@ static bool wmma_wanted(const ModelShape& s) {
   return mode == 1 || (mode == 2 && s.H / s.KVH >= 4);
 }
 
-constexpr int kTcMinRows = 1024;  // per-op tcgen05 below this row count loses to cuBLAS's small-M kernels
-
-static void tc_gemm(const CUtensorMap& a, const TcWeight& w, int M, const TcEpilogue& ep, cudaStream_t st) {
-  if (spex_k_gemm_tc(&a, &w.map, M, w.N, w.K, &ep, st) != 0) throw std::runtime_error("tcgen05 GEMM launch failed");
+static void tc_gemm(const CUtensorMap& a, const TcWeight& w, int M, const TcEpilogue& ep, unsigned int* sched,
+                    cudaStream_t st) {
+  const int rc = spex_k_gemm_tc(&a, &w.map, M, w.N, w.K, &ep, sched, st);
+  if (rc != 0) throw std::runtime_error("tcgen05 GEMM launch failed (" + std::to_string(rc) + ")");
 }
 
-// One forward over M rows. K1 launches are bracketed by events when `attn_ev`
-// is given, accumulating their device time into *attn_ms.
-static long long g_launches = 0, g_gemms = 0;
-
-static void forward(Model& m, const RowDesc* rows, const Segment* segs, int M, cublasHandle_t hb,
-                    cudaStream_t st, AttnTimer* timer, const TileDesc* tiles = nullptr, int ntiles = 0,
-                    const DecodeChunks* chunks = nullptr, const TreeGroups* groups = nullptr) {
+// K1 for one layer: PRM / prompt tiles on the TMA + tensor-core tile kernel;
+// decode rows on the per-warp TMA pipeline (GQA groups), the bulk-copy
+// pipeline (one KV head per query head) or the register pipeline (other shapes).
+static void attention(Model& m, int l, const RowDesc* rows, const Segment* segs, int M, const TileDesc* tiles,
+                      int ntiles, const DecodeChunks* chunks, const TreeGroups* groups, cudaStream_t st) {
   const ModelShape& s = m.sh;
-  if (m.use_tc) {
-    // embed -> L x [RMSNorm, QKV+RoPE+KV-append (tcgen05), K1, O-proj + residual
-    // (tcgen05), RMSNorm, gate/up + SwiGLU (tcgen05), down + residual (tcgen05)]
-    // -> RMSNorm -> LM head + logsumexp/argmax partials (tcgen05) -> combine
-    g_launches += 3 + 7LL * s.L + (m.is_prm ? 0 : 2);
-    spex_k_rope_table(rows, M, m.inv_freq, s.dh / 2, m.rope_tab, st);
-    spex_k_embed(rows, M, m.embed, s.d, m.X, st);
-    TcEpilogue eq{};
-    eq.kind = TC_EPI_ROPE_KV;
-    eq.rows = rows;
-    eq.rope = m.rope_tab;
-    eq.H = s.H;
-    eq.KVH = s.KVH;
-    eq.dh = s.dh;
-    eq.qscale = 1.0f / std::sqrt((float)s.dh);
-    eq.Qr = m.Qr;
-    eq.slots = m.slots;
-    TcEpilogue er{};
-    er.kind = TC_EPI_STORE;
-    er.y = m.X;
-    er.ldy = s.d;
-    er.accumulate = 1;
-    TcEpilogue eg{};
-    eg.kind = TC_EPI_SWIGLU;
-    eg.act = m.A;
-    eg.F = s.F;
-    for (int l = 0; l < s.L; ++l) {
-      spex_k_rmsnorm(m.X, M, s.d, s.eps, m.Xn, st);
-      eq.Kp = m.Kp[l];
-      eq.Vp = m.Vp[l];
-      tc_gemm(m.a_xn, m.tq[l], M, eq, st);
-      if (timer) timer->begin(st);
-      int rc = -1;
-      if (tiles && !m.kmap.empty())
-        rc = spex_k_tree_attn_tiles_mma(&m.kmap[l], &m.vmap[l], tiles, ntiles, rows, segs, m.Qr, s.H, s.KVH, s.dh,
-                                        m.slots, m.O, st);
-      if (rc != 0 && !tiles && !m.kmap.empty() && decode_mma_wanted(s))
-        rc = spex_k_tree_attn_decode_mma(&m.kmap[l], &m.vmap[l], rows, segs, m.Qr, s.H, s.KVH, s.dh, m.slots, m.O, M,
-                                         st);
-      if (rc != 0 && chunks)
-        rc = spex_k_tree_attn_chunked(rows, segs, m.Qr, s.H, s.KVH, s.dh, m.Kp[l], m.Vp[l], m.slots, m.O, *chunks, l,
-                                      st);
-      if (rc != 0)
-        rc = tiles ? spex_k_tree_attn_tiles(tiles, ntiles, rows, segs, m.Qr, s.H, s.KVH, s.dh, m.Kp[l], m.Vp[l],
-                                            m.slots, m.O, st)
-                   : spex_k_tree_attn(rows, segs, m.Qr, s.H, s.KVH, s.dh, m.Kp[l], m.Vp[l], m.slots, m.O, M, st);
-      if (rc != 0) throw std::runtime_error("tree attention: unsupported head shape");
-      if (timer) timer->end(st);
-      tc_gemm(m.a_o, m.to[l], M, er, st);
-      spex_k_rmsnorm(m.X, M, s.d, s.eps, m.Xn, st);
-      tc_gemm(m.a_xn, m.tgu[l], M, eg, st);
-      tc_gemm(m.a_act, m.td[l], M, er, st);
-    }
-    spex_k_rmsnorm(m.X, M, s.d, s.eps, m.Xn, st);
-    if (!m.is_prm) {
-      TcEpilogue el{};
-      el.kind = TC_EPI_LSE;
-      el.part = m.lse_part;
-      el.n_tiles = s.V / 128;
-      el.V = s.V;
-      tc_gemm(m.a_xn, m.tlm, M, el, st);
-      spex_k_lse_combine(m.lse_part, M, s.V / 128, m.amax, m.lse, m.lsum, st);
-    }
-    return;
-  }
-  g_launches += 3 + 5LL * s.L + (m.is_prm ? 0 : 1);
-  g_gemms += 4LL * s.L + (m.is_prm ? 0 : 1);
+  int rc = -1;
+  if (tiles && !m.kmap.empty())
+    rc = spex_k_tree_attn_tiles_mma(&m.kmap[l], &m.vmap[l], tiles, ntiles, rows, segs, m.Qr, s.H, s.KVH, s.dh,
+                                    m.slots, m.O, st);
+  if (rc != 0 && !tiles && groups && !m.kmap16.empty() && g_item_ctr)
+    rc = spex_k_tree_attn_group(&m.kmap16[l], &m.vmap16[l], groups, m.Qr, s.H, s.KVH, s.dh, m.slots, m.O, M,
+                                g_item_ctr, st);
+  if (rc != 0 && !tiles && !m.kmap16.empty() && wmma_wanted(s) && g_item_ctr)
+    rc = spex_k_tree_attn_wmma(&m.kmap16[l], &m.vmap16[l], rows, segs, m.Qr, s.H, s.KVH, s.dh, m.slots, m.O, M,
+                               g_item_ctr, st);
+  if (rc != 0 && !tiles && !m.kmap.empty() && decode_mma_wanted(s))
+    rc = spex_k_tree_attn_decode_mma(&m.kmap[l], &m.vmap[l], rows, segs, m.Qr, s.H, s.KVH, s.dh, m.slots, m.O, M,
+                                     st);
+  if (rc != 0 && !tiles && bulk_wanted() && g_item_ctr)
+    rc = spex_k_tree_attn_bulk(rows, segs, m.Qr, s.H, s.KVH, s.dh, m.Kp[l], m.Vp[l], m.slots, m.O, M, g_item_ctr, st);
+  if (rc != 0 && chunks)
+    rc = spex_k_tree_attn_chunked(rows, segs, m.Qr, s.H, s.KVH, s.dh, m.Kp[l], m.Vp[l], m.slots, m.O, *chunks, l, st);
+  if (rc != 0)
+    rc = tiles ? spex_k_tree_attn_tiles(tiles, ntiles, rows, segs, m.Qr, s.H, s.KVH, s.dh, m.Kp[l], m.Vp[l], m.slots,
+                                        m.O, st)
+               : spex_k_tree_attn(rows, segs, m.Qr, s.H, s.KVH, s.dh, m.Kp[l], m.Vp[l], m.slots, m.O, M, st);
+  if (rc != 0) throw std::runtime_error("tree attention: unsupported head shape");
+}
+
+// One forward over M rows. K1 launches are bracketed by events when `timer`
+// is given, accumulating their device time.
+static long long g_launches = 0;
+
+static void forward(Model& m, const RowDesc* rows, const Segment* segs, int M, cudaStream_t st, AttnTimer* timer,
+                    const TileDesc* tiles = nullptr, int ntiles = 0, const DecodeChunks* chunks = nullptr,
+                    const TreeGroups* groups = nullptr) {
+  const ModelShape& s = m.sh;
+  // embed -> L x [RMSNorm, QKV + RoPE + KV append (tcgen05), K1, O + residual
+  // (tcgen05), RMSNorm, gate/up + SwiGLU (tcgen05), down + residual (tcgen05)]
+  // -> RMSNorm -> LM head + logsumexp/argmax partials (tcgen05) -> combine
+  g_launches += 3 + 7LL * s.L + (m.is_prm ? 0 : 2);
   spex_k_rope_table(rows, M, m.inv_freq, s.dh / 2, m.rope_tab, st);  // (cos, sin) once for all layers
   spex_k_embed(rows, M, m.embed, s.d, m.X, st);
+  TcEpilogue eq{};
+  eq.kind = TC_EPI_ROPE_KV;
+  eq.rows = rows;
+  eq.rope = m.rope_tab;
+  eq.H = s.H;
+  eq.KVH = s.KVH;
+  eq.dh = s.dh;
+  eq.qscale = 1.0f / std::sqrt((float)s.dh);
+  eq.Qr = m.Qr;
+  eq.slots = m.slots;
+  TcEpilogue er{};
+  er.kind = TC_EPI_STORE;
+  er.y = m.X;
+  er.ldy = s.d;
+  er.accumulate = 1;
+  TcEpilogue eg{};
+  eg.kind = TC_EPI_SWIGLU;
+  eg.act = m.A;
+  eg.F = s.F;
   for (int l = 0; l < s.L; ++l) {
     spex_k_rmsnorm(m.X, M, s.d, s.eps, m.Xn, st);
-    if (m.tc_qkv && M >= kTcMinRows) {
-      TcEpilogue eq{};
-      eq.kind = TC_EPI_ROPE_KV;
-      eq.rows = rows;
-      eq.rope = m.rope_tab;
-      eq.H = s.H;
-      eq.KVH = s.KVH;
-      eq.dh = s.dh;
-      eq.qscale = 1.0f / std::sqrt((float)s.dh);
-      eq.Qr = m.Qr;
-      eq.Kp = m.Kp[l];
-      eq.Vp = m.Vp[l];
-      eq.slots = m.slots;
-      tc_gemm(m.a_xn, m.tq[l], M, eq, st);
-    } else {
-      gemm_bf16out(hb, m.Xn, m.wqkv[l], m.QKV, M, (s.H + 2 * s.KVH) * s.dh, s.d);
-      spex_k_rope_kv(rows, M, m.QKV, s.H, s.KVH, s.dh, m.rope_tab, m.slots, m.Kp[l], m.Vp[l], m.Qr, st);
-    }
+    eq.Kp = m.Kp[l];
+    eq.Vp = m.Vp[l];
+    tc_gemm(m.a_xn, m.tq[l], M, eq, m.sched, st);
     if (timer) timer->begin(st);
-    int rc = -1;
-    if (tiles && !m.kmap.empty())
-      rc = spex_k_tree_attn_tiles_mma(&m.kmap[l], &m.vmap[l], tiles, ntiles, rows, segs, m.Qr, s.H, s.KVH, s.dh,
-                                      m.slots, m.O, st);
-    if (rc != 0 && !tiles && groups && !m.kmap16.empty() && g_item_ctr)
-      rc = spex_k_tree_attn_group(&m.kmap16[l], &m.vmap16[l], groups, m.Qr, s.H, s.KVH, s.dh, m.slots, m.O, M,
-                                  g_item_ctr, st);
-    if (rc != 0 && !tiles && !m.kmap16.empty() && wmma_wanted(s) && g_item_ctr)
-      rc = spex_k_tree_attn_wmma(&m.kmap16[l], &m.vmap16[l], rows, segs, m.Qr, s.H, s.KVH, s.dh, m.slots, m.O, M,
-                                 g_item_ctr, st);
-    if (rc != 0 && !tiles && !m.kmap.empty() && decode_mma_wanted(s))
-      rc = spex_k_tree_attn_decode_mma(&m.kmap[l], &m.vmap[l], rows, segs, m.Qr, s.H, s.KVH, s.dh, m.slots, m.O, M,
-                                       st);
-    if (rc != 0 && !tiles && bulk_wanted() && g_item_ctr)
-      rc = spex_k_tree_attn_bulk(rows, segs, m.Qr, s.H, s.KVH, s.dh, m.Kp[l], m.Vp[l], m.slots, m.O, M, g_item_ctr,
-                                 st);
-    if (rc != 0 && chunks)
-      rc = spex_k_tree_attn_chunked(rows, segs, m.Qr, s.H, s.KVH, s.dh, m.Kp[l], m.Vp[l], m.slots, m.O, *chunks, l,
-                                    st);
-    if (rc != 0)
-      rc = tiles ? spex_k_tree_attn_tiles(tiles, ntiles, rows, segs, m.Qr, s.H, s.KVH, s.dh, m.Kp[l],
-                                                  m.Vp[l], m.slots, m.O, st)
-                         : spex_k_tree_attn(rows, segs, m.Qr, s.H, s.KVH, s.dh, m.Kp[l], m.Vp[l], m.slots, m.O, M, st);
-    if (rc != 0) throw std::runtime_error("tree attention: unsupported head shape");
+    attention(m, l, rows, segs, M, tiles, ntiles, chunks, groups, st);
     if (timer) timer->end(st);
-    if (m.tc_o && M >= 512) {
-      TcEpilogue er{};
-      er.kind = TC_EPI_STORE;
-      er.y = m.X;
-      er.ldy = s.d;
-      er.accumulate = 1;
-      tc_gemm(m.a_o, m.to[l], M, er, st);
-    } else {
-      gemm(hb, m.O, m.wo[l], m.X, M, s.d, s.H * s.dh, true);
-    }
+    tc_gemm(m.a_o, m.to[l], M, er, m.sched, st);
     spex_k_rmsnorm(m.X, M, s.d, s.eps, m.Xn, st);
-    if (m.tc_gu && M >= kTcMinRows) {
-      TcEpilogue eg{};
-      eg.kind = TC_EPI_SWIGLU;
-      eg.act = m.A;
-      eg.F = s.F;
-      tc_gemm(m.a_xn, m.tgu[l], M, eg, st);
-    } else {
-      gemm_bf16out(hb, m.Xn, m.wgu[l], m.GU, M, 2 * s.F, s.d);
-      spex_k_swiglu(m.GU, M, s.F, m.A, st);
-    }
-    gemm(hb, m.A, m.wd[l], m.X, M, s.d, s.F, true);
+    tc_gemm(m.a_xn, m.tgu[l], M, eg, m.sched, st);
+    tc_gemm(m.a_act, m.td[l], M, er, m.sched, st);
   }
   spex_k_rmsnorm(m.X, M, s.d, s.eps, m.Xn, st);
   if (!m.is_prm) {
-    if (m.lm_tc) {
-      TcEpilogue el{};
-      el.kind = TC_EPI_LSE;
-      el.part = m.lse_part;
-      el.n_tiles = s.V / 128;
-      el.V = s.V;
-      tc_gemm(m.a_xn, m.tlm, M, el, st);
-      spex_k_lse_combine(m.lse_part, M, s.V / 128, m.amax, m.lse, m.lsum, st);
-    } else {
-      gemm(hb, m.Xn, m.lm, m.logits, M, s.V, s.d, false);
-      spex_k_lm_epilogue(m.logits, M, s.V, m.amax, m.lse, m.lsum, st);
-    }
+    TcEpilogue el{};
+    el.kind = TC_EPI_LSE;
+    el.part = m.lse_part;
+    el.n_tiles = s.V / 128;
+    el.V = s.V;
+    tc_gemm(m.a_xn, m.tlm, M, el, m.sched, st);
+    spex_k_lse_combine(m.lse_part, M, s.V / 128, m.amax, m.lse, m.lsum, st);
   }
 }
 
@@ -671,7 +517,6 @@ struct ModelCache {
   Model* pol = nullptr;
   Model* prm = nullptr;
   unsigned long long seed = 0;
-  cublasHandle_t hb = nullptr;
   // replay row buffers (kept resident: no cudaMalloc while the control kernel runs)
   int rows_cap = 0;
   RowDesc* rows = nullptr;
@@ -679,10 +524,9 @@ struct ModelCache {
   int* last_row = nullptr;
   TileDesc* tiles = nullptr;
   float* scores = nullptr;
-  // PRM side: its own stream, cuBLAS handle and row buffers, so reward scoring
+  // PRM side: its own stream and row buffers, so reward scoring
   // (tensor-bound prefill GEMMs) overlaps the policy decode (HBM-bound K1)
   cudaStream_t st2 = nullptr;
-  cublasHandle_t hb2 = nullptr;
   RowDesc* rows2 = nullptr;
   Segment* segs2 = nullptr;
   TileDesc* tiles2 = nullptr;
@@ -822,26 +666,10 @@ void run_model_schedule(const ModelRunConfig& mc, const ScheduleView& sv, ModelR
   const int prompt_chunk = std::max(1, std::min(Q, 4096 / std::max(P, 1)));
   const long long slots = std::max<long long>(sv.kv_slots, 1);
 
-  if (!g_cache.hb) {
-    CB(cublasCreate(&g_cache.hb));
-    void* ws = nullptr;
-    CK(cudaMalloc(&ws, 64 << 20));  // fixed workspace: no lazy allocation while streaming
-    CB(cublasSetWorkspace(g_cache.hb, ws, 64 << 20));
-    CB(cublasCreate(&g_cache.hb2));
-    void* ws2 = nullptr;
-    CK(cudaMalloc(&ws2, 64 << 20));
-    CB(cublasSetWorkspace(g_cache.hb2, ws2, 64 << 20));
-    CK(cudaStreamCreateWithFlags(&g_cache.st2, cudaStreamNonBlocking));
-  }
-  cublasHandle_t hb = g_cache.hb;
-  CB(cublasSetStream(hb, st));
-  CB(cublasSetMathMode(hb, CUBLAS_DEFAULT_MATH));
+  if (!g_cache.st2) CK(cudaStreamCreateWithFlags(&g_cache.st2, cudaStreamNonBlocking));
   // PRM stream: same device, ordered after everything already queued on st
   const bool prm_overlap = !std::getenv("SPEX_PRM_SAME_STREAM");
   cudaStream_t st2 = prm_overlap ? g_cache.st2 : st;
-  cublasHandle_t hb2 = prm_overlap ? g_cache.hb2 : hb;
-  CB(cublasSetStream(hb2, st2));
-  CB(cublasSetMathMode(hb2, CUBLAS_DEFAULT_MATH));
   if (g_cache.seed != mc.seed) spex_model_cache_clear();
   Model* pol = cached(g_cache.pol, mc.policy, false, mc.seed, slots, std::max(max_dec, prompt_chunk * P), st);
   Model* prm = mc.with_prm ? cached(g_cache.prm, mc.prm, true, mc.seed, slots, std::max(max_prm, prompt_chunk * P), st)
@@ -918,8 +746,7 @@ void run_model_schedule(const ModelRunConfig& mc, const ScheduleView& sv, ModelR
   cudaEventRecord(e_fork, st);  // weights / pools initialised on st
   if (st2 != st) CK(cudaStreamWaitEvent(st2, e_fork, 0));
   g_launches = 0;
-  g_gemms = 0;
-  if (P > 0) {
+    if (P > 0) {
     const int q_end = std::min(sv.shard_hi, Q);
     for (int q0 = sv.shard_lo; q0 < q_end; q0 += prompt_chunk) {
       const int nq = std::min(prompt_chunk, q_end - q0);
@@ -927,12 +754,12 @@ void run_model_schedule(const ModelRunConfig& mc, const ScheduleView& sv, ModelR
       spex_k_build_prompt_rows(tv_pol, q0, nq, rows, segs, st);
       spex_k_build_prompt_tiles(nq, P, tiles, st);
       g_launches += 2;
-      forward(*pol, rows, segs, nq * P, hb, st, nullptr, tiles, ntp);
+      forward(*pol, rows, segs, nq * P, st, nullptr, tiles, ntp);
       if (prm) {
         spex_k_build_prompt_rows(tv_prm, q0, nq, rows2, segs2, st2);
         spex_k_build_prompt_tiles(nq, P, tiles2, st2);
         g_launches += 2;
-        forward(*prm, rows2, segs2, nq * P, hb2, st2, nullptr, tiles2, ntp);
+        forward(*prm, rows2, segs2, nq * P, st2, nullptr, tiles2, ntp);
       }
       res->prefill_rows += (long long)nq * P;
     }
@@ -965,7 +792,7 @@ void run_model_schedule(const ModelRunConfig& mc, const ScheduleView& sv, ModelR
           timer.cur_bytes = ((double)pe.u0 + (double)s * pe.n + pe.n) * kv_tok_bytes * ((double)n / pe.n) +
                             (double)n * mc.policy.H * mc.policy.dh * (4.0 + 2.0);
           if (chunked) spex_k_build_decode_chunks(rows, segs, n, g_cache.dc, st);
-          forward(*pol, rows, segs, n, hb, st, mc.time_attn ? &timer : nullptr, nullptr, 0,
+          forward(*pol, rows, segs, n, st, mc.time_attn ? &timer : nullptr, nullptr, 0,
                   chunked ? &g_cache.dc : nullptr, grouped ? &g_cache.tg : nullptr);
           spex_k1_set_row_order(nullptr);  // read at launch: other callers get row order
           if (dbg && dbg_n + n <= mc.out_rows_cap) {
@@ -984,7 +811,7 @@ void run_model_schedule(const ModelRunConfig& mc, const ScheduleView& sv, ModelR
       if (pe.rows > max_prm) throw std::runtime_error("PRM batch larger than the row buffers");
       spex_k_build_prm_rows(tv_prm, sv.srow_sid + pe.off, sv.srow_rstart + pe.off, sv.srow_tstart + pe.off, pe.n,
                             rows2, segs2, last_row, tiles2, st2);
-      forward(*prm, rows2, segs2, pe.rows, hb2, st2, nullptr, tiles2, pe.tiles);
+      forward(*prm, rows2, segs2, pe.rows, st2, nullptr, tiles2, pe.tiles);
       spex_k_value_head(prm->Xn, mc.prm.d, last_row, pe.n, prm->vhead, scores, st2);
       g_launches += 2;
       if (dbg_scores && dbg_s + pe.n <= mc.out_scores_cap) {
@@ -1044,7 +871,7 @@ void run_model_schedule(const ModelRunConfig& mc, const ScheduleView& sv, ModelR
   res->attn_ms = timer.total_ms;
   res->attn_launches = timer.launches;
   res->launches = g_launches;
-  res->gemm_calls = g_gemms;
+  res->gemm_calls = 0;  // no library GEMMs: every projection is on the tcgen05 kernel
   res->out_rows = dbg_n;
   res->out_scores = dbg_s;
   res->policy_flops = model_matmul_flops_per_row(mc.policy, false) * (double)(res->decode_rows + res->prefill_rows);

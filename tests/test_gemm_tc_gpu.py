@@ -50,7 +50,11 @@ def _lib():
     lib.spex_tmap_operand.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_longlong, ctypes.c_longlong]
     lib.spex_k_gemm_tc.restype = ctypes.c_int
     lib.spex_k_gemm_tc.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
-                                   ctypes.POINTER(TcEpilogue), ctypes.c_void_p]
+                                   ctypes.POINTER(TcEpilogue), ctypes.c_void_p, ctypes.c_void_p]
+    lib.spex_k_gemm_tc_ex.restype = ctypes.c_int
+    lib.spex_k_gemm_tc_ex.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                      ctypes.POINTER(TcEpilogue), ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
+                                      ctypes.c_void_p]
     lib.spex_k_lse_combine.restype = None
     lib.spex_k_lse_combine.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_void_p,
                                        ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
@@ -67,13 +71,27 @@ def _maps(lib, x, w):
     return a, b
 
 
-def _run(lib, x, w, ep):
+# tile shapes (cta_group, BN): (0, 0) = the launcher's choice; 2 = CTA pair (UMMA M=256)
+TILES = [(0, 0), (2, 256), (2, 128), (1, 256), (1, 128)]
+_sched = None
+
+
+def _run(lib, x, w, ep, tile=(0, 0), dynamic=True):
+    """One GEMM; `dynamic` uses the self-resetting device tile queue (run twice
+    to check the reset), else the static round-robin schedule."""
     import torch
+    global _sched
+    if _sched is None:
+        _sched = torch.zeros(2, dtype=torch.int32, device="cuda")
     a, b = _maps(lib, x, w)
     st = torch.cuda.current_stream()
-    rc = lib.spex_k_gemm_tc(a.ptr, b.ptr, x.shape[0], w.shape[0], x.shape[1], ctypes.byref(ep), st.cuda_stream)
-    assert rc == 0
+    for _ in range(2 if dynamic else 1):
+        rc = lib.spex_k_gemm_tc_ex(a.ptr, b.ptr, x.shape[0], w.shape[0], x.shape[1], ctypes.byref(ep),
+                                   _sched.data_ptr() if dynamic else None, tile[0], tile[1], st.cuda_stream)
+        assert rc == 0, rc
     torch.cuda.synchronize()
+    if dynamic:
+        assert _sched.tolist() == [0, 0]  # the queue reset itself
 
 
 def _rand(*shape, scale=1.0, seed=0):
@@ -82,22 +100,25 @@ def _rand(*shape, scale=1.0, seed=0):
     return (torch.randn(*shape, generator=g) * scale).to(torch.bfloat16).cuda()
 
 
-@pytest.mark.parametrize("M,N,K", [(300, 256, 192), (128, 128, 64), (2157, 1024, 1024), (77, 384, 2816)])
+@pytest.mark.parametrize("M,N,K", [(300, 256, 192), (128, 128, 64), (2157, 1024, 1024), (77, 384, 2816),
+                                   (1000, 640, 512)])
 @pytest.mark.parametrize("accumulate", [0, 1])
-def test_store(M, N, K, accumulate):
+@pytest.mark.parametrize("tile", TILES + [(1, 64)])
+def test_store(M, N, K, accumulate, tile):
     import torch
     lib = _lib()
     x, w = _rand(M, K, seed=1), _rand(N, K, scale=K ** -0.5, seed=2)
     y0 = torch.randn(M, N, device="cuda")
     y = y0.clone()
     ep = TcEpilogue(kind=EPI_STORE, y=y.data_ptr(), ldy=N, accumulate=accumulate)
-    _run(lib, x, w, ep)
+    _run(lib, x, w, ep, tile, dynamic=not accumulate)  # accumulate: one launch (y += once)
     ref = x.float() @ w.float().T + (y0 if accumulate else 0)
     err = ((y - ref).abs() / (1 + ref.abs())).max().item()
     assert err <= 2e-3, err
 
 
-def test_swiglu_interleaved():
+@pytest.mark.parametrize("tile", TILES)
+def test_swiglu_interleaved(tile):
     import torch
     lib = _lib()
     M, d, F = 333, 512, 1408
@@ -109,15 +130,16 @@ def test_swiglu_interleaved():
         il[128 * j + 64:128 * j + 128] = wu[64 * j:64 * j + 64]
     act = torch.zeros(M, F, dtype=torch.bfloat16, device="cuda")
     ep = TcEpilogue(kind=EPI_SWIGLU, act=act.data_ptr(), F=F)
-    _run(lib, x, il, ep)
+    _run(lib, x, il, ep, tile)
     g, u = x.float() @ wg.float().T, x.float() @ wu.float().T
     ref = torch.nn.functional.silu(g) * u
     err = ((act.float() - ref).abs() / (1 + ref.abs())).max().item()
     assert err <= 2e-2, err
 
 
-@pytest.mark.parametrize("H,KVH,dh", [(8, 8, 128), (4, 2, 64), (2, 2, 64)])
-def test_rope_kv(H, KVH, dh):
+@pytest.mark.parametrize("H,KVH,dh", [(8, 8, 128), (4, 2, 64), (2, 2, 64), (12, 2, 128)])
+@pytest.mark.parametrize("tile", TILES)
+def test_rope_kv(H, KVH, dh, tile):
     import torch
     lib = _lib()
     M, d, slots = 261, 256, 4096
@@ -138,7 +160,7 @@ def test_rope_kv(H, KVH, dh):
     Vp = torch.zeros(KVH, slots, dh, dtype=torch.bfloat16, device="cuda")
     ep = TcEpilogue(kind=EPI_ROPE_KV, rows=rows_d.data_ptr(), rope=rope.data_ptr(), H=H, KVH=KVH, dh=dh,
                     qscale=dh ** -0.5, Qr=Qr.data_ptr(), Kp=Kp.data_ptr(), Vp=Vp.data_ptr(), slots=slots)
-    _run(lib, x, w, ep)
+    _run(lib, x, w, ep, tile)
     y = (x.float() @ w.float().T).view(M, H + 2 * KVH, dh)
     pos = torch.from_numpy(rows["abs_pos"].astype(np.float64)).cuda()
     ang = pos[:, None] * inv_freq.double()[None, :]
@@ -156,15 +178,16 @@ def test_rope_kv(H, KVH, dh):
     assert ((vg - v_ref).abs() / (1 + v_ref.abs())).max().item() <= 2e-2
 
 
-@pytest.mark.parametrize("M,V,d", [(300, 512, 256), (129, 32000, 1024)])
-def test_lse_argmax(M, V, d):
+@pytest.mark.parametrize("M,V,d", [(300, 512, 256), (129, 32000, 1024), (515, 128256, 256)])
+@pytest.mark.parametrize("tile", TILES)
+def test_lse_argmax(M, V, d, tile):
     import torch
     lib = _lib()
     x, w = _rand(M, d, seed=8), _rand(V, d, scale=2.0 * d ** -0.5, seed=9)
     nt = V // 128
     part = torch.zeros(M, nt, 4, device="cuda")
     ep = TcEpilogue(kind=EPI_LSE, part=part.data_ptr(), n_tiles=nt, V=V)
-    _run(lib, x, w, ep)
+    _run(lib, x, w, ep, tile)
     amax = torch.zeros(M, dtype=torch.int32, device="cuda")
     lse = torch.zeros(M, device="cuda")
     lsum = torch.zeros(M, device="cuda")

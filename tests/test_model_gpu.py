@@ -19,22 +19,7 @@ pytestmark = pytest.mark.gpu
 ROOT = Path(__file__).resolve().parents[1]
 
 
-@pytest.fixture(params=["cublas", "tcgen05"])
-def k2_path(request):
-    """K2 projections on cuBLAS (default) or on the hand-written tcgen05 GEMM
-    with fused epilogues (SPEX_TC_GEMM=1); the model cache is rebuilt."""
-    import os
-    from paper_2605_10195_b200 import _lib as L
-    lib = L.lib()
-    if request.param == "tcgen05":
-        os.environ["SPEX_TC_GEMM"] = "1"
-    lib.spex_model_cache_clear()
-    yield request.param
-    os.environ.pop("SPEX_TC_GEMM", None)
-    lib.spex_model_cache_clear()
-
-
-def test_small_model_matches_numpy_oracle(k2_path):
+def test_small_model_matches_numpy_oracle():
     import paper_2605_10195_b200 as spex
     from oracle import model_ref
     if not spex.device_ok():
@@ -75,7 +60,7 @@ def test_small_model_matches_numpy_oracle(k2_path):
     print("worst abs errors", worst)
 
 
-def test_mid_model_tensor_core_paths_match_numpy_oracle(k2_path):
+def test_mid_model_tensor_core_paths_match_numpy_oracle():
     """dh=128 shapes: PRM/prompt rows go through the TMA + mma.sync tile kernel,
     decode rows through the streaming decode kernel."""
     import paper_2605_10195_b200 as spex

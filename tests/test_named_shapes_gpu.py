@@ -1,0 +1,98 @@
+"""Model numerics on the benchmarked searches vs the fp32 oracle
+(oracle/model_ref_torch.py, itself pinned to oracle/model_ref.py by
+tests/test_model_oracle_cpu.py), at north_star's stated tolerance:
+
+  logsumexp  |d| <= 1e-3 * max(1, |lse|)        (1e-3 relative)
+  PRM score  |d| <= 1e-3 * |score|               (1e-3 relative)
+  argmax     equal, unless the oracle's top-2 logits are within 1e-3 * max(1, |top|)
+  logit sum  |d| <= 1e-3 * sum |z|               (a sum of V fp32 logits)
+
+Config 5 with the named shapes (Llama-3-8B-shaped policy, 1.5B-shaped PRM):
+50 decode rows and 50 PRM scores sampled over the whole search. Config 2 (the
+bench workload, mid shapes): the same sample sizes. The oracle recomputes each
+sampled row by a full causal fp32 forward over its root -> node token sequence
+rebuilt from the event log; parity against the reference itself is unpinned
+(the reference has no model).
+"""
+import json
+import random
+from collections import defaultdict
+from pathlib import Path
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = Path(__file__).resolve().parents[1]
+TOL = 1e-3
+
+
+def _search(cfgname, policy, prm, wseed):
+    import paper_2605_10195_b200 as spex
+    from paper_2605_10195_b200 import _lib as L
+    if not spex.device_ok():
+        pytest.fail("no sm_100 device: the B200 path has no fallback")
+    cfg = (ROOT / "configs" / f"{cfgname}.json").read_text()
+    seed = json.loads(cfg)["run"]["seed"]
+    ex = spex.Executor(cfg, seed, None, trace=True)
+    ex.set_model(policy, prm, weight_seed=wseed, record_outputs=True)
+    ex.run()
+    log, dec, scores, ms = ex.log_lines(), ex.decode_outputs(), ex.prm_outputs(), ex.model_stats()
+    ex.close()
+    L.lib().spex_model_cache_clear()  # free the device weights / KV pools for the oracle
+    assert ms["decode_rows"] == len(dec) > 0 and ms["prm_thoughts"] == len(scores) > 0
+    return log, dec, scores
+
+
+def _check(cfgname, policy, prm, wseed, n_rows=50, n_scores=50):
+    import torch
+    from oracle import model_ref, model_ref_torch
+    torch.backends.cuda.matmul.allow_tf32 = False
+    torch.backends.cudnn.allow_tf32 = False
+    log, dec, scores = _search(cfgname, policy, prm, wseed)
+    tree = model_ref.TreeFromLog(log, prompt_tokens=32)
+    rng = random.Random(1234)
+    worst = {"lse_rel": 0.0, "prm_rel": 0.0}
+    # decode rows: 25 thoughts, 2 positions each (one forward per thought)
+    by_node = defaultdict(list)
+    for r in dec:
+        by_node[(r[0], r[1])].append(r)
+    nodes = rng.sample(sorted(by_node), min(len(by_node), n_rows // 2))
+    pol = model_ref_torch.Model(policy, wseed, prm=False, device="cuda")
+    for (q, node) in nodes:
+        rows = rng.sample(by_node[(q, node)], min(2, len(by_node[(q, node)])))
+        top = max(r[2] for r in rows)
+        toks = tree.sequence(q, node, top, pol.V)
+        base = len(toks) - 1 - top
+        am, lse, lsum, gap = pol.logits_stats_all(toks, [base + r[2] for r in rows])
+        z_abs = None
+        for i, (_, _, pos, amax, got_lse, got_sum) in enumerate(rows):
+            rel = abs(got_lse - lse[i]) / max(1.0, abs(lse[i]))
+            worst["lse_rel"] = max(worst["lse_rel"], rel)
+            assert rel <= TOL, (q, node, pos, lse[i], got_lse)
+            if amax != am[i]:
+                assert gap[i] <= TOL * max(1.0, abs(lse[i])), (q, node, pos, am[i], amax, gap[i])
+            if z_abs is None:
+                h = pol.forward(toks)[base + pos]
+                z_abs = float((h @ pol.lm.to(torch.float32).T).abs().sum())
+            assert abs(got_sum - lsum[i]) <= TOL * z_abs, (q, node, pos, lsum[i], got_sum)
+    del pol
+    torch.cuda.empty_cache()
+    rm = model_ref_torch.Model(prm, wseed ^ model_ref.PRM_SEED_XOR, prm=True, device="cuda")
+    for (q, node, score) in rng.sample(scores, min(n_scores, len(scores))):
+        n = tree.nodes[(q, node)][2]
+        ref = rm.prm_score(tree.sequence(q, node, n - 1, rm.V))
+        rel = abs(score - ref) / abs(ref)
+        worst["prm_rel"] = max(worst["prm_rel"], rel)
+        assert rel <= TOL, (q, node, ref, score)
+    del rm
+    torch.cuda.empty_cache()
+    print(cfgname, policy, prm, "worst relative errors", worst)
+    return worst
+
+
+def test_named_shapes_config5_match_fp32_oracle():
+    _check("c5_rebase_w32_q64", "llama3_8b", "prm_1p5b", 1)
+
+
+def test_bench_config2_mid_shapes_match_fp32_oracle():
+    _check("c2_rebase_w16_q256", "mid_policy", "mid_prm", 1)

@@ -1,0 +1,3 @@
+timeout -s KILL 600 python -m pytest tests/test_gemm_tc_gpu.py -x -q > gpurun_out/g3_gemm_test.txt 2>&1; echo rc=$? >> gpurun_out/g3_gemm_test.txt
+tail -3 gpurun_out/g3_gemm_test.txt
+timeout -s KILL 600 python tools/gemm_bench.py --sweep > gpurun_out/g3_gemm_bench.jsonl 2>&1; echo rc=$?
