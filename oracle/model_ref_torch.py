@@ -149,13 +149,20 @@ class Model:
         return self._rms(X)
 
     @torch.no_grad()
-    def logits_stats_all(self, tokens, positions):
-        """(argmax, logsumexp, logit sum, top-2 gap) of the rows at `positions` of one sequence."""
+    def logits_stats_all(self, tokens, positions, cand=None):
+        """(argmax, logsumexp, logit sum, gap) of the rows at `positions` of one
+        sequence; gap[i] = z[argmax] - z[cand[i]] (the fp32 logit margin by which
+        token cand[i] loses), or the top-2 gap when no candidates are given."""
         h = self.forward(tokens)[torch.as_tensor(positions, device=self.device)]
         z = self._mm(h, self.lm).to(torch.float64)
         lse = torch.logsumexp(z, dim=-1)
         top = torch.topk(z, 2, dim=-1).values
-        return (z.argmax(dim=-1).tolist(), lse.tolist(), z.sum(dim=-1).tolist(), (top[:, 0] - top[:, 1]).tolist())
+        if cand is None:
+            gap = top[:, 0] - top[:, 1]
+        else:
+            c = torch.as_tensor(cand, device=z.device, dtype=torch.long)
+            gap = top[:, 0] - z.gather(1, c[:, None])[:, 0]
+        return (z.argmax(dim=-1).tolist(), lse.tolist(), z.sum(dim=-1).tolist(), gap.tolist())
 
     @torch.no_grad()
     def prm_score(self, tokens) -> float:

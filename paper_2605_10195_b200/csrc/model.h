@@ -85,59 +85,6 @@ struct PrmOut {
   int pad;
 };
 
-// Decode work list of one forward step (shared by its L K1 launches): every
-// row's concatenated context is cut into at most kMaxRowChunks chunks of at
-// least kMinChunk tokens; one warp per (chunk, kv head) pulled from a device
-// work queue, partial softmax states merged by the last warp of the row.
-constexpr int kMaxRowChunks = 8;
-constexpr int kMinChunk = 128;
-constexpr int kQueueSlots = 256;  // per-launch work-queue counters (one per layer)
-struct ChunkItem {
-  int row;
-  int chunk;
-};
-struct DecodeChunks {
-  ChunkItem* items;  // (row, chunk) in row order
-  int* row_nch;     // chunks of row r
-  int* row_ch;      // chunk length (tokens) of row r
-  int* row_item0;   // first item of row r
-  int* n_items;     // device scalar
-  int* qctr;        // [kQueueSlots] work-queue heads, zeroed by the builder
-  float* part;      // partial (acc, m, l) per (item, kv head): G * DH + round4(2G) floats
-  int* cnt;         // [rows_cap * KVH] arrival counters (self-resetting)
-};
-
-// Query groups of one decode step (K1 tree-group kernel): the step's rows of
-// one query, at most kGroupRows per group (in row order), and the union of
-// their context segments with a bit mask of the rows that read each one, so a
-// shared ancestor's K/V is staged once for the whole group.
-constexpr int kGroupRows = 16;
-struct GroupDesc {
-  int nrows;
-  int seg_off;  // into GroupSeg[]
-  int nseg;
-  int pad;
-  int row[kGroupRows];
-};
-struct GroupSeg {
-  long long base;  // first KV slot
-  int len;         // tokens
-  uint32_t mask;   // bit i: group row i attends to this segment
-};
-struct TreeGroups {
-  int* q_cnt;          // [q_cap] rows per query
-  int* q_off;          // [q_cap] first sorted position of query q
-  int* q_goff;         // [q_cap] first group of query q
-  int* q_fill;         // [q_cap]
-  int* sorted;         // [rows_cap] row indices grouped by query, ascending within a query
-  GroupDesc* groups;   // [rows_cap]
-  GroupSeg* gsegs;     // [seg_cap]
-  int* n_groups;       // device scalar
-  int* seg_ctr;        // device scalar (zeroed by the builder)
-  int q_cap;
-  long long seg_cap;
-};
-
 // K2 tcgen05 GEMM epilogues (gemm_tc.cu)
 enum TcEpi : int { TC_EPI_STORE = 0, TC_EPI_ROPE_KV = 1, TC_EPI_SWIGLU = 2, TC_EPI_LSE = 3 };
 struct TcEpilogue {

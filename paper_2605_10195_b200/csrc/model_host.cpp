@@ -50,38 +50,23 @@ void spex_k_prm_scan_all(TreeView t, const int* kind, const int* off, const int*
                          cudaStream_t s);
 void spex_k_embed(const RowDesc* rows, int M, const __nv_bfloat16* E, int d, float* X, cudaStream_t s);
 void spex_k_rmsnorm(const float* X, int M, int d, float eps, __nv_bfloat16* Y, cudaStream_t s);
-void spex_k_rope_kv(const RowDesc* rows, int M, const __nv_bfloat16* QKV, int H, int KVH, int dh, const float* cs_tab,
-                    long long slots, __nv_bfloat16* Kp, __nv_bfloat16* Vp, float* Qr, cudaStream_t s);
 int spex_k_tree_attn(const RowDesc* rows, const Segment* segs, const float* Qr, int H, int KVH, int dh,
                      const __nv_bfloat16* Kp, const __nv_bfloat16* Vp, long long slots, __nv_bfloat16* O, int M,
                      cudaStream_t s);
-void spex_k_build_decode_chunks(const RowDesc* rows, const Segment* segs, int M, DecodeChunks w, cudaStream_t s);
 void spex_k1_set_kv_evict_first(int on);
 void spex_k1_set_row_order(const int* order);
 void spex_k_order_rows(const RowDesc* rows, int M, int Q, int* order, cudaStream_t s);
-void spex_k_build_groups(const RowDesc* rows, const Segment* segs, int M, int Q, TreeGroups g, cudaStream_t s);
-int spex_k_tree_attn_group(const CUtensorMap* kmap16, const CUtensorMap* vmap16, const TreeGroups* g, const float* Qr,
-                           int H, int KVH, int dh, long long slots, __nv_bfloat16* O, int M, int* item_ctr,
-                           cudaStream_t s);
 int spex_k_tree_attn_bulk(const RowDesc* rows, const Segment* segs, const float* Qr, int H, int KVH, int dh,
                           const __nv_bfloat16* Kp, const __nv_bfloat16* Vp, long long slots, __nv_bfloat16* O, int M,
                           int* item_ctr, cudaStream_t s);
 int spex_k_tree_attn_wmma(const CUtensorMap* kmap16, const CUtensorMap* vmap16, const RowDesc* rows,
                           const Segment* segs, const float* Qr, int H, int KVH, int dh, long long slots,
                           __nv_bfloat16* O, int M, int* item_ctr, cudaStream_t s);
-int spex_k_tree_attn_decode_mma(const CUtensorMap* kmap, const CUtensorMap* vmap, const RowDesc* rows,
-                                const Segment* segs, const float* Qr, int H, int KVH, int dh, long long slots,
-                                __nv_bfloat16* O, int M, cudaStream_t s);
-int spex_k_tree_attn_chunked(const RowDesc* rows, const Segment* segs, const float* Qr, int H, int KVH, int dh,
-                             const __nv_bfloat16* Kp, const __nv_bfloat16* Vp, long long slots, __nv_bfloat16* O,
-                             DecodeChunks w, int qslot, cudaStream_t s);
-void spex_k_swiglu(const __nv_bfloat16* GU, int M, int F, __nv_bfloat16* A, cudaStream_t s);
 int spex_k_gemm_tc(const CUtensorMap* tmA, const CUtensorMap* tmB, int M, int N, int K, const TcEpilogue* ep,
                    unsigned int* sched, cudaStream_t s);
 void spex_k_lse_combine(const float* part, int M, int n_tiles, int* amax, float* lse, float* lsum, cudaStream_t s);
 void spex_k_rope_table(const RowDesc* rows, int M, const float* inv_freq, int half, float* out, cudaStream_t s);
 void spex_k_interleave_gu(const __nv_bfloat16* wgu, int F, int d, __nv_bfloat16* out, cudaStream_t s);
-void spex_k_lm_epilogue(const float* logits, int M, int V, int* amax, float* lse, float* lsum, cudaStream_t s);
 void spex_k_value_head(const __nv_bfloat16* Hn, int d, const int* last_row, int n, const __nv_bfloat16* w,
                        float* score, cudaStream_t s);
 void spex_k_gather_prm(const RowDesc* rows, const int* last_row, int n, const float* score, PrmOut* out,
@@ -341,15 +326,6 @@ static Model* make_model(const ModelShape& sh, bool prm, uint64_t seed, long lon
   return m;
 }
 
-// Decode rows of GQA models (>= 4 query heads per KV head) go to the tensor-core
-// decode kernel: its staged K/V chunks serve the whole group, while the
-// per-lane FHFMA kernel's work per byte grows with the group size.
-static bool decode_mma_wanted(const ModelShape& s) {
-  static const int force = getenv("SPEX_K1_DECODE_MMA") ? atoi(getenv("SPEX_K1_DECODE_MMA")) : -1;
-  if (force >= 0) return force != 0;
-  return s.dh == 128 && s.H / s.KVH >= 4;
-}
-
 // Decode rows with one KV head per query head (G = 1) stream through the
 // bulk-copy pipeline kernel (measured 1.98 s vs 2.10 s per c2 search for the
 // register-pipelined FHFMA kernel); SPEX_K1_BULK=0 selects the latter.
@@ -376,25 +352,17 @@ static void tc_gemm(const CUtensorMap& a, const TcWeight& w, int M, const TcEpil
 // decode rows on the per-warp TMA pipeline (GQA groups), the bulk-copy
 // pipeline (one KV head per query head) or the register pipeline (other shapes).
 static void attention(Model& m, int l, const RowDesc* rows, const Segment* segs, int M, const TileDesc* tiles,
-                      int ntiles, const DecodeChunks* chunks, const TreeGroups* groups, cudaStream_t st) {
+                      int ntiles, cudaStream_t st) {
   const ModelShape& s = m.sh;
   int rc = -1;
   if (tiles && !m.kmap.empty())
     rc = spex_k_tree_attn_tiles_mma(&m.kmap[l], &m.vmap[l], tiles, ntiles, rows, segs, m.Qr, s.H, s.KVH, s.dh,
                                     m.slots, m.O, st);
-  if (rc != 0 && !tiles && groups && !m.kmap16.empty() && g_item_ctr)
-    rc = spex_k_tree_attn_group(&m.kmap16[l], &m.vmap16[l], groups, m.Qr, s.H, s.KVH, s.dh, m.slots, m.O, M,
-                                g_item_ctr, st);
   if (rc != 0 && !tiles && !m.kmap16.empty() && wmma_wanted(s) && g_item_ctr)
     rc = spex_k_tree_attn_wmma(&m.kmap16[l], &m.vmap16[l], rows, segs, m.Qr, s.H, s.KVH, s.dh, m.slots, m.O, M,
                                g_item_ctr, st);
-  if (rc != 0 && !tiles && !m.kmap.empty() && decode_mma_wanted(s))
-    rc = spex_k_tree_attn_decode_mma(&m.kmap[l], &m.vmap[l], rows, segs, m.Qr, s.H, s.KVH, s.dh, m.slots, m.O, M,
-                                     st);
   if (rc != 0 && !tiles && bulk_wanted() && g_item_ctr)
     rc = spex_k_tree_attn_bulk(rows, segs, m.Qr, s.H, s.KVH, s.dh, m.Kp[l], m.Vp[l], m.slots, m.O, M, g_item_ctr, st);
-  if (rc != 0 && chunks)
-    rc = spex_k_tree_attn_chunked(rows, segs, m.Qr, s.H, s.KVH, s.dh, m.Kp[l], m.Vp[l], m.slots, m.O, *chunks, l, st);
   if (rc != 0)
     rc = tiles ? spex_k_tree_attn_tiles(tiles, ntiles, rows, segs, m.Qr, s.H, s.KVH, s.dh, m.Kp[l], m.Vp[l], m.slots,
                                         m.O, st)
@@ -407,8 +375,7 @@ static void attention(Model& m, int l, const RowDesc* rows, const Segment* segs,
 static long long g_launches = 0;
 
 static void forward(Model& m, const RowDesc* rows, const Segment* segs, int M, cudaStream_t st, AttnTimer* timer,
-                    const TileDesc* tiles = nullptr, int ntiles = 0, const DecodeChunks* chunks = nullptr,
-                    const TreeGroups* groups = nullptr) {
+                    const TileDesc* tiles = nullptr, int ntiles = 0) {
   const ModelShape& s = m.sh;
   // embed -> L x [RMSNorm, QKV + RoPE + KV append (tcgen05), K1, O + residual
   // (tcgen05), RMSNorm, gate/up + SwiGLU (tcgen05), down + residual (tcgen05)]
@@ -441,7 +408,7 @@ static void forward(Model& m, const RowDesc* rows, const Segment* segs, int M, c
     eq.Vp = m.Vp[l];
     tc_gemm(m.a_xn, m.tq[l], M, eq, m.sched, st);
     if (timer) timer->begin(st);
-    attention(m, l, rows, segs, M, tiles, ntiles, chunks, groups, st);
+    attention(m, l, rows, segs, M, tiles, ntiles, st);
     if (timer) timer->end(st);
     tc_gemm(m.a_o, m.to[l], M, er, m.sched, st);
     spex_k_rmsnorm(m.X, M, s.d, s.eps, m.Xn, st);
@@ -533,80 +500,8 @@ struct ModelCache {
   int* item_ctr = nullptr;  // K1 bulk kernel's work counter (policy stream)
   int* row_order = nullptr;  // decode rows grouped by query (K1 bulk claim order)
   int row_order_cap = 0;
-  // query groups of a decode step (K1 tree-group kernel)
-  TreeGroups tg{};
-  int tg_rows = 0, tg_q = 0;
-  // decode work list (K1 chunked), sized for rows_cap rows of the policy shape
-  DecodeChunks dc{};
-  int dc_rows = 0;
-  long long dc_part = 0;
 };
 static ModelCache g_cache;
-
-static void ensure_decode_chunks(int rows_cap, const ModelShape& sh) {
-  // per item: KVH * (G * dh + round4(2G)) <= H * (dh + 4) floats
-  const long long part = (long long)rows_cap * kMaxRowChunks * sh.H * (sh.dh + 4);
-  if (g_cache.dc_rows >= rows_cap && g_cache.dc_part >= part && g_cache.dc.cnt) return;
-  DecodeChunks& w = g_cache.dc;
-  cudaFree(w.items);
-  cudaFree(w.row_nch);
-  cudaFree(w.row_ch);
-  cudaFree(w.row_item0);
-  cudaFree(w.n_items);
-  cudaFree(w.qctr);
-  cudaFree(w.part);
-  cudaFree(w.cnt);
-  std::vector<void*> keep;
-  w.items = dalloc<ChunkItem>((size_t)rows_cap * kMaxRowChunks, keep);
-  w.row_nch = dalloc<int>(rows_cap, keep);
-  w.row_ch = dalloc<int>(rows_cap, keep);
-  w.row_item0 = dalloc<int>(rows_cap, keep);
-  w.n_items = dalloc<int>(1, keep);
-  w.qctr = dalloc<int>(kQueueSlots, keep);
-  w.part = dalloc<float>((size_t)part, keep);
-  const size_t ncnt = (size_t)rows_cap * std::max(sh.KVH, 1) * 8;  // any KVH up to 8x the policy's
-  w.cnt = dalloc<int>(ncnt, keep);
-  CK(cudaMemset(w.cnt, 0, ncnt * sizeof(int)));
-  g_cache.dc_rows = rows_cap;
-  g_cache.dc_part = part;
-}
-
-static void ensure_groups(int rows_cap, int Q) {
-  if (g_cache.tg_rows >= rows_cap && g_cache.tg_q >= Q && g_cache.tg.groups) return;
-  TreeGroups& g = g_cache.tg;
-  cudaFree(g.q_cnt);
-  cudaFree(g.q_off);
-  cudaFree(g.q_goff);
-  cudaFree(g.q_fill);
-  cudaFree(g.sorted);
-  cudaFree(g.groups);
-  cudaFree(g.gsegs);
-  cudaFree(g.n_groups);
-  cudaFree(g.seg_ctr);
-  std::vector<void*> keep;
-  const int qc = std::max(Q, 1);
-  g.q_cnt = dalloc<int>(qc, keep);
-  g.q_off = dalloc<int>(qc, keep);
-  g.q_goff = dalloc<int>(qc, keep);
-  g.q_fill = dalloc<int>(qc, keep);
-  g.sorted = dalloc<int>(rows_cap, keep);
-  g.groups = dalloc<GroupDesc>(rows_cap, keep);
-  g.seg_cap = (long long)rows_cap * 40;  // >= the rows' segments (kMaxSeg each)
-  g.gsegs = dalloc<GroupSeg>((size_t)g.seg_cap, keep);
-  g.n_groups = dalloc<int>(1, keep);
-  g.seg_ctr = dalloc<int>(1, keep);
-  g.q_cap = qc;
-  g_cache.tg_rows = rows_cap;
-  g_cache.tg_q = qc;
-}
-
-// K1 decode rows by query groups (shared segments staged once per group).
-// SPEX_K1_GROUP=0/1 overrides the default.
-static bool group_wanted(const ModelShape& s) {
-  static const int env = getenv("SPEX_K1_GROUP") ? atoi(getenv("SPEX_K1_GROUP")) : -1;
-  const int on = env >= 0 ? env : 0;
-  return on != 0 && s.H == s.KVH && s.dh == 128;
-}
 
 // K1 bulk claim order grouped by query (SPEX_K1_QORDER=0: active order).
 static bool qorder_wanted() {
@@ -712,12 +607,6 @@ void run_model_schedule(const ModelRunConfig& mc, const ScheduleView& sv, ModelR
   Segment* segs2 = prm_overlap ? g_cache.segs2 : g_cache.segs;
   TileDesc* tiles2 = prm_overlap ? g_cache.tiles2 : g_cache.tiles;
   int* last_row = g_cache.last_row;
-  // Chunked K1 (bounded per-warp work, merged partials) is opt-in: on the
-  // benchmark's context lengths (~250 tokens/row) the one-warp-per-(row, head)
-  // kernel is faster (measured 78% vs 72% of HBM peak, profiles/r01e_*).
-  const bool chunked = std::getenv("SPEX_K1_CHUNKED") != nullptr;
-  if (chunked) ensure_decode_chunks(std::max(max_dec, 1), mc.policy);
-  if (group_wanted(mc.policy)) ensure_groups(std::max(max_dec, 1), Q);
   if (g_cache.row_order_cap < max_dec) {
     cudaFree(g_cache.row_order);
     std::vector<void*> keep;
@@ -778,22 +667,15 @@ void run_model_schedule(const ModelRunConfig& mc, const ScheduleView& sv, ModelR
           spex_k_build_decode_rows(tv_pol, sv.srow_sid + pe.off + c0, sv.srow_pos0 + pe.off + c0, n, s, rows, segs,
                                    st);
           g_launches += 1;
-          const bool grouped = group_wanted(mc.policy);
           if (qorder_wanted()) {
             spex_k_order_rows(rows, n, Q, g_cache.row_order, st);
             spex_k1_set_row_order(g_cache.row_order);
             g_launches += 1;
           }
-          if (grouped) {
-            spex_k_build_groups(rows, segs, n, Q, g_cache.tg, st);
-            g_launches += 2;
-          }
           // one K1 launch per layer: the step's unique KV tokens (this chunk's share) + Q/O rows
           timer.cur_bytes = ((double)pe.u0 + (double)s * pe.n + pe.n) * kv_tok_bytes * ((double)n / pe.n) +
                             (double)n * mc.policy.H * mc.policy.dh * (4.0 + 2.0);
-          if (chunked) spex_k_build_decode_chunks(rows, segs, n, g_cache.dc, st);
-          forward(*pol, rows, segs, n, st, mc.time_attn ? &timer : nullptr, nullptr, 0,
-                  chunked ? &g_cache.dc : nullptr, grouped ? &g_cache.tg : nullptr);
+          forward(*pol, rows, segs, n, st, mc.time_attn ? &timer : nullptr);
           spex_k1_set_row_order(nullptr);  // read at launch: other callers get row order
           if (dbg && dbg_n + n <= mc.out_rows_cap) {
             spex_k_gather_outputs(rows, n, pol->amax, pol->lse, pol->lsum, dbg + dbg_n, st);

@@ -305,70 +305,6 @@ __global__ void rmsnorm_bf16_reg_kernel(const float* X, int M, float eps, __nv_b
   }
 }
 
-// RoPE on q and k at the row's absolute position; append k, v (bf16) to the
-// layer's KV pool at the row's slot; q (fp32, pre-scaled by 1/sqrt(dh)) to Qr.
-// Pools are [KVH][slots][dh].
-__global__ void rope_kv_kernel(const RowDesc* rows, int M, const __nv_bfloat16* QKV, int H, int KVH, int dh,
-                               const float2* __restrict__ cs_tab, long long slots, __nv_bfloat16* Kp,
-                               __nv_bfloat16* Vp, float* Qr) {
-  pdl_wait();
-  // one block (128 threads) per row; (cos, sin) from the per-forward table
-  // (rope_table_kernel), rotate-half RoPE on (x[i], x[i+half]) eight pairs at a
-  // time from the bf16 projection output (16-byte loads and stores; dh % 16 == 0);
-  // V copied 16 bytes at a time
-  const int r = blockIdx.x, lane = threadIdx.x;
-  if (r >= M) return;
-  const long long slot = rows[r].slot;
-  const int width = (H + 2 * KVH) * dh;
-  const __nv_bfloat16* src = QKV + (long long)r * width;
-  const int half = dh / 2;
-  const float2* cs = cs_tab + (long long)r * half;
-  const float qscale = rsqrtf((float)dh);
-  const int ho = half / 8;  // octets per half
-  for (int idx = lane; idx < (H + KVH) * ho; idx += blockDim.x) {
-    const int head = idx / ho;
-    const int i = (idx - head * ho) * 8;
-    const __nv_bfloat16* x = src + head * dh;
-    const uint4 A = *reinterpret_cast<const uint4*>(x + i);
-    const uint4 B = *reinterpret_cast<const uint4*>(x + i + half);
-    const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&A);
-    const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&B);
-    const float4* c4 = reinterpret_cast<const float4*>(cs + i);  // (cos, sin) of pairs i .. i+7
-    float ya[8], yb[8];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const float4 c = c4[k];  // (cos, sin) of pairs i+2k, i+2k+1
-      const float ax = __low2float(a2[k]), ay = __high2float(a2[k]);
-      const float bx = __low2float(b2[k]), by = __high2float(b2[k]);
-      ya[2 * k] = ax * c.x - bx * c.y;
-      ya[2 * k + 1] = ay * c.z - by * c.w;
-      yb[2 * k] = ax * c.y + bx * c.x;
-      yb[2 * k + 1] = ay * c.w + by * c.z;
-    }
-    if (head < H) {
-      float4* qd = reinterpret_cast<float4*>(Qr + ((long long)r * H + head) * dh + i);
-      float4* qe = reinterpret_cast<float4*>(Qr + ((long long)r * H + head) * dh + i + half);
-      qd[0] = make_float4(ya[0] * qscale, ya[1] * qscale, ya[2] * qscale, ya[3] * qscale);
-      qd[1] = make_float4(ya[4] * qscale, ya[5] * qscale, ya[6] * qscale, ya[7] * qscale);
-      qe[0] = make_float4(yb[0] * qscale, yb[1] * qscale, yb[2] * qscale, yb[3] * qscale);
-      qe[1] = make_float4(yb[4] * qscale, yb[5] * qscale, yb[6] * qscale, yb[7] * qscale);
-    } else {
-      const int kh = head - H;
-      __nv_bfloat16* kd = Kp + ((long long)kh * slots + slot) * dh;
-      *reinterpret_cast<uint4*>(kd + i) =
-          make_uint4(pack_bf16(ya[0], ya[1]), pack_bf16(ya[2], ya[3]), pack_bf16(ya[4], ya[5]), pack_bf16(ya[6], ya[7]));
-      *reinterpret_cast<uint4*>(kd + i + half) =
-          make_uint4(pack_bf16(yb[0], yb[1]), pack_bf16(yb[2], yb[3]), pack_bf16(yb[4], yb[5]), pack_bf16(yb[6], yb[7]));
-    }
-  }
-  const __nv_bfloat16* vs = src + (H + KVH) * dh;
-  for (int idx = lane; idx < KVH * dh / 8; idx += blockDim.x) {
-    const int e = idx * 8;
-    const int kh = e / dh, i = e - kh * dh;
-    *reinterpret_cast<uint4*>(Vp + ((long long)kh * slots + slot) * dh + i) = *reinterpret_cast<const uint4*>(vs + e);
-  }
-}
-
 // ------------------------------------------------------------------ K1
 __device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(bar)),
@@ -580,45 +516,6 @@ __global__ void __launch_bounds__(256, (UNROLL > 4 ? 2 : (G == 1 ? 4 : (G <= 4 ?
   }
 }
 
-// Decode work list: per-row context length -> chunk count/length, exclusive
-// scan over rows (one block), (row, chunk) items; zeroes the work queues.
-__global__ void __launch_bounds__(1024) build_decode_chunks_kernel(const RowDesc* __restrict__ rows,
-                                                                  const Segment* __restrict__ segs, int M,
-                                                                  DecodeChunks w) {
-  __shared__ int sums[1024];
-  const int tid = threadIdx.x;
-  if (tid < kQueueSlots) w.qctr[tid] = 0;
-  const int per = (M + 1023) / 1024;
-  const int r0 = tid * per, r1 = min(M, r0 + per);
-  int local = 0;
-  for (int r = r0; r < r1; ++r) {
-    const RowDesc rd = rows[r];
-    int L = 0;
-    for (int k = 0; k < rd.nseg; ++k) L += segs[rd.seg_off + k].len;
-    int ch = (L + kMaxRowChunks - 1) / kMaxRowChunks;
-    if (ch < kMinChunk) ch = kMinChunk;
-    const int nch = (L + ch - 1) / ch;
-    w.row_nch[r] = nch;
-    w.row_ch[r] = ch;
-    local += nch;
-  }
-  sums[tid] = local;
-  __syncthreads();
-  for (int o = 1; o < 1024; o <<= 1) {
-    const int v = tid >= o ? sums[tid - o] : 0;
-    __syncthreads();
-    sums[tid] += v;
-    __syncthreads();
-  }
-  int base = sums[tid] - local;
-  for (int r = r0; r < r1; ++r) {
-    w.row_item0[r] = base;
-    for (int c = 0; c < w.row_nch[r]; ++c) w.items[base + c] = ChunkItem{r, c};
-    base += w.row_nch[r];
-  }
-  if (tid == 1023) *w.n_items = sums[1023];
-}
-
 // K1 decode, bulk-copy pipeline (G = 1): a persistent grid of warps; each warp
 // claims (row, kv head) items from a device counter and streams their tree
 // context through its own ring of NST shared-memory stages of CH tokens (K and
@@ -799,198 +696,6 @@ __global__ void __launch_bounds__(kBulkWarps * 32, 1)
       packed.w = pack_bf16(acc[6] * inv, acc[7] * inv);
       *reinterpret_cast<uint4*>(O + ((long long)r * H + kh) * DH + li * EPL) = packed;
     }
-  }
-}
-
-// K1 decode, chunked: a persistent grid of warps pulls (chunk, kv head) work
-// from a device queue; each streams its chunk of the row's tree context with
-// 128-bit loads and FHFMA.BF16 (as tree_attn_decode_kernel). Single-chunk rows
-// write O directly; multi-chunk rows leave a partial (m, l, acc) and the last
-// arriving warp of the (row, head) merges them. Bounded chunks keep every warp's
-// work within ~kMinChunk..ctx/8 tokens, so no long row forms a tail.
-template <int DH, int G>
-__global__ void __launch_bounds__(256, (G == 1 ? 4 : (G <= 4 ? 2 : 1)))
-    tree_attn_chunk_kernel(const RowDesc* __restrict__ rows, const Segment* __restrict__ segs,
-                           const float* __restrict__ Qr, int H, int KVH, const __nv_bfloat16* __restrict__ Kp,
-                           const __nv_bfloat16* __restrict__ Vp, long long slots, __nv_bfloat16* __restrict__ O,
-                           DecodeChunks w, int* __restrict__ qctr) {
-  constexpr int EPL = 8;
-  constexpr int LPT = DH / EPL;
-  constexpr int TPW = 32 / LPT;
-  constexpr int UNROLL = 4;
-  constexpr float L2E = 1.4426950408889634f;
-  const int lane = threadIdx.x & 31;
-  const int sub = lane / LPT;
-  const int li = lane % LPT;
-  uint64_t pol;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-  const int total = *w.n_items * KVH;
-  for (;;) {
-    int wi = 0;
-    if (lane == 0) wi = atomicAdd(qctr, 1);
-    wi = __shfl_sync(0xffffffffu, wi, 0);
-    if (wi >= total) break;
-    const int item = wi / KVH, kh = wi - item * KVH;
-    const ChunkItem rc = w.items[item];
-    const int r = rc.row, c = rc.chunk;
-    const int nch = w.row_nch[r], ch = w.row_ch[r];
-    const int tbeg = c * ch, tend = tbeg + ch;
-    const RowDesc rd = rows[r];
-    const Segment* sg = segs + rd.seg_off;
-    const __nv_bfloat16* Kh = Kp + (long long)kh * slots * DH + li * EPL;
-    const __nv_bfloat16* Vh = Vp + (long long)kh * slots * DH + li * EPL;
-    uint32_t q2[G][EPL / 2];
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-      const float4* qp = reinterpret_cast<const float4*>(Qr + ((long long)r * H + kh * G + g) * DH + li * EPL);
-      const float4 a = qp[0], b = qp[1];
-      q2[g][0] = pack_bf16(a.x * L2E, a.y * L2E);
-      q2[g][1] = pack_bf16(a.z * L2E, a.w * L2E);
-      q2[g][2] = pack_bf16(b.x * L2E, b.y * L2E);
-      q2[g][3] = pack_bf16(b.z * L2E, b.w * L2E);
-    }
-    float m[G], l[G], acc[G][EPL];
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-      m[g] = -INFINITY;
-      l[g] = 0.f;
-#pragma unroll
-      for (int e = 0; e < EPL; ++e) acc[g][e] = 0.f;
-    }
-    int off = 0;
-    for (int si = 0; si < rd.nseg && off < tend; ++si) {
-      const int len = sg[si].len;
-      const int lo = max(tbeg - off, 0), hi = min(tend - off, len);
-      const long long base = sg[si].base;
-      off += len;
-      for (int t0 = lo; t0 < hi; t0 += TPW * UNROLL) {
-        uint4 kraw[UNROLL], vraw[UNROLL];
-        bool ok[UNROLL];
-#pragma unroll
-        for (int u = 0; u < UNROLL; ++u) {
-          const int t = t0 + u * TPW + sub;
-          ok[u] = t < hi;
-          const long long o = (base + (ok[u] ? t : lo)) * DH;
-          kraw[u] = ld_stream(Kh + o, pol);
-          vraw[u] = ld_stream(Vh + o, pol);
-        }
-#pragma unroll
-        for (int g = 0; g < G; ++g) {
-          float sc[UNROLL];
-#pragma unroll
-          for (int u = 0; u < UNROLL; ++u) {
-            float a = 0.f;
-            fma2_bf16(a, q2[g][0], kraw[u].x);
-            fma2_bf16(a, q2[g][1], kraw[u].y);
-            fma2_bf16(a, q2[g][2], kraw[u].z);
-            fma2_bf16(a, q2[g][3], kraw[u].w);
-            sc[u] = a;
-          }
-#pragma unroll
-          for (int o = LPT / 2; o > 0; o >>= 1)
-#pragma unroll
-            for (int u = 0; u < UNROLL; ++u) sc[u] += __shfl_xor_sync(0xffffffffu, sc[u], o);
-          float mx = -INFINITY;
-#pragma unroll
-          for (int u = 0; u < UNROLL; ++u) {
-            if (!ok[u]) sc[u] = -INFINITY;
-            mx = fmaxf(mx, sc[u]);
-          }
-#pragma unroll
-          for (int o = LPT; o < 32; o <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-          if (mx > m[g]) {
-            const float scale = exp2f(m[g] - mx);
-            l[g] *= scale;
-#pragma unroll
-            for (int e = 0; e < EPL; ++e) acc[g][e] *= scale;
-            m[g] = mx;
-          }
-#pragma unroll
-          for (int u = 0; u < UNROLL; ++u) {
-            const float p = exp2f(sc[u] - m[g]);
-            const __nv_bfloat16 pb = __float2bfloat16_rn(p);
-            l[g] += __bfloat162float(pb);
-            const uint32_t p2 = (uint32_t)__bfloat16_as_ushort(pb) * 0x10001u;
-            fma_pv_bf16(acc[g][0], acc[g][1], p2, vraw[u].x);
-            fma_pv_bf16(acc[g][2], acc[g][3], p2, vraw[u].y);
-            fma_pv_bf16(acc[g][4], acc[g][5], p2, vraw[u].z);
-            fma_pv_bf16(acc[g][6], acc[g][7], p2, vraw[u].w);
-          }
-        }
-      }
-    }
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-#pragma unroll
-      for (int o = LPT; o < 32; o <<= 1) {
-        l[g] += __shfl_xor_sync(0xffffffffu, l[g], o);
-#pragma unroll
-        for (int e = 0; e < EPL; ++e) acc[g][e] += __shfl_xor_sync(0xffffffffu, acc[g][e], o);
-      }
-    }
-    if (nch == 1) {
-      if (sub == 0) {
-#pragma unroll
-        for (int g = 0; g < G; ++g) {
-          const float inv = 1.f / l[g];
-          uint4 packed;
-          packed.x = pack_bf16(acc[g][0] * inv, acc[g][1] * inv);
-          packed.y = pack_bf16(acc[g][2] * inv, acc[g][3] * inv);
-          packed.z = pack_bf16(acc[g][4] * inv, acc[g][5] * inv);
-          packed.w = pack_bf16(acc[g][6] * inv, acc[g][7] * inv);
-          *reinterpret_cast<uint4*>(O + ((long long)r * H + kh * G + g) * DH + li * EPL) = packed;
-        }
-      }
-      continue;
-    }
-    // partial state of this chunk: [G][DH] acc, then m[G], l[G]
-    constexpr int PS = G * DH + ((2 * G + 3) & ~3);  // 16-byte aligned per (item, head)
-    float* pp = w.part + ((long long)item * KVH + kh) * PS;
-    if (sub == 0) {
-#pragma unroll
-      for (int g = 0; g < G; ++g) {
-        float4* ap = reinterpret_cast<float4*>(pp + g * DH + li * EPL);
-        ap[0] = make_float4(acc[g][0], acc[g][1], acc[g][2], acc[g][3]);
-        ap[1] = make_float4(acc[g][4], acc[g][5], acc[g][6], acc[g][7]);
-      }
-    }
-    if (lane == 0) {
-#pragma unroll
-      for (int g = 0; g < G; ++g) {
-        pp[G * DH + g] = m[g];
-        pp[G * DH + G + g] = l[g];
-      }
-    }
-    __threadfence();
-    __syncwarp();
-    int last = 0;
-    if (lane == 0) last = atomicAdd(&w.cnt[r * KVH + kh], 1) == nch - 1;
-    last = __shfl_sync(0xffffffffu, last, 0);
-    if (!last) continue;
-    __threadfence();
-    // merge the row's nch partials: each lane owns DH/32 dims of every head
-    constexpr int DPL = DH / 32;
-    const float* p0 = w.part + ((long long)w.row_item0[r] * KVH + kh) * PS;
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-      float M = -INFINITY;
-      for (int k = 0; k < nch; ++k) M = fmaxf(M, __ldcg(p0 + (long long)k * KVH * PS + G * DH + g));
-      float Lsum = 0.f, a[DPL];
-#pragma unroll
-      for (int e = 0; e < DPL; ++e) a[e] = 0.f;
-      for (int k = 0; k < nch; ++k) {
-        const float* pk = p0 + (long long)k * KVH * PS;
-        const float sk = exp2f(__ldcg(pk + G * DH + g) - M);
-        Lsum += __ldcg(pk + G * DH + G + g) * sk;
-#pragma unroll
-        for (int e = 0; e < DPL; ++e) a[e] += __ldcg(pk + g * DH + lane * DPL + e) * sk;
-      }
-      const float inv = 1.f / Lsum;
-      __nv_bfloat16* op = O + ((long long)r * H + kh * G + g) * DH + lane * DPL;
-#pragma unroll
-      for (int e = 0; e < DPL; e += 2) *reinterpret_cast<uint32_t*>(op + e) = pack_bf16(a[e] * inv, a[e + 1] * inv);
-    }
-    if (lane == 0) w.cnt[r * KVH + kh] = 0;
   }
 }
 
@@ -1287,249 +992,6 @@ __global__ void __launch_bounds__(128) tree_attn_tile_mma_kernel(const __grid_co
   (void)L1;
 }
 
-// K1 decode on tensor cores for GQA groups: block = (decode row, KV head); the
-// MMA rows are that KV head's G query heads (zero-padded to 16), so every
-// staged 64-token K/V chunk (TMA, 2 buffers) serves all G heads; the 4 warps
-// take 16-token slices of each chunk and merge (m, l, O) through shared memory.
-// For G >= 4 this replaces the per-lane FHFMA kernel, whose work per byte
-// grows with G.
-__global__ void __launch_bounds__(128) tree_attn_decode_mma_kernel(const __grid_constant__ CUtensorMap kmap,
-                                                                  const __grid_constant__ CUtensorMap vmap,
-                                                                  const RowDesc* __restrict__ rows,
-                                                                  const Segment* __restrict__ segs,
-                                                                  const float* __restrict__ Qr, int H, long long slots,
-                                                                  __nv_bfloat16* __restrict__ O, int G) {
-  constexpr int DH = 128;
-  constexpr int SPLIT = 4;              // warps over the chunk's tokens
-  constexpr int TW = kChunk / SPLIT;    // tokens per warp per chunk (16, 32 or 64)
-  constexpr int NT = TW / 8;            // n8 score tiles per warp
-  extern __shared__ __align__(1024) unsigned char smem_raw[];
-  unsigned char* sbase = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  // [buf][K|V][16 KB]
-  __shared__ uint64_t bar[2];
-  __shared__ float sMl[4][2][kTileRows];  // per warp: m, l per row
-  const int r = blockIdx.x, kh = blockIdx.y, hbase = kh * G;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int slice = warp;
-  const RowDesc last = rows[r];
-  const Segment* sg = segs + last.seg_off;
-  const int nseg = last.nseg;
-  if (tid == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  int nchunks = 0;
-  for (int s = 0; s < nseg; ++s) nchunks += (sg[s].len + kChunk - 1) / kChunk;
-  // Q fragments (A operand, 16 rows = the group's heads x 128), rows >= G are zero
-  const int gq = lane >> 2, tq = lane & 3;
-  uint32_t qa[8][4];
-  {
-    const int r0 = gq, r1 = gq + 8;
-    const bool v0 = r0 < G, v1 = r1 < G;
-    const float* q0 = Qr + ((long long)r * H + hbase + (v0 ? r0 : 0)) * DH;
-    const float* q1 = Qr + ((long long)r * H + hbase + (v1 ? r1 : 0)) * DH;
-    const float sc = 1.4426950408889634f;
-#pragma unroll
-    for (int ks = 0; ks < 8; ++ks) {
-      const int k0 = ks * 16 + tq * 2;
-      const float2 x00 = v0 ? *reinterpret_cast<const float2*>(q0 + k0) : make_float2(0.f, 0.f);
-      const float2 x10 = v1 ? *reinterpret_cast<const float2*>(q1 + k0) : make_float2(0.f, 0.f);
-      const float2 x01 = v0 ? *reinterpret_cast<const float2*>(q0 + k0 + 8) : make_float2(0.f, 0.f);
-      const float2 x11 = v1 ? *reinterpret_cast<const float2*>(q1 + k0 + 8) : make_float2(0.f, 0.f);
-      qa[ks][0] = pack_bf16(x00.x * sc, x00.y * sc);
-      qa[ks][1] = pack_bf16(x10.x * sc, x10.y * sc);
-      qa[ks][2] = pack_bf16(x01.x * sc, x01.y * sc);
-      qa[ks][3] = pack_bf16(x11.x * sc, x11.y * sc);
-    }
-  }
-  __syncthreads();
-  int seg_i = 0, seg_o = 0;
-  long long cb[2];
-  int cl[2], cown[2];
-  auto next_chunk = [&](int b) {
-    while (seg_i < nseg && seg_o >= sg[seg_i].len) {
-      ++seg_i;
-      seg_o = 0;
-    }
-    cb[b] = sg[seg_i].base + seg_o;
-    const int l = sg[seg_i].len - seg_o;
-    cl[b] = l < kChunk ? l : kChunk;
-    cown[b] = (seg_i == nseg - 1) ? seg_o : -1;
-    seg_o += cl[b];
-  };
-  auto issue = [&](int b) {
-    unsigned char* kb = sbase + b * 32768;
-    unsigned char* vb = kb + 16384;
-    const int rowc = (int)((long long)kh * slots + cb[b]);
-    mbar_expect_tx(&bar[b], 32768);
-    tma_load_2d(kb, &kmap, 0, rowc, &bar[b]);
-    tma_load_2d(kb + 8192, &kmap, 64, rowc, &bar[b]);
-    tma_load_2d(vb, &vmap, 0, rowc, &bar[b]);
-    tma_load_2d(vb + 8192, &vmap, 64, rowc, &bar[b]);
-  };
-  for (int c = 0; c < 2 && c < nchunks; ++c) {
-    next_chunk(c);
-    if (tid == 0) issue(c);
-  }
-  float oacc[16][4];
-#pragma unroll
-  for (int n = 0; n < 16; ++n) oacc[n][0] = oacc[n][1] = oacc[n][2] = oacc[n][3] = 0.f;
-  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;  // rows gq and gq+8
-  for (int c = 0; c < nchunks; ++c) {
-    const int b = c & 1;
-    const int len = cl[b];
-    mbar_wait(&bar[b], (uint32_t)((c >> 1) & 1));
-    const uint32_t kb = (uint32_t)__cvta_generic_to_shared(sbase + b * 32768);
-    const uint32_t vb = kb + 16384;
-    const int t_base = slice * TW;
-    // S = Q K^T for this warp's token slice
-    float sacc[NT][4];
-#pragma unroll
-    for (int n = 0; n < NT; ++n) sacc[n][0] = sacc[n][1] = sacc[n][2] = sacc[n][3] = 0.f;
-#pragma unroll
-    for (int ks = 0; ks < 8; ++ks) {
-#pragma unroll
-      for (int n2 = 0; n2 < NT / 2; ++n2) {
-        // two n8 tiles (16 tokens) x k16: matrices {tok 0-7,k0-7},{tok 0-7,k8-15},{tok 8-15,k0-7},{tok 8-15,k8-15}
-        const int mi = lane >> 3, ri = lane & 7;
-        const int tok = t_base + n2 * 16 + (mi >> 1) * 8 + ri;
-        const int chunk16 = ks * 2 + (mi & 1);
-        uint32_t b0, b1, b2, b3;
-        ldsm_x4(kb + swz(tok, chunk16), b0, b1, b2, b3);
-        mma_bf16(sacc[2 * n2], qa[ks][0], qa[ks][1], qa[ks][2], qa[ks][3], b0, b1);
-        mma_bf16(sacc[2 * n2 + 1], qa[ks][0], qa[ks][1], qa[ks][2], qa[ks][3], b2, b3);
-      }
-    }
-    // mask and online softmax (rows gq: c0,c1; gq+8: c2,c3)
-    float mx0 = -INFINITY, mx1 = -INFINITY;
-#pragma unroll
-    for (int n = 0; n < NT; ++n) {
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int t = t_base + n * 8 + tq * 2 + e;
-        const bool ok0 = t < len;  // a decode row sees its whole context
-        const bool ok1 = ok0;
-        sacc[n][e] = ok0 ? sacc[n][e] : -INFINITY;
-        sacc[n][2 + e] = ok1 ? sacc[n][2 + e] : -INFINITY;
-        mx0 = fmaxf(mx0, sacc[n][e]);
-        mx1 = fmaxf(mx1, sacc[n][2 + e]);
-      }
-    }
-#pragma unroll
-    for (int o = 1; o < 4; o <<= 1) {
-      mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, o));
-      mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, o));
-    }
-    const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
-    const float a0 = mn0 == -INFINITY ? 1.f : exp2f(m0 - mn0);
-    const float a1 = mn1 == -INFINITY ? 1.f : exp2f(m1 - mn1);
-    float ps0 = 0.f, ps1 = 0.f;
-    uint32_t pa[NT / 2][4];
-#pragma unroll
-    for (int n = 0; n < NT; ++n) {
-      const float p00 = mn0 == -INFINITY ? 0.f : exp2f(sacc[n][0] - mn0);
-      const float p01 = mn0 == -INFINITY ? 0.f : exp2f(sacc[n][1] - mn0);
-      const float p10 = mn1 == -INFINITY ? 0.f : exp2f(sacc[n][2] - mn1);
-      const float p11 = mn1 == -INFINITY ? 0.f : exp2f(sacc[n][3] - mn1);
-      ps0 += p00 + p01;
-      ps1 += p10 + p11;
-      // C layout of n8 tile n -> A layout of k16 step n/2 (regs 0,1 for even n, 2,3 for odd n)
-      if ((n & 1) == 0) {
-        pa[n / 2][0] = pack_bf16(p00, p01);
-        pa[n / 2][1] = pack_bf16(p10, p11);
-      } else {
-        pa[n / 2][2] = pack_bf16(p00, p01);
-        pa[n / 2][3] = pack_bf16(p10, p11);
-      }
-    }
-    l0 = l0 * a0 + ps0;
-    l1 = l1 * a1 + ps1;
-    m0 = mn0;
-    m1 = mn1;
-#pragma unroll
-    for (int n = 0; n < 16; ++n) {
-      oacc[n][0] *= a0;
-      oacc[n][1] *= a0;
-      oacc[n][2] *= a1;
-      oacc[n][3] *= a1;
-    }
-    // O += P V : k = this warp's tokens (NT/2 k16 steps), n = 128 dh (16 n8 tiles)
-#pragma unroll
-    for (int kk = 0; kk < NT / 2; ++kk) {
-#pragma unroll
-      for (int n2 = 0; n2 < 8; ++n2) {
-        // V^T fragments via ldmatrix.trans: matrices {tok 0-7, dh 8j..}, {tok 8-15, dh 8j..}, {tok 0-7, dh 8j+8..}, {tok 8-15, dh 8j+8..}
-        const int mi = lane >> 3, ri = lane & 7;
-        const int tok = t_base + kk * 16 + (mi & 1) * 8 + ri;
-        const int chunk16 = n2 * 2 + (mi >> 1);
-        uint32_t b0, b1, b2, b3;
-        ldsm_x4_t(vb + swz(tok, chunk16), b0, b1, b2, b3);
-        mma_bf16(oacc[2 * n2], pa[kk][0], pa[kk][1], pa[kk][2], pa[kk][3], b0, b1);
-        mma_bf16(oacc[2 * n2 + 1], pa[kk][0], pa[kk][1], pa[kk][2], pa[kk][3], b2, b3);
-      }
-    }
-    __syncthreads();
-    if (c + 2 < nchunks) {
-      next_chunk(b);
-      if (tid == 0) issue(b);
-    }
-  }
-  // row sums within the quad
-#pragma unroll
-  for (int o = 1; o < 4; o <<= 1) {
-    l0 += __shfl_xor_sync(0xffffffffu, l0, o);
-    l1 += __shfl_xor_sync(0xffffffffu, l1, o);
-  }
-  // merge the SPLIT warps of head g through shared memory (reuse the K/V buffers)
-  float* sO = reinterpret_cast<float*>(sbase);  // [4 warps][16 rows][128] fp32 = 32 KB
-  if (tq == 0) {
-    sMl[warp][0][gq] = m0;
-    sMl[warp][0][gq + 8] = m1;
-    sMl[warp][1][gq] = l0;
-    sMl[warp][1][gq + 8] = l1;
-  }
-  __syncthreads();
-  float M0 = -INFINITY, M1 = -INFINITY;
-  for (int w = 0; w < SPLIT; ++w) {
-    M0 = fmaxf(M0, sMl[w][0][gq]);
-    M1 = fmaxf(M1, sMl[w][0][gq + 8]);
-  }
-  float L0 = 0.f, L1 = 0.f;
-  for (int w = 0; w < SPLIT; ++w) {
-    const float mw0 = sMl[w][0][gq], mw1 = sMl[w][0][gq + 8];
-    L0 += (mw0 == -INFINITY) ? 0.f : sMl[w][1][gq] * exp2f(mw0 - M0);
-    L1 += (mw1 == -INFINITY) ? 0.f : sMl[w][1][gq + 8] * exp2f(mw1 - M1);
-  }
-  const float f0 = (m0 == -INFINITY) ? 0.f : exp2f(m0 - M0);
-  const float f1 = (m1 == -INFINITY) ? 0.f : exp2f(m1 - M1);
-#pragma unroll
-  for (int n = 0; n < 16; ++n) {
-    const int col = n * 8 + tq * 2;
-    float* r0p = sO + (warp * 16 + gq) * DH + col;
-    float* r1p = sO + (warp * 16 + gq + 8) * DH + col;
-    r0p[0] = oacc[n][0] * f0;
-    r0p[1] = oacc[n][1] * f0;
-    r1p[0] = oacc[n][2] * f1;
-    r1p[1] = oacc[n][3] * f1;
-  }
-  __syncthreads();
-  // all 128 threads write the merged rows of the G heads
-  for (int i = tid; i < G * DH; i += 128) {
-    const int row = i / DH, col = i % DH;
-    float acc = 0.f, Lr = 0.f, Mr = -INFINITY;
-    for (int w = 0; w < SPLIT; ++w) acc += sO[(w * 16 + row) * DH + col];
-    for (int w = 0; w < SPLIT; ++w) Mr = fmaxf(Mr, sMl[w][0][row]);
-    for (int w = 0; w < SPLIT; ++w) {
-      const float mw = sMl[w][0][row];
-      Lr += (mw == -INFINITY) ? 0.f : sMl[w][1][row] * exp2f(mw - Mr);
-    }
-    O[((long long)r * H + hbase + row) * DH + col] = __float2bfloat16_rn(acc / Lr);
-  }
-  (void)L0;
-  (void)L1;
-}
-
 // K1 decode, per-warp TMA pipeline on tensor cores (any GQA group G <= 16,
 // dh = 128): the bulk kernel's structure — a persistent grid of warps claiming
 // (row, KV head) items from a device counter, each warp streaming its items'
@@ -1745,321 +1207,6 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
   }
 }
 
-// ---------------------------------------------------------------------------
-// K1 tree-group decode (G = 1, dh = 128): the rows of one decode step are
-// grouped by query (at most kGroupRows per group); each group's context is the
-// union of its rows' segments, each segment tagged with the rows that read it.
-// One warp per (group, head) streams every distinct segment ONCE through its
-// TMA ring and runs the group's rows as the M dimension of mma.sync m16n8k16:
-// a shared ancestor (the prompt, a parent thought) is read from L2/HBM and
-// multiplied once per group instead of once per row, and rows that do not
-// read a segment are masked to p = 0. Per-row numerics are those of the
-// per-row kernels up to fp32 summation order.
-
-// Groups of one step: one block; rows grouped by query, ascending row index
-// within a query (deterministic), kGroupRows per group.
-__global__ void __launch_bounds__(1024) build_groups_kernel(const RowDesc* __restrict__ rows, int n, int Q,
-                                                            TreeGroups g) {
-  __shared__ int part_r[1024], part_g[1024];
-  const int tid = threadIdx.x;
-  for (int q = tid; q < Q; q += 1024) {
-    g.q_cnt[q] = 0;
-    g.q_fill[q] = 0;
-  }
-  if (tid == 0) *g.seg_ctr = 0;
-  __syncthreads();
-  for (int r = tid; r < n; r += 1024) atomicAdd(&g.q_cnt[rows[r].q], 1);
-  __syncthreads();
-  const int per = (Q + 1023) / 1024, q0 = tid * per, q1 = min(Q, q0 + per);
-  int sr = 0, sg = 0;
-  for (int q = q0; q < q1; ++q) {
-    const int c = g.q_cnt[q];
-    sr += c;
-    sg += (c + kGroupRows - 1) / kGroupRows;
-  }
-  part_r[tid] = sr;
-  part_g[tid] = sg;
-  __syncthreads();
-  for (int o = 1; o < 1024; o <<= 1) {
-    const int a = tid >= o ? part_r[tid - o] : 0, b = tid >= o ? part_g[tid - o] : 0;
-    __syncthreads();
-    part_r[tid] += a;
-    part_g[tid] += b;
-    __syncthreads();
-  }
-  int rr = part_r[tid] - sr, gg = part_g[tid] - sg;
-  for (int q = q0; q < q1; ++q) {
-    const int c = g.q_cnt[q];
-    g.q_off[q] = rr;
-    g.q_goff[q] = gg;
-    rr += c;
-    gg += (c + kGroupRows - 1) / kGroupRows;
-  }
-  if (tid == 1023) *g.n_groups = part_g[1023];
-  __syncthreads();
-  for (int r = tid; r < n; r += 1024) {
-    const int q = rows[r].q;
-    g.sorted[g.q_off[q] + atomicAdd(&g.q_fill[q], 1)] = r;
-  }
-  __syncthreads();
-  for (int q = tid; q < Q; q += 1024) {
-    const int c = g.q_cnt[q];
-    if (c == 0) continue;
-    int* sl = g.sorted + g.q_off[q];
-    for (int i = 1; i < c; ++i) {  // the atomic fill order is arbitrary: sort
-      const int v = sl[i];
-      int j = i - 1;
-      while (j >= 0 && sl[j] > v) {
-        sl[j + 1] = sl[j];
-        --j;
-      }
-      sl[j + 1] = v;
-    }
-    for (int k = 0; k * kGroupRows < c; ++k) {
-      GroupDesc* gd = g.groups + g.q_goff[q] + k;
-      const int m = min(kGroupRows, c - k * kGroupRows);
-      gd->nrows = m;
-      for (int i = 0; i < m; ++i) gd->row[i] = sl[k * kGroupRows + i];
-    }
-  }
-}
-
-// Union of each group's segments (one thread per group): row 0's segments in
-// path order, then each further row's segments not seen yet; shared ancestors
-// sit at the same index in every row of the group, so they are found in O(1).
-__global__ void build_group_segs_kernel(const RowDesc* __restrict__ rows, const Segment* __restrict__ segs,
-                                        TreeGroups g, int max_groups) {
-  const int gi = blockIdx.x * blockDim.x + threadIdx.x;
-  if (gi >= max_groups || gi >= *g.n_groups) return;
-  GroupDesc* gd = g.groups + gi;
-  const int nr = gd->nrows;
-  int total = 0;
-  for (int i = 0; i < nr; ++i) total += rows[gd->row[i]].nseg;
-  const int off = atomicAdd(g.seg_ctr, total);
-  GroupSeg* out = g.gsegs + off;
-  int cnt = 0;
-  for (int i = 0; i < nr; ++i) {
-    const RowDesc rd = rows[gd->row[i]];
-    for (int k = 0; k < rd.nseg; ++k) {
-      const Segment sgm = segs[rd.seg_off + k];
-      int j;
-      if (k < cnt && out[k].base == sgm.base && out[k].len == sgm.len) {
-        j = k;
-      } else {
-        for (j = 0; j < cnt; ++j)
-          if (out[j].base == sgm.base && out[j].len == sgm.len) break;
-      }
-      if (j < cnt) {
-        out[j].mask |= 1u << i;
-      } else {
-        out[cnt].base = sgm.base;
-        out[cnt].len = sgm.len;
-        out[cnt].mask = 1u << i;
-        ++cnt;
-      }
-    }
-  }
-  gd->seg_off = off;
-  gd->nseg = cnt;
-}
-
-__global__ void __launch_bounds__(kMmaWarps * 32, 1)
-    tree_attn_group_kernel(const __grid_constant__ CUtensorMap kmap16, const __grid_constant__ CUtensorMap vmap16,
-                           const GroupDesc* __restrict__ groups, const GroupSeg* __restrict__ gsegs,
-                           const int* __restrict__ n_groups, const float* __restrict__ Qr, int H, long long slots,
-                           __nv_bfloat16* __restrict__ O, int* __restrict__ item_ctr) {
-  constexpr int DH = 128, CH = 16, STAGE = CH * DH * 2;  // 4 KB of K (and of V) per stage
-  extern __shared__ __align__(1024) unsigned char smem_raw[];
-  unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ uint64_t bar[kMmaWarps][kMmaNST];
-  __shared__ int queue[kMmaWarps][8];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n_items = *n_groups * H;
-  unsigned char* ring = sm + (size_t)warp * kMmaNST * 2 * STAGE;  // [stage][K|V][STAGE]
-  if (lane == 0) {
-    for (int i = 0; i < kMmaNST; ++i) mbar_init(&bar[warp][i], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncwarp();
-  // ---- producer cursor (lane 0 only): item, segment, offset
-  int p_q = 0, p_item = -1, p_seg = 0, p_off = 0, p_nseg = 0, issued = 0;
-  long long p_row0 = 0;
-  const GroupSeg* p_sg = nullptr;
-  bool p_done = false;
-  auto produce = [&]() {
-    while (!p_done) {
-      if (p_item < 0 || p_seg >= p_nseg) {
-        const int it = atomicAdd(item_ctr, 1);
-        if (it >= n_items) {
-          queue[warp][p_q & 7] = -1;
-          p_done = true;
-          return;
-        }
-        queue[warp][p_q & 7] = it;
-        ++p_q;
-        p_item = it;
-        const GroupDesc* gd = groups + it / H;
-        p_sg = gsegs + gd->seg_off;
-        p_nseg = gd->nseg;
-        p_seg = 0;
-        p_off = 0;
-        p_row0 = (long long)(it % H) * slots;
-      }
-      const int len = p_sg[p_seg].len;
-      if (p_off >= len) {
-        ++p_seg;
-        p_off = 0;
-        continue;
-      }
-      const int rowc = (int)(p_row0 + p_sg[p_seg].base + p_off);
-      const int st = issued % kMmaNST;
-      unsigned char* kb = ring + st * 2 * STAGE;
-      mbar_expect_tx(&bar[warp][st], 2 * STAGE);
-      tma_load_2d(kb, &kmap16, 0, rowc, &bar[warp][st]);
-      tma_load_2d(kb + 2048, &kmap16, 64, rowc, &bar[warp][st]);
-      tma_load_2d(kb + STAGE, &vmap16, 0, rowc, &bar[warp][st]);
-      tma_load_2d(kb + STAGE + 2048, &vmap16, 64, rowc, &bar[warp][st]);
-      p_off += CH;
-      ++issued;
-      return;
-    }
-  };
-  if (lane == 0)
-    for (int i = 0; i < kMmaNST - 1; ++i) produce();
-  __syncwarp();
-  const int gq = lane >> 2, tq = lane & 3, mi = lane >> 3, ri = lane & 7;
-  int c_q = 0, consumed = 0;
-  for (;;) {
-    const int it = queue[warp][c_q & 7];
-    if (it < 0) break;
-    ++c_q;
-    const int h = it % H;
-    const GroupDesc* gd = groups + it / H;
-    const int nr = gd->nrows;
-    const bool v0 = gq < nr, v1 = gq + 8 < nr;
-    const int r0 = v0 ? gd->row[gq] : 0, r1 = v1 ? gd->row[gq + 8] : 0;
-    const GroupSeg* sg = gsegs + gd->seg_off;
-    const int nseg = gd->nseg;
-    // Q fragments: MMA rows = the group's rows (gq, gq + 8 < nrows), dims as k
-    uint32_t qa[8][4];
-    {
-      const float* q0 = Qr + ((long long)r0 * H + h) * DH;
-      const float* q1 = Qr + ((long long)r1 * H + h) * DH;
-      constexpr float sc = 1.4426950408889634f;
-#pragma unroll
-      for (int ks = 0; ks < 8; ++ks) {
-        const int k0 = ks * 16 + tq * 2;
-        const float2 x00 = v0 ? *reinterpret_cast<const float2*>(q0 + k0) : make_float2(0.f, 0.f);
-        const float2 x10 = v1 ? *reinterpret_cast<const float2*>(q1 + k0) : make_float2(0.f, 0.f);
-        const float2 x01 = v0 ? *reinterpret_cast<const float2*>(q0 + k0 + 8) : make_float2(0.f, 0.f);
-        const float2 x11 = v1 ? *reinterpret_cast<const float2*>(q1 + k0 + 8) : make_float2(0.f, 0.f);
-        qa[ks][0] = pack_bf16(x00.x * sc, x00.y * sc);
-        qa[ks][1] = pack_bf16(x10.x * sc, x10.y * sc);
-        qa[ks][2] = pack_bf16(x01.x * sc, x01.y * sc);
-        qa[ks][3] = pack_bf16(x11.x * sc, x11.y * sc);
-      }
-    }
-    float oacc[16][4];
-#pragma unroll
-    for (int n = 0; n < 16; ++n) oacc[n][0] = oacc[n][1] = oacc[n][2] = oacc[n][3] = 0.f;
-    float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
-    for (int si = 0; si < nseg; ++si) {
-      const int len = sg[si].len;
-      const uint32_t mask = sg[si].mask;
-      const bool in0 = (mask >> gq) & 1u, in1 = (mask >> (gq + 8)) & 1u;
-      for (int off = 0; off < len; off += CH) {
-        const int n = min(CH, len - off);
-        if (lane == 0) produce();
-        const int st = consumed % kMmaNST;
-        mbar_wait(&bar[warp][st], (uint32_t)((consumed / kMmaNST) & 1));
-        const uint32_t kb = (uint32_t)__cvta_generic_to_shared(ring + st * 2 * STAGE);
-        const uint32_t vb = kb + STAGE;
-        float sacc[2][4];
-#pragma unroll
-        for (int t = 0; t < 2; ++t) sacc[t][0] = sacc[t][1] = sacc[t][2] = sacc[t][3] = 0.f;
-#pragma unroll
-        for (int ks = 0; ks < 8; ++ks) {
-          uint32_t b0, b1, b2, b3;
-          ldsm_x4(kb + swz16((mi >> 1) * 8 + ri, ks * 2 + (mi & 1)), b0, b1, b2, b3);
-          mma_bf16(sacc[0], qa[ks][0], qa[ks][1], qa[ks][2], qa[ks][3], b0, b1);
-          mma_bf16(sacc[1], qa[ks][0], qa[ks][1], qa[ks][2], qa[ks][3], b2, b3);
-        }
-        float mx0 = -INFINITY, mx1 = -INFINITY;
-#pragma unroll
-        for (int t = 0; t < 2; ++t)
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const bool tok = t * 8 + tq * 2 + e < n;
-            sacc[t][e] = tok && in0 ? sacc[t][e] : -INFINITY;
-            sacc[t][2 + e] = tok && in1 ? sacc[t][2 + e] : -INFINITY;
-            mx0 = fmaxf(mx0, sacc[t][e]);
-            mx1 = fmaxf(mx1, sacc[t][2 + e]);
-          }
-#pragma unroll
-        for (int o = 1; o < 4; o <<= 1) {
-          mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, o));
-          mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, o));
-        }
-        const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
-        const float a0 = mn0 == -INFINITY ? 1.f : exp2f(m0 - mn0);
-        const float a1 = mn1 == -INFINITY ? 1.f : exp2f(m1 - mn1);
-        uint32_t pa[4];
-        float ps0 = 0.f, ps1 = 0.f;
-#pragma unroll
-        for (int t = 0; t < 2; ++t) {
-          const float p00 = mn0 == -INFINITY ? 0.f : exp2f(sacc[t][0] - mn0);
-          const float p01 = mn0 == -INFINITY ? 0.f : exp2f(sacc[t][1] - mn0);
-          const float p10 = mn1 == -INFINITY ? 0.f : exp2f(sacc[t][2] - mn1);
-          const float p11 = mn1 == -INFINITY ? 0.f : exp2f(sacc[t][3] - mn1);
-          ps0 += p00 + p01;
-          ps1 += p10 + p11;
-          pa[2 * t] = pack_bf16(p00, p01);
-          pa[2 * t + 1] = pack_bf16(p10, p11);
-        }
-        l0 = l0 * a0 + ps0;
-        l1 = l1 * a1 + ps1;
-        m0 = mn0;
-        m1 = mn1;
-#pragma unroll
-        for (int nn = 0; nn < 16; ++nn) {
-          oacc[nn][0] *= a0;
-          oacc[nn][1] *= a0;
-          oacc[nn][2] *= a1;
-          oacc[nn][3] *= a1;
-        }
-#pragma unroll
-        for (int n2 = 0; n2 < 8; ++n2) {
-          uint32_t b0, b1, b2, b3;
-          ldsm_x4_t(vb + swz16((mi & 1) * 8 + ri, n2 * 2 + (mi >> 1)), b0, b1, b2, b3);
-          mma_bf16(oacc[2 * n2], pa[0], pa[1], pa[2], pa[3], b0, b1);
-          mma_bf16(oacc[2 * n2 + 1], pa[0], pa[1], pa[2], pa[3], b2, b3);
-        }
-        ++consumed;
-        __syncwarp();  // stage fully read before lane 0 refills it
-      }
-    }
-#pragma unroll
-    for (int o = 1; o < 4; o <<= 1) {
-      l0 += __shfl_xor_sync(0xffffffffu, l0, o);
-      l1 += __shfl_xor_sync(0xffffffffu, l1, o);
-    }
-    if (v0) {
-      __nv_bfloat16* o0 = O + ((long long)r0 * H + h) * DH + tq * 2;
-      const float inv = 1.f / l0;
-#pragma unroll
-      for (int nn = 0; nn < 16; ++nn)
-        *reinterpret_cast<uint32_t*>(o0 + nn * 8) = pack_bf16(oacc[nn][0] * inv, oacc[nn][1] * inv);
-    }
-    if (v1) {
-      __nv_bfloat16* o1 = O + ((long long)r1 * H + h) * DH + tq * 2;
-      const float inv = 1.f / l1;
-#pragma unroll
-      for (int nn = 0; nn < 16; ++nn)
-        *reinterpret_cast<uint32_t*>(o1 + nn * 8) = pack_bf16(oacc[nn][2] * inv, oacc[nn][3] * inv);
-    }
-  }
-}
-
 // K1 tile variant for prefill-shaped rows (PRM scoring): kTileRows consecutive
 // rows of one thought share their ancestors and a causal own prefix, so each
 // 64-token K/V chunk is staged once per tile instead of once per row.
@@ -2235,95 +1382,6 @@ __global__ void __launch_bounds__(kAttnThreads) tree_attn_tile_kernel(const Tile
   }
 }
 
-__global__ void swiglu_kernel(const __nv_bfloat16* GU, int M, int F, __nv_bfloat16* A) {
-  pdl_wait();
-  // flat grid-stride over M * F/8 octets (F % 8 == 0), bf16 gate/up in, 16-byte loads
-  const int F8 = F / 8;
-  const long long n = (long long)M * F8;
-  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x) {
-    const long long r = k / F8;
-    const int j = (int)(k - r * F8) * 8;
-    const __nv_bfloat16* g = GU + r * 2 * F;
-    const uint4 gr = *reinterpret_cast<const uint4*>(g + j);
-    const uint4 ur = *reinterpret_cast<const uint4*>(g + F + j);
-    const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&gr);
-    const __nv_bfloat162* u2 = reinterpret_cast<const __nv_bfloat162*>(&ur);
-    uint32_t o[4];
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const float ga = __low2float(g2[e]), gb = __high2float(g2[e]);
-      o[e] = pack_bf16(ga / (1.f + __expf(-ga)) * __low2float(u2[e]), gb / (1.f + __expf(-gb)) * __high2float(u2[e]));
-    }
-    *reinterpret_cast<uint4*>(A + r * F + j) = make_uint4(o[0], o[1], o[2], o[3]);
-  }
-}
-
-// K3: per-row argmax (first max), logsumexp and sum of the logits in one pass
-// (online max / rescaled exp-sum per thread, then a block combine).
-__global__ void __launch_bounds__(256) lm_epilogue_kernel(const float* logits, int M, int V, int* amax,
-                                                          float* lse, float* lsum) {
-  // two branch-free passes over the row (V % 4 == 0): max / first argmax / sum,
-  // then sum exp(x - max) (the row is still in L2)
-  const int r = blockIdx.x;
-  if (r >= M) return;
-  const float4* x = reinterpret_cast<const float4*>(logits + (long long)r * V);
-  const int V4 = V / 4;
-  float mx = -INFINITY, sm = 0.f;
-  int mi = 0x7fffffff;
-  for (int i = threadIdx.x; i < V4; i += blockDim.x) {
-    const float4 v = x[i];
-    sm += (v.x + v.y) + (v.z + v.w);
-    const float m01 = fmaxf(v.x, v.y), m23 = fmaxf(v.z, v.w), m4 = fmaxf(m01, m23);
-    if (m4 > mx) {  // first index of the max inside the quad
-      mx = m4;
-      mi = 4 * i + (v.x == m4 ? 0 : v.y == m4 ? 1 : v.z == m4 ? 2 : 3);
-    }
-  }
-  __shared__ float smx[8], ssm[8], sse[8];
-  __shared__ int smi[8];
-  const int w = threadIdx.x >> 5, nw = blockDim.x >> 5, lane = threadIdx.x & 31;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const float om = __shfl_xor_sync(0xffffffffu, mx, o);
-    const int oi = __shfl_xor_sync(0xffffffffu, mi, o);
-    sm += __shfl_xor_sync(0xffffffffu, sm, o);
-    if (om > mx || (om == mx && oi < mi)) mi = oi;
-    mx = fmaxf(mx, om);
-  }
-  if (lane == 0) {
-    smx[w] = mx;
-    smi[w] = mi;
-    ssm[w] = sm;
-  }
-  __syncthreads();
-  float M0 = smx[0];
-  int I0 = smi[0];
-  float T0 = ssm[0];
-  for (int k = 1; k < nw; ++k) {
-    if (smx[k] > M0 || (smx[k] == M0 && smi[k] < I0)) I0 = smi[k];
-    M0 = fmaxf(M0, smx[k]);
-    T0 += ssm[k];
-  }
-  float se = 0.f;
-  const float ml2 = M0 * 1.4426950408889634f;
-  for (int i = threadIdx.x; i < V4; i += blockDim.x) {
-    const float4 v = x[i];
-    se += exp2f(fmaf(v.x, 1.4426950408889634f, -ml2)) + exp2f(fmaf(v.y, 1.4426950408889634f, -ml2)) +
-          exp2f(fmaf(v.z, 1.4426950408889634f, -ml2)) + exp2f(fmaf(v.w, 1.4426950408889634f, -ml2));
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
-  if (lane == 0) sse[w] = se;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    float S0 = 0.f;
-    for (int k = 0; k < nw; ++k) S0 += sse[k];
-    amax[r] = I0;
-    lse[r] = M0 + logf(S0);
-    lsum[r] = T0;
-  }
-}
-
 // K4: PRM value head on the last token of each scored thought.
 __global__ void value_head_kernel(const __nv_bfloat16* Hn, int d, const int* last_row, int n,
                                   const __nv_bfloat16* w, float* score) {
@@ -2434,13 +1492,6 @@ extern "C" void spex_k_rmsnorm(const float* X, int M, int d, float eps, __nv_bfl
       default: break;
     }
   launch_maybe_pdl(rmsnorm_bf16_kernel, grid, block, 0, s, X, M, d, eps, Y);
-}
-
-extern "C" void spex_k_rope_kv(const RowDesc* rows, int M, const __nv_bfloat16* QKV, int H, int KVH, int dh,
-                               const float* cs_tab, long long slots, __nv_bfloat16* Kp, __nv_bfloat16* Vp,
-                               float* Qr, cudaStream_t s) {
-  launch_maybe_pdl(rope_kv_kernel, dim3(M), dim3(128), 0, s, rows, M, QKV, H, KVH, dh,
-                   reinterpret_cast<const float2*>(cs_tab), slots, Kp, Vp, Qr);
 }
 
 template <int DH, int G>
@@ -2572,36 +1623,6 @@ extern "C" int spex_k_tree_attn_bulk(const RowDesc* rows, const Segment* segs, c
 
 // K1 decode rows on the per-warp TMA + mma.sync pipeline (G <= 16, dh = 128);
 // kmap16/vmap16 are the pools' 2D maps with 64 x 16 boxes (spex_tmap_kv16).
-// Groups of one decode step (shared by its L K1 launches).
-extern "C" void spex_k_build_groups(const RowDesc* rows, const Segment* segs, int M, int Q, TreeGroups g,
-                                    cudaStream_t s) {
-  if (M <= 0) return;
-  build_groups_kernel<<<1, 1024, 0, s>>>(rows, M, Q, g);
-  build_group_segs_kernel<<<(M + 127) / 128, 128, 0, s>>>(rows, segs, g, M);
-}
-
-// K1 decode rows by query groups (G = 1, dh = 128); the groups come from
-// spex_k_build_groups of the same rows. item_ctr is zeroed here per launch.
-extern "C" int spex_k_tree_attn_group(const CUtensorMap* kmap16, const CUtensorMap* vmap16, const TreeGroups* g,
-                                      const float* Qr, int H, int KVH, int dh, long long slots, __nv_bfloat16* O,
-                                      int M, int* item_ctr, cudaStream_t s) {
-  if (M <= 0) return 0;
-  if (dh != 128 || H != KVH) return -1;
-  constexpr int smem = kMmaWarps * kMmaNST * 2 * 16 * 128 * 2 + 1024;
-  static int blocks = 0;
-  if (!blocks) {
-    cudaFuncSetAttribute(tree_attn_group_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    int dev = 0, sms = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    blocks = sms;
-  }
-  const int grid = std::min(blocks, (M * H + kMmaWarps - 1) / kMmaWarps);  // groups <= rows
-  cudaMemsetAsync(item_ctr, 0, sizeof(int), s);
-  tree_attn_group_kernel<<<grid, kMmaWarps * 32, smem, s>>>(*kmap16, *vmap16, g->groups, g->gsegs, g->n_groups, Qr,
-                                                            H, slots, O, item_ctr);
-  return (int)cudaGetLastError();
-}
 
 template <int NST, int W, bool SKIP = false>
 static int launch_wmma(const CUtensorMap* kmap16, const CUtensorMap* vmap16, const RowDesc* rows, const Segment* segs,
@@ -2642,50 +1663,6 @@ extern "C" int spex_k_tree_attn_wmma(const CUtensorMap* kmap16, const CUtensorMa
     default: return launch_wmma<kMmaNST, kMmaWarps>(kmap16, vmap16, rows, segs, Qr, H, KVH, G, slots, O, M, item_ctr,
                                                     s);
   }
-}
-
-extern "C" void spex_k_build_decode_chunks(const RowDesc* rows, const Segment* segs, int M, DecodeChunks w,
-                                           cudaStream_t s) {
-  build_decode_chunks_kernel<<<1, 1024, 0, s>>>(rows, segs, M, w);
-}
-
-template <int DH, int G>
-static void launch_attn_chunk(const RowDesc* rows, const Segment* segs, const float* Qr, int H, int KVH,
-                              const __nv_bfloat16* Kp, const __nv_bfloat16* Vp, long long slots, __nv_bfloat16* O,
-                              const DecodeChunks& w, int* qctr, cudaStream_t s) {
-  static int blocks = 0;
-  if (!blocks) {
-    int dev = 0, sms = 0, per = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, tree_attn_chunk_kernel<DH, G>, 256, 0);
-    blocks = sms * (per > 0 ? per : 1);
-  }
-  tree_attn_chunk_kernel<DH, G><<<blocks, 256, 0, s>>>(rows, segs, Qr, H, KVH, Kp, Vp, slots, O, w, qctr);
-}
-
-// K1 decode over the step's chunked work list (spex_k_build_decode_chunks);
-// qslot selects this launch's work-queue counter (one per layer).
-extern "C" int spex_k_tree_attn_chunked(const RowDesc* rows, const Segment* segs, const float* Qr, int H, int KVH,
-                                        int dh, const __nv_bfloat16* Kp, const __nv_bfloat16* Vp, long long slots,
-                                        __nv_bfloat16* O, DecodeChunks w, int qslot, cudaStream_t s) {
-  const int G = H / KVH;
-  int* qctr = w.qctr + (qslot % kQueueSlots);
-#define SPEX_CHUNK_CASE(D, GG)                                                        \
-  if (dh == D && G == GG) {                                                           \
-    launch_attn_chunk<D, GG>(rows, segs, Qr, H, KVH, Kp, Vp, slots, O, w, qctr, s);   \
-    return 0;                                                                         \
-  }
-  SPEX_CHUNK_CASE(128, 1)
-  SPEX_CHUNK_CASE(128, 2)
-  SPEX_CHUNK_CASE(128, 4)
-  SPEX_CHUNK_CASE(128, 6)
-  SPEX_CHUNK_CASE(128, 8)
-  SPEX_CHUNK_CASE(64, 1)
-  SPEX_CHUNK_CASE(64, 2)
-  SPEX_CHUNK_CASE(64, 4)
-#undef SPEX_CHUNK_CASE
-  return -1;
 }
 
 template <int DH, int G>
@@ -2730,24 +1707,6 @@ extern "C" int spex_k_tree_attn_tiles_mma(const CUtensorMap* kmap, const CUtenso
   return -1;
 }
 
-// K1 decode rows on tensor cores (GQA groups G in [2, 16], dh = 128).
-extern "C" int spex_k_tree_attn_decode_mma(const CUtensorMap* kmap, const CUtensorMap* vmap, const RowDesc* rows,
-                                           const Segment* segs, const float* Qr, int H, int KVH, int dh,
-                                           long long slots, __nv_bfloat16* O, int M, cudaStream_t s) {
-  const int G = H / KVH;
-  if (M <= 0) return 0;
-  if (dh != 128 || G < 1 || G > 16) return -1;
-  const size_t smem = 2 * 32768 + 1024;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(tree_attn_decode_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
-  dim3 grid(M, KVH);
-  tree_attn_decode_mma_kernel<<<grid, 128, smem, s>>>(*kmap, *vmap, rows, segs, Qr, H, slots, O, G);
-  return (int)cudaGetLastError();
-}
-
 extern "C" int spex_k_tree_attn_tiles(const TileDesc* tiles, int ntiles, const RowDesc* rows, const Segment* segs,
                                       const float* Qr, int H, int KVH, int dh, const __nv_bfloat16* Kp,
                                       const __nv_bfloat16* Vp, long long slots, __nv_bfloat16* O, cudaStream_t s) {
@@ -2766,17 +1725,6 @@ extern "C" int spex_k_tree_attn_tiles(const TileDesc* tiles, int ntiles, const R
   SPEX_TILE_CASE(64, 2)
 #undef SPEX_TILE_CASE
   return -1;
-}
-
-extern "C" void spex_k_swiglu(const __nv_bfloat16* GU, int M, int F, __nv_bfloat16* A, cudaStream_t s) {
-  const long long octets = (long long)M * (F / 8);
-  const int blocks = (int)std::min<long long>((octets + 255) / 256, 148 * 16);
-  launch_maybe_pdl(swiglu_kernel, dim3(blocks), dim3(256), 0, s, GU, M, F, A);
-}
-
-extern "C" void spex_k_lm_epilogue(const float* logits, int M, int V, int* amax, float* lse, float* lsum,
-                                   cudaStream_t s) {
-  lm_epilogue_kernel<<<M, 256, 0, s>>>(logits, M, V, amax, lse, lsum);
 }
 
 extern "C" void spex_k_value_head(const __nv_bfloat16* Hn, int d, const int* last_row, int n,

@@ -21,20 +21,7 @@ ROW = np.dtype([("q", "<i4"), ("node", "<u4"), ("pos", "<i4"), ("abs_pos", "<i4"
                 ("seg_off", "<i4"), ("nseg", "<i4"), ("token", "<i4"), ("pad", "<i4")])
 SEG = np.dtype([("base", "<i8"), ("len", "<i4"), ("pad", "<i4")])
 MAX_SEG = 40
-N_QUERIES = 5  # rows are spread over a few queries (the tree-group kernel groups by query)
-
-
-class DecodeChunks(ctypes.Structure):
-    """model.h DecodeChunks (device pointers)."""
-    _fields_ = [(n, ctypes.c_void_p) for n in
-                ("items", "row_nch", "row_ch", "row_item0", "n_items", "qctr", "part", "cnt")]
-
-
-class TreeGroups(ctypes.Structure):
-    """model.h TreeGroups (device pointers)."""
-    _fields_ = [(n, ctypes.c_void_p) for n in
-                ("q_cnt", "q_off", "q_goff", "q_fill", "sorted", "groups", "gsegs", "n_groups", "seg_ctr")] + \
-               [("q_cap", ctypes.c_int), ("seg_cap", ctypes.c_longlong)]
+N_QUERIES = 5  # rows are spread over a few queries
 
 
 def _lib():
@@ -48,15 +35,7 @@ def _lib():
     f.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                   ctypes.c_void_p, ctypes.c_void_p, ctypes.c_longlong, ctypes.c_void_p, ctypes.c_int,
                   ctypes.c_void_p]
-    b = lib.spex_k_build_decode_chunks
-    b.restype = None
-    b.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, DecodeChunks, ctypes.c_void_p]
-    c = lib.spex_k_tree_attn_chunked
-    c.restype = ctypes.c_int
-    c.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
-                  ctypes.c_void_p, ctypes.c_void_p, ctypes.c_longlong, ctypes.c_void_p, DecodeChunks, ctypes.c_int,
-                  ctypes.c_void_p]
-    return f, b, c
+    return f
 
 
 def _make_tree_rows(rng, M, slots, max_depth):
@@ -90,15 +69,15 @@ def _make_tree_rows(rng, M, slots, max_depth):
     return rows, segs, paths
 
 
-@pytest.mark.parametrize("impl", ["row", "chunked", "mma", "bulk", "wmma", "group"])
+@pytest.mark.parametrize("impl", ["row", "bulk", "wmma"])
 @pytest.mark.parametrize("H,KVH,dh,M", [(8, 8, 128, 300), (32, 8, 128, 97), (12, 2, 128, 80), (4, 2, 64, 150), (16, 4, 64, 64)])
 def test_k1_decode_matches_torch_fp32(H, KVH, dh, M, impl):
-    """impl "row": one warp per (row, kv head) (spex_k_tree_attn); "chunked": the
-    decode work list (spex_k_build_decode_chunks + spex_k_tree_attn_chunked),
-    rows up to ~2.4k tokens split into up to 8 chunks merged by the last warp,
-    launched twice to exercise the self-resetting arrival counters."""
+    """impl "row": one warp per (row, kv head), register pipeline (spex_k_tree_attn);
+    "bulk": the bulk-copy pipeline (G = 1), launched twice to exercise its
+    self-resetting work counter; "wmma": the per-warp TMA + tensor-core
+    pipeline (GQA groups)."""
     import torch
-    f, build, chunked = _lib()
+    f = _lib()
     rng = np.random.default_rng(H * 1000 + dh + M)
     slots = 200 * max(8, M // 2) + 64
     rows, segs, paths = _make_tree_rows(rng, M, slots, max_depth=12)
@@ -135,40 +114,6 @@ def test_k1_decode_matches_torch_fp32(H, KVH, dh, M, impl):
         rc = fw(kp, vp, rows_d.data_ptr(), segs_d.data_ptr(), Q.data_ptr(), H, KVH, dh, slots, O.data_ptr(), M,
                 ctr.data_ptr(), st.cuda_stream)
         assert rc == 0
-    elif impl == "group":
-        if dh != 128 or H != KVH:
-            pytest.skip("tree-group decode kernel is dh=128, G=1")
-        from paper_2605_10195_b200 import _lib as L
-        lib = L.lib()
-        lib.spex_tmap_kv16.restype = ctypes.c_int
-        lib.spex_tmap_kv16.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_longlong, ctypes.c_int]
-        bg = lib.spex_k_build_groups
-        bg.restype = None
-        bg.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int, TreeGroups, ctypes.c_void_p]
-        fg = lib.spex_k_tree_attn_group
-        fg.restype = ctypes.c_int
-        fg.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(TreeGroups), ctypes.c_void_p, ctypes.c_int,
-                       ctypes.c_int, ctypes.c_int, ctypes.c_longlong, ctypes.c_void_p, ctypes.c_int,
-                       ctypes.c_void_p, ctypes.c_void_p]
-        km, vm = ctypes.create_string_buffer(256), ctypes.create_string_buffer(256)
-        kp, vp = (ctypes.addressof(km) + 63) & ~63, (ctypes.addressof(vm) + 63) & ~63
-        assert lib.spex_tmap_kv16(kp, K.data_ptr(), KVH * slots, dh) == 0
-        assert lib.spex_tmap_kv16(vp, V.data_ptr(), KVH * slots, dh) == 0
-        i32 = lambda n: torch.zeros(n, dtype=torch.int32, device=dev)  # noqa: E731
-        gb = {"q_cnt": i32(N_QUERIES), "q_off": i32(N_QUERIES), "q_goff": i32(N_QUERIES), "q_fill": i32(N_QUERIES),
-              "sorted": i32(M), "groups": i32(M * 20), "gsegs": i32(M * MAX_SEG * 4), "n_groups": i32(1),
-              "seg_ctr": i32(1)}
-        tg = TreeGroups(**{k: v.data_ptr() for k, v in gb.items()}, q_cap=N_QUERIES, seg_cap=M * MAX_SEG)
-        ctr = torch.zeros(1, dtype=torch.int32, device=dev)
-        for _ in range(2):  # rebuilt per step: the builder re-zeroes its counters
-            O.zero_()
-            bg(rows_d.data_ptr(), segs_d.data_ptr(), M, N_QUERIES, tg, st.cuda_stream)
-            rc = fg(kp, vp, ctypes.byref(tg), Q.data_ptr(), H, KVH, dh, slots, O.data_ptr(), M, ctr.data_ptr(),
-                    st.cuda_stream)
-            assert rc == 0
-        torch.cuda.synchronize()
-        qs = rows["q"]
-        assert int(gb["n_groups"].item()) == sum((int((qs == q).sum()) + 15) // 16 for q in range(N_QUERIES))
     elif impl == "bulk":
         if dh != 128 or H != KVH:
             pytest.skip("bulk-copy decode kernel is dh=128, G=1")
@@ -188,44 +133,6 @@ def test_k1_decode_matches_torch_fp32(H, KVH, dh, M, impl):
         rc = fb(rows_d.data_ptr(), segs_d.data_ptr(), Q.data_ptr(), H, KVH, dh, K.data_ptr(), V.data_ptr(), slots,
                 O.data_ptr(), M, ctr.data_ptr(), st.cuda_stream)  # second launch on the reset counter
         assert rc == 0
-    elif impl == "mma":
-        if dh != 128:
-            pytest.skip("tensor-core decode kernel is dh=128")
-        from paper_2605_10195_b200 import _lib as L
-        lib = L.lib()
-        lib.spex_tmap_kv.restype = ctypes.c_int
-        lib.spex_tmap_kv.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_longlong, ctypes.c_int]
-        fm = lib.spex_k_tree_attn_decode_mma
-        fm.restype = ctypes.c_int
-        fm.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
-                       ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_longlong, ctypes.c_void_p, ctypes.c_int,
-                       ctypes.c_void_p]
-        km, vm = ctypes.create_string_buffer(256), ctypes.create_string_buffer(256)
-        kp, vp = (ctypes.addressof(km) + 63) & ~63, (ctypes.addressof(vm) + 63) & ~63
-        assert lib.spex_tmap_kv(kp, K.data_ptr(), KVH * slots, dh) == 0
-        assert lib.spex_tmap_kv(vp, V.data_ptr(), KVH * slots, dh) == 0
-        rc = fm(kp, vp, rows_d.data_ptr(), segs_d.data_ptr(), Q.data_ptr(), H, KVH, dh, slots, O.data_ptr(), M,
-                st.cuda_stream)
-        assert rc == 0
-    else:
-        bufs = {"items": torch.zeros(M * 8 * 2, dtype=torch.int32, device=dev),
-                "row_nch": torch.zeros(M, dtype=torch.int32, device=dev),
-                "row_ch": torch.zeros(M, dtype=torch.int32, device=dev),
-                "row_item0": torch.zeros(M, dtype=torch.int32, device=dev),
-                "n_items": torch.zeros(1, dtype=torch.int32, device=dev),
-                "qctr": torch.zeros(256, dtype=torch.int32, device=dev),
-                "part": torch.zeros(M * 8 * H * (dh + 4), dtype=torch.float32, device=dev),
-                "cnt": torch.zeros(M * KVH, dtype=torch.int32, device=dev)}
-        w = DecodeChunks(**{k: v.data_ptr() for k, v in bufs.items()})
-        build(rows_d.data_ptr(), segs_d.data_ptr(), M, w, st.cuda_stream)
-        for slot in range(2):
-            O.zero_()
-            rc = chunked(rows_d.data_ptr(), segs_d.data_ptr(), Q.data_ptr(), H, KVH, dh, K.data_ptr(), V.data_ptr(),
-                         slots, O.data_ptr(), w, slot, st.cuda_stream)
-            assert rc == 0
-        torch.cuda.synchronize()
-        assert int(bufs["cnt"].abs().sum()) == 0  # counters reset by the merging warps
-        assert int(bufs["row_nch"].max()) > 1      # multi-chunk rows exercised
     torch.cuda.synchronize()
     Kf, Vf = K.float(), V.float()
     G = H // KVH

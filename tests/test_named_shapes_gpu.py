@@ -4,7 +4,9 @@ tests/test_model_oracle_cpu.py), at north_star's stated tolerance:
 
   logsumexp  |d| <= 1e-3 * max(1, |lse|)        (1e-3 relative)
   PRM score  |d| <= 1e-3 * |score|               (1e-3 relative)
-  argmax     equal, unless the oracle's top-2 logits are within 1e-3 * max(1, |top|)
+  argmax     equal, unless the device's token loses to the oracle's argmax by
+             at most 2e-3 * max(1, |lse|) in fp32 logits (each logit within
+             1e-3 * max(1, |lse|): two logits that close may swap at bf16)
   logit sum  |d| <= 1e-3 * sum |z|               (a sum of V fp32 logits)
 
 Config 5 with the named shapes (Llama-3-8B-shaped policy, 1.5B-shaped PRM):
@@ -63,14 +65,15 @@ def _check(cfgname, policy, prm, wseed, n_rows=50, n_scores=50):
         top = max(r[2] for r in rows)
         toks = tree.sequence(q, node, top, pol.V)
         base = len(toks) - 1 - top
-        am, lse, lsum, gap = pol.logits_stats_all(toks, [base + r[2] for r in rows])
+        am, lse, lsum, gap = pol.logits_stats_all(toks, [base + r[2] for r in rows], cand=[r[3] for r in rows])
         z_abs = None
         for i, (_, _, pos, amax, got_lse, got_sum) in enumerate(rows):
             rel = abs(got_lse - lse[i]) / max(1.0, abs(lse[i]))
             worst["lse_rel"] = max(worst["lse_rel"], rel)
             assert rel <= TOL, (q, node, pos, lse[i], got_lse)
             if amax != am[i]:
-                assert gap[i] <= TOL * max(1.0, abs(lse[i])), (q, node, pos, am[i], amax, gap[i])
+                worst["argmax_flips"] = worst.get("argmax_flips", 0) + 1
+                assert gap[i] <= 2 * TOL * max(1.0, abs(lse[i])), (q, node, pos, am[i], amax, gap[i])
             if z_abs is None:
                 h = pol.forward(toks)[base + pos]
                 z_abs = float((h @ pol.lm.to(torch.float32).T).abs().sum())

@@ -18,7 +18,7 @@ if [ "$MODE" = "full" ]; then
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -s 30000 -c 6000 --csv --log-file $OUT/launches_$TAG.csv \
     python tools/model_timing.py c2_rebase_w16_q256 mid_policy mid_prm > $OUT/launches_$TAG.log 2>&1
   timeout 300 python tools/gemm_bench.py > $OUT/gemm_bench_$TAG.log 2>&1
-  timeout 600 ncu --set full --clock-control none -k 'regex:nvjet' -s 2000 -c 4 -o $OUT/gemm_$TAG \
+  timeout 600 ncu --set full --clock-control none -k 'regex:gemm_tc' -s 2000 -c 4 -o $OUT/gemm_$TAG \
     python tools/model_timing.py c2_rebase_w16_q256 mid_policy mid_prm > $OUT/ncu_gemm_$TAG.log 2>&1
 fi
 SPEX_ATTN_LOG=$OUT/k1_bytes_$TAG.txt timeout 900 ncu --set full --clock-control none --import-source on \
