@@ -78,6 +78,20 @@ typedef struct spex_model_stats {
   int pad_;
 } spex_model_stats;
 
+/* Paged tree-KV store of the last run (pages of page_tokens tokens in the
+ * policy and PRM KV pools; the root prompts hold root_pages static pages). */
+typedef struct spex_kv_stats {
+  long long pages;             /* pool pages */
+  long long page_tokens;       /* tokens per page (16) */
+  long long root_pages;        /* static root-prompt pages */
+  long long peak_pages;        /* most pages held by live thoughts at once */
+  long long freed_pages;       /* pages returned to the free ring */
+  long long live_pages_end;    /* pages still held at the end (roots + undrained) */
+  long long allocated_pages;   /* page-table entries handed out (root + thought pages) */
+  long long fresh_pages;       /* distinct pages ever touched (high-water mark of the pool) */
+  long long page_table_entries;
+} spex_kv_stats;
+
 /* Per decode row-step shadow output (K3): argmax, logsumexp, logit sum. */
 typedef struct spex_decode_out {
   int q;
@@ -132,6 +146,16 @@ int spex_executor_set_model(spex_executor* ex, const char* policy_shape, const c
  * (one server); SURVEY.md §8e. */
 int spex_executor_set_shard(spex_executor* ex, int rank, int world);
 int spex_executor_model_stats(spex_executor* ex, spex_model_stats* out);
+/* Tree-KV pool size in pages (0 = the default: the resident pools, else 55%
+ * of free HBM). Pages of dead thoughts (pruned, REBASE layers expanded,
+ * scored terminals, finished queries) are reused (no reference counterpart:
+ * the reference holds no KV, SearchTree::prune_subtree tree.cpp:119-141 and
+ * finish_query executor.cpp:234-336 define when a thought dies). The run fails
+ * with CapacityTreeKV when the live thoughts exceed the pool. Call before
+ * spex_executor_run; with the host emulation library it enables the page
+ * bookkeeping without a model. */
+int spex_executor_set_kv_pages(spex_executor* ex, long long pages);
+int spex_executor_kv_stats(spex_executor* ex, spex_kv_stats* out);
 /* Copies up to cap records; *n receives the total available. */
 int spex_executor_decode_outputs(spex_executor* ex, void* buf, long long cap, long long* n);
 int spex_executor_prm_outputs(spex_executor* ex, void* buf, long long cap, long long* n);

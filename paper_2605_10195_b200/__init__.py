@@ -186,6 +186,15 @@ class Executor:
         every rank's decisions and log equal the single-server reference's."""
         _check(self._L.spex_executor_set_shard(self._h, int(rank), int(world)))
 
+    def set_kv_pages(self, pages: int) -> None:
+        """Tree-KV pool size in pages of 16 tokens (0: the default, 55% of free HBM)."""
+        _check(self._L.spex_executor_set_kv_pages(self._h, int(pages)))
+
+    def kv_stats(self) -> dict:
+        s = _lib.KvStats()
+        _check(self._L.spex_executor_kv_stats(self._h, ctypes.byref(s)))
+        return s.as_dict()
+
     def model_stats(self) -> dict:
         s = _lib.ModelStats()
         _check(self._L.spex_executor_model_stats(self._h, ctypes.byref(s)))

@@ -99,6 +99,17 @@ class PrmOut(ctypes.Structure):
     _fields_ = [("q", ctypes.c_int), ("node", ctypes.c_uint32), ("score", ctypes.c_float), ("pad_", ctypes.c_int)]
 
 
+class KvStats(ctypes.Structure):
+    """spex_kv_stats (the paged tree-KV store of the last run)."""
+
+    _fields_ = [(n, ctypes.c_longlong) for n in (
+        "pages", "page_tokens", "root_pages", "peak_pages", "freed_pages", "live_pages_end", "allocated_pages",
+        "fresh_pages", "page_table_entries")]
+
+    def as_dict(self) -> dict:
+        return {n: getattr(self, n) for n, _ in self._fields_}
+
+
 _EXPORTS = {
     "spex_last_error": ([], ctypes.c_char_p),
     "spex_free": ([ctypes.c_void_p], None),
@@ -124,6 +135,8 @@ _EXPORTS = {
         [ctypes.c_void_p, ctypes.c_char_p, ctypes.c_char_p, ctypes.c_uint64, ctypes.c_int], ctypes.c_int),
     "spex_executor_set_shard": ([ctypes.c_void_p, ctypes.c_int, ctypes.c_int], ctypes.c_int),
     "spex_executor_model_stats": ([ctypes.c_void_p, ctypes.POINTER(ModelStats)], ctypes.c_int),
+    "spex_executor_set_kv_pages": ([ctypes.c_void_p, ctypes.c_longlong], ctypes.c_int),
+    "spex_executor_kv_stats": ([ctypes.c_void_p, ctypes.POINTER(KvStats)], ctypes.c_int),
     "spex_executor_decode_outputs": (
         [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_longlong, ctypes.POINTER(ctypes.c_longlong)], ctypes.c_int),
     "spex_executor_prm_outputs": (

@@ -44,6 +44,76 @@ SPEX_HDNI void set_err(Run* R, int code, int q, u32 node) {
 #endif
 }
 
+SPEX_HD i64 atomic_add_i64(i64* p, i64 v) {
+#if SPEX_DEVICE_PASS
+  return static_cast<i64>(atomicAdd(reinterpret_cast<unsigned long long*>(p),
+                                    static_cast<unsigned long long>(v)));
+#else
+  i64 o = *p;
+  *p += v;
+  return o;
+#endif
+}
+
+SPEX_HD int atomic_add_int(int* p, int v) {
+#if SPEX_DEVICE_PASS
+  return atomicAdd(p, v);
+#else
+  int o = *p;
+  *p += v;
+  return o;
+#endif
+}
+
+// ------------------------------------------------------- paged tree-KV store
+// A thought's K/V rows live in pages of kKvPage tokens (ctl_state.h). Each
+// node carries a hold count: its own pin (it may still get children: cleared
+// when it is pruned, when its REBASE layer has been expanded, or when its
+// query finishes; terminal thoughts never get one), one per child that still
+// holds pages, and one while its decode stream is in the engine (released at
+// the stream's completion, after the completion boundary's PRM batch is
+// recorded, or when a staged stream is erased). The last release pushes the
+// node's pages to the free ring and releases the parent's child hold.
+//
+// Reuse needs no fence against the forward, which lags behind the control:
+// the policy and PRM forwards each run the schedule entries in order on one
+// stream, a freed node is read only by entries recorded before it died, and
+// the thought that reuses its pages writes them only in entries recorded
+// after its spawn (tree.cpp:119-141 prune, executor.cpp:587-656 layers,
+// executor.cpp:234-336 finish define when a thought can have no reader).
+SPEX_HD bool kv_on(const Cfg& c, int q) { return c.kv_pages > 0 && q_owned(c, q); }
+
+SPEX_HDNI void kv_release(Run* R, int q, u32 node) {
+  const Cfg& c = R->cfg;
+  const u32 b = static_cast<u32>(q) * static_cast<u32>(c.node_cap);
+  while (node != kNoNode) {
+    const int old = atomic_add_int(&R->n_kvh[b + node], -1);
+    if (old > 1) return;
+    if (old < 1) {
+      set_err(R, ERR_INTERNAL, q, node);  // hold underflow
+      return;
+    }
+    if (node == 0) return;  // root prompt pages are static
+    const i64 pt = R->n_kvbase[b + node];
+    if (pt >= 0) {
+      const int np = kv_pages_of(R->n_tokens[b + node]);
+      const i64 pos = atomic_add_i64(&R->g->kv_free_tail, np);
+      for (int k = 0; k < np; ++k) R->kv_free[(pos + k) % c.kv_pages] = R->kv_pt[pt + k];
+      atomic_add_i64(&R->g->kv_live, -np);
+      atomic_add_i64(&R->g->kv_freed, np);
+    }
+    node = R->n_parent[b + node];
+  }
+}
+
+// Drop the node's own pin (it can get no more children).
+SPEX_HD void kv_unpin(Run* R, int q, u32 node) {
+  const u32 i = static_cast<u32>(q) * static_cast<u32>(R->cfg.node_cap) + node;
+  if (!kv_on(R->cfg, q) || !(R->n_flags[i] & NF_KV_SELF)) return;
+  R->n_flags[i] &= static_cast<u16>(~NF_KV_SELF);
+  kv_release(R, q, node);
+}
+
 struct QC {
   Run* R;
   int q;
@@ -231,6 +301,7 @@ SPEX_HDNI int prune_subtree(const QC& x, u32 id) {
       if (counted_live(x, cur)) x.qr->live_cache -= R->n_tokens[ci];
       if (R->n_status[ci] == kTerminalAnswer) x.qr->terminal_count -= 1;
       R->n_status[ci] = kPruned;
+      kv_unpin(R, x.q, cur);
       ++pruned;
     }
     // children are pushed in slot order and popped in reverse, as in the reference;
@@ -527,6 +598,13 @@ SPEX_HDNI u32 spawn_child(const QC& x, u32 parent, bool spec, int dist) {
   if (id == kNoNode) return id;
   bool term = oracle_is_terminal(x, id);
   if (term) set_fl(x, id, NF_TERMINAL);
+  R->n_kvbase[NI(x, id)] = -1;
+  if (kv_on(*x.c, x.q)) {
+    // own pin (non-terminal) + the stream's; the child holds its parent
+    R->n_kvh[NI(x, id)] = term ? 1 : 2;
+    if (!term) set_fl(x, id, NF_KV_SELF);
+    atomic_add_int(&R->n_kvh[pi], 1);
+  }
   if (Rec* r = new_rec(x, EV_NODE, id)) {
     r->a = static_cast<int>(parent);
     r->b = slot;
@@ -598,6 +676,7 @@ SPEX_HDNI void cancel_stream(const QC& x, u32 node) {
     x.it->spw[-2 - sref].cancelled = 1;
     x.it->sdelta -= 1;
     R->n_stream[ni] = -1;
+    if (kv_on(*x.c, x.q)) kv_release(R, x.q, node);  // the stream never ran
     return;
   }
   u8 s = R->st_state[sref];
@@ -612,6 +691,7 @@ SPEX_HDNI void cancel_stream(const QC& x, u32 node) {
     R->st_state[sref] = ST_GONE;
     x.it->sdelta -= 1;
     R->n_stream[ni] = -1;
+    if (kv_on(*x.c, x.q)) kv_release(R, x.q, node);  // erased before it started
   }
 }
 
@@ -683,6 +763,9 @@ SPEX_HDNI void finish_query(const QC& x, bool early) {
     int cnt = prune_subtree(x, id);
     if (Rec* r = new_rec(x, EV_PRUNE, id)) r->a = cnt;
   }
+  // the finished tree gets no more children: its thoughts' pages go as soon
+  // as their streams and scoring are done
+  for (u32 id = 0; id < n; ++id) kv_unpin(R, x.q, id);
   // conservation accounting
   for (u32 id = 1; id < n; ++id) {
     u32 ni = NI(x, id);

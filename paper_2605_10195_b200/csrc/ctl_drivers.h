@@ -289,6 +289,7 @@ SPEX_HDNI void advance_layer(const QC& x) {
         set_fl(x, c, NF_COHORT_PENDING);
         qr->cohort_pending += 1;
       }
+      kv_unpin(R, x.q, parent);  // an expanded layer gets no more children (executor.cpp:587-656)
     }
     qr->layer_n = 0;
     if (qr->cohort_pending > 0) return;

@@ -184,27 +184,6 @@ SPEX_HDNI double ex_minmax_d(EX& ex, double v, bool want_max) {
 #endif
 }
 
-SPEX_HD i64 atomic_add_i64(i64* p, i64 v) {
-#if SPEX_DEVICE_PASS
-  return static_cast<i64>(atomicAdd(reinterpret_cast<unsigned long long*>(p),
-                                    static_cast<unsigned long long>(v)));
-#else
-  i64 o = *p;
-  *p += v;
-  return o;
-#endif
-}
-
-SPEX_HD int atomic_add_int(int* p, int v) {
-#if SPEX_DEVICE_PASS
-  return atomicAdd(p, v);
-#else
-  int o = *p;
-  *p += v;
-  return o;
-#endif
-}
-
 // --------------------------------------------------------------- engine math
 // sim.cpp:277-289
 SPEX_HD double eng_elapsed(const GState* g, int steps) {
@@ -573,7 +552,15 @@ SPEX_HDNI void admit_query(Run* R, int q, Rec* rec_slot) {
   R->n_stream[b] = -1;
   R->n_ready[b] = 0;
   R->n_refc[b] = 0;
-  R->n_kvbase[b] = static_cast<i64>(q) * c.prompt_tokens;
+  R->n_kvbase[b] = -1;
+  if (kv_on(c, q)) {
+    // the root prompt's pages are static: query q owns pages [q*pp, (q+1)*pp)
+    const i64 p0 = static_cast<i64>(q) * c.kv_pp_root;
+    for (int k = 0; k < c.kv_pp_root; ++k) R->kv_pt[p0 + k] = static_cast<int>(p0 + k);
+    R->n_kvbase[b] = p0;
+    R->n_kvh[b] = 1;
+    R->n_flags[b] |= NF_KV_SELF;
+  }
   if (c.family == kRebaseBfs) {
     R->q_layer[b] = 0;
     qr->layer_n = 1;
@@ -655,8 +642,15 @@ SPEX_HDNI void process_items(Run* R, EX& ex, int n_items, int kind, int rank_fil
       R->it_fin[i] = it.fin;
       R->it_sdelta[i] = it.sdelta;
       {
+        // tree-KV pages of the spawns that still hold them (a stream erased
+        // in this very step frees a terminal thought before it has pages)
         int tk = 0;
-        for (int j = 0; j < it.nspw; ++j) tk += it.spw[j].tokens;
+        for (int j = 0; j < it.nspw; ++j) {
+          SpawnRec& sp = it.spw[j];
+          const u32 ni = static_cast<u32>(sp.q) * static_cast<u32>(c.node_cap) + sp.node;
+          sp.kvp = kv_on(c, sp.q) && R->n_kvh[ni] > 0 ? kv_pages_of(sp.tokens) : 0;
+          tk += sp.kvp;
+        }
         R->it_tok[i] = tk;
       }
       off[0] += it.nrec;
@@ -706,6 +700,7 @@ SPEX_HDNI void drain_remaining(Run* R) {
     }
     R->st_state[sid] = ST_GONE;
     R->n_stream[static_cast<u32>(q) * static_cast<u32>(R->cfg.node_cap) + node] = -1;
+    if (kv_on(R->cfg, q)) kv_release(R, q, node);
   }
   g->n_live = 0;
   g->n_active_region = 0;
@@ -786,7 +781,23 @@ SPEX_HDNI void commit_items(Run* R, EX& ex, int n) {
     ex_scan(ex, R->it_scan_d, n, &npsh);
     ex_scan(ex, R->it_scan_e, n, &ntok);
   }
+  // tree-KV pages for this commit's spawns: page-table entries [kv0, kv0 + ntok)
+  // take never-used pages first (consecutive: a thought stays one run of
+  // pages), then pages from the free ring once the pool has been touched
   const i64 kv0 = g->kv_next;
+  const i64 kv_room = c.kv_pages - g->kv_bump;
+  const i64 kv_fresh = ntok < kv_room ? ntok : kv_room;
+  const i64 kv_take = ntok - kv_fresh;
+  if (ntok > 0 && (kv_take > g->kv_free_tail - g->kv_free_head || kv0 + ntok > c.kv_pt_cap)) {
+    // error_node 1: the page table is full (the host retries with a larger
+    // one); 0: the live thoughts exceed the pool
+    if (ex.tid == 0) set_err(R, ERR_CAP_KV, -1, kv0 + ntok > c.kv_pt_cap ? 1u : 0u);
+    ex.sync();
+    return;
+  }
+  for (int k = ex.tid; k < ntok; k += ex.nthr)
+    R->kv_pt[kv0 + k] = k < kv_fresh ? static_cast<int>(g->kv_bump + k)
+                                     : R->kv_free[(g->kv_free_head + (k - kv_fresh)) % c.kv_pages];
   if (c.trace && g->log_n + nrec > c.log_cap) {
     if (ex.tid == 0) set_err(R, ERR_CAP_LOG, -1, kNoNode);
     ex.sync();
@@ -827,9 +838,9 @@ SPEX_HDNI void commit_items(Run* R, EX& ex, int n) {
       R->st_ready[sid] = now;
       R->st_state[sid] = s.cancelled ? ST_GONE : ST_STAGED;
       R->live[live0 + R->it_scan_c[i] + j] = sid;
-      {
+      if (s.kvp > 0) {
         i64 kb = kv0 + R->it_scan_e[i];
-        for (int k = 0; k < j; ++k) kb += sp[k].tokens;
+        for (int k = 0; k < j; ++k) kb += sp[k].kvp;
         R->n_kvbase[static_cast<u32>(s.q) * static_cast<u32>(c.node_cap) + s.node] = kb;
       }
       if (!s.cancelled) {
@@ -859,6 +870,10 @@ SPEX_HDNI void commit_items(Run* R, EX& ex, int n) {
     g->n_staged += static_cast<int>(sdelta);
     g->fifo_tail += npsh;
     g->kv_next += ntok;
+    g->kv_free_head += kv_take;
+    g->kv_bump += kv_fresh;
+    g->kv_live += ntok;
+    if (g->kv_live > g->kv_peak) g->kv_peak = g->kv_live;
     int admits = Q - ac0 < nfin ? Q - ac0 : nfin;
     if (admits < 0) admits = 0;
     g->admitted_count += admits;
@@ -1095,6 +1110,14 @@ SPEX_HDNI void completions(Run* R, EX& ex, int* warp_off) {
     }
     ex.sync();
   }
+  // the finished streams' own holds (after their PRM batch is recorded)
+  if (R->cfg.kv_pages > 0) {
+    for (int f = ex.tid; f < nf; f += ex.nthr) {
+      const int q = R->st_q[R->fins[f]];
+      if (kv_on(R->cfg, q)) kv_release(R, q, R->st_node[R->fins[f]]);
+    }
+    ex.sync();
+  }
   commit_items(R, ex, nf);
 }
 
@@ -1111,7 +1134,11 @@ SPEX_HD void run_loop(Run* R, EX& ex, int* warp_off) {
       admit_query(R, q, slot);
     }
     g->admitted_count = first;
-    g->kv_next = static_cast<i64>(Q) * c.prompt_tokens;
+    const i64 root_pages = c.kv_pages > 0 ? static_cast<i64>(Q) * c.kv_pp_root : 0;
+    g->kv_next = root_pages;
+    g->kv_bump = root_pages;
+    g->kv_live = root_pages;
+    g->kv_peak = root_pages;
   }
   ex.sync();
   followups(R, ex, warp_off);

@@ -54,7 +54,13 @@ enum : u16 {
   NF_HAS_READY = 1u << 10,        // ready_at_promote
   NF_GOLDEN_PATH = 1u << 11,      // every node on the path to the root passes the golden draw (oracle_reward)
   NF_DEEP = 1u << 12,             // the depth-1 ancestor's deep draw passed (oracle_is_terminal)
+  NF_KV_SELF = 1u << 13,          // the node still holds its own tree-KV pin (may get children)
 };
+
+// Tree-KV pages: a thought's K/V rows live in pages of kKvPage tokens of the
+// model's KV pools; a node's pages are listed in kv_pt[n_kvbase .. + pages).
+constexpr int kKvPage = 16;
+SPEX_HD int kv_pages_of(int tokens) { return (tokens + kKvPage - 1) / kKvPage; }
 
 // stream states
 enum : u8 { ST_NONE = 0, ST_STAGED = 1, ST_ACTIVE = 2, ST_GONE = 3 };
@@ -99,6 +105,7 @@ struct SpawnRec {
   u32 node;
   int tokens;
   int cancelled;
+  int kvp;  // tree-KV pages to allocate at commit (0: none)
 };
 
 struct PushRec {
@@ -134,6 +141,7 @@ enum : int {
   ERR_CAP_LABELS = 104,
   ERR_STALLED = 105,
   ERR_INTERNAL = 106,
+  ERR_CAP_KV = 107,  // the live tree KV exceeds the pool (pages) or the page table
 };
 
 struct Cfg {
@@ -182,6 +190,10 @@ struct Cfg {
   // Query shard whose model work this rank runs ([shard_lo, shard_hi)); the
   // search itself (every query) is replicated, so decisions are unaffected.
   int shard_lo, shard_hi;
+  // Paged tree-KV store (0 pages: no model attached, no KV bookkeeping).
+  int kv_pages;     // physical pages in the pools
+  int kv_pp_root;   // pages of a root prompt (static: query q owns pages [q*pp, (q+1)*pp))
+  i64 kv_pt_cap;    // page-table entries
   int lex_rank[kMaxLabels];   // label index -> rank of "a<idx>" in std::map order
   int lex_order[kMaxLabels];  // rank -> label index
 };
@@ -252,7 +264,10 @@ struct GState {
   int s_n_items, s_flag, s_k_total, s_leftover;
   double s_limit, s_total;
   i64 decode_rows;  // sum over decode steps of active rows (model work)
-  i64 kv_next;      // next free KV slot (bump allocation in stream-id order)
+  i64 kv_next;      // next free page-table entry (bump: entries are never reused)
+  i64 kv_bump;      // next never-used physical page
+  i64 kv_free_head, kv_free_tail;  // FIFO ring of freed physical pages (kv_free)
+  i64 kv_live, kv_peak, kv_freed;  // pages held by live thoughts (peak) and pages freed
   int n_sched, n_sched_rows;
   // device cycle counters per phase (thread 0's view)
   i64 cyc[8];
@@ -295,7 +310,10 @@ struct Run {
   int* n_stream;  // stream_of: >=0 global sid, <= -2 item-local spawn (-2-k), -1 none
   i64* n_ready;
   int* n_refc;    // active-descendant count (unique_kv_tokens bookkeeping)
-  i64* n_kvbase;  // first KV slot of the node's thought in the tree KV pools
+  i64* n_kvbase;  // first page-table entry of the node's thought (-1: no pages)
+  int* n_kvh;     // tree-KV holds: own pin + live children + running stream; 0 frees the pages
+  int* kv_pt;     // page table [kv_pt_cap]: physical page of each entry
+  int* kv_free;   // freed physical pages, FIFO ring [kv_pages]
   // per-query
   QueryRun* qs;
   QueryTally* q_tally;

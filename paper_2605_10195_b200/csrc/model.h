@@ -42,19 +42,25 @@ struct RowDesc {
   int pad;
 };
 
+// A run of physically consecutive tree-KV slots: one thought's pages are cut
+// into runs of consecutive pages (a thought on fresh pages is one run).
 struct Segment {
   long long base;  // first KV slot
   int len;         // tokens
-  int pad;
+  int own0;        // -1: an ancestor's run; else the thought position of the run's first token (causal masking)
 };
 
 struct TreeView {
   const uint32_t* parent;
   const int* tokens;
   const uint64_t* hash;
-  const long long* kvbase;
+  const long long* kvbase;  // first page-table entry of each node's thought (ctl_state.h n_kvbase)
+  const int* kv_pt;         // page table: physical page of each entry
   const int* st_q;
   const uint32_t* st_node;
+  int* seg_ctr;             // segment-pool counter of the builder's stream (zeroed before each build)
+  int* err;                 // forward error bits: 1 ancestor chain deeper than kMaxChain, 2 segment pool full
+  long long seg_cap;        // segment-pool capacity
   int node_cap;
   int prompt_tokens;
   int V;

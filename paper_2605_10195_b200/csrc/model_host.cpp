@@ -543,6 +543,20 @@ extern "C" void spex_model_cache_release_mismatch(const ModelRunConfig* mc) {
   }
 }
 
+// Tree-KV pool capacity (slots) for the next run of `mc`: the resident pools
+// when the cached models match, else 55% of the free HBM after releasing the
+// mismatched ones (both models, all layers, K and V in bf16).
+extern "C" long long spex_model_pool_slots(const ModelRunConfig* mc) {
+  spex_model_cache_release_mismatch(mc);
+  if (g_cache.pol && (!mc->with_prm || g_cache.prm))
+    return mc->with_prm ? std::min(g_cache.pol->slots, g_cache.prm->slots) : g_cache.pol->slots;
+  size_t free_b = 0, total_b = 0;
+  cudaMemGetInfo(&free_b, &total_b);
+  const double per_slot = 4.0 * (mc->policy.L * mc->policy.KVH * mc->policy.dh +
+                                 (mc->with_prm ? mc->prm.L * mc->prm.KVH * mc->prm.dh : 0));
+  return static_cast<long long>(0.55 * static_cast<double>(free_b) / per_slot);
+}
+
 extern "C" void spex_model_cache_clear() {
   delete g_cache.pol;
   delete g_cache.prm;
@@ -572,6 +586,7 @@ void run_model_schedule(const ModelRunConfig& mc, const ScheduleView& sv, ModelR
   g_cache.seed = mc.seed;
   // capacity actually resident (a cached pool may be larger than this run's request)
   const long long cap_slots = prm ? std::min(pol->slots, prm->slots) : pol->slots;
+  if (cap_slots < sv.kv_slots) throw std::runtime_error("tree KV pools smaller than the control's page count");
   const int rows_cap = std::max({max_dec, max_prm, prompt_chunk * P, 1});
   if (!g_cache.item_ctr) {
     std::vector<void*> keep;
@@ -616,10 +631,23 @@ void run_model_schedule(const ModelRunConfig& mc, const ScheduleView& sv, ModelR
   TileDesc* tiles = g_cache.tiles;
   float* scores = g_cache.scores;
 
+  // segment pools of the two streams' row builders (counters zeroed before
+  // each build) and the forward's error bits, in the shared counter block
+  int* seg_ctr_pol = g_cache.item_ctr + 16;
+  int* seg_ctr_prm = prm_overlap ? g_cache.item_ctr + 17 : seg_ctr_pol;
+  int* fwd_err = g_cache.item_ctr + 18;
+  CK(cudaMemsetAsync(fwd_err, 0, sizeof(int), st));
+  const long long seg_cap = (long long)g_cache.rows_cap * 40;
   TreeView tv_pol = sv.tree;
   tv_pol.V = mc.policy.V;
+  tv_pol.seg_ctr = seg_ctr_pol;
+  tv_pol.err = fwd_err;
+  tv_pol.seg_cap = seg_cap;
   TreeView tv_prm = sv.tree;
   tv_prm.V = mc.prm.V;
+  tv_prm.seg_ctr = seg_ctr_prm;
+  tv_prm.err = fwd_err;
+  tv_prm.seg_cap = seg_cap;
   AttnTimer timer;
   if (const char* p = std::getenv("SPEX_ATTN_LOG")) timer.dump = std::fopen(p, "w");
   // a query-block shard's forward is a fraction of the step, the replicated
@@ -659,11 +687,11 @@ void run_model_schedule(const ModelRunConfig& mc, const ScheduleView& sv, ModelR
   long long dbg_n = 0, dbg_s = 0;
 
   auto process = [&](const PubEntry& pe) {
-    if (pe.kv_next > cap_slots) throw std::runtime_error("tree KV pool capacity exceeded");
     if (pe.kind == SCHED_DECODE) {
       for (int s = 0; s < pe.steps; ++s) {
         for (int c0 = 0; c0 < pe.n; c0 += max_dec) {
           const int n = std::min(max_dec, pe.n - c0);
+          CK(cudaMemsetAsync(seg_ctr_pol, 0, sizeof(int), st));
           spex_k_build_decode_rows(tv_pol, sv.srow_sid + pe.off + c0, sv.srow_pos0 + pe.off + c0, n, s, rows, segs,
                                    st);
           g_launches += 1;
@@ -691,6 +719,7 @@ void run_model_schedule(const ModelRunConfig& mc, const ScheduleView& sv, ModelR
       }
     } else if (prm && pe.rows > 0) {
       if (pe.rows > max_prm) throw std::runtime_error("PRM batch larger than the row buffers");
+      CK(cudaMemsetAsync(seg_ctr_prm, 0, sizeof(int), st2));
       spex_k_build_prm_rows(tv_prm, sv.srow_sid + pe.off, sv.srow_rstart + pe.off, sv.srow_tstart + pe.off, pe.n,
                             rows2, segs2, last_row, tiles2, st2);
       forward(*prm, rows2, segs2, pe.rows, st2, nullptr, tiles2, pe.tiles);
@@ -744,6 +773,12 @@ void run_model_schedule(const ModelRunConfig& mc, const ScheduleView& sv, ModelR
   if (st2 != st) CK(cudaStreamWaitEvent(st, e_join, 0));
   cudaEventRecord(t1, st);
   CK(cudaEventSynchronize(t1));
+  {
+    int err = 0;
+    CK(cudaMemcpy(&err, fwd_err, sizeof(int), cudaMemcpyDeviceToHost));
+    if (err & 1) throw std::runtime_error("a thought's ancestor chain is deeper than the row builder's limit");
+    if (err & 2) throw std::runtime_error("segment pool of the row builder exhausted");
+  }
   cudaEventDestroy(e_fork);
   cudaEventDestroy(e_join);
   timer.flush();

@@ -53,36 +53,88 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
-constexpr int kMaxSegFwd = 40;
-__device__ int build_segments(const TreeView& t, int q, uint32_t node, int own_len, Segment* out,
-                              int* abs_prefix) {
-  // ancestors root-first, then the node's own prefix
-  const uint32_t b = (uint32_t)q * (uint32_t)t.node_cap;
-  uint32_t chain[64];
-  int n = 0;
-  for (uint32_t c = t.parent[b + node]; c != 0xffffffffu && n < kMaxSegFwd - 1; c = t.parent[b + c]) chain[n++] = c;
-  int pre = 0;
-  int k = 0;
-  for (int i = n - 1; i >= 0; --i) {
-    const uint32_t a = chain[i];
-    const int len = t.tokens[b + a];
-    if (len > 0) {
-      out[k].base = t.kvbase[b + a];
-      out[k].len = len;
-      out[k].pad = 0;
-      ++k;
-    }
-    pre += len;
+constexpr int kMaxChain = 128;  // ancestors of one thought (deeper trees fail loudly: err bit 1)
+constexpr int kPg = 16;         // tokens per tree-KV page (ctl_state.h kKvPage)
+
+// Runs of consecutive physical pages among a thought's first `len` tokens.
+__device__ __forceinline__ int count_runs(const int* __restrict__ pt, long long off, int len) {
+  const int np = (len + kPg - 1) / kPg;
+  int runs = 0, prev = -2;
+  for (int j = 0; j < np; ++j) {
+    const int p = pt[off + j];
+    runs += p != prev + 1;
+    prev = p;
   }
-  out[k].base = t.kvbase[b + node];
-  out[k].len = own_len;
-  out[k].pad = 0;
-  ++k;
-  *abs_prefix = pre;
+  return runs;
+}
+
+__device__ __forceinline__ int emit_runs(const int* __restrict__ pt, long long off, int len, int own, Segment* out) {
+  const int np = (len + kPg - 1) / kPg;
+  int k = 0;
+  for (int j = 0; j < np;) {
+    const int p0 = pt[off + j];
+    int r = 1;
+    while (j + r < np && pt[off + j + r] == p0 + r) ++r;
+    const int tok = min(len - j * kPg, r * kPg);
+    out[k].base = (long long)p0 * kPg;
+    out[k].len = tok;
+    out[k].own0 = own ? j * kPg : -1;
+    ++k;
+    j += r;
+  }
   return k;
 }
 
-constexpr int kMaxSeg = 40;
+// Ancestors of `node`, root first; returns their count and the tokens they hold.
+__device__ int ancestor_chain(const TreeView& t, uint32_t b, uint32_t node, uint32_t* chain, int* pre) {
+  int n = 0;
+  for (uint32_t c = t.parent[b + node]; c != 0xffffffffu && n < kMaxChain; c = t.parent[b + c]) ++n;
+  if (n == kMaxChain) atomicOr(t.err, 1);  // deeper than the chain buffer: fail loudly
+  int p = 0, i = n;
+  for (uint32_t c = t.parent[b + node]; i > 0; c = t.parent[b + c]) {
+    chain[--i] = c;
+    p += t.tokens[b + c];
+  }
+  *pre = p;
+  return n;
+}
+
+// Segment list of a row or thought: the ancestors' runs root-first, then the
+// thought's own first `own_len` tokens (runs tagged with their positions).
+// Space comes from the stream's segment pool; returns the offset (-1: full).
+__device__ int build_segments(const TreeView& t, int q, uint32_t node, int own_len, Segment* segs, int* nseg,
+                              int* abs_prefix) {
+  const uint32_t b = (uint32_t)q * (uint32_t)t.node_cap;
+  uint32_t chain[kMaxChain];
+  int pre = 0;
+  const int n = ancestor_chain(t, b, node, chain, &pre);
+  int total = 0;
+  for (int i = 0; i < n; ++i) {
+    const int len = t.tokens[b + chain[i]];
+    if (len > 0) total += count_runs(t.kv_pt, t.kvbase[b + chain[i]], len);
+  }
+  total += count_runs(t.kv_pt, t.kvbase[b + node], own_len);
+  const int off = atomicAdd(t.seg_ctr, total);
+  *abs_prefix = pre;
+  if ((long long)off + total > t.seg_cap) {
+    atomicOr(t.err, 2);
+    *nseg = 0;
+    return 0;
+  }
+  int k = 0;
+  for (int i = 0; i < n; ++i) {
+    const int len = t.tokens[b + chain[i]];
+    if (len > 0) k += emit_runs(t.kv_pt, t.kvbase[b + chain[i]], len, 0, segs + off + k);
+  }
+  k += emit_runs(t.kv_pt, t.kvbase[b + node], own_len, 1, segs + off + k);
+  *nseg = k;
+  return off;
+}
+
+// KV slot of token `pos` of a node's thought.
+__device__ __forceinline__ long long kv_slot(const TreeView& t, uint32_t b, uint32_t node, int pos) {
+  return (long long)t.kv_pt[t.kvbase[b + node] + pos / kPg] * kPg + pos % kPg;
+}
 
 __global__ void build_decode_rows_kernel(TreeView t, const int* sids, const int* pos0, int n, int step,
                                          RowDesc* rows, Segment* segs) {
@@ -92,16 +144,16 @@ __global__ void build_decode_rows_kernel(TreeView t, const int* sids, const int*
   const int q = t.st_q[sid];
   const uint32_t node = t.st_node[sid];
   const int pos = pos0[i] + step;
-  int pre = 0;
-  int ns = build_segments(t, q, node, pos + 1, segs + (long long)i * kMaxSeg, &pre);
+  int pre = 0, ns = 0;
+  const int off = build_segments(t, q, node, pos + 1, segs, &ns, &pre);
   const uint32_t b = (uint32_t)q * (uint32_t)t.node_cap;
   RowDesc r;
   r.q = q;
   r.node = node;
   r.pos = pos;
   r.abs_pos = pre + pos;
-  r.slot = t.kvbase[b + node] + pos;
-  r.seg_off = i * kMaxSeg;
+  r.slot = kv_slot(t, b, node, pos);
+  r.seg_off = off;
   r.nseg = ns;
   r.token = token_id(t.hash[b + node], pos, t.V);
   r.pad = 0;
@@ -109,6 +161,8 @@ __global__ void build_decode_rows_kernel(TreeView t, const int* sids, const int*
 }
 
 // PRM rows: thought k of the entry occupies rows [row_start[k], row_start[k] + len).
+// The thought's rows share one segment list (ancestors + the whole thought);
+// the tile kernels clip the own runs at each tile's last row (causal).
 __global__ void build_prm_rows_kernel(TreeView t, const int* sids, const int* row_start, const int* tile_start,
                                       int n, RowDesc* rows, Segment* segs, int* last_row, TileDesc* tiles) {
   const int k = blockIdx.x;
@@ -119,18 +173,24 @@ __global__ void build_prm_rows_kernel(TreeView t, const int* sids, const int* ro
   const uint32_t b = (uint32_t)q * (uint32_t)t.node_cap;
   const int len = t.tokens[b + node];
   const int r0 = row_start[k];
+  __shared__ int s_off, s_ns, s_pre;
+  if (threadIdx.x == 0) {
+    int ns = 0, pre = 0;
+    s_off = build_segments(t, q, node, len, segs, &ns, &pre);
+    s_ns = ns;
+    s_pre = pre;
+  }
+  __syncthreads();
   for (int j = threadIdx.x; j < len; j += blockDim.x) {
     const int i = r0 + j;
-    int pre = 0;
-    int ns = build_segments(t, q, node, j + 1, segs + (long long)i * kMaxSeg, &pre);
     RowDesc r;
     r.q = q;
     r.node = node;
     r.pos = j;
-    r.abs_pos = pre + j;
-    r.slot = t.kvbase[b + node] + j;
-    r.seg_off = i * kMaxSeg;
-    r.nseg = ns;
+    r.abs_pos = s_pre + j;
+    r.slot = kv_slot(t, b, node, j);
+    r.seg_off = s_off;
+    r.nseg = s_ns;
     r.token = token_id(t.hash[b + node], j, t.V);
     r.pad = 0;
     rows[i] = r;
@@ -144,7 +204,8 @@ __global__ void build_prm_rows_kernel(TreeView t, const int* sids, const int* ro
   }
 }
 
-// Root prompt rows: query q, positions 0..P-1.
+// Root prompt rows: query q, positions 0..P-1; the prompt's pages are static
+// and consecutive, so each row has one segment (segs[i]).
 __global__ void build_prompt_rows_kernel(TreeView t, int q0, int nq, RowDesc* rows, Segment* segs) {
   const int P = t.prompt_tokens;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -152,17 +213,18 @@ __global__ void build_prompt_rows_kernel(TreeView t, int q0, int nq, RowDesc* ro
   const int q = q0 + i / P;
   const int j = i % P;
   const uint32_t b = (uint32_t)q * (uint32_t)t.node_cap;
-  Segment* s = segs + (long long)i * kMaxSeg;
-  s[0].base = t.kvbase[b];
-  s[0].len = j + 1;
-  s[0].pad = 0;
+  const long long base = kv_slot(t, b, 0, 0);
+  Segment* s = segs + i;
+  s->base = base;
+  s->len = j + 1;
+  s->own0 = 0;
   RowDesc r;
   r.q = q;
   r.node = 0;
   r.pos = j;
   r.abs_pos = j;
-  r.slot = t.kvbase[b] + j;
-  r.seg_off = i * kMaxSeg;
+  r.slot = base + j;
+  r.seg_off = i;
   r.nseg = 1;
   r.token = token_id(t.hash[b], j, t.V);
   r.pad = 0;
@@ -352,6 +414,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 }
 
 constexpr int kChunk = 64;
+
+// Tokens of a segment inside a tile's causal horizon: an own-thought run is
+// cut at position `clip` (ancestor runs are whole).
+__device__ __forceinline__ int seg_len_eff(const Segment& sg, int clip) {
+  return sg.own0 < 0 ? sg.len : max(0, min(sg.len, clip - sg.own0));
+}
 constexpr int kAttnThreads = 128;
 
 
@@ -776,7 +844,8 @@ __global__ void __launch_bounds__(128) tree_attn_tile_mma_kernel(const __grid_co
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   int nchunks = 0;
-  for (int s = 0; s < nseg; ++s) nchunks += (sg[s].len + kChunk - 1) / kChunk;
+  const int clip = last.pos + 1;  // the tile's causal horizon inside its own thought
+  for (int s = 0; s < nseg; ++s) nchunks += (seg_len_eff(sg[s], clip) + kChunk - 1) / kChunk;
   // Q fragments (A operand, 16 rows x 128), rows beyond nrows are zero
   const int gq = lane >> 2, tq = lane & 3;
   uint32_t qa[8][4];
@@ -804,14 +873,14 @@ __global__ void __launch_bounds__(128) tree_attn_tile_mma_kernel(const __grid_co
   long long cb[2];
   int cl[2], cown[2];
   auto next_chunk = [&](int b) {
-    while (seg_i < nseg && seg_o >= sg[seg_i].len) {
+    while (seg_i < nseg && seg_o >= seg_len_eff(sg[seg_i], clip)) {
       ++seg_i;
       seg_o = 0;
     }
     cb[b] = sg[seg_i].base + seg_o;
-    const int l = sg[seg_i].len - seg_o;
+    const int l = seg_len_eff(sg[seg_i], clip) - seg_o;
     cl[b] = l < kChunk ? l : kChunk;
-    cown[b] = (seg_i == nseg - 1) ? seg_o : -1;
+    cown[b] = sg[seg_i].own0 >= 0 ? sg[seg_i].own0 + seg_o : -1;
     seg_o += cl[b];
   };
   auto issue = [&](int b) {
@@ -1260,21 +1329,22 @@ __global__ void __launch_bounds__(kAttnThreads) tree_attn_tile_kernel(const Tile
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   int nchunks = 0;
-  for (int s = 0; s < nseg; ++s) nchunks += (sg[s].len + kChunk - 1) / kChunk;
+  const int clip = last.pos + 1;  // the tile's causal horizon inside its own thought
+  for (int s = 0; s < nseg; ++s) nchunks += (seg_len_eff(sg[s], clip) + kChunk - 1) / kChunk;
   __syncthreads();
 
   int seg_i = 0, seg_o = 0;
   long long cb[2];
   int cl[2], cown[2];  // chunk base/len; own-segment offset of the chunk (-1: ancestor)
   auto next_chunk = [&](int b) {
-    while (seg_i < nseg && seg_o >= sg[seg_i].len) {
+    while (seg_i < nseg && seg_o >= seg_len_eff(sg[seg_i], clip)) {
       ++seg_i;
       seg_o = 0;
     }
     cb[b] = sg[seg_i].base + seg_o;
-    const int l = sg[seg_i].len - seg_o;
+    const int l = seg_len_eff(sg[seg_i], clip) - seg_o;
     cl[b] = l < kChunk ? l : kChunk;
-    cown[b] = (seg_i == nseg - 1) ? seg_o : -1;
+    cown[b] = sg[seg_i].own0 >= 0 ? sg[seg_i].own0 + seg_o : -1;
     seg_o += cl[b];
   };
   for (int c = 0; c < 2 && c < nchunks; ++c) {

@@ -80,6 +80,7 @@ const char* errc_name(int code) {
     case ERR_CAP_STAGE: return "CapacityStage";
     case ERR_CAP_LABELS: return "CapacityLabels";
     case ERR_STALLED: return "NothingExpandable(stalled)";
+    case ERR_CAP_KV: return "CapacityTreeKV";
     default: return "Internal";
   }
 }
@@ -460,6 +461,9 @@ struct spex_executor {
   int nthreads = 512;
   int record_sched = 0;
   int shard_lo = 0, shard_hi = -1;  // owned query range of the model work (-1: all)
+  long long kv_pages_req = 0;       // tree-KV pool pages (0: sized from free HBM when a model is attached)
+  long long kv_pt_cap = 0;          // page-table entries of the last run
+  long long kv_pages = 0;           // pool pages of the last run
 #ifndef SPEX_EMU
   cudaStream_t stream = nullptr;
   cudaStream_t mstream = nullptr;
@@ -480,6 +484,7 @@ extern "C" int spex_launch_control_batch_async(Run* d_runs, int n_runs, int n_qu
                                                cudaStream_t stream, cudaEvent_t a, cudaEvent_t b);
 extern "C" void spex_model_cache_clear();
 extern "C" void spex_model_cache_release_mismatch(const ModelRunConfig* mc);
+extern "C" long long spex_model_pool_slots(const ModelRunConfig* mc);
 #define CUDA_OK(x)                                                                  \
   do {                                                                              \
     cudaError_t e_ = (x);                                                           \
@@ -644,6 +649,7 @@ void layout(Arena& A, Run& R, int Q, int node_cap, int stream_cap, int log_cap, 
   A.add(R.n_ready, NN);
   A.add(R.n_refc, NN);
   A.add(R.n_kvbase, NN);
+  A.add(R.n_kvh, NN);
   A.add(R.qs, Q);
   A.add(R.q_tally, Q);
   A.add(R.q_rest_stack, NN);
@@ -872,6 +878,24 @@ int guarded(F&& f) {
   }
 }
 
+// Paged tree-KV store of one run (ctl_state.h kKvPage): `pages` physical
+// pages, root prompts static in the first Q * pp, the page table sized for
+// every page handed out over the run (ex.kv_pt_cap grows on overflow).
+void kv_configure(spex_executor& ex, Cfg& c, long long pages) {
+  const int Q = ex.hc.n_queries;
+  const long long pp = kv_pages_of(ex.hc.prompt_tokens);
+  if (pages > INT32_MAX) pages = INT32_MAX;
+  if (pages < static_cast<long long>(Q) * pp + kv_pages_of(ex.hc.token_max))
+    fail(ERR_CAP_KV, "tree KV pool of " + std::to_string(pages) + " pages cannot hold the " + std::to_string(Q) +
+                         " root prompts and one thought");
+  if (ex.kv_pt_cap < static_cast<long long>(Q) * pp + std::max(4 * pages, 1LL << 20))
+    ex.kv_pt_cap = static_cast<long long>(Q) * pp + std::max(4 * pages, 1LL << 20);
+  c.kv_pages = static_cast<int>(pages);
+  c.kv_pp_root = static_cast<int>(pp);
+  c.kv_pt_cap = ex.kv_pt_cap;
+  ex.kv_pages = pages;
+}
+
 void run_executor(spex_executor& ex, int trace) {
   const HostConfig& h = ex.hc;
   const int Q = h.n_queries;
@@ -902,6 +926,14 @@ void run_executor(spex_executor& ex, int trace) {
     std::memset(base, 0, A.total);
     A.carve(base);
     R.log_tab = tab.data();
+    std::vector<int> kv_pt_h, kv_free_h;
+    if (ex.kv_pages_req > 0) {
+      kv_configure(ex, R.cfg, ex.kv_pages_req);
+      kv_pt_h.assign(static_cast<size_t>(R.cfg.kv_pt_cap), -1);
+      kv_free_h.assign(static_cast<size_t>(R.cfg.kv_pages), -1);
+      R.kv_pt = kv_pt_h.data();
+      R.kv_free = kv_free_h.data();
+    }
     R.qs[0].admitted = 0;
     for (int q = 0; q < Q; ++q) R.qs[q].plan_empty_version = 0xffffffffu;
     std::vector<int> sm(2048);
@@ -917,6 +949,20 @@ void run_executor(spex_executor& ex, int trace) {
     auto t1 = std::chrono::steady_clock::now();
     ex.device_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
     ex.g = *R.g;
+    if (R.cfg.kv_pages > 0 && ex.g.error == 0) {
+      // page-store self-check (tests): at the end every thought page is back
+      // in the free ring exactly once and nothing else is
+      const i64 root = static_cast<i64>(Q) * R.cfg.kv_pp_root;
+      const i64 ring = ex.g.kv_free_tail - ex.g.kv_free_head;
+      std::vector<char> seen(static_cast<size_t>(ex.g.kv_bump), 0);
+      bool ok = ex.g.kv_live == root && ring == ex.g.kv_bump - root;
+      for (i64 k = 0; ok && k < ring; ++k) {
+        const int p = R.kv_free[(ex.g.kv_free_head + k) % R.cfg.kv_pages];
+        ok = p >= root && p < ex.g.kv_bump && !seen[p];
+        if (ok) seen[p] = 1;
+      }
+      if (!ok) fail(ERR_INTERNAL, "tree-KV page store inconsistent at the end of the run");
+    }
     ex.qs.assign(R.qs, R.qs + Q);
     if (trace) ex.log.assign(R.log, R.log + ex.g.log_n);
 #else
@@ -978,12 +1024,29 @@ void run_executor(spex_executor& ex, int trace) {
       CUDA_OK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&R.pub), h_head, 0));
       CUDA_OK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&R.pub_e), h_ents, 0));
     }
+    int* d_kvpt = nullptr;
+    int* d_kvfree = nullptr;
+    if (ex.with_model) {
+      // the pool: an explicit page count, else the resident cached pools or
+      // 55% of free HBM (spex_model_pool_slots)
+      const long long slots = ex.kv_pages_req > 0 ? ex.kv_pages_req * kKvPage : spex_model_pool_slots(&ex.mc);
+      kv_configure(ex, R.cfg, slots / kKvPage);
+      CUDA_OK(cudaMallocAsync(reinterpret_cast<void**>(&d_kvpt), sizeof(int) * R.cfg.kv_pt_cap, ex.stream));
+      CUDA_OK(cudaMallocAsync(reinterpret_cast<void**>(&d_kvfree), sizeof(int) * R.cfg.kv_pages, ex.stream));
+      R.kv_pt = d_kvpt;
+      R.kv_free = d_kvfree;
+      if (std::getenv("SPEX_TIMING"))
+        std::fprintf(stderr, "[spex timing] tree KV pool: %d pages x %d tokens, page table %lld entries\n",
+                     R.cfg.kv_pages, kKvPage, static_cast<long long>(R.cfg.kv_pt_cap));
+    }
     mark("arena+pinned");
     Run* d_run = nullptr;
     CUDA_OK(cudaMallocAsync(reinterpret_cast<void**>(&d_run), sizeof(Run), ex.stream));
     CUDA_OK(cudaMemcpyAsync(d_run, &R, sizeof(Run), cudaMemcpyHostToDevice, ex.stream));
     auto cleanup = [&] {
       cudaFreeAsync(base, ex.stream);
+      if (d_kvpt) cudaFreeAsync(d_kvpt, ex.stream);
+      if (d_kvfree) cudaFreeAsync(d_kvfree, ex.stream);
       cudaFreeAsync(d_tab, ex.stream);
       cudaFreeAsync(d_run, ex.stream);
       cudaStreamSynchronize(ex.stream);
@@ -996,6 +1059,7 @@ void run_executor(spex_executor& ex, int trace) {
       sv.tree.tokens = R.n_tokens;
       sv.tree.hash = R.n_hash;
       sv.tree.kvbase = R.n_kvbase;
+      sv.tree.kv_pt = R.kv_pt;
       sv.tree.st_q = R.st_q;
       sv.tree.st_node = R.st_node;
       sv.tree.node_cap = node_cap;
@@ -1027,17 +1091,9 @@ void run_executor(spex_executor& ex, int trace) {
     cudaEventCreate(&cb);
     bool model_done = false;
     ex.mres = ModelRunResult{};
+    sv.kv_slots = static_cast<long long>(R.cfg.kv_pages) * kKvPage;
     if (streaming) {
       CUDA_OK(cudaStreamSynchronize(ex.stream));
-      // KV pool capacity from the free-memory budget (both models, all layers),
-      // after releasing cached models of other shapes
-      spex_model_cache_release_mismatch(&mc);
-      size_t free_b = 0, total_b = 0;
-      cudaMemGetInfo(&free_b, &total_b);
-      const double per_slot = 4.0 * (mc.policy.L * mc.policy.KVH * mc.policy.dh +
-                                     (mc.with_prm ? mc.prm.L * mc.prm.KVH * mc.prm.dh : 0));
-      sv.kv_slots = static_cast<long long>(0.55 * static_cast<double>(free_b) / per_slot);
-      if (const char* e = std::getenv("SPEX_KV_SLOTS")) sv.kv_slots = std::atoll(e);
       sv.pub_head = h_head;
       sv.pub_entries = h_ents;
       alloc_outputs(static_cast<long long>(Q) * node_cap * 64);
@@ -1052,10 +1108,11 @@ void run_executor(spex_executor& ex, int trace) {
         model_done = true;
         mark("model-stream-done");
       } catch (const std::exception& e) {
-        // capacity exceeded while streaming: fall back to a sequential replay below
-        std::fprintf(stderr, "spex: streaming forward abandoned (%s); replaying after the control kernel\n", e.what());
         cudaDeviceSynchronize();  // the forward's streams (policy + PRM) and the control kernel
-        ex.mres = ModelRunResult{};
+        cudaFree(d_rows);
+        cudaFree(d_scores);
+        cleanup();
+        fail(201, std::string("model forward: ") + e.what());
       }
     } else {
       int lr = spex_launch_control_async(d_run, Q, ex.nthreads, ex.stream, ca, cb);
@@ -1081,7 +1138,6 @@ void run_executor(spex_executor& ex, int trace) {
       sv.pub_entries = nullptr;
       sv.entries_host = ents.data();
       sv.n_entries = static_cast<int>(ents.size());
-      sv.kv_slots = ex.g.kv_next;
       if (!d_rows) alloc_outputs(ex.g.decode_rows);
       try {
         run_model_schedule(mc, sv, &ex.mres, ex.mstream);
@@ -1136,6 +1192,15 @@ void run_executor(spex_executor& ex, int trace) {
       ex.log.clear();
       continue;
     }
+    if (ex.g.error == ERR_CAP_KV && ex.g.error_node == 1u) {
+      ex.kv_pt_cap *= 4;  // page table full: rerun with a larger one
+      ex.log.clear();
+      continue;
+    }
+    if (ex.g.error == ERR_CAP_KV)
+      fail(ERR_CAP_KV, "tree KV pool exhausted: the live thoughts need more than " + std::to_string(ex.kv_pages) +
+                           " pages of " + std::to_string(kKvPage) + " tokens (peak " + std::to_string(ex.g.kv_peak) +
+                           " pages live); set a larger pool with spex_executor_set_kv_pages or shard the queries");
     if (ex.g.error != 0 && std::getenv("SPEX_DEBUG")) {
       std::string dump;
       serialize(ex, dump);
@@ -1420,6 +1485,29 @@ int spex_executor_model_stats(spex_executor* ex, spex_model_stats* out) {
 #else
     (void)ex;
 #endif
+  });
+}
+
+int spex_executor_set_kv_pages(spex_executor* ex, long long pages) {
+  return guarded([&] {
+    if (pages < 0) fail(ERR_INVALID_ARGUMENT, "set_kv_pages: negative page count");
+    if (ex->ran) fail(ERR_INVALID_ARGUMENT, "set_kv_pages: executor already ran");
+    ex->kv_pages_req = pages;
+  });
+}
+
+int spex_executor_kv_stats(spex_executor* ex, spex_kv_stats* out) {
+  return guarded([&] {
+    std::memset(out, 0, sizeof(*out));
+    out->pages = ex->kv_pages;
+    out->page_tokens = kKvPage;
+    out->root_pages = ex->kv_pages > 0 ? static_cast<long long>(ex->hc.n_queries) * kv_pages_of(ex->hc.prompt_tokens) : 0;
+    out->peak_pages = ex->g.kv_peak;
+    out->freed_pages = ex->g.kv_freed;
+    out->live_pages_end = ex->g.kv_live;
+    out->allocated_pages = ex->g.kv_next;
+    out->fresh_pages = ex->g.kv_bump;
+    out->page_table_entries = ex->kv_pt_cap;
   });
 }
 

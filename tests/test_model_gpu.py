@@ -4,9 +4,11 @@
 by a full causal forward over its root->node token sequence, independently of
 the device's incremental tree-KV decode.
 
-Tolerances (stated): logsumexp |d| <= 2e-3 * max(1, |lse|); logit sum
-|d| <= 5e-3 * sqrt(V) (sum of V fp32 logits); argmax equal unless the top-2
-logits are within 2e-3; PRM score |d| <= 2e-3.
+Tolerances (stated, north_star's 1e-3 relative at bf16 against fp32):
+logsumexp |d| <= 1e-3 * max(1, |lse|); logit sum |d| <= 1e-3 * sum |z| (a sum
+of V fp32 logits); argmax equal unless the top-2 logits are within
+2e-3 * max(1, |lse|) (each logit within 1e-3 * max(1, |lse|)); PRM score
+|d| <= 1e-3 * |score|.
 """
 import json
 import random
@@ -46,17 +48,16 @@ def test_small_model_matches_numpy_oracle():
         ra, rl, rs, z = pol.logits_stats(toks)
         worst["lse"] = max(worst["lse"], abs(rl - lse))
         worst["sum"] = max(worst["sum"], abs(rs - lsum))
-        assert abs(rl - lse) <= 2e-3 * max(1.0, abs(rl)), (q, node, pos, rl, lse)
-        assert abs(rs - lsum) <= 5e-3 * np.sqrt(pol.V), (q, node, pos, rs, lsum)
+        assert abs(rl - lse) <= 1e-3 * max(1.0, abs(rl)), (q, node, pos, rl, lse)
+        assert abs(rs - lsum) <= 1e-3 * float(np.abs(z).sum()), (q, node, pos, rs, lsum)
         if amax != ra:
-            zs = np.sort(z)
-            assert zs[-1] - zs[-2] <= 2e-3, (q, node, pos, ra, amax)
+            assert z[ra] - z[amax] <= 2e-3 * max(1.0, abs(rl)), (q, node, pos, ra, amax)
     for (q, node, score) in rng.sample(prm, 30):
         n = tree.nodes[(q, node)][2]
         toks = tree.sequence(q, node, n - 1, rm.V)
         rs = rm.prm_score(toks)
         worst["prm"] = max(worst["prm"], abs(rs - score))
-        assert abs(rs - score) <= 2e-3, (q, node, rs, score)
+        assert abs(rs - score) <= 1e-3 * abs(rs), (q, node, rs, score)
     print("worst abs errors", worst)
 
 
@@ -79,8 +80,8 @@ def test_mid_model_tensor_core_paths_match_numpy_oracle():
     for (q, node, score) in rng.sample(prm, 4):
         n = tree.nodes[(q, node)][2]
         rs = rm.prm_score(tree.sequence(q, node, n - 1, rm.V))
-        assert abs(rs - score) <= 2e-3, (q, node, rs, score)
+        assert abs(rs - score) <= 1e-3 * abs(rs), (q, node, rs, score)
     pol = model_ref.Model("mid_policy", 3, prm=False)
     for (q, node, pos, amax, lse, lsum) in rng.sample(dec, 2):
         _, rl, rs, _ = pol.logits_stats(tree.sequence(q, node, pos, pol.V))
-        assert abs(rl - lse) <= 2e-3 * max(1.0, abs(rl)), (q, node, pos, rl, lse)
+        assert abs(rl - lse) <= 1e-3 * max(1.0, abs(rl)), (q, node, pos, rl, lse)
