@@ -65,6 +65,25 @@ SPEX_HD int atomic_add_int(int* p, int v) {
 #endif
 }
 
+SPEX_HD i64 spex_clock() {
+#if SPEX_DEVICE_PASS
+  return static_cast<i64>(clock64());
+#else
+  return 0;
+#endif
+}
+
+// Device wall clock in ns (globaltimer); 0 in the host emulation.
+SPEX_HD i64 spex_wall_ns() {
+#if SPEX_DEVICE_PASS
+  u64 t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return static_cast<i64>(t);
+#else
+  return 0;
+#endif
+}
+
 // ------------------------------------------------------- paged tree-KV store
 // A thought's K/V rows live in pages of kKvPage tokens (ctl_state.h). Each
 // node carries a hold count: its own pin (it may still get children: cleared
@@ -721,6 +740,7 @@ SPEX_HDNI void finish_query(const QC& x, bool early) {
   qr->finished = 1;
   qr->early = early ? 1 : 0;
   qr->finish_time = R->g->now;
+  qr->finish_ns = spex_wall_ns();
   x.it->fin = 1;
   touch(x);
   if (early) {

@@ -59,13 +59,43 @@ SPEX_HDNI bool on_stream_done(const QC& x, int sid, int tokens_done, int cancell
   return true;
 }
 
+// RewardOracle::reward (sim.cpp:146-152) realised by the PRM: the forward
+// scores the thought in the schedule entry recorded at its completion and
+// raises that entry's flag; the control waits for it (device only).
+SPEX_HDNI double prm_reward(const QC& x, u32 node) {
+  Run* R = x.R;
+  const u32 ni = NI(x, node);
+#if SPEX_DEVICE_PASS
+  const int e = R->n_prm_e[ni];
+  if (*reinterpret_cast<volatile int*>(&R->prm_done[e]) == 0) {
+    const i64 t0 = spex_wall_ns();
+    while (*reinterpret_cast<volatile int*>(&R->prm_done[e]) == 0) __nanosleep(256);
+    atomic_add_i64(&R->g->reward_wait_ns, spex_wall_ns() - t0);
+  }
+  __threadfence();
+  const double s = static_cast<double>(*reinterpret_cast<volatile float*>(&R->n_score[ni]));
+  return s < 0.0 ? 0.0 : (s > 1.0 ? 1.0 : s);
+#else
+  (void)R;
+  (void)ni;
+  set_err(x.R, ERR_INTERNAL, x.q, node);  // the host emulation has no PRM
+  return 0.0;
+#endif
+}
+
 // executor.cpp:413-444
 SPEX_HDNI void on_reward(const QC& x, u32 node) {
   Run* R = x.R;
   QueryRun* qr = x.qr;
   u32 ni = NI(x, node);
   if (R->n_status[ni] == kPruned) return;
-  double r = oracle_reward(x, node);
+  double r;
+  if (x.c->reward_prm && q_owned(*x.c, x.q)) {
+    // the PRM's score of the thought (K4): wait for its schedule entry
+    r = prm_reward(x, node);
+  } else {
+    r = oracle_reward(x, node);
+  }
   R->n_reward[ni] = r;
   set_fl(x, node, NF_HAS_REWARD);
   touch(x);

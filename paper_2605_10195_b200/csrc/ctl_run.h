@@ -26,13 +26,7 @@ namespace spex {
 
 constexpr double kInf = HUGE_VAL;
 
-SPEX_HD i64 spex_clock() {
-#if SPEX_DEVICE_PASS
-  return static_cast<i64>(clock64());
-#else
-  return 0;
-#endif
-}
+
 // shared int scratch (ex.sm, 1032 ints): [0, nthr] slow scan, [0, nwarp) reductions,
 // then disjoint regions for the fast scan, commit totals and query collection
 constexpr int kSmScan = 560;     // 33 ints
@@ -1090,6 +1084,9 @@ SPEX_HDNI void completions(Run* R, EX& ex, int* warp_off) {
       ex_scan(ex, R->it_scan_d, nf, &ntiles);
       for (int f = ex.tid; f < nf; f += ex.nthr)
         if (R->fin_scored[f] && q_owned(R->cfg, R->st_q[R->fins[f]])) {
+          if (R->cfg.reward_prm)
+            R->n_prm_e[static_cast<u32>(R->st_q[R->fins[f]]) * static_cast<u32>(R->cfg.node_cap) +
+                       R->st_node[R->fins[f]]] = g->n_sched;
           const int k = off + R->it_scan_a[f];
           R->srow_sid[k] = R->fins[f];
           R->srow_pos0[k] = R->fin_tokens[f];
@@ -1139,6 +1136,7 @@ SPEX_HD void run_loop(Run* R, EX& ex, int* warp_off) {
     g->kv_bump = root_pages;
     g->kv_live = root_pages;
     g->kv_peak = root_pages;
+    g->start_ns = spex_wall_ns();
   }
   ex.sync();
   followups(R, ex, warp_off);

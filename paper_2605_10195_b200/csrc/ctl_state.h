@@ -194,6 +194,9 @@ struct Cfg {
   int kv_pages;     // physical pages in the pools
   int kv_pp_root;   // pages of a root prompt (static: query q owns pages [q*pp, (q+1)*pp))
   i64 kv_pt_cap;    // page-table entries
+  // Reward source: 0 = the content oracle (RewardOracle::reward, sim.cpp:146-152,
+  // the reference); 1 = the PRM score of the thought (K4), awaited on device.
+  int reward_prm;
   int lex_rank[kMaxLabels];   // label index -> rank of "a<idx>" in std::map order
   int lex_order[kMaxLabels];  // rank -> label index
 };
@@ -229,6 +232,7 @@ struct QueryRun {
   int terminal_count;  // terminal_answer_count()
   int capacity, pending_specs;
   u32 version, plan_empty_version;
+  i64 finish_ns;  // device wall clock (globaltimer) at query_done
   int need_followup;
   int grant;
   int hits[kMaxTracked + 1], misses[kMaxTracked + 1];
@@ -269,6 +273,8 @@ struct GState {
   i64 kv_free_head, kv_free_tail;  // FIFO ring of freed physical pages (kv_free)
   i64 kv_live, kv_peak, kv_freed;  // pages held by live thoughts (peak) and pages freed
   int n_sched, n_sched_rows;
+  i64 start_ns;   // device wall clock at the start of the run
+  i64 reward_wait_ns;  // time the control spent waiting for PRM scores (reward_prm)
   // device cycle counters per phase (thread 0's view)
   i64 cyc[8];
 };
@@ -314,6 +320,11 @@ struct Run {
   int* n_kvh;     // tree-KV holds: own pin + live children + running stream; 0 frees the pages
   int* kv_pt;     // page table [kv_pt_cap]: physical page of each entry
   int* kv_free;   // freed physical pages, FIFO ring [kv_pages]
+  // PRM-scored rewards (cfg.reward_prm): the forward writes each scored
+  // thought's score and raises its schedule entry's flag
+  float* n_score;  // [NN]
+  int* n_prm_e;    // [NN] schedule entry that scores the node
+  int* prm_done;   // [sched_cap]
   // per-query
   QueryRun* qs;
   QueryTally* q_tally;

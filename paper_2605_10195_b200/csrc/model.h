@@ -61,6 +61,8 @@ struct TreeView {
   int* seg_ctr;             // segment-pool counter of the builder's stream (zeroed before each build)
   int* err;                 // forward error bits: 1 ancestor chain deeper than kMaxChain, 2 segment pool full
   long long seg_cap;        // segment-pool capacity
+  uint64_t run_seed;        // root prompts: query seeds (sim.cpp:177-180)
+  int kv_pp_root;           // root prompts: static pages per query
   int node_cap;
   int prompt_tokens;
   int V;

@@ -345,7 +345,10 @@ static bool wmma_wanted(const ModelShape& s) {
 static void tc_gemm(const CUtensorMap& a, const TcWeight& w, int M, const TcEpilogue& ep, unsigned int* sched,
                     cudaStream_t st) {
   const int rc = spex_k_gemm_tc(&a, &w.map, M, w.N, w.K, &ep, sched, st);
-  if (rc != 0) throw std::runtime_error("tcgen05 GEMM launch failed (" + std::to_string(rc) + ")");
+  if (rc != 0)
+    throw std::runtime_error("tcgen05 GEMM launch failed (" + std::to_string(rc) + ") M=" + std::to_string(M) +
+                             " N=" + std::to_string(w.N) + " K=" + std::to_string(w.K) + " epilogue " +
+                             std::to_string(ep.kind));
 }
 
 // K1 for one layer: PRM / prompt tiles on the TMA + tensor-core tile kernel;

@@ -204,16 +204,21 @@ __global__ void build_prm_rows_kernel(TreeView t, const int* sids, const int* ro
   }
 }
 
-// Root prompt rows: query q, positions 0..P-1; the prompt's pages are static
-// and consecutive, so each row has one segment (segs[i]).
+// Root prompt rows: query q, positions 0..P-1. Nothing here reads state the
+// control kernel writes (it may not have admitted the query yet): the root's
+// path hash is a pure function of the run seed (generate_workload's query
+// seed, sim.cpp:177-180, and the root hash, tree.cpp:57) and its pages are the
+// static [q*pp, (q+1)*pp), consecutive, so each row has one segment (segs[i]).
 __global__ void build_prompt_rows_kernel(TreeView t, int q0, int nq, RowDesc* rows, Segment* segs) {
   const int P = t.prompt_tokens;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nq * P) return;
   const int q = q0 + i / P;
   const int j = i % P;
-  const uint32_t b = (uint32_t)q * (uint32_t)t.node_cap;
-  const long long base = kv_slot(t, b, 0, 0);
+  const long long base = (long long)q * t.kv_pp_root * kPg;
+  const uint64_t base_seed = d_splitmix64(t.run_seed ^ 0x7175657200000008ULL);  // ctl_math.h kSaltQuery
+  const uint64_t qv = (uint64_t)q + 1 + 0x9e3779b97f4a7c15ULL;                      // ctl_math.h hash_mix
+  const uint64_t root_hash = d_splitmix64(d_splitmix64(base_seed ^ (qv + (base_seed << 6) + (base_seed >> 2))));
   Segment* s = segs + i;
   s->base = base;
   s->len = j + 1;
@@ -226,7 +231,7 @@ __global__ void build_prompt_rows_kernel(TreeView t, int q0, int nq, RowDesc* ro
   r.slot = base + j;
   r.seg_off = i;
   r.nseg = 1;
-  r.token = token_id(t.hash[b], j, t.V);
+  r.token = token_id(root_hash, j, t.V);
   r.pad = 0;
   rows[i] = r;
 }

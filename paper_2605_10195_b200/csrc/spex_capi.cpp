@@ -1060,6 +1060,8 @@ void run_executor(spex_executor& ex, int trace) {
       sv.tree.hash = R.n_hash;
       sv.tree.kvbase = R.n_kvbase;
       sv.tree.kv_pt = R.kv_pt;
+      sv.tree.run_seed = R.cfg.run_seed;
+      sv.tree.kv_pp_root = R.cfg.kv_pp_root;
       sv.tree.st_q = R.st_q;
       sv.tree.st_node = R.st_node;
       sv.tree.node_cap = node_cap;

@@ -19,7 +19,7 @@ pytestmark = pytest.mark.gpu
 
 ROW = np.dtype([("q", "<i4"), ("node", "<u4"), ("pos", "<i4"), ("abs_pos", "<i4"), ("slot", "<i8"),
                 ("seg_off", "<i4"), ("nseg", "<i4"), ("token", "<i4"), ("pad", "<i4")])
-SEG = np.dtype([("base", "<i8"), ("len", "<i4"), ("pad", "<i4")])
+SEG = np.dtype([("base", "<i8"), ("len", "<i4"), ("own0", "<i4")])
 MAX_SEG = 40
 N_QUERIES = 5  # rows are spread over a few queries
 
@@ -62,7 +62,7 @@ def _make_tree_rows(rng, M, slots, max_depth):
         own = int(rng.integers(1, lens[node] + 1))
         sl = [(int(bases[a]), int(lens[a])) for a in chain] + [(int(bases[node]), own)]
         for k, (b, n) in enumerate(sl):
-            segs[r * MAX_SEG + k] = (b, n, 0)
+            segs[r * MAX_SEG + k] = (b, n, -1 if k < len(sl) - 1 else 0)
         rows[r] = (int(rng.integers(0, N_QUERIES)), node, own - 1, 0, bases[node] + own - 1, r * MAX_SEG,
                    len(sl), 0, 0)
         paths.append(sl)
@@ -178,31 +178,41 @@ def test_k1_tile_mma_matches_torch_fp32(H, KVH):
     n_nodes = 24
     lens = rng.integers(8, 150, size=n_nodes)
     bases = np.concatenate([[0], np.cumsum(lens)[:-1]])
-    slots = int(bases[-1] + lens[-1]) + 64
+    alt0 = int(bases[-1] + lens[-1]) + 64  # second run of split thoughts (elsewhere in the pool)
+    slots = alt0 + int(lens.sum()) + 64
     parent = np.full(n_nodes, -1)
     for i in range(1, n_nodes):
         parent[i] = rng.integers(0, i)
-    rows, segs, tiles, ctx = [], [], [], []
-    for node in rng.choice(n_nodes, size=6, replace=False):
+    # The product's PRM rows: one segment list per thought (ancestor runs, then
+    # the thought's own runs tagged with their first position, own0), shared by
+    # all its rows; the kernel clips the own runs at each tile's last row.
+    # Every other thought's own tokens are split into two physical runs at a
+    # page boundary, like a thought whose pages came from the free ring.
+    rows, seg_lists, tiles, ctx = [], [], [], []
+    for ti, node in enumerate(rng.choice(n_nodes, size=6, replace=False)):
         chain, c = [], parent[node]
         while c >= 0:
             chain.append(c)
             c = parent[c]
-        anc = [(int(bases[a]), int(lens[a])) for a in chain[::-1]]
+        anc = [(int(bases[a]), int(lens[a]), -1) for a in chain[::-1]]
         n = int(lens[node])
+        split = 16 * (1 + int(rng.integers(0, max(1, (n - 1) // 16)))) if ti % 2 == 0 and n > 16 else n
+        own = [(int(bases[node]), split, 0)] + ([(alt0 + int(bases[node]), n - split, split)] if split < n else [])
+        sl = anc + own
+        off = len(seg_lists)
+        seg_lists.extend(sl)
+        anc_idx = [b + t for (b, ln, _) in anc for t in range(ln)]
+        own_idx = [int(bases[node]) + t if t < split else alt0 + int(bases[node]) + (t - split) for t in range(n)]
         for j0 in range(0, n, 16):
             tiles.append((len(rows), min(16, n - j0)))
             for j in range(j0, min(n, j0 + 16)):
-                sl = anc + [(int(bases[node]), j + 1)]
-                rows.append((0, node, j, 0, int(bases[node]) + j, len(rows) * MAX_SEG, len(sl), 0, 0))
-                segs.append(sl)
-                ctx.append(sl)
+                rows.append((0, node, j, 0, own_idx[j], off, len(sl), 0, 0))
+                ctx.append(anc_idx + own_idx[: j + 1])
     M = len(rows)
     rows_np = np.array(rows, ROW)
-    segs_np = np.zeros(M * MAX_SEG, SEG)
-    for r, sl in enumerate(segs):
-        for k, (b, n) in enumerate(sl):
-            segs_np[r * MAX_SEG + k] = (b, n, 0)
+    segs_np = np.zeros(max(len(seg_lists), 1), SEG)
+    for k, (b, ln, o) in enumerate(seg_lists):
+        segs_np[k] = (b, ln, o)
     tiles_np = np.array(tiles, TILE)
     dev = torch.device("cuda", 0)
     g = torch.Generator(device="cpu").manual_seed(H * 7 + KVH)
@@ -225,7 +235,7 @@ def test_k1_tile_mma_matches_torch_fp32(H, KVH):
     G = H // KVH
     worst = 0.0
     for r in range(M):
-        idx = torch.cat([torch.arange(b, b + n) for b, n in ctx[r]]).to(dev)
+        idx = torch.as_tensor(ctx[r], device=dev)
         for h in range(H):
             kh = h // G
             p = torch.softmax(Kf[kh, idx] @ Q[r, h], dim=0)

@@ -70,10 +70,10 @@ def test_page_reuse_keeps_outputs(cfgname, policy, prm, wseed):
     else:
         cfg = (ROOT / "configs" / f"{cfgname}.json").read_text()
     seed = json.loads(cfg)["run"].get("seed", 1)
-    log, dec, prm_out, kv, ms = _run(cfg, seed, policy, prm, wseed, 1 << 20)
+    log, dec, prm_out, kv, ms = _run(cfg, seed, policy, prm, wseed, 0)  # default pool: free HBM
     assert ms["streamed"] == 1
     assert kv["live_pages_end"] == kv["root_pages"], kv
-    assert kv["fresh_pages"] == kv["allocated_pages"], kv  # roomy: no reuse
+    assert kv["allocated_pages"] < kv["pages"] and kv["fresh_pages"] == kv["allocated_pages"], kv  # no reuse
     tight = kv["peak_pages"] + 25
     log2, dec2, prm2, kv2, ms2 = _run(cfg, seed, policy, prm, wseed, tight)
     assert ms2["streamed"] == 1
@@ -97,7 +97,7 @@ def test_pool_below_live_peak_fails_loudly():
     import paper_2605_10195_b200 as spex
     cfg = (ROOT / "configs" / "c1_rebase_w4_q16.json").read_text()
     seed = json.loads(cfg)["run"]["seed"]
-    _, _, _, kv, _ = _run(cfg, seed, "small_policy", "small_prm", 7, 1 << 20)
+    _, _, _, kv, _ = _run(cfg, seed, "small_policy", "small_prm", 7, 0)
     ex = spex.Executor(cfg, seed, None, trace=False)
     ex.set_model("small_policy", "small_prm", weight_seed=7)
     ex.set_kv_pages((kv["peak_pages"] + kv["root_pages"]) // 2)
