@@ -166,6 +166,18 @@ int spex_executor_prm_outputs(spex_executor* ex, void* buf, long long cap, long 
 int spex_run_batch(const char* config_json, const uint64_t* seeds, int n, const char* flags_csv, int device,
                    spex_totals* totals, double* device_ms);
 
+/* Reward source: 0 = the content oracle (RewardOracle::reward, sim.cpp:146-152;
+ * the reference, event logs byte-compatible), 1 = the PRM score of the
+ * thought (K4; "model mode"). With 1 the control kernel waits on device for
+ * each scored thought's PRM batch before its reward event, so the search is
+ * steered by the model; needs set_model with a PRM, no shard, the streamed
+ * forward. Call before spex_executor_run. */
+int spex_executor_set_reward_source(spex_executor* ex, int source);
+/* Device wall-clock latency of each query (ms from the run's start to its
+ * query_done; -1 if unfinished) and the total time the control kernel spent
+ * waiting for PRM scores. */
+int spex_executor_query_wall_ms(spex_executor* ex, double* out, int cap, int* n, double* reward_wait_ms);
+
 /* Per-query virtual finish time (query_done.t; admission is at t = 0 when
  * batch_size = n_queries): the search latency of each query. */
 int spex_executor_query_finish(spex_executor* ex, double* out, int cap, int* n);

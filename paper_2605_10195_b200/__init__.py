@@ -190,6 +190,22 @@ class Executor:
         """Tree-KV pool size in pages of 16 tokens (0: the default, 55% of free HBM)."""
         _check(self._L.spex_executor_set_kv_pages(self._h, int(pages)))
 
+    def set_reward_source(self, source: str) -> None:
+        """"oracle": rewards from the content oracle (the reference's RewardOracle);
+        "prm": rewards are the PRM's scores, awaited on device (model mode)."""
+        if source not in ("oracle", "prm"):
+            raise ValueError("reward source is 'oracle' or 'prm'")
+        _check(self._L.spex_executor_set_reward_source(self._h, 1 if source == "prm" else 0))
+
+    def query_wall_ms(self) -> tuple:
+        """(per-query device wall-clock latency in ms, ms the control waited for PRM scores)."""
+        n = ctypes.c_int()
+        w = ctypes.c_double()
+        _check(self._L.spex_executor_query_wall_ms(self._h, None, 0, ctypes.byref(n), ctypes.byref(w)))
+        buf = (ctypes.c_double * max(n.value, 1))()
+        _check(self._L.spex_executor_query_wall_ms(self._h, buf, n.value, ctypes.byref(n), ctypes.byref(w)))
+        return list(buf[: n.value]), w.value
+
     def kv_stats(self) -> dict:
         s = _lib.KvStats()
         _check(self._L.spex_executor_kv_stats(self._h, ctypes.byref(s)))

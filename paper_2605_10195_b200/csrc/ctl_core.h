@@ -740,7 +740,7 @@ SPEX_HDNI void finish_query(const QC& x, bool early) {
   qr->finished = 1;
   qr->early = early ? 1 : 0;
   qr->finish_time = R->g->now;
-  qr->finish_ns = spex_wall_ns();
+  R->q_finish_ns[x.q] = spex_wall_ns();
   x.it->fin = 1;
   touch(x);
   if (early) {

@@ -232,11 +232,12 @@ struct QueryRun {
   int terminal_count;  // terminal_answer_count()
   int capacity, pending_specs;
   u32 version, plan_empty_version;
-  i64 finish_ns;  // device wall clock (globaltimer) at query_done
   int need_followup;
   int grant;
   int hits[kMaxTracked + 1], misses[kMaxTracked + 1];
 };
+
+static_assert(sizeof(QueryRun) % 16 == 0, "QueryRun is staged to shared memory in 16-byte units");
 
 // AnswerTally::by_label_ (termination.hpp:15-43), by label index; kept apart
 // from QueryRun so the hot per-query records stay small (shared-memory resident
@@ -328,6 +329,7 @@ struct Run {
   // per-query
   QueryRun* qs;
   QueryTally* q_tally;
+  i64* q_finish_ns;  // device wall clock (globaltimer) at each query's query_done
   u32* q_rest_stack;
   u32* q_layer;
   u32* q_cohort;

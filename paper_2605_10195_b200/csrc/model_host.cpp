@@ -67,6 +67,8 @@ int spex_k_gemm_tc(const CUtensorMap* tmA, const CUtensorMap* tmB, int M, int N,
 void spex_k_lse_combine(const float* part, int M, int n_tiles, int* amax, float* lse, float* lsum, cudaStream_t s);
 void spex_k_rope_table(const RowDesc* rows, int M, const float* inv_freq, int half, float* out, cudaStream_t s);
 void spex_k_interleave_gu(const __nv_bfloat16* wgu, int F, int d, __nv_bfloat16* out, cudaStream_t s);
+void spex_k_prm_publish(const RowDesc* rows, const int* last_row, int n, const float* score, int node_cap,
+                        float* node_score, int* done, cudaStream_t s);
 void spex_k_value_head(const __nv_bfloat16* Hn, int d, const int* last_row, int n, const __nv_bfloat16* w,
                        float* score, cudaStream_t s);
 void spex_k_gather_prm(const RowDesc* rows, const int* last_row, int n, const float* score, PrmOut* out,
@@ -689,7 +691,7 @@ void run_model_schedule(const ModelRunConfig& mc, const ScheduleView& sv, ModelR
   PrmOut* dbg_scores = mc.record_outputs ? reinterpret_cast<PrmOut*>(mc.out_scores) : nullptr;
   long long dbg_n = 0, dbg_s = 0;
 
-  auto process = [&](const PubEntry& pe) {
+  auto process = [&](const PubEntry& pe, int e) {
     if (pe.kind == SCHED_DECODE) {
       for (int s = 0; s < pe.steps; ++s) {
         for (int c0 = 0; c0 < pe.n; c0 += max_dec) {
@@ -727,6 +729,10 @@ void run_model_schedule(const ModelRunConfig& mc, const ScheduleView& sv, ModelR
                             rows2, segs2, last_row, tiles2, st2);
       forward(*prm, rows2, segs2, pe.rows, st2, nullptr, tiles2, pe.tiles);
       spex_k_value_head(prm->Xn, mc.prm.d, last_row, pe.n, prm->vhead, scores, st2);
+      if (sv.prm_done) {
+        spex_k_prm_publish(rows2, last_row, pe.n, scores, sv.tree.node_cap, sv.node_score, sv.prm_done + e, st2);
+        g_launches += 1;
+      }
       g_launches += 2;
       if (dbg_scores && dbg_s + pe.n <= mc.out_scores_cap) {
         spex_k_gather_prm(rows2, last_row, pe.n, scores, dbg_scores + dbg_s, st2);
@@ -738,7 +744,7 @@ void run_model_schedule(const ModelRunConfig& mc, const ScheduleView& sv, ModelR
   };
 
   if (!streaming) {
-    for (int e = 0; e < sv.n_entries; ++e) process(sv.entries_host[e]);
+    for (int e = 0; e < sv.n_entries; ++e) process(sv.entries_host[e], e);
   } else {
     volatile PubHead* head = reinterpret_cast<volatile PubHead*>(sv.pub_head);
     volatile PubEntry* ents = reinterpret_cast<volatile PubEntry*>(sv.pub_entries);
@@ -758,7 +764,7 @@ void run_model_schedule(const ModelRunConfig& mc, const ScheduleView& sv, ModelR
           pe.tiles = ents[e].tiles;
           pe.u0 = ents[e].u0;
           pe.kv_next = ents[e].kv_next;
-          process(pe);
+          process(pe, e);
         }
         continue;
       }

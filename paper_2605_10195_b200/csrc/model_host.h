@@ -43,6 +43,10 @@ struct ScheduleView {
   const int* srow_pos0;
   const int* srow_rstart;
   const int* srow_tstart;
+  // PRM rewards (reward source 1): each scored thought's score at node_score[q*node_cap+node],
+  // then prm_done[entry] = 1 (the control kernel waits on it)
+  float* node_score = nullptr;
+  int* prm_done = nullptr;
 };
 
 struct ModelRunResult {

@@ -1802,6 +1802,24 @@ extern "C" int spex_k_tree_attn_tiles(const TileDesc* tiles, int ntiles, const R
   return -1;
 }
 
+// PRM rewards: scatter the entry's scores to their nodes, then raise the
+// entry's flag for the control kernel (which spins on it in prm_reward).
+__global__ void prm_publish_kernel(const RowDesc* __restrict__ rows, const int* __restrict__ last_row, int n,
+                                   const float* __restrict__ score, int node_cap, float* node_score, int* done) {
+  for (int k = threadIdx.x; k < n; k += blockDim.x) {
+    const RowDesc r = rows[last_row[k]];
+    node_score[(long long)r.q * node_cap + r.node] = score[k];
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) atomicExch(done, 1);
+}
+
+extern "C" void spex_k_prm_publish(const RowDesc* rows, const int* last_row, int n, const float* score, int node_cap,
+                                   float* node_score, int* done, cudaStream_t s) {
+  prm_publish_kernel<<<1, 256, 0, s>>>(rows, last_row, n, score, node_cap, node_score, done);
+}
+
 extern "C" void spex_k_value_head(const __nv_bfloat16* Hn, int d, const int* last_row, int n,
                                   const __nv_bfloat16* w, float* score, cudaStream_t s) {
   value_head_kernel<<<n, 128, 0, s>>>(Hn, d, last_row, n, w, score);

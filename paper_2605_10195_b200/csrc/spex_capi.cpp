@@ -464,6 +464,8 @@ struct spex_executor {
   long long kv_pages_req = 0;       // tree-KV pool pages (0: sized from free HBM when a model is attached)
   long long kv_pt_cap = 0;          // page-table entries of the last run
   long long kv_pages = 0;           // pool pages of the last run
+  int reward_prm = 0;               // reward source: 0 content oracle (reference), 1 PRM score
+  std::vector<long long> finish_ns; // per-query device wall clock at query_done
 #ifndef SPEX_EMU
   cudaStream_t stream = nullptr;
   cudaStream_t mstream = nullptr;
@@ -612,6 +614,7 @@ void set_cfg(const spex_executor& ex, Cfg& c, int node_cap, int stream_cap, int 
   c.stage_cap = stage_cap;
   c.trace = trace;
   c.record_sched = record_sched;
+  c.reward_prm = ex.reward_prm;
   c.shard_lo = std::min(ex.shard_lo, h.n_queries);
   c.shard_hi = ex.shard_hi < 0 ? h.n_queries : std::min(ex.shard_hi, h.n_queries);
   c.sched_cap = record_sched ? 4 * stream_cap + 1024 : 1;
@@ -652,6 +655,7 @@ void layout(Arena& A, Run& R, int Q, int node_cap, int stream_cap, int log_cap, 
   A.add(R.n_kvh, NN);
   A.add(R.qs, Q);
   A.add(R.q_tally, Q);
+  A.add(R.q_finish_ns, Q);
   A.add(R.q_rest_stack, NN);
   A.add(R.q_layer, NN);
   A.add(R.q_cohort, NN);
@@ -719,6 +723,11 @@ void layout(Arena& A, Run& R, int Q, int node_cap, int stream_cap, int log_cap, 
   A.add(R.srow_rstart, static_cast<size_t>(R.cfg.sched_rows_cap));
   A.add(R.srow_tstart, static_cast<size_t>(R.cfg.sched_rows_cap));
   if (R.cfg.record_sched) A.add(R.pub_e, static_cast<size_t>(R.cfg.sched_cap));
+  if (R.cfg.reward_prm) {
+    A.add(R.n_score, NN);
+    A.add(R.n_prm_e, NN);
+    A.add(R.prm_done, static_cast<size_t>(R.cfg.sched_cap));
+  }
 }
 
 std::string label_str(int idx) { return idx < 0 ? std::string() : "a" + std::to_string(idx); }
@@ -898,6 +907,16 @@ void kv_configure(spex_executor& ex, Cfg& c, long long pages) {
 
 void run_executor(spex_executor& ex, int trace) {
   const HostConfig& h = ex.hc;
+#ifndef SPEX_EMU
+  if (ex.reward_prm && (!ex.with_model || !ex.mc.with_prm))
+    fail(ERR_INVALID_ARGUMENT, "PRM rewards need a model with a PRM (spex_executor_set_model)");
+  if (ex.reward_prm && (ex.shard_lo > 0 || (ex.shard_hi >= 0 && ex.shard_hi < h.n_queries)))
+    fail(ERR_INVALID_ARGUMENT, "PRM rewards need every query's PRM on this executor (no shard)");
+  if (ex.reward_prm && std::getenv("SPEX_SEQUENTIAL"))
+    fail(ERR_INVALID_ARGUMENT, "PRM rewards need the streamed forward (SPEX_SEQUENTIAL is set)");
+#else
+  if (ex.reward_prm) fail(ERR_INVALID_ARGUMENT, "PRM rewards need the CUDA build");
+#endif
   const int Q = h.n_queries;
   int node_cap = 512;
   if (const char* e = std::getenv("SPEX_NODE_CAP")) node_cap = std::max(16, std::atoi(e));
@@ -1061,6 +1080,8 @@ void run_executor(spex_executor& ex, int trace) {
       sv.tree.kvbase = R.n_kvbase;
       sv.tree.kv_pt = R.kv_pt;
       sv.tree.run_seed = R.cfg.run_seed;
+      sv.node_score = R.cfg.reward_prm ? R.n_score : nullptr;
+      sv.prm_done = R.cfg.reward_prm ? R.prm_done : nullptr;
       sv.tree.kv_pp_root = R.cfg.kv_pp_root;
       sv.tree.st_q = R.st_q;
       sv.tree.st_node = R.st_node;
@@ -1166,6 +1187,9 @@ void run_executor(spex_executor& ex, int trace) {
     cudaEventDestroy(cb);
     ex.qs.resize(Q);
     CUDA_OK(cudaMemcpyAsync(ex.qs.data(), R.qs, sizeof(QueryRun) * Q, cudaMemcpyDeviceToHost, ex.stream));
+    ex.finish_ns.resize(Q);
+    CUDA_OK(cudaMemcpyAsync(ex.finish_ns.data(), R.q_finish_ns, sizeof(long long) * Q, cudaMemcpyDeviceToHost,
+                            ex.stream));
     CUDA_OK(cudaStreamSynchronize(ex.stream));
     if (trace && ex.g.log_n > 0) {
       ex.log.resize(ex.g.log_n);
@@ -1540,6 +1564,24 @@ int spex_executor_prm_outputs(spex_executor* ex, void* buf, long long cap, long 
     (void)cap;
     *n = 0;
 #endif
+  });
+}
+
+int spex_executor_set_reward_source(spex_executor* ex, int source) {
+  return guarded([&] {
+    if (source != 0 && source != 1) fail(ERR_INVALID_ARGUMENT, "set_reward_source: 0 (content oracle) or 1 (PRM)");
+    if (ex->ran) fail(ERR_INVALID_ARGUMENT, "set_reward_source: executor already ran");
+    ex->reward_prm = source;
+  });
+}
+
+int spex_executor_query_wall_ms(spex_executor* ex, double* out, int cap, int* n, double* reward_wait_ms) {
+  return guarded([&] {
+    const int q = static_cast<int>(ex->finish_ns.size());
+    for (int i = 0; i < q && i < cap; ++i)
+      out[i] = ex->finish_ns[i] > 0 ? 1e-6 * static_cast<double>(ex->finish_ns[i] - ex->g.start_ns) : -1.0;
+    *n = q;
+    if (reward_wait_ms) *reward_wait_ms = 1e-6 * static_cast<double>(ex->g.reward_wait_ns);
   });
 }
 
