@@ -69,7 +69,13 @@ SPEX_HDNI double prm_reward(const QC& x, u32 node) {
   const int e = R->n_prm_e[ni];
   if (*reinterpret_cast<volatile int*>(&R->prm_done[e]) == 0) {
     const i64 t0 = spex_wall_ns();
-    while (*reinterpret_cast<volatile int*>(&R->prm_done[e]) == 0) __nanosleep(256);
+    while (*reinterpret_cast<volatile int*>(&R->prm_done[e]) == 0) {
+      __nanosleep(256);
+      if (spex_wall_ns() - t0 > 120000000000LL) {  // watchdog: no score in 120 s (forward gone)
+        set_err(R, ERR_STALLED, x.q, node);
+        return 0.0;
+      }
+    }
     atomic_add_i64(&R->g->reward_wait_ns, spex_wall_ns() - t0);
   }
   __threadfence();

@@ -1067,6 +1067,7 @@ SPEX_HDNI void completions(Run* R, EX& ex, int* warp_off) {
     for (int f = ex.tid; f < nf; f += ex.nthr)
       R->it_scan_a[f] = R->fin_scored[f] && q_owned(R->cfg, R->st_q[R->fins[f]]) ? 1 : 0;
     ex.sync();
+    const int e_prm = g->n_sched;  // this boundary's PRM entry (read before thread 0 bumps it)
     int ns = 0;
     ex_scan(ex, R->it_scan_a, nf, &ns);
     const int off = g->n_sched_rows;
@@ -1086,7 +1087,7 @@ SPEX_HDNI void completions(Run* R, EX& ex, int* warp_off) {
         if (R->fin_scored[f] && q_owned(R->cfg, R->st_q[R->fins[f]])) {
           if (R->cfg.reward_prm)
             R->n_prm_e[static_cast<u32>(R->st_q[R->fins[f]]) * static_cast<u32>(R->cfg.node_cap) +
-                       R->st_node[R->fins[f]]] = g->n_sched;
+                       R->st_node[R->fins[f]]] = e_prm;
           const int k = off + R->it_scan_a[f];
           R->srow_sid[k] = R->fins[f];
           R->srow_pos0[k] = R->fin_tokens[f];
