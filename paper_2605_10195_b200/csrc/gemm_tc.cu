@@ -830,3 +830,34 @@ extern "C" void spex_k_interleave_gu(const __nv_bfloat16* wgu, int F, int d, __n
   const long long n = 2LL * F * d;
   interleave_gu_kernel<<<(int)((n + 255) / 256), 256, 0, s>>>(wgu, F, d, out);
 }
+
+namespace spex {
+namespace {
+template <class K>
+void preload_fn(K k) {
+  cudaFuncAttributes a;
+  cudaFuncGetAttributes(&a, k);
+}
+template <int EPI, int DH>
+void preload_epi() {
+  preload_fn(gemm_tc_kernel<EPI, DH, 256, 2>);
+  preload_fn(gemm_tc_kernel<EPI, DH, 128, 2>);
+  preload_fn(gemm_tc_kernel<EPI, DH, 256, 1>);
+  preload_fn(gemm_tc_kernel<EPI, DH, 128, 1>);
+  if constexpr (EPI == TC_EPI_STORE) preload_fn(gemm_tc_kernel<EPI, DH, 64, 1>);
+}
+}  // namespace
+}  // namespace spex
+
+// Loads every GEMM instantiation launch_shape can pick (see spex_k_preload).
+extern "C" void spex_k_gemm_preload() {
+  using namespace spex;
+  preload_epi<TC_EPI_STORE, 128>();
+  preload_epi<TC_EPI_SWIGLU, 128>();
+  preload_epi<TC_EPI_LSE, 128>();
+  preload_epi<TC_EPI_ROPE_KV, 128>();
+  preload_epi<TC_EPI_ROPE_KV, 64>();
+  preload_fn(lse_combine_kernel);
+  preload_fn(rope_table_kernel);
+  preload_fn(interleave_gu_kernel);
+}

@@ -572,18 +572,25 @@ extern "C" void spex_model_cache_clear() {
 // finished control run (sv.entries_host) or live from the running control
 // kernel through host-mapped memory (sv.pub_head / sv.pub_entries): the model
 // stream then works on entry e while the control kernel produces e+1, ...
-void run_model_schedule(const ModelRunConfig& mc, const ScheduleView& sv, ModelRunResult* res, cudaStream_t st) {
-  std::vector<void*> owned;
+// Everything the forward allocates or (re)creates — models, KV pools, row
+// buffers — before the control kernel starts: with PRM rewards the control
+// waits on the forward, so nothing that synchronises the device (cudaFree,
+// model init) may run while it is live.
+extern "C" void spex_k_preload();
+extern "C" void spex_k_gemm_preload();
+
+static void prepare_cache(const ModelRunConfig& mc, const ScheduleView& sv, cudaStream_t st) {
+  static const bool preloaded = [] {
+    spex_k_preload();
+    spex_k_gemm_preload();
+    return true;
+  }();
+  (void)preloaded;
   const int Q = sv.n_queries, P = sv.tree.prompt_tokens;
-  const bool streaming = sv.pub_head != nullptr;
   const int max_dec = sv.max_decode_rows, max_prm = sv.max_prm_rows;
   const int prompt_chunk = std::max(1, std::min(Q, 4096 / std::max(P, 1)));
   const long long slots = std::max<long long>(sv.kv_slots, 1);
-
   if (!g_cache.st2) CK(cudaStreamCreateWithFlags(&g_cache.st2, cudaStreamNonBlocking));
-  // PRM stream: same device, ordered after everything already queued on st
-  const bool prm_overlap = !std::getenv("SPEX_PRM_SAME_STREAM");
-  cudaStream_t st2 = prm_overlap ? g_cache.st2 : st;
   if (g_cache.seed != mc.seed) spex_model_cache_clear();
   Model* pol = cached(g_cache.pol, mc.policy, false, mc.seed, slots, std::max(max_dec, prompt_chunk * P), st);
   Model* prm = mc.with_prm ? cached(g_cache.prm, mc.prm, true, mc.seed, slots, std::max(max_prm, prompt_chunk * P), st)
@@ -621,18 +628,38 @@ void run_model_schedule(const ModelRunConfig& mc, const ScheduleView& sv, ModelR
     g_cache.tiles2 = dalloc<TileDesc>(rows_cap, keep);
     g_cache.rows_cap = rows_cap;
   }
-  RowDesc* rows = g_cache.rows;
-  Segment* segs = g_cache.segs;
-  RowDesc* rows2 = prm_overlap ? g_cache.rows2 : g_cache.rows;
-  Segment* segs2 = prm_overlap ? g_cache.segs2 : g_cache.segs;
-  TileDesc* tiles2 = prm_overlap ? g_cache.tiles2 : g_cache.tiles;
-  int* last_row = g_cache.last_row;
   if (g_cache.row_order_cap < max_dec) {
     cudaFree(g_cache.row_order);
     std::vector<void*> keep;
     g_cache.row_order = dalloc<int>(std::max(max_dec, 1), keep);
     g_cache.row_order_cap = max_dec;
   }
+  CK(cudaStreamSynchronize(st));
+}
+
+extern "C" void spex_model_prepare(const ModelRunConfig* mc, const ScheduleView* sv, cudaStream_t st) {
+  prepare_cache(*mc, *sv, st);
+}
+
+void run_model_schedule(const ModelRunConfig& mc, const ScheduleView& sv, ModelRunResult* res, cudaStream_t st) {
+  std::vector<void*> owned;
+  const int Q = sv.n_queries, P = sv.tree.prompt_tokens;
+  const bool streaming = sv.pub_head != nullptr;
+  const int max_dec = sv.max_decode_rows, max_prm = sv.max_prm_rows;
+  const int prompt_chunk = std::max(1, std::min(Q, 4096 / std::max(P, 1)));
+  const long long slots = std::max<long long>(sv.kv_slots, 1);
+
+  prepare_cache(mc, sv, st);
+  const bool prm_overlap = !std::getenv("SPEX_PRM_SAME_STREAM");
+  cudaStream_t st2 = prm_overlap ? g_cache.st2 : st;
+  Model* pol = g_cache.pol;
+  Model* prm = mc.with_prm ? g_cache.prm : nullptr;
+  RowDesc* rows = g_cache.rows;
+  Segment* segs = g_cache.segs;
+  RowDesc* rows2 = prm_overlap ? g_cache.rows2 : g_cache.rows;
+  Segment* segs2 = prm_overlap ? g_cache.segs2 : g_cache.segs;
+  TileDesc* tiles2 = prm_overlap ? g_cache.tiles2 : g_cache.tiles;
+  int* last_row = g_cache.last_row;
   TileDesc* tiles = g_cache.tiles;
   float* scores = g_cache.scores;
 

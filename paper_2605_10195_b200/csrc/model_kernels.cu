@@ -1681,19 +1681,8 @@ extern "C" int spex_k_tree_attn_bulk(const RowDesc* rows, const Segment* segs, c
                                      __nv_bfloat16* O, int M, int* item_ctr, cudaStream_t s) {
   if (M <= 0) return 0;
   if (dh != 128 || H != KVH) return -1;
-  static const int cfg = getenv("SPEX_K1_BULK_CFG") ? atoi(getenv("SPEX_K1_BULK_CFG")) : 0;
-  switch (cfg) {
-    case 1: return launch_bulk<8, 3, 16>(rows, segs, Qr, H, KVH, Kp, Vp, slots, O, M, item_ctr, s);
-    case 2: return launch_bulk<16, 2, 12>(rows, segs, Qr, H, KVH, Kp, Vp, slots, O, M, item_ctr, s);
-    case 3: return launch_bulk<32, 2, 6>(rows, segs, Qr, H, KVH, Kp, Vp, slots, O, M, item_ctr, s);
-    case 4: return launch_bulk<8, 2, 24>(rows, segs, Qr, H, KVH, Kp, Vp, slots, O, M, item_ctr, s);
-    case 5: return launch_bulk<16, 2, 14>(rows, segs, Qr, H, KVH, Kp, Vp, slots, O, M, item_ctr, s);
-    case 6: return launch_bulk<8, 3, 18>(rows, segs, Qr, H, KVH, Kp, Vp, slots, O, M, item_ctr, s);
-    case 7: return launch_bulk<8, 4, 14>(rows, segs, Qr, H, KVH, Kp, Vp, slots, O, M, item_ctr, s);
-    case 8: return launch_bulk<16, 3, 8>(rows, segs, Qr, H, KVH, Kp, Vp, slots, O, M, item_ctr, s);
-    default:  // measured best on c2 (tools: SPEX_K1_BULK_CFG sweep)
-      return launch_bulk<16, 2, 14>(rows, segs, Qr, H, KVH, Kp, Vp, slots, O, M, item_ctr, s);
-  }
+  // 16-token stages, 2 per warp, 14 warps: the best of an 8-point sweep on c2
+  return launch_bulk<16, 2, 14>(rows, segs, Qr, H, KVH, Kp, Vp, slots, O, M, item_ctr, s);
 }
 
 // K1 decode rows on the per-warp TMA + mma.sync pipeline (G <= 16, dh = 128);
@@ -1726,18 +1715,8 @@ extern "C" int spex_k_tree_attn_wmma(const CUtensorMap* kmap16, const CUtensorMa
   const int G = H / KVH;
   if (M <= 0) return 0;
   if (dh != 128 || G < 1 || G > 16) return -1;
-  // stages x warps (8 KB per stage): bytes in flight per SM vs warps to hide the math
-  static const int cfg = getenv("SPEX_K1_WMMA_CFG") ? atoi(getenv("SPEX_K1_WMMA_CFG")) : 0;
-  switch (cfg) {
-    case 1: return launch_wmma<3, 8>(kmap16, vmap16, rows, segs, Qr, H, KVH, G, slots, O, M, item_ctr, s);
-    case 2: return launch_wmma<4, 6>(kmap16, vmap16, rows, segs, Qr, H, KVH, G, slots, O, M, item_ctr, s);
-    case 3: return launch_wmma<3, 9>(kmap16, vmap16, rows, segs, Qr, H, KVH, G, slots, O, M, item_ctr, s);
-    case 4: return launch_wmma<2, 13>(kmap16, vmap16, rows, segs, Qr, H, KVH, G, slots, O, M, item_ctr, s);
-    case 5: return launch_wmma<kMmaNST, kMmaWarps, true>(kmap16, vmap16, rows, segs, Qr, H, KVH, G, slots, O, M,
-                                                         item_ctr, s);
-    default: return launch_wmma<kMmaNST, kMmaWarps>(kmap16, vmap16, rows, segs, Qr, H, KVH, G, slots, O, M, item_ctr,
-                                                    s);
-  }
+  // 2 stages x 12 warps (8 KB per stage): the best of a stages x warps sweep on c5
+  return launch_wmma<kMmaNST, kMmaWarps>(kmap16, vmap16, rows, segs, Qr, H, KVH, G, slots, O, M, item_ctr, s);
 }
 
 template <int DH, int G>
@@ -1823,4 +1802,55 @@ extern "C" void spex_k_prm_publish(const RowDesc* rows, const int* last_row, int
 extern "C" void spex_k_value_head(const __nv_bfloat16* Hn, int d, const int* last_row, int n,
                                   const __nv_bfloat16* w, float* score, cudaStream_t s) {
   value_head_kernel<<<n, 128, 0, s>>>(Hn, d, last_row, n, w, score);
+}
+
+// Loads every kernel the forward can launch (cudaFuncGetAttributes forces the
+// lazy loader), so no module load — which may synchronise the context — can
+// happen while the control kernel spins on a PRM score (model mode).
+namespace spex {
+template <class K>
+static void preload_one(K k) {
+  cudaFuncAttributes a;
+  cudaFuncGetAttributes(&a, k);
+}
+}  // namespace spex
+
+extern "C" void spex_k_preload() {
+  using namespace spex;
+  preload_one(init_weights_kernel);
+  preload_one(build_decode_rows_kernel);
+  preload_one(build_prm_rows_kernel);
+  preload_one(build_prompt_rows_kernel);
+  preload_one(build_prompt_tiles_kernel);
+  preload_one(prm_scan_all_kernel);
+  preload_one(gather_prm_kernel);
+  preload_one(gather_outputs_kernel);
+  preload_one(embed_kernel);
+  preload_one(rmsnorm_bf16_kernel);
+  preload_one(rmsnorm_bf16_reg_kernel<4>);
+  preload_one(rmsnorm_bf16_reg_kernel<8>);
+  preload_one(rmsnorm_bf16_reg_kernel<12>);
+#define SPEX_PRELOAD_DEC(D, GG)                      \
+  preload_one(tree_attn_decode_kernel<D, GG, 8>);    \
+  preload_one(tree_attn_decode_kernel<D, GG, 4>);    \
+  preload_one(tree_attn_tile_kernel<D, GG>);
+  SPEX_PRELOAD_DEC(128, 1)
+  SPEX_PRELOAD_DEC(128, 2)
+  SPEX_PRELOAD_DEC(128, 4)
+  SPEX_PRELOAD_DEC(128, 6)
+  SPEX_PRELOAD_DEC(64, 1)
+  SPEX_PRELOAD_DEC(64, 2)
+#undef SPEX_PRELOAD_DEC
+  preload_one(tree_attn_decode_kernel<128, 8, 8>);
+  preload_one(tree_attn_decode_kernel<128, 8, 4>);
+  preload_one(tree_attn_decode_kernel<64, 4, 8>);
+  preload_one(tree_attn_decode_kernel<64, 4, 4>);
+  preload_one(tree_attn_bulk_kernel<16, 2, 14>);
+  preload_one(tree_attn_wmma_kernel<kMmaNST, kMmaWarps, false>);
+  preload_one(tree_attn_tile_mma_kernel<1>);
+  preload_one(tree_attn_tile_mma_kernel<2>);
+  preload_one(tree_attn_tile_mma_kernel<4>);
+  preload_one(order_rows_kernel);
+  preload_one(value_head_kernel);
+  preload_one(prm_publish_kernel);
 }

@@ -487,6 +487,7 @@ extern "C" int spex_launch_control_batch_async(Run* d_runs, int n_runs, int n_qu
 extern "C" void spex_model_cache_clear();
 extern "C" void spex_model_cache_release_mismatch(const ModelRunConfig* mc);
 extern "C" long long spex_model_pool_slots(const ModelRunConfig* mc);
+extern "C" void spex_model_prepare(const ModelRunConfig* mc, const ScheduleView* sv, cudaStream_t st);
 #define CUDA_OK(x)                                                                  \
   do {                                                                              \
     cudaError_t e_ = (x);                                                           \
@@ -1115,6 +1116,16 @@ void run_executor(spex_executor& ex, int trace) {
     bool model_done = false;
     ex.mres = ModelRunResult{};
     sv.kv_slots = static_cast<long long>(R.cfg.kv_pages) * kKvPage;
+    if (ex.with_model) {
+      // models, pools and row buffers exist before the control kernel starts
+      // (nothing may synchronise the device while it waits on PRM scores)
+      try {
+        spex_model_prepare(&mc, &sv, ex.mstream);
+      } catch (const std::exception& e) {
+        cleanup();
+        fail(201, std::string("model forward: ") + e.what());
+      }
+    }
     if (streaming) {
       CUDA_OK(cudaStreamSynchronize(ex.stream));
       sv.pub_head = h_head;
