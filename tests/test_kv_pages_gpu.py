@@ -5,10 +5,12 @@ peak, so the pages of dead thoughts (pruned, REBASE layers expanded, scored
 terminals, finished queries) are handed to new thoughts while the forward —
 which lags the control kernel — still streams the schedule. Reuse must not
 change a decision (same event log) or an output: every decode row's
-logsumexp / argmax and every PRM score equals the roomy run's within 1e-5
-relative (fp32 summation order may differ where a thought's pages are split
-into several runs), and sampled rows match the fp32 oracle at 1e-3. A pool
-below the live peak fails with CapacityTreeKV instead of corrupting KV.
+logsumexp / argmax equals the roomy run's within 1e-5 relative (the decode
+kernels stage 16-token pages either way), every PRM score within 1e-3 (the PRM
+tile kernel stages 64-token chunks across a thought's runs, so a split thought
+moves chunk boundaries and with them the bf16 rounding of the softmax
+weights), and sampled rows match the fp32 oracle at 1e-3. A pool below the
+live peak fails with CapacityTreeKV instead of corrupting KV.
 """
 import json
 import random
@@ -33,7 +35,7 @@ def _run(cfg, seed, policy, prm, wseed, pages):
     return out
 
 
-def _same_outputs(a, b, rel=1e-5):
+def _same_outputs(a, b, rel=1e-5, rel_prm=1e-3):
     (log_a, dec_a, prm_a), (log_b, dec_b, prm_b) = a, b
     assert log_a == log_b
     da = {(q, n, p): (am, lse) for (q, n, p, am, lse, _) in dec_a}
@@ -49,7 +51,7 @@ def _same_outputs(a, b, rel=1e-5):
     pb = {(q, n): s for (q, n, s) in prm_b}
     assert pa.keys() == pb.keys()
     for k, s in pa.items():
-        assert abs(s - pb[k]) <= rel * abs(s), (k, s, pb[k])
+        assert abs(s - pb[k]) <= rel_prm * abs(s), (k, s, pb[k])
 
 
 @pytest.mark.parametrize("cfgname,policy,prm,wseed", [
