@@ -336,6 +336,7 @@ def main():
             ex.set_model("llama3_8b", "prm_1p5b", weight_seed=1)
             t = ex.run()
             m = ex.model_stats()
+            m["kv"] = ex.kv_stats()
             ex.close()
             return t, m
 
@@ -347,10 +348,46 @@ def main():
                  "prm": "prm_1p5b (28 L, d 1536, 12/2 heads x 128, FFN 8960)",
                  "queries_per_s": n_tot.queries / sec, "thoughts_per_s": n_ms["prm_thoughts"] / sec,
                  "step_ms": n_ms["step_ms"], "decode_rows": n_ms["decode_rows"], "prm_rows": n_ms["prm_rows"],
+                 "streamed": n_ms["streamed"],
+                 "tree_kv": {"pool_pages": n_ms["kv"]["pages"], "page_tokens": n_ms["kv"]["page_tokens"],
+                             "peak_live_pages": n_ms["kv"]["peak_pages"],
+                             "pages_handed_out": n_ms["kv"]["allocated_pages"],
+                             "distinct_pages_touched": n_ms["kv"]["fresh_pages"],
+                             "bytes_per_token": 4 * (32 * 8 * 128 + 28 * 2 * 128)},
                  "k1_hbm_frac": (n_ms["attn_alg_bytes"] / (n_ms["attn_ms"] / 1000.0) / 1e9) / load_peaks()[0]["hbm_gbs"],
                  "projection_tflops": (n_ms["policy_flops"] + n_ms["prm_flops"]) / sec / 1e12,
                  "projection_tensor_frac": (n_ms["policy_flops"] + n_ms["prm_flops"]) / sec / 1e12 /
                  load_peaks()[0].get("bf16_tflops_sustained", load_peaks()[0].get("bf16_tflops", 1590.0))}
+    # model mode: the PRM's scores are the rewards (awaited on device by the
+    # control kernel), so the GPU sees the reward barrier; per-query device
+    # wall-clock latency of SPEX (the config's flags) vs barrier-synchronous
+    model_mode = None
+    if world == 1:
+        def mm_search(flags):
+            ex = spex.Executor(cfg_text, seed, flags, trace=False, device=local)
+            ex.set_model(args.policy, args.prm, weight_seed=1)
+            ex.set_reward_source("prm")
+            t = ex.run()
+            m = ex.model_stats()
+            wall_ms, wait_ms = ex.query_wall_ms()
+            ex.close()
+            return t, m, wall_ms, wait_ms
+
+        model_mode = {"note": "rewards = PRM scores (K4), the control kernel waits on device for each scored "
+                              "thought; device wall clock from the run start to each query_done"}
+        for name, flags in (("spex", None), ("barrier_sync", "")):
+            mm_search(flags)  # warm-up (its own schedule shapes)
+            t_m, m_m, wall_ms, wait_ms = mm_search(flags)
+            model_mode[name] = {"queries_per_s": t_m.queries / (m_m["step_ms"] / 1000.0),
+                                "p50_query_latency_ms": statistics.median(wall_ms),
+                                "p90_query_latency_ms": sorted(wall_ms)[int(0.9 * (len(wall_ms) - 1))],
+                                "step_ms": m_m["step_ms"], "control_reward_wait_ms": wait_ms,
+                                "decode_rows": m_m["decode_rows"], "prm_thoughts": m_m["prm_thoughts"],
+                                "virtual_makespan": t_m.makespan}
+        model_mode["p50_latency_speedup"] = (model_mode["barrier_sync"]["p50_query_latency_ms"] /
+                                             model_mode["spex"]["p50_query_latency_ms"])
+        model_mode["queries_per_s_speedup"] = (model_mode["spex"]["queries_per_s"] /
+                                               model_mode["barrier_sync"]["queries_per_s"])
     # the same search barrier-synchronously (no T1/T2/T3: the reference's
     # baseline arm, experiment.cpp:68-70), same model work, for the metric's
     # "vs barrier-synchronous search"
@@ -420,6 +457,7 @@ def main():
                      "comparison with the reference arm",
         "thoughts_per_s": agg["prm_thoughts"] / dev_s,
         "named_model_shapes": named,
+        "model_mode": model_mode,
         "control_only": ctl_only,
         "gpu_launches": int(agg["launches"]),
         "roofline": {"bound": "hbm", "kernel": "K1 tree_attn_bulk_kernel (policy decode rows, bulk-copy pipeline)",
