@@ -11,7 +11,7 @@
 // Each function cites the reference code it restates.
 #pragma once
 
-#include "ctl_math_fast.h"
+#include "ctl_rng.h"
 #include "ctl_state.h"
 
 namespace spex {
@@ -397,7 +397,7 @@ SPEX_HDNI int oracle_answer_label(const QC& x, u32 id) {
 // -------------------------------------------------------------- policy.cpp
 SPEX_HD double log_int(const Run* R, int n) {
   if (n >= 1 && n < R->log_tab_n) return R->log_tab[n];
-  return log_cr(static_cast<double>(n));
+  return glibc::log(static_cast<double>(n));
 }
 
 // policy.cpp:25-30
@@ -471,7 +471,7 @@ SPEX_HDNI bool rebase_widths(Run* R, int q, const double* __restrict__ rewards, 
     if (rmax < rewards[i]) rmax = rewards[i];
   double total = 0.0;
   for (int i = 0; i < n; ++i) {
-    w[i] = exp_fast((rewards[i] - rmax) / temperature);
+    w[i] = glibc::exp((rewards[i] - rmax) / temperature);
     total += w[i];
   }
   for (int i = 0; i < n; ++i) quota[i] = budget * w[i] / total;

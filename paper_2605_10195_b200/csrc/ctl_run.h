@@ -957,7 +957,7 @@ SPEX_HDNI void scheduling_round(Run* R, EX& ex, int* warp_off) {
     hi = ex_minmax_d(ex, hi, true);
     for (int i = ex.tid; i < n; i += ex.nthr) {
       double norm = hi > lo ? (R->al_score[i] - lo) / (hi - lo) : 0.0;
-      R->al_w[i] = exp_fast(c.tau * norm);
+      R->al_w[i] = glibc::exp(c.tau * norm);
     }
     ex.sync();
     if (ex.tid == 0) {

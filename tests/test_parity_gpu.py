@@ -28,7 +28,7 @@ def _spex():
 def _check(name, ref, got):
     res = refutil.compare_logs(ref, got)
     assert res["decision_ok"], (name, res)
-    assert res["float_max_rel"] <= 1e-15, (name, res)
+    assert res["byte_equal"], (name, res)  # byte parity (SURVEY.md §8c gate 2)
     return res
 
 
