@@ -183,6 +183,29 @@ int spex_executor_query_wall_ms(spex_executor* ex, double* out, int cap, int* n,
 int spex_executor_query_finish(spex_executor* ex, double* out, int cap, int* n);
 void spex_executor_destroy(spex_executor* ex);
 
+/* ---- policy and budget hooks (csrc/spex_hooks.cu): the reference's free
+ * functions as batched device calls running the control kernel's own
+ * arithmetic. Per-problem status: 0 ok, else Errc ordinal + 1. */
+/* ucb_score (policy.hpp:43-47): n independent scores. */
+int spex_policy_ucb_score(const double* value, const int* child_visits, const int* parent_visits, int n,
+                          double exploration_c, double* out, int* status);
+/* ucb_select (policy.hpp:49-55): problem p's children are entries
+ * [offsets[p], offsets[p+1]) in NodeId order; out[p] = the chosen child's
+ * index within its problem. */
+int spex_policy_ucb_select(const double* value, const int* visits, const int* pruned, const int* offsets,
+                           const int* parent_visits, int n_problems, double exploration_c, int* out, int* status);
+/* rebase_widths (policy.hpp:63-70): problem p's rewards are entries
+ * [offsets[p], offsets[p+1]); sum_preserving = WidthMode::SumPreserving. */
+int spex_policy_rebase_widths(const double* rewards, const int* offsets, const int* budgets, int n_problems,
+                              double temperature, int sum_preserving, int* widths, int* status);
+/* roofline_k_total (budget.hpp:37-42); hw4 = {weight_bytes, mem_bandwidth,
+ * peak_compute, flops_per_token}. */
+int spex_budget_k_total(const double* hw4, int active_batch, double avg_kv_bytes, int cap, int* out);
+/* allocate_budgets (budget.hpp:47-55) over n queries (capacity, hit_ema,
+ * kv_bytes), query_score = capacity * hit_ema * (weight_bytes + kv_bytes). */
+int spex_budget_allocate(const int* capacity, const double* hit_ema, const double* kv_bytes, int n, int k_total,
+                         double tau, double weight_bytes, int* out);
+
 /* run_once: traced run returning totals and the JSON-lines log. */
 int spex_run_once(const char* config_json, uint64_t seed, const char* flags_csv,
                   spex_totals* totals, char** out_lines);

@@ -136,6 +136,22 @@ _EXPORTS = {
     "spex_executor_set_shard": ([ctypes.c_void_p, ctypes.c_int, ctypes.c_int], ctypes.c_int),
     "spex_executor_model_stats": ([ctypes.c_void_p, ctypes.POINTER(ModelStats)], ctypes.c_int),
     "spex_executor_set_kv_pages": ([ctypes.c_void_p, ctypes.c_longlong], ctypes.c_int),
+    "spex_policy_ucb_score": (
+        [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int), ctypes.c_int,
+         ctypes.c_double, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
+    "spex_policy_ucb_select": (
+        [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int),
+         ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int), ctypes.c_int, ctypes.c_double,
+         ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
+    "spex_policy_rebase_widths": (
+        [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int), ctypes.c_int,
+         ctypes.c_double, ctypes.c_int, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
+    "spex_budget_k_total": (
+        [ctypes.POINTER(ctypes.c_double), ctypes.c_int, ctypes.c_double, ctypes.c_int, ctypes.POINTER(ctypes.c_int)],
+        ctypes.c_int),
+    "spex_budget_allocate": (
+        [ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double), ctypes.c_int,
+         ctypes.c_int, ctypes.c_double, ctypes.c_double, ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
     "spex_executor_set_reward_source": ([ctypes.c_void_p, ctypes.c_int], ctypes.c_int),
     "spex_executor_query_wall_ms": (
         [ctypes.c_void_p, ctypes.POINTER(ctypes.c_double), ctypes.c_int, ctypes.POINTER(ctypes.c_int),

@@ -915,6 +915,74 @@ SPEX_HD int collect_queries(Run* R, EX& ex, Pred pred) {
 }
 
 // scheduling_round (executor.cpp:705-740) with allocate_budgets (budget.cpp:45-96)
+// allocate_budgets (budget.cpp:45-96) over arrays, block-parallel: min-max
+// normalised scores, exp(tau * norm) shares (left-fold sum), floors capped by
+// capacity, then the flooring loss round-robin over a stable descending-score
+// order to queries with spare capacity. Shared by scheduling_round and the
+// spex_budget_allocate hook (spex_hooks.cu).
+template <class EX>
+SPEX_HDNI void allocate_block(EX& ex, GState* g, int n, int k_total, double tau, const double* score, const int* cap,
+                              double* w, int* out, int* order) {
+  double lo = kInf, hi = -kInf;
+  for (int i = ex.tid; i < n; i += ex.nthr) {
+    const double s = score[i];
+    if (s < lo) lo = s;
+    if (s > hi) hi = s;
+  }
+  lo = ex_minmax_d(ex, lo, false);
+  hi = ex_minmax_d(ex, hi, true);
+  for (int i = ex.tid; i < n; i += ex.nthr) {
+    double norm = hi > lo ? (score[i] - lo) / (hi - lo) : 0.0;
+    w[i] = glibc::exp(tau * norm);
+  }
+  ex.sync();
+  if (ex.tid == 0) {
+    double total = 0.0;
+    for (int i = 0; i < n; ++i) total += w[i];
+    g->s_total = total;
+  }
+  ex.sync();
+  const double total = g->s_total;
+  i64 fsum = 0;
+  for (int i = ex.tid; i < n; i += ex.nthr) {
+    int f = static_cast<int>(floor(k_total * w[i] / total));
+    fsum += f;
+    out[i] = cap[i] < f ? cap[i] : f;
+  }
+  const i64 floor_sum = ex_sum_i64(ex, fsum);
+  const int leftover = k_total - static_cast<int>(floor_sum);
+  if (leftover > 0) {
+    // stable order by raw score, descending
+    for (int i = ex.tid; i < n; i += ex.nthr) {
+      const double si = score[i];
+      int rank = 0;
+      for (int j = 0; j < n; ++j) {
+        const double sj = score[j];
+        if (sj > si || (sj == si && j < i)) ++rank;
+      }
+      order[rank] = i;
+    }
+    ex.sync();
+    if (ex.tid == 0) {
+      int left = leftover;
+      bool progress = true;
+      while (left > 0 && progress) {
+        progress = false;
+        for (int r = 0; r < n; ++r) {
+          if (left == 0) break;
+          const int idx = order[r];
+          if (out[idx] < cap[idx]) {
+            out[idx] += 1;
+            --left;
+            progress = true;
+          }
+        }
+      }
+    }
+    ex.sync();
+  }
+}
+
 template <class EX>
 SPEX_HDNI void scheduling_round(Run* R, EX& ex, int* warp_off) {
   GState* g = R->g;
@@ -944,68 +1012,14 @@ SPEX_HDNI void scheduling_round(Run* R, EX& ex, int* warp_off) {
   if (c.t2) {
     const int idle = c.producer_slots - (g->n_act + g->n_staged);
     if (idle <= 0) return;
-    // scores (budget.cpp:41-43), min/max
-    double lo = kInf, hi = -kInf;
+    // scores (budget.cpp:41-43) and capacities of the candidates, then the split
     for (int i = ex.tid; i < n; i += ex.nthr) {
       const QueryRun* qr = &R->qs[R->it_key[i]];
-      double s = qr->capacity * qr->hit_ema * (c.weight_bytes + qr->kv_bytes);
-      R->al_score[i] = s;
-      if (s < lo) lo = s;
-      if (s > hi) hi = s;
-    }
-    lo = ex_minmax_d(ex, lo, false);
-    hi = ex_minmax_d(ex, hi, true);
-    for (int i = ex.tid; i < n; i += ex.nthr) {
-      double norm = hi > lo ? (R->al_score[i] - lo) / (hi - lo) : 0.0;
-      R->al_w[i] = glibc::exp(c.tau * norm);
+      R->al_score[i] = qr->capacity * qr->hit_ema * (c.weight_bytes + qr->kv_bytes);
+      R->al_rank[i] = qr->capacity;
     }
     ex.sync();
-    if (ex.tid == 0) {
-      double total = 0.0;
-      for (int i = 0; i < n; ++i) total += R->al_w[i];
-      g->s_total = total;
-    }
-    ex.sync();
-    const double total = g->s_total;
-    i64 fsum = 0;
-    for (int i = ex.tid; i < n; i += ex.nthr) {
-      int f = static_cast<int>(floor(idle * R->al_w[i] / total));
-      fsum += f;
-      const int cap = R->qs[R->it_key[i]].capacity;
-      R->al_out[i] = cap < f ? cap : f;
-    }
-    const i64 floor_sum = ex_sum_i64(ex, fsum);
-    const int leftover = idle - static_cast<int>(floor_sum);
-    if (leftover > 0) {
-      // stable order by raw score, descending
-      for (int i = ex.tid; i < n; i += ex.nthr) {
-        const double si = R->al_score[i];
-        int rank = 0;
-        for (int j = 0; j < n; ++j) {
-          const double sj = R->al_score[j];
-          if (sj > si || (sj == si && j < i)) ++rank;
-        }
-        R->al_order[rank] = i;
-      }
-      ex.sync();
-      if (ex.tid == 0) {
-        int left = leftover;
-        bool progress = true;
-        while (left > 0 && progress) {
-          progress = false;
-          for (int r = 0; r < n; ++r) {
-            if (left == 0) break;
-            const int idx = R->al_order[r];
-            if (R->al_out[idx] < R->qs[R->it_key[idx]].capacity) {
-              R->al_out[idx] += 1;
-              --left;
-              progress = true;
-            }
-          }
-        }
-      }
-      ex.sync();
-    }
+    allocate_block(ex, g, n, idle, c.tau, R->al_score, R->al_rank, R->al_w, R->al_out, R->al_order);
     for (int i = ex.tid; i < n; i += ex.nthr) R->qs[R->it_key[i]].grant = R->al_out[i];
     ex.sync();
   }

@@ -906,8 +906,19 @@ void kv_configure(spex_executor& ex, Cfg& c, long long pages) {
   ex.kv_pages = pages;
 }
 
+// The policy / PRM models, their tree-KV pools and row buffers are one
+// process-wide cache (model_host.cpp g_cache, with the K1 claim-order and L2
+// policy settings): model-attached runs of distinct executors take turns on
+// it. Control-only runs (no model) stay fully concurrent, as the reference's
+// independent Executors are (experiment.cpp:61-78).
+std::mutex g_model_mu;
+
 void run_executor(spex_executor& ex, int trace) {
   const HostConfig& h = ex.hc;
+#ifndef SPEX_EMU
+  std::unique_lock<std::mutex> model_lock(g_model_mu, std::defer_lock);
+  if (ex.with_model) model_lock.lock();
+#endif
 #ifndef SPEX_EMU
   if (ex.reward_prm && (!ex.with_model || !ex.mc.with_prm))
     fail(ERR_INVALID_ARGUMENT, "PRM rewards need a model with a PRM (spex_executor_set_model)");
@@ -1624,3 +1635,108 @@ int spex_run_once(const char* config_json, uint64_t seed, const char* flags_csv,
 }
 
 }  // extern "C"
+
+#ifdef SPEX_EMU
+// ---- the policy / budget hooks of spex_hooks.cu, evaluated on the host by
+// the same control functions (test-only emulation library: single thread).
+namespace {
+int emu_alloc_scratch(std::vector<int>& sm, std::vector<double>& smd, std::vector<i64>& sml, HostExec& hx) {
+  sm.assign(2048, 0);
+  smd.assign(64, 0.0);
+  sml.assign(64, 0);
+  hx.sm = sm.data();
+  hx.smd = smd.data();
+  hx.sml = sml.data();
+  return 0;
+}
+}  // namespace
+
+extern "C" int spex_policy_ucb_score(const double* value, const int* child_visits, const int* parent_visits, int n,
+                                     double exploration_c, double* out, int* status) {
+  for (int i = 0; i < n; ++i) {
+    status[i] = child_visits[i] <= 0 || parent_visits[i] <= 0 ? ERR_ZERO_VISITS : 0;
+    out[i] = status[i] ? 0.0
+                       : value[i] + exploration_c * std::sqrt(glibc::log(static_cast<double>(parent_visits[i])) /
+                                                              child_visits[i]);
+  }
+  return 0;
+}
+
+extern "C" int spex_policy_ucb_select(const double* value, const int* visits, const int* pruned, const int* offsets,
+                                      const int* parent_visits, int n_problems, double exploration_c, int* out,
+                                      int* status) {
+  for (int p = 0; p < n_problems; ++p) {
+    out[p] = -1;
+    status[p] = ERR_NO_CHILDREN;
+    double best_score = 0.0;
+    bool unvisited = false;
+    for (int i = offsets[p]; i < offsets[p + 1] && !unvisited; ++i) {
+      if (pruned[i]) continue;
+      status[p] = 0;
+      if (visits[i] == 0) {
+        out[p] = i - offsets[p];
+        unvisited = true;
+      }
+    }
+    if (unvisited || status[p]) continue;
+    for (int i = offsets[p]; i < offsets[p + 1]; ++i) {
+      if (pruned[i]) continue;
+      if (visits[i] <= 0 || parent_visits[p] <= 0) {
+        out[p] = -1;
+        status[p] = ERR_ZERO_VISITS;
+        break;
+      }
+      const double s = value[i] + exploration_c * std::sqrt(glibc::log(static_cast<double>(parent_visits[p])) /
+                                                            visits[i]);
+      if (out[p] < 0 || s > best_score) {
+        out[p] = i - offsets[p];
+        best_score = s;
+      }
+    }
+  }
+  return 0;
+}
+
+extern "C" int spex_policy_rebase_widths(const double* rewards, const int* offsets, const int* budgets, int n_problems,
+                                         double temperature, int sum_preserving, int* widths, int* status) {
+  for (int p = 0; p < n_problems; ++p) {
+    const int a = offsets[p], n = offsets[p + 1] - offsets[p];
+    GState g{};
+    Run R{};
+    R.g = &g;
+    std::vector<double> w(std::max(n, 1)), quota(std::max(n, 1));
+    std::vector<int> order(std::max(n, 1));
+    rebase_widths(&R, p, rewards + a, n, budgets[p], temperature, sum_preserving != 0, widths + a, w.data(),
+                  quota.data(), order.data());
+    status[p] = g.error;
+  }
+  return 0;
+}
+
+extern "C" int spex_budget_k_total(const double* hw4, int active_batch, double avg_kv_bytes, int cap, int* out) {
+  HostConfig h;
+  h.weight_bytes = hw4[0];
+  h.mem_bandwidth = hw4[1];
+  h.peak_compute = hw4[2];
+  h.flops_per_token = hw4[3];
+  *out = roofline_k_total(h, active_batch, avg_kv_bytes, cap);
+  return 0;
+}
+
+extern "C" int spex_budget_allocate(const int* capacity, const double* hit_ema, const double* kv_bytes, int n,
+                                    int k_total, double tau, double weight_bytes, int* out) {
+  for (int i = 0; i < n; ++i) out[i] = 0;
+  if (n <= 0 || k_total <= 0) return 0;
+  std::vector<double> score(n), w(n);
+  std::vector<int> order(n);
+  for (int i = 0; i < n; ++i) score[i] = capacity[i] * hit_ema[i] * (weight_bytes + kv_bytes[i]);
+  std::vector<int> sm;
+  std::vector<double> smd;
+  std::vector<i64> sml;
+  HostExec hx;
+  emu_alloc_scratch(sm, smd, sml, hx);
+  GState g{};
+  allocate_block(hx, &g, n, k_total, tau, score.data(), capacity, w.data(), out, order.data());
+  return 0;
+}
+#endif

@@ -7,7 +7,7 @@
 
 #if defined(__CUDACC__)
 #define SPEX_HD __host__ __device__ __forceinline__
-#define SPEX_HDNI __host__ __device__ __noinline__
+#define SPEX_HDNI __host__ __device__ __noinline__ inline
 #define SPEX_D __device__ __forceinline__
 #else
 #define SPEX_HD inline

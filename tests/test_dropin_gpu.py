@@ -24,3 +24,31 @@ def test_reference_executor_tests_pass_on_b200_path():
     print(p.stdout[-2000:], p.stderr[-4000:])
     assert p.returncode == 0, p.stderr[-4000:]
     assert "test cases: 8 | 8 passed | 0 failed" in p.stdout, p.stdout
+
+
+POLICY_BIN = ROOT / "oracle" / "_ref" / "dropin_test_policy"
+
+
+def test_reference_policy_and_budget_tests_pass_on_b200_hooks():
+    """The reference's own tests/test_policy.cpp and tests/test_budget.cpp
+    (unmodified) with ucb_score / ucb_select / rebase_widths /
+    roofline_k_total / allocate_budgets routed to the device hooks
+    (integration/policy_b200.cpp -> csrc/spex_hooks.cu): the KATs of
+    test_policy.cpp:57-280 and test_budget.cpp:106-255, brute-force UCB
+    oracles on random stars, and the policy_step shapes per family."""
+    if not POLICY_BIN.exists():
+        pytest.skip("oracle/_ref/dropin_test_policy not built (needs /root/reference at build time)")
+    p = subprocess.run([str(POLICY_BIN)], capture_output=True, text=True, timeout=600)
+    print(p.stdout[-2000:], p.stderr[-4000:])
+    assert p.returncode == 0, p.stdout[-4000:] + p.stderr[-4000:]
+    assert "| 0 failed" in p.stdout, p.stdout
+
+
+def test_hooks_match_reference_on_random_problems():
+    """Batched device hooks against the compiled reference's functions on
+    random inputs (many problems per launch): tests/hooks_check.py."""
+    from paper_2605_10195_b200 import _lib
+    from tests import hooks_check, refutil
+    if refutil.ref_lib() is None:
+        pytest.skip("oracle/_ref not built")
+    hooks_check.check_hooks(_lib.lib(), refutil.ref_lib())
