@@ -65,9 +65,9 @@ def test_baseline_configs_match_reference(cfgname):
 
 def test_config4_matches_reference_digest():
     """Config 4 (rest_hybrid, 4096 queries, t1+t2+t3): the reference log has
-    520k lines, so it is pinned by a SHA-256 of the decision-masked log and the
-    line count (tests/golden/c4_digest.json, made by make_c4_digest.py from the
-    compiled reference)."""
+    520k lines, so it is pinned by SHA-256s of the decision-masked log and of
+    the log bytes, and the line count (tests/golden/c4_digest.json, made by
+    make_c4_digest.py from the compiled reference)."""
     import hashlib
     spex = _spex()
     dg = json.loads((GOLDEN / "c4_digest.json").read_text())
@@ -75,10 +75,14 @@ def test_config4_matches_reference_digest():
     got = spex.run_once(cfg, dg["seed"], None).log
     assert len(got) == dg["lines"]
     h = hashlib.sha256()
+    hb = hashlib.sha256()
     for ln in got:
         h.update(json.dumps(refutil.strip_floats(ln), sort_keys=True).encode())
         h.update(b"\n")
+        hb.update(ln.encode())
+        hb.update(b"\n")
     assert h.hexdigest() == dg["masked_sha256"]
+    assert hb.hexdigest() == dg["byte_sha256"]  # byte parity (gate 2)
 
 
 def test_config3_literal_matches_reference_digest():
@@ -87,8 +91,8 @@ def test_config3_literal_matches_reference_digest():
     simulate_next path (speculation.cpp:124-218, executor.cpp:674-703) that
     takes ~25 min on one CPU core. Pinned by the SHA-256 of the decision-masked
     reference log, its line count and run_end totals
-    (tests/golden/c3_rstar_w4_q512_t1t3_digest.json, make_digest.py); the full
-    byte digest is checked too and reported (gate 2)."""
+    (tests/golden/c3_rstar_w4_q512_t1t3_digest.json, make_digest.py), and the
+    full byte digest (gate 2)."""
     import hashlib
     import time
     spex = _spex()
@@ -114,6 +118,7 @@ def test_config3_literal_matches_reference_digest():
     for k in ("makespan", "generated", "committed", "reused", "wasted", "queries"):
         assert end[k] == dg["run_end"][k], k
     assert tot.queries == 512
+    assert hb.hexdigest() == dg["byte_sha256"]
     print(json.dumps({"c3_literal_device_control_ms": dev_ms, "wall_s": round(wall, 3),
                       "reference_cpu_s": dg["reference_cpu_s"], "byte_equal": hb.hexdigest() == dg["byte_sha256"]}))
 
