@@ -1077,7 +1077,7 @@ __global__ void __launch_bounds__(128) tree_attn_tile_mma_kernel(const __grid_co
 // group at the cost of one row-vector of MMA work. The pools are zero-filled at
 // allocation, so rows of a box past a segment's end are finite (masked to p = 0).
 constexpr int kMmaNST = 2;     // stages per warp
-constexpr int kMmaWarps = 12;  // warps per block (12 x (2 x 8 KB + G x 512 B) <= 216 KB for G <= 4; 168 registers)
+constexpr int kMmaWarps = 11;  // warps per block (11 x (2 x 8 KB + 2 x G x 512 B) <= 220 KB for G <= 4)
 
 // byte offset of (row, 16-byte chunk c in [0,16)) in a swizzled [2 halves][16 rows][128 B] box pair
 __device__ __forceinline__ uint32_t swz16(int row, int c) {
@@ -1108,7 +1108,9 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
   __shared__ int4 meta[kWarps][kNST];  // n tokens (-1: no more work), flags (1 first, 2 last), row, kv head
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   unsigned char* ring = sm + (size_t)warp * kNST * 2 * STAGE;  // [stage][K|V][STAGE]
-  float* qbuf = reinterpret_cast<float*>(sm + (size_t)kWarps * kNST * 2 * STAGE) + (size_t)warp * G * DH;
+  // two fp32 query buffers per warp (items alternate): the producer may issue
+  // the next item's first stage while this item's queries are not yet read
+  float* qbuf = reinterpret_cast<float*>(sm + (size_t)kWarps * kNST * 2 * STAGE) + (size_t)warp * 2 * G * DH;
   if (lane == 0) {
     for (int i = 0; i < kNST; ++i) mbar_init(&bar[warp][i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -1121,6 +1123,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
   long long n_base = 0;
   int n_len = 0;
   bool c_first = true, have_cur = false, p_done = false;
+  int c_qb = 1;  // query buffer of the current item
   // prefetched next item: step 0 claimed, 1 row known, 2 segment list known, 3 first segment known
   int f_it = -1, f_step = -1, f_r = 0, f_segoff = 0, f_nseg = 0, f_len = 0;
   long long f_base = 0;
@@ -1161,6 +1164,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
     c_len = f_len;
     c_row0 = (long long)c_kh * slots;
     c_first = true;
+    c_qb ^= 1;
     if (c_nseg > 1) {
       n_base = segs[c_segoff + 1].base;
       n_len = segs[c_segoff + 1].len;
@@ -1184,12 +1188,13 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
     const int n = min(CH, c_len - c_off);
     const bool last_in_seg = c_off + CH >= c_len;
     const bool last = last_in_seg && c_seg + 1 >= c_nseg;
-    meta[warp][st] = make_int4(n, (c_first ? 1 : 0) | (last ? 2 : 0), c_r, c_kh);
+    meta[warp][st] = make_int4(n, (c_first ? 1 : 0) | (last ? 2 : 0) | (c_qb << 2), c_r, c_kh);
     unsigned char* kb = ring + st * 2 * STAGE;
     const int rowc = (int)(c_row0 + c_base + c_off);
     const uint32_t qbytes = c_first ? (uint32_t)G * DH * 4 : 0u;
     mbar_expect_tx(&bar[warp][st], 2 * STAGE + qbytes);
-    if (c_first) bulk_g2s(qbuf, Qr + ((long long)c_r * H + (long long)c_kh * G) * DH, qbytes, &bar[warp][st]);
+    if (c_first)
+      bulk_g2s(qbuf + c_qb * G * DH, Qr + ((long long)c_r * H + (long long)c_kh * G) * DH, qbytes, &bar[warp][st]);
     tma_load_2d(kb, &kmap16, 0, rowc, &bar[warp][st]);
     tma_load_2d(kb + 2048, &kmap16, 64, rowc, &bar[warp][st]);
     tma_load_2d(kb + STAGE, &vmap16, 0, rowc, &bar[warp][st]);
@@ -1224,6 +1229,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
     __syncwarp();  // lane 0's metadata writes are visible to the warp
     const int4 md = meta[warp][st];
     if (md.x < 0) break;
+    if (lane == 0) produce();  // the next stage is in flight while this one lands
     mbar_wait(&bar[warp][st], (uint32_t)((consumed / kNST) & 1));
     const int n = md.x;
     if (md.y & 1) {
@@ -1231,8 +1237,9 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
       r = md.z;
       kh = md.w;
       const bool v0 = gq < G, v1 = gq + 8 < G;
-      const float* q0 = qbuf + (v0 ? gq : 0) * DH;
-      const float* q1 = qbuf + (v1 ? gq + 8 : 0) * DH;
+      const float* qb = qbuf + ((md.y >> 2) & 1) * G * DH;
+      const float* q0 = qb + (v0 ? gq : 0) * DH;
+      const float* q1 = qb + (v1 ? gq + 8 : 0) * DH;
       constexpr float sc = 1.4426950408889634f;
 #pragma unroll
       for (int ks = 0; ks < 8; ++ks) {
@@ -1251,8 +1258,6 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
       m0 = m1 = -INFINITY;
       l0 = l1 = 0.f;
     }
-    __syncwarp();  // the query buffer is read before lane 0 issues the next item's copy
-    if (lane == 0) produce();
     const uint32_t kb = (uint32_t)__cvta_generic_to_shared(ring + st * 2 * STAGE);
     const uint32_t vb = kb + STAGE;
     float sacc[2][4];
@@ -1754,8 +1759,8 @@ template <int NST, int W>
 static int launch_wmma(const CUtensorMap* kmap16, const CUtensorMap* vmap16, const RowDesc* rows, const Segment* segs,
                        const float* Qr, int H, int KVH, int G, long long slots, __nv_bfloat16* O, int M,
                        int* item_ctr, cudaStream_t s) {
-  // ring + one fp32 query buffer (G heads) per warp
-  const size_t smem = (size_t)W * NST * 2 * 16 * 128 * 2 + (size_t)W * G * 128 * 4 + 1024;
+  // ring + two fp32 query buffers (G heads) per warp
+  const size_t smem = (size_t)W * NST * 2 * 16 * 128 * 2 + (size_t)W * 2 * G * 128 * 4 + 1024;
   if (smem > 227 * 1024 || (long long)KVH * slots >= (1LL << 31)) return -1;
   static int blocks = 0;
   static size_t attr_smem = 0;
@@ -1785,7 +1790,7 @@ extern "C" int spex_k_tree_attn_wmma(const CUtensorMap* kmap16, const CUtensorMa
   if (dh != 128 || G < 1 || G > 16) return -1;
   // 2 stages x 12 warps (8 KB per stage): the best of a stages x warps sweep on c5
   if (G <= 4) return launch_wmma<kMmaNST, kMmaWarps>(kmap16, vmap16, rows, segs, Qr, H, KVH, G, slots, O, M, item_ctr, s);
-  if (G <= 8) return launch_wmma<kMmaNST, 10>(kmap16, vmap16, rows, segs, Qr, H, KVH, G, slots, O, M, item_ctr, s);
+  if (G <= 8) return launch_wmma<kMmaNST, 9>(kmap16, vmap16, rows, segs, Qr, H, KVH, G, slots, O, M, item_ctr, s);
   return -1;  // the query buffers of larger groups do not fit beside the rings
 }
 
@@ -1917,7 +1922,7 @@ extern "C" void spex_k_preload() {
   preload_one(tree_attn_decode_kernel<64, 4, 4>);
   preload_one(tree_attn_bulk_kernel<16, 2, 14>);
   preload_one(tree_attn_wmma_kernel<kMmaNST, kMmaWarps>);
-  preload_one(tree_attn_wmma_kernel<kMmaNST, 10>);
+  preload_one(tree_attn_wmma_kernel<kMmaNST, 9>);
   preload_one(tree_attn_tile_mma_kernel<1>);
   preload_one(tree_attn_tile_mma_kernel<2>);
   preload_one(tree_attn_tile_mma_kernel<4>);
