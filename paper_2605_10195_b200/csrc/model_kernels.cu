@@ -1097,10 +1097,10 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
   // item's fp32 query rows by a bulk copy on its first stage) with the stage's
   // metadata (tokens, first/last flags, row, KV head) in shared memory, so the
   // consumer lanes never touch global memory but for O. The producer hides its
-  // own dependent loads: the next item is claimed as soon as the current one
-  // starts and its row index, segment list and first segment are fetched one
-  // step per stage (atomic -> row_order -> RowDesc -> Segment), and each
-  // segment's successor is loaded when the segment starts.
+  // own dependent loads: the next item is claimed a few stages before the
+  // current one ends and its row index, segment list and first segment are
+  // fetched one step per stage (atomic -> row_order -> RowDesc -> Segment),
+  // and each segment's successor is loaded when the segment starts.
   constexpr int DH = 128, CH = 16, STAGE = CH * DH * 2;  // 4 KB of K (and of V) per stage
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -1128,12 +1128,14 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
   int f_it = -1, f_step = -1, f_r = 0, f_segoff = 0, f_nseg = 0, f_len = 0;
   long long f_base = 0;
   int issued = 0;
+  bool claimed = false;  // the item after the current one is claimed
   auto pref_claim = [&]() {
     f_it = atomicAdd(item_ctr, 1);
     f_step = 0;
+    claimed = true;
   };
   auto pref_advance = [&]() {
-    if (f_it < 0 || f_it >= n_items) return;
+    if (!claimed || f_it >= n_items) return;
     if (f_step == 0) {
       f_r = row_order ? row_order[f_it / KVH] : f_it / KVH;
       f_step = 1;
@@ -1152,7 +1154,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
   };
   // adopt the prefetched item as current (completing its fetch if needed)
   auto adopt = [&]() -> bool {
-    if (f_it < 0 || f_it >= n_items) return false;
+    if (!claimed) pref_claim();
+    if (f_it >= n_items) return false;
     while (f_step < 3) pref_advance();
     c_r = f_r;
     c_kh = f_it % KVH;
@@ -1169,11 +1172,15 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
       n_base = segs[c_segoff + 1].base;
       n_len = segs[c_segoff + 1].len;
     }
-    pref_claim();
+    claimed = false;
     return true;
   };
   auto produce = [&]() {
     if (p_done) return;
+    // claim the next item late (from the current item's second-to-last
+    // segment, ~8 stages ahead): an early claim would strand items on busy
+    // warps at the end of the launch
+    if (have_cur && !claimed && c_seg + 2 >= c_nseg) pref_claim();
     pref_advance();
     while (!have_cur || c_seg >= c_nseg) {
       if (!adopt()) {
@@ -1215,10 +1222,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
       }
     }
   };
-  if (lane == 0) {
-    pref_claim();
+  if (lane == 0)
     for (int i = 0; i < kNST - 1; ++i) produce();
-  }
   const int gq = lane >> 2, tq = lane & 3, mi = lane >> 3, ri = lane & 7;
   int consumed = 0, r = 0, kh = 0;
   uint32_t qa[8][4];
