@@ -1077,7 +1077,7 @@ __global__ void __launch_bounds__(128) tree_attn_tile_mma_kernel(const __grid_co
 // group at the cost of one row-vector of MMA work. The pools are zero-filled at
 // allocation, so rows of a box past a segment's end are finite (masked to p = 0).
 constexpr int kMmaNST = 2;     // stages per warp
-constexpr int kMmaWarps = 11;  // warps per block (11 x (2 x 8 KB + 2 x G x 512 B) <= 220 KB for G <= 4)
+constexpr int kMmaWarps = 12;  // warps per block (12 x 2 x 8 KB = 192 KB; 170 registers)
 
 // byte offset of (row, 16-byte chunk c in [0,16)) in a swizzled [2 halves][16 rows][128 B] box pair
 __device__ __forceinline__ uint32_t swz16(int row, int c) {
@@ -1085,166 +1085,86 @@ __device__ __forceinline__ uint32_t swz16(int row, int c) {
   return (uint32_t)(half * 2048 + row * 128 + ((cc ^ (row & 7)) << 4));
 }
 
-template <int kNST, int kWarps>  // stages per warp, warps per block
+template <int kNST, int kWarps, bool kSkipRescale>  // stages per warp, warps per block
 __global__ void __launch_bounds__(kWarps * 32, 1)
     tree_attn_wmma_kernel(const __grid_constant__ CUtensorMap kmap16, const __grid_constant__ CUtensorMap vmap16,
                           const RowDesc* __restrict__ rows, const Segment* __restrict__ segs,
                           const float* __restrict__ Qr, int H, int KVH, int G, int n_items, long long slots,
                           __nv_bfloat16* __restrict__ O, int* __restrict__ item_ctr,
                           const int* __restrict__ row_order) {
-  // Lane 0 of each warp is the warp's producer: it walks the claimed items'
-  // segments and issues each 16-token stage (K and V rows by 2D TMA, plus the
-  // item's fp32 query rows by a bulk copy on its first stage) with the stage's
-  // metadata (tokens, first/last flags, row, KV head) in shared memory, so the
-  // consumer lanes never touch global memory but for O. The producer hides its
-  // own dependent loads: the next item is claimed a few stages before the
-  // current one ends and its row index, segment list and first segment are
-  // fetched one step per stage (atomic -> row_order -> RowDesc -> Segment),
-  // and each segment's successor is loaded when the segment starts.
   constexpr int DH = 128, CH = 16, STAGE = CH * DH * 2;  // 4 KB of K (and of V) per stage
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ uint64_t bar[kWarps][kNST];
-  __shared__ int4 meta[kWarps][kNST];  // n tokens (-1: no more work), flags (1 first, 2 last), row, kv head
+  __shared__ int queue[kWarps][8];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   unsigned char* ring = sm + (size_t)warp * kNST * 2 * STAGE;  // [stage][K|V][STAGE]
-  // two fp32 query buffers per warp (items alternate): the producer may issue
-  // the next item's first stage while this item's queries are not yet read
-  float* qbuf = reinterpret_cast<float*>(sm + (size_t)kWarps * kNST * 2 * STAGE) + (size_t)warp * 2 * G * DH;
   if (lane == 0) {
     for (int i = 0; i < kNST; ++i) mbar_init(&bar[warp][i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncwarp();
-  // ---- producer state (lane 0 only)
-  // current item: row, kv head, segment cursor; next segment prefetched
-  int c_r = 0, c_kh = 0, c_nseg = 0, c_seg = 0, c_off = 0, c_len = 0, c_segoff = 0;
-  long long c_base = 0, c_row0 = 0;
-  long long n_base = 0;
-  int n_len = 0;
-  bool c_first = true, have_cur = false, p_done = false;
-  int c_qb = 1;  // query buffer of the current item
-  // prefetched next item: step 0 claimed, 1 row known, 2 segment list known, 3 first segment known
-  int f_it = -1, f_step = -1, f_r = 0, f_segoff = 0, f_nseg = 0, f_len = 0;
-  long long f_base = 0;
-  int issued = 0;
-  bool claimed = false;  // the item after the current one is claimed
-  auto pref_claim = [&]() {
-    f_it = atomicAdd(item_ctr, 1);
-    f_step = 0;
-    claimed = true;
-  };
-  auto pref_advance = [&]() {
-    if (!claimed || f_it >= n_items) return;
-    if (f_step == 0) {
-      f_r = row_order ? row_order[f_it / KVH] : f_it / KVH;
-      f_step = 1;
-    } else if (f_step == 1) {
-      const int2 so = *reinterpret_cast<const int2*>(&rows[f_r].seg_off);
-      f_segoff = so.x;
-      f_nseg = so.y;
-      f_step = 2;
-    } else if (f_step == 2) {
-      if (f_nseg > 0) {
-        f_base = segs[f_segoff].base;
-        f_len = segs[f_segoff].len;
-      }
-      f_step = 3;
-    }
-  };
-  // adopt the prefetched item as current (completing its fetch if needed)
-  auto adopt = [&]() -> bool {
-    if (!claimed) pref_claim();
-    if (f_it >= n_items) return false;
-    while (f_step < 3) pref_advance();
-    c_r = f_r;
-    c_kh = f_it % KVH;
-    c_nseg = f_nseg;
-    c_segoff = f_segoff;
-    c_seg = 0;
-    c_off = 0;
-    c_base = f_base;
-    c_len = f_len;
-    c_row0 = (long long)c_kh * slots;
-    c_first = true;
-    c_qb ^= 1;
-    if (c_nseg > 1) {
-      n_base = segs[c_segoff + 1].base;
-      n_len = segs[c_segoff + 1].len;
-    }
-    claimed = false;
-    return true;
-  };
+  // ---- producer cursor (lane 0 only)
+  int p_q = 0, p_item = -1, p_seg = 0, p_off = 0, p_nseg = 0, issued = 0;
+  long long p_row0 = 0;
+  const Segment* p_sg = nullptr;
+  bool p_done = false;
   auto produce = [&]() {
-    if (p_done) return;
-    // claim the next item late (from the current item's second-to-last
-    // segment, ~8 stages ahead): an early claim would strand items on busy
-    // warps at the end of the launch
-    if (have_cur && !claimed && c_seg + 2 >= c_nseg) pref_claim();
-    pref_advance();
-    while (!have_cur || c_seg >= c_nseg) {
-      if (!adopt()) {
-        const int st = issued % kNST;
-        meta[warp][st] = make_int4(-1, 0, 0, 0);
-        p_done = true;
-        return;
-      }
-      have_cur = c_nseg > 0;
-    }
-    const int st = issued % kNST;
-    const int n = min(CH, c_len - c_off);
-    const bool last_in_seg = c_off + CH >= c_len;
-    const bool last = last_in_seg && c_seg + 1 >= c_nseg;
-    meta[warp][st] = make_int4(n, (c_first ? 1 : 0) | (last ? 2 : 0) | (c_qb << 2), c_r, c_kh);
-    unsigned char* kb = ring + st * 2 * STAGE;
-    const int rowc = (int)(c_row0 + c_base + c_off);
-    const uint32_t qbytes = c_first ? (uint32_t)G * DH * 4 : 0u;
-    mbar_expect_tx(&bar[warp][st], 2 * STAGE + qbytes);
-    if (c_first)
-      bulk_g2s(qbuf + c_qb * G * DH, Qr + ((long long)c_r * H + (long long)c_kh * G) * DH, qbytes, &bar[warp][st]);
-    tma_load_2d(kb, &kmap16, 0, rowc, &bar[warp][st]);
-    tma_load_2d(kb + 2048, &kmap16, 64, rowc, &bar[warp][st]);
-    tma_load_2d(kb + STAGE, &vmap16, 0, rowc, &bar[warp][st]);
-    tma_load_2d(kb + STAGE + 2048, &vmap16, 64, rowc, &bar[warp][st]);
-    c_first = false;
-    ++issued;
-    c_off += CH;
-    if (last_in_seg) {
-      ++c_seg;
-      c_off = 0;
-      if (c_seg < c_nseg) {
-        c_base = n_base;
-        c_len = n_len;
-        if (c_seg + 1 < c_nseg) {
-          n_base = segs[c_segoff + c_seg + 1].base;
-          n_len = segs[c_segoff + c_seg + 1].len;
+    while (!p_done) {
+      if (p_item < 0 || p_seg >= p_nseg) {
+        const int it = atomicAdd(item_ctr, 1);
+        if (it >= n_items) {
+          queue[warp][p_q & 7] = -1;
+          p_done = true;
+          return;
         }
+        queue[warp][p_q & 7] = it;
+        ++p_q;
+        p_item = it;
+        const RowDesc rd = rows[row_order ? row_order[it / KVH] : it / KVH];
+        p_sg = segs + rd.seg_off;
+        p_nseg = rd.nseg;
+        p_seg = 0;
+        p_off = 0;
+        p_row0 = (long long)(it % KVH) * slots;
       }
+      const int len = p_sg[p_seg].len;
+      if (p_off >= len) {
+        ++p_seg;
+        p_off = 0;
+        continue;
+      }
+      const int rowc = (int)(p_row0 + p_sg[p_seg].base + p_off);
+      const int st = issued % kNST;
+      unsigned char* kb = ring + st * 2 * STAGE;
+      mbar_expect_tx(&bar[warp][st], 2 * STAGE);
+      tma_load_2d(kb, &kmap16, 0, rowc, &bar[warp][st]);
+      tma_load_2d(kb + 2048, &kmap16, 64, rowc, &bar[warp][st]);
+      tma_load_2d(kb + STAGE, &vmap16, 0, rowc, &bar[warp][st]);
+      tma_load_2d(kb + STAGE + 2048, &vmap16, 64, rowc, &bar[warp][st]);
+      p_off += CH;
+      ++issued;
+      return;
     }
   };
   if (lane == 0)
     for (int i = 0; i < kNST - 1; ++i) produce();
+  __syncwarp();
   const int gq = lane >> 2, tq = lane & 3, mi = lane >> 3, ri = lane & 7;
-  int consumed = 0, r = 0, kh = 0;
-  uint32_t qa[8][4];
-  float oacc[16][4];
-  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+  int c_q = 0, consumed = 0;
   for (;;) {
-    const int st = consumed % kNST;
-    __syncwarp();  // lane 0's metadata writes are visible to the warp
-    const int4 md = meta[warp][st];
-    if (md.x < 0) break;
-    if (lane == 0) produce();  // the next stage is in flight while this one lands
-    mbar_wait(&bar[warp][st], (uint32_t)((consumed / kNST) & 1));
-    const int n = md.x;
-    if (md.y & 1) {
-      // first stage of an item: its query rows arrived with this stage
-      r = md.z;
-      kh = md.w;
+    const int it = queue[warp][c_q & 7];
+    if (it < 0) break;
+    ++c_q;
+    const int r = row_order ? row_order[it / KVH] : it / KVH, kh = it % KVH;
+    const RowDesc rd = rows[r];
+    const Segment* sg = segs + rd.seg_off;
+    // Q fragments: rows = the group's heads (gq, gq + 8 < G), dims as k
+    uint32_t qa[8][4];
+    {
       const bool v0 = gq < G, v1 = gq + 8 < G;
-      const float* qb = qbuf + ((md.y >> 2) & 1) * G * DH;
-      const float* q0 = qb + (v0 ? gq : 0) * DH;
-      const float* q1 = qb + (v1 ? gq + 8 : 0) * DH;
+      const float* q0 = Qr + ((long long)r * H + kh * G + (v0 ? gq : 0)) * DH;
+      const float* q1 = Qr + ((long long)r * H + kh * G + (v1 ? gq + 8 : 0)) * DH;
       constexpr float sc = 1.4426950408889634f;
 #pragma unroll
       for (int ks = 0; ks < 8; ++ks) {
@@ -1258,98 +1178,106 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
         qa[ks][2] = pack_bf16(x01.x * sc, x01.y * sc);
         qa[ks][3] = pack_bf16(x11.x * sc, x11.y * sc);
       }
-#pragma unroll
-      for (int nn = 0; nn < 16; ++nn) oacc[nn][0] = oacc[nn][1] = oacc[nn][2] = oacc[nn][3] = 0.f;
-      m0 = m1 = -INFINITY;
-      l0 = l1 = 0.f;
     }
-    const uint32_t kb = (uint32_t)__cvta_generic_to_shared(ring + st * 2 * STAGE);
-    const uint32_t vb = kb + STAGE;
-    float sacc[2][4];
+    float oacc[16][4];
 #pragma unroll
-    for (int t = 0; t < 2; ++t) sacc[t][0] = sacc[t][1] = sacc[t][2] = sacc[t][3] = 0.f;
+    for (int n = 0; n < 16; ++n) oacc[n][0] = oacc[n][1] = oacc[n][2] = oacc[n][3] = 0.f;
+    float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+    for (int si = 0; si < rd.nseg; ++si) {
+      const int len = sg[si].len;
+      for (int off = 0; off < len; off += CH) {
+        const int n = min(CH, len - off);
+        if (lane == 0) produce();
+        const int st = consumed % kNST;
+        mbar_wait(&bar[warp][st], (uint32_t)((consumed / kNST) & 1));
+        const uint32_t kb = (uint32_t)__cvta_generic_to_shared(ring + st * 2 * STAGE);
+        const uint32_t vb = kb + STAGE;
+        float sacc[2][4];
 #pragma unroll
-    for (int ks = 0; ks < 8; ++ks) {
-      uint32_t b0, b1, b2, b3;
-      ldsm_x4(kb + swz16((mi >> 1) * 8 + ri, ks * 2 + (mi & 1)), b0, b1, b2, b3);
-      mma_bf16(sacc[0], qa[ks][0], qa[ks][1], qa[ks][2], qa[ks][3], b0, b1);
-      mma_bf16(sacc[1], qa[ks][0], qa[ks][1], qa[ks][2], qa[ks][3], b2, b3);
-    }
-    float mx0 = -INFINITY, mx1 = -INFINITY;
+        for (int t = 0; t < 2; ++t) sacc[t][0] = sacc[t][1] = sacc[t][2] = sacc[t][3] = 0.f;
 #pragma unroll
-    for (int t = 0; t < 2; ++t)
+        for (int ks = 0; ks < 8; ++ks) {
+          uint32_t b0, b1, b2, b3;
+          ldsm_x4(kb + swz16((mi >> 1) * 8 + ri, ks * 2 + (mi & 1)), b0, b1, b2, b3);
+          mma_bf16(sacc[0], qa[ks][0], qa[ks][1], qa[ks][2], qa[ks][3], b0, b1);
+          mma_bf16(sacc[1], qa[ks][0], qa[ks][1], qa[ks][2], qa[ks][3], b2, b3);
+        }
+        float mx0 = -INFINITY, mx1 = -INFINITY;
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const bool ok = t * 8 + tq * 2 + e < n;
-        sacc[t][e] = ok ? sacc[t][e] : -INFINITY;
-        sacc[t][2 + e] = ok ? sacc[t][2 + e] : -INFINITY;
-        mx0 = fmaxf(mx0, sacc[t][e]);
-        mx1 = fmaxf(mx1, sacc[t][2 + e]);
+        for (int t = 0; t < 2; ++t)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const bool ok = t * 8 + tq * 2 + e < n;
+            sacc[t][e] = ok ? sacc[t][e] : -INFINITY;
+            sacc[t][2 + e] = ok ? sacc[t][2 + e] : -INFINITY;
+            mx0 = fmaxf(mx0, sacc[t][e]);
+            mx1 = fmaxf(mx1, sacc[t][2 + e]);
+          }
+#pragma unroll
+        for (int o = 1; o < 4; o <<= 1) {
+          mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, o));
+          mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, o));
+        }
+        const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
+        const float a0 = mn0 == -INFINITY ? 1.f : exp2f(m0 - mn0);
+        const float a1 = mn1 == -INFINITY ? 1.f : exp2f(m1 - mn1);
+        uint32_t pa[4];
+        float ps0 = 0.f, ps1 = 0.f;
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+          const float p00 = mn0 == -INFINITY ? 0.f : exp2f(sacc[t][0] - mn0);
+          const float p01 = mn0 == -INFINITY ? 0.f : exp2f(sacc[t][1] - mn0);
+          const float p10 = mn1 == -INFINITY ? 0.f : exp2f(sacc[t][2] - mn1);
+          const float p11 = mn1 == -INFINITY ? 0.f : exp2f(sacc[t][3] - mn1);
+          ps0 += p00 + p01;
+          ps1 += p10 + p11;
+          pa[2 * t] = pack_bf16(p00, p01);
+          pa[2 * t + 1] = pack_bf16(p10, p11);
+        }
+        l0 = l0 * a0 + ps0;
+        l1 = l1 * a1 + ps1;
+        // a == 1 exactly when a row's running max did not move: the rescale can be skipped
+        if (!kSkipRescale || !__all_sync(0xffffffffu, mn0 == m0 && mn1 == m1)) {
+#pragma unroll
+          for (int nn = 0; nn < 16; ++nn) {
+            oacc[nn][0] *= a0;
+            oacc[nn][1] *= a0;
+            oacc[nn][2] *= a1;
+            oacc[nn][3] *= a1;
+          }
+        }
+        m0 = mn0;
+        m1 = mn1;
+#pragma unroll
+        for (int n2 = 0; n2 < 8; ++n2) {
+          uint32_t b0, b1, b2, b3;
+          ldsm_x4_t(vb + swz16((mi & 1) * 8 + ri, n2 * 2 + (mi >> 1)), b0, b1, b2, b3);
+          mma_bf16(oacc[2 * n2], pa[0], pa[1], pa[2], pa[3], b0, b1);
+          mma_bf16(oacc[2 * n2 + 1], pa[0], pa[1], pa[2], pa[3], b2, b3);
+        }
+        ++consumed;
+        __syncwarp();  // stage fully read before lane 0 refills it
       }
+    }
 #pragma unroll
     for (int o = 1; o < 4; o <<= 1) {
-      mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, o));
-      mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, o));
+      l0 += __shfl_xor_sync(0xffffffffu, l0, o);
+      l1 += __shfl_xor_sync(0xffffffffu, l1, o);
     }
-    const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
-    const float a0 = mn0 == -INFINITY ? 1.f : exp2f(m0 - mn0);
-    const float a1 = mn1 == -INFINITY ? 1.f : exp2f(m1 - mn1);
-    uint32_t pa[4];
-    float ps0 = 0.f, ps1 = 0.f;
+    if (gq < G) {
+      __nv_bfloat16* o0 = O + ((long long)r * H + kh * G + gq) * DH + tq * 2;
+      const float inv = 1.f / l0;
 #pragma unroll
-    for (int t = 0; t < 2; ++t) {
-      const float p00 = mn0 == -INFINITY ? 0.f : exp2f(sacc[t][0] - mn0);
-      const float p01 = mn0 == -INFINITY ? 0.f : exp2f(sacc[t][1] - mn0);
-      const float p10 = mn1 == -INFINITY ? 0.f : exp2f(sacc[t][2] - mn1);
-      const float p11 = mn1 == -INFINITY ? 0.f : exp2f(sacc[t][3] - mn1);
-      ps0 += p00 + p01;
-      ps1 += p10 + p11;
-      pa[2 * t] = pack_bf16(p00, p01);
-      pa[2 * t + 1] = pack_bf16(p10, p11);
+      for (int nn = 0; nn < 16; ++nn)
+        *reinterpret_cast<uint32_t*>(o0 + nn * 8) = pack_bf16(oacc[nn][0] * inv, oacc[nn][1] * inv);
     }
-    l0 = l0 * a0 + ps0;
-    l1 = l1 * a1 + ps1;
+    if (gq + 8 < G) {
+      __nv_bfloat16* o1 = O + ((long long)r * H + kh * G + gq + 8) * DH + tq * 2;
+      const float inv = 1.f / l1;
 #pragma unroll
-    for (int nn = 0; nn < 16; ++nn) {
-      oacc[nn][0] *= a0;
-      oacc[nn][1] *= a0;
-      oacc[nn][2] *= a1;
-      oacc[nn][3] *= a1;
+      for (int nn = 0; nn < 16; ++nn)
+        *reinterpret_cast<uint32_t*>(o1 + nn * 8) = pack_bf16(oacc[nn][2] * inv, oacc[nn][3] * inv);
     }
-    m0 = mn0;
-    m1 = mn1;
-#pragma unroll
-    for (int n2 = 0; n2 < 8; ++n2) {
-      uint32_t b0, b1, b2, b3;
-      ldsm_x4_t(vb + swz16((mi & 1) * 8 + ri, n2 * 2 + (mi >> 1)), b0, b1, b2, b3);
-      mma_bf16(oacc[2 * n2], pa[0], pa[1], pa[2], pa[3], b0, b1);
-      mma_bf16(oacc[2 * n2 + 1], pa[0], pa[1], pa[2], pa[3], b2, b3);
-    }
-    ++consumed;
-    if (md.y & 2) {
-      // last stage of the item: normalise and write the group's O rows
-      float s0 = l0, s1 = l1;
-#pragma unroll
-      for (int o = 1; o < 4; o <<= 1) {
-        s0 += __shfl_xor_sync(0xffffffffu, s0, o);
-        s1 += __shfl_xor_sync(0xffffffffu, s1, o);
-      }
-      if (gq < G) {
-        __nv_bfloat16* o0 = O + ((long long)r * H + kh * G + gq) * DH + tq * 2;
-        const float inv = 1.f / s0;
-#pragma unroll
-        for (int nn = 0; nn < 16; ++nn)
-          *reinterpret_cast<uint32_t*>(o0 + nn * 8) = pack_bf16(oacc[nn][0] * inv, oacc[nn][1] * inv);
-      }
-      if (gq + 8 < G) {
-        __nv_bfloat16* o1 = O + ((long long)r * H + kh * G + gq + 8) * DH + tq * 2;
-        const float inv = 1.f / s1;
-#pragma unroll
-        for (int nn = 0; nn < 16; ++nn)
-          *reinterpret_cast<uint32_t*>(o1 + nn * 8) = pack_bf16(oacc[nn][2] * inv, oacc[nn][3] * inv);
-      }
-    }
-    __syncwarp();  // stage fully read before lane 0 refills it
   }
 }
 
@@ -1760,20 +1688,14 @@ extern "C" int spex_k_tree_attn_bulk(const RowDesc* rows, const Segment* segs, c
 // K1 decode rows on the per-warp TMA + mma.sync pipeline (G <= 16, dh = 128);
 // kmap16/vmap16 are the pools' 2D maps with 64 x 16 boxes (spex_tmap_kv16).
 
-template <int NST, int W>
+template <int NST, int W, bool SKIP = false>
 static int launch_wmma(const CUtensorMap* kmap16, const CUtensorMap* vmap16, const RowDesc* rows, const Segment* segs,
                        const float* Qr, int H, int KVH, int G, long long slots, __nv_bfloat16* O, int M,
                        int* item_ctr, cudaStream_t s) {
-  // ring + two fp32 query buffers (G heads) per warp
-  const size_t smem = (size_t)W * NST * 2 * 16 * 128 * 2 + (size_t)W * 2 * G * 128 * 4 + 1024;
-  if (smem > 227 * 1024 || (long long)KVH * slots >= (1LL << 31)) return -1;
+  const size_t smem = (size_t)W * NST * 2 * 16 * 128 * 2 + 1024;
   static int blocks = 0;
-  static size_t attr_smem = 0;
-  if (attr_smem < smem) {
-    cudaFuncSetAttribute(tree_attn_wmma_kernel<NST, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr_smem = smem;
-  }
   if (!blocks) {
+    cudaFuncSetAttribute(tree_attn_wmma_kernel<NST, W, SKIP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -1782,8 +1704,8 @@ static int launch_wmma(const CUtensorMap* kmap16, const CUtensorMap* vmap16, con
   const int n_items = M * KVH;
   const int grid = std::min(blocks, (n_items + W - 1) / W);
   cudaMemsetAsync(item_ctr, 0, sizeof(int), s);
-  tree_attn_wmma_kernel<NST, W><<<grid, W * 32, smem, s>>>(*kmap16, *vmap16, rows, segs, Qr, H, KVH, G, n_items, slots,
-                                                           O, item_ctr, g_k1_row_order);
+  tree_attn_wmma_kernel<NST, W, SKIP><<<grid, W * 32, smem, s>>>(*kmap16, *vmap16, rows, segs, Qr, H, KVH, G, n_items,
+                                                                 slots, O, item_ctr, g_k1_row_order);
   return (int)cudaGetLastError();
 }
 
@@ -1794,9 +1716,7 @@ extern "C" int spex_k_tree_attn_wmma(const CUtensorMap* kmap16, const CUtensorMa
   if (M <= 0) return 0;
   if (dh != 128 || G < 1 || G > 16) return -1;
   // 2 stages x 12 warps (8 KB per stage): the best of a stages x warps sweep on c5
-  if (G <= 4) return launch_wmma<kMmaNST, kMmaWarps>(kmap16, vmap16, rows, segs, Qr, H, KVH, G, slots, O, M, item_ctr, s);
-  if (G <= 8) return launch_wmma<kMmaNST, 9>(kmap16, vmap16, rows, segs, Qr, H, KVH, G, slots, O, M, item_ctr, s);
-  return -1;  // the query buffers of larger groups do not fit beside the rings
+  return launch_wmma<kMmaNST, kMmaWarps>(kmap16, vmap16, rows, segs, Qr, H, KVH, G, slots, O, M, item_ctr, s);
 }
 
 template <int DH, int G>
@@ -1926,8 +1846,7 @@ extern "C" void spex_k_preload() {
   preload_one(tree_attn_decode_kernel<64, 4, 8>);
   preload_one(tree_attn_decode_kernel<64, 4, 4>);
   preload_one(tree_attn_bulk_kernel<16, 2, 14>);
-  preload_one(tree_attn_wmma_kernel<kMmaNST, kMmaWarps>);
-  preload_one(tree_attn_wmma_kernel<kMmaNST, 9>);
+  preload_one(tree_attn_wmma_kernel<kMmaNST, kMmaWarps, false>);
   preload_one(tree_attn_tile_mma_kernel<1>);
   preload_one(tree_attn_tile_mma_kernel<2>);
   preload_one(tree_attn_tile_mma_kernel<4>);
