@@ -429,7 +429,9 @@ def main():
         "vs_baseline": None,
         "dtype": "bf16",
         "data": "synthetic (hash-seeded prompts and teacher-forced tokens, random-init weights)",
-        "config": {"workload": f"{args.config}: rebase_bfs w16 d16 target16, T1, "
+        "config": {"workload": f"{args.config}: {cfg['family']} w{cfg['policy'].get('width', 4)} "
+                               f"d{cfg['policy'].get('max_depth', 16)} target{cfg['policy'].get('target_answers', 10)}, "
+                               f"{'+'.join(f.upper() for f in cfg['run'].get('flags', [])) or 'no flags'}, "
                                f"{cfg['run']['n_queries']} queries/{'step' if coupled else 'GPU/step'}",
                    "policy": args.policy, "prm": args.prm,
                    "queries_per_step_per_gpu": cfg["run"]["n_queries"],

@@ -507,6 +507,16 @@ SPEX_HDNI void engine_advance(Run* R, EX& ex, double limit) {
   ex.sync();
 }
 
+// A query needs a follow-up pass: flag it and, on the flag's 0 -> 1 edge,
+// push it on the dirty list so followups() need not scan every query record
+// (the items of one phase own disjoint queries, so the edge test is race-free).
+SPEX_HD void mark_followup(Run* R, int q) {
+  QueryRun* qr = &R->qs[q];
+  if (qr->need_followup) return;
+  qr->need_followup = 1;
+  R->q_dirty[atomic_add_int(&R->g->n_dirty, 1)] = q;
+}
+
 // --------------------------------------------------------------- admission
 // executor.cpp:765-783 plus generate_workload seeds (sim.cpp:177-180)
 SPEX_HDNI void admit_query(Run* R, int q, Rec* rec_slot) {
@@ -521,7 +531,7 @@ SPEX_HDNI void admit_query(Run* R, int q, Rec* rec_slot) {
   qr->golden = golden_label_of(c, seed);
   qr->hit_ema = c.initial_hit_ema;
   qr->admitted = 1;
-  qr->need_followup = 1;
+  mark_followup(R, q);
   qr->nnodes = 1;
   qr->chain_tip = kNoNode;
   qr->rest_cur = 0;
@@ -610,12 +620,12 @@ SPEX_HDNI void process_items(Run* R, EX& ex, int n_items, int kind, int rank_fil
         q = R->st_q[sid];
         QC x = make_qc(R, q, &it, slot);
         R->fin_scored[i] = on_stream_done(x, sid, R->fin_tokens[i], R->fin_cancel[i]) ? 1 : 0;
-        R->qs[q].need_followup = 1;
+        mark_followup(R, q);
       } else if (kind == IK_REWARD) {
         q = R->it_key[i];
         QC x = make_qc(R, q, &it, slot);
         on_reward(x, R->ev_node[g->fifo_head - 1]);
-        R->qs[q].need_followup = 1;
+        mark_followup(R, q);
       } else if (kind == IK_FOLLOWUP) {
         q = R->it_key[i];
         QC x = make_qc(R, q, &it, slot);
@@ -988,6 +998,11 @@ SPEX_HDNI void scheduling_round(Run* R, EX& ex, int* warp_off) {
   GState* g = R->g;
   const Cfg& c = R->cfg;
   if (!c.t1) return;
+  // With T2 a round grants nothing while the producers are saturated
+  // (executor.cpp:730-731, idle <= 0 returns); the per-query fields the
+  // candidate scan writes are read only by this round, so skip it outright
+  // (at Q = 4096 the scan of every query record is most of the control time).
+  if (c.t2 && c.producer_slots - (g->n_act + g->n_staged) <= 0) return;
   const int Q = c.n_queries;
   for (int q = ex.tid; q < Q; q += ex.nthr) {
     QueryRun* qr = &R->qs[q];
@@ -1035,15 +1050,46 @@ SPEX_HDNI void scheduling_round(Run* R, EX& ex, int* warp_off) {
   commit_items(R, ex, m);
 }
 
+// The queries needing a follow-up, ascending (item order = log order): from
+// the dirty list when it is short (sorted by rank counting), else by a scan of
+// every query record; the list is emptied either way.
+template <class EX>
+SPEX_HDNI int collect_dirty(Run* R, EX& ex) {
+  GState* g = R->g;
+  const int nd = g->n_dirty;
+  auto need = [&](int q) {
+    const QueryRun* qr = &R->qs[q];
+    return qr->admitted && !qr->finished && qr->need_followup;
+  };
+  int n;
+  if (nd > 512) {
+    n = collect_queries(R, ex, need);
+  } else {
+    int* keep = R->it_scan_a;
+    for (int i = ex.tid; i < nd; i += ex.nthr) keep[i] = need(R->q_dirty[i]) ? R->q_dirty[i] : -1;
+    ex.sync();
+    for (int i = ex.tid; i < nd; i += ex.nthr) {
+      const int q = keep[i];
+      if (q < 0) continue;
+      int rank = 0;
+      for (int j = 0; j < nd; ++j) rank += keep[j] >= 0 && keep[j] < q;
+      R->it_key[rank] = q;
+    }
+    int m = 0;
+    for (int i = ex.tid; i < nd; i += ex.nthr) m += keep[i] >= 0;
+    n = static_cast<int>(ex_sum_i64(ex, m));
+  }
+  ex.sync();
+  if (ex.tid == 0) g->n_dirty = 0;
+  ex.sync();
+  return n;
+}
+
 // consumer_step_followups (executor.cpp:746-763)
 template <class EX>
 SPEX_HDNI void followups(Run* R, EX& ex, int* warp_off) {
   for (int pass = 0; pass < 4; ++pass) {
-    auto need = [&](int q) {
-      const QueryRun* qr = &R->qs[q];
-      return qr->admitted && !qr->finished && qr->need_followup;
-    };
-    const int n = collect_queries(R, ex, need);
+    const int n = collect_dirty(R, ex);
     if (n == 0 || R->g->error) break;
     for (int i = ex.tid; i < n; i += ex.nthr) R->qs[R->it_key[i]].need_followup = 0;
     ex.sync();

@@ -274,6 +274,8 @@ struct GState {
   i64 kv_free_head, kv_free_tail;  // FIFO ring of freed physical pages (kv_free)
   i64 kv_live, kv_peak, kv_freed;  // pages held by live thoughts (peak) and pages freed
   int n_sched, n_sched_rows;
+  int n_dirty;    // queries pushed on q_dirty since the last follow-up pass
+  int pad_dirty;
   i64 start_ns;   // device wall clock at the start of the run
   i64 reward_wait_ns;  // time the control spent waiting for PRM scores (reward_prm)
   // device cycle counters per phase (thread 0's view)
@@ -330,6 +332,7 @@ struct Run {
   QueryRun* qs;
   QueryTally* q_tally;
   i64* q_finish_ns;  // device wall clock (globaltimer) at each query's query_done
+  int* q_dirty;      // queries whose need_followup went 0 -> 1 (unordered; follow-up work list)
   u32* q_rest_stack;
   u32* q_layer;
   u32* q_cohort;

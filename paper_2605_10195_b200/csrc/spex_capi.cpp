@@ -657,6 +657,7 @@ void layout(Arena& A, Run& R, int Q, int node_cap, int stream_cap, int log_cap, 
   A.add(R.qs, Q);
   A.add(R.q_tally, Q);
   A.add(R.q_finish_ns, Q);
+  A.add(R.q_dirty, Q + 64);
   A.add(R.q_rest_stack, NN);
   A.add(R.q_layer, NN);
   A.add(R.q_cohort, NN);
