@@ -1062,7 +1062,8 @@ SPEX_HDNI int collect_dirty(Run* R, EX& ex) {
     return qr->admitted && !qr->finished && qr->need_followup;
   };
   int n;
-  if (nd > 512) {
+  if (nd > 512 || R->cfg.n_queries <= ex.nthr) {
+    // a long list, or few enough queries for one ballot pass over all of them
     n = collect_queries(R, ex, need);
   } else {
     int* keep = R->it_scan_a;
