@@ -13,13 +13,23 @@
  *   spex_canonical_config     <- ExperimentConfig::from_json + to_json
  *                                (proj/src/config.cpp:73-137,177-275)
  *   spex_totals               <- totsim::RunTotals (executor.hpp:20-33)
+ *   spex_policy_ucb_score / ucb_select / rebase_widths
+ *                             <- totsim::ucb_score / ucb_select / rebase_widths
+ *                                (policy.hpp:43-70, policy.cpp:25-118)
+ *   spex_budget_k_total / allocate
+ *                             <- totsim::roofline_k_total / allocate_budgets
+ *                                (budget.hpp:37-55, budget.cpp:23-96)
+ *   spex_executor_set_reward_source
+ *                             <- RewardOracle::reward (sim.hpp:115-142), the
+ *                                content oracle or the PRM's score (model mode)
  *
  * Conventions: plain pointers and sizes, no exceptions across the ABI, status
  * 0 = ok, otherwise totsim::Errc ordinal + 1 (errors.hpp:9-28) or >= 100 for
  * capacity/device failures. One CUDA stream per executor handle; distinct
  * handles may be driven from different threads (single writer per handle, as
- * executor.hpp:92-99 requires). Memory returned through char** is released
- * with spex_free.
+ * executor.hpp:92-99 requires); runs with a model attached share the
+ * process-wide model cache and take turns on a process lock. Memory returned
+ * through char** is released with spex_free.
  */
 #ifndef SPEX_H_
 #define SPEX_H_
@@ -146,7 +156,7 @@ int spex_executor_set_model(spex_executor* ex, const char* policy_shape, const c
  * (one server); SURVEY.md §8e. */
 int spex_executor_set_shard(spex_executor* ex, int rank, int world);
 int spex_executor_model_stats(spex_executor* ex, spex_model_stats* out);
-/* Tree-KV pool size in pages (0 = the default: the resident pools, else 55%
+/* Tree-KV pool size in pages (0 = the default: the resident pools, else 62%
  * of free HBM). Pages of dead thoughts (pruned, REBASE layers expanded,
  * scored terminals, finished queries) are reused (no reference counterpart:
  * the reference holds no KV, SearchTree::prune_subtree tree.cpp:119-141 and

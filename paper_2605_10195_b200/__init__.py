@@ -187,7 +187,7 @@ class Executor:
         _check(self._L.spex_executor_set_shard(self._h, int(rank), int(world)))
 
     def set_kv_pages(self, pages: int) -> None:
-        """Tree-KV pool size in pages of 16 tokens (0: the default, 55% of free HBM)."""
+        """Tree-KV pool size in pages of 16 tokens (0: the default, 62% of free HBM)."""
         _check(self._L.spex_executor_set_kv_pages(self._h, int(pages)))
 
     def set_reward_source(self, source: str) -> None:

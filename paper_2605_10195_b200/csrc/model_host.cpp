@@ -549,7 +549,7 @@ extern "C" void spex_model_cache_release_mismatch(const ModelRunConfig* mc) {
 }
 
 // Tree-KV pool capacity (slots) for the next run of `mc`: the resident pools
-// when the cached models match, else 55% of the free HBM after releasing the
+// when the cached models match, else 62% of the free HBM after releasing the
 // mismatched ones (both models, all layers, K and V in bf16).
 extern "C" long long spex_model_pool_slots(const ModelRunConfig* mc) {
   spex_model_cache_release_mismatch(mc);
@@ -559,7 +559,7 @@ extern "C" long long spex_model_pool_slots(const ModelRunConfig* mc) {
   cudaMemGetInfo(&free_b, &total_b);
   const double per_slot = 4.0 * (mc->policy.L * mc->policy.KVH * mc->policy.dh +
                                  (mc->with_prm ? mc->prm.L * mc->prm.KVH * mc->prm.dh : 0));
-  return static_cast<long long>(0.55 * static_cast<double>(free_b) / per_slot);
+  return static_cast<long long>(0.62 * static_cast<double>(free_b) / per_slot);
 }
 
 extern "C" void spex_model_cache_clear() {
