@@ -254,6 +254,24 @@ __device__ __forceinline__ void store_block(float* buf, const float* vals, int l
 
 }  // namespace tc
 
+#ifdef SPEX_GEMM_PROBE
+// Timing probes (tools/gemm_probe.py, a separate probe build only): globaltimer
+// stamps per CTA at the kernel's milestones.
+__device__ unsigned long long* g_probe = nullptr;
+__device__ __forceinline__ void probe(int k) {
+  if (g_probe) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_probe[blockIdx.x * 16 + k] = t;
+  }
+}
+#define SPEX_PROBE(k) probe(k)
+#else
+#define SPEX_PROBE(k) \
+  do {                \
+  } while (0)
+#endif
+
 template <int EPI, int DH, int BN, int CG>
 __global__ void __launch_bounds__(tc::kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -276,6 +294,7 @@ __global__ void __launch_bounds__(tc::kThreads, 1)
   int* tq = reinterpret_cast<int*>(tmem_slot + 4);  // [kTq]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) SPEX_PROBE(0);
   const uint32_t rank = CG == 2 ? cluster_rank() : 0;
   const int kblocks = K / BK;
   // tile t = (mb, nb) with mb fastest: the row blocks that share a weight tile
@@ -319,6 +338,7 @@ __global__ void __launch_bounds__(tc::kThreads, 1)
   // programmatic dependent launch: everything above overlapped the previous
   // kernel's tail; operands (and the tile counter's reset) are ready after this
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (threadIdx.x == 0) SPEX_PROBE(1);
 
   if (warp == 0) {
     // ---------------- TMA producer
@@ -358,6 +378,7 @@ __global__ void __launch_bounds__(tc::kThreads, 1)
           const uint32_t fb = full_leader + s * 8;
           unsigned char* a = sA + s * C::kABytes;
           unsigned char* b = sB + s * C::kBBytes;
+          if (it == 0 && kb == 0) SPEX_PROBE(2);
           tma_load_2d<CG>(a, &tmA, kb * BK, arow, fb);
           tma_load_2d<CG>(a + 64 * BK * 2, &tmA, kb * BK, arow + 64, fb);
 #pragma unroll
@@ -372,6 +393,7 @@ __global__ void __launch_bounds__(tc::kThreads, 1)
       for (int it = 0;; ++it) {
         const int acc = it & 1;
         mbar_wait(&full[g % STAGES], (g / STAGES) & 1);  // first stage of tile `it` (or the sentinel)
+        if (it == 0) SPEX_PROBE(3);
         const int t = tq[it % kTq];
         // accumulator `acc` must be drained before its barrier moves again
         // (also for the sentinel: two unobserved phases would alias the parity)
@@ -395,6 +417,8 @@ __global__ void __launch_bounds__(tc::kThreads, 1)
           mma_commit<CG>(&empty[s]);
         }
         mma_commit<CG>(&tfull[acc]);
+        if (it == 0) SPEX_PROBE(4);
+        if (it == 1) SPEX_PROBE(10);
       }
     }
     __syncwarp();
@@ -409,6 +433,7 @@ __global__ void __launch_bounds__(tc::kThreads, 1)
     for (int it = 0;; ++it) {
       const int acc = it & 1;
       mbar_wait(&tfull[acc], (it >> 1) & 1);
+      if (ew == 0 && lane == 0 && it < 3) SPEX_PROBE(5 + 2 * it);
       if (rank != 0) mbar_wait_cluster(&tqbar[it % kTq], (it / kTq) & 1);
       const int t = *reinterpret_cast<volatile int*>(&tq[it % kTq]);
       if (t < 0) break;
@@ -577,6 +602,7 @@ __global__ void __launch_bounds__(tc::kThreads, 1)
       }
     }
   }
+  if (warp == 2 && lane == 0) SPEX_PROBE(11);
   if constexpr (EPI == TC_EPI_STORE)
     if (warp >= 2 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // stores landed
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -591,6 +617,7 @@ __global__ void __launch_bounds__(tc::kThreads, 1)
     else
       asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C::kAllocCols));
   }
+  if (threadIdx.x == 0) SPEX_PROBE(12);
   // self-resetting tile queue: the last leader out zeroes it for the next launch
   if (sched && threadIdx.x == 0 && rank == 0) {
     __threadfence();
@@ -861,3 +888,9 @@ extern "C" void spex_k_gemm_preload() {
   preload_fn(rope_table_kernel);
   preload_fn(interleave_gu_kernel);
 }
+
+#ifdef SPEX_GEMM_PROBE
+extern "C" int spex_gemm_probe_set(unsigned long long* p) {
+  return (int)cudaMemcpyToSymbol(spex::g_probe, &p, sizeof(p));
+}
+#endif
