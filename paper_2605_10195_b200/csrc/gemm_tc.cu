@@ -335,6 +335,19 @@ __global__ void __launch_bounds__(tc::kThreads, 1)
     __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
+  // The weights do not depend on the previous kernel: pull the first tile's
+  // weight boxes into L2 while that kernel drains (programmatic dependent launch)
+  if (warp == 0 && lane == 0 && cluster_id < n_tiles) {
+    const int nb0 = cluster_id / n_mb;
+    const int brow0 = nb0 * BN + (int)rank * BNL;
+    const int kpf = kblocks < STAGES ? kblocks : STAGES;
+    for (int kb = 0; kb < kpf; ++kb)
+#pragma unroll
+      for (int r = 0; r < BNL / 64; ++r)
+        asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(&tmB), "r"(kb * BK),
+                     "r"(brow0 + r * 64)
+                     : "memory");
+  }
   // programmatic dependent launch: everything above overlapped the previous
   // kernel's tail; operands (and the tile counter's reset) are ready after this
   asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -349,7 +362,11 @@ __global__ void __launch_bounds__(tc::kThreads, 1)
         const int slot = it % kTq;
         int t;
         if (rank == 0) {
-          long long tl = sched ? (long long)atomicAdd(sched, 1u) : (long long)cluster_id + (long long)it * n_clusters;
+          // the first tile is static (no atomic on the critical path of the
+          // pipeline's start); later ones come from the dynamic queue
+          long long tl = it == 0 ? (long long)cluster_id
+                         : sched ? (long long)n_clusters + atomicAdd(sched, 1u)
+                                 : (long long)cluster_id + (long long)it * n_clusters;
           t = tl < n_tiles ? (int)tl : -1;
           tq[slot] = t;
           if constexpr (CG == 2) {
@@ -765,12 +782,37 @@ int launch_gemm_tc(const CUtensorMap* tmA, const CUtensorMap* tmB, const CUtenso
   return (int)cudaLaunchKernelEx(&cfg, kern, *tmA, *tmB, *tmY, M, N, K, *ep, sched);
 }
 
+// Output tensor maps by (pointer, M, N, ldy): encoding one costs microseconds
+// of host time per launch, and the forward launches the same few shapes.
+struct OutMapEntry {
+  const float* y;
+  int M, N, ldy;
+  alignas(64) CUtensorMap map;
+};
+bool out_map_cached(CUtensorMap* m, const float* y, int M, int N, int ldy) {
+  static thread_local OutMapEntry cache[32];
+  static thread_local int n_used = 0, next = 0;
+  for (int i = 0; i < n_used; ++i)
+    if (cache[i].y == y && cache[i].M == M && cache[i].N == N && cache[i].ldy == ldy) {
+      *m = cache[i].map;
+      return true;
+    }
+  if (!make_out_map(m, y, M, N, ldy)) return false;
+  OutMapEntry& e = cache[n_used < 32 ? n_used++ : (next++ & 31)];
+  e.y = y;
+  e.M = M;
+  e.N = N;
+  e.ldy = ldy;
+  e.map = *m;
+  return true;
+}
+
 template <int EPI, int DH>
 int launch_shape(int cg, int bn, const CUtensorMap* tmA, const CUtensorMap* tmB, int M, int N, int K,
                  const TcEpilogue* ep, unsigned int* sched, cudaStream_t s) {
   alignas(64) CUtensorMap tmY{};
   if constexpr (EPI == TC_EPI_STORE)
-    if (!make_out_map(&tmY, ep->y, M, N, ep->ldy)) return -2;
+    if (!out_map_cached(&tmY, ep->y, M, N, ep->ldy)) return -2;
   const CUtensorMap* y = &tmY;
   if (cg == 2 && bn == 256) return launch_gemm_tc<EPI, DH, 256, 2>(tmA, tmB, y, M, N, K, ep, sched, s);
   if (cg == 2 && bn == 128) return launch_gemm_tc<EPI, DH, 128, 2>(tmA, tmB, y, M, N, K, ep, sched, s);
