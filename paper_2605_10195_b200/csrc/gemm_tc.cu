@@ -824,21 +824,25 @@ int launch_shape(int cg, int bn, const CUtensorMap* tmA, const CUtensorMap* tmB,
 }
 
 // Tile shape: the candidate whose waves of tiles over the SMs finish first.
-// Per-tile cost ~ BN columns x a per-shape efficiency (pairs halve the weight
-// traffic per row; 64-wide tiles re-read X four times per 256 columns).
-void pick_shape(int M, int N, int epi, int* cg, int* bn) {
+// Per-tile cost ~ BN columns x a per-shape efficiency; a CTA pair adds a fixed
+// cost (cluster launch and sync, ~2 us) that short-K GEMMs do not amortise,
+// and single CTAs re-read the weights per 128 rows, which long-K GEMMs
+// (K > 3072) cannot afford. Fitted to tools/gemm_bench.py --sweep on the model
+// shapes (profiles/r02r_gemm_tile_sweep.txt).
+void pick_shape(int M, int N, int K, int epi, int* cg, int* bn) {
   struct Cand {
     int cg, bn;
     double eff;
   };
-  const Cand cands[] = {{2, 256, 1.00}, {2, 128, 1.10}, {1, 256, 1.08}, {1, 128, 1.20}, {1, 64, 1.45}};
+  const Cand cands[] = {{2, 256, 1.00}, {2, 128, 1.35}, {1, 256, 1.08}, {1, 128, 1.20}, {1, 64, 1.45}};
   double best = 1e300;
   for (const Cand& c : cands) {
     if (c.bn == 64 && epi != TC_EPI_STORE) continue;
+    if (c.cg == 1 && K > 3072) continue;
     const long long tiles = (long long)((M + 128 * c.cg - 1) / (128 * c.cg)) * ((N + c.bn - 1) / c.bn);
     const int slots = sm_count() / c.cg;
     const long long waves = (tiles + slots - 1) / slots;
-    const double cost = (double)waves * c.bn * c.eff;
+    const double cost = (double)waves * c.bn * c.eff + (c.cg == 2 ? 80.0 : 0.0);
     if (cost < best - 1e-9) {
       best = cost;
       *cg = c.cg;
@@ -858,7 +862,7 @@ extern "C" int spex_k_gemm_tc_ex(const CUtensorMap* tmA, const CUtensorMap* tmB,
   if (M <= 0) return 0;
   if (N % 64 || K % tc::BK) return -1;
   if (ep->kind != TC_EPI_STORE && N % 128) return -1;
-  if (cg == 0 || bn == 0) pick_shape(M, N, ep->kind, &cg, &bn);
+  if (cg == 0 || bn == 0) pick_shape(M, N, K, ep->kind, &cg, &bn);
   switch (ep->kind) {
     case TC_EPI_STORE:
       return launch_shape<TC_EPI_STORE, 128>(cg, bn, tmA, tmB, M, N, K, ep, sched, s);
@@ -880,7 +884,7 @@ extern "C" int spex_k_gemm_tc(const CUtensorMap* tmA, const CUtensorMap* tmB, in
   return spex_k_gemm_tc_ex(tmA, tmB, M, N, K, ep, sched, 0, 0, s);
 }
 
-extern "C" void spex_k_gemm_tc_shape(int M, int N, int epi, int* cg, int* bn) { pick_shape(M, N, epi, cg, bn); }
+extern "C" void spex_k_gemm_tc_shape(int M, int N, int K, int epi, int* cg, int* bn) { pick_shape(M, N, K, epi, cg, bn); }
 
 extern "C" void spex_k_lse_combine(const float* part, int M, int n_tiles, int* amax, float* lse, float* lsum,
                                    cudaStream_t s) {

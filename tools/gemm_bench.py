@@ -95,7 +95,7 @@ def main():
                 ep = TcEpilogue(kind=EPI_ROPE_KV, rows=rows_d.data_ptr(), rope=rope.data_ptr(), H=H, KVH=KVH, dh=dh,
                                 qscale=dh ** -0.5, Qr=Qr.data_ptr(), Kp=Kp.data_ptr(), Vp=Vp.data_ptr(), slots=slots)
             fl = 2.0 * M * N * K
-            lib.spex_k_gemm_tc_shape(M, N, epi, ctypes.byref(cg), ctypes.byref(bn))
+            lib.spex_k_gemm_tc_shape(M, N, K, epi, ctypes.byref(cg), ctypes.byref(bn))
             res = {"model": name, "op": op, "M": M, "N": N, "K": K, "auto": [cg.value, bn.value]}
 
             def run(c=0, n=0):
