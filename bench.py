@@ -388,6 +388,30 @@ def main():
                                              model_mode["spex"]["p50_query_latency_ms"])
         model_mode["queries_per_s_speedup"] = (model_mode["spex"]["queries_per_s"] /
                                                model_mode["barrier_sync"]["queries_per_s"])
+        # config 3 (rstar_dfs, T1+T2+T3, 512 queries): where the reference's
+        # virtual clock shows speculation paying off (185 s vs 258 s makespan)
+        c3 = (ROOT / "configs" / "c3_rstar_w4_q512.json").read_text()
+        c3_seed = json.loads(c3)["run"]["seed"]
+        mm3 = {"workload": "c3_rstar_w4_q512: rstar_dfs w4 d16 target10, T1+T2+T3, 512 queries"}
+        for name, flags in (("spex", None), ("barrier_sync", "")):
+            def c3_search():
+                ex = spex.Executor(c3, c3_seed, flags, trace=False, device=local)
+                ex.set_model(args.policy, args.prm, weight_seed=1)
+                ex.set_reward_source("prm")
+                t = ex.run()
+                m = ex.model_stats()
+                wall_ms, wait_ms = ex.query_wall_ms()
+                ex.close()
+                return t, m, wall_ms, wait_ms
+            c3_search()
+            t_m, m_m, wall_ms, wait_ms = c3_search()
+            mm3[name] = {"queries_per_s": t_m.queries / (m_m["step_ms"] / 1000.0),
+                         "p50_query_latency_ms": statistics.median(wall_ms), "step_ms": m_m["step_ms"],
+                         "control_reward_wait_ms": wait_ms, "decode_rows": m_m["decode_rows"],
+                         "virtual_makespan": t_m.makespan}
+        mm3["p50_latency_speedup"] = mm3["barrier_sync"]["p50_query_latency_ms"] / mm3["spex"]["p50_query_latency_ms"]
+        mm3["queries_per_s_speedup"] = mm3["spex"]["queries_per_s"] / mm3["barrier_sync"]["queries_per_s"]
+        model_mode["c3"] = mm3
     # the same search barrier-synchronously (no T1/T2/T3: the reference's
     # baseline arm, experiment.cpp:68-70), same model work, for the metric's
     # "vs barrier-synchronous search"
