@@ -1614,32 +1614,57 @@ extern "C" void spex_k1_set_row_order(const int* order) { g_k1_row_order = order
 // within a query arbitrary): the bulk K1's warps then work on one tree's rows
 // at the same time, so their shared prefixes are read from L2 while resident.
 __global__ void __launch_bounds__(1024) order_rows_kernel(const RowDesc* __restrict__ rows, int M, int Q,
-                                                           int* __restrict__ order) {
+                                                           int* __restrict__ order, int lpt) {
+  // Rows grouped by query (a tree's rows run together, so shared prefixes are
+  // served from L2), queries taken longest context first (the longest items
+  // start early instead of trailing the launch).
   constexpr int NB = 1024;
-  __shared__ int hist[NB], part[NB];
+  __shared__ int hist[NB], part[NB], key[NB], rnk[NB];
   const int tid = threadIdx.x;
   hist[tid] = 0;
+  key[tid] = 0;
   __syncthreads();
-  auto bucket = [&](int q) { return (int)(((long long)q * NB) / (Q > 0 ? Q : 1)); };
-  for (int r = tid; r < M; r += 1024) atomicAdd(&hist[min(bucket(rows[r].q), NB - 1)], 1);
+  auto bucket = [&](int q) { return min((int)(((long long)q * NB) / (Q > 0 ? Q : 1)), NB - 1); };
+  for (int r = tid; r < M; r += 1024) {
+    const int bq = bucket(rows[r].q);
+    atomicAdd(&hist[bq], 1);
+    if (lpt) atomicMax(&key[bq], rows[r].abs_pos + 1);
+  }
   __syncthreads();
-  const int v = hist[tid];
-  part[tid] = v;
+  // rank of each bucket: longer first, then by index (deterministic)
+  {
+    const int kb = key[tid];
+    int r = 0;
+    for (int j = 0; j < NB; ++j) {
+      const int kj = key[j];
+      r += kj > kb || (kj == kb && j < tid);
+    }
+    rnk[tid] = r;
+  }
   __syncthreads();
+  part[rnk[tid]] = hist[tid];
+  __syncthreads();
+  const int v = part[tid];
   for (int o = 1; o < NB; o <<= 1) {
     const int a = tid >= o ? part[tid - o] : 0;
     __syncthreads();
     part[tid] += a;
     __syncthreads();
   }
-  hist[tid] = part[tid] - v;
+  const int excl = part[tid] - v;  // start of the bucket ranked tid
   __syncthreads();
-  for (int r = tid; r < M; r += 1024) order[atomicAdd(&hist[min(bucket(rows[r].q), NB - 1)], 1)] = r;
+  part[tid] = excl;
+  __syncthreads();
+  hist[tid] = part[rnk[tid]];  // start of bucket tid
+  __syncthreads();
+  for (int r = tid; r < M; r += 1024) order[atomicAdd(&hist[bucket(rows[r].q)], 1)] = r;
 }
 
 extern "C" void spex_k_order_rows(const RowDesc* rows, int M, int Q, int* order, cudaStream_t s) {
   if (M <= 0) return;
-  order_rows_kernel<<<1, 1024, 0, s>>>(rows, M, Q, order);
+  // SPEX_K1_QLPT=0: queries in index order (round 1's claim order)
+  static const int lpt = !getenv("SPEX_K1_QLPT") || atoi(getenv("SPEX_K1_QLPT")) != 0;
+  order_rows_kernel<<<1, 1024, 0, s>>>(rows, M, Q, order, lpt);
 }
 extern "C" void spex_k1_set_kv_evict_first(int on) { g_k1_kv_evict_first = on ? 1 : 0; }
 
