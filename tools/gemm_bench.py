@@ -1,7 +1,8 @@
 """Microbenchmark: the hand-written tcgen05 GEMM (gemm_tc.cu) with the epilogue
 each projection uses in the model, on the model's shapes, against cuBLAS
-(torch.matmul, bf16 out — no epilogue) on the same shapes. CUDA-event timed,
-L2 flushed between launches (a 256 MB write), median of `reps`.
+(torch.matmul, bf16 out — no epilogue) on the same shapes. Each side is
+captured in a CUDA graph and timed by CUDA events around its replay right after
+an L2 flush (a 256 MB write): device time, no host launch path; median of `reps`.
 
   python tools/gemm_bench.py [--shapes mid|named|all] [--sweep]
 """
@@ -27,12 +28,26 @@ MODELS = {  # d, H, KVH, dh, F, V, rows per forward (c2 decode step / PRM batch;
 
 
 def timed(fn, flush, reps=15):
+    """Device time of one launch of `fn` with a cold L2: `fn` is captured in a
+    CUDA graph and replayed between events right after an L2 flush, so neither
+    side pays its host launch path (Python/ctypes for ours, the ATen dispatch
+    for cuBLAS) inside the timed region."""
+    fn()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(g, stream=s):
+            fn()
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
     ts = []
     for i in range(reps + 3):
         flush.zero_()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
-        fn()
+        g.replay()
         b.record()
         torch.cuda.synchronize()
         if i >= 3:
@@ -99,7 +114,8 @@ def main():
             res = {"model": name, "op": op, "M": M, "N": N, "K": K, "auto": [cg.value, bn.value]}
 
             def run(c=0, n=0):
-                rc = lib.spex_k_gemm_tc_ex(a.ptr, b.ptr, M, N, K, ctypes.byref(ep), sched.data_ptr(), c, n, st)
+                rc = lib.spex_k_gemm_tc_ex(a.ptr, b.ptr, M, N, K, ctypes.byref(ep), sched.data_ptr(), c, n,
+                                           torch.cuda.current_stream().cuda_stream)
                 assert rc == 0, rc
 
             t = timed(run, flush)
