@@ -778,7 +778,7 @@ int launch_gemm_tc(const CUtensorMap* tmA, const CUtensorMap* tmB, const CUtenso
   at[1].val.clusterDim.y = 1;
   at[1].val.clusterDim.z = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 2;
+  cfg.numAttrs = CG == 2 ? 2 : 1;  // single CTAs launch without a cluster
   return (int)cudaLaunchKernelEx(&cfg, kern, *tmA, *tmB, *tmY, M, N, K, *ep, sched);
 }
 

@@ -48,12 +48,23 @@ for (name, M, N, K, epi) in [("mid o", 2157, 1024, 1024, EPI_STORE), ("mid down"
             ev1.record()
             torch.cuda.synchronize()
             assert rc == 0
+        # back-to-back: the marginal device time of a second identical launch
+        flush.zero_()
+        e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        e0.record()
+        lib.spex_k_gemm_tc_ex(a.ptr, b.ptr, M, N, K, ctypes.byref(ep), sched.data_ptr(), cg, bn, st)
+        e1.record()
+        lib.spex_k_gemm_tc_ex(a.ptr, b.ptr, M, N, K, ctypes.byref(ep), sched.data_ptr(), cg, bn, st)
+        e2.record()
+        torch.cuda.synchronize()
+        b2b = (e0.elapsed_time(e1) * 1e3, e1.elapsed_time(e2) * 1e3)
         d = dbg.view(296, 16).cpu().numpy().astype(np.int64)
         live = d[:, 0] > 0
         d = d[live]
         t0 = d[:, 0].min()
         res = {"shape": name, "cg": cg, "bn": bn, "ctas": int(live.sum()), "event_us": round(ev0.elapsed_time(ev1) * 1e3, 2),
-               "span_us": round((d[:, 12].max() - t0) / 1e3, 2)}
+               "span_us": round((d[:, 12].max() - t0) / 1e3, 2),
+               "first_us": round(b2b[0], 2), "second_us": round(b2b[1], 2)}
         for k, nm in NAMES.items():
             col = d[:, k]
             col = col[col > 0]
