@@ -216,6 +216,53 @@ int spex_budget_k_total(const double* hw4, int active_batch, double avg_kv_bytes
 int spex_budget_allocate(const int* capacity, const double* hit_ema, const double* kv_bytes, int n, int k_total,
                          double tau, double weight_bytes, int* out);
 
+/* ---- content hooks: RewardOracle (sim.hpp:115-142) evaluated on the device
+ * with the search's own draws (glibc exp/log/cos restated bit for bit). */
+typedef struct spex_workload { /* WorkloadSpec (sim.hpp:82-108) */
+  double token_mu, token_sigma;
+  int token_min, token_max;
+  int shallow_min;
+  int shallow_max;
+  double shallow_p;
+  int deep_min;
+  int deep_max;
+  double deep_p;
+  double skew, golden_density, reward_on, reward_off, noise_sigma;
+  double correct_base, correct_slope, correct_floor;
+  int answer_alphabet, prompt_tokens;
+} spex_workload;
+/* token_len (sim.cpp:112-115) of n child path hashes. */
+int spex_content_token_len(const uint64_t* child_hash, int n, const spex_workload* wl, int* out);
+/* is_terminal / reward / answer_label (sim.cpp:117-169) of n nodes of one
+ * query: node i's path is path_hash[offsets[i] .. offsets[i+1]) = the path
+ * hashes of its depth-1 ancestor .. itself (empty: the root). Labels are the
+ * index k of "a<k>". */
+int spex_content_eval(const uint64_t* path_hash, const int* offsets, int n, uint64_t query_seed, int max_depth,
+                      const spex_workload* wl, int* terminal, double* reward, int* label);
+
+/* ---- expand seam: DecodeEngine::advance (sim.hpp:165-220, sim.cpp:305-384)
+ * on the device. The engine's active and staged stream vectors go in and come
+ * back out in the reference's order; each stream lists its strict ancestors
+ * as entries [anc_off, anc_off + anc_n) of anc_key (one key per distinct
+ * (tree, node), tokens in anc_tokens[key]) for the unique-KV-token cost.
+ * Completions come back in active order (cap entries; CapacityStage when more). */
+typedef struct spex_engine_hw { /* HardwareProfile (budget.hpp:13-22) */
+  double weight_bytes, mem_bandwidth, peak_compute, flops_per_token, kv_bytes_per_token, reward_latency;
+} spex_engine_hw;
+typedef struct spex_engine_stream {
+  int id, remaining, done, cancelled;
+  double ready;
+  int anc_off, anc_n;
+} spex_engine_stream;
+typedef struct spex_engine_finished {
+  int id, tokens_done, cancelled, pad;
+  double time;
+} spex_engine_finished;
+int spex_engine_advance(const spex_engine_hw* hw, double now, double limit, spex_engine_stream* active,
+                        int* n_active, spex_engine_stream* staged, int* n_staged, const int* anc_key,
+                        const int* anc_tokens, int n_keys, spex_engine_finished* out, int cap, int* n_out,
+                        double* now_out);
+
 /* run_once: traced run returning totals and the JSON-lines log. */
 int spex_run_once(const char* config_json, uint64_t seed, const char* flags_csv,
                   spex_totals* totals, char** out_lines);

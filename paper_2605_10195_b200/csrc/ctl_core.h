@@ -394,6 +394,47 @@ SPEX_HDNI int oracle_answer_label(const QC& x, u32 id) {
   return static_cast<int>((gold + off) % alpha);
 }
 
+// RewardOracle (sim.cpp:112-169) over a node given by its path hashes
+// path[0..depth) (its depth-1 ancestor .. itself): terminality (depth windows
+// by the depth-1 ancestor's draw), reward (golden path + clamped noise) and
+// answer label. Shared by the spex_content_* hooks (device and emulation);
+// the search itself memoises the same draws per node (add_node, oracle_*).
+template <class W>
+SPEX_HD void content_eval(const u64* path, int depth, u64 query_seed, int max_depth, const W& wl, int* terminal,
+                          double* reward, int* label) {
+  const u64 own = depth > 0 ? path[depth - 1] : splitmix64(query_seed);  // the root's hash (tree.cpp:57)
+  // is_terminal (sim.cpp:127-139) with deep_dominant (:117-125)
+  if (depth == 0) {
+    *terminal = 0;
+  } else {
+    const bool deep = uniform01(path[0], kSaltDeep) < wl.skew;
+    const int lo = deep ? wl.deep_min : wl.shallow_min;
+    int hi = deep ? wl.deep_max : wl.shallow_max;
+    const double p = deep ? wl.deep_p : wl.shallow_p;
+    if (hi > max_depth) hi = max_depth;
+    *terminal = depth >= hi ? 1 : depth < lo ? 0 : (uniform01(path[depth - 1], kSaltTerminal) < p ? 1 : 0);
+  }
+  // on_golden_path (:141-146) and reward (:148-154)
+  bool golden = true;
+  for (int i = depth - 1; i >= 0 && golden; --i) golden = uniform01(path[i], kSaltGolden) < wl.golden_density;
+  double r = golden ? wl.reward_on : wl.reward_off;
+  if (wl.noise_sigma > 0.0) r += wl.noise_sigma * normal01(own, kSaltNoise);
+  *reward = r < 0.0 ? 0.0 : (r > 1.0 ? 1.0 : r);
+  // answer_label (:162-169)
+  double pc = wl.correct_base - wl.correct_slope * depth;
+  if (pc < wl.correct_floor) pc = wl.correct_floor;
+  else if (wl.correct_base < pc) pc = wl.correct_base;
+  const u64 h = own;
+  const u64 alpha = static_cast<u64>(wl.answer_alphabet);
+  const u64 gold = splitmix64(query_seed ^ kSaltLabel) % alpha;
+  if (uniform01(h, kSaltCorrect) < pc) {
+    *label = static_cast<int>(gold);
+  } else {
+    const u64 off = 1 + splitmix64(h ^ kSaltLabel) % (alpha - 1);
+    *label = static_cast<int>((gold + off) % alpha);
+  }
+}
+
 // -------------------------------------------------------------- policy.cpp
 SPEX_HD double log_int(const Run* R, int n) {
   if (n >= 1 && n < R->log_tab_n) return R->log_tab[n];

@@ -1724,6 +1724,27 @@ extern "C" int spex_budget_k_total(const double* hw4, int active_batch, double a
   return 0;
 }
 
+extern "C" int spex_content_token_len(const uint64_t* child_hash, int n, const spex_workload* wl, int* out) {
+  for (int i = 0; i < n; ++i)
+    out[i] = lognormal_tokens(child_hash[i], kSaltTokens, wl->token_mu, wl->token_sigma, wl->token_min, wl->token_max);
+  return 0;
+}
+
+extern "C" int spex_content_eval(const uint64_t* path_hash, const int* offsets, int n, uint64_t query_seed,
+                                 int max_depth, const spex_workload* wl, int* terminal, double* reward, int* label) {
+  for (int i = 0; i < n; ++i)
+    content_eval(reinterpret_cast<const u64*>(path_hash) + offsets[i], offsets[i + 1] - offsets[i], query_seed,
+                 max_depth, *wl, terminal + i, reward + i, label + i);
+  return 0;
+}
+
+extern "C" int spex_engine_advance(const spex_engine_hw*, double, double, spex_engine_stream*, int*,
+                                   spex_engine_stream*, int*, const int*, const int*, int, spex_engine_finished*, int,
+                                   int*, double*) {
+  g_err = "spex_engine_advance needs the CUDA build";
+  return 200;
+}
+
 extern "C" int spex_budget_allocate(const int* capacity, const double* hit_ema, const double* kv_bytes, int n,
                                     int k_total, double tau, double weight_bytes, int* out) {
   for (int i = 0; i < n; ++i) out[i] = 0;

@@ -6,6 +6,10 @@
 //   spex_policy_rebase_widths  <- totsim::rebase_widths    (policy.cpp:65-118)
 //   spex_budget_k_total        <- totsim::roofline_k_total (budget.cpp:23-39)
 //   spex_budget_allocate       <- totsim::allocate_budgets (budget.cpp:45-96)
+//   spex_content_token_len     <- RewardOracle::token_len  (sim.cpp:112-115)
+//   spex_content_eval          <- RewardOracle::is_terminal / reward / answer_label
+//                                 (sim.cpp:117-169)
+//   spex_engine_advance        <- DecodeEngine::advance    (sim.cpp:305-384)
 //
 // Each call runs the same device functions the control kernel runs inside a
 // search (ctl_core.h, ctl_run.h allocate_block), so a reference-side binding
@@ -21,6 +25,7 @@
 #include <mutex>
 #include <vector>
 
+#include "../../include/spex.h"
 #include "ctl_run.h"
 
 namespace spex {
@@ -142,6 +147,182 @@ __global__ void __launch_bounds__(256) allocate_kernel(const int* capacity, cons
   for (int i = ex.tid; i < n; i += ex.nthr) score[i] = capacity[i] * hit_ema[i] * (weight_bytes + kv_bytes[i]);
   __syncthreads();
   allocate_block(ex, &g, n, k_total, tau, score, capacity, w, out, order);
+}
+
+// RewardOracle::token_len per child hash (the lognormal draw with glibc's
+// own exp / log / cos, ctl_rng.h).
+__global__ void token_len_kernel(const u64* h, int n, spex_workload wl, int* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = lognormal_tokens(h[i], kSaltTokens, wl.token_mu, wl.token_sigma, wl.token_min, wl.token_max);
+}
+
+// is_terminal / reward / answer_label per node (path hashes in CSR).
+__global__ void content_kernel(const u64* path, const int* off, int n, u64 query_seed, int max_depth,
+                               spex_workload wl, int* terminal, double* reward, int* label) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) content_eval(path + off[i], off[i + 1] - off[i], query_seed, max_depth, wl, terminal + i, reward + i,
+                          label + i);
+}
+
+// DecodeEngine::advance (sim.cpp:305-384), one block: joins in staged order,
+// the epoch cost series from the active set's unique KV tokens (distinct
+// ancestor keys flagged in parallel, sim.cpp:54-78), epochs to the first
+// completion / the limit / a pending join, completions in active order. The
+// stream tables come in and go back out in the reference's vector order.
+__global__ void __launch_bounds__(256) engine_advance_kernel(spex_engine_hw hw, double now, double limit,
+                                                             spex_engine_stream* act, int* n_act,
+                                                             spex_engine_stream* stg, int* n_stg,
+                                                             const int* anc_key, const int* anc_tokens, int n_keys,
+                                                             int* key_flag, spex_engine_finished* out, int cap,
+                                                             int* n_out, double* now_out, int* status) {
+  __shared__ GState cost;  // compute_, mem_a_, mem_d_ of the cached series
+  __shared__ int s_flag, s_target, s_mlimit, s_min;
+  __shared__ long long s_u;
+  __shared__ double s_now;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    s_now = now;
+    *n_out = 0;
+    *status = 0;
+  }
+  __syncthreads();
+  bool dirty = true;
+  for (int guard = 0; guard < (1 << 24); ++guard) {
+    if (tid == 0) {
+      // joins: staged streams whose ready time has arrived, in staged order
+      int na = *n_act, w = 0;
+      bool joined = false;
+      for (int j = 0; j < *n_stg; ++j) {
+        if (stg[j].ready <= s_now + kTimeEps) {
+          act[na++] = stg[j];
+          joined = true;
+        } else {
+          stg[w++] = stg[j];
+        }
+      }
+      *n_act = na;
+      *n_stg = w;
+      s_flag = joined ? 1 : 0;
+      if (na == 0) {
+        if (w == 0) {
+          s_flag = 2;  // return limit
+        } else {
+          double r = HUGE_VAL;
+          for (int j = 0; j < w; ++j) r = stg[j].ready < r ? stg[j].ready : r;
+          if (r > limit + kTimeEps) {
+            s_flag = 2;
+          } else {
+            s_now = r;
+            s_flag = 3;  // retry the joins
+          }
+        }
+      }
+    }
+    __syncthreads();
+    if (s_flag == 2) {
+      if (tid == 0) *now_out = limit;
+      return;
+    }
+    if (s_flag == 3) continue;
+    if (s_flag == 1) dirty = true;
+    const int na = *n_act;
+    if (dirty) {
+      // refresh_costs: U = sum of partial tokens + distinct strict-ancestor tokens
+      for (int k = tid; k < n_keys; k += blockDim.x) key_flag[k] = 0;
+      if (tid == 0) s_u = 0;
+      __syncthreads();
+      long long part = 0;
+      for (int i = tid; i < na; i += blockDim.x) {
+        part += act[i].done;
+        for (int a = act[i].anc_off; a < act[i].anc_off + act[i].anc_n; ++a) key_flag[anc_key[a]] = 1;
+      }
+      __syncthreads();
+      for (int k = tid; k < n_keys; k += blockDim.x)
+        if (key_flag[k]) part += anc_tokens[k];
+      atomicAdd(reinterpret_cast<unsigned long long*>(&s_u), static_cast<unsigned long long>(part));
+      __syncthreads();
+      if (tid == 0) {
+        cost.compute_ = static_cast<double>(na) * hw.flops_per_token / hw.peak_compute;
+        const double kv_bytes = hw.kv_bytes_per_token * static_cast<double>(s_u);
+        cost.mem_a_ = (hw.weight_bytes + kv_bytes) / hw.mem_bandwidth;
+        cost.mem_d_ = hw.kv_bytes_per_token * static_cast<double>(na) / hw.mem_bandwidth;
+      }
+      dirty = false;
+    }
+    if (tid == 0) {
+      int m_complete = act[0].remaining;
+      for (int i = 1; i < na; ++i) m_complete = act[i].remaining < m_complete ? act[i].remaining : m_complete;
+      const int m_limit = eng_steps_within(&cost, limit - s_now, m_complete);
+      int target = m_complete;
+      if (*n_stg > 0) {
+        double r = HUGE_VAL;
+        for (int j = 0; j < *n_stg; ++j) r = stg[j].ready < r ? stg[j].ready : r;
+        const int cap2 = m_complete < m_limit ? m_complete : m_limit;
+        if (cap2 >= 1 && s_now + eng_elapsed(&cost, cap2) >= r - kTimeEps) {
+          int lo = 1, hi = cap2;
+          while (hi > lo) {
+            const int mid = lo + (hi - lo) / 2;
+            if (s_now + eng_elapsed(&cost, mid) >= r - kTimeEps)
+              hi = mid;
+            else
+              lo = mid + 1;
+          }
+          target = lo;
+        }
+      }
+      s_mlimit = m_limit;
+      s_target = target;
+    }
+    __syncthreads();
+    if (s_target > s_mlimit) {
+      // partial epoch: stop at the last boundary inside the window
+      const int m = s_mlimit;
+      if (m > 0) {
+        for (int i = tid; i < na; i += blockDim.x) {
+          act[i].done += m;
+          act[i].remaining -= m;
+        }
+      }
+      __syncthreads();
+      if (tid == 0) *now_out = m > 0 ? s_now + eng_elapsed(&cost, m) : s_now;
+      return;
+    }
+    const int target = s_target;
+    for (int i = tid; i < na; i += blockDim.x) {
+      act[i].done += target;
+      act[i].remaining -= target;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      s_now += eng_elapsed(&cost, target);
+      int w = 0, f = 0;
+      for (int i = 0; i < na; ++i) {
+        if (act[i].remaining <= 0) {
+          if (f < cap) {
+            out[f].id = act[i].id;
+            out[f].tokens_done = act[i].done;
+            out[f].cancelled = act[i].cancelled;
+            out[f].time = s_now;
+          } else {
+            *status = ERR_CAP_STAGE;
+          }
+          ++f;
+        } else {
+          act[w++] = act[i];
+        }
+      }
+      *n_act = w;
+      *n_out = f;
+      s_flag = f > 0 ? 1 : 0;
+    }
+    dirty = true;
+    __syncthreads();
+    if (s_flag) {
+      if (tid == 0) *now_out = s_now;
+      return;
+    }
+  }
+  if (tid == 0) *status = ERR_STALLED;
 }
 
 // Device buffers of the host-facing calls (one stream, serialised).
@@ -297,4 +478,93 @@ extern "C" int spex_budget_allocate(const int* capacity, const double* hit_ema, 
     rc = finish();
   }
   return rc ? rc : finish();
+}
+
+extern "C" int spex_content_token_len(const uint64_t* child_hash, int n, const spex_workload* wl, int* out) {
+  std::lock_guard<std::mutex> lk(g_hook_mu);
+  if (int rc = ensure_stream()) return rc;
+  if (n <= 0) return 0;
+  int rc;
+  {
+    Dev d;
+    const u64* dh = d.put(reinterpret_cast<const u64*>(child_hash), n);
+    int* dout = d.put<int>(nullptr, n);
+    if (!dh || !dout) return 200;
+    token_len_kernel<<<(n + 127) / 128, 128, 0, g_hook_stream>>>(dh, n, *wl, dout);
+    d.get(out, dout, n);
+    rc = finish();
+  }
+  return rc ? rc : finish();
+}
+
+extern "C" int spex_content_eval(const uint64_t* path_hash, const int* offsets, int n, uint64_t query_seed,
+                                 int max_depth, const spex_workload* wl, int* terminal, double* reward, int* label) {
+  std::lock_guard<std::mutex> lk(g_hook_mu);
+  if (int rc = ensure_stream()) return rc;
+  if (n <= 0) return 0;
+  const int np = offsets[n];
+  int rc;
+  {
+    Dev d;
+    const u64* dp = d.put(reinterpret_cast<const u64*>(path_hash), np);
+    const int* doff = d.put(offsets, n + 1);
+    int* dt = d.put<int>(nullptr, n);
+    double* dr = d.put<double>(nullptr, n);
+    int* dl = d.put<int>(nullptr, n);
+    if (!dp || !doff || !dt || !dr || !dl) return 200;
+    content_kernel<<<(n + 127) / 128, 128, 0, g_hook_stream>>>(dp, doff, n, query_seed, max_depth, *wl, dt, dr, dl);
+    d.get(terminal, dt, n);
+    d.get(reward, dr, n);
+    d.get(label, dl, n);
+    rc = finish();
+  }
+  return rc ? rc : finish();
+}
+
+extern "C" int spex_engine_advance(const spex_engine_hw* hw, double now, double limit, spex_engine_stream* active,
+                                   int* n_active, spex_engine_stream* staged, int* n_staged, const int* anc_key,
+                                   const int* anc_tokens, int n_keys, spex_engine_finished* out, int cap, int* n_out,
+                                   double* now_out) {
+  std::lock_guard<std::mutex> lk(g_hook_mu);
+  if (int rc = ensure_stream()) return rc;
+  const int na = *n_active, ns = *n_staged, tot = na + ns;
+  int n_anc = 0;
+  for (int i = 0; i < na; ++i) n_anc = std::max(n_anc, active[i].anc_off + active[i].anc_n);
+  for (int i = 0; i < ns; ++i) n_anc = std::max(n_anc, staged[i].anc_off + staged[i].anc_n);
+  int rc, status = 0;
+  {
+    Dev d;
+    spex_engine_stream* da = d.put<spex_engine_stream>(nullptr, tot);
+    spex_engine_stream* ds = d.put<spex_engine_stream>(nullptr, tot);
+    if (!da || !ds) return 200;
+    if (na) cudaMemcpyAsync(da, active, sizeof(spex_engine_stream) * na, cudaMemcpyHostToDevice, g_hook_stream);
+    if (ns) cudaMemcpyAsync(ds, staged, sizeof(spex_engine_stream) * ns, cudaMemcpyHostToDevice, g_hook_stream);
+    int cnt[2] = {na, ns};
+    int* dcnt = d.put(cnt, 2);
+    const int* dk = d.put(anc_key, n_anc);
+    const int* dtok = d.put(anc_tokens, n_keys);
+    int* dflag = d.put<int>(nullptr, n_keys);
+    spex_engine_finished* dout = d.put<spex_engine_finished>(nullptr, std::max(cap, 1));
+    int* dn = d.put<int>(nullptr, 2);
+    double* dnow = d.put<double>(nullptr, 1);
+    if (!dcnt || !dk || !dtok || !dflag || !dout || !dn || !dnow) return 200;
+    engine_advance_kernel<<<1, 256, 0, g_hook_stream>>>(*hw, now, limit, da, dcnt, ds, dcnt + 1, dk, dtok, n_keys,
+                                                         dflag, dout, cap, dn, dnow, dn + 1);
+    d.get(cnt, dcnt, 2);
+    int nres[2];
+    d.get(nres, dn, 2);
+    d.get(now_out, dnow, 1);
+    rc = finish();
+    if (rc) return rc;
+    *n_active = cnt[0];
+    *n_staged = cnt[1];
+    *n_out = nres[0];
+    status = nres[1];
+    if (cnt[0]) cudaMemcpyAsync(active, da, sizeof(spex_engine_stream) * cnt[0], cudaMemcpyDeviceToHost, g_hook_stream);
+    if (cnt[1]) cudaMemcpyAsync(staged, ds, sizeof(spex_engine_stream) * cnt[1], cudaMemcpyDeviceToHost, g_hook_stream);
+    if (nres[0]) d.get(out, dout, std::min(nres[0], cap));
+    rc = finish();
+  }
+  if (rc) return rc;
+  return status ? status : finish();
 }

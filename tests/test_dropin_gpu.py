@@ -52,3 +52,22 @@ def test_hooks_match_reference_on_random_problems():
     if refutil.ref_lib() is None:
         pytest.skip("oracle/_ref not built")
     hooks_check.check_hooks(_lib.lib(), refutil.ref_lib())
+
+
+SIM_BIN = ROOT / "oracle" / "_ref" / "dropin_test_sim"
+
+
+def test_reference_sim_tests_pass_on_b200_content_and_engine_seams():
+    """The reference's own tests/test_sim.cpp (unmodified) with
+    RewardOracle::token_len / is_terminal / reward / answer_label and
+    DecodeEngine::advance on the device (integration/sim_b200.cpp ->
+    csrc/spex_hooks.cu): the oracle's purity, reward levels and noise, token
+    length distribution, terminal windows, answer correctness (test_sim.cpp:
+    155-332) and the decode engine's batching, staggered joins, limits,
+    farewell steps, staged cancels and determinism (:334-460)."""
+    if not SIM_BIN.exists():
+        pytest.skip("oracle/_ref/dropin_test_sim not built (needs /root/reference at build time)")
+    p = subprocess.run([str(SIM_BIN)], capture_output=True, text=True, timeout=900)
+    print(p.stdout[-2000:], p.stderr[-4000:])
+    assert p.returncode == 0, p.stdout[-4000:] + p.stderr[-4000:]
+    assert "| 0 failed" in p.stdout, p.stdout
