@@ -19,6 +19,10 @@
  *   spex_budget_k_total / allocate
  *                             <- totsim::roofline_k_total / allocate_budgets
  *                                (budget.hpp:37-55, budget.cpp:23-96)
+ *   spex_engine_advance       <- totsim::DecodeEngine::advance (sim.cpp:305-384)
+ *   spex_content_token_len / eval
+ *                             <- RewardOracle::token_len / is_terminal / reward /
+ *                                answer_label (sim.cpp:112-169)
  *   spex_executor_set_reward_source
  *                             <- RewardOracle::reward (sim.hpp:115-142), the
  *                                content oracle or the PRM's score (model mode)
