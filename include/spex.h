@@ -159,6 +159,43 @@ int spex_executor_set_model(spex_executor* ex, const char* policy_shape, const c
  * exchange. Call before spex_executor_run. Replaces nothing in the reference
  * (one server); SURVEY.md §8e. */
 int spex_executor_set_shard(spex_executor* ex, int rank, int world);
+
+/* Split mode (north_star's multi-GPU data path): one job of Q
+ * queries over `world` GPUs, rank r owning query block [Q*r/world,
+ * Q*(r+1)/world) with its OWN decode engine, clock and tree KV. The only
+ * exchange is T2's: the k-th allocate_budgets call of every rank
+ * (executor.cpp:727-733) is one round in which each rank posts its idle
+ * producer slots and its candidates' (score, capacity) to its outbox and the
+ * allocation (budget.cpp:45-96) runs over every rank's candidates in rank
+ * order with k_total = the ranks' idle slots summed. The control kernels
+ * exchange through the outboxes directly (peer loads over NVLink), no host
+ * round trip. world = 1 is the reference's single server.
+ *
+ *   spex_split_outbox_bytes   bytes of one rank's outbox (-1: bad arguments)
+ *   spex_split_outbox_alloc   zeroed outbox on `device` + its CUDA IPC handle
+ *                             (64 bytes) for the other ranks' processes
+ *   spex_split_outbox_open    map another rank's outbox (peer access)
+ *   spex_executor_set_split   this executor is rank `rank`: outboxes[world]
+ *                             (device pointers, [rank] its own), `epoch` a run
+ *                             id >= 1, the same on every rank and new for each
+ *                             run (outboxes are never reset). The executor's
+ *                             n_queries becomes its block's size.
+ *   spex_split_run            every rank of one job on ONE device, as CTAs of
+ *                             one control launch (tests; control only); fills
+ *                             out[world] with executors that have run (logs,
+ *                             totals, stats; destroy each).
+ *   spex_executor_split_stats exchange rounds and the time spent waiting.
+ * Oracle: oracle/ref_split.cpp (the reference's executor, one thread per rank,
+ * coupled by the same exchange). */
+long long spex_split_outbox_bytes(int n_queries_job, int world);
+int spex_split_outbox_alloc(int device, long long bytes, void** dptr, unsigned char* ipc_handle);
+int spex_split_outbox_open(int device, const unsigned char* ipc_handle, void** dptr);
+int spex_split_outbox_close(void* dptr);
+int spex_split_outbox_free(void* dptr);
+int spex_executor_set_split(spex_executor* ex, int rank, int world, void* const* outboxes, long long epoch);
+int spex_split_run(const char* config_json, uint64_t seed, const char* flags_csv, int world, int device, int trace,
+                   spex_executor** out);
+int spex_executor_split_stats(spex_executor* ex, long long* rounds, double* wait_ms);
 int spex_executor_model_stats(spex_executor* ex, spex_model_stats* out);
 /* Tree-KV pool size in pages (0 = the default: the resident pools, else 62%
  * of free HBM). Pages of dead thoughts (pruned, REBASE layers expanded,

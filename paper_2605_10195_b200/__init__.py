@@ -186,6 +186,19 @@ class Executor:
         every rank's decisions and log equal the single-server reference's."""
         _check(self._L.spex_executor_set_shard(self._h, int(rank), int(world)))
 
+    def set_split(self, rank: int, world: int, outboxes, epoch: int) -> None:
+        """Split mode (shard.Outboxes builds ``outboxes``): this executor is
+        rank ``rank`` of a ``world``-rank job — its query block with its own
+        engine and clock, T2 budgets allocated over every rank's candidates.
+        ``epoch`` >= 1 is the run id, the same on every rank."""
+        arr = (ctypes.c_void_p * int(world))(*outboxes)
+        _check(self._L.spex_executor_set_split(self._h, int(rank), int(world), arr, int(epoch)))
+
+    def split_stats(self) -> dict:
+        r, w = ctypes.c_longlong(), ctypes.c_double()
+        _check(self._L.spex_executor_split_stats(self._h, ctypes.byref(r), ctypes.byref(w)))
+        return {"rounds": r.value, "wait_ms": w.value}
+
     def set_kv_pages(self, pages: int) -> None:
         """Tree-KV pool size in pages of 16 tokens (0: the default, 62% of free HBM)."""
         _check(self._L.spex_executor_set_kv_pages(self._h, int(pages)))
@@ -281,6 +294,21 @@ def run_batch(cfg: Any, seeds, flags: SpexFlags | str | None = None, device: int
     return [RunTotals(**t.as_dict()) for t in tots], ms.value
 
 
+def split_run(cfg: Any, seed: int, world: int, flags: SpexFlags | str | None = None, trace: bool = True,
+              device: int = 0) -> list:
+    """Every rank of one split job (shard.py) on one device, as CTAs of one
+    control launch (control only). One dict per rank: log, rounds, stats."""
+    from . import shard
+    if isinstance(flags, SpexFlags):
+        fcsv = flags.to_csv()
+    else:
+        fcsv = flags
+    L = _lib.lib()
+    if not L.spex_device_ok():
+        raise RuntimeError("no sm_100 CUDA device: the SPEX B200 path has no CPU fallback")
+    return shard.split_run(L, _cfg_text(cfg), seed, world, fcsv, trace, device)
+
+
 __all__ = [
     "Executor",
     "RunOutcome",
@@ -291,4 +319,5 @@ __all__ = [
     "device_ok",
     "run_batch",
     "run_once",
+    "split_run",
 ]

@@ -134,6 +134,20 @@ _EXPORTS = {
     "spex_executor_set_model": (
         [ctypes.c_void_p, ctypes.c_char_p, ctypes.c_char_p, ctypes.c_uint64, ctypes.c_int], ctypes.c_int),
     "spex_executor_set_shard": ([ctypes.c_void_p, ctypes.c_int, ctypes.c_int], ctypes.c_int),
+    "spex_split_outbox_bytes": ([ctypes.c_int, ctypes.c_int], ctypes.c_longlong),
+    "spex_split_outbox_alloc": (
+        [ctypes.c_int, ctypes.c_longlong, ctypes.POINTER(ctypes.c_void_p), ctypes.c_char_p], ctypes.c_int),
+    "spex_split_outbox_open": ([ctypes.c_int, ctypes.c_char_p, ctypes.POINTER(ctypes.c_void_p)], ctypes.c_int),
+    "spex_split_outbox_close": ([ctypes.c_void_p], ctypes.c_int),
+    "spex_split_outbox_free": ([ctypes.c_void_p], ctypes.c_int),
+    "spex_executor_set_split": (
+        [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_void_p), ctypes.c_longlong],
+        ctypes.c_int),
+    "spex_split_run": (
+        [ctypes.c_char_p, ctypes.c_uint64, ctypes.c_char_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+         ctypes.POINTER(ctypes.c_void_p)], ctypes.c_int),
+    "spex_executor_split_stats": (
+        [ctypes.c_void_p, ctypes.POINTER(ctypes.c_longlong), ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
     "spex_executor_model_stats": ([ctypes.c_void_p, ctypes.POINTER(ModelStats)], ctypes.c_int),
     "spex_executor_set_kv_pages": ([ctypes.c_void_p, ctypes.c_longlong], ctypes.c_int),
     "spex_policy_ucb_score": (

@@ -523,7 +523,7 @@ SPEX_HDNI void admit_query(Run* R, int q, Rec* rec_slot) {
   const Cfg& c = R->cfg;
   QueryRun* qr = &R->qs[q];
   const u64 base = splitmix64(c.run_seed ^ kSaltQuery);
-  const u64 seed = hash_mix(base, static_cast<u64>(q) + 1);
+  const u64 seed = hash_mix(base, static_cast<u64>(q + c.q_offset) + 1);  // the job's query (split mode)
   // zero the query
   char* p = reinterpret_cast<char*>(qr);
   for (size_t i = 0; i < sizeof(QueryRun); ++i) p[i] = 0;
@@ -993,6 +993,180 @@ SPEX_HDNI void allocate_block(EX& ex, GState* g, int n, int k_total, double tau,
   }
 }
 
+// ------------------------------------------------ split mode budget exchange
+// north_star's multi-GPU data path: each rank owns a query block and runs its
+// own engine; the only exchange is the T2 allocation's per-query gains. The
+// k-th allocate_budgets call of every rank (executor.cpp:727-733: T2 on, a
+// candidate, idle producer slots) is exchange round k: the rank posts its idle
+// slots and its candidates' (score, capacity) to its outbox, waits until every
+// other rank has posted round k or finished its run, and allocates over the
+// concatenation in rank order with k_total = the posted idle slots' sum,
+// keeping its own candidates' grants (oracle: oracle/ref_split.cpp, the
+// reference's own executor in W threads). The outboxes live in each rank's HBM
+// and are read by the others over NVLink (peer-mapped; on one GPU, one
+// allocation); flags are epoch-tagged, so an outbox is never reset:
+//   [0] u64 started = epoch   [8] u64 posted = epoch << 32 | round
+//   [16] u64 done = epoch     [64 + (round & 1) * slot_bytes] slot:
+//   int idle, int n, 8 pad, double score[qmax], int cap[qmax]
+// A rank overwrites slot (k & 1) at round k + 2 only after every live rank
+// posted round k + 1, i.e. finished reading round k; a run starts only after
+// every rank started it, so no rank reads an earlier run's slots.
+constexpr int kSmXch = 700;  // 3 * kMaxSplit ints of ex.sm
+
+SPEX_HD u64 xch_load(const char* p) {
+#if SPEX_DEVICE_PASS
+  u64 v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+#else
+  return __atomic_load_n(reinterpret_cast<const u64*>(p), __ATOMIC_ACQUIRE);
+#endif
+}
+
+SPEX_HD void xch_store(char* p, u64 v) {
+#if SPEX_DEVICE_PASS
+  __threadfence_system();
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+#else
+  __atomic_store_n(reinterpret_cast<u64*>(p), v, __ATOMIC_RELEASE);
+#endif
+}
+
+SPEX_HD void xch_fence() {
+#if SPEX_DEVICE_PASS
+  __threadfence_system();
+#else
+  __atomic_thread_fence(__ATOMIC_SEQ_CST);
+#endif
+}
+
+SPEX_HD void xch_pause() {
+#if SPEX_DEVICE_PASS
+  __nanosleep(128);
+#else
+  __builtin_ia32_pause();
+#endif
+}
+
+// wait until `pred` holds; false after the 120 s watchdog (a rank gone)
+template <class P>
+SPEX_HD bool xch_wait(P pred) {
+  const i64 t0 = spex_wall_ns();
+  for (long long spin = 0; !pred(); ++spin) {
+    xch_pause();
+#if SPEX_DEVICE_PASS
+    if ((spin & 1023) == 1023 && spex_wall_ns() - t0 > 120000000000LL) return false;
+#else
+    if (spin > (1LL << 36)) return false;
+#endif
+  }
+  return true;
+}
+
+// run start: publish `started`, then wait until every rank started this run
+template <class EX>
+SPEX_HDNI void split_start(Run* R, EX& ex) {
+  const Cfg& c = R->cfg;
+  const u64 e = static_cast<u64>(c.split_epoch);
+  if (ex.tid == 0) xch_store(R->xch[c.split_rank], e);
+  ex.sync();
+  for (int s = ex.tid; s < c.split_world; s += ex.nthr) {
+    if (s == c.split_rank) continue;
+    const char* p = R->xch[s];
+    if (!xch_wait([&] { return xch_load(p) >= e; })) set_err(R, ERR_STALLED, -1, kNoNode);
+  }
+  ex.sync();
+}
+
+// run end: this rank takes part in no further round
+template <class EX>
+SPEX_HDNI void split_finish(Run* R, EX& ex) {
+  const Cfg& c = R->cfg;
+  if (ex.tid == 0) xch_store(R->xch[c.split_rank] + 16, static_cast<u64>(c.split_epoch));
+  ex.sync();
+}
+
+// One exchange round over the local candidates' al_score / al_rank [0, n):
+// on return al_score / al_rank [0, N) hold every posting rank's candidates in
+// rank order; *k_total is the posted idle slots' sum, *my_off this rank's
+// first candidate. Returns N.
+template <class EX>
+SPEX_HDNI int split_exchange(Run* R, EX& ex, int n, int idle, int* k_total, int* my_off) {
+  GState* g = R->g;
+  const Cfg& c = R->cfg;
+  const int W = c.split_world, me = c.split_rank;
+  const u64 e = static_cast<u64>(c.split_epoch);
+  const i64 t0 = ex.tid == 0 ? spex_wall_ns() : 0;
+  if (ex.tid == 0) g->xch_rounds += 1;
+  ex.sync();
+  const u64 k = static_cast<u64>(g->xch_rounds);
+  auto slot_of = [&](int s) { return R->xch[s] + kXchHead + static_cast<i64>(k & 1) * c.xch_slot_bytes; };
+  {
+    char* slot = slot_of(me);
+    double* sc = reinterpret_cast<double*>(slot + 16);
+    int* cp = reinterpret_cast<int*>(sc + c.split_qmax);
+    for (int i = ex.tid; i < n; i += ex.nthr) {
+      sc[i] = R->al_score[i];
+      cp[i] = R->al_rank[i];
+    }
+    if (ex.tid == 0) {
+      reinterpret_cast<int*>(slot)[0] = idle;
+      reinterpret_cast<int*>(slot)[1] = n;
+    }
+    xch_fence();
+  }
+  ex.sync();
+  if (ex.tid == 0) xch_store(R->xch[me] + 8, (e << 32) | k);
+  int* inc = ex.sm + kSmXch;          // [W] rank s posted round k
+  int* off = inc + kMaxSplit;         // [W] its first candidate in the concatenation
+  int* cnt = off + kMaxSplit;         // [W] its candidates
+  for (int s = ex.tid; s < W; s += ex.nthr) {
+    int in = 1;
+    if (s != me) {
+      const char* p = R->xch[s];
+      auto posted = [&] {
+        const u64 v = xch_load(p + 8);
+        return (v >> 32) == e && (v & 0xffffffffULL) >= k;
+      };
+      const bool ok = xch_wait([&] { return posted() || xch_load(p + 16) == e; });
+      if (!ok) set_err(R, ERR_STALLED, -1, kNoNode);
+      in = ok && posted() ? 1 : 0;  // `done` is stored after the last post: re-read
+    }
+    inc[s] = in;
+  }
+  ex.sync();
+  if (ex.tid == 0) {
+    int N = 0, K = 0;
+    for (int s = 0; s < W; ++s) {
+      off[s] = N;
+      cnt[s] = 0;
+      if (!inc[s]) continue;
+      const volatile int* h = reinterpret_cast<const volatile int*>(slot_of(s));
+      cnt[s] = h[1];
+      K += h[0];
+      N += cnt[s];
+    }
+    g->s_k_total = K;
+    g->s_n_items = N;
+    g->xch_wait_ns += spex_wall_ns() - t0;
+  }
+  ex.sync();
+  for (int s = 0; s < W; ++s) {
+    if (!cnt[s]) continue;
+    const volatile double* sc = reinterpret_cast<const volatile double*>(slot_of(s) + 16);
+    const volatile int* cp = reinterpret_cast<const volatile int*>(sc + c.split_qmax);
+    for (int i = ex.tid; i < cnt[s]; i += ex.nthr) {
+      R->al_score[off[s] + i] = sc[i];
+      R->al_rank[off[s] + i] = cp[i];
+    }
+  }
+  *k_total = g->s_k_total;
+  *my_off = off[me];
+  const int N = g->s_n_items;
+  ex.sync();
+  return N;
+}
+
 template <class EX>
 SPEX_HDNI void scheduling_round(Run* R, EX& ex, int* warp_off) {
   GState* g = R->g;
@@ -1034,8 +1208,10 @@ SPEX_HDNI void scheduling_round(Run* R, EX& ex, int* warp_off) {
       R->al_rank[i] = qr->capacity;
     }
     ex.sync();
-    allocate_block(ex, g, n, idle, c.tau, R->al_score, R->al_rank, R->al_w, R->al_out, R->al_order);
-    for (int i = ex.tid; i < n; i += ex.nthr) R->qs[R->it_key[i]].grant = R->al_out[i];
+    int n_all = n, k_total = idle, my_off = 0;
+    if (c.split_world > 1) n_all = split_exchange(R, ex, n, idle, &k_total, &my_off);
+    allocate_block(ex, g, n_all, k_total, c.tau, R->al_score, R->al_rank, R->al_w, R->al_out, R->al_order);
+    for (int i = ex.tid; i < n; i += ex.nthr) R->qs[R->it_key[i]].grant = R->al_out[my_off + i];
     ex.sync();
   }
   // issue: candidates with a grant and a plan that may be non-empty
@@ -1186,6 +1362,7 @@ SPEX_HD void run_loop(Run* R, EX& ex, int* warp_off) {
   GState* g = R->g;
   const Cfg& c = R->cfg;
   const int Q = c.n_queries;
+  if (c.split_world > 1) split_start(R, ex);
   if (ex.tid == 0) {
     const int first = c.batch_size < Q ? c.batch_size : Q;
     for (int q = 0; q < first; ++q) {
@@ -1249,6 +1426,7 @@ SPEX_HD void run_loop(Run* R, EX& ex, int* warp_off) {
     g->makespan = ms;
   }
   ex.sync();
+  if (c.split_world > 1) split_finish(R, ex);
 #if SPEX_DEVICE_PASS
   if (R->pub && ex.tid == 0) {
     __threadfence_system();

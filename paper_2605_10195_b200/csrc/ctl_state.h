@@ -197,6 +197,14 @@ struct Cfg {
   // Reward source: 0 = the content oracle (RewardOracle::reward, sim.cpp:146-152,
   // the reference); 1 = the PRM score of the thought (K4), awaited on device.
   int reward_prm;
+  // Split multi-GPU mode: this run is rank split_rank of the
+  // split_world query blocks of one job. Local query q is the job's query
+  // q + q_offset (its seed and golden label), the decode engine and clock are
+  // this rank's own, and T2 budget allocation is global through the ranks'
+  // outboxes (ctl_run.h split_exchange). split_world = 1: the single server.
+  int split_world, split_rank, q_offset, split_qmax;
+  i64 split_epoch;     // run id tagging the outbox flags (>= 1)
+  i64 xch_slot_bytes;  // bytes of one outbox slot
   int lex_rank[kMaxLabels];   // label index -> rank of "a<idx>" in std::map order
   int lex_order[kMaxLabels];  // rank -> label index
 };
@@ -207,6 +215,10 @@ SPEX_HD int budget_at(const Cfg& c, int depth) {
   if (depth >= 0 && depth < c.n_depth_widths) return c.depth_widths[depth];
   return c.width;
 }
+
+// split mode outboxes (ctl_run.h split_exchange): header bytes, most ranks
+constexpr int kXchHead = 64;
+constexpr int kMaxSplit = 64;
 
 struct QueryRun {
   u64 seed;
@@ -278,6 +290,8 @@ struct GState {
   int pad_dirty;
   i64 start_ns;   // device wall clock at the start of the run
   i64 reward_wait_ns;  // time the control spent waiting for PRM scores (reward_prm)
+  i64 xch_rounds;      // split mode: budget exchange rounds of this rank
+  i64 xch_wait_ns;     // split mode: time spent waiting for the other ranks
   // device cycle counters per phase (thread 0's view)
   i64 cyc[8];
 };
@@ -404,6 +418,8 @@ struct Run {
   int* al_out;
   int* al_rank;
   int* al_order;
+  // split mode: the ranks' outboxes (peer-mapped device pointers), [split_rank] own
+  char* const* xch;
   // host-built glibc log table for integer arguments (UCB)
   const double* log_tab;
   int log_tab_n;

@@ -63,6 +63,7 @@ struct TreeView {
   long long seg_cap;        // segment-pool capacity
   uint64_t run_seed;        // root prompts: query seeds (sim.cpp:177-180)
   int kv_pp_root;           // root prompts: static pages per query
+  int q_offset;             // root prompts: local query q is the job's q + q_offset (split mode)
   int node_cap;
   int prompt_tokens;
   int V;

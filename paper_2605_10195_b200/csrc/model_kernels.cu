@@ -217,7 +217,7 @@ __global__ void build_prompt_rows_kernel(TreeView t, int q0, int nq, RowDesc* ro
   const int j = i % P;
   const long long base = (long long)q * t.kv_pp_root * kPg;
   const uint64_t base_seed = d_splitmix64(t.run_seed ^ 0x7175657200000008ULL);  // ctl_math.h kSaltQuery
-  const uint64_t qv = (uint64_t)q + 1 + 0x9e3779b97f4a7c15ULL;                      // ctl_math.h hash_mix
+  const uint64_t qv = (uint64_t)(q + t.q_offset) + 1 + 0x9e3779b97f4a7c15ULL;                      // ctl_math.h hash_mix
   const uint64_t root_hash = d_splitmix64(d_splitmix64(base_seed ^ (qv + (base_seed << 6) + (base_seed >> 2))));
   Segment* s = segs + i;
   s->base = base;

@@ -21,6 +21,7 @@
 #include <cstring>
 #include <mutex>
 #include <sstream>
+#include <thread>
 #include <string>
 #include <unordered_map>
 #include <vector>
@@ -466,6 +467,11 @@ struct spex_executor {
   long long kv_pages = 0;           // pool pages of the last run
   int reward_prm = 0;               // reward source: 0 content oracle (reference), 1 PRM score
   std::vector<long long> finish_ns; // per-query device wall clock at query_done
+  // split mode (spex_executor_set_split): rank / world of the job's query blocks
+  int split_rank = 0, split_world = 1, split_qjob = 0;
+  long long split_epoch = 0;
+  std::vector<char*> split_boxes;   // the ranks' outboxes (device pointers; host memory in the emulation)
+  int node_cap0 = 0;                // initial node capacity (0: 512 or SPEX_NODE_CAP)
 #ifndef SPEX_EMU
   cudaStream_t stream = nullptr;
   cudaStream_t mstream = nullptr;
@@ -555,6 +561,13 @@ void pinned_release(void* p) {
 }
 #endif
 
+// split mode: query block [lo(r), lo(r + 1)) of rank r, its largest size and
+// the outbox geometry (ctl_run.h split_exchange)
+int split_block_lo(int q, int r, int w) { return static_cast<int>(static_cast<long long>(q) * r / w); }
+int split_qmax(int q, int w) { return (q + w - 1) / w; }
+long long split_slot_bytes(int qmax) { return (16 + 12LL * qmax + 15) / 16 * 16; }
+long long split_outbox_bytes(int qmax) { return kXchHead + 2 * split_slot_bytes(qmax); }
+
 void set_cfg(const spex_executor& ex, Cfg& c, int node_cap, int stream_cap, int log_cap,
              int stage_cap, int trace, int record_sched) {
   const HostConfig& h = ex.hc;
@@ -618,6 +631,12 @@ void set_cfg(const spex_executor& ex, Cfg& c, int node_cap, int stream_cap, int 
   c.reward_prm = ex.reward_prm;
   c.shard_lo = std::min(ex.shard_lo, h.n_queries);
   c.shard_hi = ex.shard_hi < 0 ? h.n_queries : std::min(ex.shard_hi, h.n_queries);
+  c.split_world = ex.split_world;
+  c.split_rank = ex.split_rank;
+  c.q_offset = ex.split_world > 1 ? split_block_lo(ex.split_qjob, ex.split_rank, ex.split_world) : 0;
+  c.split_qmax = ex.split_world > 1 ? split_qmax(ex.split_qjob, ex.split_world) : 0;
+  c.split_epoch = ex.split_epoch;
+  c.xch_slot_bytes = split_slot_bytes(c.split_qmax);
   c.sched_cap = record_sched ? 4 * stream_cap + 1024 : 1;
   c.sched_rows_cap = record_sched ? 64 * stream_cap + 4096 : 1;
   // std::map<std::string,...> order of "a0".."a{n-1}" (termination.hpp:39)
@@ -707,12 +726,14 @@ void layout(Arena& A, Run& R, int Q, int node_cap, int stream_cap, int log_cap, 
   A.add(R.sp_stack, SS);
   A.add(R.sp_dbl, 3 * SS);
   A.add(R.sp_int, 3 * SS);
+  // allocation scratch: in split mode it holds every rank's candidates
+  const size_t QA = static_cast<size_t>(std::max(Q, R.cfg.split_qmax * R.cfg.split_world)) + 64;
   A.add(R.al_cand, Q + 64);
-  A.add(R.al_score, Q + 64);
-  A.add(R.al_w, Q + 64);
-  A.add(R.al_out, Q + 64);
-  A.add(R.al_rank, Q + 64);
-  A.add(R.al_order, Q + 64);
+  A.add(R.al_score, QA);
+  A.add(R.al_w, QA);
+  A.add(R.al_out, QA);
+  A.add(R.al_rank, QA);
+  A.add(R.al_order, QA);
   A.mark_hot();  // everything above is touched every consumer iteration; below: log and model schedule
   A.add(R.log, static_cast<size_t>(log_cap));
   A.add(R.sched_kind, static_cast<size_t>(R.cfg.sched_cap));
@@ -933,6 +954,7 @@ void run_executor(spex_executor& ex, int trace) {
   const int Q = h.n_queries;
   int node_cap = 512;
   if (const char* e = std::getenv("SPEX_NODE_CAP")) node_cap = std::max(16, std::atoi(e));
+  if (ex.node_cap0 > 0) node_cap = ex.node_cap0;
   for (int attempt = 0; attempt < 4; ++attempt) {
     const long long sc = static_cast<long long>(Q) * (node_cap - 1) + 64;
     if (sc > (1LL << 30)) fail(ERR_CAP_STREAMS, "stream table too large");
@@ -968,6 +990,7 @@ void run_executor(spex_executor& ex, int trace) {
     }
     R.qs[0].admitted = 0;
     for (int q = 0; q < Q; ++q) R.qs[q].plan_empty_version = 0xffffffffu;
+    R.xch = ex.split_world > 1 ? ex.split_boxes.data() : nullptr;
     std::vector<int> sm(2048);
     std::vector<double> smd(64);
     std::vector<i64> sml(64);
@@ -1045,6 +1068,13 @@ void run_executor(spex_executor& ex, int trace) {
     CUDA_OK(cudaMemcpyAsync(d_tab, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice,
                             ex.stream));
     R.log_tab = d_tab;
+    char** d_xch = nullptr;
+    if (ex.split_world > 1) {
+      CUDA_OK(cudaMallocAsync(reinterpret_cast<void**>(&d_xch), sizeof(char*) * ex.split_world, ex.stream));
+      CUDA_OK(cudaMemcpyAsync(d_xch, ex.split_boxes.data(), sizeof(char*) * ex.split_world, cudaMemcpyHostToDevice,
+                              ex.stream));
+      R.xch = d_xch;
+    }
     // streaming schedule: head + entries in pinned, device-mapped host memory
     const bool streaming = ex.with_model && !std::getenv("SPEX_SEQUENTIAL");
     PubHead* h_head = nullptr;
@@ -1080,6 +1110,7 @@ void run_executor(spex_executor& ex, int trace) {
       if (d_kvpt) cudaFreeAsync(d_kvpt, ex.stream);
       if (d_kvfree) cudaFreeAsync(d_kvfree, ex.stream);
       cudaFreeAsync(d_tab, ex.stream);
+      if (d_xch) cudaFreeAsync(d_xch, ex.stream);
       cudaFreeAsync(d_run, ex.stream);
       cudaStreamSynchronize(ex.stream);
       if (h_head) pinned_release(h_head);
@@ -1096,6 +1127,7 @@ void run_executor(spex_executor& ex, int trace) {
       sv.node_score = R.cfg.reward_prm ? R.n_score : nullptr;
       sv.prm_done = R.cfg.reward_prm ? R.prm_done : nullptr;
       sv.tree.kv_pp_root = R.cfg.kv_pp_root;
+      sv.tree.q_offset = R.cfg.q_offset;
       sv.tree.st_q = R.st_q;
       sv.tree.st_node = R.st_node;
       sv.tree.node_cap = node_cap;
@@ -1236,6 +1268,15 @@ void run_executor(spex_executor& ex, int trace) {
       for (auto& m : ex.host_marks) std::fprintf(stderr, "[spex timing] %-20s %10.2f ms\n", m.first, m.second);
     }
 #endif
+    if (ex.split_world > 1 && (ex.g.error == ERR_CAP_NODES || ex.g.error == ERR_CAP_STAGE)) {
+      // a rank cannot rerun alone (its budget rounds pair with the others'):
+      // every rank reruns, with a new epoch and this capacity (spex_split_run,
+      // split.run_split_rank)
+      ex.node_cap0 = node_cap * 2;
+      fail(ex.g.error, "split rank " + std::to_string(ex.split_rank) + ": node capacity " +
+                           std::to_string(node_cap) + " exhausted; rerun every rank with node capacity " +
+                           std::to_string(node_cap * 2));
+    }
     if (ex.g.error == ERR_CAP_NODES || ex.g.error == ERR_CAP_STAGE) {
       node_cap *= 2;  // capacity, not semantics: rerun with a larger arena
       ex.log.clear();
@@ -1337,6 +1378,90 @@ bool run_batch_device(std::vector<spex_executor*>& exs, int device, cudaStream_t
   cudaFreeAsync(d_tab, st);
   cudaStreamSynchronize(st);
   return ok;
+}
+
+// The ranks of one split job on ONE device, CTA r = rank r of one launch of
+// the control kernel (co-resident: the exchange spins on the other ranks), the
+// outboxes in one allocation. Control only; with the event logs when `trace`.
+// Returns the first rank error (0: all ran).
+int run_group_device(std::vector<spex_executor*>& exs, int device, int trace, int node_cap, float* ms_out) {
+  const int n = static_cast<int>(exs.size());
+  CUDA_OK(cudaSetDevice(device));
+  cudaStream_t st = nullptr;
+  CUDA_OK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  const int nthreads = exs[0]->nthreads, nwarps = nthreads / 32;
+  std::vector<double>& tab = log_table();
+  const long long box = split_outbox_bytes(split_qmax(exs[0]->split_qjob, n));
+  std::vector<Run> runs(n);
+  std::vector<Arena> arenas(n);
+  std::vector<size_t> at(n + 1, 0);
+  int qmax = 0;
+  for (int b = 0; b < n; ++b) {
+    Run& R = runs[b];
+    R = Run{};
+    spex_executor& ex = *exs[b];
+    const int Q = ex.hc.n_queries;
+    qmax = std::max(qmax, Q);
+    const int stream_cap = static_cast<int>(static_cast<long long>(Q) * (node_cap - 1) + 64);
+    const long long lc = trace ? static_cast<long long>(Q) * node_cap * 6 + 64 : 64;
+    if (lc > (1LL << 31) - 1) fail(ERR_CAP_LOG, "log too large");
+    ex.record_sched = 0;
+    set_cfg(ex, R.cfg, node_cap, stream_cap, static_cast<int>(lc), std::max(512, node_cap), trace, 0);
+    layout(arenas[b], R, Q, node_cap, stream_cap, static_cast<int>(lc), nthreads, std::max(512, node_cap));
+    R.nwarps = nwarps;
+    R.log_tab_n = static_cast<int>(tab.size());
+    at[b + 1] = at[b] + ((arenas[b].total + 255) & ~size_t(255));
+  }
+  const size_t tab_off = at[n];
+  const size_t box_off = tab_off + ((tab.size() * sizeof(double) + 255) & ~size_t(255));
+  const size_t ptr_off = box_off + static_cast<size_t>(box) * n;
+  const size_t total = ptr_off + sizeof(char*) * n + 256;
+  char* big = nullptr;
+  CUDA_OK(cudaMallocAsync(reinterpret_cast<void**>(&big), total, st));
+  CUDA_OK(cudaMemsetAsync(big, 0, total, st));
+  CUDA_OK(cudaMemcpyAsync(big + tab_off, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice, st));
+  std::vector<char*> boxes(n);
+  for (int b = 0; b < n; ++b) boxes[b] = big + box_off + static_cast<size_t>(box) * b;
+  CUDA_OK(cudaMemcpyAsync(big + ptr_off, boxes.data(), sizeof(char*) * n, cudaMemcpyHostToDevice, st));
+  for (int b = 0; b < n; ++b) {
+    arenas[b].carve(big + at[b]);
+    runs[b].log_tab = reinterpret_cast<double*>(big + tab_off);
+    runs[b].xch = reinterpret_cast<char**>(big + ptr_off);
+  }
+  Run* d_runs = nullptr;
+  CUDA_OK(cudaMallocAsync(reinterpret_cast<void**>(&d_runs), sizeof(Run) * n, st));
+  CUDA_OK(cudaMemcpyAsync(d_runs, runs.data(), sizeof(Run) * n, cudaMemcpyHostToDevice, st));
+  cudaEvent_t ca, cb;
+  cudaEventCreate(&ca);
+  cudaEventCreate(&cb);
+  const int lr = spex_launch_control_batch_async(d_runs, n, qmax, nthreads, st, ca, cb);
+  if (lr != 0) fail(200, std::string("control kernel launch failed: ") + cudaGetErrorString(static_cast<cudaError_t>(lr)));
+  CUDA_OK(cudaEventSynchronize(cb));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, ca, cb);
+  cudaEventDestroy(ca);
+  cudaEventDestroy(cb);
+  if (ms_out) *ms_out = ms;
+  int err = 0;
+  for (int b = 0; b < n; ++b) {
+    spex_executor& ex = *exs[b];
+    const int Q = ex.hc.n_queries;
+    CUDA_OK(cudaMemcpyAsync(&ex.g, runs[b].g, sizeof(GState), cudaMemcpyDeviceToHost, st));
+    ex.qs.resize(Q);
+    CUDA_OK(cudaMemcpyAsync(ex.qs.data(), runs[b].qs, sizeof(QueryRun) * Q, cudaMemcpyDeviceToHost, st));
+    CUDA_OK(cudaStreamSynchronize(st));
+    if (trace && ex.g.log_n > 0) {
+      ex.log.resize(ex.g.log_n);
+      CUDA_OK(cudaMemcpyAsync(ex.log.data(), runs[b].log, sizeof(Rec) * ex.g.log_n, cudaMemcpyDeviceToHost, st));
+    }
+    ex.device_ms = ms;
+    if (ex.g.error != 0 && err == 0) err = ex.g.error;
+  }
+  cudaFreeAsync(big, st);
+  cudaFreeAsync(d_runs, st);
+  cudaStreamSynchronize(st);
+  cudaStreamDestroy(st);
+  return err;
 }
 #endif
 
@@ -1507,6 +1632,167 @@ int spex_executor_set_shard(spex_executor* ex, int rank, int world) {
     const long long Q = ex->hc.n_queries;
     ex->shard_lo = static_cast<int>(Q * rank / world);
     ex->shard_hi = static_cast<int>(Q * (rank + 1) / world);
+  });
+}
+
+long long spex_split_outbox_bytes(int n_queries_job, int world) {
+  if (world < 1 || world > kMaxSplit || n_queries_job < world) return -1;
+  return split_outbox_bytes(split_qmax(n_queries_job, world));
+}
+
+int spex_executor_set_split(spex_executor* ex, int rank, int world, void* const* outboxes, long long epoch) {
+  return guarded([&] {
+    if (ex->ran) fail(ERR_INVALID_ARGUMENT, "set_split: executor already ran");
+    if (world < 1 || world > kMaxSplit || rank < 0 || rank >= world)
+      fail(ERR_INVALID_ARGUMENT, "set_split: need 0 <= rank < world <= " + std::to_string(kMaxSplit));
+    if (ex->shard_lo != 0 || ex->shard_hi >= 0) fail(ERR_INVALID_ARGUMENT, "set_split: executor has a coupled shard");
+    const int qjob = ex->split_world > 1 ? ex->split_qjob : ex->hc.n_queries;
+    if (qjob < world) fail(ERR_INVALID_ARGUMENT, "set_split: fewer queries than ranks");
+    if (world > 1 && (!outboxes || epoch < 1)) fail(ERR_INVALID_ARGUMENT, "set_split: need the outboxes and epoch >= 1");
+    if (world > 1 && epoch >= (1LL << 31)) fail(ERR_INVALID_ARGUMENT, "set_split: epoch out of range");
+    ex->split_rank = rank;
+    ex->split_world = world;
+    ex->split_qjob = qjob;
+    ex->split_epoch = epoch;
+    ex->split_boxes.clear();
+    for (int r = 0; world > 1 && r < world; ++r) ex->split_boxes.push_back(static_cast<char*>(outboxes[r]));
+    // the rank's executor is the reference Executor over its block (n_queries = block size)
+    ex->hc.n_queries = split_block_lo(qjob, rank + 1, world) - split_block_lo(qjob, rank, world);
+    ex->cfg_dump = to_json(ex->hc, ex->t1, ex->t2, ex->t3).dump();
+  });
+}
+
+int spex_split_run(const char* config_json, uint64_t seed, const char* flags_csv, int world, int device, int trace,
+                   spex_executor** out) {
+  return guarded([&] {
+    if (world < 1 || world > kMaxSplit) fail(ERR_INVALID_ARGUMENT, "split_run: world out of range");
+    int node_cap = 512;
+    if (const char* e = std::getenv("SPEX_NODE_CAP")) node_cap = std::max(16, std::atoi(e));
+    for (int attempt = 0;; ++attempt) {
+      std::vector<spex_executor*> exs;
+      auto free_all = [&] {
+        for (auto* e : exs) spex_executor_destroy(e);
+        exs.clear();
+      };
+      const HostConfig hc = parse_config(config_json);
+      const long long box = world > 1 ? spex_split_outbox_bytes(hc.n_queries, world) : 0;
+      if (box < 0) fail(ERR_INVALID_ARGUMENT, "split_run: fewer queries than ranks");
+      std::vector<char> host_boxes(static_cast<size_t>(box) * world + 64, 0);
+      std::vector<void*> boxes(world, nullptr);
+      for (int r = 0; r < world; ++r) boxes[r] = host_boxes.data() + box * r;  // emulation; the device runner has its own
+      for (int r = 0; r < world; ++r) {
+        spex_executor* e = nullptr;
+        int rc = spex_executor_create(config_json, seed, flags_csv, device, &e);
+        if (!rc) {
+          exs.push_back(e);
+          rc = spex_executor_set_split(e, r, world, boxes.data(), 1);
+        }
+        if (rc) {
+          const std::string m = g_err;
+          free_all();
+          fail(rc, m);
+        }
+        e->node_cap0 = node_cap;
+      }
+      int err = 0;
+#ifdef SPEX_EMU
+      std::vector<std::thread> th;
+      std::vector<int> rc(world, 0);
+      std::vector<std::string> msg(world);
+      for (int r = 0; r < world; ++r)
+        th.emplace_back([&, r] {
+          try {
+            run_executor(*exs[r], trace);
+          } catch (const SpexError& e) {
+            rc[r] = e.code;
+            msg[r] = e.what;
+          } catch (const std::exception& e) {
+            rc[r] = ERR_INTERNAL;
+            msg[r] = e.what();
+          }
+        });
+      for (auto& t : th) t.join();
+      for (int r = 0; r < world && !err; ++r)
+        if (rc[r]) err = rc[r];
+      std::string first_msg;
+      for (int r = 0; r < world; ++r)
+        if (rc[r] && first_msg.empty()) first_msg = msg[r];
+#else
+      float ms = 0.f;
+      try {
+        err = run_group_device(exs, device, trace, node_cap, &ms);
+      } catch (...) {
+        free_all();
+        throw;
+      }
+      const std::string first_msg = "device control error";
+#endif
+      if ((err == ERR_CAP_NODES || err == ERR_CAP_STAGE) && attempt < 3) {
+        free_all();
+        node_cap *= 2;  // every rank reruns with the larger arena
+        continue;
+      }
+      if (err) {
+        free_all();
+        fail(err, "split_run: " + first_msg);
+      }
+      for (int r = 0; r < world; ++r) {
+        exs[r]->ran = true;
+        out[r] = exs[r];
+      }
+      return;
+    }
+  });
+}
+
+#ifndef SPEX_EMU
+int spex_split_outbox_alloc(int device, long long bytes, void** dptr, unsigned char* ipc_handle) {
+  return guarded([&] {
+    CUDA_OK(cudaSetDevice(device));
+    void* p = nullptr;
+    CUDA_OK(cudaMalloc(&p, static_cast<size_t>(bytes)));
+    CUDA_OK(cudaMemset(p, 0, static_cast<size_t>(bytes)));
+    CUDA_OK(cudaDeviceSynchronize());
+    if (ipc_handle) {
+      cudaIpcMemHandle_t h;
+      CUDA_OK(cudaIpcGetMemHandle(&h, p));
+      std::memcpy(ipc_handle, &h, sizeof(h));
+    }
+    *dptr = p;
+  });
+}
+
+int spex_split_outbox_open(int device, const unsigned char* ipc_handle, void** dptr) {
+  return guarded([&] {
+    CUDA_OK(cudaSetDevice(device));
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, ipc_handle, sizeof(h));
+    CUDA_OK(cudaIpcOpenMemHandle(dptr, h, cudaIpcMemLazyEnablePeerAccess));
+  });
+}
+
+int spex_split_outbox_close(void* dptr) {
+  return guarded([&] { CUDA_OK(cudaIpcCloseMemHandle(dptr)); });
+}
+
+int spex_split_outbox_free(void* dptr) {
+  return guarded([&] { CUDA_OK(cudaFree(dptr)); });
+}
+#else
+int spex_split_outbox_alloc(int, long long, void**, unsigned char*) {
+  return guarded([&] { fail(ERR_INVALID_ARGUMENT, "outboxes need the CUDA build"); });
+}
+int spex_split_outbox_open(int, const unsigned char*, void**) {
+  return guarded([&] { fail(ERR_INVALID_ARGUMENT, "outboxes need the CUDA build"); });
+}
+int spex_split_outbox_close(void*) { return 0; }
+int spex_split_outbox_free(void*) { return 0; }
+#endif
+
+int spex_executor_split_stats(spex_executor* ex, long long* rounds, double* wait_ms) {
+  return guarded([&] {
+    if (rounds) *rounds = ex->g.xch_rounds;
+    if (wait_ms) *wait_ms = ex->g.xch_wait_ns * 1e-6;
   });
 }
 

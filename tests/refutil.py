@@ -140,3 +140,48 @@ def random_configs(n=60, seed=2026):
                        "max_producers": rng.choice([4, 16, 64])}}
         out.append((f"rand{i}-{fam}", json.dumps(cfg), rng.randint(1, 10000), rng.choice(flagsets)))
     return out
+
+
+REF_SPLIT_SO = ROOT / "oracle" / "_ref" / "libspexref_split.so"
+_ref_split = None
+
+
+def ref_split_lib():
+    """The split mode's oracle (oracle/ref_split.cpp): the reference's executor,
+    one thread per rank, coupled by the T2 budget exchange."""
+    global _ref_split
+    if _ref_split is None:
+        if not REF_SPLIT_SO.exists():
+            return None
+        L = ctypes.CDLL(str(REF_SPLIT_SO))
+        L.ref_split_run_log.argtypes = [ctypes.c_char_p, ctypes.c_uint64, ctypes.c_char_p, ctypes.c_int, ctypes.c_int,
+                                        ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(ctypes.c_double),
+                                        ctypes.POINTER(ctypes.c_longlong)]
+        L.ref_split_last_error.restype = ctypes.c_char_p
+        _ref_split = L
+    return _ref_split
+
+
+def ref_split_log(cfg: str, seed: int, flags: str | None, world: int) -> tuple:
+    """(rank logs, rank exchange rounds) of one split job."""
+    L = ref_split_lib()
+    logs = (ctypes.c_char_p * world)()
+    tot = (ctypes.c_double * (24 * world))()
+    rounds = (ctypes.c_longlong * world)()
+    rc = L.ref_split_run_log(cfg.encode(), seed, None if flags is None else flags.encode(), world, 1, logs, tot,
+                             rounds)
+    if rc != 0:
+        raise RuntimeError(f"split reference failed rc={rc}: {L.ref_split_last_error().decode()}")
+    return [logs[r].decode().splitlines() for r in range(world)], list(rounds)
+
+
+def split_configs():
+    """T2 configs of every family for the split mode (the exchange only runs
+    with T2): queued admission, several widths / noise levels, 12-40 queries."""
+    out = []
+    for fam in ("rstar_dfs", "rest_hybrid", "rebase_bfs"):
+        for fl, q, bs, seed in (("t1,t2", 12, 12, 1), ("t1,t2,t3", 24, 8, 2), ("t1,t2,t3", 40, 40, 5)):
+            cfg = {"family": fam, "policy": {"width": 4, "max_depth": 10, "target_answers": 6},
+                   "workload": {"noise_sigma": 0.05}, "run": {"batch_size": bs, "n_queries": q, "max_producers": 24}}
+            out.append((f"{fam}-{fl.replace(',', '')}-q{q}-s{seed}", json.dumps(cfg), seed, fl))
+    return out
