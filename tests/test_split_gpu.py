@@ -28,9 +28,12 @@ def _digest(lines):
     return hashlib.sha256("\n".join(lines).encode()).hexdigest()
 
 
+CASES = [(n, w) for n in ("c1_rebase_w4_q16", "c3_rstar_w4_q512") for w in (1, 2, 3, 4, 8)]
+CASES += [("c3_rstar_w4_q512_t1t3", 8)]  # the literal config 3 (no T2: blocks without exchange)
+
+
 @needs_oracle
-@pytest.mark.parametrize("W", [1, 2, 3, 4, 8])
-@pytest.mark.parametrize("name", ["c1_rebase_w4_q16", "c3_rstar_w4_q512", "c3_rstar_w4_q512_t1t3"])
+@pytest.mark.parametrize("name,W", CASES)
 def test_split_matches_oracle(name, W):
     cfg = (CFG / f"{name}.json").read_text()
     ref, rounds = refutil.ref_split_log(cfg, 1, None, W)
@@ -96,6 +99,7 @@ def _rank_main(rank, world, port, cfg, seed, out_dir, model):
             ex = spex.Executor(cfg, seed, None, trace=True)
             if model:
                 ex.set_model("small_policy", "small_prm", 1)
+                ex.set_kv_pages(1 << 15)  # two processes share this GPU
             ex.set_split(rank, world, boxes.pointers, epoch)
             dist.barrier()
             ex.run()
