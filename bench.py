@@ -55,10 +55,13 @@ def parse():
     ap.add_argument("--policy", default="mid_policy")
     ap.add_argument("--prm", default="mid_prm")
     ap.add_argument("--cpu-sample-runs", type=int, default=4)
-    ap.add_argument("--sharding", default="independent", choices=["independent", "coupled"],
-                    help="independent: each rank a whole search of its own queries (run seed + rank, weak "
-                         "scaling); coupled: ONE search, the control replicated on every rank and the model "
-                         "work of query block r on rank r (single virtual clock, global T2; strong scaling)")
+    ap.add_argument("--sharding", default="split", choices=["split", "independent", "coupled"],
+                    help="split (north_star): ONE job of n_queries x N queries, rank r owns query block r with "
+                         "its own engine and clock, T2 budgets allocated over every rank's candidates through "
+                         "peer-memory outboxes (weak scaling: per-GPU queries fixed); independent: each rank a "
+                         "whole search of its own queries (run seed + rank, weak scaling, no exchange); coupled: "
+                         "ONE search, the control replicated on every rank and the model work of query block r "
+                         "on rank r (single virtual clock, global T2; strong scaling)")
     ap.add_argument("--control-only", type=int, default=296,
                     help="also time N control-only searches in one batched launch (no model), 0 = off")
     ap.add_argument("--named-shapes", type=int, default=1,
@@ -220,10 +223,17 @@ def main():
     cfg = json.loads(cfg_text)
     base_seed = cfg["run"]["seed"]
     coupled = args.sharding == "coupled"
+    split = args.sharding == "split" and world > 1
     # independent: disjoint query sets per rank (weak scaling); coupled: one
-    # search whose query blocks' model work is split over the ranks
-    seed = base_seed if coupled else shard_seed(base_seed, rank)
+    # search whose query blocks' model work is split over the ranks; split: one
+    # job of n_queries x world queries, rank r owning block r (weak scaling)
+    seed = base_seed if (coupled or split) else shard_seed(base_seed, rank)
     q_lo, q_hi = query_block(cfg["run"]["n_queries"], rank, world) if coupled else (0, cfg["run"]["n_queries"])
+    job_text = cfg_text
+    if split:
+        job = json.loads(cfg_text)
+        job["run"]["n_queries"] = cfg["run"]["n_queries"] * world
+        job_text = json.dumps(job)
     if args.impl == "reference":
         run_reference(args, cfg_text, base_seed, rank, world)
         return
@@ -242,11 +252,19 @@ def main():
         if pg:
             pg.barrier()
 
+    boxes, epoch = None, [0]
+    if split:
+        from paper_2605_10195_b200 import _lib, shard
+        boxes = shard.Outboxes(_lib.lib(), rank, world, cfg["run"]["n_queries"] * world, device=local)
+
     def one_search(trace: bool, flags=None):
-        ex = spex.Executor(cfg_text, seed, flags, trace=trace, device=local)
+        ex = spex.Executor(job_text, seed, flags, trace=trace, device=local)
         ex.set_model(args.policy, args.prm, weight_seed=1)
         if coupled:
             ex.set_shard(rank, world)
+        if split:
+            epoch[0] += 1  # the same on every rank: every rank runs the same searches
+            ex.set_split(rank, world, boxes.pointers, epoch[0])
         tot = ex.run()
         tot.queries = q_hi - q_lo  # queries whose model work ran here
         d2h = 0
@@ -461,7 +479,9 @@ def main():
                    "queries_per_step_per_gpu": cfg["run"]["n_queries"],
                    "l2": "inputs larger than L2 (tree KV pools of tens of GB per search)",
                    "parallelism": (f"query-block model work x{world}, search replicated (single virtual clock)"
-                                   if coupled else f"query-sharded x{world}")},
+                                   if coupled else
+                                   f"query-sharded x{world}, one job, T2 budget exchange between the control "
+                                   f"kernels through peer-memory outboxes" if split else f"query-sharded x{world}")},
         "e2e": {"value": total_e2e_q / e2e_wall, "unit": "queries/s",
                 "h2d_bytes_per_step": len(cfg_text.encode()),
                 "d2h_bytes_per_step": 256 + 256 * cfg["run"]["n_queries"],

@@ -185,6 +185,8 @@ int spex_executor_set_shard(spex_executor* ex, int rank, int world);
  *                             out[world] with executors that have run (logs,
  *                             totals, stats; destroy each).
  *   spex_executor_split_stats exchange rounds and the time spent waiting.
+ *   spex_executor_emulate_split  one rank with its model, the others beside it
+ *                             on the same device (per-rank timing on one GPU).
  * Oracle: oracle/ref_split.cpp (the reference's executor, one thread per rank,
  * coupled by the same exchange). */
 long long spex_split_outbox_bytes(int n_queries_job, int world);
@@ -196,6 +198,14 @@ int spex_executor_set_split(spex_executor* ex, int rank, int world, void* const*
 int spex_split_run(const char* config_json, uint64_t seed, const char* flags_csv, int world, int device, int trace,
                    spex_executor** out);
 int spex_executor_split_stats(spex_executor* ex, long long* rounds, double* wait_ms);
+/* Single-GPU emulation of one rank of a `world`-GPU split job: this executor
+ * runs rank `rank` (with its model, if attached) while the other ranks'
+ * control kernels run beside it on the same device (CTAs of one launch,
+ * control only), exchanging through outboxes in this device's memory. The
+ * exchange is timing-independent, so the rank's decisions, log and model work
+ * are those of the multi-GPU run; its step time is the multi-GPU one up to the
+ * world - 1 SMs the other ranks' control occupies. */
+int spex_executor_emulate_split(spex_executor* ex, int rank, int world);
 int spex_executor_model_stats(spex_executor* ex, spex_model_stats* out);
 /* Tree-KV pool size in pages (0 = the default: the resident pools, else 62%
  * of free HBM). Pages of dead thoughts (pruned, REBASE layers expanded,

@@ -194,6 +194,12 @@ class Executor:
         arr = (ctypes.c_void_p * int(world))(*outboxes)
         _check(self._L.spex_executor_set_split(self._h, int(rank), int(world), arr, int(epoch)))
 
+    def emulate_split(self, rank: int, world: int) -> None:
+        """One GPU standing in for ``world``: this executor runs rank ``rank``
+        (model included) while the other ranks' control runs beside it on the
+        same device; decisions and this rank's work are the multi-GPU run's."""
+        _check(self._L.spex_executor_emulate_split(self._h, int(rank), int(world)))
+
     def split_stats(self) -> dict:
         r, w = ctypes.c_longlong(), ctypes.c_double()
         _check(self._L.spex_executor_split_stats(self._h, ctypes.byref(r), ctypes.byref(w)))

@@ -146,6 +146,7 @@ _EXPORTS = {
     "spex_split_run": (
         [ctypes.c_char_p, ctypes.c_uint64, ctypes.c_char_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
          ctypes.POINTER(ctypes.c_void_p)], ctypes.c_int),
+    "spex_executor_emulate_split": ([ctypes.c_void_p, ctypes.c_int, ctypes.c_int], ctypes.c_int),
     "spex_executor_split_stats": (
         [ctypes.c_void_p, ctypes.POINTER(ctypes.c_longlong), ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
     "spex_executor_model_stats": ([ctypes.c_void_p, ctypes.POINTER(ModelStats)], ctypes.c_int),

@@ -472,6 +472,9 @@ struct spex_executor {
   long long split_epoch = 0;
   std::vector<char*> split_boxes;   // the ranks' outboxes (device pointers; host memory in the emulation)
   int node_cap0 = 0;                // initial node capacity (0: 512 or SPEX_NODE_CAP)
+  int split_emulate = 0;            // spex_executor_emulate_split: the other ranks run beside this one
+  std::string cfg_text, flags_text; // as created (the emulated ranks' executors)
+  char* emu_boxes = nullptr;        // the emulation's outboxes (device)
 #ifndef SPEX_EMU
   cudaStream_t stream = nullptr;
   cudaStream_t mstream = nullptr;
@@ -935,6 +938,15 @@ void kv_configure(spex_executor& ex, Cfg& c, long long pages) {
 // independent Executors are (experiment.cpp:61-78).
 std::mutex g_model_mu;
 
+#ifndef SPEX_EMU
+struct GroupLaunch;
+void group_launch(GroupLaunch& G, std::vector<spex_executor*>& exs, int device, int trace, int node_cap,
+                  const std::vector<char*>* ext);
+int group_finish(GroupLaunch& G, std::vector<spex_executor*>& exs, int trace, float* ms_out);
+GroupLaunch* group_new();
+void group_delete(GroupLaunch* G);
+#endif
+
 void run_executor(spex_executor& ex, int trace) {
   const HostConfig& h = ex.hc;
 #ifndef SPEX_EMU
@@ -1026,6 +1038,36 @@ void run_executor(spex_executor& ex, int trace) {
       ex.host_marks.emplace_back(nm, std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tm0).count());
     };
     CUDA_OK(cudaSetDevice(ex.device));
+    // single-GPU split emulation: the other ranks' control runs beside this
+    // one (CTAs of one launch), exchanging through outboxes on this device
+    std::vector<spex_executor*> peers;
+    GroupLaunch* peer_group = nullptr;
+    auto launch_peers = [&] {
+      if (!ex.split_emulate) return;
+      for (int r = 0; r < ex.split_world; ++r) {
+        if (r == ex.split_rank) continue;
+        spex_executor* p = nullptr;
+        std::vector<void*> bx(ex.split_boxes.begin(), ex.split_boxes.end());
+        if (spex_executor_create(ex.cfg_text.c_str(), ex.run_seed, ex.flags_text.empty() ? nullptr : ex.flags_text.c_str(),
+                                 ex.device, &p) ||
+            (peers.push_back(p), spex_executor_set_split(p, r, ex.split_world, bx.data(), ex.split_epoch)))
+          fail(ERR_INTERNAL, "split emulation: peer rank setup failed: " + g_err);
+      }
+      peer_group = group_new();
+      group_launch(*peer_group, peers, ex.device, 0, node_cap, &ex.split_boxes);
+    };
+    auto finish_peers = [&]() -> int {
+      int e = 0;
+      if (peer_group) {
+        e = group_finish(*peer_group, peers, 0, nullptr);
+        group_delete(peer_group);
+        peer_group = nullptr;
+      }
+      for (auto* p : peers) spex_executor_destroy(p);
+      peers.clear();
+      return e;
+    };
+    int peer_err = 0;
     if (!ex.stream) CUDA_OK(cudaStreamCreateWithFlags(&ex.stream, cudaStreamNonBlocking));
     if (!ex.mstream) CUDA_OK(cudaStreamCreateWithFlags(&ex.mstream, cudaStreamNonBlocking));
     keep_pool_memory(ex.device);
@@ -1106,6 +1148,7 @@ void run_executor(spex_executor& ex, int trace) {
     CUDA_OK(cudaMallocAsync(reinterpret_cast<void**>(&d_run), sizeof(Run), ex.stream));
     CUDA_OK(cudaMemcpyAsync(d_run, &R, sizeof(Run), cudaMemcpyHostToDevice, ex.stream));
     auto cleanup = [&] {
+      finish_peers();
       cudaFreeAsync(base, ex.stream);
       if (d_kvpt) cudaFreeAsync(d_kvpt, ex.stream);
       if (d_kvfree) cudaFreeAsync(d_kvfree, ex.stream);
@@ -1176,6 +1219,7 @@ void run_executor(spex_executor& ex, int trace) {
       sv.pub_entries = h_ents;
       alloc_outputs(static_cast<long long>(Q) * node_cap * 64);
       mark("pre-launch");
+      launch_peers();
       int lr = spex_launch_control_async(d_run, Q, ex.nthreads, ex.stream, ca, cb);
       if (lr != 0) {
         cleanup();
@@ -1193,6 +1237,7 @@ void run_executor(spex_executor& ex, int trace) {
         fail(201, std::string("model forward: ") + e.what());
       }
     } else {
+      launch_peers();
       int lr = spex_launch_control_async(d_run, Q, ex.nthreads, ex.stream, ca, cb);
       if (lr != 0) {
         cleanup();
@@ -1200,6 +1245,7 @@ void run_executor(spex_executor& ex, int trace) {
       }
     }
     CUDA_OK(cudaEventSynchronize(cb));
+    peer_err = finish_peers();
     mark("control-done");
     float ms = 0.f;
     cudaEventElapsedTime(&ms, ca, cb);
@@ -1266,6 +1312,19 @@ void run_executor(spex_executor& ex, int trace) {
     mark("cleanup");
     if (std::getenv("SPEX_TIMING")) {
       for (auto& m : ex.host_marks) std::fprintf(stderr, "[spex timing] %-20s %10.2f ms\n", m.first, m.second);
+    }
+#endif
+#ifndef SPEX_EMU
+    if (ex.split_emulate) {
+      const bool cap = ex.g.error == ERR_CAP_NODES || ex.g.error == ERR_CAP_STAGE || peer_err == ERR_CAP_NODES ||
+                       peer_err == ERR_CAP_STAGE;
+      if (cap) {
+        node_cap *= 2;  // every rank reruns, a new epoch on the same outboxes
+        ex.split_epoch += 1;
+        ex.log.clear();
+        continue;
+      }
+      if (peer_err) fail(peer_err, "split emulation: a peer rank failed");
     }
 #endif
     if (ex.split_world > 1 && (ex.g.error == ERR_CAP_NODES || ex.g.error == ERR_CAP_STAGE)) {
@@ -1381,24 +1440,35 @@ bool run_batch_device(std::vector<spex_executor*>& exs, int device, cudaStream_t
 }
 
 // The ranks of one split job on ONE device, CTA r = rank r of one launch of
-// the control kernel (co-resident: the exchange spins on the other ranks), the
-// outboxes in one allocation. Control only; with the event logs when `trace`.
-// Returns the first rank error (0: all ran).
-int run_group_device(std::vector<spex_executor*>& exs, int device, int trace, int node_cap, float* ms_out) {
-  const int n = static_cast<int>(exs.size());
-  CUDA_OK(cudaSetDevice(device));
+// the control kernel (co-resident: the exchange spins on the other ranks).
+// Control only; with the event logs when `trace`. The outboxes are `ext`
+// (device pointers, [rank] per executor's split_rank) or W fresh ones in the
+// launch's allocation. group_launch returns with the kernel running on its
+// own stream; group_finish waits and returns the first rank error (0: all ran).
+struct GroupLaunch {
   cudaStream_t st = nullptr;
-  CUDA_OK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  char* big = nullptr;
+  Run* d_runs = nullptr;
+  std::vector<Run> runs;
+  cudaEvent_t ca = nullptr, cb = nullptr;
+};
+
+void group_launch(GroupLaunch& G, std::vector<spex_executor*>& exs, int device, int trace, int node_cap,
+                  const std::vector<char*>* ext) {
+  const int n = static_cast<int>(exs.size());
+  const int world = exs[0]->split_world;
+  CUDA_OK(cudaSetDevice(device));
+  CUDA_OK(cudaStreamCreateWithFlags(&G.st, cudaStreamNonBlocking));
+  cudaStream_t st = G.st;
   const int nthreads = exs[0]->nthreads, nwarps = nthreads / 32;
   std::vector<double>& tab = log_table();
-  const long long box = split_outbox_bytes(split_qmax(exs[0]->split_qjob, n));
-  std::vector<Run> runs(n);
+  const long long box = world > 1 ? split_outbox_bytes(split_qmax(exs[0]->split_qjob, world)) : 0;
+  G.runs.assign(n, Run{});
   std::vector<Arena> arenas(n);
   std::vector<size_t> at(n + 1, 0);
   int qmax = 0;
   for (int b = 0; b < n; ++b) {
-    Run& R = runs[b];
-    R = Run{};
+    Run& R = G.runs[b];
     spex_executor& ex = *exs[b];
     const int Q = ex.hc.n_queries;
     qmax = std::max(qmax, Q);
@@ -1414,54 +1484,67 @@ int run_group_device(std::vector<spex_executor*>& exs, int device, int trace, in
   }
   const size_t tab_off = at[n];
   const size_t box_off = tab_off + ((tab.size() * sizeof(double) + 255) & ~size_t(255));
-  const size_t ptr_off = box_off + static_cast<size_t>(box) * n;
-  const size_t total = ptr_off + sizeof(char*) * n + 256;
-  char* big = nullptr;
-  CUDA_OK(cudaMallocAsync(reinterpret_cast<void**>(&big), total, st));
-  CUDA_OK(cudaMemsetAsync(big, 0, total, st));
-  CUDA_OK(cudaMemcpyAsync(big + tab_off, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice, st));
-  std::vector<char*> boxes(n);
-  for (int b = 0; b < n; ++b) boxes[b] = big + box_off + static_cast<size_t>(box) * b;
-  CUDA_OK(cudaMemcpyAsync(big + ptr_off, boxes.data(), sizeof(char*) * n, cudaMemcpyHostToDevice, st));
+  const size_t ptr_off = box_off + (ext ? 0 : static_cast<size_t>(box) * world);
+  const size_t total = ptr_off + sizeof(char*) * std::max(world, 1) + 256;
+  CUDA_OK(cudaMallocAsync(reinterpret_cast<void**>(&G.big), total, st));
+  CUDA_OK(cudaMemsetAsync(G.big, 0, total, st));
+  CUDA_OK(cudaMemcpyAsync(G.big + tab_off, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice, st));
+  std::vector<char*> boxes(world);
+  for (int r = 0; r < world; ++r) boxes[r] = ext ? (*ext)[r] : G.big + box_off + static_cast<size_t>(box) * r;
+  if (world > 1)
+    CUDA_OK(cudaMemcpyAsync(G.big + ptr_off, boxes.data(), sizeof(char*) * world, cudaMemcpyHostToDevice, st));
   for (int b = 0; b < n; ++b) {
-    arenas[b].carve(big + at[b]);
-    runs[b].log_tab = reinterpret_cast<double*>(big + tab_off);
-    runs[b].xch = reinterpret_cast<char**>(big + ptr_off);
+    arenas[b].carve(G.big + at[b]);
+    G.runs[b].log_tab = reinterpret_cast<double*>(G.big + tab_off);
+    G.runs[b].xch = world > 1 ? reinterpret_cast<char**>(G.big + ptr_off) : nullptr;
   }
-  Run* d_runs = nullptr;
-  CUDA_OK(cudaMallocAsync(reinterpret_cast<void**>(&d_runs), sizeof(Run) * n, st));
-  CUDA_OK(cudaMemcpyAsync(d_runs, runs.data(), sizeof(Run) * n, cudaMemcpyHostToDevice, st));
-  cudaEvent_t ca, cb;
-  cudaEventCreate(&ca);
-  cudaEventCreate(&cb);
-  const int lr = spex_launch_control_batch_async(d_runs, n, qmax, nthreads, st, ca, cb);
+  CUDA_OK(cudaMallocAsync(reinterpret_cast<void**>(&G.d_runs), sizeof(Run) * n, st));
+  CUDA_OK(cudaMemcpyAsync(G.d_runs, G.runs.data(), sizeof(Run) * n, cudaMemcpyHostToDevice, st));
+  cudaEventCreate(&G.ca);
+  cudaEventCreate(&G.cb);
+  const int lr = spex_launch_control_batch_async(G.d_runs, n, qmax, nthreads, st, G.ca, G.cb);
   if (lr != 0) fail(200, std::string("control kernel launch failed: ") + cudaGetErrorString(static_cast<cudaError_t>(lr)));
-  CUDA_OK(cudaEventSynchronize(cb));
+}
+
+int group_finish(GroupLaunch& G, std::vector<spex_executor*>& exs, int trace, float* ms_out) {
+  const int n = static_cast<int>(exs.size());
+  cudaStream_t st = G.st;
+  CUDA_OK(cudaEventSynchronize(G.cb));
   float ms = 0.f;
-  cudaEventElapsedTime(&ms, ca, cb);
-  cudaEventDestroy(ca);
-  cudaEventDestroy(cb);
+  cudaEventElapsedTime(&ms, G.ca, G.cb);
+  cudaEventDestroy(G.ca);
+  cudaEventDestroy(G.cb);
   if (ms_out) *ms_out = ms;
   int err = 0;
   for (int b = 0; b < n; ++b) {
     spex_executor& ex = *exs[b];
     const int Q = ex.hc.n_queries;
-    CUDA_OK(cudaMemcpyAsync(&ex.g, runs[b].g, sizeof(GState), cudaMemcpyDeviceToHost, st));
+    CUDA_OK(cudaMemcpyAsync(&ex.g, G.runs[b].g, sizeof(GState), cudaMemcpyDeviceToHost, st));
     ex.qs.resize(Q);
-    CUDA_OK(cudaMemcpyAsync(ex.qs.data(), runs[b].qs, sizeof(QueryRun) * Q, cudaMemcpyDeviceToHost, st));
+    CUDA_OK(cudaMemcpyAsync(ex.qs.data(), G.runs[b].qs, sizeof(QueryRun) * Q, cudaMemcpyDeviceToHost, st));
     CUDA_OK(cudaStreamSynchronize(st));
     if (trace && ex.g.log_n > 0) {
       ex.log.resize(ex.g.log_n);
-      CUDA_OK(cudaMemcpyAsync(ex.log.data(), runs[b].log, sizeof(Rec) * ex.g.log_n, cudaMemcpyDeviceToHost, st));
+      CUDA_OK(cudaMemcpyAsync(ex.log.data(), G.runs[b].log, sizeof(Rec) * ex.g.log_n, cudaMemcpyDeviceToHost, st));
     }
     ex.device_ms = ms;
     if (ex.g.error != 0 && err == 0) err = ex.g.error;
   }
-  cudaFreeAsync(big, st);
-  cudaFreeAsync(d_runs, st);
+  cudaFreeAsync(G.big, st);
+  cudaFreeAsync(G.d_runs, st);
   cudaStreamSynchronize(st);
   cudaStreamDestroy(st);
+  G = GroupLaunch{};
   return err;
+}
+
+GroupLaunch* group_new() { return new GroupLaunch(); }
+void group_delete(GroupLaunch* G) { delete G; }
+
+int run_group_device(std::vector<spex_executor*>& exs, int device, int trace, int node_cap, float* ms_out) {
+  GroupLaunch G;
+  group_launch(G, exs, device, trace, node_cap, nullptr);
+  return group_finish(G, exs, trace, ms_out);
 }
 #endif
 
@@ -1551,6 +1634,9 @@ int spex_executor_create(const char* config_json, uint64_t run_seed, const char*
       ex->t3 = tmp.t3;
       ex->run_seed = run_seed;
       ex->device = device;
+      ex->cfg_text = config_json;
+      ex->flags_text = flags_csv ? flags_csv : "";
+      ex->split_qjob = ex->hc.n_queries;
       ex->cfg_dump = to_json(ex->hc, ex->t1, ex->t2, ex->t3).dump();
       if (const char* e = std::getenv("SPEX_CTL_THREADS")) {
         const int t = std::atoi(e);  // same clamp as the launcher: slots must match threads
@@ -1659,6 +1745,32 @@ int spex_executor_set_split(spex_executor* ex, int rank, int world, void* const*
     // the rank's executor is the reference Executor over its block (n_queries = block size)
     ex->hc.n_queries = split_block_lo(qjob, rank + 1, world) - split_block_lo(qjob, rank, world);
     ex->cfg_dump = to_json(ex->hc, ex->t1, ex->t2, ex->t3).dump();
+  });
+}
+
+int spex_executor_emulate_split(spex_executor* ex, int rank, int world) {
+  return guarded([&] {
+#ifdef SPEX_EMU
+    (void)ex;
+    (void)rank;
+    (void)world;
+    fail(ERR_INVALID_ARGUMENT, "split emulation needs the CUDA build");
+#else
+    if (ex->ran) fail(ERR_INVALID_ARGUMENT, "emulate_split: executor already ran");
+    const long long box = spex_split_outbox_bytes(ex->split_qjob, world);
+    if (box < 0 || rank < 0 || rank >= world) fail(ERR_INVALID_ARGUMENT, "emulate_split: bad rank / world");
+    if (world == 1) return;
+    CUDA_OK(cudaSetDevice(ex->device));
+    if (ex->emu_boxes) cudaFree(ex->emu_boxes);
+    CUDA_OK(cudaMalloc(reinterpret_cast<void**>(&ex->emu_boxes), static_cast<size_t>(box) * world));
+    CUDA_OK(cudaMemset(ex->emu_boxes, 0, static_cast<size_t>(box) * world));
+    CUDA_OK(cudaDeviceSynchronize());
+    std::vector<void*> bx(world);
+    for (int r = 0; r < world; ++r) bx[r] = ex->emu_boxes + box * r;
+    const int rc = spex_executor_set_split(ex, rank, world, bx.data(), 1);
+    if (rc) fail(rc, g_err);
+    ex->split_emulate = 1;
+#endif
   });
 }
 
@@ -1904,6 +2016,7 @@ int spex_executor_query_finish(spex_executor* ex, double* out, int cap, int* n) 
 
 void spex_executor_destroy(spex_executor* ex) {
 #ifndef SPEX_EMU
+  if (ex && ex->emu_boxes) cudaFree(ex->emu_boxes);
   if (ex && ex->stream) cudaStreamDestroy(ex->stream);
   if (ex && ex->mstream) cudaStreamDestroy(ex->mstream);
 #endif

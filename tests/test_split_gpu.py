@@ -135,3 +135,20 @@ def test_split_one_process_per_rank_ipc(tmp_path, model):
             assert got[epoch]["log"] == ref[r], (r, epoch, refutil.compare_logs(ref[r], got[epoch]["log"]))
             if model:
                 assert got[epoch]["model"]["decode_rows"] > 0
+
+
+@needs_oracle
+@pytest.mark.parametrize("W,rank", [(2, 1), (4, 0), (4, 3)])
+def test_emulated_rank_matches_oracle(W, rank):
+    """One rank live (with the small policy + PRM forward), the others' control
+    beside it on this GPU: the rank's log is the split oracle's."""
+    cfg = (CFG / "c3_rstar_w4_q512.json").read_text()
+    ref, rounds = refutil.ref_split_log(cfg, 1, None, W)
+    ex = spex.Executor(cfg, 1, None, trace=True)
+    ex.set_model("small_policy", "small_prm", 1)
+    ex.emulate_split(rank, W)
+    ex.run()
+    assert ex.split_stats()["rounds"] == rounds[rank]
+    assert ex.log_lines() == ref[rank]
+    assert ex.model_stats()["decode_rows"] > 0
+    ex.close()
