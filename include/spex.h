@@ -207,7 +207,7 @@ int spex_executor_split_stats(spex_executor* ex, long long* rounds, double* wait
  * world - 1 SMs the other ranks' control occupies. */
 int spex_executor_emulate_split(spex_executor* ex, int rank, int world);
 int spex_executor_model_stats(spex_executor* ex, spex_model_stats* out);
-/* Tree-KV pool size in pages (0 = the default: the resident pools, else 62%
+/* Tree-KV pool size in pages (0 = the default: the resident pools, else 70%
  * of free HBM). Pages of dead thoughts (pruned, REBASE layers expanded,
  * scored terminals, finished queries) are reused (no reference counterpart:
  * the reference holds no KV, SearchTree::prune_subtree tree.cpp:119-141 and

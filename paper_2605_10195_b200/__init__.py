@@ -206,7 +206,7 @@ class Executor:
         return {"rounds": r.value, "wait_ms": w.value}
 
     def set_kv_pages(self, pages: int) -> None:
-        """Tree-KV pool size in pages of 16 tokens (0: the default, 62% of free HBM)."""
+        """Tree-KV pool size in pages of 16 tokens (0: the default, 70% of free HBM)."""
         _check(self._L.spex_executor_set_kv_pages(self._h, int(pages)))
 
     def set_reward_source(self, source: str) -> None:

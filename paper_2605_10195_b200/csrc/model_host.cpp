@@ -559,7 +559,7 @@ extern "C" long long spex_model_pool_slots(const ModelRunConfig* mc) {
   cudaMemGetInfo(&free_b, &total_b);
   const double per_slot = 4.0 * (mc->policy.L * mc->policy.KVH * mc->policy.dh +
                                  (mc->with_prm ? mc->prm.L * mc->prm.KVH * mc->prm.dh : 0));
-  return static_cast<long long>(0.62 * static_cast<double>(free_b) / per_slot);
+  return static_cast<long long>(0.70 * static_cast<double>(free_b) / per_slot);
 }
 
 extern "C" void spex_model_cache_clear() {

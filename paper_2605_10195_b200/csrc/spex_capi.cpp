@@ -1132,7 +1132,7 @@ void run_executor(spex_executor& ex, int trace) {
     int* d_kvfree = nullptr;
     if (ex.with_model) {
       // the pool: an explicit page count, else the resident cached pools or
-      // 62% of free HBM (spex_model_pool_slots)
+      // 70% of free HBM (spex_model_pool_slots)
       const long long slots = ex.kv_pages_req > 0 ? ex.kv_pages_req * kKvPage : spex_model_pool_slots(&ex.mc);
       kv_configure(ex, R.cfg, slots / kKvPage);
       CUDA_OK(cudaMallocAsync(reinterpret_cast<void**>(&d_kvpt), sizeof(int) * R.cfg.kv_pt_cap, ex.stream));
