@@ -598,6 +598,13 @@ __global__ void __launch_bounds__(256, (UNROLL > 4 ? 2 : (G == 1 ? 4 : (G <= 4 ?
 // holding registers; lanes read the staged rows with 128-bit shared loads
 // (half a warp per 256-byte row) into the same FHFMA.BF16 math as
 // tree_attn_decode_kernel, one online-softmax update per chunk.
+// One Segment (16 bytes) in a single load.
+__device__ __forceinline__ void load_seg(const Segment* sp, long long& base, int& len) {
+  const int4 v = __ldg(reinterpret_cast<const int4*>(sp));
+  base = (long long)(((unsigned long long)(unsigned)v.y << 32) | (unsigned)v.x);
+  len = v.z;
+}
+
 template <int kBulkCH, int kBulkNST, int kBulkWarps>  // tokens per stage, stages per warp, warps per block
 __global__ void __launch_bounds__(kBulkWarps * 32, 1)
     tree_attn_bulk_kernel(const RowDesc* __restrict__ rows, const Segment* __restrict__ segs,
@@ -625,6 +632,10 @@ __global__ void __launch_bounds__(kBulkWarps * 32, 1)
   int p_item = -1, p_seg = 0, p_off = 0, p_nseg = 0;
   long long p_segoff = 0;
   const Segment* p_sg = nullptr;
+  // the current segment and the next one, loaded a segment ahead so a segment
+  // change issues its first chunk without waiting on the list
+  long long p_base = 0, p_nbase = 0;
+  int p_len = 0, p_nlen = 0;
   bool p_done = false;
   int issued = 0;
   auto produce = [&]() {  // lane 0: issue the next chunk into stage issued % NST
@@ -651,15 +662,20 @@ __global__ void __launch_bounds__(kBulkWarps * 32, 1)
         p_seg = 0;
         p_off = 0;
         p_segoff = (long long)(it % KVH) * slots;
+        p_len = 0;
+        if (p_nseg > 0) load_seg(p_sg, p_base, p_len);
+        if (p_nseg > 1) load_seg(p_sg + 1, p_nbase, p_nlen);
       }
-      const int len = p_sg[p_seg].len;
-      if (p_off >= len) {
-        ++p_seg;
+      if (p_off >= p_len) {
+        if (++p_seg >= p_nseg) continue;
+        p_base = p_nbase;
+        p_len = p_nlen;
+        if (p_seg + 1 < p_nseg) load_seg(p_sg + p_seg + 1, p_nbase, p_nlen);
         p_off = 0;
         continue;
       }
-      const int n = min(kBulkCH, len - p_off);
-      const long long tok = p_segoff + p_sg[p_seg].base + p_off;
+      const int n = min(kBulkCH, p_len - p_off);
+      const long long tok = p_segoff + p_base + p_off;
       const int st = issued % kBulkNST;
       unsigned char* kb = ring + st * 2 * STAGE;
       mbar_expect_tx(&bar[warp][st], 2u * n * DH * 2);
@@ -700,8 +716,11 @@ __global__ void __launch_bounds__(kBulkWarps * 32, 1)
     float m = -INFINITY, l = 0.f, acc[EPL];
 #pragma unroll
     for (int e = 0; e < EPL; ++e) acc[e] = 0.f;
+    // segment lengths: 32 at a time, one per lane (one load latency instead of one per segment)
+    int seg_len = 0;
     for (int si = 0; si < rd.nseg; ++si) {
-      const int len = sg[si].len;
+      if ((si & 31) == 0) seg_len = si + lane < rd.nseg ? sg[si + lane].len : 0;
+      const int len = __shfl_sync(0xffffffffu, seg_len, si & 31);
       for (int off = 0; off < len; off += kBulkCH) {
         const int n = min(kBulkCH, len - off);
         if (lane == 0) produce();  // keep NST-1 chunks in flight (stage consumed last round is free)
