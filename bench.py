@@ -69,9 +69,14 @@ def parse():
     return ap.parse_args()
 
 
+# SPEX_BENCH_ONE_GPU=1 (tests only): every rank on cuda:0 with a gloo process
+# group, so the multi-rank path (outbox exchange, reductions) runs on one GPU
+ONE_GPU = os.environ.get("SPEX_BENCH_ONE_GPU") == "1"
+
+
 def dist_env():
-    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), int(
-        os.environ.get("LOCAL_RANK", "0"))
+    local = 0 if ONE_GPU else int(os.environ.get("LOCAL_RANK", "0"))
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), local
 
 
 class Clocks:
@@ -244,7 +249,10 @@ def main():
     pg = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if ONE_GPU:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         pg = dist
 
     def barrier():
@@ -252,14 +260,21 @@ def main():
         if pg:
             pg.barrier()
 
-    boxes, epoch = None, [0]
+    boxes, epoch, split_note = None, [0], None
     if split:
         from paper_2605_10195_b200 import _lib, shard
-        boxes = shard.Outboxes(_lib.lib(), rank, world, cfg["run"]["n_queries"] * world, device=local)
+        try:
+            boxes = shard.Outboxes(_lib.lib(), rank, world, cfg["run"]["n_queries"] * world, device=local)
+        except shard.SplitUnavailable as e:  # raised on every rank alike: all run independent shards
+            split, split_note = False, f"split sharding unavailable ({e}); independent shards instead"
+            seed = shard_seed(base_seed, rank)
+            job_text = cfg_text
 
     def one_search(trace: bool, flags=None):
         ex = spex.Executor(job_text, seed, flags, trace=trace, device=local)
         ex.set_model(args.policy, args.prm, weight_seed=1)
+        if ONE_GPU and world > 1:
+            ex.set_kv_pages(50000)  # the ranks share one GPU's HBM (tests only)
         if coupled:
             ex.set_shard(rank, world)
         if split:
@@ -436,10 +451,11 @@ def main():
     one_search(False, "")  # warm-up (its own schedule shapes)
     bs_tot, bs_st, bs_ms, _ = one_search(False, "")
     sp_makespan = tot.makespan
-    times = torch.tensor([dev_s, wall, e2e_wall, tr_wall], dtype=torch.float64, device="cuda")
+    red_dev = "cpu" if ONE_GPU else "cuda"
+    times = torch.tensor([dev_s, wall, e2e_wall, tr_wall], dtype=torch.float64, device=red_dev)
     if pg:
         pg.all_reduce(times, op=pg.ReduceOp.MAX)
-        qt = torch.tensor([float(agg["queries"]), float(e2e_q), float(tr_q)], dtype=torch.float64, device="cuda")
+        qt = torch.tensor([float(agg["queries"]), float(e2e_q), float(tr_q)], dtype=torch.float64, device=red_dev)
         pg.all_reduce(qt)
         total_q, total_e2e_q, total_tr_q = qt.tolist()
     else:
@@ -481,7 +497,8 @@ def main():
                    "parallelism": (f"query-block model work x{world}, search replicated (single virtual clock)"
                                    if coupled else
                                    f"query-sharded x{world}, one job, T2 budget exchange between the control "
-                                   f"kernels through peer-memory outboxes" if split else f"query-sharded x{world}")},
+                                   f"kernels through peer-memory outboxes" if split else
+                                   f"query-sharded x{world}" + (f" ({split_note})" if split_note else ""))},
         "e2e": {"value": total_e2e_q / e2e_wall, "unit": "queries/s",
                 "h2d_bytes_per_step": len(cfg_text.encode()),
                 "d2h_bytes_per_step": 256 + 256 * cfg["run"]["n_queries"],

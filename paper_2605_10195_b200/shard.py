@@ -96,6 +96,10 @@ def rank_result(L, h, trace: bool = True) -> dict:
     return {"log": log, "rounds": rounds.value, "wait_ms": wait.value, "stats": st.as_dict()}
 
 
+class SplitUnavailable(RuntimeError):
+    """The outboxes could not be set up on some rank (raised on every rank)."""
+
+
 class Outboxes:
     """The ranks' split-mode outboxes, one process per rank.
 
@@ -115,39 +119,56 @@ class Outboxes:
             raise ValueError("split: need 1 <= world <= min(64, n_queries)")
         self._shm = []
         self._opened = []
-        if kind == "cuda":
-            own = ctypes.c_void_p()
-            handle = ctypes.create_string_buffer(64)
-            if L.spex_split_outbox_alloc(device, nbytes, ctypes.byref(own), handle):
-                raise RuntimeError(L.spex_last_error().decode())
-            self._own = own.value
-            mine = bytes(handle.raw)
-        elif kind == "shm":
-            from multiprocessing import shared_memory
-            shm = shared_memory.SharedMemory(create=True, size=int(nbytes), name=f"{tag}_{rank}_{world}")
-            shm.buf[:nbytes] = bytes(nbytes)
-            self._shm.append(shm)
-            self._own = ctypes.addressof(ctypes.c_char.from_buffer(shm.buf))
-            mine = shm.name
-        else:
-            raise ValueError("kind is 'cuda' or 'shm'")
-        handles = [None] * world
-        dist.all_gather_object(handles, mine, group=group)
-        ptrs = []
-        for s, h in enumerate(handles):
-            if s == rank:
-                ptrs.append(self._own)
-            elif kind == "cuda":
-                p = ctypes.c_void_p()
-                if L.spex_split_outbox_open(device, h, ctypes.byref(p)):
+        self._own = None
+        mine, err = None, ""
+        try:
+            if kind == "cuda":
+                own = ctypes.c_void_p()
+                handle = ctypes.create_string_buffer(64)
+                if L.spex_split_outbox_alloc(device, nbytes, ctypes.byref(own), handle):
                     raise RuntimeError(L.spex_last_error().decode())
-                self._opened.append(p.value)
-                ptrs.append(p.value)
-            else:
+                self._own = own.value
+                mine = bytes(handle.raw)
+            elif kind == "shm":
                 from multiprocessing import shared_memory
-                peer = shared_memory.SharedMemory(name=h)
-                self._shm.append(peer)
-                ptrs.append(ctypes.addressof(ctypes.c_char.from_buffer(peer.buf)))
+                shm = shared_memory.SharedMemory(create=True, size=int(nbytes), name=f"{tag}_{rank}_{world}")
+                shm.buf[:nbytes] = bytes(nbytes)
+                self._shm.append(shm)
+                self._own = ctypes.addressof(ctypes.c_char.from_buffer(shm.buf))
+                mine = shm.name
+            else:
+                raise ValueError("kind is 'cuda' or 'shm'")
+        except Exception as e:  # every rank learns it below, so all ranks take the same path
+            err = f"rank {rank}: {e}"
+        handles = [None] * world
+        dist.all_gather_object(handles, (mine, err), group=group)
+        errs = [e for _, e in handles if e]
+        if errs:
+            self.close()
+            raise SplitUnavailable("; ".join(errs))
+        ptrs, err = [], ""
+        try:
+            for s, (h, _) in enumerate(handles):
+                if s == rank:
+                    ptrs.append(self._own)
+                elif kind == "cuda":
+                    p = ctypes.c_void_p()
+                    if L.spex_split_outbox_open(device, h, ctypes.byref(p)):
+                        raise RuntimeError(L.spex_last_error().decode())
+                    self._opened.append(p.value)
+                    ptrs.append(p.value)
+                else:
+                    from multiprocessing import shared_memory
+                    peer = shared_memory.SharedMemory(name=h)
+                    self._shm.append(peer)
+                    ptrs.append(ctypes.addressof(ctypes.c_char.from_buffer(peer.buf)))
+        except Exception as e:
+            err = f"rank {rank}: {e}"
+        oks = [None] * world
+        dist.all_gather_object(oks, err, group=group)
+        if any(oks):
+            self.close()
+            raise SplitUnavailable("; ".join(e for e in oks if e))
         self.pointers = ptrs
 
     def attach(self, h, epoch: int) -> None:
