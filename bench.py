@@ -274,7 +274,7 @@ def main():
         ex = spex.Executor(job_text, seed, flags, trace=trace, device=local)
         ex.set_model(args.policy, args.prm, weight_seed=1)
         if ONE_GPU and world > 1:
-            ex.set_kv_pages(50000)  # the ranks share one GPU's HBM (tests only)
+            ex.set_kv_pages(110000)  # the ranks share one GPU's HBM (tests only)
         if coupled:
             ex.set_shard(rank, world)
         if split:
