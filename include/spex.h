@@ -6,6 +6,7 @@
  * one of them and is what a reference-side binding would call:
  *
  *   spex_executor_create/run  <- totsim::Executor(cfg, seed, flags, trace) + run()
+ *   spex_frontier_step        <- one main_loop iteration at a time (executor.cpp:785-807)
  *                                (proj/include/totsim/executor.hpp:50-58,
  *                                 proj/src/executor.cpp:809-860)
  *   spex_run_once             <- totsim::run_once (proj/include/totsim/experiment.hpp:27,
@@ -142,6 +143,17 @@ int spex_executor_create(const char* config_json, uint64_t run_seed, const char*
 /* Run to completion (call once; a second call returns InvalidArgument + 1).
  * trace != 0 records the event log (trace.hpp:14-29) on the device. */
 int spex_executor_run(spex_executor* ex, int trace, spex_totals* totals);
+/* Stepwise execution, the fused device frontier step (SURVEY.md §8b
+ * spex_frontier_step): each call runs up to `iterations` consumer-loop
+ * iterations of the search on the device (executor.cpp:785-807: one engine
+ * epoch with its completions and follow-ups, or one reward event; 0 = to the
+ * end) and returns, the run's state staying on the device between calls.
+ * `events` (spex_free) receives the event-log lines produced by this call (the
+ * first call starts with run_begin, the last ends with run_end), so the
+ * concatenation over calls is the run_once log byte for byte; *done = 1 after
+ * the last. Control only (no model attached), not for split ranks; the
+ * executor then counts as run (stats, log, totals). */
+int spex_frontier_step(spex_executor* ex, long long iterations, int* done, char** events, size_t* events_len);
 /* Event log of a traced run as JSON lines, byte-compatible with TraceWriter. */
 int spex_executor_log(spex_executor* ex, char** out_lines, size_t* out_len);
 int spex_executor_stats(spex_executor* ex, spex_stats* out);

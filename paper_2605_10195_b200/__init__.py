@@ -159,6 +159,21 @@ class Executor:
         d = t.as_dict()
         return RunTotals(**d)
 
+    def step(self, iterations: int = 1) -> tuple:
+        """The fused device frontier step: run up to ``iterations`` iterations
+        of the consumer loop (executor.cpp:785-807; 0 = to the end) on the
+        device. Returns (done, event-log lines of this call)."""
+        done = ctypes.c_int()
+        out = ctypes.c_void_p()
+        n = ctypes.c_size_t()
+        _check(self._L.spex_frontier_step(self._h, int(iterations), ctypes.byref(done), ctypes.byref(out),
+                                          ctypes.byref(n)))
+        try:
+            lines = ctypes.string_at(out.value, n.value).decode().splitlines() if out.value else []
+        finally:
+            self._L.spex_free(out)
+        return bool(done.value), lines
+
     def log_lines(self) -> list:
         out = ctypes.c_void_p()
         n = ctypes.c_size_t()

@@ -125,6 +125,9 @@ _EXPORTS = {
         ctypes.c_int,
     ),
     "spex_executor_stats": ([ctypes.c_void_p, ctypes.POINTER(Stats)], ctypes.c_int),
+    "spex_frontier_step": (
+        [ctypes.c_void_p, ctypes.c_longlong, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_void_p),
+         ctypes.POINTER(ctypes.c_size_t)], ctypes.c_int),
     "spex_executor_destroy": ([ctypes.c_void_p], None),
     "spex_run_batch": (
         [ctypes.c_char_p, ctypes.POINTER(ctypes.c_uint64), ctypes.c_int, ctypes.c_char_p, ctypes.c_int,

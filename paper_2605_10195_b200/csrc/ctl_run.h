@@ -1362,8 +1362,10 @@ SPEX_HD void run_loop(Run* R, EX& ex, int* warp_off) {
   GState* g = R->g;
   const Cfg& c = R->cfg;
   const int Q = c.n_queries;
-  if (c.split_world > 1) split_start(R, ex);
-  if (ex.tid == 0) {
+  if (g->phase == 2) return;  // a finished run (stepwise execution called once more)
+  const bool resume = g->phase == 1;
+  if (!resume && c.split_world > 1) split_start(R, ex);
+  if (!resume && ex.tid == 0) {
     const int first = c.batch_size < Q ? c.batch_size : Q;
     for (int q = 0; q < first; ++q) {
       Rec* slot = c.trace ? &R->log[g->log_n++] : nullptr;
@@ -1378,10 +1380,19 @@ SPEX_HD void run_loop(Run* R, EX& ex, int* warp_off) {
     g->start_ns = spex_wall_ns();
   }
   ex.sync();
-  followups(R, ex, warp_off);
+  if (!resume) followups(R, ex, warp_off);
+  // stepwise execution: at most step_iters consumer-loop iterations this launch
+  const i64 budget = g->step_iters;
+  i64 done_iters = 0;
+  bool paused = false;
   for (;;) {
     ex.sync();
     if (g->error || g->finished_count >= Q) break;
+    if (budget > 0 && done_iters >= budget) {
+      paused = true;
+      break;
+    }
+    ++done_iters;
     if (ex.tid == 0) g->iterations += 1;
     const double t_evt = g->fifo_head < g->fifo_tail ? R->ev_time[g->fifo_head] : kInf;
     if (g->n_act + g->n_staged > 0) {
@@ -1419,7 +1430,13 @@ SPEX_HD void run_loop(Run* R, EX& ex, int* warp_off) {
     });
     followups(R, ex, warp_off);
   }
+  if (paused) {
+    if (ex.tid == 0) g->phase = 1;
+    ex.sync();
+    return;
+  }
   if (ex.tid == 0) {
+    g->phase = 2;
     double ms = 0.0;
     for (int q = 0; q < Q; ++q)
       if (R->qs[q].finished && R->qs[q].finish_time > ms) ms = R->qs[q].finish_time;

@@ -290,6 +290,11 @@ struct GState {
   int pad_dirty;
   i64 start_ns;   // device wall clock at the start of the run
   i64 reward_wait_ns;  // time the control spent waiting for PRM scores (reward_prm)
+  // stepwise execution (spex_frontier_step): 0 not started, 1 admitted and
+  // paused between calls, 2 finished; step_iters = consumer-loop iterations of
+  // the next launch (0: run to the end)
+  int phase, pad_phase;
+  i64 step_iters;
   i64 xch_rounds;      // split mode: budget exchange rounds of this rank
   i64 xch_wait_ns;     // split mode: time spent waiting for the other ranks
   // device cycle counters per phase (thread 0's view)

@@ -19,6 +19,7 @@
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <memory>
 #include <mutex>
 #include <sstream>
 #include <thread>
@@ -443,6 +444,21 @@ struct Arena {
 }  // namespace
 
 // ================================================================ executor
+// Stepwise execution state (spex_frontier_step): the run's arena stays on the
+// device (host memory in the emulation) between calls.
+struct StepRun {
+  Run R{};
+  char* base = nullptr;
+  Run* d_run = nullptr;
+  double* d_tab = nullptr;
+  std::vector<char> host_mem;  // emulation arena
+  std::vector<int> sm;
+  std::vector<double> smd;
+  std::vector<long long> sml;
+  std::vector<int> warp_off;
+  long long sent = 0;  // records already returned
+};
+
 struct spex_executor {
   HostConfig hc;
   bool t1 = false, t2 = false, t3 = false;
@@ -475,6 +491,7 @@ struct spex_executor {
   int split_emulate = 0;            // spex_executor_emulate_split: the other ranks run beside this one
   std::string cfg_text, flags_text; // as created (the emulated ranks' executors)
   char* emu_boxes = nullptr;        // the emulation's outboxes (device)
+  std::unique_ptr<StepRun> step;    // stepwise execution in progress
 #ifndef SPEX_EMU
   cudaStream_t stream = nullptr;
   cudaStream_t mstream = nullptr;
@@ -760,122 +777,128 @@ std::string label_str(int idx) { return idx < 0 ? std::string() : "a" + std::to_
 
 // TraceWriter::emit (trace.cpp:32-36) with the executor's field order
 // (executor.cpp:134-155,179-186,214-221,244-250,288-292,318-325,346-354,381-403,421-426)
+void serialize_header(const spex_executor& ex, std::string& out) {
+  ordered_json j;
+  j["t"] = 0.0;
+  j["ev"] = "run_begin";
+  j["seed"] = ex.run_seed;
+  j["config"] = ordered_json::parse(ex.cfg_dump);
+  out += j.dump();
+  out += '\n';
+}
+
+void serialize_record(const Rec& r, std::string& out) {
+  ordered_json j;
+  j["t"] = r.t;
+  switch (r.kind) {
+    case EV_ADMIT:
+      j["ev"] = "admit";
+      j["q"] = r.q;
+      j["seed"] = static_cast<std::uint64_t>(r.y);
+      break;
+    case EV_NODE:
+      j["ev"] = "node";
+      j["q"] = r.q;
+      j["node"] = r.node;
+      j["parent"] = static_cast<std::uint32_t>(r.a);
+      j["slot"] = r.b;
+      j["spec"] = (r.flags & RF_SPEC) != 0;
+      j["tokens"] = r.c;
+      j["terminal"] = (r.flags & RF_TERMINAL) != 0;
+      break;
+    case EV_REQ:
+      j["ev"] = "req";
+      j["q"] = r.q;
+      j["node"] = r.node;
+      j["stream"] = r.a;
+      j["spec"] = (r.flags & RF_SPEC) != 0;
+      j["dist"] = r.b;
+      break;
+    case EV_DONE:
+      j["ev"] = "done";
+      j["q"] = r.q;
+      j["node"] = r.node;
+      j["stream"] = r.a;
+      j["tokens"] = r.b;
+      j["cancelled"] = (r.flags & RF_CANCELLED) != 0;
+      j["stale"] = (r.flags & RF_STALE) != 0;
+      break;
+    case EV_REWARD:
+      j["ev"] = "reward";
+      j["q"] = r.q;
+      j["node"] = r.node;
+      j["r"] = r.x;
+      break;
+    case EV_PROMOTE:
+      j["ev"] = "promote";
+      j["q"] = r.q;
+      j["node"] = r.node;
+      j["ready"] = static_cast<long long>(r.y);
+      j["dist"] = r.a;
+      break;
+    case EV_PRUNE:
+      j["ev"] = "prune";
+      j["q"] = r.q;
+      j["node"] = r.node;
+      j["count"] = r.a;
+      break;
+    case EV_ANSWER:
+      j["ev"] = "answer";
+      j["q"] = r.q;
+      j["node"] = r.node;
+      j["label"] = label_str(r.a);
+      j["weight"] = r.x;
+      j["correct"] = (r.flags & RF_CORRECT) != 0;
+      break;
+    case EV_TERMINATE:
+      j["ev"] = "terminate";
+      j["q"] = r.q;
+      j["label"] = label_str(r.a);
+      j["answers"] = r.b;
+      break;
+    case EV_QUERY_DONE:
+      j["ev"] = "query_done";
+      j["q"] = r.q;
+      j["label"] = label_str(r.a);
+      j["correct"] = (r.flags & RF_CORRECT) != 0;
+      j["answers"] = r.b;
+      j["early"] = (r.flags & RF_EARLY) != 0;
+      break;
+    default:
+      j["ev"] = "?";
+      break;
+  }
+  out += j.dump();
+  out += '\n';
+}
+
+void serialize_footer(const spex_executor& ex, std::string& out) {
+  long long gen = 0, com = 0, reu = 0, was = 0;
+  for (const QueryRun& q : ex.qs) {
+    gen += q.generated;
+    com += q.committed;
+    reu += q.reused;
+    was += q.wasted;
+  }
+  ordered_json j;
+  j["t"] = ex.g.makespan;
+  j["ev"] = "run_end";
+  j["makespan"] = ex.g.makespan;
+  j["generated"] = gen;
+  j["committed"] = com;
+  j["reused"] = reu;
+  j["wasted"] = was;
+  j["queries"] = ex.g.finished_count;
+  out += j.dump();
+  out += '\n';
+}
+
 void serialize(const spex_executor& ex, std::string& out) {
   out.clear();
   out.reserve(ex.log.size() * 96 + 4096);
-  {
-    ordered_json j;
-    j["t"] = 0.0;
-    j["ev"] = "run_begin";
-    j["seed"] = ex.run_seed;
-    j["config"] = ordered_json::parse(ex.cfg_dump);
-    out += j.dump();
-    out += '\n';
-  }
-  for (const Rec& r : ex.log) {
-    ordered_json j;
-    j["t"] = r.t;
-    switch (r.kind) {
-      case EV_ADMIT:
-        j["ev"] = "admit";
-        j["q"] = r.q;
-        j["seed"] = static_cast<std::uint64_t>(r.y);
-        break;
-      case EV_NODE:
-        j["ev"] = "node";
-        j["q"] = r.q;
-        j["node"] = r.node;
-        j["parent"] = static_cast<std::uint32_t>(r.a);
-        j["slot"] = r.b;
-        j["spec"] = (r.flags & RF_SPEC) != 0;
-        j["tokens"] = r.c;
-        j["terminal"] = (r.flags & RF_TERMINAL) != 0;
-        break;
-      case EV_REQ:
-        j["ev"] = "req";
-        j["q"] = r.q;
-        j["node"] = r.node;
-        j["stream"] = r.a;
-        j["spec"] = (r.flags & RF_SPEC) != 0;
-        j["dist"] = r.b;
-        break;
-      case EV_DONE:
-        j["ev"] = "done";
-        j["q"] = r.q;
-        j["node"] = r.node;
-        j["stream"] = r.a;
-        j["tokens"] = r.b;
-        j["cancelled"] = (r.flags & RF_CANCELLED) != 0;
-        j["stale"] = (r.flags & RF_STALE) != 0;
-        break;
-      case EV_REWARD:
-        j["ev"] = "reward";
-        j["q"] = r.q;
-        j["node"] = r.node;
-        j["r"] = r.x;
-        break;
-      case EV_PROMOTE:
-        j["ev"] = "promote";
-        j["q"] = r.q;
-        j["node"] = r.node;
-        j["ready"] = static_cast<long long>(r.y);
-        j["dist"] = r.a;
-        break;
-      case EV_PRUNE:
-        j["ev"] = "prune";
-        j["q"] = r.q;
-        j["node"] = r.node;
-        j["count"] = r.a;
-        break;
-      case EV_ANSWER:
-        j["ev"] = "answer";
-        j["q"] = r.q;
-        j["node"] = r.node;
-        j["label"] = label_str(r.a);
-        j["weight"] = r.x;
-        j["correct"] = (r.flags & RF_CORRECT) != 0;
-        break;
-      case EV_TERMINATE:
-        j["ev"] = "terminate";
-        j["q"] = r.q;
-        j["label"] = label_str(r.a);
-        j["answers"] = r.b;
-        break;
-      case EV_QUERY_DONE:
-        j["ev"] = "query_done";
-        j["q"] = r.q;
-        j["label"] = label_str(r.a);
-        j["correct"] = (r.flags & RF_CORRECT) != 0;
-        j["answers"] = r.b;
-        j["early"] = (r.flags & RF_EARLY) != 0;
-        break;
-      default:
-        j["ev"] = "?";
-        break;
-    }
-    out += j.dump();
-    out += '\n';
-  }
-  {
-    long long gen = 0, com = 0, reu = 0, was = 0;
-    for (const QueryRun& q : ex.qs) {
-      gen += q.generated;
-      com += q.committed;
-      reu += q.reused;
-      was += q.wasted;
-    }
-    ordered_json j;
-    j["t"] = ex.g.makespan;
-    j["ev"] = "run_end";
-    j["makespan"] = ex.g.makespan;
-    j["generated"] = gen;
-    j["committed"] = com;
-    j["reused"] = reu;
-    j["wasted"] = was;
-    j["queries"] = ex.g.finished_count;
-    out += j.dump();
-    out += '\n';
-  }
+  serialize_header(ex, out);
+  for (const Rec& r : ex.log) serialize_record(r, out);
+  serialize_footer(ex, out);
 }
 
 void fill_totals(const spex_executor& ex, spex_totals* t) {
@@ -911,6 +934,110 @@ int guarded(F&& f) {
     g_err = e.what();
     return ERR_INTERNAL;
   }
+}
+
+// ---------------------------------------------------------- stepwise execution
+void step_release(spex_executor& ex) {
+  if (!ex.step) return;
+#ifndef SPEX_EMU
+  if (ex.step->base) cudaFree(ex.step->base);
+  if (ex.step->d_run) cudaFree(ex.step->d_run);
+  if (ex.step->d_tab) cudaFree(ex.step->d_tab);
+#endif
+  ex.step.reset();
+}
+
+// Set up the run's arena (trace on) for stepwise execution.
+void step_begin(spex_executor& ex) {
+  const int Q = ex.hc.n_queries;
+  int node_cap = 512;
+  if (const char* e = std::getenv("SPEX_NODE_CAP")) node_cap = std::max(16, std::atoi(e));
+  if (ex.node_cap0 > 0) node_cap = ex.node_cap0;
+  const long long sc = static_cast<long long>(Q) * (node_cap - 1) + 64;
+  const long long lc = static_cast<long long>(Q) * node_cap * 6 + 64;
+  if (sc > (1LL << 30) || lc > (1LL << 31) - 1) fail(ERR_CAP_STREAMS, "stepwise run too large");
+  const int stage_cap = std::max(512, node_cap);
+  auto st = std::make_unique<StepRun>();
+  Run& R = st->R;
+  ex.record_sched = 0;
+  set_cfg(ex, R.cfg, node_cap, static_cast<int>(sc), static_cast<int>(lc), stage_cap, 1, 0);
+  Arena A;
+  layout(A, R, Q, node_cap, static_cast<int>(sc), static_cast<int>(lc), ex.nthreads, stage_cap);
+  R.nwarps = ex.nthreads / 32;
+  std::vector<double>& tab = log_table();
+  R.log_tab_n = static_cast<int>(tab.size());
+#ifdef SPEX_EMU
+  st->host_mem.assign(A.total + 256, 0);
+  char* base = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(st->host_mem.data()) + 255) & ~uintptr_t(255));
+  A.carve(base);
+  R.log_tab = tab.data();
+  for (int q = 0; q < Q; ++q) R.qs[q].plan_empty_version = 0xffffffffu;
+  st->sm.assign(2048, 0);
+  st->smd.assign(64, 0.0);
+  st->sml.assign(64, 0);
+  st->warp_off.assign(3 * 64, 0);
+#else
+  CUDA_OK(cudaSetDevice(ex.device));
+  if (!ex.stream) CUDA_OK(cudaStreamCreateWithFlags(&ex.stream, cudaStreamNonBlocking));
+  CUDA_OK(cudaMalloc(reinterpret_cast<void**>(&st->base), A.total + 256));
+  CUDA_OK(cudaMemsetAsync(st->base, 0, A.total + 256, ex.stream));
+  A.carve(st->base);
+  CUDA_OK(cudaMalloc(reinterpret_cast<void**>(&st->d_tab), tab.size() * sizeof(double)));
+  CUDA_OK(cudaMemcpyAsync(st->d_tab, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice, ex.stream));
+  R.log_tab = st->d_tab;
+  CUDA_OK(cudaMalloc(reinterpret_cast<void**>(&st->d_run), sizeof(Run)));
+  CUDA_OK(cudaMemcpyAsync(st->d_run, &R, sizeof(Run), cudaMemcpyHostToDevice, ex.stream));
+  CUDA_OK(cudaStreamSynchronize(ex.stream));
+#endif
+  ex.step = std::move(st);
+  ex.log.clear();
+}
+
+// Run up to `iters` consumer-loop iterations (0: to the end), then bring the
+// run scalars and the new records back.
+void step_run(spex_executor& ex, long long iters) {
+  StepRun& st = *ex.step;
+  Run& R = st.R;
+  const int Q = ex.hc.n_queries;
+#ifdef SPEX_EMU
+  R.g->step_iters = iters;
+  HostExec hx;
+  hx.sm = st.sm.data();
+  hx.smd = st.smd.data();
+  hx.sml = st.sml.data();
+  run_loop(&R, hx, st.warp_off.data());
+  ex.g = *R.g;
+  const long long n0 = static_cast<long long>(ex.log.size());
+  for (long long i = n0; i < ex.g.log_n; ++i) ex.log.push_back(R.log[i]);
+  if (ex.g.phase == 2 || ex.g.error) ex.qs.assign(R.qs, R.qs + Q);
+#else
+  CUDA_OK(cudaMemcpyAsync(reinterpret_cast<char*>(R.g) + offsetof(GState, step_iters), &iters, sizeof(iters),
+                          cudaMemcpyHostToDevice, ex.stream));
+  cudaEvent_t ca, cb;
+  cudaEventCreate(&ca);
+  cudaEventCreate(&cb);
+  const int lr = spex_launch_control_async(st.d_run, Q, ex.nthreads, ex.stream, ca, cb);
+  if (lr != 0) fail(200, std::string("control kernel launch failed: ") + cudaGetErrorString(static_cast<cudaError_t>(lr)));
+  CUDA_OK(cudaEventSynchronize(cb));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, ca, cb);
+  cudaEventDestroy(ca);
+  cudaEventDestroy(cb);
+  ex.device_ms += ms;
+  CUDA_OK(cudaMemcpyAsync(&ex.g, R.g, sizeof(GState), cudaMemcpyDeviceToHost, ex.stream));
+  CUDA_OK(cudaStreamSynchronize(ex.stream));
+  const long long n0 = static_cast<long long>(ex.log.size());
+  if (ex.g.log_n > n0) {
+    ex.log.resize(ex.g.log_n);
+    CUDA_OK(cudaMemcpyAsync(ex.log.data() + n0, R.log + n0, sizeof(Rec) * (ex.g.log_n - n0), cudaMemcpyDeviceToHost,
+                            ex.stream));
+  }
+  if (ex.g.phase == 2 || ex.g.error) {
+    ex.qs.resize(Q);
+    CUDA_OK(cudaMemcpyAsync(ex.qs.data(), R.qs, sizeof(QueryRun) * Q, cudaMemcpyDeviceToHost, ex.stream));
+  }
+  CUDA_OK(cudaStreamSynchronize(ex.stream));
+#endif
 }
 
 // Paged tree-KV store of one run (ctl_state.h kKvPage): `pages` physical
@@ -1659,6 +1786,50 @@ int spex_executor_run(spex_executor* ex, int trace, spex_totals* totals) {
   });
 }
 
+int spex_frontier_step(spex_executor* ex, long long iterations, int* done, char** events, size_t* events_len) {
+  return guarded([&] {
+    if (done) *done = 0;
+    if (ex->ran && !ex->step) fail(ERR_INVALID_ARGUMENT, "frontier_step: the executor already ran");
+#ifndef SPEX_EMU
+    if (ex->with_model) fail(ERR_INVALID_ARGUMENT, "frontier_step: stepwise execution is control only (no model)");
+#endif
+    if (ex->split_world > 1) fail(ERR_INVALID_ARGUMENT, "frontier_step: not with a split rank");
+    if (iterations < 0) fail(ERR_INVALID_ARGUMENT, "frontier_step: negative iteration count");
+    const bool first = !ex->step;
+    if (first) step_begin(*ex);
+    const long long from = static_cast<long long>(ex->log.size());
+    step_run(*ex, iterations);
+    if (ex->g.error == ERR_CAP_NODES || ex->g.error == ERR_CAP_STAGE || ex->g.error == ERR_CAP_STREAMS) {
+      step_release(*ex);
+      ex->ran = true;
+      fail(ex->g.error, "frontier_step: node capacity exhausted (a stepwise run cannot be replayed); "
+                        "rerun with a larger SPEX_NODE_CAP");
+    }
+    if (ex->g.error) {
+      step_release(*ex);
+      ex->ran = true;
+      fail(ex->g.error, "device control error at query " + std::to_string(ex->g.error_q) + " node " +
+                            std::to_string(static_cast<int>(ex->g.error_node)));
+    }
+    std::string out;
+    if (first) serialize_header(*ex, out);
+    for (long long i = from; i < static_cast<long long>(ex->log.size()); ++i) serialize_record(ex->log[i], out);
+    const bool finished = ex->g.phase == 2;
+    if (finished) {
+      serialize_footer(*ex, out);
+      step_release(*ex);
+      ex->ran = true;
+      if (done) *done = 1;
+    }
+    if (events) {
+      *events = static_cast<char*>(std::malloc(out.size() + 1));
+      std::memcpy(*events, out.data(), out.size());
+      (*events)[out.size()] = 0;
+    }
+    if (events_len) *events_len = out.size();
+  });
+}
+
 int spex_executor_log(spex_executor* ex, char** out_lines, size_t* out_len) {
   return guarded([&] {
     std::string s;
@@ -2015,6 +2186,7 @@ int spex_executor_query_finish(spex_executor* ex, double* out, int cap, int* n) 
 }
 
 void spex_executor_destroy(spex_executor* ex) {
+  if (ex) step_release(*ex);
 #ifndef SPEX_EMU
   if (ex && ex->emu_boxes) cudaFree(ex->emu_boxes);
   if (ex && ex->stream) cudaStreamDestroy(ex->stream);
