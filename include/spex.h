@@ -21,6 +21,8 @@
  *                             <- totsim::roofline_k_total / allocate_budgets
  *                                (budget.hpp:37-55, budget.cpp:23-96)
  *   spex_engine_advance       <- totsim::DecodeEngine::advance (sim.cpp:305-384)
+ *   spex_engine_create / add_stream / cancel / drop / step / done_tokens ...
+ *                             <- totsim::DecodeEngine as a handle (sim.hpp:165-220)
  *   spex_content_token_len / eval
  *                             <- RewardOracle::token_len / is_terminal / reward /
  *                                answer_label (sim.cpp:112-169)
@@ -325,6 +327,33 @@ int spex_engine_advance(const spex_engine_hw* hw, double now, double limit, spex
                         int* n_active, spex_engine_stream* staged, int* n_staged, const int* anc_key,
                         const int* anc_tokens, int n_keys, spex_engine_finished* out, int cap, int* n_out,
                         double* now_out);
+
+/* The decode engine as a handle (SURVEY.md §8b spex_engine_*; DecodeEngine,
+ * sim.hpp:165-220): the stream tables on the host side of the handle, each
+ * step's epochs on the device (the same code as spex_engine_advance). A stream
+ * names its strict ancestors by caller keys, unique per (tree, node) — e.g.
+ * tree << 32 | node — with their token lengths; the unique-KV-token cost
+ * (sim.cpp:54-78) deduplicates by key as the reference does by (tree, node).
+ *   spex_engine_create / destroy   DecodeEngine(hw)
+ *   spex_engine_add_stream         add_stream(id, tree, node, tokens, ready)   sim.cpp:204-214
+ *   spex_engine_cancel             cancel(id), *started = its return value      sim.cpp:216-233
+ *   spex_engine_drop               drop(id)                                     sim.cpp:235-249
+ *   spex_engine_step               advance(now, limit, out): finished streams
+ *                                  in out[cap], *reached = the clock reached    sim.cpp:305-384
+ *   spex_engine_done_tokens / stream_count / active_count / next_ready */
+typedef struct spex_engine spex_engine;
+int spex_engine_create(const spex_engine_hw* hw, int device, spex_engine** out);
+void spex_engine_destroy(spex_engine* e);
+int spex_engine_add_stream(spex_engine* e, int id, uint32_t node, int tokens, double ready, const uint64_t* anc_keys,
+                           const int* anc_tokens, int n_anc);
+int spex_engine_cancel(spex_engine* e, int id, int* started);
+int spex_engine_drop(spex_engine* e, int id);
+int spex_engine_step(spex_engine* e, double now, double limit, spex_engine_finished* out, int cap, int* n_out,
+                     double* reached);
+int spex_engine_done_tokens(const spex_engine* e, int id);
+int spex_engine_stream_count(const spex_engine* e);
+int spex_engine_active_count(const spex_engine* e);
+double spex_engine_next_ready(const spex_engine* e);
 
 /* run_once: traced run returning totals and the JSON-lines log. */
 int spex_run_once(const char* config_json, uint64_t seed, const char* flags_csv,

@@ -15,6 +15,7 @@
 //   roofline_k_total    budget.cpp:23-39
 //   RewardOracle::*     sim.cpp:106-169
 //   unique_kv_tokens    sim.cpp:54-68
+//   DecodeEngine        sim.cpp:204-384 (ref_engine_*, over SearchTrees built by ref_tree_*)
 #include <chrono>
 #include <cstdint>
 #include <cstdlib>
@@ -34,6 +35,7 @@
 #include "totsim/sim.hpp"
 #include "totsim/termination.hpp"
 #include "totsim/trace.hpp"
+#include "totsim/tree.hpp"
 
 using namespace totsim;
 
@@ -292,6 +294,57 @@ int ref_workload(int n, std::uint64_t seed, int max_depth, std::uint64_t* seeds,
   }
   return 0;
 }
+
+/* The reference DecodeEngine over reference SearchTrees (engine-handle parity tests). */
+void* ref_tree_create(int prompt_tokens, std::uint64_t seed) { return new SearchTree(prompt_tokens, seed); }
+void ref_tree_destroy(void* t) { delete static_cast<SearchTree*>(t); }
+int ref_tree_add(void* t, std::uint32_t parent, int token_len) {
+  try {
+    return static_cast<int>(static_cast<SearchTree*>(t)->add_node(parent, token_len, false));
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+void* ref_engine_create(const double* hw) {
+  HardwareProfile h;
+  h.weight_bytes = hw[0];
+  h.mem_bandwidth = hw[1];
+  h.peak_compute = hw[2];
+  h.flops_per_token = hw[3];
+  h.kv_bytes_per_token = hw[4];
+  h.reward_latency = hw[5];
+  return new DecodeEngine(h);
+}
+void ref_engine_destroy(void* e) { delete static_cast<DecodeEngine*>(e); }
+int ref_engine_add_stream(void* e, int id, void* tree, std::uint32_t node, int tokens, double ready) {
+  try {
+    static_cast<DecodeEngine*>(e)->add_stream(id, static_cast<SearchTree*>(tree), node, tokens, ready);
+    return 0;
+  } catch (const Error& x) {
+    g_err = x.what();
+    return static_cast<int>(x.code()) + 1;
+  }
+}
+int ref_engine_cancel(void* e, int id) { return static_cast<DecodeEngine*>(e)->cancel(id) ? 1 : 0; }
+void ref_engine_drop(void* e, int id) { static_cast<DecodeEngine*>(e)->drop(id); }
+double ref_engine_advance(void* e, double now, double limit, int* ids, int* tokens, int* cancelled, double* times,
+                          int cap, int* n) {
+  std::vector<DecodeEngine::Finished> out;
+  const double r = static_cast<DecodeEngine*>(e)->advance(now, limit, out);
+  *n = static_cast<int>(out.size());
+  for (int i = 0; i < *n && i < cap; ++i) {
+    ids[i] = out[i].id;
+    tokens[i] = out[i].tokens_done;
+    cancelled[i] = out[i].cancelled ? 1 : 0;
+    times[i] = out[i].time;
+  }
+  return r;
+}
+int ref_engine_done_tokens(void* e, int id) { return static_cast<DecodeEngine*>(e)->done_tokens(id); }
+int ref_engine_stream_count(void* e) { return static_cast<DecodeEngine*>(e)->stream_count(); }
+int ref_engine_active_count(void* e) { return static_cast<DecodeEngine*>(e)->active_count(); }
+double ref_engine_next_ready(void* e) { return static_cast<DecodeEngine*>(e)->next_ready(); }
 
 }  // extern "C"
 

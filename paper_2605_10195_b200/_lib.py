@@ -175,6 +175,20 @@ _EXPORTS = {
          ctypes.c_void_p, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int),
          ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_double)],
         ctypes.c_int),
+    "spex_engine_create": ([ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)], ctypes.c_int),
+    "spex_engine_destroy": ([ctypes.c_void_p], None),
+    "spex_engine_add_stream": (
+        [ctypes.c_void_p, ctypes.c_int, ctypes.c_uint32, ctypes.c_int, ctypes.c_double,
+         ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_int), ctypes.c_int], ctypes.c_int),
+    "spex_engine_cancel": ([ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
+    "spex_engine_drop": ([ctypes.c_void_p, ctypes.c_int], ctypes.c_int),
+    "spex_engine_step": (
+        [ctypes.c_void_p, ctypes.c_double, ctypes.c_double, ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(ctypes.c_int),
+         ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
+    "spex_engine_done_tokens": ([ctypes.c_void_p, ctypes.c_int], ctypes.c_int),
+    "spex_engine_stream_count": ([ctypes.c_void_p], ctypes.c_int),
+    "spex_engine_active_count": ([ctypes.c_void_p], ctypes.c_int),
+    "spex_engine_next_ready": ([ctypes.c_void_p], ctypes.c_double),
     "spex_budget_k_total": (
         [ctypes.POINTER(ctypes.c_double), ctypes.c_int, ctypes.c_double, ctypes.c_int, ctypes.POINTER(ctypes.c_int)],
         ctypes.c_int),

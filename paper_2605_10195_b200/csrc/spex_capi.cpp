@@ -2333,3 +2333,155 @@ extern "C" int spex_budget_allocate(const int* capacity, const double* hit_ema, 
   return 0;
 }
 #endif
+
+// ============================================================ engine handle
+// The decode engine as a handle (SURVEY.md §8b spex_engine_*): the stream
+// tables live here, each step runs DecodeEngine::advance's epochs on the
+// device (spex_engine_advance, csrc/spex_hooks.cu). A stream names its strict
+// ancestors by caller keys (unique per (tree, node), e.g. tree << 32 | node)
+// with their token lengths: the engine's unique-KV-token cost (sim.cpp:54-78)
+// deduplicates by key, as the reference does by (tree pointer, node).
+struct spex_engine {
+  spex_engine_hw hw{};
+  int device = 0;
+  struct Stream {
+    spex_engine_stream s{};
+    uint32_t node = 0;
+    std::vector<int> anc;  // key indices
+  };
+  std::vector<Stream> active, staged;
+  std::unordered_map<uint64_t, int> key_index;
+  std::vector<int> key_tokens;
+};
+
+extern "C" {
+
+int spex_engine_create(const spex_engine_hw* hw, int device, spex_engine** out) {
+  return guarded([&] {
+    if (!hw || !out) fail(ERR_INVALID_ARGUMENT, "engine_create: null argument");
+    auto* e = new spex_engine();
+    e->hw = *hw;
+    e->device = device;
+    *out = e;
+  });
+}
+
+void spex_engine_destroy(spex_engine* e) { delete e; }
+
+int spex_engine_add_stream(spex_engine* e, int id, uint32_t node, int tokens, double ready, const uint64_t* anc_keys,
+                           const int* anc_tokens, int n_anc) {
+  return guarded([&] {
+    if (tokens <= 0) fail(ERR_INVALID_ARGUMENT, "add_stream: non-positive token budget");  // sim.cpp:206
+    if (n_anc < 0 || (n_anc > 0 && (!anc_keys || !anc_tokens))) fail(ERR_INVALID_ARGUMENT, "add_stream: ancestors");
+    spex_engine::Stream st;
+    st.s.id = id;
+    st.s.remaining = tokens;
+    st.s.ready = ready;
+    st.node = node;
+    for (int i = 0; i < n_anc; ++i) {
+      auto it = e->key_index.emplace(anc_keys[i], static_cast<int>(e->key_tokens.size()));
+      if (it.second) e->key_tokens.push_back(anc_tokens[i]);
+      else e->key_tokens[it.first->second] = anc_tokens[i];
+      st.anc.push_back(it.first->second);
+    }
+    e->staged.push_back(std::move(st));
+  });
+}
+
+// DecodeEngine::cancel (sim.cpp:216-233): *started = its return value
+int spex_engine_cancel(spex_engine* e, int id, int* started) {
+  return guarded([&] {
+    int r = 1;
+    bool hit = false;
+    for (auto& st : e->active)
+      if (st.s.id == id && !st.s.cancelled) {
+        st.s.cancelled = 1;
+        st.s.remaining = 1;
+        hit = true;
+        break;
+      }
+    if (!hit)
+      for (auto it = e->staged.begin(); it != e->staged.end(); ++it)
+        if (it->s.id == id) {
+          e->staged.erase(it);
+          r = 0;
+          break;
+        }
+    if (started) *started = r;
+  });
+}
+
+int spex_engine_drop(spex_engine* e, int id) {  // DecodeEngine::drop (sim.cpp:235-249)
+  return guarded([&] {
+    for (auto* v : {&e->active, &e->staged})
+      for (auto it = v->begin(); it != v->end(); ++it)
+        if (it->s.id == id) {
+          v->erase(it);
+          return;
+        }
+  });
+}
+
+// DecodeEngine::advance (sim.cpp:305-384) on the handle's streams
+int spex_engine_step(spex_engine* e, double now, double limit, spex_engine_finished* out, int cap, int* n_out,
+                     double* reached) {
+  return guarded([&] {
+    const int na0 = static_cast<int>(e->active.size()), ns0 = static_cast<int>(e->staged.size());
+    const int tot = std::max(na0 + ns0, 1);
+    std::vector<spex_engine_stream> act(tot), stg(tot);
+    std::vector<int> anc;
+    std::unordered_map<int, const spex_engine::Stream*> by_id;
+    auto pack = [&](const spex_engine::Stream& st) {
+      spex_engine_stream s = st.s;
+      s.anc_off = static_cast<int>(anc.size());
+      s.anc_n = static_cast<int>(st.anc.size());
+      anc.insert(anc.end(), st.anc.begin(), st.anc.end());
+      by_id[st.s.id] = &st;
+      return s;
+    };
+    int na = 0, ns = 0;
+    for (const auto& st : e->active) act[na++] = pack(st);
+    for (const auto& st : e->staged) stg[ns++] = pack(st);
+    int nf = 0;
+    double now_out = now;
+#ifndef SPEX_EMU
+    CUDA_OK(cudaSetDevice(e->device));
+#endif
+    const int rc = spex_engine_advance(&e->hw, now, limit, act.data(), &na, stg.data(), &ns, anc.data(),
+                                       e->key_tokens.data(), static_cast<int>(e->key_tokens.size()), out, cap, &nf,
+                                       &now_out);
+    if (rc) fail(rc, std::string("engine_step: ") + g_err);
+    auto unpack = [&](const spex_engine_stream& s) {
+      spex_engine::Stream st = *by_id.at(s.id);
+      st.s.remaining = s.remaining;
+      st.s.done = s.done;
+      st.s.cancelled = s.cancelled;
+      return st;
+    };
+    std::vector<spex_engine::Stream> a2, s2;
+    for (int i = 0; i < na; ++i) a2.push_back(unpack(act[i]));
+    for (int i = 0; i < ns; ++i) s2.push_back(unpack(stg[i]));
+    e->active = std::move(a2);
+    e->staged = std::move(s2);
+    if (n_out) *n_out = nf;
+    if (reached) *reached = now_out;
+  });
+}
+
+int spex_engine_done_tokens(const spex_engine* e, int id) {  // DecodeEngine::done_tokens (sim.cpp:251-257)
+  for (const auto* v : {&e->active, &e->staged})
+    for (const auto& st : *v)
+      if (st.s.id == id) return st.s.done;
+  return 0;
+}
+
+int spex_engine_stream_count(const spex_engine* e) { return static_cast<int>(e->active.size() + e->staged.size()); }
+int spex_engine_active_count(const spex_engine* e) { return static_cast<int>(e->active.size()); }
+
+double spex_engine_next_ready(const spex_engine* e) {  // DecodeEngine::next_ready (sim.cpp:259-263)
+  double r = HUGE_VAL;
+  for (const auto& st : e->staged) r = std::min(r, st.s.ready);
+  return r;
+}
+
+}  // extern "C"
