@@ -26,6 +26,7 @@
  *   spex_content_token_len / eval
  *                             <- RewardOracle::token_len / is_terminal / reward /
  *                                answer_label (sim.cpp:112-169)
+ *   spex_score_batch          <- RewardOracle::reward realised by the PRM, standalone
  *   spex_executor_set_reward_source
  *                             <- RewardOracle::reward (sim.hpp:115-142), the
  *                                content oracle or the PRM's score (model mode)
@@ -354,6 +355,17 @@ int spex_engine_done_tokens(const spex_engine* e, int id);
 int spex_engine_stream_count(const spex_engine* e);
 int spex_engine_active_count(const spex_engine* e);
 double spex_engine_next_ready(const spex_engine* e);
+
+/* PRM scoring of standalone token sequences (SURVEY.md §8b spex_score_batch;
+ * the score hook RewardOracle::reward, sim.hpp:115-142, realised by the PRM):
+ * sequence i is tokens[offsets[i], offsets[i + 1]), scores[i] the PRM's
+ * value-head score (sigmoid) at its last token — the executor's PRM arithmetic
+ * (K4 prefill tiles on the tensor cores) with the weights
+ * spex_executor_set_model gives the PRM for the same weight_seed. Host buffers
+ * in and out; InvalidArgument for an unknown shape, an empty sequence or a
+ * token outside the vocabulary. */
+int spex_score_batch(const char* prm_shape, uint64_t weight_seed, const int32_t* tokens, const int64_t* offsets,
+                     int n, float* scores, int device);
 
 /* run_once: traced run returning totals and the JSON-lines log. */
 int spex_run_once(const char* config_json, uint64_t seed, const char* flags_csv,

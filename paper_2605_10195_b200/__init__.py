@@ -315,6 +315,25 @@ def run_batch(cfg: Any, seeds, flags: SpexFlags | str | None = None, device: int
     return [RunTotals(**t.as_dict()) for t in tots], ms.value
 
 
+def score_batch(prm_shape: str, weight_seed: int, sequences, device: int = 0) -> list:
+    """PRM scores of standalone token sequences (spex_score_batch): the value
+    head at each sequence's last token, with the PRM weights
+    Executor.set_model gives for ``weight_seed``."""
+    L = _lib.lib()
+    if not L.spex_device_ok():
+        raise RuntimeError("no sm_100 CUDA device: the SPEX B200 path has no CPU fallback")
+    seqs = [list(map(int, s)) for s in sequences]
+    flat = [t for s in seqs for t in s]
+    offs = [0]
+    for s in seqs:
+        offs.append(offs[-1] + len(s))
+    toks = (ctypes.c_int32 * max(1, len(flat)))(*flat)
+    off = (ctypes.c_int64 * len(offs))(*offs)
+    out = (ctypes.c_float * max(1, len(seqs)))()
+    _check(L.spex_score_batch(prm_shape.encode(), int(weight_seed), toks, off, len(seqs), out, device))
+    return [out[i] for i in range(len(seqs))]
+
+
 def split_run(cfg: Any, seed: int, world: int, flags: SpexFlags | str | None = None, trace: bool = True,
               device: int = 0) -> list:
     """Every rank of one split job (shard.py) on one device, as CTAs of one
@@ -340,5 +359,6 @@ __all__ = [
     "device_ok",
     "run_batch",
     "run_once",
+    "score_batch",
     "split_run",
 ]

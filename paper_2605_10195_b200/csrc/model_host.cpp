@@ -836,3 +836,105 @@ void run_model_schedule(const ModelRunConfig& mc, const ScheduleView& sv, ModelR
 }
 
 }  // namespace spex
+
+// ------------------------------------------------- standalone PRM scoring
+// spex_score_batch: each sequence is one thought with no ancestors (one own
+// segment, causal within it), its tokens the PRM rows, 16-row tiles on the
+// tensor-core tile kernel, the value head at the last row: the arithmetic of
+// the executor's PRM scoring (run_model_schedule's PRM entries), with the
+// weights of spex_executor_set_model's PRM for the same seed. Its own model
+// instance and buffers, grown on demand; serialised with the executor runs.
+namespace spex {
+namespace {
+struct ScoreCache {
+  Model* m = nullptr;
+  ModelShape sh{};
+  uint64_t seed = 0;
+  long long rows_cap = 0;
+  int seq_cap = 0;
+  RowDesc* rows = nullptr;
+  Segment* segs = nullptr;
+  TileDesc* tiles = nullptr;
+  int* last_row = nullptr;
+  float* scores = nullptr;
+  std::vector<void*> bufs;
+  cudaStream_t st = nullptr;
+};
+ScoreCache g_score;
+}  // namespace
+
+void prm_score_sequences(const ModelShape& sh, uint64_t weight_seed, const int* tokens, const long long* offsets,
+                         int n, float* scores, int device) {
+  if (n <= 0) return;
+  CK(cudaSetDevice(device));
+  long long M = 0;
+  int ntiles = 0;
+  for (int i = 0; i < n; ++i) {
+    const long long len = offsets[i + 1] - offsets[i];
+    if (len <= 0) throw std::runtime_error("score_batch: empty sequence " + std::to_string(i));
+    for (long long j = offsets[i]; j < offsets[i + 1]; ++j)
+      if (tokens[j] < 0 || tokens[j] >= sh.V) throw std::runtime_error("score_batch: token id out of the vocabulary");
+    M += len;
+    ntiles += static_cast<int>((len + kTileRows - 1) / kTileRows);
+  }
+  if (M > (1LL << 30)) throw std::runtime_error("score_batch: too many tokens");
+  ScoreCache& c = g_score;
+  if (!c.st) CK(cudaStreamCreateWithFlags(&c.st, cudaStreamNonBlocking));
+  if (!c.m || !same_shape(c.sh, sh) || c.seed != weight_seed || c.m->slots < M || c.m->max_rows < M) {
+    CK(cudaStreamSynchronize(c.st));
+    delete c.m;
+    const long long cap = std::max<long long>(M, 4096);
+    c.m = make_model(sh, true, weight_seed ^ 0x50524d00ULL, cap + cap / 8 + 1024, static_cast<int>(cap + cap / 8 + 256),
+                     c.st);
+    c.sh = sh;
+    c.seed = weight_seed;
+  }
+  if (c.rows_cap < M || c.seq_cap < n) {
+    CK(cudaStreamSynchronize(c.st));
+    for (void* p : c.bufs) cudaFree(p);
+    c.bufs.clear();
+    c.rows_cap = std::max<long long>(M, c.rows_cap);
+    c.seq_cap = std::max(n, c.seq_cap);
+    c.rows = dalloc<RowDesc>(c.rows_cap, c.bufs);
+    c.segs = dalloc<Segment>(c.seq_cap, c.bufs);
+    c.tiles = dalloc<TileDesc>(c.rows_cap, c.bufs);
+    c.last_row = dalloc<int>(c.seq_cap, c.bufs);
+    c.scores = dalloc<float>(c.seq_cap, c.bufs);
+  }
+  std::vector<RowDesc> rows(M);
+  std::vector<Segment> segs(n);
+  std::vector<TileDesc> tiles;
+  std::vector<int> last(n);
+  tiles.reserve(ntiles);
+  long long r = 0;
+  for (int i = 0; i < n; ++i) {
+    const long long len = offsets[i + 1] - offsets[i];
+    const long long base = r;  // the sequence's KV slots: its rows' own
+    segs[i] = Segment{base, static_cast<int>(len), 0};
+    for (long long j = 0; j < len; ++j, ++r) {
+      RowDesc& d = rows[r];
+      d.q = i;
+      d.node = 0;
+      d.pos = static_cast<int>(j);
+      d.abs_pos = static_cast<int>(j);
+      d.slot = base + j;
+      d.seg_off = i;
+      d.nseg = 1;
+      d.token = tokens[offsets[i] + j];
+      d.pad = 0;
+    }
+    for (long long j = 0; j < len; j += kTileRows)
+      tiles.push_back(TileDesc{static_cast<int>(base + j), static_cast<int>(std::min<long long>(kTileRows, len - j))});
+    last[i] = static_cast<int>(r - 1);
+  }
+  CK(cudaMemcpyAsync(c.rows, rows.data(), sizeof(RowDesc) * M, cudaMemcpyHostToDevice, c.st));
+  CK(cudaMemcpyAsync(c.segs, segs.data(), sizeof(Segment) * n, cudaMemcpyHostToDevice, c.st));
+  CK(cudaMemcpyAsync(c.tiles, tiles.data(), sizeof(TileDesc) * tiles.size(), cudaMemcpyHostToDevice, c.st));
+  CK(cudaMemcpyAsync(c.last_row, last.data(), sizeof(int) * n, cudaMemcpyHostToDevice, c.st));
+  forward(*c.m, c.rows, c.segs, static_cast<int>(M), c.st, nullptr, c.tiles, static_cast<int>(tiles.size()));
+  spex_k_value_head(c.m->Xn, sh.d, c.last_row, n, c.m->vhead, c.scores, c.st);
+  CK(cudaMemcpyAsync(scores, c.scores, sizeof(float) * n, cudaMemcpyDeviceToHost, c.st));
+  CK(cudaStreamSynchronize(c.st));
+}
+
+}  // namespace spex

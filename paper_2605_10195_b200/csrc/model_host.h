@@ -85,5 +85,9 @@ ModelShape shape_by_name(const std::string& name);
 long long model_weight_params(const ModelShape& s, bool prm);
 double model_matmul_flops_per_row(const ModelShape& s, bool prm);
 void run_model_schedule(const ModelRunConfig& mc, const ScheduleView& sv, ModelRunResult* res, cudaStream_t st);
+// PRM scores of standalone token sequences (spex_score_batch): sequence i is
+// tokens[offsets[i], offsets[i + 1]); scores[i] = the value head at its last token.
+void prm_score_sequences(const ModelShape& sh, uint64_t weight_seed, const int* tokens, const long long* offsets,
+                         int n, float* scores, int device);
 
 }  // namespace spex

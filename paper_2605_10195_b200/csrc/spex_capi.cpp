@@ -2485,3 +2485,26 @@ double spex_engine_next_ready(const spex_engine* e) {  // DecodeEngine::next_rea
 }
 
 }  // extern "C"
+
+extern "C" int spex_score_batch(const char* prm_shape, uint64_t weight_seed, const int32_t* tokens,
+                                const int64_t* offsets, int n, float* scores, int device) {
+  return guarded([&] {
+    if (n < 0 || (n > 0 && (!tokens || !offsets || !scores))) fail(ERR_INVALID_ARGUMENT, "score_batch: arguments");
+#ifdef SPEX_EMU
+    (void)prm_shape;
+    (void)weight_seed;
+    (void)device;
+    fail(ERR_INVALID_ARGUMENT, "score_batch needs the CUDA build");
+#else
+    std::lock_guard<std::mutex> lk(g_model_mu);  // the forward's kernels share process-wide state
+    try {
+      prm_score_sequences(shape_by_name(prm_shape ? prm_shape : ""), weight_seed, tokens,
+                          reinterpret_cast<const long long*>(offsets), n, scores, device);
+    } catch (const SpexError&) {
+      throw;
+    } catch (const std::exception& e) {
+      fail(ERR_INVALID_ARGUMENT, std::string("score_batch: ") + e.what());
+    }
+#endif
+  });
+}
