@@ -20,6 +20,8 @@
  *   spex_budget_k_total / allocate
  *                             <- totsim::roofline_k_total / allocate_budgets
  *                                (budget.hpp:37-55, budget.cpp:23-96)
+ *   spex_termination_should_terminate
+ *                             <- totsim::AnswerTally::should_terminate (termination.cpp:30-48)
  *   spex_engine_advance       <- totsim::DecodeEngine::advance (sim.cpp:305-384)
  *   spex_engine_create / add_stream / cancel / drop / step / done_tokens ...
  *                             <- totsim::DecodeEngine as a handle (sim.hpp:165-220)
@@ -328,6 +330,14 @@ int spex_engine_advance(const spex_engine_hw* hw, double now, double limit, spex
                         int* n_active, spex_engine_stream* staged, int* n_staged, const int* anc_key,
                         const int* anc_tokens, int n_keys, spex_engine_finished* out, int cap, int* n_out,
                         double* now_out);
+
+/* Termination hook: AnswerTally::should_terminate (termination.hpp:15-55,
+ * termination.cpp:30-48) for n_tallies tallies, on the device with the
+ * control kernel's own code. Tally t's labels are [offsets[t],
+ * offsets[t + 1]) in the tally's label (std::map) order with their answer
+ * counts and weight sums; n_total[t] its answer count; out[t] = 0/1. */
+int spex_termination_should_terminate(const int* counts, const double* weights, const int* offsets,
+                                      const int* n_total, int n_tallies, int min_answers, double alpha, int* out);
 
 /* The decode engine as a handle (SURVEY.md §8b spex_engine_*; DecodeEngine,
  * sim.hpp:165-220): the stream tables on the host side of the handle, each

@@ -295,6 +295,14 @@ int ref_workload(int n, std::uint64_t seed, int max_depth, std::uint64_t* seeds,
   return 0;
 }
 
+/* AnswerTally::should_terminate after recording answers (label index, weight)
+ * as labels "a<idx>" (termination.cpp:7-48). */
+int ref_should_terminate(const int* label, const double* weight, int n, int min_answers, double alpha) {
+  AnswerTally t;
+  for (int i = 0; i < n; ++i) t.record_answer("a" + std::to_string(label[i]), weight[i]);
+  return t.should_terminate(min_answers, alpha) ? 1 : 0;
+}
+
 /* The reference DecodeEngine over reference SearchTrees (engine-handle parity tests). */
 void* ref_tree_create(int prompt_tokens, std::uint64_t seed) { return new SearchTree(prompt_tokens, seed); }
 void ref_tree_destroy(void* t) { delete static_cast<SearchTree*>(t); }

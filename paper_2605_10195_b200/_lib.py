@@ -189,6 +189,10 @@ _EXPORTS = {
     "spex_engine_stream_count": ([ctypes.c_void_p], ctypes.c_int),
     "spex_engine_active_count": ([ctypes.c_void_p], ctypes.c_int),
     "spex_engine_next_ready": ([ctypes.c_void_p], ctypes.c_double),
+    "spex_termination_should_terminate": (
+        [ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int),
+         ctypes.POINTER(ctypes.c_int), ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.POINTER(ctypes.c_int)],
+        ctypes.c_int),
     "spex_score_batch": (
         [ctypes.c_char_p, ctypes.c_uint64, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int64),
          ctypes.c_int, ctypes.POINTER(ctypes.c_float), ctypes.c_int], ctypes.c_int),

@@ -614,26 +614,46 @@ SPEX_HD int leading_label(const QC& x) {
   return best;
 }
 
-// termination.cpp:30-48
-SPEX_HDNI bool should_terminate(const QC& x, int min_answers, double alpha) {
-  const QueryRun* qr = x.qr;
-  if (qr->n_answers < min_answers || qr->n_labels == 0) return false;
-  if (qr->n_labels < 2) return true;
-  const QueryTally* ta = &x.R->q_tally[x.q];
-  int first = -1, second = -1;
-  for (int r = 0; r < x.c->answer_alphabet; ++r) {
-    int l = x.c->lex_order[r];
-    if (ta->count[l] == 0) continue;
-    if (first < 0 || ta->w[l] > ta->w[first]) {
-      second = first;
-      first = l;
-    } else if (second < 0 || ta->w[l] > ta->w[second]) {
-      second = l;
+// AnswerTally::should_terminate (termination.cpp:30-48) over a tally whose
+// n_slots label slots are visited in std::map (lexicographic) order; slot r's
+// (answer count, weight sum) come from get(r, &count, &w), empty slots skipped.
+// Shared by the control kernel and the spex_termination_should_terminate hook.
+template <class F>
+SPEX_HD bool tally_should_terminate(int n_total, int n_labels, int n_slots, F get, int min_answers, double alpha) {
+  if (n_total < min_answers || n_labels == 0) return false;
+  if (n_labels < 2) return true;
+  int c1 = 0, c2 = 0;
+  double w1 = 0.0, w2 = 0.0;
+  bool has1 = false, has2 = false;
+  for (int r = 0; r < n_slots; ++r) {
+    int cnt;
+    double w;
+    get(r, &cnt, &w);
+    if (cnt == 0) continue;
+    if (!has1 || w > w1) {
+      c2 = c1, w2 = w1, has2 = has1;
+      c1 = cnt, w1 = w, has1 = true;
+    } else if (!has2 || w > w2) {
+      c2 = cnt, w2 = w, has2 = true;
     }
   }
-  double margin = ta->w[first] - ta->w[second];
-  double avg_second = ta->count[second] > 0 ? ta->w[second] / ta->count[second] : 0.0;
+  const double margin = w1 - w2;
+  const double avg_second = c2 > 0 ? w2 / c2 : 0.0;
   return margin > alpha * avg_second;
+}
+
+SPEX_HDNI bool should_terminate(const QC& x, int min_answers, double alpha) {
+  const QueryRun* qr = x.qr;
+  const QueryTally* ta = &x.R->q_tally[x.q];
+  const int* order = x.c->lex_order;
+  return tally_should_terminate(
+      qr->n_answers, qr->n_labels, x.c->answer_alphabet,
+      [&](int r, int* cnt, double* w) {
+        const int l = order[r];
+        *cnt = ta->count[l];
+        *w = ta->w[l];
+      },
+      min_answers, alpha);
 }
 
 // ============================================================ executor.cpp

@@ -2309,6 +2309,26 @@ extern "C" int spex_content_eval(const uint64_t* path_hash, const int* offsets, 
   return 0;
 }
 
+extern "C" int spex_termination_should_terminate(const int* counts, const double* weights, const int* offsets,
+                                                 const int* n_total, int n_tallies, int min_answers, double alpha,
+                                                 int* out) {
+  for (int t = 0; t < n_tallies; ++t) {
+    const int b = offsets[t], m = offsets[t + 1] - b;
+    int labels = 0;
+    for (int r = 0; r < m; ++r) labels += counts[b + r] > 0;
+    out[t] = tally_should_terminate(
+                 n_total[t], labels, m,
+                 [&](int r, int* c, double* x) {
+                   *c = counts[b + r];
+                   *x = weights[b + r];
+                 },
+                 min_answers, alpha)
+                 ? 1
+                 : 0;
+  }
+  return 0;
+}
+
 extern "C" int spex_engine_advance(const spex_engine_hw*, double, double, spex_engine_stream*, int*,
                                    spex_engine_stream*, int*, const int*, const int*, int, spex_engine_finished*, int,
                                    int*, double*) {

@@ -134,6 +134,25 @@ __global__ void k_total_kernel(double weight_bytes, double mem_bandwidth, double
 }
 
 // allocate_budgets (budget.cpp:45-96): one block, the control's allocate_block.
+// AnswerTally::should_terminate per tally (the control kernel's tally_should_terminate)
+__global__ void terminate_kernel(const int* count, const double* w, const int* off, const int* n_total, int n,
+                                 int min_answers, double alpha, int* out) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const int b = off[t], m = off[t + 1] - b;
+  int labels = 0;
+  for (int r = 0; r < m; ++r) labels += count[b + r] > 0;
+  out[t] = tally_should_terminate(
+               n_total[t], labels, m,
+               [&](int r, int* c, double* x) {
+                 *c = count[b + r];
+                 *x = w[b + r];
+               },
+               min_answers, alpha)
+               ? 1
+               : 0;
+}
+
 __global__ void __launch_bounds__(256) allocate_kernel(const int* capacity, const double* hit_ema,
                                                        const double* kv_bytes, int n, int k_total, double tau,
                                                        double weight_bytes, double* score, double* w, int* out,
@@ -567,4 +586,28 @@ extern "C" int spex_engine_advance(const spex_engine_hw* hw, double now, double 
   }
   if (rc) return rc;
   return status ? status : finish();
+}
+
+extern "C" int spex_termination_should_terminate(const int* counts, const double* weights, const int* offsets,
+                                                 const int* n_total, int n_tallies, int min_answers, double alpha,
+                                                 int* out) {
+  std::lock_guard<std::mutex> lk(g_hook_mu);
+  if (int rc = ensure_stream()) return rc;
+  if (n_tallies <= 0) return 0;
+  const int n = offsets[n_tallies];
+  int rc;
+  {
+    Dev d;
+    int* dc = d.put(counts, n);
+    double* dw = d.put(weights, n);
+    int* doff = d.put(offsets, n_tallies + 1);
+    int* dn = d.put(n_total, n_tallies);
+    int* dout = d.put<int>(nullptr, n_tallies);
+    if ((n > 0 && (!dc || !dw)) || !doff || !dn || !dout) return 200;
+    terminate_kernel<<<(n_tallies + 127) / 128, 128, 0, g_hook_stream>>>(dc, dw, doff, dn, n_tallies, min_answers,
+                                                                          alpha, dout);
+    d.get(out, dout, n_tallies);
+    rc = finish();
+  }
+  return rc ? rc : finish();
 }

@@ -52,3 +52,39 @@ def check_hooks(L, R):
                                k_total, tau, (ctypes.c_double * 6)(*hw), ref)
         assert list(got) == list(ref), (n, k_total, tau)
     
+
+    # AnswerTally::should_terminate vs the reference: random answer streams over
+    # up to 12 labels (label order = the tally's std::map order of "a<idx>")
+    R.ref_should_terminate.argtypes = [ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_double), ctypes.c_int,
+                                       ctypes.c_int, ctypes.c_double]
+    tallies, refs, params = [], [], []
+    for _ in range(400):
+        n = rng.randint(0, 14)
+        k = rng.randint(1, 12)
+        lab = [rng.randrange(k) for _ in range(n)]
+        w = [rng.choice([0.0, 1.0, 0.5, rng.random()]) for _ in range(n)]
+        min_a = rng.randint(0, 10)
+        alpha = rng.choice([0.0, 0.5, 1.0, 1e18])
+        agg = {}
+        for l, x in zip(lab, w):
+            c, s_ = agg.get(f"a{l}", (0, 0.0))
+            agg[f"a{l}"] = (c + 1, s_ + x)
+        order = sorted(agg)  # std::map<std::string> order
+        tallies.append(([agg[o][0] for o in order], [agg[o][1] for o in order], n))
+        params.append((min_a, alpha))
+        refs.append(R.ref_should_terminate((ctypes.c_int * max(1, n))(*lab), (ctypes.c_double * max(1, n))(*w), n,
+                                           min_a, alpha))
+    for (min_a, alpha) in sorted(set(params)):
+        idx = [i for i, p in enumerate(params) if p == (min_a, alpha)]
+        cnt = [c for i in idx for c in tallies[i][0]]
+        wts = [x for i in idx for x in tallies[i][1]]
+        offs = [0]
+        for i in idx:
+            offs.append(offs[-1] + len(tallies[i][0]))
+        ntot = [tallies[i][2] for i in idx]
+        out = (ctypes.c_int * len(idx))()
+        assert L.spex_termination_should_terminate((ctypes.c_int * max(1, len(cnt)))(*cnt),
+                                                   (ctypes.c_double * max(1, len(wts)))(*wts),
+                                                   (ctypes.c_int * len(offs))(*offs), (ctypes.c_int * len(ntot))(*ntot),
+                                                   len(idx), min_a, alpha, out) == 0
+        assert list(out) == [refs[i] for i in idx], (min_a, alpha)
