@@ -20,6 +20,7 @@
  *   spex_budget_k_total / allocate
  *                             <- totsim::roofline_k_total / allocate_budgets
  *                                (budget.hpp:37-55, budget.cpp:23-96)
+ *   spex_speculation_dfs_plan <- totsim::dfs_speculative_select (speculation.cpp:182-218)
  *   spex_termination_should_terminate
  *                             <- totsim::AnswerTally::should_terminate (termination.cpp:30-48)
  *   spex_engine_advance       <- totsim::DecodeEngine::advance (sim.cpp:305-384)
@@ -330,6 +331,21 @@ int spex_engine_advance(const spex_engine_hw* hw, double now, double limit, spex
                         int* n_active, spex_engine_stream* staged, int* n_staged, const int* anc_key,
                         const int* anc_tokens, int n_keys, spex_engine_finished* out, int cap, int* n_out,
                         double* now_out);
+
+/* T1 planning hook: dfs_speculative_select (speculation.hpp:95-139,
+ * speculation.cpp:182-218) on one tree, on the device with the control
+ * kernel's dfs_plan (Algorithm 1's simulated selections over a visit overlay
+ * with phantom children). The tree: n_nodes nodes in NodeId order (children in
+ * NodeId order, as add_node appends them), parent[0] = -1, status = the
+ * NodeStatus ordinal, bits = terminal | gen_done << 1 | has_reward << 2, the
+ * reward where present; the PolicyConfig fields; k <= 64. Writes up to k
+ * targets (node, predicted distance); 0 targets for rebase_bfs (frontier
+ * policies plan by allocation). */
+int spex_speculation_dfs_plan(const int32_t* parent, const uint8_t* status, const uint8_t* bits, const double* reward,
+                              const int32_t* visits, const double* value, const int32_t* depth, int n_nodes,
+                              int terminal_answers, int family, double exploration_c, int width,
+                              const int32_t* depth_widths, int n_depth_widths, int target_answers, int k,
+                              uint32_t* out_node, int32_t* out_dist, int* n_out);
 
 /* Termination hook: AnswerTally::should_terminate (termination.hpp:15-55,
  * termination.cpp:30-48) for n_tallies tallies, on the device with the

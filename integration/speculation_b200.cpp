@@ -1,6 +1,11 @@
-// integration/termination_b200.cpp — the reference-side binding of the B200
-// termination and BFS-speculation hooks (include/spex.h).
+// integration/speculation_b200.cpp — the reference-side binding of the B200
+// speculation (T1) and termination (T3) hooks (include/spex.h).
 //
+//   dfs_speculative_select (speculation.hpp:95-139, speculation.cpp:182-218)
+//       over spex_speculation_dfs_plan: the tree's nodes marshalled into the
+//       control kernel's layout, Algorithm 1's simulated selections (descend /
+//       simulate_next with phantom children on the visit overlay) run by the
+//       control kernel's own dfs_plan on the device;
 //   AnswerTally::should_terminate (termination.hpp:15-55, termination.cpp:30-48)
 //       over spex_termination_should_terminate: the tally's labels in its own
 //       std::map order, the control kernel's tally_should_terminate on the device;
@@ -10,7 +15,8 @@
 //       widths computed by the control kernel's rebase_widths on the device.
 //
 // oracle/Makefile weakens exactly these symbols in copies of the reference's
-// termination.o / speculation.o (objcopy), so these definitions win; the
+// termination.o / speculation.o (objcopy), so these definitions win (the
+// reference's simulate_next, verify_bfs_speculation, record_outcome stay); the
 // reference's unmodified tests/test_termination.cpp and tests/test_speculation.cpp
 // then run through the device (tests/test_dropin_gpu.py).
 #include <string>
@@ -21,6 +27,7 @@
 #include "totsim/errors.hpp"
 #include "totsim/speculation.hpp"
 #include "totsim/termination.hpp"
+#include "totsim/tree.hpp"
 
 namespace totsim {
 
@@ -48,6 +55,37 @@ bool AnswerTally::should_terminate(int min_answers, double alpha) const {
   check(spex_termination_should_terminate(counts.data(), weights.data(), off, &n_total, 1, min_answers, alpha, &out),
         "should_terminate");
   return out != 0;
+}
+
+SpeculationPlan dfs_speculative_select(const SearchTree& tree, const SpeculationLedger& ledger, int k,
+                                       const PolicyConfig& cfg) {
+  (void)ledger;  // outstanding speculation is visible through node state (speculation.cpp:184)
+  const int n = static_cast<int>(tree.size());
+  std::vector<int32_t> parent(n), visits(n), depth(n);
+  std::vector<uint8_t> status(n), bits(n);
+  std::vector<double> reward(n), value(n);
+  for (int i = 0; i < n; ++i) {
+    const ThoughtNode& t = tree.node(static_cast<NodeId>(i));
+    parent[i] = t.parent == kNoNode ? -1 : static_cast<int32_t>(t.parent);
+    status[i] = static_cast<uint8_t>(t.status);
+    bits[i] = static_cast<uint8_t>((t.terminal ? 1 : 0) | (t.gen_done ? 2 : 0) | (t.reward.has_value() ? 4 : 0));
+    reward[i] = t.reward.value_or(0.0);
+    visits[i] = t.visits;
+    value[i] = t.value;
+    depth[i] = t.depth;
+  }
+  const std::vector<int32_t> dw(cfg.depth_widths.begin(), cfg.depth_widths.end());
+  std::vector<uint32_t> node(64);
+  std::vector<int32_t> dist(64);
+  int nt = 0;
+  check(spex_speculation_dfs_plan(parent.data(), status.data(), bits.data(), reward.data(), visits.data(), value.data(),
+                                  depth.data(), n, tree.terminal_answer_count(), static_cast<int>(cfg.family),
+                                  cfg.exploration_c, cfg.width, dw.data(), static_cast<int>(dw.size()),
+                                  cfg.target_answers, k, node.data(), dist.data(), &nt),
+        "dfs_speculative_select");
+  SpeculationPlan plan;
+  for (int i = 0; i < nt; ++i) plan.targets.push_back(SpecTarget{node[i], dist[i]});
+  return plan;
 }
 
 std::vector<std::pair<NodeId, int>> bfs_speculative_allocate(const std::vector<FrontierEntry>& frontier_status,

@@ -32,6 +32,7 @@
 #include "totsim/experiment.hpp"
 #include "totsim/policy.hpp"
 #include "totsim/rng.hpp"
+#include "totsim/speculation.hpp"
 #include "totsim/sim.hpp"
 #include "totsim/termination.hpp"
 #include "totsim/trace.hpp"
@@ -293,6 +294,44 @@ int ref_workload(int n, std::uint64_t seed, int max_depth, std::uint64_t* seeds,
     probe_depth[i] = p[i].probe_depth;
   }
   return 0;
+}
+
+/* dfs_speculative_select (speculation.cpp:182-218) on a tree built from plain
+ * arrays (the layout of spex_speculation_dfs_plan). Returns 0 or Errc + 1. */
+int ref_dfs_plan(const std::int32_t* parent, const std::uint8_t* status, const std::uint8_t* bits,
+                 const double* reward, const std::int32_t* visits, const double* value, int n, int family,
+                 double exploration_c, int width, const std::int32_t* depth_widths, int n_dw, int target_answers,
+                 int k, std::uint32_t* out_node, std::int32_t* out_dist, int* n_out) {
+  try {
+    SearchTree t(32, 1);
+    for (int i = 1; i < n; ++i) t.add_node(static_cast<NodeId>(parent[i]), 10, false);
+    for (int i = 0; i < n; ++i) {
+      ThoughtNode& d = t.node(static_cast<NodeId>(i));
+      d.status = static_cast<NodeStatus>(status[i]);
+      d.terminal = bits[i] & 1;
+      d.gen_done = (bits[i] & 2) != 0;
+      if (bits[i] & 4) d.reward = reward[i];
+      d.visits = visits[i];
+      d.value = value[i];
+    }
+    PolicyConfig cfg;
+    cfg.family = static_cast<Family>(family);
+    cfg.exploration_c = exploration_c;
+    cfg.width = width;
+    cfg.depth_widths.assign(depth_widths, depth_widths + n_dw);
+    cfg.target_answers = target_answers;
+    SpeculationLedger ledger;
+    SpeculationPlan plan = dfs_speculative_select(t, ledger, k, cfg);
+    *n_out = static_cast<int>(plan.targets.size());
+    for (int i = 0; i < *n_out; ++i) {
+      out_node[i] = plan.targets[i].node;
+      out_dist[i] = plan.targets[i].predicted_distance;
+    }
+    return 0;
+  } catch (const Error& e) {
+    g_err = e.what();
+    return static_cast<int>(e.code()) + 1;
+  }
 }
 
 /* AnswerTally::should_terminate after recording answers (label index, weight)

@@ -526,9 +526,10 @@ SPEX_HDNI u32 simulate_next(Snap& s, int* consumed) {
   return kNoNode;
 }
 
-// speculation.cpp:182-218 fused with executor.cpp:699-702 (spawn each target).
-// Returns the number of speculative children spawned.
-SPEX_HDNI int dfs_speculate(const QC& x, int k) {
+// dfs_speculative_select (speculation.cpp:182-218): up to k targets (node,
+// predicted distance) planned on the overlay; the live tree is not changed.
+// Shared by dfs_speculate and the spex_speculation_dfs_plan hook.
+SPEX_HDNI int dfs_plan(const QC& x, int k, u32* tnode, int* tdist) {
   Run* R = x.R;
   const int n = x.qr->nnodes;
   Snap s;
@@ -548,8 +549,6 @@ SPEX_HDNI int dfs_speculate(const QC& x, int k) {
   int horizon = x.c->target_answers - x.qr->terminal_count;
   if (horizon < 1) horizon = 1;
   int ordinal = 0;
-  u32 tnode[64];
-  int tdist[64];
   int nt = 0;
   if (k > 64) k = 64;  // spec_k <= 64 is enforced at config time
   for (int t = 1; t <= k; ++t) {
@@ -573,6 +572,15 @@ SPEX_HDNI int dfs_speculate(const QC& x, int k) {
     x.snch[node] += 1;
     snap_bump_path(s, ph);
   }
+  return nt;
+}
+
+// dfs_speculative_select fused with executor.cpp:699-702 (spawn each target).
+// Returns the number of speculative children spawned.
+SPEX_HDNI int dfs_speculate(const QC& x, int k) {
+  u32 tnode[64];
+  int tdist[64];
+  const int nt = dfs_plan(x, k, tnode, tdist);
   for (int i = 0; i < nt; ++i) spawn_child(x, tnode[i], true, tdist[i]);
   return nt;
 }

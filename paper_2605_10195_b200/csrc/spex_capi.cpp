@@ -34,6 +34,7 @@
 
 #ifdef SPEX_EMU
 #include "ctl_run.h"
+#include "hook_tree.h"
 #else
 #include <cuda_runtime.h>
 
@@ -2306,6 +2307,51 @@ extern "C" int spex_content_eval(const uint64_t* path_hash, const int* offsets, 
   for (int i = 0; i < n; ++i)
     content_eval(reinterpret_cast<const u64*>(path_hash) + offsets[i], offsets[i + 1] - offsets[i], query_seed,
                  max_depth, *wl, terminal + i, reward + i, label + i);
+  return 0;
+}
+
+extern "C" int spex_speculation_dfs_plan(const int32_t* parent, const uint8_t* status, const uint8_t* bits,
+                                         const double* reward, const int32_t* visits, const double* value,
+                                         const int32_t* depth, int n_nodes, int terminal_answers, int family,
+                                         double exploration_c, int width, const int32_t* depth_widths,
+                                         int n_depth_widths, int target_answers, int k, uint32_t* out_node,
+                                         int32_t* out_dist, int* n_out) {
+  *n_out = 0;
+  if (k < 0 || k > 64) return ERR_INVALID_ARGUMENT;
+  HookTree t;
+  if (!hook_tree_build(t, parent, status, bits, reward, visits, value, depth, n_nodes, terminal_answers, family,
+                       exploration_c, width, depth_widths, n_depth_widths, target_answers, k))
+    return ERR_INVALID_ARGUMENT;
+  if (family == kRebaseBfs || k == 0) return 0;
+  std::vector<int> spv(t.S), spn(t.S), spi(3 * t.S);
+  std::vector<double> spval(t.S), spd(3 * t.S);
+  std::vector<u32> sps(t.S);
+  GState g{};
+  Run R{};
+  R.cfg = t.cfg;
+  R.n_parent = t.parent.data();
+  R.n_first_child = t.first_child.data();
+  R.n_next_sib = t.next_sib.data();
+  R.n_status = t.status.data();
+  R.n_flags = t.flags.data();
+  R.n_reward = t.reward.data();
+  R.n_value = t.value.data();
+  R.n_visits = t.visits.data();
+  R.n_depth = t.depth.data();
+  R.n_nchildren = t.nchildren.data();
+  R.qs = &t.qr;
+  R.g = &g;
+  R.sp_visits = spv.data();
+  R.sp_value = spval.data();
+  R.sp_nchild = spn.data();
+  R.sp_stack = sps.data();
+  R.sp_dbl = spd.data();
+  R.sp_int = spi.data();
+  R.log_tab_n = 0;
+  QC x = make_qc(&R, 0, nullptr, 0);
+  const int n = dfs_plan(x, k, out_node, out_dist);
+  if (g.error) return ERR_INTERNAL;
+  *n_out = n;
   return 0;
 }
 

@@ -27,6 +27,7 @@
 
 #include "../../include/spex.h"
 #include "ctl_run.h"
+#include "hook_tree.h"
 
 namespace spex {
 namespace {
@@ -151,6 +152,13 @@ __global__ void terminate_kernel(const int* count, const double* w, const int* o
                min_answers, alpha)
                ? 1
                : 0;
+}
+
+// dfs_speculative_select on one tree (the control kernel's dfs_plan)
+__global__ void dfs_plan_kernel(Run* R, int k, u32* out_node, int* out_dist, int* n_out) {
+  QC x = make_qc(R, 0, nullptr, 0);
+  *n_out = dfs_plan(x, k, out_node, out_dist);
+  if (R->g->error) *n_out = -1;
 }
 
 __global__ void __launch_bounds__(256) allocate_kernel(const int* capacity, const double* hit_ema,
@@ -610,4 +618,65 @@ extern "C" int spex_termination_should_terminate(const int* counts, const double
     rc = finish();
   }
   return rc ? rc : finish();
+}
+
+extern "C" int spex_speculation_dfs_plan(const int32_t* parent, const uint8_t* status, const uint8_t* bits,
+                                         const double* reward, const int32_t* visits, const double* value,
+                                         const int32_t* depth, int n_nodes, int terminal_answers, int family,
+                                         double exploration_c, int width, const int32_t* depth_widths,
+                                         int n_depth_widths, int target_answers, int k, uint32_t* out_node,
+                                         int32_t* out_dist, int* n_out) {
+  *n_out = 0;
+  if (k < 0 || k > 64) return ERR_INVALID_ARGUMENT;  // spec_k <= 64 (config.cpp)
+  HookTree t;
+  if (!hook_tree_build(t, parent, status, bits, reward, visits, value, depth, n_nodes, terminal_answers, family,
+                       exploration_c, width, depth_widths, n_depth_widths, target_answers, k))
+    return ERR_INVALID_ARGUMENT;
+  if (family == kRebaseBfs || k == 0) return 0;  // frontier policies plan by allocation (speculation.cpp:125-126)
+  std::lock_guard<std::mutex> lk(g_hook_mu);
+  if (int rc = ensure_stream()) return rc;
+  int rc, n = 0;
+  {
+    Dev d;
+    Run R{};
+    R.cfg = t.cfg;
+    R.n_parent = d.put(t.parent.data(), t.cap);
+    R.n_first_child = d.put(t.first_child.data(), t.cap);
+    R.n_next_sib = d.put(t.next_sib.data(), t.cap);
+    R.n_status = d.put(t.status.data(), t.cap);
+    R.n_flags = d.put(t.flags.data(), t.cap);
+    R.n_reward = d.put(t.reward.data(), t.cap);
+    R.n_value = d.put(t.value.data(), t.cap);
+    R.n_visits = d.put(t.visits.data(), t.cap);
+    R.n_depth = d.put(t.depth.data(), t.cap);
+    R.n_nchildren = d.put(t.nchildren.data(), t.cap);
+    R.qs = d.put(&t.qr, 1);
+    GState g{};
+    R.g = d.put(&g, 1);
+    R.sp_visits = d.put<int>(nullptr, t.S);
+    R.sp_value = d.put<double>(nullptr, t.S);
+    R.sp_nchild = d.put<int>(nullptr, t.S);
+    R.sp_stack = d.put<u32>(nullptr, t.S);
+    R.sp_dbl = d.put<double>(nullptr, 3 * static_cast<size_t>(t.S));
+    R.sp_int = d.put<int>(nullptr, 3 * static_cast<size_t>(t.S));
+    R.log_tab = nullptr;
+    R.log_tab_n = 0;  // log via glibc::log itself (the table only caches it)
+    Run* dR = d.put(&R, 1);
+    u32* dn = d.put<u32>(nullptr, 64);
+    int* dd = d.put<int>(nullptr, 64);
+    int* dc = d.put<int>(nullptr, 1);
+    if (!dR || !dn || !dd || !dc || !R.sp_dbl || !R.n_parent) return 200;
+    dfs_plan_kernel<<<1, 1, 0, g_hook_stream>>>(dR, k, dn, dd, dc);
+    d.get(&n, dc, 1);
+    rc = finish();
+    if (!rc && n > 0) {
+      d.get(out_node, dn, n);
+      d.get(out_dist, dd, n);
+      rc = finish();
+    }
+  }
+  if (rc) return rc;
+  if (n < 0) return ERR_INTERNAL;
+  *n_out = n;
+  return finish();
 }

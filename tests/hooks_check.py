@@ -88,3 +88,78 @@ def check_hooks(L, R):
                                                    (ctypes.c_int * len(offs))(*offs), (ctypes.c_int * len(ntot))(*ntot),
                                                    len(idx), min_a, alpha, out) == 0
         assert list(out) == [refs[i] for i in idx], (min_a, alpha)
+
+    # dfs_speculative_select vs the reference on random trees (committed scored
+    # nodes, in-flight and speculative work, pruned branches, terminal answers)
+    check_dfs_plan(L, R, rng)
+
+
+def random_tree(rng, n):
+    parent, status, bits, reward, visits, value = [-1], [3], [2], [0.0], [1], [0.0]
+    for i in range(1, n):
+        p = rng.randrange(i)
+        while status[p] in (6, 7):  # no children under pruned nodes or answers
+            p = parent[p] if parent[p] >= 0 else 0
+            if p == 0:
+                break
+        r = rng.random()
+        kind = rng.choices(["commit", "expanding", "awaiting", "spec", "specdone", "pruned", "answer", "pending"],
+                           [10, 1, 1, 1, 1, 1, 1, 1])[0]
+        st = {"commit": 3, "expanding": 1, "awaiting": 2, "spec": 4, "specdone": 5, "pruned": 6, "answer": 7,
+              "pending": 0}[kind]
+        gen = kind in ("commit", "awaiting", "specdone", "answer")
+        has_r = kind in ("commit", "specdone", "answer")
+        term = kind == "answer" or (kind == "specdone" and rng.random() < 0.2)
+        parent.append(p)
+        status.append(st)
+        bits.append((1 if term else 0) | (2 if gen else 0) | (4 if has_r else 0))
+        reward.append(r if has_r else 0.0)
+        visits.append(rng.randint(1, 4) if kind in ("commit", "answer") else 0)
+        value.append(r if kind in ("commit", "answer") else 0.0)
+    for i in range(n - 1, 0, -1):  # ancestors carry their children's traffic
+        visits[parent[i]] = max(visits[parent[i]], sum(visits[j] for j in range(n) if parent[j] == i) + visits[i])
+    return parent, status, bits, reward, visits, value
+
+
+def check_dfs_plan(L, R, rng):
+    I32, U8, F64, U32 = ctypes.c_int32, ctypes.c_uint8, ctypes.c_double, ctypes.c_uint32
+    R.ref_dfs_plan.argtypes = [ctypes.POINTER(I32), ctypes.POINTER(U8), ctypes.POINTER(U8), ctypes.POINTER(F64),
+                               ctypes.POINTER(I32), ctypes.POINTER(F64), ctypes.c_int, ctypes.c_int, ctypes.c_double,
+                               ctypes.c_int, ctypes.POINTER(I32), ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                               ctypes.POINTER(U32), ctypes.POINTER(I32), ctypes.POINTER(ctypes.c_int)]
+    fn = L.spex_speculation_dfs_plan
+    fn.restype = ctypes.c_int
+    fn.argtypes = [ctypes.POINTER(I32), ctypes.POINTER(U8), ctypes.POINTER(U8), ctypes.POINTER(F64),
+                   ctypes.POINTER(I32), ctypes.POINTER(F64), ctypes.POINTER(I32), ctypes.c_int, ctypes.c_int,
+                   ctypes.c_int, ctypes.c_double, ctypes.c_int, ctypes.POINTER(I32), ctypes.c_int, ctypes.c_int,
+                   ctypes.c_int, ctypes.POINTER(U32), ctypes.POINTER(I32), ctypes.POINTER(ctypes.c_int)]
+    planned = 0
+    for trial in range(300):
+        n = rng.randint(1, 40)
+        parent, status, bits, reward, visits, value = random_tree(rng, n)
+        depth = [0] * n
+        for i in range(1, n):
+            depth[i] = depth[parent[i]] + 1
+        family = rng.choice([0, 0, 1, 2])
+        c = rng.choice([0.5, 1.0, 1.414])
+        width = rng.randint(1, 4)
+        dw = [rng.randint(1, 5) for _ in range(rng.randint(0, 3))]
+        target = rng.randint(1, 12)
+        k = rng.randint(0, 8)
+        args = ((I32 * n)(*parent), (U8 * n)(*status), (U8 * n)(*bits), (F64 * n)(*reward), (I32 * n)(*visits),
+                (F64 * n)(*value))
+        dwa = (I32 * max(1, len(dw)))(*dw)
+        rn, rd, rc_n = (U32 * 64)(), (I32 * 64)(), ctypes.c_int()
+        rrc = R.ref_dfs_plan(*args, n, family, c, width, dwa, len(dw), target, k, rn, rd, ctypes.byref(rc_n))
+        gn, gd, g_n = (U32 * 64)(), (I32 * 64)(), ctypes.c_int()
+        terminal_answers = sum(1 for s_ in status if s_ == 7)
+        grc = fn(*args, (I32 * n)(*depth), n, terminal_answers, family, c, width, dwa, len(dw), target, k, gn, gd,
+                 ctypes.byref(g_n))
+        assert (rrc != 0) == (grc != 0), (trial, rrc, grc)
+        if rrc:
+            continue
+        got = [(gn[i], gd[i]) for i in range(g_n.value)]
+        exp = [(rn[i], rd[i]) for i in range(rc_n.value)]
+        assert got == exp, (trial, family, k, got, exp)
+        planned += len(exp)
+    assert planned > 100

@@ -78,12 +78,14 @@ TERM_BIN = ROOT / "oracle" / "_ref" / "dropin_test_termination"
 
 def test_reference_termination_and_speculation_tests_pass_on_b200_hooks():
     """The reference's own tests/test_termination.cpp and
-    tests/test_speculation.cpp (unmodified) with AnswerTally::should_terminate
-    and bfs_speculative_allocate on the device (integration/termination_b200.cpp
-    -> the control kernel's tally_should_terminate and rebase_widths): the n >= t
-    gate, margins, ties, alpha extremes (test_termination.cpp:80-160) and the BFS
-    allocation cases (test_speculation.cpp:349-391); the rest of both files runs
-    the reference's own code beside them."""
+    tests/test_speculation.cpp (unmodified) with AnswerTally::should_terminate,
+    dfs_speculative_select and bfs_speculative_allocate on the device
+    (integration/speculation_b200.cpp -> the control kernel's
+    tally_should_terminate, dfs_plan and rebase_widths): the n >= t gate,
+    margins, ties, alpha extremes (test_termination.cpp:80-160), Algorithm 1
+    against the clone-and-simulate oracle on 60 random trees, planned-child
+    identities, distances (test_speculation.cpp:254-345) and the BFS allocation
+    cases (:349-391); the rest of both files runs the reference's own code."""
     if not TERM_BIN.exists():
         pytest.skip("oracle/_ref/dropin_test_termination not built (needs /root/reference at build time)")
     p = subprocess.run([str(TERM_BIN)], capture_output=True, text=True, timeout=900)
