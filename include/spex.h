@@ -20,6 +20,8 @@
  *   spex_budget_k_total / allocate
  *                             <- totsim::roofline_k_total / allocate_budgets
  *                                (budget.hpp:37-55, budget.cpp:23-96)
+ *   spex_tree_transition_legal / prune_subtree
+ *                             <- totsim::transition_legal, SearchTree::prune_subtree (tree.cpp:23-45,119-141)
  *   spex_speculation_dfs_plan <- totsim::dfs_speculative_select (speculation.cpp:182-218)
  *   spex_termination_should_terminate
  *                             <- totsim::AnswerTally::should_terminate (termination.cpp:30-48)
@@ -331,6 +333,15 @@ int spex_engine_advance(const spex_engine_hw* hw, double now, double limit, spex
                         int* n_active, spex_engine_stream* staged, int* n_staged, const int* anc_key,
                         const int* anc_tokens, int n_keys, spex_engine_finished* out, int cap, int* n_out,
                         double* now_out);
+
+/* Tree maintenance hooks (tree.hpp:43,104): transition_legal (tree.cpp:23-45)
+ * for n (from, to) NodeStatus pairs, and SearchTree::prune_subtree
+ * (tree.cpp:119-141) on one tree given by parents (parent[0] = -1, children in
+ * NodeId order) and statuses — the statuses are updated in place, *pruned =
+ * the nodes newly tombstoned; UnknownNode + 1 for an id outside the tree. The
+ * control kernel's own transition_legal / prune_subtree. */
+int spex_tree_transition_legal(const uint8_t* from, const uint8_t* to, int n, uint8_t* out);
+int spex_tree_prune_subtree(const int32_t* parent, uint8_t* status, int n_nodes, uint32_t id, int* pruned);
 
 /* T1 planning hook: dfs_speculative_select (speculation.hpp:95-139,
  * speculation.cpp:182-218) on one tree, on the device with the control

@@ -296,6 +296,25 @@ int ref_workload(int n, std::uint64_t seed, int max_depth, std::uint64_t* seeds,
   return 0;
 }
 
+/* transition_legal (tree.cpp:23-45) and SearchTree::prune_subtree
+ * (tree.cpp:119-141) on a tree built from parents / statuses. */
+int ref_transition_legal(int from, int to) {
+  return transition_legal(static_cast<NodeStatus>(from), static_cast<NodeStatus>(to)) ? 1 : 0;
+}
+int ref_prune_subtree(const std::int32_t* parent, std::uint8_t* status, int n, std::uint32_t id, int* pruned) {
+  try {
+    SearchTree t(32, 1);
+    for (int i = 1; i < n; ++i) t.add_node(static_cast<NodeId>(parent[i]), 10, false);
+    for (int i = 0; i < n; ++i) t.node(static_cast<NodeId>(i)).status = static_cast<NodeStatus>(status[i]);
+    *pruned = t.prune_subtree(id);
+    for (int i = 0; i < n; ++i) status[i] = static_cast<std::uint8_t>(t.node(static_cast<NodeId>(i)).status);
+    return 0;
+  } catch (const Error& e) {
+    g_err = e.what();
+    return static_cast<int>(e.code()) + 1;
+  }
+}
+
 /* dfs_speculative_select (speculation.cpp:182-218) on a tree built from plain
  * arrays (the layout of spex_speculation_dfs_plan). Returns 0 or Errc + 1. */
 int ref_dfs_plan(const std::int32_t* parent, const std::uint8_t* status, const std::uint8_t* bits,

@@ -19,7 +19,7 @@ struct HookTree {
   std::vector<u8> status;
   std::vector<u16> flags;
   std::vector<double> reward, value;
-  std::vector<int> visits, depth, nchildren;
+  std::vector<int> visits, depth, nchildren, tokens;
   Cfg cfg{};
   QueryRun qr{};
 };
@@ -44,6 +44,7 @@ inline bool hook_tree_build(HookTree& t, const int32_t* parent, const uint8_t* s
   t.visits.assign(t.cap, 0);
   t.depth.assign(t.cap, 0);
   t.nchildren.assign(t.cap, 0);
+  t.tokens.assign(t.cap, 0);
   std::vector<u32> last(t.cap, kNoNode);
   for (int i = 0; i < n; ++i) {
     if (status[i] > kTerminalAnswer) return false;
@@ -78,6 +79,16 @@ inline bool hook_tree_build(HookTree& t, const int32_t* parent, const uint8_t* s
   t.qr.nnodes = n;
   t.qr.terminal_count = terminal_answers;
   return true;
+}
+
+// The tree alone (parents and statuses; the other node fields zero), for the
+// tree-maintenance hooks (spex_tree_prune_subtree).
+inline bool hook_tree_build_min(HookTree& t, const int32_t* parent, const uint8_t* status, int n) {
+  std::vector<uint8_t> zb(n, 0);
+  std::vector<double> zd(n, 0.0);
+  std::vector<int32_t> zi(n, 0);
+  return hook_tree_build(t, parent, status, zb.data(), zd.data(), zi.data(), zd.data(), zi.data(), n, 0, 0, 1.0, 1,
+                         nullptr, 0, 1, 0);
 }
 
 }  // namespace spex

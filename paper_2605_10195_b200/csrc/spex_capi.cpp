@@ -2310,6 +2310,37 @@ extern "C" int spex_content_eval(const uint64_t* path_hash, const int* offsets, 
   return 0;
 }
 
+extern "C" int spex_tree_transition_legal(const uint8_t* from, const uint8_t* to, int n, uint8_t* out) {
+  for (int i = 0; i < n; ++i) out[i] = transition_legal(from[i], to[i]) ? 1 : 0;
+  return 0;
+}
+
+extern "C" int spex_tree_prune_subtree(const int32_t* parent, uint8_t* status, int n_nodes, uint32_t id, int* pruned) {
+  *pruned = 0;
+  HookTree t;
+  if (!hook_tree_build_min(t, parent, status, n_nodes)) return ERR_INVALID_ARGUMENT;
+  if (id >= static_cast<uint32_t>(n_nodes)) return ERR_UNKNOWN_NODE;
+  std::vector<u32> stack(t.S);
+  GState g{};
+  Run R{};
+  R.cfg = t.cfg;
+  R.n_parent = t.parent.data();
+  R.n_first_child = t.first_child.data();
+  R.n_next_sib = t.next_sib.data();
+  R.n_status = t.status.data();
+  R.n_flags = t.flags.data();
+  R.n_tokens = t.tokens.data();
+  R.qs = &t.qr;
+  R.g = &g;
+  R.sp_stack = stack.data();
+  QC x = make_qc(&R, 0, nullptr, 0);
+  const int cnt = prune_subtree(x, id);
+  if (g.error) return ERR_INTERNAL;
+  for (int i = 0; i < n_nodes; ++i) status[i] = t.status[i];
+  *pruned = cnt;
+  return 0;
+}
+
 extern "C" int spex_speculation_dfs_plan(const int32_t* parent, const uint8_t* status, const uint8_t* bits,
                                          const double* reward, const int32_t* visits, const double* value,
                                          const int32_t* depth, int n_nodes, int terminal_answers, int family,

@@ -161,6 +161,19 @@ __global__ void dfs_plan_kernel(Run* R, int k, u32* out_node, int* out_dist, int
   if (R->g->error) *n_out = -1;
 }
 
+// SearchTree::prune_subtree on one tree (the control kernel's prune_subtree)
+__global__ void prune_kernel(Run* R, u32 id, int* out) {
+  QC x = make_qc(R, 0, nullptr, 0);
+  *out = prune_subtree(x, id);
+  if (R->g->error) *out = -1;
+}
+
+// transition_legal (tree.cpp:23-45) for n pairs
+__global__ void transition_kernel(const u8* from, const u8* to, int n, u8* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = transition_legal(from[i], to[i]) ? 1 : 0;
+}
+
 __global__ void __launch_bounds__(256) allocate_kernel(const int* capacity, const double* hit_ema,
                                                        const double* kv_bytes, int n, int k_total, double tau,
                                                        double weight_bytes, double* score, double* w, int* out,
@@ -678,5 +691,65 @@ extern "C" int spex_speculation_dfs_plan(const int32_t* parent, const uint8_t* s
   if (rc) return rc;
   if (n < 0) return ERR_INTERNAL;
   *n_out = n;
+  return finish();
+}
+
+extern "C" int spex_tree_transition_legal(const uint8_t* from, const uint8_t* to, int n, uint8_t* out) {
+  std::lock_guard<std::mutex> lk(g_hook_mu);
+  if (int rc = ensure_stream()) return rc;
+  if (n <= 0) return 0;
+  int rc;
+  {
+    Dev d;
+    u8* df = d.put(from, n);
+    u8* dt = d.put(to, n);
+    u8* dout = d.put<u8>(nullptr, n);
+    if (!df || !dt || !dout) return 200;
+    transition_kernel<<<(n + 127) / 128, 128, 0, g_hook_stream>>>(df, dt, n, dout);
+    d.get(out, dout, n);
+    rc = finish();
+  }
+  return rc ? rc : finish();
+}
+
+extern "C" int spex_tree_prune_subtree(const int32_t* parent, uint8_t* status, int n_nodes, uint32_t id, int* pruned) {
+  *pruned = 0;
+  HookTree t;
+  if (!hook_tree_build_min(t, parent, status, n_nodes)) return ERR_INVALID_ARGUMENT;
+  if (id >= static_cast<uint32_t>(n_nodes)) return ERR_UNKNOWN_NODE;  // check_known (tree.cpp:96-99)
+  std::lock_guard<std::mutex> lk(g_hook_mu);
+  if (int rc = ensure_stream()) return rc;
+  int rc, cnt = 0;
+  {
+    Dev d;
+    Run R{};
+    R.cfg = t.cfg;
+    R.n_parent = d.put(t.parent.data(), t.cap);
+    R.n_first_child = d.put(t.first_child.data(), t.cap);
+    R.n_next_sib = d.put(t.next_sib.data(), t.cap);
+    R.n_status = d.put(t.status.data(), t.cap);
+    R.n_flags = d.put(t.flags.data(), t.cap);
+    R.n_tokens = d.put(t.tokens.data(), t.cap);
+    R.qs = d.put(&t.qr, 1);
+    GState g{};
+    R.g = d.put(&g, 1);
+    R.sp_stack = d.put<u32>(nullptr, t.S);
+    R.sp_visits = d.put<int>(nullptr, t.S);
+    R.sp_value = d.put<double>(nullptr, t.S);
+    R.sp_nchild = d.put<int>(nullptr, t.S);
+    R.sp_dbl = d.put<double>(nullptr, 3 * static_cast<size_t>(t.S));
+    R.sp_int = d.put<int>(nullptr, 3 * static_cast<size_t>(t.S));
+    Run* dR = d.put(&R, 1);
+    int* dc = d.put<int>(nullptr, 1);
+    if (!dR || !dc || !R.sp_stack || !R.n_status) return 200;
+    prune_kernel<<<1, 1, 0, g_hook_stream>>>(dR, id, dc);
+    d.get(&cnt, dc, 1);
+    d.get(t.status.data(), R.n_status, t.cap);
+    rc = finish();
+  }
+  if (rc) return rc;
+  if (cnt < 0) return ERR_INTERNAL;
+  for (int i = 0; i < n_nodes; ++i) status[i] = t.status[i];
+  *pruned = cnt;
   return finish();
 }

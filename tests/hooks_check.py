@@ -92,6 +92,7 @@ def check_hooks(L, R):
     # dfs_speculative_select vs the reference on random trees (committed scored
     # nodes, in-flight and speculative work, pruned branches, terminal answers)
     check_dfs_plan(L, R, rng)
+    check_tree_hooks(L, R, rng)
 
 
 def random_tree(rng, n):
@@ -163,3 +164,29 @@ def check_dfs_plan(L, R, rng):
         assert got == exp, (trial, family, k, got, exp)
         planned += len(exp)
     assert planned > 100
+
+
+def check_tree_hooks(L, R, rng):
+    """transition_legal on all 64 status pairs; prune_subtree on random trees."""
+    U8, I32 = ctypes.c_uint8, ctypes.c_int32
+    frm = [a for a in range(8) for _ in range(8)]
+    to = [b for _ in range(8) for b in range(8)]
+    out = (U8 * 64)()
+    assert L.spex_tree_transition_legal((U8 * 64)(*frm), (U8 * 64)(*to), 64, out) == 0
+    assert list(out) == [R.ref_transition_legal(a, b) for a, b in zip(frm, to)]
+    R.ref_prune_subtree.argtypes = [ctypes.POINTER(I32), ctypes.POINTER(U8), ctypes.c_int, ctypes.c_uint32,
+                                    ctypes.POINTER(ctypes.c_int)]
+    fn = L.spex_tree_prune_subtree
+    fn.restype = ctypes.c_int
+    fn.argtypes = [ctypes.POINTER(I32), ctypes.POINTER(U8), ctypes.c_int, ctypes.c_uint32, ctypes.POINTER(ctypes.c_int)]
+    for _ in range(200):
+        n = rng.randint(1, 60)
+        parent = [-1] + [rng.randrange(i) for i in range(1, n)]
+        status = [rng.randrange(8) for _ in range(n)]
+        node = rng.randrange(n + 2)  # sometimes outside the tree: UnknownNode
+        a, b = (U8 * n)(*status), (U8 * n)(*status)
+        pa, pb = ctypes.c_int(), ctypes.c_int()
+        ra = R.ref_prune_subtree((I32 * n)(*parent), a, n, node, ctypes.byref(pa))
+        rb = fn((I32 * n)(*parent), b, n, node, ctypes.byref(pb))
+        assert ra == rb, (ra, rb)
+        assert list(a) == list(b) and pa.value == pb.value

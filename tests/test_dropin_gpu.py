@@ -92,3 +92,20 @@ def test_reference_termination_and_speculation_tests_pass_on_b200_hooks():
     print(p.stdout[-2000:], p.stderr[-4000:])
     assert p.returncode == 0, p.stdout[-4000:] + p.stderr[-4000:]
     assert "| 0 failed" in p.stdout, p.stdout
+
+
+TREE_BIN = ROOT / "oracle" / "_ref" / "dropin_test_tree"
+
+
+def test_reference_tree_tests_pass_on_b200_hooks():
+    """The reference's own tests/test_tree.cpp (unmodified) with
+    transition_legal and SearchTree::prune_subtree on the device
+    (integration/tree_b200.cpp -> the control kernel's transition_legal and
+    tombstone prune): lifecycle legality, prune counts, re-prunes, frontier
+    filtering and the snapshot round trips of test_tree.cpp."""
+    if not TREE_BIN.exists():
+        pytest.skip("oracle/_ref/dropin_test_tree not built (needs /root/reference at build time)")
+    p = subprocess.run([str(TREE_BIN)], capture_output=True, text=True, timeout=900)
+    print(p.stdout[-2000:], p.stderr[-4000:])
+    assert p.returncode == 0, p.stdout[-4000:] + p.stderr[-4000:]
+    assert "| 0 failed" in p.stdout, p.stdout
