@@ -9,6 +9,7 @@
  *   spex_frontier_step        <- one main_loop iteration at a time (executor.cpp:785-807)
  *                                (proj/include/totsim/executor.hpp:50-58,
  *                                 proj/src/executor.cpp:809-860)
+ *   spex_run                  <- Executor::run with a TraceWriter sink, events streamed
  *   spex_run_once             <- totsim::run_once (proj/include/totsim/experiment.hpp:27,
  *                                 proj/src/experiment.cpp:23-30)
  *   spex_canonical_config     <- ExperimentConfig::from_json + to_json
@@ -403,6 +404,15 @@ double spex_engine_next_ready(const spex_engine* e);
  * token outside the vocabulary. */
 int spex_score_batch(const char* prm_shape, uint64_t weight_seed, const int32_t* tokens, const int64_t* offsets,
                      int n, float* scores, int device);
+
+/* spex_run (SURVEY.md §8b spex_run(config, seed, flags, trace_cb)): the whole
+ * run stepped through spex_frontier_step `chunk` consumer-loop iterations at a
+ * time (<= 0: 4096), each event-log line handed to trace_cb as it is produced
+ * (line without its newline, its length, `user`); the lines are the run_once
+ * log. trace_cb may be NULL. */
+typedef void (*spex_trace_cb)(const char* line, size_t len, void* user);
+int spex_run(const char* config_json, uint64_t seed, const char* flags_csv, spex_trace_cb trace_cb, void* user,
+             long long chunk, spex_totals* totals);
 
 /* run_once: traced run returning totals and the JSON-lines log. */
 int spex_run_once(const char* config_json, uint64_t seed, const char* flags_csv,

@@ -294,6 +294,21 @@ def run_once(cfg: Any, seed: int, flags: SpexFlags | str | None = None) -> RunOu
         ex.close()
 
 
+def run(cfg: Any, seed: int, flags: SpexFlags | str | None = None, on_event=None, chunk: int = 4096) -> RunTotals:
+    """spex_run: the whole run stepped on the device ``chunk`` consumer-loop
+    iterations at a time, each event-log line passed to ``on_event(line)`` as
+    it is produced (the run_once log, streamed)."""
+    L = _lib.lib()
+    if not L.spex_device_ok():
+        raise RuntimeError("no sm_100 CUDA device: the SPEX B200 path has no CPU fallback")
+    fcsv = flags.to_csv().encode() if isinstance(flags, SpexFlags) else (flags.encode() if isinstance(flags, str)
+                                                                          else None)
+    cb = _lib.TRACE_CB(lambda line, n, user: on_event(line[:n].decode()) if on_event else None)
+    t = _lib.Totals()
+    _check(L.spex_run(_cfg_text(cfg).encode(), int(seed), fcsv, cb, None, int(chunk), ctypes.byref(t)))
+    return RunTotals(**t.as_dict())
+
+
 def run_batch(cfg: Any, seeds, flags: SpexFlags | str | None = None, device: int = 0):
     """Independent searches of one config, one per seed, in ONE launch of the
     control kernel (one CTA per search; control only, no model). The device
@@ -357,6 +372,7 @@ __all__ = [
     "TotsimError",
     "canonical_config",
     "device_ok",
+    "run",
     "run_batch",
     "run_once",
     "score_batch",

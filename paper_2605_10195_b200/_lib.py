@@ -217,6 +217,10 @@ _EXPORTS = {
     ),
 }
 
+TRACE_CB = ctypes.CFUNCTYPE(None, ctypes.c_char_p, ctypes.c_size_t, ctypes.c_void_p)
+_EXPORTS["spex_run"] = ([ctypes.c_char_p, ctypes.c_uint64, ctypes.c_char_p, TRACE_CB, ctypes.c_void_p,
+                         ctypes.c_longlong, ctypes.POINTER(Totals)], ctypes.c_int)
+
 _lib = None
 
 

@@ -2207,6 +2207,34 @@ int spex_run_once(const char* config_json, uint64_t seed, const char* flags_csv,
   return rc;
 }
 
+int spex_run(const char* config_json, uint64_t seed, const char* flags_csv, spex_trace_cb trace_cb, void* user,
+             long long chunk, spex_totals* totals) {
+  spex_executor* ex = nullptr;
+  int rc = spex_executor_create(config_json, seed, flags_csv, 0, &ex);
+  if (rc) return rc;
+  for (int done = 0; !rc && !done;) {
+    char* ev = nullptr;
+    size_t n = 0;
+    rc = spex_frontier_step(ex, chunk > 0 ? chunk : 4096, &done, &ev, &n);
+    if (!rc && trace_cb) {
+      // one callback per event-log line, as TraceWriter::emit (trace.cpp:32-36)
+      for (size_t a = 0; a < n;) {
+        size_t b = a;
+        while (b < n && ev[b] != '\n') ++b;
+        const char keep = ev[b < n ? b : n];
+        if (b < n) ev[b] = 0;
+        trace_cb(ev + a, b - a, user);
+        if (b < n) ev[b] = keep;
+        a = b + 1;
+      }
+    }
+    std::free(ev);
+  }
+  if (!rc && totals) rc = guarded([&] { fill_totals(*ex, totals); });
+  spex_executor_destroy(ex);
+  return rc;
+}
+
 }  // extern "C"
 
 #ifdef SPEX_EMU

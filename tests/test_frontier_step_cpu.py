@@ -65,3 +65,20 @@ def test_stepped_log_is_the_run_once_log(case, sizes):
         assert calls == 1
     if sizes == [1]:
         assert calls > 10
+
+
+def test_spex_run_streams_the_run_once_log():
+    """spex_run: the event lines through a callback as the steps produce them."""
+    import gzip
+    L = emu()
+    case = MANIFEST[0]
+    with gzip.open(GOLDEN / f"{case['name']}.jsonl.gz", "rt") as f:
+        golden = f.read().splitlines()
+    got = []
+    cb = _lib.TRACE_CB(lambda line, n, user: got.append(line[:n].decode()))
+    t = _lib.Totals()
+    flags = case["flags"]
+    assert L.spex_run(json.dumps(case["config"]).encode(), case["seed"], None if flags is None else flags.encode(), cb,
+                      None, 5, ctypes.byref(t)) == 0, L.spex_last_error()
+    assert got == golden
+    assert t.queries == json.loads(golden[-1])["queries"]

@@ -54,3 +54,13 @@ def test_step_refuses_a_model_run():
     with pytest.raises(spex.TotsimError):
         ex.step(1)
     ex.close()
+
+
+@needs_ref
+def test_spex_run_streams_the_reference_log():
+    cfg = (ROOT / "configs" / "c3_rstar_w4_q512.json").read_text()
+    got = []
+    t = spex.run(cfg, 1, None, on_event=got.append, chunk=2000)
+    ref = refutil.ref_run_log(cfg, 1, None)
+    assert got == ref
+    assert t.queries == 512
