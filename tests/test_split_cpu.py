@@ -165,3 +165,35 @@ def test_split_one_process_per_rank_gloo(tmp_path):
         got = json.loads((tmp_path / f"rank{r}.json").read_text())
         assert got["rounds"] == rounds[r]
         assert got["log"] == ref[r]
+
+
+def _rank_fail_main(rank, world, port, out_dir, tag):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        L = _lib.bind(refutil.EMU_SO)
+        kind = "shm" if rank == 0 else "no-such-kind"  # rank 1 cannot set up its outbox
+        try:
+            shard.Outboxes(L, rank, world, 16, kind=kind, tag=tag)
+            res = "ok"
+        except shard.SplitUnavailable as e:
+            res = "unavailable: " + str(e)
+        (Path(out_dir) / f"rank{rank}.txt").write_text(res)
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_split_setup_failure_is_agreed_by_every_rank(tmp_path):
+    """One rank failing to set up its outbox makes every rank raise
+    SplitUnavailable (bench.py then runs independent shards on all ranks)
+    instead of leaving the others waiting in a collective."""
+    emu()
+    import torch.multiprocessing as mp
+    mp.start_processes(_rank_fail_main, args=(2, _free_port(), str(tmp_path), f"spexf{os.getpid()}"), nprocs=2,
+                       join=True, start_method="spawn")
+    for r in range(2):
+        msg = (tmp_path / f"rank{r}.txt").read_text()
+        assert msg.startswith("unavailable") and "rank 1" in msg, msg
