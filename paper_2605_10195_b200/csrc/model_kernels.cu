@@ -1640,23 +1640,29 @@ __global__ void __launch_bounds__(1024) order_rows_kernel(const RowDesc* __restr
   constexpr int NB = 1024;
   __shared__ int hist[NB], part[NB], key[NB], rnk[NB];
   const int tid = threadIdx.x;
+  // one bucket per query up to 1024 queries (buckets past nb stay empty)
+  const int nb = Q > 0 && Q < NB ? Q : NB;
   hist[tid] = 0;
   key[tid] = 0;
   __syncthreads();
-  auto bucket = [&](int q) { return min((int)(((long long)q * NB) / (Q > 0 ? Q : 1)), NB - 1); };
+  auto bucket = [&](int q) { return min((int)(((long long)q * nb) / (Q > 0 ? Q : 1)), nb - 1); };
   for (int r = tid; r < M; r += 1024) {
     const int bq = bucket(rows[r].q);
     atomicAdd(&hist[bq], 1);
     if (lpt) atomicMax(&key[bq], rows[r].abs_pos + 1);
   }
   __syncthreads();
-  // rank of each bucket: longer first, then by index (deterministic)
+  // rank of each bucket: longer first, then by index (deterministic); the
+  // empty buckets past nb rank last, in index order
   {
-    const int kb = key[tid];
-    int r = 0;
-    for (int j = 0; j < NB; ++j) {
-      const int kj = key[j];
-      r += kj > kb || (kj == kb && j < tid);
+    int r = tid;
+    if (tid < nb) {
+      const int kb = key[tid];
+      r = 0;
+      for (int j = 0; j < nb; ++j) {
+        const int kj = key[j];
+        r += kj > kb || (kj == kb && j < tid);
+      }
     }
     rnk[tid] = r;
   }
