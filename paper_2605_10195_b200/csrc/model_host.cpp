@@ -59,7 +59,7 @@ void spex_k_order_rows(const RowDesc* rows, int M, int Q, int* order, cudaStream
 int spex_k_tree_attn_bulk(const RowDesc* rows, const Segment* segs, const float* Qr, int H, int KVH, int dh,
                           const __nv_bfloat16* Kp, const __nv_bfloat16* Vp, long long slots, __nv_bfloat16* O, int M,
                           int* item_ctr, cudaStream_t s);
-int spex_k_tree_attn_wmma(const CUtensorMap* kmap16, const CUtensorMap* vmap16, const RowDesc* rows,
+int spex_k_tree_attn_wmma(const CUtensorMap* kvmap16, const RowDesc* rows,
                           const Segment* segs, const float* Qr, int H, int KVH, int dh, long long slots,
                           __nv_bfloat16* O, int M, int* item_ctr, cudaStream_t s);
 int spex_k_gemm_tc(const CUtensorMap* tmA, const CUtensorMap* tmB, int M, int N, int K, const TcEpilogue* ep,
@@ -133,9 +133,27 @@ extern "C" int spex_tmap_kv(CUtensorMap* m, void* base, long long rows, int dh) 
   return make_kv_tmap(m, base, rows, dh) ? 0 : -1;
 }
 
-// ... with 16-row boxes for the per-warp decode pipeline (tree_attn_wmma_kernel).
-extern "C" int spex_tmap_kv16(CUtensorMap* m, void* base, long long rows, int dh) {
-  return make_kv_tmap(m, base, rows, dh, 16) ? 0 : -1;
+// ... for the per-warp decode pipeline (tree_attn_wmma_kernel): the layer's K
+// and V pools (V above K) as one 4D view (64 columns, rows, the 2 column
+// halves at +128 B, K|V at +(V - K)) with (64, 16, 2, 2) boxes, so ONE copy of
+// 8 KB fills a decode stage: K then V, each [half][16 rows][64], 128-byte
+// swizzled (the producer lane issues one copy per stage instead of four: it is
+// on the critical path of every stage, profiles/r02zt_k1_gqa_tma_ab.txt).
+static bool make_kv_tmap16(CUtensorMap* m, void* k, void* v, long long rows, int dh) {
+  PFN_tmap_encode enc = tmap_encoder();
+  const uintptr_t kb = reinterpret_cast<uintptr_t>(k), vb = reinterpret_cast<uintptr_t>(v);
+  if (!enc || dh != 128 || vb <= kb || (vb - kb) % 16 != 0 || (vb - kb) >= (1ULL << 40)) return false;
+  cuuint64_t dims[4] = {64, (cuuint64_t)rows, 2, 2};
+  cuuint64_t strides[3] = {(cuuint64_t)dh * 2, 128, (cuuint64_t)(vb - kb)};
+  cuuint32_t box[4] = {64, 16, 2, 2};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, k, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+extern "C" int spex_tmap_kv16(CUtensorMap* m, void* k, void* v, long long rows, int dh) {
+  return make_kv_tmap16(m, k, v, rows, dh) ? 0 : -1;
 }
 
 // TMA descriptor of a row-major bf16 matrix [rows][cols] as a GEMM operand of
@@ -163,7 +181,7 @@ struct TcWeight {
 struct Model {
   ModelShape sh;
   std::vector<CUtensorMap> kmap, vmap;      // per layer (empty when TMA maps are unavailable)
-  std::vector<CUtensorMap> kmap16, vmap16;  // 16-row boxes (decode pipeline)
+  std::vector<CUtensorMap> kvmap16;  // K|V pair, 16-row boxes (decode pipeline)
   bool is_prm;
   long long slots;
   int max_rows;
@@ -236,8 +254,11 @@ static Model* make_model(const ModelShape& sh, bool prm, uint64_t seed, long lon
     init(m->wo.back(), no, 100 + 8 * l + 1, kStd);
     init(m->wgu.back(), ng, 100 + 8 * l + 2, kStd);
     init(m->wd.back(), nd, 100 + 8 * l + 3, kStd);
-    m->Kp.push_back(dalloc<__nv_bfloat16>((size_t)sh.KVH * slots * sh.dh, o));
-    m->Vp.push_back(dalloc<__nv_bfloat16>((size_t)sh.KVH * slots * sh.dh, o));
+    // K and V of a layer in one allocation, V above K (the decode pipeline's
+    // K|V tensor map, make_kv_tmap16)
+    __nv_bfloat16* kv = dalloc<__nv_bfloat16>((size_t)2 * sh.KVH * slots * sh.dh, o);
+    m->Kp.push_back(kv);
+    m->Vp.push_back(kv + (size_t)sh.KVH * slots * sh.dh);
     // zero-filled: decode boxes may cover slots past a segment (masked to p = 0,
     // which must not meet a NaN bit pattern)
     CK(cudaMemsetAsync(m->Kp.back(), 0, (size_t)sh.KVH * slots * sh.dh * 2, st));
@@ -254,13 +275,10 @@ static Model* make_model(const ModelShape& sh, bool prm, uint64_t seed, long lon
         break;
       }
     }
-    m->kmap16.resize(sh.L);
-    m->vmap16.resize(sh.L);
+    m->kvmap16.resize(sh.L);
     for (int l = 0; l < sh.L && !m->kmap.empty(); ++l) {
-      if (!make_kv_tmap(&m->kmap16[l], m->Kp[l], (long long)sh.KVH * slots, sh.dh, 16) ||
-          !make_kv_tmap(&m->vmap16[l], m->Vp[l], (long long)sh.KVH * slots, sh.dh, 16)) {
-        m->kmap16.clear();
-        m->vmap16.clear();
+      if (!make_kv_tmap16(&m->kvmap16[l], m->Kp[l], m->Vp[l], (long long)sh.KVH * slots, sh.dh)) {
+        m->kvmap16.clear();
         break;
       }
     }
@@ -363,8 +381,8 @@ static void attention(Model& m, int l, const RowDesc* rows, const Segment* segs,
   if (tiles && !m.kmap.empty())
     rc = spex_k_tree_attn_tiles_mma(&m.kmap[l], &m.vmap[l], tiles, ntiles, rows, segs, m.Qr, s.H, s.KVH, s.dh,
                                     m.slots, m.O, st);
-  if (rc != 0 && !tiles && !m.kmap16.empty() && wmma_wanted(s) && g_item_ctr)
-    rc = spex_k_tree_attn_wmma(&m.kmap16[l], &m.vmap16[l], rows, segs, m.Qr, s.H, s.KVH, s.dh, m.slots, m.O, M,
+  if (rc != 0 && !tiles && !m.kvmap16.empty() && wmma_wanted(s) && g_item_ctr)
+    rc = spex_k_tree_attn_wmma(&m.kvmap16[l], rows, segs, m.Qr, s.H, s.KVH, s.dh, m.slots, m.O, M,
                                g_item_ctr, st);
   if (rc != 0 && !tiles && bulk_wanted() && g_item_ctr)
     rc = spex_k_tree_attn_bulk(rows, segs, m.Qr, s.H, s.KVH, s.dh, m.Kp[l], m.Vp[l], m.slots, m.O, M, g_item_ctr, st);

@@ -808,6 +808,17 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       : "memory");
 }
 
+// 4D box (64 columns, rows, 2 column halves, K|V): ONE copy lands a whole
+// decode stage — K then V, each as [half][row][64] (tree_attn_wmma_kernel,
+// spex_tmap_kv16)
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
+      "[%6];" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+      "l"(map), "r"(0), "r"(c1), "r"(0), "r"(0), "r"((uint32_t)__cvta_generic_to_shared(bar))
+      : "memory");
+}
+
 __device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
                : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr));
@@ -1106,7 +1117,7 @@ __device__ __forceinline__ uint32_t swz16(int row, int c) {
 
 template <int kNST, int kWarps, bool kSkipRescale>  // stages per warp, warps per block
 __global__ void __launch_bounds__(kWarps * 32, 1)
-    tree_attn_wmma_kernel(const __grid_constant__ CUtensorMap kmap16, const __grid_constant__ CUtensorMap vmap16,
+    tree_attn_wmma_kernel(const __grid_constant__ CUtensorMap kvmap16,
                           const RowDesc* __restrict__ rows, const Segment* __restrict__ segs,
                           const float* __restrict__ Qr, int H, int KVH, int G, int n_items, long long slots,
                           __nv_bfloat16* __restrict__ O, int* __restrict__ item_ctr,
@@ -1124,46 +1135,46 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
   }
   __syncwarp();
   // ---- producer cursor (lane 0 only)
-  int p_q = 0, p_item = -1, p_seg = 0, p_off = 0, p_nseg = 0, issued = 0;
+  // The producer lane is on the critical path of every stage: per stage it only
+  // issues one copy at a running row coordinate; a segment costs one 16-byte load.
+  int p_q = 0, p_item = -1, p_seg = 0, p_nseg = 0, issued = 0;
+  int p_row = 0, p_left = 0;  // next stage's pool row, tokens left in the current segment
   long long p_row0 = 0;
   const Segment* p_sg = nullptr;
   bool p_done = false;
   auto produce = [&]() {
     while (!p_done) {
-      if (p_item < 0 || p_seg >= p_nseg) {
-        const int it = atomicAdd(item_ctr, 1);
-        if (it >= n_items) {
-          queue[warp][p_q & 7] = -1;
-          p_done = true;
-          return;
-        }
-        queue[warp][p_q & 7] = it;
-        ++p_q;
-        p_item = it;
-        const RowDesc rd = rows[row_order ? row_order[it / KVH] : it / KVH];
-        p_sg = segs + rd.seg_off;
-        p_nseg = rd.nseg;
-        p_seg = 0;
-        p_off = 0;
-        p_row0 = (long long)(it % KVH) * slots;
+      if (p_left > 0) {
+        const int st = issued % kNST;
+        unsigned char* kb = ring + st * 2 * STAGE;
+        mbar_expect_tx(&bar[warp][st], 2 * STAGE);
+        tma_load_4d(kb, &kvmap16, p_row, &bar[warp][st]);  // K at kb, V at kb + STAGE
+        p_row += CH;
+        p_left -= CH;
+        ++issued;
+        return;
       }
-      const int len = p_sg[p_seg].len;
-      if (p_off >= len) {
+      if (p_item >= 0 && p_seg < p_nseg) {
+        const int4 v = __ldg(reinterpret_cast<const int4*>(p_sg + p_seg));  // Segment {base, len, own0}
         ++p_seg;
-        p_off = 0;
+        p_row = (int)(p_row0 + (long long)(((unsigned long long)(unsigned)v.y << 32) | (unsigned)v.x));
+        p_left = v.z;
         continue;
       }
-      const int rowc = (int)(p_row0 + p_sg[p_seg].base + p_off);
-      const int st = issued % kNST;
-      unsigned char* kb = ring + st * 2 * STAGE;
-      mbar_expect_tx(&bar[warp][st], 2 * STAGE);
-      tma_load_2d(kb, &kmap16, 0, rowc, &bar[warp][st]);
-      tma_load_2d(kb + 2048, &kmap16, 64, rowc, &bar[warp][st]);
-      tma_load_2d(kb + STAGE, &vmap16, 0, rowc, &bar[warp][st]);
-      tma_load_2d(kb + STAGE + 2048, &vmap16, 64, rowc, &bar[warp][st]);
-      p_off += CH;
-      ++issued;
-      return;
+      const int it = atomicAdd(item_ctr, 1);
+      if (it >= n_items) {
+        queue[warp][p_q & 7] = -1;
+        p_done = true;
+        return;
+      }
+      queue[warp][p_q & 7] = it;
+      ++p_q;
+      p_item = it;
+      const RowDesc rd = rows[row_order ? row_order[it / KVH] : it / KVH];
+      p_sg = segs + rd.seg_off;
+      p_nseg = rd.nseg;
+      p_seg = 0;
+      p_row0 = (long long)(it % KVH) * slots;
     }
   };
   if (lane == 0)
@@ -1736,10 +1747,10 @@ extern "C" int spex_k_tree_attn_bulk(const RowDesc* rows, const Segment* segs, c
 }
 
 // K1 decode rows on the per-warp TMA + mma.sync pipeline (G <= 16, dh = 128);
-// kmap16/vmap16 are the pools' 2D maps with 64 x 16 boxes (spex_tmap_kv16).
+// kvmap16 is the layer's K|V pool pair as one 4D map (spex_tmap_kv16).
 
 template <int NST, int W, bool SKIP = false>
-static int launch_wmma(const CUtensorMap* kmap16, const CUtensorMap* vmap16, const RowDesc* rows, const Segment* segs,
+static int launch_wmma(const CUtensorMap* kvmap16, const RowDesc* rows, const Segment* segs,
                        const float* Qr, int H, int KVH, int G, long long slots, __nv_bfloat16* O, int M,
                        int* item_ctr, cudaStream_t s) {
   const size_t smem = (size_t)W * NST * 2 * 16 * 128 * 2 + 1024;
@@ -1754,19 +1765,19 @@ static int launch_wmma(const CUtensorMap* kmap16, const CUtensorMap* vmap16, con
   const int n_items = M * KVH;
   const int grid = std::min(blocks, (n_items + W - 1) / W);
   cudaMemsetAsync(item_ctr, 0, sizeof(int), s);
-  tree_attn_wmma_kernel<NST, W, SKIP><<<grid, W * 32, smem, s>>>(*kmap16, *vmap16, rows, segs, Qr, H, KVH, G, n_items,
+  tree_attn_wmma_kernel<NST, W, SKIP><<<grid, W * 32, smem, s>>>(*kvmap16, rows, segs, Qr, H, KVH, G, n_items,
                                                                  slots, O, item_ctr, g_k1_row_order);
   return (int)cudaGetLastError();
 }
 
-extern "C" int spex_k_tree_attn_wmma(const CUtensorMap* kmap16, const CUtensorMap* vmap16, const RowDesc* rows,
+extern "C" int spex_k_tree_attn_wmma(const CUtensorMap* kvmap16, const RowDesc* rows,
                                      const Segment* segs, const float* Qr, int H, int KVH, int dh, long long slots,
                                      __nv_bfloat16* O, int M, int* item_ctr, cudaStream_t s) {
   const int G = H / KVH;
   if (M <= 0) return 0;
   if (dh != 128 || G < 1 || G > 16) return -1;
   // 2 stages x 12 warps (8 KB per stage): the best of a stages x warps sweep on c5
-  return launch_wmma<kMmaNST, kMmaWarps>(kmap16, vmap16, rows, segs, Qr, H, KVH, G, slots, O, M, item_ctr, s);
+  return launch_wmma<kMmaNST, kMmaWarps>(kvmap16, rows, segs, Qr, H, KVH, G, slots, O, M, item_ctr, s);
 }
 
 template <int DH, int G>

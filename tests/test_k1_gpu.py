@@ -100,18 +100,23 @@ def test_k1_decode_matches_torch_fp32(H, KVH, dh, M, impl):
         from paper_2605_10195_b200 import _lib as L
         lib = L.lib()
         lib.spex_tmap_kv16.restype = ctypes.c_int
-        lib.spex_tmap_kv16.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_longlong, ctypes.c_int]
+        lib.spex_tmap_kv16.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_longlong,
+                                       ctypes.c_int]
         fw = lib.spex_k_tree_attn_wmma
         fw.restype = ctypes.c_int
-        fw.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+        fw.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                        ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_longlong, ctypes.c_void_p, ctypes.c_int,
                        ctypes.c_void_p, ctypes.c_void_p]
-        km, vm = ctypes.create_string_buffer(256), ctypes.create_string_buffer(256)
-        kp, vp = (ctypes.addressof(km) + 63) & ~63, (ctypes.addressof(vm) + 63) & ~63
-        assert lib.spex_tmap_kv16(kp, K.data_ptr(), KVH * slots, dh) == 0
-        assert lib.spex_tmap_kv16(vp, V.data_ptr(), KVH * slots, dh) == 0
+        # the pools' K|V pair as one map: V must sit above K (one allocation, as the model's pools)
+        KV = torch.stack([K, V])
+        K, V = KV[0], KV[1]
+        km = ctypes.create_string_buffer(256)
+        kp = (ctypes.addressof(km) + 63) & ~63
+        assert lib.spex_tmap_kv16(kp, K.data_ptr(), V.data_ptr(), KVH * slots, dh) == 0
+        assert lib.spex_tmap_kv16(kp, V.data_ptr(), K.data_ptr(), KVH * slots, dh) != 0  # V below K: refused
+        assert lib.spex_tmap_kv16(kp, K.data_ptr(), V.data_ptr(), KVH * slots, dh) == 0
         ctr = torch.zeros(1, dtype=torch.int32, device=dev)
-        rc = fw(kp, vp, rows_d.data_ptr(), segs_d.data_ptr(), Q.data_ptr(), H, KVH, dh, slots, O.data_ptr(), M,
+        rc = fw(kp, rows_d.data_ptr(), segs_d.data_ptr(), Q.data_ptr(), H, KVH, dh, slots, O.data_ptr(), M,
                 ctr.data_ptr(), st.cuda_stream)
         assert rc == 0
     elif impl == "bulk":
