@@ -379,7 +379,9 @@ int spex_termination_should_terminate(const int* counts, const double* weights, 
  *   spex_engine_drop               drop(id)                                     sim.cpp:235-249
  *   spex_engine_step               advance(now, limit, out): finished streams
  *                                  in out[cap], *reached = the clock reached    sim.cpp:305-384
- *   spex_engine_done_tokens / stream_count / active_count / next_ready */
+ *   spex_engine_done_tokens / stream_count / active_count / next_ready
+ * Stream ids must be unique among the handle's streams (the reference looks
+ * them up by id, first match). */
 typedef struct spex_engine spex_engine;
 int spex_engine_create(const spex_engine_hw* hw, int device, spex_engine** out);
 void spex_engine_destroy(spex_engine* e);

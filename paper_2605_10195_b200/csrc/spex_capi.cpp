@@ -1461,8 +1461,8 @@ void run_executor(spex_executor& ex, int trace) {
       // split.run_split_rank)
       ex.node_cap0 = node_cap * 2;
       fail(ex.g.error, "split rank " + std::to_string(ex.split_rank) + ": node capacity " +
-                           std::to_string(node_cap) + " exhausted; rerun every rank with node capacity " +
-                           std::to_string(node_cap * 2));
+                           std::to_string(node_cap) + " exhausted; rerun every rank with SPEX_NODE_CAP=" +
+                           std::to_string(node_cap * 2) + " (a new epoch)");
     }
     if (ex.g.error == ERR_CAP_NODES || ex.g.error == ERR_CAP_STAGE) {
       node_cap *= 2;  // capacity, not semantics: rerun with a larger arena
