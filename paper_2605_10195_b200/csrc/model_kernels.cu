@@ -627,68 +627,67 @@ __global__ void __launch_bounds__(kBulkWarps * 32, 1)
   __syncwarp();
   uint64_t kv_pol;  // KV is streamed once per step: evict first
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(kv_pol));
-  // ---- producer cursor (lane 0 only): item, segment, offset
+  // ---- producer cursor (lane 0 only). The producer lane is on the critical
+  // path of every stage: per stage it only issues the two copies from running
+  // K / V pointers; a segment costs one 16-byte load (the GQA kernel's lesson,
+  // profiles/r02zt_k1_gqa_tma_ab.txt).
   int p_q = 0;                   // items claimed so far (queue position)
-  int p_item = -1, p_seg = 0, p_off = 0, p_nseg = 0;
+  int p_item = -1, p_seg = 0, p_nseg = 0;
   long long p_segoff = 0;
   const Segment* p_sg = nullptr;
-  // the current segment and the next one, loaded a segment ahead so a segment
-  // change issues its first chunk without waiting on the list
-  long long p_base = 0, p_nbase = 0;
-  int p_len = 0, p_nlen = 0;
+  const __nv_bfloat16* p_k = nullptr;  // next chunk's K / V rows
+  const __nv_bfloat16* p_v = nullptr;
+  int p_left = 0;                      // tokens left in the current segment
   bool p_done = false;
   int issued = 0;
   auto produce = [&]() {  // lane 0: issue the next chunk into stage issued % NST
     while (!p_done) {
-      if (p_item < 0 || p_seg >= p_nseg) {  // next item
-        const int it = atomicAdd(item_ctr, 1);
-        if (it >= n_items) {
-          queue[warp][p_q & 7] = -1;
-          p_done = true;
-          // item_ctr[1] counts warps past their last claim; the last one
-          // re-zeroes both, so the next launch needs no memset
-          if (atomicAdd(item_ctr + 1, 1) == (int)gridDim.x * kBulkWarps - 1) {
-            item_ctr[1] = 0;
-            atomicExch(item_ctr, 0);
-          }
-          return;
+      if (p_left > 0) {
+        const int n = p_left < kBulkCH ? p_left : kBulkCH;
+        const int st = issued % kBulkNST;
+        unsigned char* kb = ring + st * 2 * STAGE;
+        mbar_expect_tx(&bar[warp][st], 2u * n * DH * 2);
+        if (kv_evict_first) {
+          bulk_g2s_hint(kb, p_k, n * DH * 2, &bar[warp][st], kv_pol);
+          bulk_g2s_hint(kb + STAGE, p_v, n * DH * 2, &bar[warp][st], kv_pol);
+        } else {
+          bulk_g2s(kb, p_k, n * DH * 2, &bar[warp][st]);
+          bulk_g2s(kb + STAGE, p_v, n * DH * 2, &bar[warp][st]);
         }
-        queue[warp][p_q & 7] = it;
-        ++p_q;
-        p_item = it;
-        const RowDesc rd = rows[row_order ? row_order[it / KVH] : it / KVH];
-        p_sg = segs + rd.seg_off;
-        p_nseg = rd.nseg;
-        p_seg = 0;
-        p_off = 0;
-        p_segoff = (long long)(it % KVH) * slots;
-        p_len = 0;
-        if (p_nseg > 0) load_seg(p_sg, p_base, p_len);
-        if (p_nseg > 1) load_seg(p_sg + 1, p_nbase, p_nlen);
+        p_k += kBulkCH * DH;
+        p_v += kBulkCH * DH;
+        p_left -= n;
+        ++issued;
+        return;
       }
-      if (p_off >= p_len) {
-        if (++p_seg >= p_nseg) continue;
-        p_base = p_nbase;
-        p_len = p_nlen;
-        if (p_seg + 1 < p_nseg) load_seg(p_sg + p_seg + 1, p_nbase, p_nlen);
-        p_off = 0;
+      if (p_item >= 0 && p_seg < p_nseg) {  // next segment of the item
+        long long base;
+        load_seg(p_sg + p_seg, base, p_left);
+        ++p_seg;
+        p_k = Kp + (p_segoff + base) * DH;
+        p_v = Vp + (p_segoff + base) * DH;
         continue;
       }
-      const int n = min(kBulkCH, p_len - p_off);
-      const long long tok = p_segoff + p_base + p_off;
-      const int st = issued % kBulkNST;
-      unsigned char* kb = ring + st * 2 * STAGE;
-      mbar_expect_tx(&bar[warp][st], 2u * n * DH * 2);
-      if (kv_evict_first) {
-        bulk_g2s_hint(kb, Kp + tok * DH, n * DH * 2, &bar[warp][st], kv_pol);
-        bulk_g2s_hint(kb + STAGE, Vp + tok * DH, n * DH * 2, &bar[warp][st], kv_pol);
-      } else {
-        bulk_g2s(kb, Kp + tok * DH, n * DH * 2, &bar[warp][st]);
-        bulk_g2s(kb + STAGE, Vp + tok * DH, n * DH * 2, &bar[warp][st]);
+      const int it = atomicAdd(item_ctr, 1);  // next item
+      if (it >= n_items) {
+        queue[warp][p_q & 7] = -1;
+        p_done = true;
+        // item_ctr[1] counts warps past their last claim; the last one
+        // re-zeroes both, so the next launch needs no memset
+        if (atomicAdd(item_ctr + 1, 1) == (int)gridDim.x * kBulkWarps - 1) {
+          item_ctr[1] = 0;
+          atomicExch(item_ctr, 0);
+        }
+        return;
       }
-      p_off += n;
-      ++issued;
-      return;
+      queue[warp][p_q & 7] = it;
+      ++p_q;
+      p_item = it;
+      const RowDesc rd = rows[row_order ? row_order[it / KVH] : it / KVH];
+      p_sg = segs + rd.seg_off;
+      p_nseg = rd.nseg;
+      p_seg = 0;
+      p_segoff = (long long)(it % KVH) * slots;
     }
   };
   if (lane == 0)
