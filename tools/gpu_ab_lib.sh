@@ -4,7 +4,7 @@
 # runs of config 5 (8B + 1.5B PRM) and config 2 (mid) timing; K1 tests first.
 TAG=${1:-x}
 OUT=gpurun_out; mkdir -p $OUT
-timeout 900 python -m pytest tests/test_k1_gpu.py tests/test_model_gpu.py -q -x --timeout 600 > $OUT/ab_tests_$TAG.log 2>&1; echo "pytest rc=$?" >> $OUT/ab_tests_$TAG.log
+timeout 900 python -m pytest tests/test_k1_gpu.py tests/test_model_gpu.py tests/test_gemm_tc_gpu.py -q -x --timeout 600 > $OUT/ab_tests_$TAG.log 2>&1; echo "pytest rc=$?" >> $OUT/ab_tests_$TAG.log
 tail -2 $OUT/ab_tests_$TAG.log
 BASE=paper_2605_10195_b200/lib/ab/libspex_b200_base.so
 NEW=paper_2605_10195_b200/lib/libspex_b200.so
