@@ -1182,7 +1182,13 @@ void run_executor(spex_executor& ex, int trace) {
           fail(ERR_INTERNAL, "split emulation: peer rank setup failed: " + g_err);
       }
       peer_group = group_new();
-      group_launch(*peer_group, peers, ex.device, 0, node_cap, &ex.split_boxes);
+      try {
+        group_launch(*peer_group, peers, ex.device, 0, node_cap, &ex.split_boxes);
+      } catch (...) {  // nothing launched: drop the group so finish_peers has nothing to wait for
+        group_delete(peer_group);
+        peer_group = nullptr;
+        throw;
+      }
     };
     auto finish_peers = [&]() -> int {
       int e = 0;
@@ -1347,7 +1353,12 @@ void run_executor(spex_executor& ex, int trace) {
       sv.pub_entries = h_ents;
       alloc_outputs(static_cast<long long>(Q) * node_cap * 64);
       mark("pre-launch");
-      launch_peers();
+      try {
+        launch_peers();
+      } catch (...) {
+        cleanup();
+        throw;
+      }
       int lr = spex_launch_control_async(d_run, Q, ex.nthreads, ex.stream, ca, cb);
       if (lr != 0) {
         cleanup();
@@ -1365,7 +1376,12 @@ void run_executor(spex_executor& ex, int trace) {
         fail(201, std::string("model forward: ") + e.what());
       }
     } else {
-      launch_peers();
+      try {
+        launch_peers();
+      } catch (...) {
+        cleanup();
+        throw;
+      }
       int lr = spex_launch_control_async(d_run, Q, ex.nthreads, ex.stream, ca, cb);
       if (lr != 0) {
         cleanup();
@@ -1631,7 +1647,16 @@ void group_launch(GroupLaunch& G, std::vector<spex_executor*>& exs, int device, 
   cudaEventCreate(&G.ca);
   cudaEventCreate(&G.cb);
   const int lr = spex_launch_control_batch_async(G.d_runs, n, qmax, nthreads, st, G.ca, G.cb);
-  if (lr != 0) fail(200, std::string("control kernel launch failed: ") + cudaGetErrorString(static_cast<cudaError_t>(lr)));
+  if (lr != 0) {
+    cudaFreeAsync(G.big, st);
+    cudaFreeAsync(G.d_runs, st);
+    cudaStreamSynchronize(st);
+    cudaStreamDestroy(st);
+    cudaEventDestroy(G.ca);
+    cudaEventDestroy(G.cb);
+    G = GroupLaunch{};
+    fail(200, std::string("control kernel launch failed: ") + cudaGetErrorString(static_cast<cudaError_t>(lr)));
+  }
 }
 
 int group_finish(GroupLaunch& G, std::vector<spex_executor*>& exs, int trace, float* ms_out) {
