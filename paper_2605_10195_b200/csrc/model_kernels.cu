@@ -1593,6 +1593,7 @@ extern "C" void spex_k_rmsnorm(const float* X, int M, int d, float eps, __nv_bfl
       case 512: return launch_maybe_pdl(rmsnorm_bf16_reg_kernel<4>, grid, block, 0, s, X, M, eps, Y);
       case 1024: return launch_maybe_pdl(rmsnorm_bf16_reg_kernel<8>, grid, block, 0, s, X, M, eps, Y);
       case 1536: return launch_maybe_pdl(rmsnorm_bf16_reg_kernel<12>, grid, block, 0, s, X, M, eps, Y);
+      case 4096: return launch_maybe_pdl(rmsnorm_bf16_reg_kernel<32>, grid, block, 0, s, X, M, eps, Y);  // Llama-3-8B
       default: break;
     }
   launch_maybe_pdl(rmsnorm_bf16_kernel, grid, block, 0, s, X, M, d, eps, Y);
@@ -1889,6 +1890,7 @@ extern "C" void spex_k_preload() {
   preload_one(rmsnorm_bf16_kernel);
   preload_one(rmsnorm_bf16_reg_kernel<4>);
   preload_one(rmsnorm_bf16_reg_kernel<8>);
+  preload_one(rmsnorm_bf16_reg_kernel<32>);
   preload_one(rmsnorm_bf16_reg_kernel<12>);
 #define SPEX_PRELOAD_DEC(D, GG)                      \
   preload_one(tree_attn_decode_kernel<D, GG, 8>);    \
