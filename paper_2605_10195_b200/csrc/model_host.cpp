@@ -38,7 +38,7 @@ void spex_k_build_decode_rows(TreeView t, const int* sids, const int* pos0, int 
 void spex_k_build_prm_rows(TreeView t, const int* sids, const int* row_start, const int* tile_start, int n,
                            RowDesc* rows, Segment* segs, int* last_row, TileDesc* tiles, cudaStream_t s);
 void spex_k_build_prompt_tiles(int nq, int P, TileDesc* tiles, cudaStream_t s);
-int spex_k_tree_attn_tiles_mma(const CUtensorMap* kmap, const CUtensorMap* vmap, const TileDesc* tiles, int ntiles,
+int spex_k_tree_attn_tiles_mma(const CUtensorMap* kvmap, const TileDesc* tiles, int ntiles,
                                const RowDesc* rows, const Segment* segs, const float* Qr, int H, int KVH, int dh,
                                long long slots, __nv_bfloat16* O, cudaStream_t s);
 int spex_k_tree_attn_tiles(const TileDesc* tiles, int ntiles, const RowDesc* rows, const Segment* segs,
@@ -116,44 +116,34 @@ static PFN_tmap_encode tmap_encoder() {
   return fn;
 }
 
-static bool make_kv_tmap(CUtensorMap* m, void* base, long long rows, int dh, int box_rows = 64) {
-  PFN_tmap_encode enc = tmap_encoder();
-  if (!enc || dh != 128) return false;
-  cuuint64_t dims[2] = {(cuuint64_t)dh, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)dh * 2};
-  cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
-  cuuint32_t es[2] = {1, 1};
-  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
-// TMA descriptor of one layer's tree-KV pool for the tile attention kernel.
-extern "C" int spex_tmap_kv(CUtensorMap* m, void* base, long long rows, int dh) {
-  return make_kv_tmap(m, base, rows, dh) ? 0 : -1;
-}
-
-// ... for the per-warp decode pipeline (tree_attn_wmma_kernel): the layer's K
-// and V pools (V above K) as one 4D view (64 columns, rows, the 2 column
-// halves at +128 B, K|V at +(V - K)) with (64, 16, 2, 2) boxes, so ONE copy of
-// 8 KB fills a decode stage: K then V, each [half][16 rows][64], 128-byte
-// swizzled (the producer lane issues one copy per stage instead of four: it is
-// on the critical path of every stage, profiles/r02zt_k1_gqa_tma_ab.txt).
-static bool make_kv_tmap16(CUtensorMap* m, void* k, void* v, long long rows, int dh) {
+// TMA descriptors of one layer's tree-KV pools: the K and V pools (one
+// allocation, V above K) as one 4D view — 64 columns, rows, the 2 column
+// halves at +128 B, K|V at +(V - K) — with (64, box_rows, 2, 2) boxes, so ONE
+// copy fills a whole K+V stage: K then V, each [half][box_rows rows][64],
+// 128-byte swizzled (conflict-free ldmatrix). The K1 kernels issue their stage
+// copies from inside the consumer loop, where every extra copy is on the
+// critical path (profiles/r02zt_k1_gqa_tma_ab.txt).
+static bool make_kv_pair_tmap(CUtensorMap* m, void* k, void* v, long long rows, int dh, int box_rows) {
   PFN_tmap_encode enc = tmap_encoder();
   const uintptr_t kb = reinterpret_cast<uintptr_t>(k), vb = reinterpret_cast<uintptr_t>(v);
   if (!enc || dh != 128 || vb <= kb || (vb - kb) % 16 != 0 || (vb - kb) >= (1ULL << 40)) return false;
   cuuint64_t dims[4] = {64, (cuuint64_t)rows, 2, 2};
   cuuint64_t strides[3] = {(cuuint64_t)dh * 2, 128, (cuuint64_t)(vb - kb)};
-  cuuint32_t box[4] = {64, 16, 2, 2};
+  cuuint32_t box[4] = {64, (cuuint32_t)box_rows, 2, 2};
   cuuint32_t es[4] = {1, 1, 1, 1};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, k, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// 64-token chunks of the tile kernel (PRM / prompt rows, tree_attn_tile_mma_kernel).
+extern "C" int spex_tmap_kv(CUtensorMap* m, void* k, void* v, long long rows, int dh) {
+  return make_kv_pair_tmap(m, k, v, rows, dh, 64) ? 0 : -1;
+}
+
+// 16-token stages of the per-warp decode pipeline (tree_attn_wmma_kernel).
 extern "C" int spex_tmap_kv16(CUtensorMap* m, void* k, void* v, long long rows, int dh) {
-  return make_kv_tmap16(m, k, v, rows, dh) ? 0 : -1;
+  return make_kv_pair_tmap(m, k, v, rows, dh, 16) ? 0 : -1;
 }
 
 // TMA descriptor of a row-major bf16 matrix [rows][cols] as a GEMM operand of
@@ -180,7 +170,7 @@ struct TcWeight {
 
 struct Model {
   ModelShape sh;
-  std::vector<CUtensorMap> kmap, vmap;      // per layer (empty when TMA maps are unavailable)
+  std::vector<CUtensorMap> kvmap;           // per layer, K|V pair, 64-row boxes (empty without TMA maps)
   std::vector<CUtensorMap> kvmap16;  // K|V pair, 16-row boxes (decode pipeline)
   bool is_prm;
   long long slots;
@@ -265,19 +255,13 @@ static Model* make_model(const ModelShape& sh, bool prm, uint64_t seed, long lon
     CK(cudaMemsetAsync(m->Vp.back(), 0, (size_t)sh.KVH * slots * sh.dh * 2, st));
   }
   if (!getenv("SPEX_NO_MMA_ATTN")) {
-    m->kmap.resize(sh.L);
-    m->vmap.resize(sh.L);
-    for (int l = 0; l < sh.L; ++l) {
-      if (!make_kv_tmap(&m->kmap[l], m->Kp[l], (long long)sh.KVH * slots, sh.dh) ||
-          !make_kv_tmap(&m->vmap[l], m->Vp[l], (long long)sh.KVH * slots, sh.dh)) {
-        m->kmap.clear();
-        m->vmap.clear();
-        break;
-      }
-    }
+    m->kvmap.resize(sh.L);
     m->kvmap16.resize(sh.L);
-    for (int l = 0; l < sh.L && !m->kmap.empty(); ++l) {
-      if (!make_kv_tmap16(&m->kvmap16[l], m->Kp[l], m->Vp[l], (long long)sh.KVH * slots, sh.dh)) {
+    for (int l = 0; l < sh.L; ++l) {
+      const long long rows = (long long)sh.KVH * slots;
+      if (!make_kv_pair_tmap(&m->kvmap[l], m->Kp[l], m->Vp[l], rows, sh.dh, 64) ||
+          !make_kv_pair_tmap(&m->kvmap16[l], m->Kp[l], m->Vp[l], rows, sh.dh, 16)) {
+        m->kvmap.clear();
         m->kvmap16.clear();
         break;
       }
@@ -378,8 +362,8 @@ static void attention(Model& m, int l, const RowDesc* rows, const Segment* segs,
                       int ntiles, cudaStream_t st) {
   const ModelShape& s = m.sh;
   int rc = -1;
-  if (tiles && !m.kmap.empty())
-    rc = spex_k_tree_attn_tiles_mma(&m.kmap[l], &m.vmap[l], tiles, ntiles, rows, segs, m.Qr, s.H, s.KVH, s.dh,
+  if (tiles && !m.kvmap.empty())
+    rc = spex_k_tree_attn_tiles_mma(&m.kvmap[l], tiles, ntiles, rows, segs, m.Qr, s.H, s.KVH, s.dh,
                                     m.slots, m.O, st);
   if (rc != 0 && !tiles && !m.kvmap16.empty() && wmma_wanted(s) && g_item_ctr)
     rc = spex_k_tree_attn_wmma(&m.kvmap16[l], rows, segs, m.Qr, s.H, s.KVH, s.dh, m.slots, m.O, M,

@@ -844,8 +844,7 @@ __device__ __forceinline__ uint32_t swz(int row, int c) {
 }
 
 template <int G>
-__global__ void __launch_bounds__(128) tree_attn_tile_mma_kernel(const __grid_constant__ CUtensorMap kmap,
-                                                                const __grid_constant__ CUtensorMap vmap,
+__global__ void __launch_bounds__(128) tree_attn_tile_mma_kernel(const __grid_constant__ CUtensorMap kvmap,
                                                                 const TileDesc* __restrict__ tiles,
                                                                 const RowDesc* __restrict__ rows,
                                                                 const Segment* __restrict__ segs,
@@ -922,10 +921,8 @@ __global__ void __launch_bounds__(128) tree_attn_tile_mma_kernel(const __grid_co
     unsigned char* vb = kb + 16384;
     const int rowc = (int)((long long)kh * slots + cb[b]);
     mbar_expect_tx(&bar[b], 32768);
-    tma_load_2d(kb, &kmap, 0, rowc, &bar[b]);
-    tma_load_2d(kb + 8192, &kmap, 64, rowc, &bar[b]);
-    tma_load_2d(vb, &vmap, 0, rowc, &bar[b]);
-    tma_load_2d(vb + 8192, &vmap, 64, rowc, &bar[b]);
+    tma_load_4d(kb, &kvmap, rowc, &bar[b]);  // one copy: K at kb, V at kb + 16384 (= vb)
+    (void)vb;
   };
   for (int c = 0; c < 2 && c < nchunks; ++c) {
     next_chunk(c);
@@ -1795,7 +1792,7 @@ static void launch_tile(const TileDesc* tiles, int ntiles, const RowDesc* rows, 
   tree_attn_tile_kernel<DH, G><<<grid, kAttnThreads, smem, s>>>(tiles, rows, segs, Qr, H, Kp, Vp, slots, O);
 }
 
-extern "C" int spex_k_tree_attn_tiles_mma(const CUtensorMap* kmap, const CUtensorMap* vmap, const TileDesc* tiles,
+extern "C" int spex_k_tree_attn_tiles_mma(const CUtensorMap* kvmap, const TileDesc* tiles,
                                           int ntiles, const RowDesc* rows, const Segment* segs, const float* Qr, int H,
                                           int KVH, int dh, long long slots, __nv_bfloat16* O, cudaStream_t s) {
   const int G = H / KVH;
@@ -1812,7 +1809,7 @@ extern "C" int spex_k_tree_attn_tiles_mma(const CUtensorMap* kmap, const CUtenso
                            (int)smem);                                                               \
       attr = true;                                                                                   \
     }                                                                                                \
-    tree_attn_tile_mma_kernel<GG><<<grid, 128, smem, s>>>(*kmap, *vmap, tiles, rows, segs, Qr, H, slots, O, G); \
+    tree_attn_tile_mma_kernel<GG><<<grid, 128, smem, s>>>(*kvmap, tiles, rows, segs, Qr, H, slots, O, G);        \
     return 0;                                                                                        \
   }
   SPEX_MMA_CASE(1)

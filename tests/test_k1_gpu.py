@@ -172,10 +172,10 @@ def test_k1_tile_mma_matches_torch_fp32(H, KVH):
         pytest.fail("no sm_100 device")
     lib = L.lib()
     lib.spex_tmap_kv.restype = ctypes.c_int
-    lib.spex_tmap_kv.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_longlong, ctypes.c_int]
+    lib.spex_tmap_kv.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_longlong, ctypes.c_int]
     f = lib.spex_k_tree_attn_tiles_mma
     f.restype = ctypes.c_int
-    f.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
+    f.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
                   ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_longlong, ctypes.c_void_p,
                   ctypes.c_void_p]
     dh = 128
@@ -226,13 +226,13 @@ def test_k1_tile_mma_matches_torch_fp32(H, KVH):
     Q = (torch.randn(M, H, dh, generator=g) * 2.0 / dh ** 0.5).to(dev)
     O = torch.zeros(M, H, dh, dtype=torch.bfloat16, device=dev)
     bufs = [torch.from_numpy(a.view(np.uint8).copy()).to(dev) for a in (rows_np, segs_np, tiles_np)]
-    km, vm = ctypes.create_string_buffer(256), ctypes.create_string_buffer(256)
+    KV = torch.stack([K, V])  # the pools' K|V pair as one map: V above K, as the model allocates them
+    K, V = KV[0], KV[1]
+    km = ctypes.create_string_buffer(256)
     kp = (ctypes.addressof(km) + 63) & ~63
-    vp = (ctypes.addressof(vm) + 63) & ~63
-    assert lib.spex_tmap_kv(kp, K.data_ptr(), KVH * slots, dh) == 0
-    assert lib.spex_tmap_kv(vp, V.data_ptr(), KVH * slots, dh) == 0
+    assert lib.spex_tmap_kv(kp, K.data_ptr(), V.data_ptr(), KVH * slots, dh) == 0
     st = torch.cuda.current_stream(dev)
-    rc = f(kp, vp, bufs[2].data_ptr(), len(tiles), bufs[0].data_ptr(), bufs[1].data_ptr(), Q.data_ptr(), H, KVH, dh,
+    rc = f(kp, bufs[2].data_ptr(), len(tiles), bufs[0].data_ptr(), bufs[1].data_ptr(), Q.data_ptr(), H, KVH, dh,
            slots, O.data_ptr(), st.cuda_stream)
     assert rc == 0
     torch.cuda.synchronize()
