@@ -1111,7 +1111,7 @@ __device__ __forceinline__ uint32_t swz16(int row, int c) {
   return (uint32_t)(half * 2048 + row * 128 + ((cc ^ (row & 7)) << 4));
 }
 
-template <int kNST, int kWarps>  // stages per warp, warps per block
+template <int kNST, int kWarps, bool kSkipRescale>  // stages per warp, warps per block
 __global__ void __launch_bounds__(kWarps * 32, 1)
     tree_attn_wmma_kernel(const __grid_constant__ CUtensorMap kvmap16,
                           const RowDesc* __restrict__ rows, const Segment* __restrict__ segs,
@@ -1244,14 +1244,9 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
           mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, o));
           mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, o));
         }
-        // lazy rescale: a row's running max moves only when a tile's max exceeds
-        // it by more than 8 (log2 units), so p <= 2^8 and most stages skip the
-        // accumulator rescale; O and l share the same max, so O / l is the
-        // softmax up to rounding (a per-quad decision, no warp vote)
-        const bool up0 = mx0 > m0 + 8.f, up1 = mx1 > m1 + 8.f;  // m = -inf: any finite max moves it
-        const float mn0 = up0 ? mx0 : m0, mn1 = up1 ? mx1 : m1;
-        const float a0 = (up0 && m0 != -INFINITY) ? exp2f(m0 - mn0) : 1.f;
-        const float a1 = (up1 && m1 != -INFINITY) ? exp2f(m1 - mn1) : 1.f;
+        const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
+        const float a0 = mn0 == -INFINITY ? 1.f : exp2f(m0 - mn0);
+        const float a1 = mn1 == -INFINITY ? 1.f : exp2f(m1 - mn1);
         uint32_t pa[4];
         float ps0 = 0.f, ps1 = 0.f;
 #pragma unroll
@@ -1267,7 +1262,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
         }
         l0 = l0 * a0 + ps0;
         l1 = l1 * a1 + ps1;
-        if (up0 || up1) {
+        // a == 1 exactly when a row's running max did not move: the rescale can be skipped
+        if (!kSkipRescale || !__all_sync(0xffffffffu, mn0 == m0 && mn1 == m1)) {
 #pragma unroll
           for (int nn = 0; nn < 16; ++nn) {
             oacc[nn][0] *= a0;
@@ -1750,14 +1746,14 @@ extern "C" int spex_k_tree_attn_bulk(const RowDesc* rows, const Segment* segs, c
 // K1 decode rows on the per-warp TMA + mma.sync pipeline (G <= 16, dh = 128);
 // kvmap16 is the layer's K|V pool pair as one 4D map (spex_tmap_kv16).
 
-template <int NST, int W>
+template <int NST, int W, bool SKIP = false>
 static int launch_wmma(const CUtensorMap* kvmap16, const RowDesc* rows, const Segment* segs,
                        const float* Qr, int H, int KVH, int G, long long slots, __nv_bfloat16* O, int M,
                        int* item_ctr, cudaStream_t s) {
   const size_t smem = (size_t)W * NST * 2 * 16 * 128 * 2 + 1024;
   static int blocks = 0;
   if (!blocks) {
-    cudaFuncSetAttribute(tree_attn_wmma_kernel<NST, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(tree_attn_wmma_kernel<NST, W, SKIP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -1766,7 +1762,7 @@ static int launch_wmma(const CUtensorMap* kvmap16, const RowDesc* rows, const Se
   const int n_items = M * KVH;
   const int grid = std::min(blocks, (n_items + W - 1) / W);
   cudaMemsetAsync(item_ctr, 0, sizeof(int), s);
-  tree_attn_wmma_kernel<NST, W><<<grid, W * 32, smem, s>>>(*kvmap16, rows, segs, Qr, H, KVH, G, n_items,
+  tree_attn_wmma_kernel<NST, W, SKIP><<<grid, W * 32, smem, s>>>(*kvmap16, rows, segs, Qr, H, KVH, G, n_items,
                                                                  slots, O, item_ctr, g_k1_row_order);
   return (int)cudaGetLastError();
 }
@@ -1909,7 +1905,7 @@ extern "C" void spex_k_preload() {
   preload_one(tree_attn_decode_kernel<64, 4, 8>);
   preload_one(tree_attn_decode_kernel<64, 4, 4>);
   preload_one(tree_attn_bulk_kernel<16, 2, 14>);
-  preload_one(tree_attn_wmma_kernel<kMmaNST, kMmaWarps>);
+  preload_one(tree_attn_wmma_kernel<kMmaNST, kMmaWarps, false>);
   preload_one(tree_attn_tile_mma_kernel<1>);
   preload_one(tree_attn_tile_mma_kernel<2>);
   preload_one(tree_attn_tile_mma_kernel<4>);
