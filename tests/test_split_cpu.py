@@ -197,3 +197,17 @@ def test_split_setup_failure_is_agreed_by_every_rank(tmp_path):
     for r in range(2):
         msg = (tmp_path / f"rank{r}.txt").read_text()
         assert msg.startswith("unavailable") and "rank 1" in msg, msg
+
+
+@needs_oracle
+def test_emulation_split_random_configs():
+    """The GPU file's random T2 cases (tests/test_split_gpu.py) in the emulation."""
+    from tests.test_split_gpu import _random_split_cases
+    L = emu()
+    for name, cfg, seed, flags, W in _random_split_cases():
+        W = min(W, json.loads(cfg)["run"]["n_queries"])
+        ref, rounds = refutil.ref_split_log(cfg, seed, flags, W)
+        got = shard.split_run(L, cfg, seed, W, flags)
+        assert [g["rounds"] for g in got] == rounds, name
+        for r in range(W):
+            assert got[r]["log"] == ref[r], (name, W, r, refutil.compare_logs(ref[r], got[r]["log"]))

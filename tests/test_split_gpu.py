@@ -152,3 +152,27 @@ def test_emulated_rank_matches_oracle(W, rank):
     assert ex.log_lines() == ref[rank]
     assert ex.model_stats()["decode_rows"] > 0
     ex.close()
+
+
+def _random_split_cases():
+    """Random configurations (tests/refutil.random_configs) with T2 forced on,
+    so every case exercises the budget exchange, at 2-4 ranks."""
+    out = []
+    for k, (name, cfg, seed, flags) in enumerate(refutil.random_configs(n=40, seed=77)):
+        c = json.loads(cfg)
+        if c["run"]["n_queries"] < 2:
+            continue
+        fl = ",".join(sorted(set((flags.split(",") if flags else []) + ["t1", "t2"])))
+        out.append((name, json.dumps(c), seed, fl, 2 + k % 3))
+    return out[:24]
+
+
+@needs_oracle
+@pytest.mark.parametrize("name,cfg,seed,flags,W", _random_split_cases())
+def test_split_random_configs(name, cfg, seed, flags, W):
+    W = min(W, json.loads(cfg)["run"]["n_queries"])
+    ref, rounds = refutil.ref_split_log(cfg, seed, flags, W)
+    got = spex.split_run(cfg, seed, W, flags)
+    assert [g["rounds"] for g in got] == rounds
+    for r in range(W):
+        assert got[r]["log"] == ref[r], (name, W, r, refutil.compare_logs(ref[r], got[r]["log"]))
